@@ -1,0 +1,255 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+The paper prints no worked numeric example of logL or the gradient, so every
+pin is a closed form, an invariant, an independent brute force or a finite
+difference (SURVEY.md §8(c) "pins" table).  None of these re-types the
+oracle's own formulas: brute force marginalises latent states with scipy's
+Padé expm, the JC69 values are analytic, FD differentiates logL numerically.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+from scipy.linalg import expm
+
+import oracle
+import phylo_synth as ps
+from tests import bruteforce
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _rel(a, b):
+    return np.max(np.abs(np.asarray(a) - np.asarray(b)) / np.maximum(np.abs(b), 1e-300))
+
+
+# ---------------------------------------------------------------- Eq. 1 ----
+
+def test_jc69_transition_closed_form():
+    """P_ss(t) = 1/4 + 3/4 e^{-4t/3}, P_st = 1/4 - 1/4 e^{-4t/3}; dP_ss = -e^{-4t/3}."""
+    g = json.load(open(os.path.join(GOLD, "jc69_two_taxon.json")))
+    V, Vi, lam = ps.eigen_reversible(ps.jc69(), np.full(4, 0.25))
+    P = oracle.transition(V, Vi, lam, 0.75)
+    assert abs(P[0, 0] - g["P_jc_t0.75"]["same"]) < 1e-15
+    assert abs(P[0, 1] - g["P_jc_t0.75"]["diff"]) < 1e-15
+    dP = oracle.transition_deriv(V, Vi, lam, 1.0, 0.75)
+    assert abs(dP[2, 2] - g["P_jc_t0.75"]["dsame"]) < 1e-15
+    for t in (0.0, 5.0, 1e3):
+        P = oracle.transition(V, Vi, lam, t)
+        e = np.exp(-4 * t / 3)
+        ref = np.full((4, 4), 0.25 - 0.25 * e) + np.eye(4) * e
+        assert np.max(np.abs(P - ref)) < 2e-14   # eigh rounding ~ S * eps
+
+
+@pytest.mark.parametrize("model", ["hky", "gtr", "mmm4", "codon"])
+def test_transition_matches_pade_expm(model):
+    pb = ps.small_problem(4, model, seed=3)
+    for t in (1e-4, 0.1, 1.0, 10.0):
+        P = oracle.transition(pb.evec, pb.ievec, pb.evals, t)
+        assert np.max(np.abs(P - expm(t * pb.Q))) < 1e-12
+        dP = oracle.transition_deriv(pb.evec, pb.ievec, pb.evals, 0.7, t)
+        assert np.max(np.abs(dP - 0.7 * pb.Q @ expm(0.7 * t * pb.Q))) < 1e-12
+
+
+def test_transition_semigroup_and_limits():
+    pb = ps.small_problem(4, "gtr", seed=5)
+    P1 = oracle.transition(pb.evec, pb.ievec, pb.evals, 0.3)
+    P2 = oracle.transition(pb.evec, pb.ievec, pb.evals, 0.9)
+    P12 = oracle.transition(pb.evec, pb.ievec, pb.evals, 1.2)
+    assert np.max(np.abs(P1 @ P2 - P12)) < 1e-13
+    assert np.max(np.abs(oracle.transition(pb.evec, pb.ievec, pb.evals, 0.0) - np.eye(4))) < 1e-14
+    Pinf = oracle.transition(pb.evec, pb.ievec, pb.evals, 200.0)
+    stat = ps.small_problem(4, "gtr", seed=5).pi
+    assert np.max(np.abs(Pinf - stat[None, :])) < 1e-12
+    assert np.max(np.abs(P1.sum(axis=1) - 1)) < 1e-14
+
+
+# ------------------------------------------------------ two-taxon JC ----
+
+def test_two_taxon_jc_closed_form():
+    g = json.load(open(os.path.join(GOLD, "jc69_two_taxon.json")))
+    b1, b2 = g["b"]
+    pb = ps.two_taxon_jc(b1, b2, [(0, 0), (0, 1)])
+    r = oracle.loglik_grad(pb)
+    L = np.exp(r["site_logL"])
+    assert abs(L[0] - g["equal_tips"]["L"]) < 1e-14 * g["equal_tips"]["L"] * 10
+    assert abs(L[1] - g["unequal_tips"]["L"]) < 1e-14 * g["unequal_tips"]["L"] * 10
+    # analytic derivative from the closed form (independent of Eq. 8)
+    T = b1 + b2
+    e = np.exp(-4 * T / 3)
+    d_eq, d_ne = -e / (0.25 + 0.75 * e), (4 / 3) * e / (1 - e)
+    assert abs(d_eq - g["equal_tips"]["dlogL_db1"]) < 1e-11
+    assert abs(d_ne - g["unequal_tips"]["dlogL_db1"]) < 1e-10
+    pe = ps.two_taxon_jc(b1, b2, [(0, 0)])
+    pn = ps.two_taxon_jc(b1, b2, [(2, 3)])
+    ge, gn = oracle.loglik_grad(pe)["grad"], oracle.loglik_grad(pn)["grad"]
+    for gg, d in ((ge, d_eq), (gn, d_ne)):
+        assert abs(gg[0] - d) < 1e-13 * abs(d)
+        assert abs(gg[1] - d) < 1e-13 * abs(d)        # symmetric in b1, b2
+
+
+def test_zero_branch_lengths_indicator_case():
+    """P(0) = I: L = sum_s pi_s [all tips = s]."""
+    pb = ps.small_problem(4, "hky", C=6, seed=1)
+    pb.branch_lengths[:] = 0.0
+    pb.tip_states[:, 0] = 2
+    pb.tip_states[:, 1] = 1
+    pb.tip_states[1, 1] = 3
+    r = oracle.loglik_grad(pb)
+    assert abs(r["site_logL"][0] - np.log(pb.pi[2])) < 1e-14
+    assert r["status"] == 1 and r["logL"] == -np.inf
+    assert r["zero_pattern"] == 1 or np.isinf(r["site_logL"][1])
+
+
+def test_all_missing_pattern_has_unit_likelihood():
+    pb = ps.small_problem(6, "gtr", R=3, C=3, seed=2)
+    pb.tip_states[:, 1] = pb.states
+    r = oracle.loglik_grad(pb)
+    assert abs(r["site_logL"][1]) < 1e-14
+    pb.pattern_weights[:] = [0, 1, 0]
+    assert np.max(np.abs(oracle.loglik_grad(pb)["grad"])) < 1e-13
+
+
+# ------------------------------------------------------- brute force ----
+
+BRUTE = [("jc", 3, 1), ("hky", 4, 2), ("gtr", 5, 4), ("hky", 6, 2), ("mmm2", 4, 2),
+         ("mmm4", 4, 1), ("codon", 3, 2)]
+
+
+@pytest.mark.parametrize("model,N,R", BRUTE)
+def test_brute_force_loglik_and_gradient(model, N, R):
+    # simulated states: random states on short codon branches route the
+    # likelihood through O(1e-8) transition entries whose absolute rounding
+    # (~1e-16 in both expm and the eigen path) is then a 1e-8 relative error.
+    pb = ps.small_problem(N, model, R=R, C=5, seed=N * 7 + R, missing=0.15, simulate=True)
+    lb, gb = bruteforce.loglik_grad(pb)
+    r = oracle.loglik_grad(pb)
+    assert abs(r["logL"] - lb) <= 1e-12 * abs(lb)
+    scale = np.maximum(np.abs(gb), r["grad_abs"])
+    assert np.all(np.abs(r["grad"] - gb) <= 1e-11 * scale + 1e-14)
+    gq = oracle.grad_quadratic(pb)
+    assert np.all(np.abs(gq - gb) <= 1e-11 * scale + 1e-14)
+
+
+def test_brute_force_tip_partials_and_nonstationary_root():
+    pb = ps.small_problem(5, "mmm2", R=2, C=4, seed=11, partial_tips=True,
+                          stationary_root=False)
+    lb, gb = bruteforce.loglik_grad(pb)
+    r = oracle.loglik_grad(pb)
+    assert abs(r["logL"] - lb) <= 1e-12 * abs(lb)
+    assert np.all(np.abs(r["grad"] - gb) <= 1e-11 * np.maximum(np.abs(gb), r["grad_abs"]))
+
+
+# ---------------------------------------------------- invariants ----
+
+@pytest.mark.parametrize("model,N,R", [("hky", 12, 4), ("mmm4", 9, 1), ("codon", 7, 2)])
+def test_node_invariance_eq5(model, N, R):
+    """sum_r P(gamma_r) p_i'q_i = L_c at every node (Eq. 5)."""
+    pb = ps.small_problem(N, model, R=R, C=9, seed=4, missing=0.1)
+    r = oracle.loglik_grad(pb, node_likelihoods=True)
+    dev = np.abs(r["node_logL"] - r["site_logL"][None, :])
+    assert dev.max() < 1e-12 * max(1.0, np.abs(r["site_logL"]).max())
+
+
+@pytest.mark.parametrize("model,N,R", [("hky", 16, 4), ("gtr", 32, 2), ("mmm4", 8, 2),
+                                       ("codon", 8, 2), ("hky", 64, 1)])
+def test_quadratic_reprune_matches_eq8(model, N, R):
+    pb = ps.small_problem(N, model, R=R, C=6, seed=N, missing=0.05, simulate=True)
+    r = oracle.loglik_grad(pb)
+    gq = oracle.grad_quadratic(pb)
+    assert np.all(np.abs(r["grad"] - gq) <= 1e-11 * np.maximum(np.abs(gq), r["grad_abs"]))
+
+
+def test_finite_differences():
+    pb = ps.small_problem(10, "gtr", R=4, C=8, seed=9)
+    r = oracle.loglik_grad(pb)
+    h = 1e-6
+    fd = np.zeros_like(r["grad"])
+    for i in range(len(fd)):
+        bp, bm = pb.branch_lengths.copy(), pb.branch_lengths.copy()
+        bp[i] += h
+        bm[i] -= h
+        pb.branch_lengths[:] = bp
+        lp = oracle.loglik_grad(pb)["logL"]
+        pb.branch_lengths[:] = bm
+        lm = oracle.loglik_grad(pb)["logL"]
+        pb.branch_lengths[:] = (bp + bm) / 2
+        fd[i] = (lp - lm) / (2 * h)
+    assert np.all(np.abs(fd - r["grad"]) <= 1e-6 * np.maximum(1.0, np.abs(fd)))
+
+
+def test_pulley_principle():
+    """Reversible Q, stationary root: the two root-branch gradients coincide;
+    with a non-stationary root prior they do not."""
+    pb = ps.small_problem(8, "hky", R=4, C=10, seed=21)
+    root = 2 * pb.n_tips - 2
+    d, a, b = pb.ops[-1]
+    assert d == root
+    g = oracle.loglik_grad(pb)["grad"]
+    assert abs(g[a] - g[b]) < 1e-11 * abs(g[a])
+    pb2 = ps.small_problem(8, "hky", R=4, C=10, seed=21, stationary_root=False)
+    g2 = oracle.loglik_grad(pb2)["grad"]
+    assert abs(g2[a] - g2[b]) > 1e-3 * abs(g2[a])
+
+
+def test_euler_identity():
+    """sum_i b_i g_i = d/dalpha logL(alpha b) at alpha = 1."""
+    pb = ps.small_problem(12, "gtr", R=4, C=10, seed=5)
+    g = oracle.loglik_grad(pb)["grad"]
+    b0 = pb.branch_lengths.copy()
+    h = 1e-6
+    vals = []
+    for a in (1 + h, 1 - h):
+        pb.branch_lengths[:] = a * b0
+        vals.append(oracle.loglik_grad(pb)["logL"])
+    pb.branch_lengths[:] = b0
+    fd = (vals[0] - vals[1]) / (2 * h)
+    assert abs(fd - np.dot(b0, g)) < 1e-6 * abs(fd)
+
+
+def test_compression_invariance():
+    """Compressed patterns with weights == raw columns."""
+    rng = np.random.default_rng(7)
+    pb = ps.small_problem(10, "hky", R=2, C=1, seed=7)
+    tree_ops = pb.ops
+    raw = rng.integers(0, 4, size=(10, 60))
+    raw[:, 30:] = raw[:, :30]                       # duplicates
+    raw[:, 45:] = raw[:, 10:25]
+    pats, w = ps.compress_patterns(raw)
+    assert w.sum() == 60 and pats.shape[1] < 60
+    pr = ps.Problem(**{**pb.__dict__, "tip_states": raw.astype(np.int32),
+                       "pattern_weights": np.ones(60), "ops": tree_ops})
+    pc = ps.Problem(**{**pb.__dict__, "tip_states": pats.astype(np.int32),
+                       "pattern_weights": w, "ops": tree_ops})
+    rr, rc = oracle.loglik_grad(pr), oracle.loglik_grad(pc)
+    assert abs(rr["logL"] - rc["logL"]) < 1e-12 * abs(rr["logL"])
+    assert np.max(np.abs(rr["grad"] - rc["grad"]) / rr["grad_abs"]) < 1e-12
+
+
+def test_rescaling_invariance():
+    pb = ps.small_problem(24, "hky", R=4, C=20, seed=8, missing=0.1)
+    a = oracle.loglik_grad(pb, rescale=True)
+    b = oracle.loglik_grad(pb, rescale=False)
+    assert abs(a["logL"] - b["logL"]) < 1e-13 * abs(b["logL"])
+    assert np.max(np.abs(a["grad"] - b["grad"]) / b["grad_abs"]) < 1e-13
+
+
+def test_rescaling_prevents_underflow():
+    """A 400-taxon codon-like deep tree underflows double without rescaling."""
+    pb = ps.small_problem(300, "mmm4", R=1, C=3, seed=2, root_height=3.0)
+    a = oracle.loglik_grad(pb, rescale=True)
+    assert np.isfinite(a["logL"]) and a["status"] == 0
+    assert a["logL"] < -745 * 1  # below exp() range => would underflow unscaled
+    b = oracle.loglik_grad(pb, rescale=False)
+    assert b["status"] == 1 or not np.isfinite(b["logL"])
+
+
+def test_pattern_range_partial_sums():
+    pb = ps.small_problem(9, "gtr", R=3, C=30, seed=12)
+    full = oracle.loglik_grad(pb)
+    parts = [oracle.loglik_grad(pb, lo, hi) for lo, hi in ((0, 7), (7, 19), (19, 30))]
+    assert abs(sum(p["logL"] for p in parts) - full["logL"]) < 1e-12 * abs(full["logL"])
+    assert np.max(np.abs(sum(p["grad"] for p in parts) - full["grad"])) < 1e-10
+    thr = oracle.loglik_grad(pb, threads=3, block=8)
+    assert abs(thr["logL"] - full["logL"]) < 1e-12 * abs(full["logL"])
