@@ -1,0 +1,83 @@
+// common.cuh -- device helpers shared by the phylograd kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "schedule.hpp"
+
+namespace pg {
+
+// Arguments of one traversal launch (both kernel variants).
+struct TravArgs {
+    const Op4 *post;            // [N-1] post program (schedule.hpp)
+    const Op4 *pre;             // [N-1] pre program
+    const void *P;              // Real [B][R][SP][SP]   P[s][t] = Pr(child t | parent s)
+    const void *PT;             // Real [B][R][SP][SP]   transposed copy (large-S kernel)
+    const void *Q;              // Real [SP][SP]         generator (zero padded)
+    const void *QT;             // Real [SP][SP]         transposed generator
+    const void *pi;             // Real [SP]             root prior
+    const double *cat_w;        // [R]  P(gamma_r)
+    const double *cat_g;        // [R]  gamma_r
+    const double *pat_w;        // [Cpad] pattern weights, 0 on padding
+    const uint8_t *tip_states;  // [N][Cpad], code >= S = missing
+    const void *tip_partials;   // Real [N][Cpad][SP] (tips flagged partial)
+    void *u;                    // Real [N-2][R][Cpad][SP] branch-top post vectors
+    double *grad_part;          // [B][n_tiles] per-tile gradient partial sums
+    double *logl_part;          // [n_tiles] per-tile logL partial sums
+    int *status;                // first zero-likelihood pattern (INT_MAX = none)
+    int N, S, R, Cpad, C, n_tiles, depth, prefetch;
+};
+
+// ---- cp.async (LDGSTS) ----------------------------------------------------
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void cp_async_wait_dyn(int n) {
+    switch (n) {
+        case 0: cp_async_wait<0>(); break;
+        case 1: cp_async_wait<1>(); break;
+        case 2: cp_async_wait<2>(); break;
+        case 3: cp_async_wait<3>(); break;
+        case 4: cp_async_wait<4>(); break;
+        case 5: cp_async_wait<5>(); break;
+        case 6: cp_async_wait<6>(); break;
+        default: cp_async_wait<7>(); break;
+    }
+}
+
+// Copy `bytes` (multiple of 16, 16-B aligned) with 16-B cp.async.
+template <int BYTES>
+__device__ __forceinline__ void cp_async_vec(void *smem, const void *gmem) {
+    static_assert(BYTES % 16 == 0, "vector copies are 16-B granular");
+#pragma unroll
+    for (int i = 0; i < BYTES / 16; ++i)
+        cp_async16((char *)smem + 16 * i, (const char *)gmem + 16 * i);
+}
+
+// ---- exact power-of-two rescaling (reading R4) --------
+// exponent e with m = f * 2^e, f in [0.5, 1); 0 for m == 0.
+__device__ __forceinline__ int exponent_of(double m) {
+    int e;
+    (void)frexp(m, &e);
+    return m > 0.0 ? e : 0;
+}
+__device__ __forceinline__ int exponent_of(float m) {
+    int e;
+    (void)frexpf(m, &e);
+    return m > 0.0f ? e : 0;
+}
+__device__ __forceinline__ double scale_pow2(double x, int k) { return ldexp(x, k); }
+__device__ __forceinline__ float scale_pow2(float x, int k) { return ldexpf(x, k); }
+
+template <typename Real>
+__device__ __forceinline__ Real ldg(const Real *p) { return __ldg(p); }
+
+}  // namespace pg

@@ -1,0 +1,699 @@
+// phylograd.cu -- C ABI (include/phylograd.h) and runtime: validation, device
+// workspace layout, traversal planning, launch configuration and CUDA-graph
+// capture of one evaluation:
+//     memset(status) -> pmat_kernel (A1) -> traverse_*_kernel (A2-A5)
+//                    -> reduce_kernel (A6)
+// A7 (the cross-GPU allreduce) is the caller's, on the same stream, over the
+// 2N-1 doubles pg_compute_device leaves in device memory.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/phylograd.h"
+#include "aux_kernels.cuh"
+#include "common.cuh"
+#include "schedule.hpp"
+#include "traverse_large.cuh"
+#include "traverse_small.cuh"
+
+using pg::Op4;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
+
+struct Layout {
+    int SP = 0, variant = 0, Cpad = 0, n_tiles = 0, B = 0, tpl = 32;
+    size_t real = 8;
+    size_t off_P, off_PT, off_Q, off_QT, off_pi, off_V, off_Vi, off_lam, off_rates, off_cw,
+        off_bl, off_patw, off_tips, off_tipp, off_u, off_gpart, off_lpart, off_out, off_status,
+        off_post, off_pre, total;
+};
+
+int padded_states(int S) {
+    if (S <= 4) return 4;
+    if (S <= 8) return 8;
+    if (S <= 16) return 16;
+    if (S <= 32) return 32;
+    if (S <= 64) return 64;
+    return 0;
+}
+
+int make_layout(const pg_config *c, Layout *L, std::string *err) {
+    if (!c) { if (err) *err = "config is NULL"; return PG_ERR_ARG; }
+    if (c->tips < 2 || c->patterns < 1 || c->states < 2 || c->categories < 1) {
+        if (err) *err = "need tips >= 2, patterns >= 1, states >= 2, categories >= 1";
+        return PG_ERR_ARG;
+    }
+    if (c->precision != PG_FP64 && c->precision != PG_FP32) {
+        if (err) *err = "precision must be PG_FP64 or PG_FP32";
+        return PG_ERR_ARG;
+    }
+    const int SP = padded_states(c->states);
+    if (!SP) { if (err) *err = "states > 64 are not supported by this build"; return PG_ERR_UNSUPPORTED; }
+    if (c->states > 254) { if (err) *err = "states > 254"; return PG_ERR_UNSUPPORTED; }
+    const int R = c->categories;
+    L->SP = SP;
+    L->variant = SP <= 16 ? 0 : 1;
+    L->real = c->precision == PG_FP64 ? 8 : 4;
+    if (L->variant == 0) {
+        if (R > (SP == 16 ? 8 : 16)) {
+            if (err) *err = "too many rate categories for this state count (max 16; 8 for S > 8)";
+            return PG_ERR_UNSUPPORTED;
+        }
+        L->tpl = 32;
+    } else {
+        if (R > 16) { if (err) *err = "too many rate categories (max 16)"; return PG_ERR_UNSUPPORTED; }
+        L->tpl = (L->real == 8) ? pg::LargeCfg<double, 64>::tpl(R) : pg::LargeCfg<float, 64>::tpl(R);
+        if (SP == 32) L->tpl = (L->real == 8) ? pg::LargeCfg<double, 32>::tpl(R) : pg::LargeCfg<float, 32>::tpl(R);
+    }
+    const long long N = c->tips, C = c->patterns;
+    L->Cpad = (int)((C + 31) / 32 * 32);
+    L->n_tiles = L->Cpad / L->tpl;
+    L->B = (int)(2 * N - 2);
+    const size_t mats = (size_t)L->B * R * SP * SP * L->real;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t at = o; o = align_up(o + bytes); return at; };
+    L->off_P = take(mats);
+    L->off_PT = take(L->variant == 1 ? mats : 0);
+    L->off_Q = take((size_t)SP * SP * L->real);
+    L->off_QT = take((size_t)SP * SP * L->real);
+    L->off_pi = take((size_t)SP * L->real);
+    L->off_V = take((size_t)c->states * c->states * 8);
+    L->off_Vi = take((size_t)c->states * c->states * 8);
+    L->off_lam = take((size_t)c->states * 8);
+    L->off_rates = take((size_t)R * 8);
+    L->off_cw = take((size_t)R * 8);
+    L->off_bl = take((size_t)L->B * 8);
+    L->off_patw = take((size_t)L->Cpad * 8);
+    L->off_tips = take((size_t)N * L->Cpad);
+    L->off_tipp = take((c->flags & PG_FLAG_TIP_PARTIALS) ? (size_t)N * L->Cpad * SP * L->real : 0);
+    L->off_u = take((size_t)(N - 2) * R * L->Cpad * SP * L->real);
+    L->off_gpart = take((size_t)L->B * L->n_tiles * 8);
+    L->off_lpart = take((size_t)L->n_tiles * 8);
+    L->off_out = take((size_t)(L->B + 1) * 8);
+    L->off_status = take(sizeof(int) * 4);
+    L->off_post = take((size_t)(N - 1) * sizeof(Op4));
+    L->off_pre = take((size_t)(N - 1) * sizeof(Op4));
+    L->total = o;
+    return PG_OK;
+}
+
+const char *code_name(int code) {
+    switch (code) {
+        case PG_OK: return "ok";
+        case PG_ERR_ARG: return "invalid argument";
+        case PG_ERR_DOMAIN: return "value outside its domain";
+        case PG_ERR_TOPOLOGY: return "invalid tree topology";
+        case PG_ERR_SEQUENCE: return "inputs not set before compute";
+        case PG_ERR_ZERO_LIKELIHOOD: return "zero site likelihood";
+        case PG_ERR_CUDA: return "CUDA error";
+        case PG_ERR_UNSUPPORTED: return "unsupported configuration";
+        case PG_ERR_MEMORY: return "out of memory";
+        default: return "unknown error";
+    }
+}
+
+}  // namespace
+
+struct pg_instance {
+    pg_config cfg{};
+    Layout L{};
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    char *ws = nullptr;
+    bool own_ws = false;
+    int sm_count = 148;
+    // host-side state
+    std::vector<uint8_t> tips_h;        // [N][Cpad]
+    std::vector<uint8_t> tip_is_partial, tip_set;
+    bool have_ops = false, have_eigen = false, have_pi = false, have_rates = false,
+         have_cw = false, have_bl = false, have_patw = false;
+    pg::Plan plan;
+    bool plan_dirty = true, tips_dirty = true, partial_modes_dirty = false;
+    double *bl_pinned = nullptr, *out_pinned = nullptr;
+    int *status_pinned = nullptr;
+    bool bl_host_pending = false;
+    // launch configuration
+    int prefetch = 4, smem = 0, grid = 0, block = 0;
+    cudaGraphExec_t gexec = nullptr;
+    double *gexec_out = nullptr;
+    bool timing = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    std::string err;
+
+    template <typename T> T *at(size_t off) { return reinterpret_cast<T *>(ws + off); }
+    int fail(int code, const std::string &msg) { err = msg; return code; }
+    int cuda_fail(cudaError_t e, const char *what) {
+        err = std::string(what) + ": " + cudaGetErrorString(e);
+        return PG_ERR_CUDA;
+    }
+};
+
+#define CK(call, what)                                            \
+    do {                                                          \
+        cudaError_t _e = (call);                                  \
+        if (_e != cudaSuccess) return inst->cuda_fail(_e, what);  \
+    } while (0)
+
+// Exported functions get C linkage from their declarations in phylograd.h.
+
+int pg_version(void) { return 100; }
+
+const char *pg_strerror(int code) { return code_name(code); }
+
+const char *pg_last_error(const pg_instance *inst) { return inst ? inst->err.c_str() : "NULL instance"; }
+
+int pg_workspace_bytes(const pg_config *cfg, size_t *bytes) {
+    Layout L;
+    int rc = make_layout(cfg, &L, nullptr);
+    if (rc) return rc;
+    if (!bytes) return PG_ERR_ARG;
+    *bytes = L.total;
+    return PG_OK;
+}
+
+int pg_plan_check(int32_t tips, const int32_t *ops, int32_t n_ops, int32_t *post_depth, int32_t *pre_depth) {
+    pg::Plan p;
+    std::string e;
+    int rc = pg::build_plan(tips, ops, n_ops, &p, &e);
+    if (rc) return rc;
+    if (post_depth) *post_depth = p.post_depth;
+    if (pre_depth) *pre_depth = p.pre_depth;
+    return PG_OK;
+}
+
+int pg_create(const pg_config *cfg, void *cuda_stream, void *dev_workspace, size_t workspace_bytes,
+              pg_instance **out) {
+    if (!out) return PG_ERR_ARG;
+    *out = nullptr;
+    Layout L;
+    std::string err;
+    int rc = make_layout(cfg, &L, &err);
+    if (rc) return rc;
+    pg_instance *inst = new pg_instance();
+    inst->cfg = *cfg;
+    inst->L = L;
+    auto bail = [&](int code) { pg_destroy(inst); return code; };
+    cudaError_t e = cudaSetDevice(cfg->device);
+    if (e != cudaSuccess) { inst->cuda_fail(e, "cudaSetDevice"); return bail(PG_ERR_CUDA); }
+    int dev_sms = 0;
+    if (cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device) == cudaSuccess && dev_sms > 0)
+        inst->sm_count = dev_sms;
+    if (cuda_stream) {
+        inst->stream = (cudaStream_t)cuda_stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&inst->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(PG_ERR_CUDA);
+        inst->own_stream = true;
+    }
+    if (dev_workspace) {
+        if (workspace_bytes < L.total || ((uintptr_t)dev_workspace % kAlign) != 0) return bail(PG_ERR_MEMORY);
+        inst->ws = (char *)dev_workspace;
+    } else {
+        if (cudaMalloc((void **)&inst->ws, L.total) != cudaSuccess) return bail(PG_ERR_MEMORY);
+        inst->own_ws = true;
+    }
+    if (cudaMallocHost((void **)&inst->bl_pinned, sizeof(double) * L.B) != cudaSuccess ||
+        cudaMallocHost((void **)&inst->out_pinned, sizeof(double) * (L.B + 1)) != cudaSuccess ||
+        cudaMallocHost((void **)&inst->status_pinned, sizeof(int) * 4) != cudaSuccess)
+        return bail(PG_ERR_MEMORY);
+    const int N = cfg->tips;
+    inst->tips_h.assign((size_t)N * L.Cpad, (uint8_t)cfg->states);   // all missing
+    inst->tip_is_partial.assign(N, 0);
+    inst->tip_set.assign(N, 0);
+    // zero padded weights, partials (all-ones for padding is set per tip), Q, pi, matrices
+    if (cudaMemsetAsync(inst->ws, 0, L.total, inst->stream) != cudaSuccess) return bail(PG_ERR_CUDA);
+    *out = inst;
+    return PG_OK;
+}
+
+int pg_destroy(pg_instance *inst) {
+    if (!inst) return PG_OK;
+    if (inst->stream) cudaStreamSynchronize(inst->stream);
+    if (inst->gexec) cudaGraphExecDestroy(inst->gexec);
+    for (auto &e : inst->ev) if (e) cudaEventDestroy(e);
+    if (inst->own_ws && inst->ws) cudaFree(inst->ws);
+    if (inst->bl_pinned) cudaFreeHost(inst->bl_pinned);
+    if (inst->out_pinned) cudaFreeHost(inst->out_pinned);
+    if (inst->status_pinned) cudaFreeHost(inst->status_pinned);
+    if (inst->own_stream && inst->stream) cudaStreamDestroy(inst->stream);
+    delete inst;
+    return PG_OK;
+}
+
+static bool finite_all(const double *p, size_t n) {
+    for (size_t i = 0; i < n; ++i) if (!std::isfinite(p[i])) return false;
+    return true;
+}
+
+// upload `n` doubles to a double buffer (synchronous w.r.t. the host copy)
+static int upload_doubles(pg_instance *inst, size_t off, const double *src, size_t n) {
+    CK(cudaMemcpyAsync(inst->ws + off, src, n * sizeof(double), cudaMemcpyHostToDevice, inst->stream), "upload");
+    CK(cudaStreamSynchronize(inst->stream), "upload sync");
+    return PG_OK;
+}
+// upload `n` doubles converted to the compute precision, zero padded to n_pad
+static int upload_real(pg_instance *inst, size_t off, const std::vector<double> &v) {
+    if (inst->L.real == 8) {
+        CK(cudaMemcpyAsync(inst->ws + off, v.data(), v.size() * 8, cudaMemcpyHostToDevice, inst->stream), "upload");
+    } else {
+        std::vector<float> f(v.begin(), v.end());
+        CK(cudaMemcpyAsync(inst->ws + off, f.data(), f.size() * 4, cudaMemcpyHostToDevice, inst->stream), "upload");
+    }
+    CK(cudaStreamSynchronize(inst->stream), "upload sync");
+    return PG_OK;
+}
+
+int pg_set_tip_states(pg_instance *inst, int32_t tip, const int32_t *states) {
+    if (!inst) return PG_ERR_ARG;
+    const pg_config &c = inst->cfg;
+    if (tip < 0 || tip >= c.tips || !states) return inst->fail(PG_ERR_ARG, "tip index out of range or NULL states");
+    for (int i = 0; i < c.patterns; ++i)
+        if (states[i] < 0 || states[i] > c.states)
+            return inst->fail(PG_ERR_ARG, "tip state outside 0..S (S = missing) at pattern " + std::to_string(i));
+    uint8_t *row = inst->tips_h.data() + (size_t)tip * inst->L.Cpad;
+    for (int i = 0; i < c.patterns; ++i) row[i] = (uint8_t)states[i];
+    if (inst->tip_is_partial[tip]) { inst->tip_is_partial[tip] = 0; inst->partial_modes_dirty = true; }
+    inst->tip_set[tip] = 1;
+    inst->tips_dirty = true;
+    return PG_OK;
+}
+
+int pg_set_tip_partials(pg_instance *inst, int32_t tip, const double *partials) {
+    if (!inst) return PG_ERR_ARG;
+    const pg_config &c = inst->cfg;
+    if (!(c.flags & PG_FLAG_TIP_PARTIALS))
+        return inst->fail(PG_ERR_UNSUPPORTED, "instance created without PG_FLAG_TIP_PARTIALS");
+    if (tip < 0 || tip >= c.tips || !partials) return inst->fail(PG_ERR_ARG, "tip index out of range or NULL");
+    const int S = c.states, SP = inst->L.SP, Cp = inst->L.Cpad;
+    for (size_t i = 0; i < (size_t)c.patterns * S; ++i)
+        if (!(partials[i] >= 0.0) || !std::isfinite(partials[i]))
+            return inst->fail(PG_ERR_DOMAIN, "tip partials must be finite and >= 0");
+    std::vector<double> v((size_t)Cp * SP, 0.0);
+    for (int p = 0; p < Cp; ++p)
+        for (int s = 0; s < S; ++s) v[(size_t)p * SP + s] = p < c.patterns ? partials[(size_t)p * S + s] : 1.0;
+    int rc = upload_real(inst, inst->L.off_tipp + (size_t)tip * Cp * SP * inst->L.real, v);
+    if (rc) return rc;
+    if (!inst->tip_is_partial[tip]) { inst->tip_is_partial[tip] = 1; inst->partial_modes_dirty = true; }
+    inst->tip_set[tip] = 1;
+    return PG_OK;
+}
+
+int pg_set_pattern_weights(pg_instance *inst, const double *w) {
+    if (!inst || !w) return PG_ERR_ARG;
+    const int C = inst->cfg.patterns;
+    for (int i = 0; i < C; ++i)
+        if (!(w[i] >= 0.0) || !std::isfinite(w[i])) return inst->fail(PG_ERR_DOMAIN, "pattern weights must be finite and >= 0");
+    std::vector<double> v(inst->L.Cpad, 0.0);
+    std::copy(w, w + C, v.begin());
+    int rc = upload_doubles(inst, inst->L.off_patw, v.data(), v.size());
+    if (rc) return rc;
+    inst->have_patw = true;
+    return PG_OK;
+}
+
+int pg_set_state_frequencies(pg_instance *inst, const double *pi) {
+    if (!inst || !pi) return PG_ERR_ARG;
+    const int S = inst->cfg.states, SP = inst->L.SP;
+    for (int s = 0; s < S; ++s)
+        if (!(pi[s] >= 0.0) || !std::isfinite(pi[s])) return inst->fail(PG_ERR_DOMAIN, "pi must be finite and >= 0");
+    std::vector<double> v(SP, 0.0);
+    std::copy(pi, pi + S, v.begin());
+    int rc = upload_real(inst, inst->L.off_pi, v);
+    if (rc) return rc;
+    inst->have_pi = true;
+    return PG_OK;
+}
+
+int pg_set_eigen(pg_instance *inst, const double *evec, const double *ievec, const double *eval) {
+    if (!inst || !evec || !ievec || !eval) return PG_ERR_ARG;
+    const int S = inst->cfg.states, SP = inst->L.SP;
+    if (!finite_all(evec, (size_t)S * S) || !finite_all(ievec, (size_t)S * S) || !finite_all(eval, S))
+        return inst->fail(PG_ERR_ARG, "eigensystem must be finite");
+    int rc;
+    if ((rc = upload_doubles(inst, inst->L.off_V, evec, (size_t)S * S))) return rc;
+    if ((rc = upload_doubles(inst, inst->L.off_Vi, ievec, (size_t)S * S))) return rc;
+    if ((rc = upload_doubles(inst, inst->L.off_lam, eval, S))) return rc;
+    // Q = V diag(lambda) V^{-1} (host, double), padded; and Q'
+    std::vector<double> Q((size_t)SP * SP, 0.0), QT((size_t)SP * SP, 0.0);
+    for (int s = 0; s < S; ++s)
+        for (int t = 0; t < S; ++t) {
+            double acc = 0.0;
+            for (int k = 0; k < S; ++k) acc += evec[s * S + k] * eval[k] * ievec[k * S + t];
+            Q[(size_t)s * SP + t] = acc;
+            QT[(size_t)t * SP + s] = acc;
+        }
+    if ((rc = upload_real(inst, inst->L.off_Q, Q))) return rc;
+    if ((rc = upload_real(inst, inst->L.off_QT, QT))) return rc;
+    inst->have_eigen = true;
+    return PG_OK;
+}
+
+int pg_set_category_rates(pg_instance *inst, const double *rates) {
+    if (!inst || !rates) return PG_ERR_ARG;
+    for (int r = 0; r < inst->cfg.categories; ++r)
+        if (!(rates[r] > 0.0) || !std::isfinite(rates[r])) return inst->fail(PG_ERR_DOMAIN, "category rates must be > 0");
+    int rc = upload_doubles(inst, inst->L.off_rates, rates, inst->cfg.categories);
+    if (rc) return rc;
+    inst->have_rates = true;
+    return PG_OK;
+}
+
+int pg_set_category_weights(pg_instance *inst, const double *w) {
+    if (!inst || !w) return PG_ERR_ARG;
+    for (int r = 0; r < inst->cfg.categories; ++r)
+        if (!(w[r] >= 0.0) || !std::isfinite(w[r])) return inst->fail(PG_ERR_DOMAIN, "category weights must be >= 0");
+    int rc = upload_doubles(inst, inst->L.off_cw, w, inst->cfg.categories);
+    if (rc) return rc;
+    inst->have_cw = true;
+    return PG_OK;
+}
+
+int pg_set_operations(pg_instance *inst, const int32_t *ops, int32_t n_ops) {
+    if (!inst) return PG_ERR_ARG;
+    pg::Plan p;
+    std::string e;
+    int rc = pg::build_plan(inst->cfg.tips, ops, n_ops, &p, &e);
+    if (rc) return inst->fail(rc, e);
+    inst->plan = std::move(p);
+    inst->have_ops = true;
+    inst->plan_dirty = true;
+    return PG_OK;
+}
+
+int pg_set_branch_lengths(pg_instance *inst, const double *b) {
+    if (!inst || !b) return PG_ERR_ARG;
+    const int B = inst->L.B;
+    for (int i = 0; i < B; ++i)
+        if (!(b[i] >= 0.0) || !std::isfinite(b[i]))
+            return inst->fail(PG_ERR_DOMAIN, "branch length " + std::to_string(i) + " is negative or not finite");
+    std::memcpy(inst->bl_pinned, b, sizeof(double) * B);
+    inst->bl_host_pending = true;
+    inst->have_bl = true;
+    return PG_OK;
+}
+
+int pg_set_branch_lengths_device(pg_instance *inst, const double *d_b) {
+    if (!inst || !d_b) return PG_ERR_ARG;
+    CK(cudaMemcpyAsync(inst->ws + inst->L.off_bl, d_b, sizeof(double) * inst->L.B, cudaMemcpyDeviceToDevice,
+                       inst->stream), "branch lengths D2D");
+    inst->bl_host_pending = false;
+    inst->have_bl = true;
+    return PG_OK;
+}
+
+// -------------------------------------------------------------------------
+// launch configuration
+// -------------------------------------------------------------------------
+
+template <typename Real, int SP>
+static void *small_kernel() { return (void *)pg::traverse_small_kernel<Real, SP>; }
+template <typename Real, int SP>
+static void *large_kernel() { return (void *)pg::traverse_large_kernel<Real, SP>; }
+template <typename Real, int SP>
+static void *pmat_fn() { return (void *)pg::pmat_kernel<Real, SP>; }
+
+static void *traverse_fn(const Layout &L) {
+    const bool d = L.real == 8;
+    switch (L.SP) {
+        case 4: return d ? small_kernel<double, 4>() : small_kernel<float, 4>();
+        case 8: return d ? small_kernel<double, 8>() : small_kernel<float, 8>();
+        case 16: return d ? small_kernel<double, 16>() : small_kernel<float, 16>();
+        case 32: return d ? large_kernel<double, 32>() : large_kernel<float, 32>();
+        case 64: return d ? large_kernel<double, 64>() : large_kernel<float, 64>();
+    }
+    return nullptr;
+}
+static void *pmat_kernel_fn(const Layout &L) {
+    const bool d = L.real == 8;
+    switch (L.SP) {
+        case 4: return d ? pmat_fn<double, 4>() : pmat_fn<float, 4>();
+        case 8: return d ? pmat_fn<double, 8>() : pmat_fn<float, 8>();
+        case 16: return d ? pmat_fn<double, 16>() : pmat_fn<float, 16>();
+        case 32: return d ? pmat_fn<double, 32>() : pmat_fn<float, 32>();
+        case 64: return d ? pmat_fn<double, 64>() : pmat_fn<float, 64>();
+    }
+    return nullptr;
+}
+
+static size_t small_smem(const Layout &L, int R, int D, int depth) {
+    const size_t nthr = (size_t)R * 32;
+    return (size_t)2 * 4 * nthr * 8 + (size_t)2 * 2 * nthr * 4 + (size_t)D * 2 * nthr * L.SP * L.real +
+           (size_t)depth * nthr * L.SP * L.real;
+}
+static size_t large_smem(const Layout &L, int R, int depth) {
+    const size_t nvec = (size_t)L.tpl * R;
+    const size_t vb = nvec * L.SP * L.real;
+    return (5 + (size_t)depth) * vb + nvec * (4 * 8 + 2 * 4) + (size_t)L.tpl * 16;
+}
+
+static int configure(pg_instance *inst) {
+    const Layout &L = inst->L;
+    const int R = inst->cfg.categories;
+    const int depth = std::max(inst->plan.post_depth, inst->plan.pre_depth);
+    void *fn = traverse_fn(L);
+    inst->grid = L.n_tiles;
+    if (L.variant == 0) {
+        inst->block = R * 32;
+        int best_D = 2, best_waves = INT_MAX;
+        for (int D = 6; D >= 2; --D) {
+            size_t sm = small_smem(L, R, D, depth);
+            if (sm > 227 * 1024) continue;
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "smem attr");
+            int occ = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, inst->block, sm), "occupancy");
+            if (occ < 1) continue;
+            int waves = (inst->grid + occ * inst->sm_count - 1) / (occ * inst->sm_count);
+            if (waves < best_waves) { best_waves = waves; best_D = D; }
+        }
+        if (best_waves == INT_MAX) return inst->fail(PG_ERR_UNSUPPORTED, "traversal does not fit in shared memory");
+        inst->prefetch = best_D;
+        inst->smem = (int)small_smem(L, R, best_D, depth);
+    } else {
+        inst->block = L.tpl * R * (L.SP / 4);
+        inst->prefetch = 0;
+        inst->smem = (int)large_smem(L, R, depth);
+        if (inst->smem > 227 * 1024) return inst->fail(PG_ERR_UNSUPPORTED, "traversal does not fit in shared memory");
+    }
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, inst->smem), "smem attr");
+    return PG_OK;
+}
+
+static int refresh_plan(pg_instance *inst) {
+    if (!inst->plan_dirty && !inst->partial_modes_dirty) return PG_OK;
+    pg::encode_tip_modes(&inst->plan, inst->tip_is_partial);
+    const int N = inst->cfg.tips;
+    CK(cudaMemcpyAsync(inst->ws + inst->L.off_post, inst->plan.post.data(), sizeof(Op4) * (N - 1),
+                       cudaMemcpyHostToDevice, inst->stream), "plan upload");
+    CK(cudaMemcpyAsync(inst->ws + inst->L.off_pre, inst->plan.pre.data(), sizeof(Op4) * (N - 1),
+                       cudaMemcpyHostToDevice, inst->stream), "plan upload");
+    CK(cudaStreamSynchronize(inst->stream), "plan upload sync");
+    int rc = configure(inst);
+    if (rc) return rc;
+    inst->plan_dirty = inst->partial_modes_dirty = false;
+    if (inst->gexec) { cudaGraphExecDestroy(inst->gexec); inst->gexec = nullptr; }
+    return PG_OK;
+}
+
+static pg::TravArgs trav_args(pg_instance *inst) {
+    const Layout &L = inst->L;
+    pg::TravArgs a{};
+    a.post = inst->at<Op4>(L.off_post);
+    a.pre = inst->at<Op4>(L.off_pre);
+    a.P = inst->ws + L.off_P;
+    a.PT = L.variant == 1 ? inst->ws + L.off_PT : nullptr;
+    a.Q = inst->ws + L.off_Q;
+    a.QT = inst->ws + L.off_QT;
+    a.pi = inst->ws + L.off_pi;
+    a.cat_w = inst->at<double>(L.off_cw);
+    a.cat_g = inst->at<double>(L.off_rates);
+    a.pat_w = inst->at<double>(L.off_patw);
+    a.tip_states = inst->at<uint8_t>(L.off_tips);
+    a.tip_partials = (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? inst->ws + L.off_tipp : nullptr;
+    a.u = inst->ws + L.off_u;
+    a.grad_part = inst->at<double>(L.off_gpart);
+    a.logl_part = inst->at<double>(L.off_lpart);
+    a.status = inst->at<int>(L.off_status);
+    a.N = inst->cfg.tips;
+    a.S = inst->cfg.states;
+    a.R = inst->cfg.categories;
+    a.Cpad = L.Cpad;
+    a.C = inst->cfg.patterns;
+    a.n_tiles = L.n_tiles;
+    a.depth = std::max(inst->plan.post_depth, inst->plan.pre_depth);
+    a.prefetch = inst->prefetch;
+    return a;
+}
+
+// enqueue one evaluation (no host sync) writing [logL, g] to d_out
+static int enqueue_eval(pg_instance *inst, double *d_out) {
+    const Layout &L = inst->L;
+    const int R = inst->cfg.categories;
+    CK(cudaMemsetAsync(inst->at<int>(L.off_status), 0x7f, sizeof(int), inst->stream), "status reset");
+    if (inst->timing) CK(cudaEventRecord(inst->ev[0], inst->stream), "event");
+    {
+        void *fn = pmat_kernel_fn(L);
+        const double *V = inst->at<double>(L.off_V), *Vi = inst->at<double>(L.off_Vi),
+                     *lam = inst->at<double>(L.off_lam), *rates = inst->at<double>(L.off_rates),
+                     *bl = inst->at<double>(L.off_bl);
+        int S = inst->cfg.states;
+        void *P = inst->ws + L.off_P;
+        void *PT = L.variant == 1 ? inst->ws + L.off_PT : nullptr;
+        void *args[] = {&V, &Vi, &lam, &rates, &bl, &S, (void *)&R, &P, &PT};
+        CK(cudaLaunchKernel(fn, dim3(L.B * R), dim3(std::min(256, L.SP * L.SP)), args, 0, inst->stream), "pmat launch");
+    }
+    if (inst->timing) CK(cudaEventRecord(inst->ev[1], inst->stream), "event");
+    {
+        pg::TravArgs a = trav_args(inst);
+        void *args[] = {&a};
+        CK(cudaLaunchKernel(traverse_fn(L), dim3(inst->grid), dim3(inst->block), args, inst->smem, inst->stream),
+           "traverse launch");
+    }
+    if (inst->timing) CK(cudaEventRecord(inst->ev[2], inst->stream), "event");
+    {
+        const double *gp = inst->at<double>(L.off_gpart), *lp = inst->at<double>(L.off_lpart);
+        int B = L.B, nt = L.n_tiles;
+        void *args[] = {&gp, &lp, &B, &nt, &d_out};
+        CK(cudaLaunchKernel((void *)pg::reduce_kernel, dim3(L.B + 1), dim3(256), args, 0, inst->stream),
+           "reduce launch");
+    }
+    if (inst->timing) CK(cudaEventRecord(inst->ev[3], inst->stream), "event");
+    return PG_OK;
+}
+
+static int prepare(pg_instance *inst) {
+    if (!inst->have_ops) return inst->fail(PG_ERR_SEQUENCE, "operations not set");
+    if (!inst->have_eigen) return inst->fail(PG_ERR_SEQUENCE, "eigensystem not set");
+    if (!inst->have_pi) return inst->fail(PG_ERR_SEQUENCE, "state frequencies not set");
+    if (!inst->have_rates || !inst->have_cw) return inst->fail(PG_ERR_SEQUENCE, "category rates/weights not set");
+    if (!inst->have_patw) return inst->fail(PG_ERR_SEQUENCE, "pattern weights not set");
+    if (!inst->have_bl) return inst->fail(PG_ERR_SEQUENCE, "branch lengths not set");
+    for (int t = 0; t < inst->cfg.tips; ++t)
+        if (!inst->tip_set[t]) return inst->fail(PG_ERR_SEQUENCE, "tip " + std::to_string(t) + " has no data");
+    int rc = refresh_plan(inst);
+    if (rc) return rc;
+    if (inst->tips_dirty) {
+        CK(cudaMemcpyAsync(inst->ws + inst->L.off_tips, inst->tips_h.data(), inst->tips_h.size(),
+                           cudaMemcpyHostToDevice, inst->stream), "tips upload");
+        CK(cudaStreamSynchronize(inst->stream), "tips sync");
+        inst->tips_dirty = false;
+    }
+    return PG_OK;
+}
+
+// one evaluation via a cached CUDA graph (captured per output pointer)
+static int launch_eval(pg_instance *inst, double *d_out) {
+    if (!inst->gexec || inst->gexec_out != d_out) {
+        if (inst->gexec) { cudaGraphExecDestroy(inst->gexec); inst->gexec = nullptr; }
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(inst->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+        int rc = enqueue_eval(inst, d_out);
+        cudaError_t e2 = cudaStreamEndCapture(inst->stream, &g);
+        if (rc) return rc;
+        if (e2 != cudaSuccess) return inst->cuda_fail(e2, "end capture");
+        cudaError_t e3 = cudaGraphInstantiate(&inst->gexec, g, 0);
+        cudaGraphDestroy(g);
+        if (e3 != cudaSuccess) return inst->cuda_fail(e3, "graph instantiate");
+        inst->gexec_out = d_out;
+    }
+    CK(cudaGraphLaunch(inst->gexec, inst->stream), "graph launch");
+    return PG_OK;
+}
+
+int pg_compute_device(pg_instance *inst, double *d_out) {
+    if (!inst || !d_out) return PG_ERR_ARG;
+    int rc = prepare(inst);
+    if (rc) return rc;
+    if (inst->bl_host_pending) {
+        CK(cudaMemcpyAsync(inst->ws + inst->L.off_bl, inst->bl_pinned, sizeof(double) * inst->L.B,
+                           cudaMemcpyHostToDevice, inst->stream), "branch lengths H2D");
+        inst->bl_host_pending = false;
+    }
+    return launch_eval(inst, d_out);
+}
+
+int pg_compute(pg_instance *inst, double *log_likelihood, double *gradient) {
+    if (!inst || !log_likelihood) return PG_ERR_ARG;
+    int rc = prepare(inst);
+    if (rc) return rc;
+    const Layout &L = inst->L;
+    if (inst->bl_host_pending) {
+        CK(cudaMemcpyAsync(inst->ws + L.off_bl, inst->bl_pinned, sizeof(double) * L.B, cudaMemcpyHostToDevice,
+                           inst->stream), "branch lengths H2D");
+        // host branch lengths stay "pending": every pg_compute re-uploads them
+    }
+    double *d_out = inst->at<double>(L.off_out);
+    if ((rc = launch_eval(inst, d_out))) return rc;
+    CK(cudaMemcpyAsync(inst->out_pinned, d_out, sizeof(double) * (L.B + 1), cudaMemcpyDeviceToHost, inst->stream),
+       "result D2H");
+    CK(cudaMemcpyAsync(inst->status_pinned, inst->at<int>(L.off_status), sizeof(int), cudaMemcpyDeviceToHost,
+                       inst->stream), "status D2H");
+    CK(cudaStreamSynchronize(inst->stream), "compute sync");
+    const int zp = inst->status_pinned[0];
+    if (zp != 0x7f7f7f7f) {
+        *log_likelihood = -INFINITY;
+        return inst->fail(PG_ERR_ZERO_LIKELIHOOD, "site likelihood is zero at pattern " + std::to_string(zp));
+    }
+    *log_likelihood = inst->out_pinned[0];
+    if (gradient) std::memcpy(gradient, inst->out_pinned + 1, sizeof(double) * L.B);
+    return PG_OK;
+}
+
+int pg_check_status(pg_instance *inst, int32_t *zero_pattern) {
+    if (!inst) return PG_ERR_ARG;
+    int v = 0;
+    CK(cudaMemcpyAsync(inst->status_pinned, inst->at<int>(inst->L.off_status), sizeof(int), cudaMemcpyDeviceToHost,
+                       inst->stream), "status D2H");
+    CK(cudaStreamSynchronize(inst->stream), "status sync");
+    v = inst->status_pinned[0];
+    const bool bad = v != 0x7f7f7f7f;
+    if (zero_pattern) *zero_pattern = bad ? v : -1;
+    if (bad) return inst->fail(PG_ERR_ZERO_LIKELIHOOD, "site likelihood is zero at pattern " + std::to_string(v));
+    return PG_OK;
+}
+
+int pg_set_kernel_timing(pg_instance *inst, int enable) {
+    if (!inst) return PG_ERR_ARG;
+    if (enable && !inst->ev[0])
+        for (auto &e : inst->ev) CK(cudaEventCreate(&e), "event create");
+    if ((bool)enable != inst->timing && inst->gexec) {
+        cudaGraphExecDestroy(inst->gexec);
+        inst->gexec = nullptr;
+    }
+    inst->timing = enable != 0;
+    return PG_OK;
+}
+
+int pg_get_kernel_times(pg_instance *inst, float *ms) {
+    if (!inst || !ms) return PG_ERR_ARG;
+    if (!inst->timing) return inst->fail(PG_ERR_SEQUENCE, "kernel timing is not enabled");
+    CK(cudaEventSynchronize(inst->ev[3]), "event sync");
+    for (int k = 0; k < 3; ++k) CK(cudaEventElapsedTime(&ms[k], inst->ev[k], inst->ev[k + 1]), "elapsed");
+    return PG_OK;
+}
+
+int pg_kernels_per_eval(const pg_instance *inst, int32_t *n) {
+    if (!inst || !n) return PG_ERR_ARG;
+    *n = 3;   // pmat, traverse, reduce
+    return PG_OK;
+}
+
+int pg_get_plan_info(const pg_instance *inst, pg_plan_info *info) {
+    if (!inst || !info) return PG_ERR_ARG;
+    info->post_depth = inst->plan.post_depth;
+    info->pre_depth = inst->plan.pre_depth;
+    info->grid = inst->grid;
+    info->block = inst->block;
+    info->smem_bytes = inst->smem;
+    info->prefetch_depth = inst->prefetch;
+    info->padded_patterns = inst->L.Cpad;
+    info->kernel_variant = inst->L.variant;
+    return PG_OK;
+}

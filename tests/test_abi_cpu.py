@@ -1,0 +1,82 @@
+"""Host-side checks of the C ABI library that need no GPU (-m "not gpu").
+
+The library must load and export every symbol include/phylograd.h declares;
+topology validation and traversal planning run on the host.
+"""
+import ctypes
+import subprocess
+
+import numpy as np
+import pytest
+
+import phylo_synth as ps
+
+
+@pytest.fixture(scope="module")
+def pg():
+    import paper_2303_04390_b200 as m
+    return m
+
+
+def test_library_exports_every_header_symbol(pg):
+    syms = pg.header_symbols()
+    assert len(syms) >= 20
+    missing = [s for s in syms if not hasattr(pg._lib, s)]
+    assert not missing, missing
+    nm = subprocess.run(["nm", "-D", "--defined-only", pg.LIB_PATH], capture_output=True, text=True).stdout
+    for s in syms:
+        assert f" T {s}" in nm, s
+
+
+def test_library_is_sm100a(pg):
+    out = subprocess.run(["cuobjdump", "--list-elf", pg.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version_and_strerror(pg):
+    assert pg._lib.pg_version() >= 100
+    assert pg._lib.pg_strerror(pg.PG_ERR_TOPOLOGY).decode() == "invalid tree topology"
+
+
+def test_plan_check_depths(pg):
+    assert pg.plan_check(5, ps.tree_from_newick_fixed5().ops) == (2, 2)
+    for N in (49, 62, 104, 997, 4000):
+        tr = ps.coalescent_tree(N, np.random.default_rng(N), 1.0)
+        post, pre = pg.plan_check(N, tr.ops)
+        # Sethi-Ullman / smaller-subtree-first bounds: O(log N) stack slots
+        assert 1 <= post <= np.log2(N) + 2 and 1 <= pre <= np.log2(N) + 2, (N, post, pre)
+    N = 500                                  # caterpillar: constant stack
+    ops = [(N, 0, 1)] + [(N + k - 1, N + k - 2, k) for k in range(2, N)]
+    assert pg.plan_check(N, ops) == (1, 1)
+
+
+@pytest.mark.parametrize("bad", [
+    [(5, 0, 1), (6, 2, 3), (7, 5, 6), (8, 7, 4)][:3],           # too few ops
+    [(5, 0, 1), (6, 2, 3), (7, 5, 6), (8, 7, 7)],               # repeated child
+    [(5, 0, 1), (6, 2, 3), (7, 5, 9), (8, 7, 4)],               # child out of range
+    [(5, 0, 1), (6, 2, 7), (7, 5, 3), (8, 6, 4)],               # child used before defined
+    [(5, 0, 1), (6, 0, 3), (7, 5, 6), (8, 7, 4)],               # two parents
+    [(5, 0, 1), (6, 2, 3), (8, 5, 6), (7, 8, 4)],               # root not last
+    [(4, 0, 1), (6, 2, 3), (7, 5, 6), (8, 7, 4)],               # dest is a tip
+])
+def test_plan_check_rejects_bad_topologies(pg, bad):
+    with pytest.raises(pg.PhyloGradError) as ei:
+        pg.plan_check(5, bad)
+    assert ei.value.code in (pg.PG_ERR_TOPOLOGY, pg.PG_ERR_ARG)
+
+
+def test_workspace_bytes(pg):
+    b = pg.workspace_bytes(997, 10000, 4, 4)
+    u = (997 - 2) * 4 * 10016 * 4 * 8
+    assert u < b < u * 1.1
+    assert pg.workspace_bytes(997, 10000, 4, 4, "fp32") < b
+    with pytest.raises(pg.PhyloGradError) as ei:
+        pg.workspace_bytes(10, 10, 300, 1)
+    assert ei.value.code == pg.PG_ERR_UNSUPPORTED
+
+
+def test_shard_range_covers_patterns(pg):
+    for C, w in ((10000, 8), (37, 4), (5, 2)):
+        spans = [pg.shard_range(C, w, r) for r in range(w)]
+        assert spans[0][0] == 0 and spans[-1][1] == C
+        assert all(spans[i][1] == spans[i + 1][0] for i in range(w - 1))

@@ -1,0 +1,240 @@
+"""CUDA path vs the CPU oracle, through the C ABI (pytest -m gpu).
+
+Metric: logL relative error; every gradient
+entry |g - g*| <= tol * max(|g*|, sum_c w_c |d*_c|) where the second term is
+the oracle's condition scale (gradient entries are sums of mixed-sign
+per-pattern terms).  tol = 1e-10 in fp64, 1e-4 in fp32 (BJ:north_star).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import phylo_synth as ps
+
+pytestmark = pytest.mark.gpu
+
+
+def _pg():
+    import paper_2303_04390_b200 as pg
+    return pg
+
+
+def _compare(pb, precision="fp64", tol=None, threads=8, inst=None):
+    pg = _pg()
+    tol = tol or (1e-10 if precision == "fp64" else 1e-4)
+    own = inst is None
+    inst = inst or pg.from_problem(pb, precision=precision)
+    logl, g = inst.compute()
+    ref = oracle.loglik_grad(pb, threads=threads)
+    el = abs(logl - ref["logL"]) / abs(ref["logL"])
+    scale = np.maximum(np.abs(ref["grad"]), ref["grad_abs"])
+    eg = np.abs(g - ref["grad"]) / np.where(scale > 0, scale, 1.0)
+    assert el <= tol, f"{pb.name} {precision}: logL {logl!r} vs {ref['logL']!r} (rel {el:.3e})"
+    bad = np.argmax(eg)
+    assert eg.max() <= tol, (f"{pb.name} {precision}: grad[{bad}] {g[bad]!r} vs {ref['grad'][bad]!r} "
+                             f"(C17 err {eg.max():.3e})")
+    if own:
+        inst.close()
+    return logl, g, ref
+
+
+# --------------------------------------------------------------- configs ----
+
+def test_config0_jc5_fp64():
+    _compare(ps.config0_jc5())
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_dengue_reduced(precision):
+    # several 32-pattern tiles plus a ragged tail, 1% gaps, Gamma-4
+    _compare(ps.config1_dengue(N=150, C=333), precision)
+
+
+@pytest.mark.parametrize("K,R", [(4, 1), (3, 1), (4, 4), (2, 2)])
+def test_mmm_reduced(K, R):
+    _compare(ps.config2_mmm(N=30, C=201, K=K, R=R))
+
+
+def test_mmm_reduced_fp32():
+    _compare(ps.config2_mmm(N=30, C=201), "fp32")
+
+
+def test_yeast_codon_reduced():
+    _compare(ps.config3_yeast(N=20, C=77))
+
+
+def test_wnv_codon_reduced():
+    _compare(ps.config4_wnv(N=30, C=45))
+
+
+def test_codon_fp32_reduced():
+    _compare(ps.config3_yeast(N=16, C=50, precision="fp32"), "fp32")
+
+
+@pytest.mark.slow
+def test_dengue_full_fp64():
+    """BJ:configs[1] at full size in the bench launch configuration."""
+    _compare(ps.config1_dengue(), "fp64", threads=16)
+
+
+@pytest.mark.slow
+def test_dengue_full_fp32():
+    _compare(ps.config1_dengue(precision="fp32"), "fp32", threads=16)
+
+
+@pytest.mark.slow
+def test_mmm_full():
+    _compare(ps.config2_mmm(), threads=16)
+
+
+@pytest.mark.slow
+def test_yeast_full():
+    _compare(ps.config3_yeast(), threads=16)
+
+
+@pytest.mark.slow
+def test_wnv_full():
+    _compare(ps.config4_wnv(), threads=16)
+
+
+# ------------------------------------------------------------ edge cases ----
+
+@pytest.mark.parametrize("model,N,R,C", [("jc", 2, 1, 1), ("hky", 3, 4, 31), ("gtr", 17, 3, 33),
+                                         ("hky", 64, 2, 95), ("mmm2", 9, 3, 40), ("mmm4", 12, 2, 64),
+                                         ("codon", 5, 1, 9), ("codon", 9, 4, 20)])
+def test_small_shapes(model, N, R, C):
+    pb = ps.small_problem(N, model, R=R, C=C, seed=N + C, missing=0.1, simulate=True)
+    _compare(pb)
+
+
+@pytest.mark.parametrize("model", ["hky", "mmm4", "codon"])
+def test_tip_partials_nonstationary_root(model):
+    pb = ps.small_problem(10, model, R=2, C=37, seed=5, partial_tips=True, stationary_root=False,
+                          simulate=True)
+    _compare(pb)
+
+
+def test_caterpillar_tree():
+    pb = ps.small_problem(60, "hky", R=4, C=50, seed=3, simulate=True)
+    N = pb.n_tips
+    ops, prev = [], 0
+    for k in range(1, N):
+        d = N + k - 1
+        ops.append((d, prev, k))
+        prev = d
+    pb.ops = np.array(ops, np.int32)
+    pb.branch_lengths = np.random.default_rng(0).uniform(0.01, 0.1, 2 * N - 2)
+    _compare(pb)
+
+
+def test_zero_branch_lengths_and_unrooted_convention():
+    pb = ps.small_problem(12, "gtr", R=2, C=40, seed=9, simulate=True)
+    d, a, b = pb.ops[-1]
+    pb.branch_lengths[a] = 0.0          # unrooted tree as a zero root branch
+    pb.branch_lengths[3] = 0.0
+    _compare(pb)
+
+
+def test_zero_weights_and_all_missing_patterns():
+    pb = ps.small_problem(15, "hky", R=4, C=70, seed=4, simulate=True)
+    pb.pattern_weights[::3] = 0.0
+    pb.tip_states[:, 5] = pb.states
+    _compare(pb)
+
+
+def test_deep_tree_needs_rescaling():
+    """Without rescaling these partials underflow double (logL < -745/pattern)."""
+    pb = ps.small_problem(300, "mmm4", R=1, C=40, seed=2, root_height=3.0, simulate=True)
+    _compare(pb)
+
+
+def test_zero_likelihood_reports_pattern():
+    pg = _pg()
+    pb = ps.small_problem(6, "hky", R=1, C=40, seed=1)
+    pb.branch_lengths[:] = 0.0
+    pb.tip_states[:, :] = 0
+    pb.tip_states[2, 33] = 1                      # impossible with P(0) = I
+    inst = pg.from_problem(pb)
+    with pytest.raises(pg.PhyloGradError) as ei:
+        inst.compute()
+    assert ei.value.code == pg.PG_ERR_ZERO_LIKELIHOOD
+    assert "33" in str(ei.value)
+    assert inst.check_status() == 33
+
+
+# --------------------------------------------------- boundary behaviour ----
+
+def test_branch_lengths_update_between_computes_and_determinism():
+    pg = _pg()
+    pb = ps.config1_dengue(N=80, C=200)
+    inst = pg.from_problem(pb)
+    l1, g1 = inst.compute()
+    l1b, g1b = inst.compute()
+    assert l1 == l1b and np.array_equal(g1, g1b)      # bitwise reproducible (no atomics)
+    rng = np.random.default_rng(0)
+    for _ in range(3):
+        pb.branch_lengths = pb.branch_lengths * rng.uniform(0.9, 1.1, pb.branch_lengths.shape)
+        inst.set_branch_lengths(pb.branch_lengths)
+        _compare(pb, inst=inst)
+    inst.close()
+
+
+def test_device_path_matches_host_path():
+    pg = _pg()
+    import torch
+    pb = ps.config1_dengue(N=60, C=150)
+    inst = pg.from_problem(pb)
+    logl, g = inst.compute()
+    out = torch.zeros(2 * pb.n_tips - 1, dtype=torch.float64, device="cuda")
+    bl = torch.tensor(pb.branch_lengths, dtype=torch.float64, device="cuda")
+    with torch.cuda.stream(inst.stream):
+        inst.set_branch_lengths_device(bl)
+        inst.compute_device(out)
+    inst.stream.synchronize()
+    o = out.cpu().numpy()
+    assert o[0] == logl and np.array_equal(o[1:], g)
+    assert inst.check_status() == -1
+
+
+def test_sequencing_errors_and_replanning():
+    pg = _pg()
+    pb = ps.small_problem(8, "hky", R=2, C=20, seed=1, simulate=True)
+    inst = pg.Instance(pb.n_tips, pb.patterns, 4, 2)
+    with pytest.raises(pg.PhyloGradError) as ei:
+        inst.compute()
+    assert ei.value.code == pg.PG_ERR_SEQUENCE
+    inst.close()
+    inst = pg.from_problem(pb)
+    _compare(pb, inst=inst)
+    # a different topology on the same instance re-plans and re-captures
+    pb2 = ps.small_problem(8, "hky", R=2, C=20, seed=77, simulate=True)
+    pb2.tip_states, pb2.pattern_weights = pb.tip_states, pb.pattern_weights
+    pb2.evec, pb2.ievec, pb2.evals, pb2.Q, pb2.pi = pb.evec, pb.ievec, pb.evals, pb.Q, pb.pi
+    pb2.cat_rates, pb2.cat_weights = pb.cat_rates, pb.cat_weights
+    inst.set_operations(pb2.ops)
+    inst.set_branch_lengths(pb2.branch_lengths)
+    _compare(pb2, inst=inst)
+    with pytest.raises(pg.PhyloGradError) as ei:
+        inst.set_branch_lengths(-np.ones(14))
+    assert ei.value.code == pg.PG_ERR_DOMAIN
+    inst.close()
+
+
+def test_caller_owned_stream_and_virtual_sharding():
+    """T3(a): g instances over disjoint pattern shards on one GPU, summed,
+    equal the unsharded evaluation (the multi-GPU maths without g GPUs)."""
+    pg = _pg()
+    pb = ps.config1_dengue(N=100, C=500)
+    full = pg.from_problem(pb)
+    l0, g0 = full.compute()
+    lt, gt = 0.0, np.zeros_like(g0)
+    for rank in range(4):
+        lo, hi = pg.shard_range(pb.patterns, 4, rank)
+        inst = pg.from_problem(pb, lo=lo, hi=hi)
+        l, g = inst.compute()
+        lt += l
+        gt += g
+        inst.close()
+    assert abs(lt - l0) <= 1e-13 * abs(l0)
+    ref = oracle.loglik_grad(pb, threads=8)
+    assert np.max(np.abs(gt - g0) / ref["grad_abs"]) < 1e-13
