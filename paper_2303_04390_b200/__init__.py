@@ -28,7 +28,7 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "phylograd.h")
 if not os.path.exists(LIB_PATH):
     raise ImportError(
         f"native library {LIB_PATH} is missing; build it with "
-        "`python -m paper_2303_04390_b200.build` (nvcc, sm_100a). There is no fallback.")
+        "`python paper_2303_04390_b200/build.py` (nvcc, sm_100a). There is no fallback.")
 
 _lib = ctypes.CDLL(LIB_PATH)
 
@@ -81,6 +81,9 @@ _SIGS = {
     "pg_strerror": ([ctypes.c_int], ctypes.c_char_p),
 }
 for _name, (_args, _res) in _SIGS.items():
+    if not hasattr(_lib, _name):
+        raise ImportError(f"{LIB_PATH} lacks {_name} (stale build); rebuild with "
+                          "`python paper_2303_04390_b200/build.py`")
     _f = getattr(_lib, _name)
     _f.argtypes = _args
     _f.restype = _res

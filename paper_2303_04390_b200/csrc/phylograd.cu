@@ -537,7 +537,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
     const Layout &L = inst->L;
     const int R = inst->cfg.categories;
     CK(cudaMemsetAsync(inst->at<int>(L.off_status), 0x7f, sizeof(int), inst->stream), "status reset");
-    if (inst->timing) CK(cudaEventRecord(inst->ev[0], inst->stream), "event");
+    if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[0], inst->stream, cudaEventRecordExternal), "event");
     {
         void *fn = pmat_kernel_fn(L);
         const double *V = inst->at<double>(L.off_V), *Vi = inst->at<double>(L.off_Vi),
@@ -549,14 +549,14 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         void *args[] = {&V, &Vi, &lam, &rates, &bl, &S, (void *)&R, &P, &PT};
         CK(cudaLaunchKernel(fn, dim3(L.B * R), dim3(std::min(256, L.SP * L.SP)), args, 0, inst->stream), "pmat launch");
     }
-    if (inst->timing) CK(cudaEventRecord(inst->ev[1], inst->stream), "event");
+    if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[1], inst->stream, cudaEventRecordExternal), "event");
     {
         pg::TravArgs a = trav_args(inst);
         void *args[] = {&a};
         CK(cudaLaunchKernel(traverse_fn(L), dim3(inst->grid), dim3(inst->block), args, inst->smem, inst->stream),
            "traverse launch");
     }
-    if (inst->timing) CK(cudaEventRecord(inst->ev[2], inst->stream), "event");
+    if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[2], inst->stream, cudaEventRecordExternal), "event");
     {
         const double *gp = inst->at<double>(L.off_gpart), *lp = inst->at<double>(L.off_lpart);
         int B = L.B, nt = L.n_tiles;
@@ -564,7 +564,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         CK(cudaLaunchKernel((void *)pg::reduce_kernel, dim3(L.B + 1), dim3(256), args, 0, inst->stream),
            "reduce launch");
     }
-    if (inst->timing) CK(cudaEventRecord(inst->ev[3], inst->stream), "event");
+    if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[3], inst->stream, cudaEventRecordExternal), "event");
     return PG_OK;
 }
 
