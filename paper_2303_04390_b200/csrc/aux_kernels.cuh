@@ -6,7 +6,7 @@ namespace pg {
 
 // A1 -- Eq. 1: P^{(r)}(b_i) = V diag(exp(gamma_r b_i lambda)) V^{-1}
 // for every branch i and category r, in the compute precision, zero padded to
-// SP x SP.  One CTA per (branch, category): the S exponentials go to shared
+// SP x SP (category blocks `cs` Reals apart).  One CTA per (branch, category): the S exponentials go to shared
 // memory, then every thread forms entries of P and (optionally) P'.  Padded
 // rows/columns are exactly 0.  The work is ~2% of an evaluation.
 template <typename Real, int SP>
@@ -15,14 +15,14 @@ __global__ void __launch_bounds__(256) pmat_kernel(const double *__restrict__ V,
                                                    const double *__restrict__ lam,
                                                    const double *__restrict__ rates,
                                                    const double *__restrict__ bl, int S, int R,
-                                                   Real *__restrict__ P, Real *__restrict__ PT) {
+                                                   int cs, Real *__restrict__ P, Real *__restrict__ PT) {
     __shared__ double e[SP];
     const int br = blockIdx.x;          // branch * R + r
     const int r = br % R, b = br / R;
     const double t = rates[r] * bl[b];
     for (int k = threadIdx.x; k < SP; k += blockDim.x) e[k] = k < S ? exp(lam[k] * t) : 0.0;
     __syncthreads();
-    Real *Pm = P + (size_t)br * SP * SP;
+    Real *Pm = P + (size_t)br * cs;     // cs = category stride (>= SP*SP, zero padded)
     Real *PTm = PT ? PT + (size_t)br * SP * SP : nullptr;
     for (int idx = threadIdx.x; idx < SP * SP; idx += blockDim.x) {
         const int s = idx / SP, u = idx % SP;

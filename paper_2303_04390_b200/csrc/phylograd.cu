@@ -30,7 +30,7 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
 
 struct Layout {
-    int SP = 0, variant = 0, Cpad = 0, n_tiles = 0, B = 0, tpl = 32;
+    int SP = 0, variant = 0, Cpad = 0, n_tiles = 0, B = 0, tpl = 32, cat_stride = 0;
     size_t real = 8;
     size_t off_P, off_PT, off_Q, off_QT, off_pi, off_V, off_Vi, off_lam, off_rates, off_cw,
         off_bl, off_patw, off_tips, off_tipp, off_u, off_gpart, off_lpart, off_out, off_status,
@@ -68,7 +68,9 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
             if (err) *err = "too many rate categories for this state count (max 16; 8 for S > 8)";
             return PG_ERR_UNSUPPORTED;
         }
-        L->tpl = 32;
+        int Rp = 1;
+        while (Rp < R) Rp <<= 1;
+        L->tpl = 32 / Rp;      // patterns per warp tile (lane = pattern x category)
     } else {
         if (R > 16) { if (err) *err = "too many rate categories (max 16)"; return PG_ERR_UNSUPPORTED; }
         L->tpl = (L->real == 8) ? pg::LargeCfg<double, 64>::tpl(R) : pg::LargeCfg<float, 64>::tpl(R);
@@ -78,11 +80,13 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
     L->Cpad = (int)((C + 31) / 32 * 32);
     L->n_tiles = L->Cpad / L->tpl;
     L->B = (int)(2 * N - 2);
-    const size_t mats = (size_t)L->B * R * SP * SP * L->real;
+    // small-S kernels read P with a padded category stride (SmallCfg::CS)
+    L->cat_stride = SP * SP + ((L->variant == 0 && R > 1) ? (int)(16 / L->real) : 0);
+    const size_t mats = (size_t)L->B * R * L->cat_stride * L->real;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t at = o; o = align_up(o + bytes); return at; };
     L->off_P = take(mats);
-    L->off_PT = take(L->variant == 1 ? mats : 0);
+    L->off_PT = take(L->variant == 1 ? (size_t)L->B * R * SP * SP * L->real : 0);
     L->off_Q = take((size_t)SP * SP * L->real);
     L->off_QT = take((size_t)SP * SP * L->real);
     L->off_pi = take((size_t)SP * L->real);
@@ -413,19 +417,37 @@ int pg_set_branch_lengths_device(pg_instance *inst, const double *d_b) {
 // launch configuration
 // -------------------------------------------------------------------------
 
-template <typename Real, int SP>
-static void *small_kernel() { return (void *)pg::traverse_small_kernel<Real, SP>; }
+template <typename Real, int SP, int RP>
+static void *small_kernel() { return (void *)pg::traverse_small_kernel<Real, SP, RP>; }
 template <typename Real, int SP>
 static void *large_kernel() { return (void *)pg::traverse_large_kernel<Real, SP>; }
 template <typename Real, int SP>
 static void *pmat_fn() { return (void *)pg::pmat_kernel<Real, SP>; }
 
-static void *traverse_fn(const Layout &L) {
+static int pad_categories(int R) {
+    int p = 1;
+    while (p < R) p <<= 1;
+    return p;
+}
+
+template <typename Real, int SP>
+static void *small_by_rp(int RP) {
+    switch (RP) {
+        case 1: return small_kernel<Real, SP, 1>();
+        case 2: return small_kernel<Real, SP, 2>();
+        case 4: return small_kernel<Real, SP, 4>();
+        case 8: return small_kernel<Real, SP, 8>();
+        default: return small_kernel<Real, SP, 16>();
+    }
+}
+
+static void *traverse_fn(const Layout &L, int R) {
     const bool d = L.real == 8;
+    const int RP = pad_categories(R);
     switch (L.SP) {
-        case 4: return d ? small_kernel<double, 4>() : small_kernel<float, 4>();
-        case 8: return d ? small_kernel<double, 8>() : small_kernel<float, 8>();
-        case 16: return d ? small_kernel<double, 16>() : small_kernel<float, 16>();
+        case 4: return d ? small_by_rp<double, 4>(RP) : small_by_rp<float, 4>(RP);
+        case 8: return d ? small_by_rp<double, 8>(RP) : small_by_rp<float, 8>(RP);
+        case 16: return d ? small_by_rp<double, 16>(RP) : small_by_rp<float, 16>(RP);
         case 32: return d ? large_kernel<double, 32>() : large_kernel<float, 32>();
         case 64: return d ? large_kernel<double, 64>() : large_kernel<float, 64>();
     }
@@ -443,10 +465,24 @@ static void *pmat_kernel_fn(const Layout &L) {
     return nullptr;
 }
 
-static size_t small_smem(const Layout &L, int R, int D, int depth) {
-    const size_t nthr = (size_t)R * 32;
-    return (size_t)2 * 4 * nthr * 8 + (size_t)2 * 2 * nthr * 4 + (size_t)D * 2 * nthr * L.SP * L.real +
-           (size_t)depth * nthr * L.SP * L.real;
+template <typename Real, int SP>
+static size_t small_smem_t(int RP, int R, int depth) {
+    switch (RP) {
+        case 1: return pg::SmallCfg<Real, SP, 1>::smem(1, depth);
+        case 2: return pg::SmallCfg<Real, SP, 2>::smem(2, depth);
+        case 4: return pg::SmallCfg<Real, SP, 4>::smem(R, depth);
+        case 8: return pg::SmallCfg<Real, SP, 8>::smem(R, depth);
+        default: return pg::SmallCfg<Real, SP, 16>::smem(R, depth);
+    }
+}
+static size_t small_smem(const Layout &L, int R, int depth) {
+    const bool d = L.real == 8;
+    const int RP = pad_categories(R);
+    switch (L.SP) {
+        case 4: return d ? small_smem_t<double, 4>(RP, R, depth) : small_smem_t<float, 4>(RP, R, depth);
+        case 8: return d ? small_smem_t<double, 8>(RP, R, depth) : small_smem_t<float, 8>(RP, R, depth);
+        default: return d ? small_smem_t<double, 16>(RP, R, depth) : small_smem_t<float, 16>(RP, R, depth);
+    }
 }
 static size_t large_smem(const Layout &L, int R, int depth) {
     const size_t nvec = (size_t)L.tpl * R;
@@ -458,24 +494,13 @@ static int configure(pg_instance *inst) {
     const Layout &L = inst->L;
     const int R = inst->cfg.categories;
     const int depth = std::max(inst->plan.post_depth, inst->plan.pre_depth);
-    void *fn = traverse_fn(L);
+    void *fn = traverse_fn(L, R);
     inst->grid = L.n_tiles;
     if (L.variant == 0) {
-        inst->block = R * 32;
-        int best_D = 2, best_waves = INT_MAX;
-        for (int D = 6; D >= 2; --D) {
-            size_t sm = small_smem(L, R, D, depth);
-            if (sm > 227 * 1024) continue;
-            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "smem attr");
-            int occ = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, inst->block, sm), "occupancy");
-            if (occ < 1) continue;
-            int waves = (inst->grid + occ * inst->sm_count - 1) / (occ * inst->sm_count);
-            if (waves < best_waves) { best_waves = waves; best_D = D; }
-        }
-        if (best_waves == INT_MAX) return inst->fail(PG_ERR_UNSUPPORTED, "traversal does not fit in shared memory");
-        inst->prefetch = best_D;
-        inst->smem = (int)small_smem(L, R, best_D, depth);
+        inst->block = 32;     // one warp per CTA, warps fully independent
+        inst->prefetch = (L.SP <= 8) ? 4 : 2;
+        inst->smem = (int)small_smem(L, R, depth);
+        if (inst->smem > 227 * 1024) return inst->fail(PG_ERR_UNSUPPORTED, "traversal does not fit in shared memory");
     } else {
         inst->block = L.tpl * R * (L.SP / 4);
         inst->prefetch = 0;
@@ -546,14 +571,15 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         int S = inst->cfg.states;
         void *P = inst->ws + L.off_P;
         void *PT = L.variant == 1 ? inst->ws + L.off_PT : nullptr;
-        void *args[] = {&V, &Vi, &lam, &rates, &bl, &S, (void *)&R, &P, &PT};
+        int cs = L.cat_stride;
+        void *args[] = {&V, &Vi, &lam, &rates, &bl, &S, (void *)&R, &cs, &P, &PT};
         CK(cudaLaunchKernel(fn, dim3(L.B * R), dim3(std::min(256, L.SP * L.SP)), args, 0, inst->stream), "pmat launch");
     }
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[1], inst->stream, cudaEventRecordExternal), "event");
     {
         pg::TravArgs a = trav_args(inst);
         void *args[] = {&a};
-        CK(cudaLaunchKernel(traverse_fn(L), dim3(inst->grid), dim3(inst->block), args, inst->smem, inst->stream),
+        CK(cudaLaunchKernel(traverse_fn(L, inst->cfg.categories), dim3(inst->grid), dim3(inst->block), args, inst->smem, inst->stream),
            "traverse launch");
     }
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[2], inst->stream, cudaEventRecordExternal), "event");
