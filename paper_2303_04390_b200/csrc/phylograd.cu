@@ -146,7 +146,7 @@ struct pg_instance {
     int *status_pinned = nullptr;
     bool bl_host_pending = false;
     // launch configuration
-    int prefetch = 4, smem = 0, grid = 0, block = 0;
+    int prefetch = 4, smem = 0, grid = 0, block = 0, tiles_per_cta = 1;
     cudaGraphExec_t gexec = nullptr;
     double *gexec_out = nullptr;
     bool timing = false;
@@ -466,22 +466,22 @@ static void *pmat_kernel_fn(const Layout &L) {
 }
 
 template <typename Real, int SP>
-static size_t small_smem_t(int RP, int R, int depth) {
+static size_t small_smem_t(int RP, int R, int K, int depth) {
     switch (RP) {
-        case 1: return pg::SmallCfg<Real, SP, 1>::smem(1, depth);
-        case 2: return pg::SmallCfg<Real, SP, 2>::smem(2, depth);
-        case 4: return pg::SmallCfg<Real, SP, 4>::smem(R, depth);
-        case 8: return pg::SmallCfg<Real, SP, 8>::smem(R, depth);
-        default: return pg::SmallCfg<Real, SP, 16>::smem(R, depth);
+        case 1: return pg::SmallCfg<Real, SP, 1>::smem(R, K, depth);
+        case 2: return pg::SmallCfg<Real, SP, 2>::smem(R, K, depth);
+        case 4: return pg::SmallCfg<Real, SP, 4>::smem(R, K, depth);
+        case 8: return pg::SmallCfg<Real, SP, 8>::smem(R, K, depth);
+        default: return pg::SmallCfg<Real, SP, 16>::smem(R, K, depth);
     }
 }
-static size_t small_smem(const Layout &L, int R, int depth) {
+static size_t small_smem(const Layout &L, int R, int K, int depth) {
     const bool d = L.real == 8;
     const int RP = pad_categories(R);
     switch (L.SP) {
-        case 4: return d ? small_smem_t<double, 4>(RP, R, depth) : small_smem_t<float, 4>(RP, R, depth);
-        case 8: return d ? small_smem_t<double, 8>(RP, R, depth) : small_smem_t<float, 8>(RP, R, depth);
-        default: return d ? small_smem_t<double, 16>(RP, R, depth) : small_smem_t<float, 16>(RP, R, depth);
+        case 4: return d ? small_smem_t<double, 4>(RP, R, K, depth) : small_smem_t<float, 4>(RP, R, K, depth);
+        case 8: return d ? small_smem_t<double, 8>(RP, R, K, depth) : small_smem_t<float, 8>(RP, R, K, depth);
+        default: return d ? small_smem_t<double, 16>(RP, R, K, depth) : small_smem_t<float, 16>(RP, R, K, depth);
     }
 }
 static size_t large_smem(const Layout &L, int R, int depth) {
@@ -497,9 +497,15 @@ static int configure(pg_instance *inst) {
     void *fn = traverse_fn(L, R);
     inst->grid = L.n_tiles;
     if (L.variant == 0) {
-        inst->block = 32;     // one warp per CTA, warps fully independent
+        // CTA = K tile warps + 1 producer warp; K = tiles / SMs (one wave), at
+        // most 9 (launch bounds) and within the shared-memory budget.
+        int K = std::max(1, std::min(9, (L.n_tiles + inst->sm_count - 1) / inst->sm_count));
+        while (K > 1 && small_smem(L, R, K, depth) > 227 * 1024) --K;
+        inst->tiles_per_cta = K;
+        inst->block = 32 * (K + 1);
+        inst->grid = (L.n_tiles + K - 1) / K;
         inst->prefetch = (L.SP <= 8) ? 4 : 2;
-        inst->smem = (int)small_smem(L, R, depth);
+        inst->smem = (int)small_smem(L, R, K, depth);
         if (inst->smem > 227 * 1024) return inst->fail(PG_ERR_UNSUPPORTED, "traversal does not fit in shared memory");
     } else {
         inst->block = L.tpl * R * (L.SP / 4);

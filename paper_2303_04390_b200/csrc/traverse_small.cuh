@@ -8,14 +8,17 @@
 //   * lane = (pattern, category), category fastest (RP = R rounded up to a
 //     power of two; lanes with category >= R shadow category R-1 with zero
 //     weight).  Each lane keeps the SP states of its vector in registers.
-//   * The two per-pattern programs (schedule.hpp) are static, so every input
-//     of a step is fetched ahead of time by lane 0 with 1-D bulk copies (TMA
-//     engine, mbarrier completion) into a D-stage shared-memory ring: ops in
-//     32-op chunks, the R transition matrices of each branch involved (one
-//     contiguous copy) and the warp's contiguous u chunk or tip codes of each
-//     child.  HBM-resident u chunks are also pulled into L2 PF steps ahead
-//     (bulk prefetch).  The dependent chain of a step touches only registers
-//     and shared memory.
+//   * A CTA is K such warps (K consecutive tiles, K = ceil(tiles / #SMs) so the
+//     grid is one wave) plus one PRODUCER warp.  The two per-pattern programs
+//     (schedule.hpp) are static and identical for every tile, so the producer
+//     walks them D steps ahead of the consumers and, per step, issues 1-D bulk
+//     copies (TMA engine, mbarrier transaction counts) into a D-stage shared
+//     ring: the op, the R transition matrices of each branch involved (one
+//     contiguous copy, shared by the K warps) and each child's u chunk or tip
+//     codes for all K tiles (contiguous in HBM: one copy).  u chunks are also
+//     pulled into L2 PF steps ahead (bulk prefetch).  Consumers wait on the
+//     stage's "full" barrier, compute, and arrive on its "empty" barrier; the
+//     dependent chain of a step touches only registers and shared memory.
 //   * post program (Eq. 2): p_k = u_a o u_b; u_k = P_k p_k streamed to HBM
 //     once and kept on a per-lane stack for the parent.
 //   * root (Eq. 3): L_c = sum_r P(gamma_r) pi' p_root; logL partial per tile.
@@ -39,32 +42,34 @@
 
 namespace pg {
 
-// ---- compile-time shape of one warp's work --------------------------------
-// Global layout of the transition matrices for this kernel: per branch, R
-// category blocks of SP*SP Reals padded to CS bytes (16 extra bytes when
-// R > 1 so the categories of a warp hit distinct shared-memory banks); one
-// branch's matrices are one contiguous bulk copy.
+// ---- shape of one CTA's work ----------------------------------------------
+// A CTA = K consumer warps (one pattern tile each) + 1 producer warp.  Global
+// layout of the transition matrices for this kernel: per branch, R category
+// blocks of SP*SP Reals padded to CS bytes (16 extra bytes when R > 1 so the
+// categories of a warp hit distinct shared-memory banks): one branch's
+// matrices are one contiguous bulk copy.
 template <typename Real, int SP, int RP>
 struct SmallCfg {
     static constexpr int TP = 32 / RP;                        // patterns per warp tile
-    static constexpr int D = (SP <= 8) ? 4 : 2;                // bulk-copy ring depth
+    static constexpr int D = (SP <= 8) ? 4 : 2;                // stage ring depth
     static constexpr int PF = 16;                              // L2 prefetch distance (steps)
     static constexpr int W = 2;                                // gradient window (steps)
     static constexpr int VB = SP * (int)sizeof(Real);          // vector bytes
     static constexpr int MATB = SP * SP * (int)sizeof(Real);   // one category's matrix
     static constexpr int CS = MATB + (RP > 1 ? 16 : 0);        // padded category stride
-    static constexpr int TIPW = TP > 16 ? TP : 16;             // tip-code window bytes
-    static constexpr int OPS = 64 * 16;                        // 2 x 32-op chunks
-    static constexpr int ND = W * 2 * 32 * 16;                 // (num, den) window
+    static constexpr int ND = W * 2 * 32 * 16;                 // (num, den) window per warp
+    static constexpr int BARS = 128;                           // mbarrier area
     static __host__ __device__ int mat_slot(int R) { return R * CS; }
-    static __host__ __device__ int vss() { return TP * VB > TIPW ? TP * VB : TIPW; }      // post vec slot
-    static __host__ __device__ int vsb(int R) { return TP * R * VB > vss() ? TP * R * VB : vss(); }  // pre
-    static __host__ __device__ int stage(int R) {
-        const int a = 3 * mat_slot(R) + 2 * vss(), b = 2 * mat_slot(R) + 2 * vsb(R);
-        return ((a > b ? a : b) + 15) / 16 * 16;
+    static __host__ __device__ int vslot(int R, int K) {       // one child's vectors for K warps
+        int a = K * TP * R * VB, b = K * TP * VB, c = (15 + K * TP + 15) / 16 * 16;
+        int m = a > b ? a : b;
+        m = m > c ? m : c;
+        return (m + 15) / 16 * 16;
     }
-    static __host__ __device__ size_t smem(int R, int depth) {
-        return 64 + (size_t)OPS + ND + (size_t)D * stage(R) + (size_t)depth * 32 * VB + TP * 8;
+    static __host__ __device__ int stage(int R, int K) { return 16 + 3 * mat_slot(R) + 2 * vslot(R, K); }
+    static __host__ __device__ int warp_bytes(int depth) { return (depth * 32 * VB + ND + TP * 8 + W * 2 * 4 + 8 + 15) / 16 * 16; }
+    static __host__ __device__ size_t smem(int R, int K, int depth) {
+        return (size_t)BARS + (size_t)D * stage(R, K) + (size_t)K * warp_bytes(depth);
     }
 };
 
@@ -200,140 +205,165 @@ __device__ __forceinline__ int maybe_rescale(Real (&v)[SP]) {
 
 
 template <typename Real, int SP, int RP>
-__global__ void __launch_bounds__(32) traverse_small_kernel(const TravArgs a) {
+__global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a) {
     using Cfg = SmallCfg<Real, SP, RP>;
     constexpr int TP = Cfg::TP, D = Cfg::D, PF = Cfg::PF, W = Cfg::W, VB = Cfg::VB, CS = Cfg::CS;
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem_s[];
+    unsigned char *smem = smem_s;
     const int R = a.R, N = a.N, S = a.S;
-    const int lane = threadIdx.x;
-    const int cat = lane & (RP - 1);
-    const int r = min(cat, R - 1);                  // shadow lanes reuse category R-1
-    const bool live = cat < R;
-    const int pl = lane / RP;                       // pattern within the tile
-    const int tile = blockIdx.x;
-    const int pat0 = tile * TP;
-    const int pat = pat0 + pl;                      // < Cpad
-    const int root = 2 * N - 2;
-    const int nops = N - 1;
-    const int MS = Cfg::mat_slot(R), VSS = Cfg::vss(), VSB = Cfg::vsb(R), ST = Cfg::stage(R);
+    const int K = blockDim.x / 32 - 1;              // consumer warps; warp K = producer
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nops = N - 1, root = 2 * N - 2;
+    const int MS = Cfg::mat_slot(R), VS = Cfg::vslot(R, K), ST = Cfg::stage(R, K);
+    const size_t Cpad = (size_t)a.Cpad;
+    const int cta_tile0 = blockIdx.x * K;
+    const int ntile = min(K, a.n_tiles - cta_tile0);               // live tiles of this CTA
+    const int cta_pat0 = cta_tile0 * TP;
+    const size_t u_node = Cpad * R * VB;                           // one node's u block (bytes)
 
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem);                          // [D] stages + [1] prologue
-    Op4 *opbuf = reinterpret_cast<Op4 *>(smem + 64);
-    double2 *nd = reinterpret_cast<double2 *>(smem + 64 + Cfg::OPS);              // [W][2][32]
-    unsigned char *stages = smem + 64 + Cfg::OPS + Cfg::ND;
-    unsigned char *stackb = stages + D * ST;
-    double *wbuf = reinterpret_cast<double *>(stackb + (size_t)a.depth * 32 * VB); // [TP]
-
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);            // [D]
+    uint64_t *empty = full + D;                                     // [D]
+    uint64_t *post_done = empty + D;                                // [1]
+    unsigned char *stages = smem + Cfg::BARS;
     const char *__restrict__ Pb = static_cast<const char *>(a.P);
     const char *__restrict__ tipP = static_cast<const char *>(a.tip_partials);
     const uint8_t *__restrict__ tipS = a.tip_states;
     char *__restrict__ Ub = static_cast<char *>(a.u);
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < D; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, K); }
+        mbar_init(post_done, K);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // =============================== producer ===================================
+    if (warp == K) {
+        const unsigned u_bytes = ntile * TP * R * VB;
+        const size_t u_cta = (size_t)cta_pat0 * R * VB;
+        const unsigned tipp_bytes = ntile * TP * VB;
+        const int tip_lead = cta_pat0 & 15;
+        const unsigned tipw_bytes = (tip_lead + ntile * TP + 15) / 16 * 16;
+        auto tip_bytes = [&](int code) -> unsigned { return (code & kTipPartialBit) ? tipp_bytes : tipw_bytes; };
+        auto copy_tip = [&](unsigned char *dst, int code, uint64_t *bar) {
+            const int node = code & ~kTipPartialBit;
+            if (code & kTipPartialBit) bulk_g2s(dst, tipP + ((size_t)node * Cpad + cta_pat0) * VB, tipp_bytes, bar);
+            else bulk_g2s(dst, tipS + ((size_t)node * Cpad + cta_pat0 - tip_lead), tipw_bytes, bar);
+        };
+        auto u_src = [&](int node) -> const char * { return Ub + (size_t)(node - N) * u_node + u_cta; };
+        for (int t = 0; t < 2 * nops; ++t) {
+            const bool pre = t >= nops;
+            const int m = pre ? t - nops : t;
+            if (t == nops) mbar_wait(post_done, 0);       // u of every tile stored + fenced
+            if (t >= D) mbar_wait(empty + t % D, (uint32_t)(t / D + 1) & 1u);
+            if (lane == 0) {
+                unsigned char *st = stages + (t % D) * ST;
+                uint64_t *bar = full + t % D;
+                const Op4 *prog = pre ? a.pre : a.post;
+                const Op4 op = prog[m];
+                fence_proxy_async_smem();
+                if (!pre) {
+                    // [op][P_k][P_a][P_b][tip a][tip b]
+                    const unsigned bytes = 16 + (op.x != root ? MS : 0) + (op.y >= 0 ? MS + tip_bytes(op.y) : 0) +
+                                           (op.z >= 0 ? MS + tip_bytes(op.z) : 0);
+                    mbar_arrive_expect_tx(bar, bytes);
+                    bulk_g2s(st, prog + m, 16, bar);
+                    if (op.x != root) bulk_g2s(st + 16, Pb + (size_t)op.x * MS, MS, bar);
+                    if (op.y >= 0) {
+                        bulk_g2s(st + 16 + MS, Pb + (size_t)(op.y & ~kTipPartialBit) * MS, MS, bar);
+                        copy_tip(st + 16 + 3 * MS, op.y, bar);
+                    }
+                    if (op.z >= 0) {
+                        bulk_g2s(st + 16 + 2 * MS, Pb + (size_t)(op.z & ~kTipPartialBit) * MS, MS, bar);
+                        copy_tip(st + 16 + 3 * MS + VS, op.z, bar);
+                    }
+                } else {
+                    // [op][P_a][P_b][-][vec a][vec b]
+                    const int na = op.y & ~kTipPartialBit, nb = op.z & ~kTipPartialBit;
+                    const unsigned bytes = 16 + 2 * MS + (na >= N ? u_bytes : tip_bytes(op.y)) +
+                                           (nb >= N ? u_bytes : tip_bytes(op.z));
+                    mbar_arrive_expect_tx(bar, bytes);
+                    bulk_g2s(st, prog + m, 16, bar);
+                    bulk_g2s(st + 16, Pb + (size_t)na * MS, MS, bar);
+                    bulk_g2s(st + 16 + MS, Pb + (size_t)nb * MS, MS, bar);
+                    if (na >= N) bulk_g2s(st + 16 + 3 * MS, u_src(na), u_bytes, bar);
+                    else copy_tip(st + 16 + 3 * MS, op.y, bar);
+                    if (nb >= N) bulk_g2s(st + 16 + 3 * MS + VS, u_src(nb), u_bytes, bar);
+                    else copy_tip(st + 16 + 3 * MS + VS, op.z, bar);
+                    if (m + PF < nops) {                         // pull later u chunks into L2
+                        const Op4 o2 = prog[m + PF];
+                        const int pa = o2.y & ~kTipPartialBit, pb = o2.z & ~kTipPartialBit;
+                        if (pa >= N) prefetch_l2(u_src(pa), u_bytes);
+                        if (pb >= N) prefetch_l2(u_src(pb), u_bytes);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        return;
+    }
+
+    // =============================== consumers ==================================
+    const int tile = cta_tile0 + warp;
+    const bool active = warp < ntile;
+    const int cat = lane & (RP - 1);
+    const int r = min(cat, R - 1);                  // shadow lanes reuse category R-1
+    const bool live = cat < R;
+    const int pl = lane / RP;
+    const int pat0 = tile * TP;
+    const int pat = pat0 + pl;
+    unsigned char *wsm = stages + D * ST + (size_t)warp * Cfg::warp_bytes(a.depth);
+    unsigned char *stackb = wsm;
+    double2 *nd = reinterpret_cast<double2 *>(wsm + a.depth * 32 * VB);          // [W][2][32]
+    double *wbuf = reinterpret_cast<double *>(wsm + a.depth * 32 * VB + Cfg::ND); // [TP]
+    int *nodes_w = reinterpret_cast<int *>(wbuf + TP);                            // [W][2] branch ids
     const double wr = live ? a.cat_w[r] : 0.0;
     const double gwr = wr * a.cat_g[r];
     Real pi[SP];
 #pragma unroll
     for (int s = 0; s < SP; ++s) pi[s] = static_cast<const Real *>(a.pi)[s];
-    if (lane < TP) wbuf[lane] = a.pat_w[pat0 + lane];
-    if (lane == 0) {
-        for (int i = 0; i <= D; ++i) mbar_init(bars + i, 1);
-        fence_mbar_init();
-    }
+    if (active && lane < TP) wbuf[lane] = a.pat_w[pat0 + lane];
     __syncwarp();
 
-    // constant offsets
-    const size_t Cpad = (size_t)a.Cpad;
-    const size_t u_node = Cpad * R * VB;                           // one node's u block (bytes)
-    const size_t u_warp = (size_t)pat0 * R * VB;                   // this warp's contiguous chunk
-    const unsigned u_chunk = TP * R * VB;
-    const unsigned u_vec = (pl * R + r) * VB;                      // my vector inside a u chunk
-    const int tip_off = pat0 & 15;                                 // my tile inside a tip window
     const unsigned mat_lane = r * CS;
-
-    auto op_at = [&](int n) -> Op4 { return opbuf[(n >> 5 & 1) * 32 + (n & 31)]; };
-    auto stage_at = [&](int t) -> unsigned char * { return stages + (t & (D - 1)) * ST; };
-    auto bar_at = [&](int t) -> uint64_t * { return bars + (t & (D - 1)); };
-    auto parity_at = [&](int t) -> uint32_t { return (uint32_t)(t / D) & 1u; };
+    const unsigned u_vec = ((warp * TP + pl) * R + r) * VB;        // my vector inside a CTA u chunk
+    const int tip_idx = (cta_pat0 & 15) + warp * TP + pl;          // my code inside a tip window
+    const unsigned tipp_vec = (warp * TP + pl) * VB;               // my tip partial vector
+    const size_t u_lane = (size_t)pat * R * VB + r * VB;
     auto stack_at = [&](int slot) -> unsigned char * { return stackb + (slot * 32 + lane) * VB; };
-    auto tip_bytes = [&](int code) -> unsigned { return (code & kTipPartialBit) ? TP * VB : Cfg::TIPW; };
-    // lane 0: bulk copy of tip data (16-B window of codes, or the tile's partial vectors)
-    auto copy_tip = [&](unsigned char *dst, int code, uint64_t *bar) {
-        const int node = code & ~kTipPartialBit;
-        if (code & kTipPartialBit) bulk_g2s(dst, tipP + ((size_t)node * Cpad + pat0) * VB, TP * VB, bar);
-        else bulk_g2s(dst, tipS + (((size_t)node * Cpad + pat0) & ~(size_t)15), Cfg::TIPW, bar);
+    auto release = [&](int t) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + t % D);
     };
-    auto ops_bytes = [&](int chunk) -> unsigned {
-        const int n = nops - chunk * 32;
-        return n <= 0 ? 0u : (unsigned)(n < 32 ? n : 32) * 16u;
-    };
-    auto copy_ops = [&](const Op4 *prog, int chunk, uint64_t *bar) {
-        const unsigned b = ops_bytes(chunk);
-        if (b) bulk_g2s(opbuf + (chunk & 1) * 32, prog + chunk * 32, b, bar);
-    };
-    // child vector from a stage: state tip (column of P), partial tip (P p)
     auto child_tip = [&](Real (&u)[SP], const unsigned char *M_, const unsigned char *vs, int code) {
         const Real *M = reinterpret_cast<const Real *>(M_ + mat_lane);
         if (code & kTipPartialBit) {
             Real tp[SP];
-            lds_vec<Real, SP>(tp, vs + pl * VB);
+            lds_vec<Real, SP>(tp, vs + tipp_vec);
             mv<Real, SP>(u, M, tp);
         } else {
-            mcol<Real, SP>(u, M, vs[tip_off + pl], S);
+            mcol<Real, SP>(u, M, vs[tip_idx], S);
         }
-    };
-    auto load_prologue_ops = [&](const Op4 *prog, uint32_t parity) {
-        if (lane == 0) {
-            mbar_arrive_expect_tx(bars + D, ops_bytes(0) + ops_bytes(1));
-            copy_ops(prog, 0, bars + D);
-            copy_ops(prog, 1, bars + D);
-        }
-        mbar_wait(bars + D, parity);
     };
 
-    // ====================== post program (Eq. 2, Eq. 3) =======================
-    // stage layout: [P_k][P_a][P_b][tip a][tip b]
-    auto issue_post = [&](int m) {           // lane 0 only
-        if (m >= nops) return;
-        unsigned char *st = stage_at(m);
-        uint64_t *bar = bar_at(m);
-        const Op4 op = op_at(m);
-        const bool ops_next = (m & 31) == D - 1;     // op chunk (m/32)+1 rides on stage m
-        const int chunk = m / 32 + 1;
-        unsigned bytes = (op.x != root ? MS : 0) + (op.y >= 0 ? MS + tip_bytes(op.y) : 0) +
-                         (op.z >= 0 ? MS + tip_bytes(op.z) : 0) + ((ops_next && chunk >= 2) ? ops_bytes(chunk) : 0);
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(bar, bytes);
-        if (op.x != root) bulk_g2s(st, Pb + (size_t)op.x * MS, MS, bar);
-        if (op.y >= 0) {
-            bulk_g2s(st + MS, Pb + (size_t)(op.y & ~kTipPartialBit) * MS, MS, bar);
-            copy_tip(st + 3 * MS, op.y, bar);
-        }
-        if (op.z >= 0) {
-            bulk_g2s(st + 2 * MS, Pb + (size_t)(op.z & ~kTipPartialBit) * MS, MS, bar);
-            copy_tip(st + 3 * MS + VSS, op.z, bar);
-        }
-        if (ops_next && chunk >= 2) copy_ops(a.post, chunk, bar);
-    };
-    load_prologue_ops(a.post, 0);
-    if (lane == 0)
-        for (int m = 0; m < D - 1; ++m) issue_post(m);
-
+    // ------------------------- post program (Eq. 2, Eq. 3) -----------------------
     int E = 0;                    // post-order exponents removed from this pattern
     double logl_local = 0.0;
-    for (int n = 0; n < nops; ++n) {
-        __syncwarp();                                       // stage (n-1) consumed by all lanes
-        if (lane == 0) issue_post(n + D - 1);
-        mbar_wait(bar_at(n), parity_at(n));
-        const Op4 op = op_at(n);
-        const unsigned char *st = stage_at(n);
+    for (int t = 0; t < nops; ++t) {
+        mbar_wait(full + t % D, (uint32_t)(t / D) & 1u);
+        if (!active) { release(t); continue; }
+        const unsigned char *st = stages + (t % D) * ST;
+        const Op4 op = *reinterpret_cast<const Op4 *>(st);
         Real ua[SP], ub[SP];
         if (op.y < 0) lds_vec<Real, SP>(ua, stack_at(-op.y - 1));
-        else child_tip(ua, st + MS, st + 3 * MS, op.y);
+        else child_tip(ua, st + 16 + MS, st + 16 + 3 * MS, op.y);
         if (op.z < 0) lds_vec<Real, SP>(ub, stack_at(-op.z - 1));
-        else child_tip(ub, st + 2 * MS, st + 3 * MS + VSS, op.z);
+        else child_tip(ub, st + 16 + 2 * MS, st + 16 + 3 * MS + VS, op.z);
         Real p[SP];
 #pragma unroll
         for (int s = 0; s < SP; ++s) p[s] = ua[s] * ub[s];
         if (op.x == root) {
+            release(t);
             double L = 0.0;
 #pragma unroll
             for (int s = 0; s < SP; ++s) L = fma((double)pi[s], (double)p[s], L);
@@ -345,12 +375,13 @@ __global__ void __launch_bounds__(32) traverse_small_kernel(const TravArgs a) {
         } else {
             E += maybe_rescale<Real, SP, RP>(p);
             Real u[SP];
-            mv<Real, SP>(u, reinterpret_cast<const Real *>(st + mat_lane), p);
-            if (live) stg_vec<Real, SP>(Ub + (size_t)(op.x - N) * u_node + u_warp + u_vec, u);
+            mv<Real, SP>(u, reinterpret_cast<const Real *>(st + 16 + mat_lane), p);
+            release(t);
+            if (live) stg_vec<Real, SP>(Ub + (size_t)(op.x - N) * u_node + u_lane, u);
             sts_vec<Real, SP>(stack_at(op.w), u);
         }
     }
-    {
+    if (active) {
         double v = logl_local;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -358,79 +389,9 @@ __global__ void __launch_bounds__(32) traverse_small_kernel(const TravArgs a) {
     }
     fence_proxy_async_global();          // u stores (generic proxy) before bulk reads (async proxy)
     __syncwarp();
+    if (lane == 0) mbar_arrive(post_done);
 
-    // =============== pre program (Eq. 4) + gradient (Eq. 6-8) =================
-    // stage layout: [P_a][P_b][vec a][vec b]; step t = nops + n for ring/parity
-    auto issue_pre = [&](int m) {            // lane 0 only
-        if (m >= nops) return;
-        const int t = nops + m;
-        unsigned char *st = stage_at(t);
-        uint64_t *bar = bar_at(t);
-        const Op4 op = op_at(m);
-        const int cs[2] = {op.y, op.z};
-        const bool ops_next = (m & 31) == D - 1;
-        const int chunk = m / 32 + 1;
-        unsigned bytes = (ops_next && chunk >= 2) ? ops_bytes(chunk) : 0;
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int node = cs[c] & ~kTipPartialBit;
-            bytes += MS + (node >= N ? u_chunk : tip_bytes(cs[c]));
-        }
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(bar, bytes);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int node = cs[c] & ~kTipPartialBit;
-            bulk_g2s(st + c * MS, Pb + (size_t)node * MS, MS, bar);
-            unsigned char *vs = st + 2 * MS + c * VSB;
-            if (node >= N) bulk_g2s(vs, Ub + (size_t)(node - N) * u_node + u_warp, u_chunk, bar);
-            else copy_tip(vs, cs[c], bar);
-        }
-        if (ops_next && chunk >= 2) copy_ops(a.pre, chunk, bar);
-    };
-    auto prefetch_pre = [&](int m) {         // lane 0: pull step m's u chunks into L2
-        if (m >= nops) return;
-        const Op4 op = op_at(m);
-        const int ny = op.y & ~kTipPartialBit, nz = op.z & ~kTipPartialBit;
-        if (ny >= N) prefetch_l2(Ub + (size_t)(ny - N) * u_node + u_warp, u_chunk);
-        if (nz >= N) prefetch_l2(Ub + (size_t)(nz - N) * u_node + u_warp, u_chunk);
-    };
-    // W steps of per-lane (num_r, den_r) -> Eq. 8 ratio per pattern, weighted by
-    // w_c and summed over the tile's patterns (Eq. 6): all 32 lanes busy.
-    auto flush = [&](int n_last) {
-        __syncwarp();
-        constexpr int PAIRS = 2 * W, LPP = 32 / PAIRS, PPL = TP / LPP > 0 ? TP / LPP : 1;
-        const int pair = lane / LPP, sub = lane % LPP;
-        const int wstep = pair >> 1, c = pair & 1;
-        const int n = n_last - (n_last % W) + wstep;
-        double acc = 0.0;
-        if (n <= n_last && sub * PPL < TP) {
-#pragma unroll
-            for (int k = 0; k < PPL; ++k) {
-                const int p = sub * PPL + k;
-                const double2 *src = nd + ((wstep * 2 + c) * 32 + p * RP);
-                double num = 0.0, den = 0.0;
-#pragma unroll
-                for (int q = 0; q < RP; ++q) { const double2 v = src[q]; num += v.x; den += v.y; }
-                const double w = wbuf[p];
-                acc += (w != 0.0) ? w * (num / den) : 0.0;
-            }
-        }
-#pragma unroll
-        for (int o = 1; o < LPP; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (sub == 0 && n <= n_last) {
-            const Op4 op = op_at(n);
-            const int node = (c == 0 ? op.y : op.z) & ~kTipPartialBit;
-            a.grad_part[(size_t)node * a.n_tiles + tile] = acc;
-        }
-    };
-
-    load_prologue_ops(a.pre, 1);
-    if (lane == 0) {
-        for (int m = 0; m < PF; ++m) prefetch_pre(m);
-        for (int m = 0; m < D - 1; ++m) issue_pre(m);
-    }
-
+    // -------------------- pre program (Eq. 4) + gradient (Eq. 6-8) ---------------
     Real Qr[SP][SP <= 4 ? SP : 1];
     if constexpr (SP <= 4) {
 #pragma unroll
@@ -439,16 +400,12 @@ __global__ void __launch_bounds__(32) traverse_small_kernel(const TravArgs a) {
             for (int t = 0; t < SP; ++t) Qr[s][t] = static_cast<const Real *>(a.Q)[s * SP + t];
     }
     const Real *Qg = static_cast<const Real *>(a.Q);
-
     for (int n = 0; n < nops; ++n) {
-        __syncwarp();
-        if (lane == 0) {
-            prefetch_pre(n + PF);
-            issue_pre(n + D - 1);
-        }
-        mbar_wait(bar_at(nops + n), parity_at(nops + n));
-        const Op4 op = op_at(n);
-        const unsigned char *st = stage_at(nops + n);
+        const int t = nops + n;
+        mbar_wait(full + t % D, (uint32_t)(t / D) & 1u);
+        if (!active) { release(t); continue; }
+        const unsigned char *st = stages + (t % D) * ST;
+        const Op4 op = *reinterpret_cast<const Op4 *>(st);
         Real q[SP];
         if (op.x < 0) {
 #pragma unroll
@@ -461,41 +418,73 @@ __global__ void __launch_bounds__(32) traverse_small_kernel(const TravArgs a) {
         Real uc[2][SP];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-            const unsigned char *vs = st + 2 * MS + c * VSB;
+            const unsigned char *vs = st + 16 + 3 * MS + c * VS;
             if ((cs[c] & ~kTipPartialBit) >= N) lds_vec<Real, SP>(uc[c], vs + u_vec);
-            else child_tip(uc[c], st + c * MS, vs, cs[c]);
+            else child_tip(uc[c], st + 16 + c * MS, vs, cs[c]);
         }
+        Real qc[2][SP];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+            if (slots[c] >= 0) {
+                Real x[SP];
+#pragma unroll
+                for (int s = 0; s < SP; ++s) x[s] = q[s] * uc[1 - c][s];
+                mvt<Real, SP>(qc[c], reinterpret_cast<const Real *>(st + 16 + c * MS + mat_lane), x);
+            }
+        release(t);                                 // stage no longer needed
         double2 *ndw = nd + (n % W) * 64 + lane;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-            Real x[SP];
-#pragma unroll
-            for (int s = 0; s < SP; ++s) x[s] = q[s] * uc[1 - c][s];
+            if (lane == 0) nodes_w[(n % W) * 2 + c] = cs[c] & ~kTipPartialBit;
             Real num = 0, den = 0;
 #pragma unroll
             for (int s = 0; s < SP; ++s) {
+                const Real xs = q[s] * uc[1 - c][s];
                 Real Qu;
                 if constexpr (SP <= 4) {
                     Qu = Qr[s][0] * uc[c][0];
 #pragma unroll
-                    for (int t = 1; t < SP; ++t) Qu = fma(Qr[s][t], uc[c][t], Qu);
+                    for (int t2 = 1; t2 < SP; ++t2) Qu = fma(Qr[s][t2], uc[c][t2], Qu);
                 } else {
                     Qu = __ldg(Qg + s * SP) * uc[c][0];
 #pragma unroll
-                    for (int t = 1; t < SP; ++t) Qu = fma(__ldg(Qg + s * SP + t), uc[c][t], Qu);
+                    for (int t2 = 1; t2 < SP; ++t2) Qu = fma(__ldg(Qg + s * SP + t2), uc[c][t2], Qu);
                 }
-                num = fma(x[s], Qu, num);
-                den = fma(x[s], uc[c][s], den);
+                num = fma(xs, Qu, num);
+                den = fma(xs, uc[c][s], den);
             }
             ndw[c * 32] = make_double2(gwr * (double)num, wr * (double)den);
-            if (slots[c] >= 0) {               // q_c = P_c' x_c (Eq. 4), pushed
-                Real qc[SP];
-                mvt<Real, SP>(qc, reinterpret_cast<const Real *>(st + c * MS + mat_lane), x);
-                maybe_rescale<Real, SP, RP>(qc);
-                sts_vec<Real, SP>(stack_at(slots[c]), qc);
+            if (slots[c] >= 0) {
+                maybe_rescale<Real, SP, RP>(qc[c]);
+                sts_vec<Real, SP>(stack_at(slots[c]), qc[c]);
             }
         }
-        if (n % W == W - 1 || n == nops - 1) flush(n);
+        if (n % W == W - 1 || n == nops - 1) {
+            // W steps of (num_r, den_r) -> Eq. 8 ratio per pattern, weighted (Eq. 6),
+            // summed over the tile's patterns; all 32 lanes busy.
+            __syncwarp();
+            constexpr int PAIRS = 2 * W, LPP = 32 / PAIRS, PPL = TP / LPP > 0 ? TP / LPP : 1;
+            const int pair = lane / LPP, sub = lane % LPP;
+            const int wstep = pair >> 1, c = pair & 1;
+            const int n2 = n - (n % W) + wstep;
+            double acc = 0.0;
+            if (n2 <= n && sub * PPL < TP) {
+#pragma unroll
+                for (int k = 0; k < PPL; ++k) {
+                    const int p = sub * PPL + k;
+                    const double2 *src = nd + ((wstep * 2 + c) * 32 + p * RP);
+                    double num = 0.0, den = 0.0;
+#pragma unroll
+                    for (int q2 = 0; q2 < RP; ++q2) { const double2 v = src[q2]; num += v.x; den += v.y; }
+                    const double w = wbuf[p];
+                    acc += (w != 0.0) ? w * (num / den) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int o = 1; o < LPP; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (sub == 0 && n2 <= n) a.grad_part[(size_t)nodes_w[wstep * 2 + c] * a.n_tiles + tile] = acc;
+            __syncwarp();
+        }
     }
 }
 
