@@ -19,6 +19,7 @@
 #include "aux_kernels.cuh"
 #include "common.cuh"
 #include "schedule.hpp"
+#include "traverse_codon.cuh"
 #include "traverse_large.cuh"
 #include "traverse_small.cuh"
 
@@ -35,6 +36,9 @@ struct Layout {
     size_t off_P, off_PT, off_Q, off_QT, off_pi, off_V, off_Vi, off_lam, off_rates, off_cw,
         off_bl, off_patw, off_tips, off_tipp, off_u, off_gpart, off_lpart, off_out, off_status,
         off_post, off_pre, total;
+    // codon (variant 2) extras
+    size_t off_PBpre = 0, off_DT = 0, off_PONE = 0, off_QB = 0, off_q = 0, off_E = 0, off_child = 0,
+           off_levels = 0, off_tipmode = 0;
 };
 
 int padded_states(int S) {
@@ -56,12 +60,15 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         if (err) *err = "precision must be PG_FP64 or PG_FP32";
         return PG_ERR_ARG;
     }
-    const int SP = padded_states(c->states);
+    int SP = padded_states(c->states);
     if (!SP) { if (err) *err = "states > 64 are not supported by this build"; return PG_ERR_UNSUPPORTED; }
+    // fp64 with S > 16: level-batched FP64 tensor-core path, states padded to 64
+    const bool codon = SP > 16 && c->precision == PG_FP64;
+    if (codon) SP = 64;
     if (c->states > 254) { if (err) *err = "states > 254"; return PG_ERR_UNSUPPORTED; }
     const int R = c->categories;
     L->SP = SP;
-    L->variant = SP <= 16 ? 0 : 1;
+    L->variant = SP <= 16 ? 0 : (codon ? 2 : 1);
     L->real = c->precision == PG_FP64 ? 8 : 4;
     if (L->variant == 0) {
         if (R > (SP == 16 ? 8 : 16)) {
@@ -71,6 +78,9 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         int Rp = 1;
         while (Rp < R) Rp <<= 1;
         L->tpl = 32 / Rp;      // patterns per warp tile (lane = pattern x category)
+    } else if (L->variant == 2) {
+        if (R > 16) { if (err) *err = "too many rate categories (max 16)"; return PG_ERR_UNSUPPORTED; }
+        L->tpl = pg::codon::T;
     } else {
         if (R > 16) { if (err) *err = "too many rate categories (max 16)"; return PG_ERR_UNSUPPORTED; }
         L->tpl = (L->real == 8) ? pg::LargeCfg<double, 64>::tpl(R) : pg::LargeCfg<float, 64>::tpl(R);
@@ -86,7 +96,13 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t at = o; o = align_up(o + bytes); return at; };
     L->off_P = take(mats);
-    L->off_PT = take(L->variant == 1 ? (size_t)L->B * R * SP * SP * L->real : 0);
+    L->off_PT = take(L->variant >= 1 ? (size_t)L->B * R * SP * SP * L->real : 0);
+    if (L->variant == 2) {
+        L->off_PBpre = take(mats);
+        L->off_DT = take(mats);
+        L->off_PONE = take((size_t)L->B * R * SP * 8);
+        L->off_QB = take((size_t)SP * SP * 8);
+    }
     L->off_Q = take((size_t)SP * SP * L->real);
     L->off_QT = take((size_t)SP * SP * L->real);
     L->off_pi = take((size_t)SP * L->real);
@@ -106,6 +122,13 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
     L->off_status = take(sizeof(int) * 4);
     L->off_post = take((size_t)(N - 1) * sizeof(Op4));
     L->off_pre = take((size_t)(N - 1) * sizeof(Op4));
+    if (L->variant == 2) {
+        L->off_q = take((size_t)(N - 2) * R * L->Cpad * SP * 8);
+        L->off_E = take((size_t)(N - 1) * L->Cpad * 4);
+        L->off_child = take((size_t)2 * (2 * N - 1) * 4);
+        L->off_levels = take((size_t)2 * (N - 1) * 4);
+        L->off_tipmode = take((size_t)N);
+    }
     L->total = o;
     return PG_OK;
 }
@@ -356,6 +379,14 @@ int pg_set_eigen(pg_instance *inst, const double *evec, const double *ievec, con
         }
     if ((rc = upload_real(inst, inst->L.off_Q, Q))) return rc;
     if ((rc = upload_real(inst, inst->L.off_QT, QT))) return rc;
+    if (inst->L.variant == 2) {      // Q as the fragment-ordered B operand of Qu = u Q'
+        std::vector<double> QB((size_t)SP * SP);
+        for (int idx = 0; idx < SP * SP; ++idx) {
+            const int lane = idx & 31, kt = (idx >> 5) & 15, nt = idx >> 9;
+            QB[idx] = Q[(size_t)(nt * 8 + (lane >> 2)) * SP + kt * 4 + (lane & 3)];
+        }
+        if ((rc = upload_doubles(inst, inst->L.off_QB, QB.data(), QB.size()))) return rc;
+    }
     inst->have_eigen = true;
     return PG_OK;
 }
@@ -507,6 +538,17 @@ static int configure(pg_instance *inst) {
         inst->prefetch = (L.SP <= 8) ? 4 : 2;
         inst->smem = (int)small_smem(L, R, K, depth);
         if (inst->smem > 227 * 1024) return inst->fail(PG_ERR_UNSUPPORTED, "traversal does not fit in shared memory");
+    } else if (L.variant == 2) {
+        inst->block = pg::codon::NT;
+        inst->prefetch = 0;
+        inst->smem = (int)pg::codon::pre_smem();
+        CK(cudaFuncSetAttribute((void *)pg::codon::codon_post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pg::codon::post_smem()), "smem attr");
+        CK(cudaFuncSetAttribute((void *)pg::codon::codon_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pg::codon::pre_smem()), "smem attr");
+        CK(cudaFuncSetAttribute((void *)pg::codon::codon_pmat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pg::codon::pmat_smem()), "smem attr");
+        return PG_OK;
     } else {
         inst->block = L.tpl * R * (L.SP / 4);
         inst->prefetch = 0;
@@ -525,6 +567,16 @@ static int refresh_plan(pg_instance *inst) {
                        cudaMemcpyHostToDevice, inst->stream), "plan upload");
     CK(cudaMemcpyAsync(inst->ws + inst->L.off_pre, inst->plan.pre.data(), sizeof(Op4) * (N - 1),
                        cudaMemcpyHostToDevice, inst->stream), "plan upload");
+    if (inst->L.variant == 2) {
+        std::vector<int32_t> ch(2 * (2 * N - 1));
+        for (int v = 0; v < 2 * N - 1; ++v) { ch[v] = inst->plan.child_a[v]; ch[2 * N - 1 + v] = inst->plan.child_b[v]; }
+        CK(cudaMemcpyAsync(inst->ws + inst->L.off_child, ch.data(), ch.size() * 4, cudaMemcpyHostToDevice, inst->stream),
+           "children upload");
+        CK(cudaMemcpyAsync(inst->ws + inst->L.off_levels, inst->plan.level_nodes.data(), inst->plan.level_nodes.size() * 4,
+                           cudaMemcpyHostToDevice, inst->stream), "levels upload");
+        CK(cudaMemcpyAsync(inst->ws + inst->L.off_tipmode, inst->tip_is_partial.data(), N, cudaMemcpyHostToDevice,
+                           inst->stream), "tip modes upload");
+    }
     CK(cudaStreamSynchronize(inst->stream), "plan upload sync");
     int rc = configure(inst);
     if (rc) return rc;
@@ -563,18 +615,59 @@ static pg::TravArgs trav_args(pg_instance *inst) {
     return a;
 }
 
+static pg::codon::CodonArgs codon_args(pg_instance *inst) {
+    const Layout &L = inst->L;
+    pg::codon::CodonArgs c{};
+    const int N = inst->cfg.tips;
+    c.child_a = inst->at<int>(L.off_child);
+    c.child_b = c.child_a + (2 * N - 1);
+    c.levels = inst->at<int>(L.off_levels);
+    c.PBpost = inst->at<double>(L.off_P);
+    c.PBpre = inst->at<double>(L.off_PBpre);
+    c.PT = inst->at<double>(L.off_PT);
+    c.DT = inst->at<double>(L.off_DT);
+    c.PONE = inst->at<double>(L.off_PONE);
+    c.QB = inst->at<double>(L.off_QB);
+    c.pi = inst->at<double>(L.off_pi);
+    c.cat_w = inst->at<double>(L.off_cw);
+    c.cat_g = inst->at<double>(L.off_rates);
+    c.pat_w = inst->at<double>(L.off_patw);
+    c.tip_states = inst->at<uint8_t>(L.off_tips);
+    c.tip_partials = (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? inst->at<double>(L.off_tipp) : nullptr;
+    c.tip_is_partial = inst->at<uint8_t>(L.off_tipmode);
+    c.u = inst->at<double>(L.off_u);
+    c.q = inst->at<double>(L.off_q);
+    c.E = inst->at<int>(L.off_E);
+    c.grad_part = inst->at<double>(L.off_gpart);
+    c.logl_part = inst->at<double>(L.off_lpart);
+    c.status = inst->at<int>(L.off_status);
+    c.N = N;
+    c.S = inst->cfg.states;
+    c.R = inst->cfg.categories;
+    c.Cpad = L.Cpad;
+    c.C = inst->cfg.patterns;
+    c.ntiles = L.n_tiles;
+    return c;
+}
+
 // enqueue one evaluation (no host sync) writing [logL, g] to d_out
 static int enqueue_eval(pg_instance *inst, double *d_out) {
     const Layout &L = inst->L;
     const int R = inst->cfg.categories;
     CK(cudaMemsetAsync(inst->at<int>(L.off_status), 0x7f, sizeof(int), inst->stream), "status reset");
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[0], inst->stream, cudaEventRecordExternal), "event");
-    {
+    const double *V = inst->at<double>(L.off_V), *Vi = inst->at<double>(L.off_Vi),
+                 *lam = inst->at<double>(L.off_lam), *rates = inst->at<double>(L.off_rates),
+                 *bl = inst->at<double>(L.off_bl);
+    int S = inst->cfg.states;
+    if (L.variant == 2) {
+        double *PBpost = inst->at<double>(L.off_P), *PBpre = inst->at<double>(L.off_PBpre),
+               *PT = inst->at<double>(L.off_PT), *DT = inst->at<double>(L.off_DT), *PONE = inst->at<double>(L.off_PONE);
+        void *args[] = {&V, &Vi, &lam, &rates, &bl, &S, (void *)&R, &PBpost, &PBpre, &PT, &DT, &PONE};
+        CK(cudaLaunchKernel((void *)pg::codon::codon_pmat_kernel, dim3(L.B * R), dim3(256), args,
+                            pg::codon::pmat_smem(), inst->stream), "codon pmat launch");
+    } else {
         void *fn = pmat_kernel_fn(L);
-        const double *V = inst->at<double>(L.off_V), *Vi = inst->at<double>(L.off_Vi),
-                     *lam = inst->at<double>(L.off_lam), *rates = inst->at<double>(L.off_rates),
-                     *bl = inst->at<double>(L.off_bl);
-        int S = inst->cfg.states;
         void *P = inst->ws + L.off_P;
         void *PT = L.variant == 1 ? inst->ws + L.off_PT : nullptr;
         int cs = L.cat_stride;
@@ -582,7 +675,22 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         CK(cudaLaunchKernel(fn, dim3(L.B * R), dim3(std::min(256, L.SP * L.SP)), args, 0, inst->stream), "pmat launch");
     }
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[1], inst->stream, cudaEventRecordExternal), "event");
-    {
+    if (L.variant == 2) {
+        pg::codon::CodonArgs c = codon_args(inst);
+        const auto &pl = inst->plan;
+        for (size_t i = 0; i + 1 < pl.post_off.size(); ++i) {
+            int off = pl.post_off[i], cnt = pl.post_off[i + 1] - off;
+            void *args[] = {&c, &off};
+            CK(cudaLaunchKernel((void *)pg::codon::codon_post_kernel, dim3(L.n_tiles, cnt), dim3(pg::codon::NT), args,
+                                pg::codon::post_smem(), inst->stream), "codon post launch");
+        }
+        for (size_t i = 0; i + 1 < pl.pre_off.size(); ++i) {
+            int off = pl.pre_off[i], cnt = pl.pre_off[i + 1] - off;
+            void *args[] = {&c, &off};
+            CK(cudaLaunchKernel((void *)pg::codon::codon_pre_kernel, dim3(L.n_tiles, cnt), dim3(pg::codon::NT), args,
+                                pg::codon::pre_smem(), inst->stream), "codon pre launch");
+        }
+    } else {
         pg::TravArgs a = trav_args(inst);
         void *args[] = {&a};
         CK(cudaLaunchKernel(traverse_fn(L, inst->cfg.categories), dim3(inst->grid), dim3(inst->block), args, inst->smem, inst->stream),
@@ -714,6 +822,8 @@ int pg_get_kernel_times(pg_instance *inst, float *ms) {
 int pg_kernels_per_eval(const pg_instance *inst, int32_t *n) {
     if (!inst || !n) return PG_ERR_ARG;
     *n = 3;   // pmat, traverse, reduce
+    if (inst->L.variant == 2)   // pmat + one launch per post level + per pre level + reduce
+        *n = 2 + (int32_t)(inst->plan.post_off.size() - 1) + (int32_t)(inst->plan.pre_off.size() - 1);
     return PG_OK;
 }
 

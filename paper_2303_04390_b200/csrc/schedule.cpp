@@ -127,6 +127,36 @@ int build_plan(int32_t N, const int32_t *ops, int32_t n_ops, Plan *out, std::str
         }
         plan.pre_depth = std::max(maxsp, 1);
     }
+    // ---- level-batched schedule (codon path) -------------------------------
+    {
+        std::vector<int32_t> height(nn, 0), depth(nn, 0);
+        int32_t H = 0;
+        for (int32_t o = 0; o < n_ops; ++o) {
+            const int32_t d = ops[3 * o];
+            height[d] = 1 + std::max(height[ca[d]], height[cb[d]]);
+            H = std::max(H, height[d]);
+        }
+        int32_t Dmax = 0;
+        for (int32_t o = n_ops - 1; o >= 0; --o) {
+            const int32_t d = ops[3 * o];
+            depth[ca[d]] = depth[cb[d]] = depth[d] + 1;
+            Dmax = std::max(Dmax, depth[d]);
+        }
+        // bucket by level (stable in op order): O(N)
+        std::vector<std::vector<int32_t>> byh(H + 1), byd(Dmax + 1);
+        for (int32_t o = 0; o < n_ops; ++o) byh[height[ops[3 * o]]].push_back(ops[3 * o]);
+        for (int32_t o = n_ops - 1; o >= 0; --o) byd[depth[ops[3 * o]]].push_back(ops[3 * o]);
+        plan.post_off.assign(1, 0);
+        for (int32_t h = 1; h <= H; ++h) {
+            plan.level_nodes.insert(plan.level_nodes.end(), byh[h].begin(), byh[h].end());
+            plan.post_off.push_back((int32_t)plan.level_nodes.size());
+        }
+        plan.pre_off.assign(1, (int32_t)plan.level_nodes.size());
+        for (int32_t dd = 0; dd <= Dmax; ++dd) {
+            plan.level_nodes.insert(plan.level_nodes.end(), byd[dd].begin(), byd[dd].end());
+            plan.pre_off.push_back((int32_t)plan.level_nodes.size());
+        }
+    }
     if ((int32_t)plan.post.size() != N - 1 || (int32_t)plan.pre.size() != N - 1)
         return fail(err, PG_ERR_TOPOLOGY, "internal planning error (%ld/%ld ops)",
                     (long)plan.post.size(), (long)plan.pre.size());

@@ -37,6 +37,10 @@ struct Plan {
     std::vector<Op4> post, pre;
     int32_t post_depth = 0, pre_depth = 0;
     std::vector<int32_t> child_a, child_b;   // by node (internal only)
+    // level-batched schedule (codon path): internal nodes grouped by height
+    // (post, tips = 0) and by depth (pre, root = 0); level i of each is
+    // level_nodes[off[i] .. off[i+1])
+    std::vector<int32_t> level_nodes, post_off, pre_off;
 };
 
 // Returns 0 on success, else a PG_ERR_* code with *err filled.

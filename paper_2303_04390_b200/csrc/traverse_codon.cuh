@@ -1,0 +1,429 @@
+// traverse_codon.cuh -- codon-sized state spaces (S <= 64, padded to 64) in
+// fp64 on the FP64 tensor path: level-batched post-order and pre-order
+// kernels whose inner operation is a [32 patterns x 64] x [64 x 64] product per
+// rate category, issued as mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).
+//
+// Layout ("fragment order").  A 32-pattern x 64-state tile of partials is
+// stored as [mt 4][kt 16][lane 32] doubles so that the m8n8k4 A fragment of
+// (mt, kt) is 32 consecutive doubles: element (m, k) lives at
+//     apos(m, k) = ((m/8)*16 + k/4)*32 + (m%8)*4 + k%4.
+// u and q are stored per (node, category, tile) in this order in HBM, so a
+// tile is one contiguous 16 KB block, and element-wise products (Eq. 2's
+// u_a o u_b, Eq. 4's q o u) are plain position-wise products.  B operands
+// (64 x 64) are stored as [nt 8][kt 16][lane 32] with element
+// B[k = kt*4 + lane%4][n = nt*8 + lane/4]:
+//   post  u_k = p P'      : B[t][s] = P[s][t]          (PBpost)
+//   pre   q_c = x P       : B[s][t] = P[s][t]          (PBpre)
+//   grad  Qu  = u Q'      : B[t][s] = Q[s][t]          (QB)
+// Tip vectors are gathered from P' rows (u_tip[s] = P[s][state]) and, for
+// the gradient, from D' rows with D = gamma_r Q P (Eq. 8's factor), so tips
+// need no product at all.  Warp w of 8 computes output columns 8w..8w+7.
+#pragma once
+#include "common.cuh"
+
+namespace pg {
+namespace codon {
+
+constexpr int SP = 64, T = 32, TILE = T * SP, NW = 8, NT = NW * 32;
+constexpr int MAT = SP * SP;
+
+__host__ __device__ __forceinline__ int apos(int m, int k) {
+    return (((m >> 3) * 16 + (k >> 2)) << 5) + ((m & 7) << 2) + (k & 3);
+}
+// inverse of apos
+__device__ __forceinline__ void apos_inv(int idx, int &m, int &k) {
+    const int lane = idx & 31, kt = (idx >> 5) & 15, mt = idx >> 9;
+    m = mt * 8 + (lane >> 2);
+    k = kt * 4 + (lane & 3);
+}
+
+struct CodonArgs {
+    const int *child_a, *child_b;     // [2N-1] children of internal nodes (-1 for tips)
+    const int *levels;                // node lists of all levels
+    const double *PBpost, *PBpre;     // [B][R][MAT] fragment-ordered B operands
+    const double *PT, *DT;            // [B][R][SP][SP]  P' and (gamma Q P)' row-major
+    const double *PONE;               // [B][R][SP]      P 1 (missing-data tips)
+    const double *QB;                 // [MAT]           Q as B operand of Qu = u Q'
+    const double *pi;                 // [SP]
+    const double *cat_w, *cat_g;      // [R]
+    const double *pat_w;              // [Cpad]
+    const uint8_t *tip_states;        // [N][Cpad]
+    const double *tip_partials;       // [N][Cpad][SP] or null
+    const uint8_t *tip_is_partial;    // [N]
+    double *u;                        // [N-2][R][ntiles][TILE]
+    double *q;                        // [N-2][R][ntiles][TILE]
+    int *E;                           // [N-1][Cpad] cumulative post-order exponents (internal + root)
+    double *grad_part;                // [B][ntiles]
+    double *logl_part;                // [ntiles]
+    int *status;
+    int N, S, R, Cpad, C, ntiles;
+};
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+// acc[mt] (rows mt*8 + lane/4, cols w*8 + 2*(lane%4) + {0,1}) = A(32x64) * B(64x64)[:, 8w..8w+7]
+__device__ __forceinline__ void gemm_tile(double (&acc)[4][2], const double *As, const double *Bs, int w, int lane) {
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+    const double *Bw = Bs + w * 16 * 32 + lane;
+#pragma unroll 4
+    for (int kt = 0; kt < 16; ++kt) {
+        const double b = Bw[kt * 32];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) dmma(acc[mt], As[(mt * 16 + kt) * 32 + lane], b);
+    }
+}
+
+// copy n doubles (n % 2 == 0, 16-B aligned) global -> shared with all threads
+__device__ __forceinline__ void load_block(double *dst, const double *src, int n) {
+    for (int i = threadIdx.x; i < n / 2; i += blockDim.x)
+        reinterpret_cast<double2 *>(dst)[i] = __ldg(reinterpret_cast<const double2 *>(src) + i);
+}
+
+// Fill a tile with child vectors for category r: internal (u from HBM) or tip.
+__device__ void load_child(double *dst, const CodonArgs &a, int child, int r, int tile) {
+    if (child >= a.N) {
+        load_block(dst, a.u + (((size_t)(child - a.N) * a.R + r) * a.ntiles + tile) * TILE, TILE);
+        return;
+    }
+    const size_t br = (size_t)child * a.R + r;
+    const int pat0 = tile * T;
+    if (a.tip_is_partial[child]) {
+        const double *PT = a.PT + br * MAT;   // u[s] = sum_t P[s][t] p[t] = sum_t PT[t][s] p[t]
+        for (int idx = threadIdx.x; idx < TILE; idx += blockDim.x) {
+            int m, k;
+            apos_inv(idx, m, k);
+            const double *p = a.tip_partials + ((size_t)child * a.Cpad + pat0 + m) * SP;
+            double acc = 0.0;
+            for (int t = 0; t < SP; ++t) acc = fma(__ldg(PT + t * SP + k), __ldg(p + t), acc);
+            dst[idx] = acc;
+        }
+        return;
+    }
+    const double *PT = a.PT + br * MAT;
+    const double *ONE = a.PONE + br * SP;
+    const uint8_t *st = a.tip_states + (size_t)child * a.Cpad + pat0;
+    for (int idx = threadIdx.x; idx < TILE; idx += blockDim.x) {
+        int m, k;
+        apos_inv(idx, m, k);
+        const int s = st[m];
+        dst[idx] = s < a.S ? __ldg(PT + s * SP + k) : __ldg(ONE + k);
+    }
+}
+
+template <typename F>
+__device__ __forceinline__ int tile_max_exponent_reduce(int *pmax, F &&) { return 0; }
+
+// ---------------------------------------------------------------------------
+// post-order level: one CTA per (tile, node of the level), all categories.
+// u_k = (u_a o u_b) P_k' per category (Eq. 2); exact power-of-two rescale
+// shared across categories when a pattern's max falls below 2^-256 (R4);
+// root: L_c = sum_r P(gamma_r) pi' p (Eq. 3) -> logL tile partial.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) codon_post_kernel(const CodonArgs a, int level_off) {
+    extern __shared__ __align__(16) unsigned char smem_c[];
+    double *As = reinterpret_cast<double *>(smem_c);      // A tile (p)
+    double *Ts = As + TILE;                                 // child b tile
+    double *Bs = Ts + TILE;                                 // B operand (MAT)
+    int *pmax = reinterpret_cast<int *>(Bs + MAT);          // [T]
+    double *Lsum = reinterpret_cast<double *>(pmax + T);    // [T]
+    const int tile = blockIdx.x;
+    const int k = a.levels[level_off + blockIdx.y];
+    const int ca = a.child_a[k], cb = a.child_b[k];
+    const int root = 2 * a.N - 2;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x < T) { pmax[threadIdx.x] = 0; Lsum[threadIdx.x] = 0.0; }
+    for (int r = 0; r < a.R; ++r) {
+        load_child(As, a, ca, r, tile);
+        load_child(Ts, a, cb, r, tile);
+        if (k != root) load_block(Bs, a.PBpost + ((size_t)k * a.R + r) * MAT, MAT);
+        __syncthreads();
+        for (int i = threadIdx.x; i < TILE; i += NT) As[i] *= Ts[i];
+        __syncthreads();
+        if (k == root) {
+            // thread -> (pattern m = tid/8, 8 states); deterministic shuffle sum
+            const int m = threadIdx.x >> 3, j = threadIdx.x & 7;
+            double s = 0.0;
+            for (int kk = j; kk < SP; kk += 8) s = fma(a.pi[kk], As[apos(m, kk)], s);
+            s += __shfl_xor_sync(0xffffffffu, s, 1);
+            s += __shfl_xor_sync(0xffffffffu, s, 2);
+            s += __shfl_xor_sync(0xffffffffu, s, 4);
+            if (j == 0) Lsum[m] += a.cat_w[r] * s;
+        } else {
+            double acc[4][2];
+            gemm_tile(acc, As, Bs, w, lane);
+            double *out = a.u + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE;
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
+                const int f = max(__double2hiint(acc[mt][0]) >> 20, __double2hiint(acc[mt][1]) >> 20);
+                atomicMax(pmax + m, f);
+            }
+        }
+        __syncthreads();
+    }
+    const int pat0 = tile * T;
+    if (k == root) {
+        if (threadIdx.x < 32) {
+            const int m = threadIdx.x, c = pat0 + m;
+            const int E = a.E[(size_t)(k - a.N) * a.Cpad + c];
+            const double L = Lsum[m];
+            double v = 0.0;
+            if (c < a.C) {
+                if (!(L > 0.0) || !isfinite(L)) atomicMin(a.status, c);
+                v = a.pat_w[c] * (log(L) + (double)E * 0.69314718055994530942);
+            }
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (threadIdx.x == 0) a.logl_part[tile] = v;
+        }
+        return;
+    }
+    // lazy exact rescale of the R stored tiles + cumulative exponents
+    __shared__ int need;
+    if (threadIdx.x == 0) need = 0;
+    __syncthreads();
+    if (threadIdx.x < T && pmax[threadIdx.x] < 1023 - 256) need = 1;
+    __syncthreads();
+    int *Ek = a.E + (size_t)(k - a.N) * a.Cpad + pat0;
+    if (threadIdx.x < T) {
+        const int m = threadIdx.x;
+        const int e = need ? min(max(pmax[m] - 1022, -1021), 1022) : 0;
+        pmax[m] = e;
+        const int Ea = ca >= a.N ? a.E[(size_t)(ca - a.N) * a.Cpad + pat0 + m] : 0;
+        const int Eb = cb >= a.N ? a.E[(size_t)(cb - a.N) * a.Cpad + pat0 + m] : 0;
+        Ek[m] = e + Ea + Eb;
+    }
+    if (!need) return;
+    __syncthreads();
+    for (int r = 0; r < a.R; ++r) {
+        double *out = a.u + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE;
+        for (int idx = threadIdx.x; idx < TILE; idx += NT) {
+            int m, kk;
+            apos_inv(idx, m, kk);
+            out[idx] *= __longlong_as_double((long long)(1023 - pmax[m]) << 52);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// pre-order level: one CTA per (tile, parent of the level), all categories.
+// x_c = q_k o u_sibling; q_c = x_c P_c (Eq. 4) for internal children;
+// Eq. 8 terms num_r = gamma_r P(gamma_r) x_c'Q u_c (internal: Qu = u Q' on the
+// tensor path; tip: D' row gather), den_r = P(gamma_r) x_c'u_c; per pattern
+// ratio, weighted (Eq. 6), summed over the tile -> grad_part.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int level_off) {
+    extern __shared__ __align__(16) unsigned char smem_c[];
+    double *Qs = reinterpret_cast<double *>(smem_c);
+    double *Us[2] = {Qs + TILE, Qs + 2 * TILE};
+    double *Xs[2] = {Qs + 3 * TILE, Qs + 4 * TILE};
+    double *Bs = Qs + 5 * TILE;
+    double *part = Bs + MAT;                                 // [2 (num,den)][NW][T]
+    double *numden = part + 2 * NW * T;                      // [2 child][2][T]
+    int *pmax = reinterpret_cast<int *>(numden + 4 * T);     // [2][T]
+    const int tile = blockIdx.x;
+    const int k = a.levels[level_off + blockIdx.y];
+    const int root = 2 * a.N - 2;
+    const int ch[2] = {a.child_a[k], a.child_b[k]};
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pat0 = tile * T;
+    if (threadIdx.x < 4 * T) numden[threadIdx.x] = 0.0;
+    if (threadIdx.x < 2 * T) pmax[threadIdx.x] = 0;
+    for (int r = 0; r < a.R; ++r) {
+        if (k == root) {
+            for (int idx = threadIdx.x; idx < TILE; idx += NT) {
+                int m, kk;
+                apos_inv(idx, m, kk);
+                Qs[idx] = a.pi[kk];
+            }
+        } else {
+            load_block(Qs, a.q + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE, TILE);
+        }
+        load_child(Us[0], a, ch[0], r, tile);
+        load_child(Us[1], a, ch[1], r, tile);
+        __syncthreads();
+        for (int i = threadIdx.x; i < TILE; i += NT) {
+            const double qv = Qs[i];
+            Xs[0][i] = qv * Us[1][i];
+            Xs[1][i] = qv * Us[0][i];
+        }
+        __syncthreads();
+        const double wr = a.cat_w[r], gr = a.cat_g[r];
+        for (int c = 0; c < 2; ++c) {
+            const int node = ch[c];
+            const size_t br = (size_t)node * a.R + r;
+            // --- Eq. 8 terms ------------------------------------------------
+            double acc[4][2];
+            double scale;
+            if (node >= a.N) {
+                load_block(Bs, a.QB, MAT);
+                __syncthreads();
+                gemm_tile(acc, Us[c], Bs, w, lane);
+                scale = gr * wr;
+            } else {
+                // tip: (Q u)[s] gamma = D[s][state]; missing data: D 1 = gamma Q 1 = 0
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) {
+                    const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                    if (a.tip_is_partial[node]) {
+                        double s0 = 0.0, s1 = 0.0;     // D p = sum_t D[s][t] p[t]
+                        const double *p = a.tip_partials + ((size_t)node * a.Cpad + pat0 + m) * SP;
+                        const double *DT = a.DT + br * MAT;
+                        for (int t = 0; t < SP; ++t) {
+                            s0 = fma(__ldg(DT + t * SP + n), __ldg(p + t), s0);
+                            s1 = fma(__ldg(DT + t * SP + n + 1), __ldg(p + t), s1);
+                        }
+                        acc[mt][0] = s0;
+                        acc[mt][1] = s1;
+                    } else {
+                        const int s = a.tip_states[(size_t)node * a.Cpad + pat0 + m];
+                        if (s < a.S) {
+                            const double2 v = __ldg(reinterpret_cast<const double2 *>(a.DT + br * MAT + s * SP + n));
+                            acc[mt][0] = v.x;
+                            acc[mt][1] = v.y;
+                        } else {
+                            acc[mt][0] = acc[mt][1] = 0.0;
+                        }
+                    }
+                }
+                scale = wr;
+            }
+            double pn[4], pd[4];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                const int p = apos(m, n);
+                const double2 x2 = *reinterpret_cast<const double2 *>(Xs[c] + p);
+                const double2 u2 = *reinterpret_cast<const double2 *>(Us[c] + p);
+                double sn = x2.x * acc[mt][0] + x2.y * acc[mt][1];
+                double sd = x2.x * u2.x + x2.y * u2.y;
+                sn += __shfl_xor_sync(0xffffffffu, sn, 1);
+                sd += __shfl_xor_sync(0xffffffffu, sd, 1);
+                sn += __shfl_xor_sync(0xffffffffu, sn, 2);
+                sd += __shfl_xor_sync(0xffffffffu, sd, 2);
+                pn[mt] = sn;
+                pd[mt] = sd;
+            }
+            if ((lane & 3) == 0) {
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) {
+                    const int m = mt * 8 + (lane >> 2);
+                    part[(0 * NW + w) * T + m] = pn[mt];
+                    part[(1 * NW + w) * T + m] = pd[mt];
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x < T) {                // fixed-order sum over the 8 warps
+                const int m = threadIdx.x;
+                double sn = 0.0, sd = 0.0;
+                for (int ww = 0; ww < NW; ++ww) { sn += part[ww * T + m]; sd += part[(NW + ww) * T + m]; }
+                numden[(c * 2 + 0) * T + m] += scale * sn;
+                numden[(c * 2 + 1) * T + m] += wr * sd;
+            }
+            // --- q_c = x_c P_c (Eq. 4) for internal children ------------------
+            if (node >= a.N) {
+                load_block(Bs, a.PBpre + br * MAT, MAT);
+                __syncthreads();
+                gemm_tile(acc, Xs[c], Bs, w, lane);
+                double *out = a.q + (((size_t)(node - a.N) * a.R + r) * a.ntiles + tile) * TILE;
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) {
+                    const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                    *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
+                    atomicMax(pmax + c * T + m, max(__double2hiint(acc[mt][0]) >> 20, __double2hiint(acc[mt][1]) >> 20));
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // Eq. 8 ratio per pattern, weighted, summed over the tile (fixed order)
+    if (threadIdx.x < 64) {
+        const int c = threadIdx.x >> 5, m = threadIdx.x & 31, pat = pat0 + m;
+        const double wc = a.pat_w[pat];
+        double d = wc != 0.0 ? wc * (numden[(c * 2) * T + m] / numden[(c * 2 + 1) * T + m]) : 0.0;
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        if (m == 0) a.grad_part[(size_t)ch[c] * a.ntiles + tile] = d;
+    }
+    // lazy exact rescale of the stored q tiles (shared across categories)
+    __shared__ int need[2];
+    if (threadIdx.x < 2) need[threadIdx.x] = 0;
+    __syncthreads();
+    if (threadIdx.x < 2 * T && ch[threadIdx.x / T] >= a.N && pmax[threadIdx.x] < 1023 - 256) need[threadIdx.x / T] = 1;
+    __syncthreads();
+    for (int c = 0; c < 2; ++c) {
+        if (!need[c]) continue;
+        for (int r = 0; r < a.R; ++r) {
+            double *out = a.q + (((size_t)(ch[c] - a.N) * a.R + r) * a.ntiles + tile) * TILE;
+            for (int idx = threadIdx.x; idx < TILE; idx += NT) {
+                int m, kk;
+                apos_inv(idx, m, kk);
+                const int e = min(max(pmax[c * T + m] - 1022, -1021), 1022);
+                out[idx] *= __longlong_as_double((long long)(1023 - e) << 52);
+            }
+        }
+    }
+}
+
+constexpr size_t post_smem() { return (size_t)(2 * TILE + MAT) * 8 + T * 4 + T * 8; }
+constexpr size_t pre_smem() { return (size_t)(5 * TILE + MAT) * 8 + (2 * NW * T + 4 * T) * 8 + 2 * T * 4; }
+
+// ---------------------------------------------------------------------------
+// A1 for this path: per (branch, category) P and D = gamma Q P from the
+// eigensystem (Eq. 1; Eq. 8's factor), written as PBpost, PBpre, P', D', P 1.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restrict__ V, const double *__restrict__ Vi,
+                                                         const double *__restrict__ lam,
+                                                         const double *__restrict__ rates,
+                                                         const double *__restrict__ bl, int S, int R,
+                                                         double *PBpost, double *PBpre, double *PT, double *DT,
+                                                         double *PONE) {
+    extern __shared__ __align__(16) unsigned char smem_p[];
+    double *Ps = reinterpret_cast<double *>(smem_p);     // [SP][SP+1]
+    double *Ds = Ps + SP * (SP + 1);
+    __shared__ double e[SP], de[SP];
+    const int br = blockIdx.x, r = br % R, b = br / R;
+    const double g = rates[r], t = g * bl[b];
+    for (int k = threadIdx.x; k < SP; k += blockDim.x) {
+        const double ex = k < S ? exp(lam[k] * t) : 0.0;
+        e[k] = ex;
+        de[k] = k < S ? g * lam[k] * ex : 0.0;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < SP * SP; idx += blockDim.x) {
+        const int s = idx / SP, u = idx % SP;
+        double p = 0.0, d = 0.0;
+        if (s < S && u < S)
+            for (int k = 0; k < S; ++k) {
+                const double vv = V[s * S + k] * Vi[k * S + u];
+                p = fma(vv, e[k], p);
+                d = fma(vv, de[k], d);
+            }
+        Ps[s * (SP + 1) + u] = p;
+        Ds[s * (SP + 1) + u] = d;
+    }
+    __syncthreads();
+    const size_t base = (size_t)br * MAT;
+    for (int idx = threadIdx.x; idx < MAT; idx += blockDim.x) {
+        const int lane = idx & 31, kt = (idx >> 5) & 15, nt = idx >> 9;
+        const int kk = kt * 4 + (lane & 3), nn = nt * 8 + (lane >> 2);
+        PBpost[base + idx] = Ps[nn * (SP + 1) + kk];    // B[k=t][n=s] = P[s][t]
+        PBpre[base + idx] = Ps[kk * (SP + 1) + nn];     // B[k=s][n=t] = P[s][t]
+        const int row = idx / SP, col = idx % SP;
+        PT[base + idx] = Ps[col * (SP + 1) + row];      // P'[t][s] = P[s][t]
+        DT[base + idx] = Ds[col * (SP + 1) + row];
+    }
+    for (int s = threadIdx.x; s < SP; s += blockDim.x) {
+        double acc = 0.0;
+        for (int u = 0; u < SP; ++u) acc += Ps[s * (SP + 1) + u];
+        PONE[(size_t)br * SP + s] = acc;
+    }
+}
+constexpr size_t pmat_smem() { return (size_t)2 * SP * (SP + 1) * 8; }
+
+}  // namespace codon
+}  // namespace pg
