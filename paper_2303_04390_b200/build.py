@@ -13,18 +13,27 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIB_DIR, "libphylograd.so")
 SOURCES = ["phylograd.cu", "schedule.cpp"]
-HEADERS = ["common.cuh", "aux_kernels.cuh", "traverse_small.cuh", "traverse_large.cuh",
-           "schedule.hpp", os.path.join("..", "..", "include", "phylograd.h")]
+HEADER_GLOBS = ("*.cuh", "*.hpp", "*.h")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
+
+
+def _inputs():
+    import glob
+    files = [os.path.join(CSRC, f) for f in SOURCES]
+    for g in HEADER_GLOBS:
+        files += glob.glob(os.path.join(CSRC, g))
+    files.append(os.path.join(os.path.dirname(HERE), "include", "phylograd.h"))
+    files.append(os.path.abspath(__file__))
+    return files
 
 
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(os.path.join(CSRC, f)) > t for f in SOURCES + HEADERS)
+    return any(os.path.getmtime(f) > t for f in _inputs())
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -78,6 +78,23 @@ __device__ __forceinline__ void gemm_tile(double (&acc)[4][2], const double *As,
     }
 }
 
+// same with A = A1 o A2 (element-wise, e.g. x = q o u_sibling), formed on the fly
+__device__ __forceinline__ void gemm_tile2(double (&acc)[4][2], const double *A1, const double *A2, const double *Bs,
+                                           int w, int lane) {
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+    const double *Bw = Bs + w * 16 * 32 + lane;
+#pragma unroll 4
+    for (int kt = 0; kt < 16; ++kt) {
+        const double b = Bw[kt * 32];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            const int i = (mt * 16 + kt) * 32 + lane;
+            dmma(acc[mt], A1[i] * A2[i], b);
+        }
+    }
+}
+
 // copy n doubles (n % 2 == 0, 16-B aligned) global -> shared with all threads
 __device__ __forceinline__ void load_block(double *dst, const double *src, int n) {
     for (int i = threadIdx.x; i < n / 2; i += blockDim.x)
@@ -221,8 +238,7 @@ __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int le
     extern __shared__ __align__(16) unsigned char smem_c[];
     double *Qs = reinterpret_cast<double *>(smem_c);
     double *Us[2] = {Qs + TILE, Qs + 2 * TILE};
-    double *Xs[2] = {Qs + 3 * TILE, Qs + 4 * TILE};
-    double *Bs = Qs + 5 * TILE;
+    double *Bs = Qs + 3 * TILE;
     double *part = Bs + MAT;                                 // [2 (num,den)][NW][T]
     double *numden = part + 2 * NW * T;                      // [2 child][2][T]
     int *pmax = reinterpret_cast<int *>(numden + 4 * T);     // [2][T]
@@ -246,12 +262,6 @@ __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int le
         }
         load_child(Us[0], a, ch[0], r, tile);
         load_child(Us[1], a, ch[1], r, tile);
-        __syncthreads();
-        for (int i = threadIdx.x; i < TILE; i += NT) {
-            const double qv = Qs[i];
-            Xs[0][i] = qv * Us[1][i];
-            Xs[1][i] = qv * Us[0][i];
-        }
         __syncthreads();
         const double wr = a.cat_w[r], gr = a.cat_g[r];
         for (int c = 0; c < 2; ++c) {
@@ -298,10 +308,12 @@ __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int le
             for (int mt = 0; mt < 4; ++mt) {
                 const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
                 const int p = apos(m, n);
-                const double2 x2 = *reinterpret_cast<const double2 *>(Xs[c] + p);
+                const double2 q2 = *reinterpret_cast<const double2 *>(Qs + p);
+                const double2 o2 = *reinterpret_cast<const double2 *>(Us[1 - c] + p);
                 const double2 u2 = *reinterpret_cast<const double2 *>(Us[c] + p);
-                double sn = x2.x * acc[mt][0] + x2.y * acc[mt][1];
-                double sd = x2.x * u2.x + x2.y * u2.y;
+                const double x0 = q2.x * o2.x, x1 = q2.y * o2.y;     // x_c = q_k o u_sibling
+                double sn = x0 * acc[mt][0] + x1 * acc[mt][1];
+                double sd = x0 * u2.x + x1 * u2.y;
                 sn += __shfl_xor_sync(0xffffffffu, sn, 1);
                 sd += __shfl_xor_sync(0xffffffffu, sd, 1);
                 sn += __shfl_xor_sync(0xffffffffu, sn, 2);
@@ -329,7 +341,7 @@ __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int le
             if (node >= a.N) {
                 load_block(Bs, a.PBpre + br * MAT, MAT);
                 __syncthreads();
-                gemm_tile(acc, Xs[c], Bs, w, lane);
+                gemm_tile2(acc, Qs, Us[1 - c], Bs, w, lane);
                 double *out = a.q + (((size_t)(node - a.N) * a.R + r) * a.ntiles + tile) * TILE;
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt) {
@@ -370,7 +382,7 @@ __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int le
 }
 
 constexpr size_t post_smem() { return (size_t)(2 * TILE + MAT) * 8 + T * 4 + T * 8; }
-constexpr size_t pre_smem() { return (size_t)(5 * TILE + MAT) * 8 + (2 * NW * T + 4 * T) * 8 + 2 * T * 4; }
+constexpr size_t pre_smem() { return (size_t)(3 * TILE + MAT) * 8 + (2 * NW * T + 4 * T) * 8 + 2 * T * 4; }
 
 // ---------------------------------------------------------------------------
 // A1 for this path: per (branch, category) P and D = gamma Q P from the
