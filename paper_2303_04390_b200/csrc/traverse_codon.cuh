@@ -65,34 +65,36 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
+// B fragments of warp w (output columns 8w..8w+7) straight from L2 into
+// registers: 16 independent coalesced 256-B loads per warp.
+__device__ __forceinline__ void load_bfrag(double (&b)[16], const double *__restrict__ Bg, int w, int lane) {
+    const double *Bw = Bg + w * 16 * 32 + lane;
+#pragma unroll
+    for (int kt = 0; kt < 16; ++kt) b[kt] = __ldg(Bw + kt * 32);
+}
+
 // acc[mt] (rows mt*8 + lane/4, cols w*8 + 2*(lane%4) + {0,1}) = A(32x64) * B(64x64)[:, 8w..8w+7]
-__device__ __forceinline__ void gemm_tile(double (&acc)[4][2], const double *As, const double *Bs, int w, int lane) {
+__device__ __forceinline__ void gemm_tile(double (&acc)[4][2], const double *As, const double (&b)[16], int lane) {
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
-    const double *Bw = Bs + w * 16 * 32 + lane;
-#pragma unroll 4
-    for (int kt = 0; kt < 16; ++kt) {
-        const double b = Bw[kt * 32];
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) dmma(acc[mt], As[(mt * 16 + kt) * 32 + lane], b);
-    }
+    for (int kt = 0; kt < 16; ++kt)
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) dmma(acc[mt], As[(mt * 16 + kt) * 32 + lane], b[kt]);
 }
 
 // same with A = A1 o A2 (element-wise, e.g. x = q o u_sibling), formed on the fly
-__device__ __forceinline__ void gemm_tile2(double (&acc)[4][2], const double *A1, const double *A2, const double *Bs,
-                                           int w, int lane) {
+__device__ __forceinline__ void gemm_tile2(double (&acc)[4][2], const double *A1, const double *A2,
+                                           const double (&b)[16], int lane) {
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
-    const double *Bw = Bs + w * 16 * 32 + lane;
-#pragma unroll 4
-    for (int kt = 0; kt < 16; ++kt) {
-        const double b = Bw[kt * 32];
+#pragma unroll
+    for (int kt = 0; kt < 16; ++kt)
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) {
             const int i = (mt * 16 + kt) * 32 + lane;
-            dmma(acc[mt], A1[i] * A2[i], b);
+            dmma(acc[mt], A1[i] * A2[i], b[kt]);
         }
-    }
 }
 
 // copy n doubles (n % 2 == 0, 16-B aligned) global -> shared with all threads
@@ -145,8 +147,7 @@ __global__ void __launch_bounds__(NT) codon_post_kernel(const CodonArgs a, int l
     extern __shared__ __align__(16) unsigned char smem_c[];
     double *As = reinterpret_cast<double *>(smem_c);      // A tile (p)
     double *Ts = As + TILE;                                 // child b tile
-    double *Bs = Ts + TILE;                                 // B operand (MAT)
-    int *pmax = reinterpret_cast<int *>(Bs + MAT);          // [T]
+    int *pmax = reinterpret_cast<int *>(Ts + TILE);         // [T]
     double *Lsum = reinterpret_cast<double *>(pmax + T);    // [T]
     const int tile = blockIdx.x;
     const int k = a.levels[level_off + blockIdx.y];
@@ -155,9 +156,10 @@ __global__ void __launch_bounds__(NT) codon_post_kernel(const CodonArgs a, int l
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x < T) { pmax[threadIdx.x] = 0; Lsum[threadIdx.x] = 0.0; }
     for (int r = 0; r < a.R; ++r) {
+        double b[16];
+        if (k != root) load_bfrag(b, a.PBpost + ((size_t)k * a.R + r) * MAT, w, lane);
         load_child(As, a, ca, r, tile);
         load_child(Ts, a, cb, r, tile);
-        if (k != root) load_block(Bs, a.PBpost + ((size_t)k * a.R + r) * MAT, MAT);
         __syncthreads();
         for (int i = threadIdx.x; i < TILE; i += NT) As[i] *= Ts[i];
         __syncthreads();
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(NT) codon_post_kernel(const CodonArgs a, int l
             if (j == 0) Lsum[m] += a.cat_w[r] * s;
         } else {
             double acc[4][2];
-            gemm_tile(acc, As, Bs, w, lane);
+            gemm_tile(acc, As, b, lane);
             double *out = a.u + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE;
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
@@ -238,8 +240,7 @@ __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int le
     extern __shared__ __align__(16) unsigned char smem_c[];
     double *Qs = reinterpret_cast<double *>(smem_c);
     double *Us[2] = {Qs + TILE, Qs + 2 * TILE};
-    double *Bs = Qs + 3 * TILE;
-    double *part = Bs + MAT;                                 // [2 (num,den)][NW][T]
+    double *part = Qs + 3 * TILE;                            // [2 (num,den)][NW][T]
     double *numden = part + 2 * NW * T;                      // [2 child][2][T]
     int *pmax = reinterpret_cast<int *>(numden + 4 * T);     // [2][T]
     const int tile = blockIdx.x;
@@ -271,9 +272,9 @@ __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int le
             double acc[4][2];
             double scale;
             if (node >= a.N) {
-                load_block(Bs, a.QB, MAT);
-                __syncthreads();
-                gemm_tile(acc, Us[c], Bs, w, lane);
+                double b[16];
+                load_bfrag(b, a.QB, w, lane);
+                gemm_tile(acc, Us[c], b, lane);
                 scale = gr * wr;
             } else {
                 // tip: (Q u)[s] gamma = D[s][state]; missing data: D 1 = gamma Q 1 = 0
@@ -339,9 +340,9 @@ __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int le
             }
             // --- q_c = x_c P_c (Eq. 4) for internal children ------------------
             if (node >= a.N) {
-                load_block(Bs, a.PBpre + br * MAT, MAT);
-                __syncthreads();
-                gemm_tile2(acc, Qs, Us[1 - c], Bs, w, lane);
+                double b[16];
+                load_bfrag(b, a.PBpre + br * MAT, w, lane);
+                gemm_tile2(acc, Qs, Us[1 - c], b, lane);
                 double *out = a.q + (((size_t)(node - a.N) * a.R + r) * a.ntiles + tile) * TILE;
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt) {
@@ -381,8 +382,8 @@ __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int le
     }
 }
 
-constexpr size_t post_smem() { return (size_t)(2 * TILE + MAT) * 8 + T * 4 + T * 8; }
-constexpr size_t pre_smem() { return (size_t)(3 * TILE + MAT) * 8 + (2 * NW * T + 4 * T) * 8 + 2 * T * 4; }
+constexpr size_t post_smem() { return (size_t)(2 * TILE) * 8 + T * 4 + T * 8; }
+constexpr size_t pre_smem() { return (size_t)(3 * TILE) * 8 + (2 * NW * T + 4 * T) * 8 + 2 * T * 4; }
 
 // ---------------------------------------------------------------------------
 // A1 for this path: per (branch, category) P and D = gamma Q P from the
