@@ -38,7 +38,7 @@ struct Layout {
         off_post, off_pre, total;
     // codon (variant 2) extras
     size_t off_PBpre = 0, off_DT = 0, off_PONE = 0, off_QB = 0, off_q = 0, off_E = 0, off_child = 0,
-           off_levels = 0, off_tipmode = 0;
+           off_levels = 0, off_tipmode = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0;
 };
 
 int padded_states(int S) {
@@ -125,6 +125,10 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
     if (L->variant == 2) {
         L->off_q = take((size_t)(N - 2) * R * L->Cpad * SP * 8);
         L->off_E = take((size_t)(N - 1) * L->Cpad * 4);
+        L->off_fmax = take((size_t)(2 * N - 3) * L->Cpad * 4);     // fmax [N-1] then qmax [N-2] (one memset)
+        L->off_qmax = L->off_fmax + (size_t)(N - 1) * L->Cpad * 4;
+        L->off_numden = take((size_t)L->B * R * L->Cpad * 16);
+        L->off_Lpart = take((size_t)R * L->Cpad * 8);
         L->off_child = take((size_t)2 * (2 * N - 1) * 4);
         L->off_levels = take((size_t)2 * (N - 1) * 4);
         L->off_tipmode = take((size_t)N);
@@ -638,6 +642,10 @@ static pg::codon::CodonArgs codon_args(pg_instance *inst) {
     c.u = inst->at<double>(L.off_u);
     c.q = inst->at<double>(L.off_q);
     c.E = inst->at<int>(L.off_E);
+    c.fmax = inst->at<int>(L.off_fmax);
+    c.qmax = inst->at<int>(L.off_qmax);
+    c.numden = inst->at<double>(L.off_numden);
+    c.Lpart = inst->at<double>(L.off_Lpart);
     c.grad_part = inst->at<double>(L.off_gpart);
     c.logl_part = inst->at<double>(L.off_lpart);
     c.status = inst->at<int>(L.off_status);
@@ -678,16 +686,18 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
     if (L.variant == 2) {
         pg::codon::CodonArgs c = codon_args(inst);
         const auto &pl = inst->plan;
+        const int N = inst->cfg.tips;
+        CK(cudaMemsetAsync(inst->ws + L.off_fmax, 0, (size_t)(2 * N - 3) * L.Cpad * 4, inst->stream), "fmax reset");
         for (size_t i = 0; i + 1 < pl.post_off.size(); ++i) {
             int off = pl.post_off[i], cnt = pl.post_off[i + 1] - off;
             void *args[] = {&c, &off};
-            CK(cudaLaunchKernel((void *)pg::codon::codon_post_kernel, dim3(L.n_tiles, cnt), dim3(pg::codon::NT), args,
+            CK(cudaLaunchKernel((void *)pg::codon::codon_post_kernel, dim3(L.n_tiles, cnt, R), dim3(pg::codon::NT), args,
                                 pg::codon::post_smem(), inst->stream), "codon post launch");
         }
         for (size_t i = 0; i + 1 < pl.pre_off.size(); ++i) {
             int off = pl.pre_off[i], cnt = pl.pre_off[i + 1] - off;
             void *args[] = {&c, &off};
-            CK(cudaLaunchKernel((void *)pg::codon::codon_pre_kernel, dim3(L.n_tiles, cnt), dim3(pg::codon::NT), args,
+            CK(cudaLaunchKernel((void *)pg::codon::codon_pre_kernel, dim3(L.n_tiles, cnt, R), dim3(pg::codon::NT), args,
                                 pg::codon::pre_smem(), inst->stream), "codon pre launch");
         }
     } else {
@@ -697,7 +707,12 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
            "traverse launch");
     }
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[2], inst->stream, cudaEventRecordExternal), "event");
-    {
+    if (L.variant == 2) {
+        pg::codon::CodonArgs c = codon_args(inst);
+        void *args[] = {&c, &d_out};
+        CK(cudaLaunchKernel((void *)pg::codon::codon_ratio_kernel, dim3(L.B + 1), dim3(256), args, 0, inst->stream),
+           "codon ratio launch");
+    } else {
         const double *gp = inst->at<double>(L.off_gpart), *lp = inst->at<double>(L.off_lpart);
         int B = L.B, nt = L.n_tiles;
         void *args[] = {&gp, &lp, &B, &nt, &d_out};

@@ -52,7 +52,11 @@ struct CodonArgs {
     const uint8_t *tip_is_partial;    // [N]
     double *u;                        // [N-2][R][ntiles][TILE]
     double *q;                        // [N-2][R][ntiles][TILE]
-    int *E;                           // [N-1][Cpad] cumulative post-order exponents (internal + root)
+    int *E;                           // [N-1][Cpad] cumulative exponent inside the stored u (internal + root)
+    int *fmax;                        // [N-1][Cpad] max exponent field of u over categories (atomicMax)
+    int *qmax;                        // [N-2][Cpad] same for q
+    double *numden;                   // [B][R][Cpad][2] Eq. 8 terms per category
+    double *Lpart;                    // [R][Cpad] root likelihood terms per category
     double *grad_part;                // [B][ntiles]
     double *logl_part;                // [ntiles]
     int *status;
@@ -134,256 +138,260 @@ __device__ void load_child(double *dst, const CodonArgs &a, int child, int r, in
     }
 }
 
-template <typename F>
-__device__ __forceinline__ int tile_max_exponent_reduce(int *pmax, F &&) { return 0; }
+
+// Lazy exact rescaling across categories (R4).  Categories of a node run in
+// different CTAs, so the stored u / q tiles are unscaled; every CTA atomically
+// maxes the IEEE exponent field of its values into fmax/qmax[node][pattern],
+// and the consumer at the next level multiplies by 2^-e with
+// e = exponent of that max when it fell below 2^-256 (else e = 0).
+__device__ __forceinline__ int lazy_exp(int field) {
+    return field < 1023 - 256 ? min(max(field - 1022, -1021), 1022) : 0;
+}
+__device__ __forceinline__ double pow2neg(int e) { return __longlong_as_double((long long)(1023 - e) << 52); }
+
+// per-pattern scale of a child tile (1 for tips)
+__device__ __forceinline__ void child_scale(double *sc, const CodonArgs &a, int child, const int *mx, int pat0) {
+    if (threadIdx.x < T) sc[threadIdx.x] = child >= a.N ? pow2neg(lazy_exp(mx[(size_t)(child - a.N) * a.Cpad + pat0 + threadIdx.x])) : 1.0;
+}
 
 // ---------------------------------------------------------------------------
-// post-order level: one CTA per (tile, node of the level), all categories.
-// u_k = (u_a o u_b) P_k' per category (Eq. 2); exact power-of-two rescale
-// shared across categories when a pattern's max falls below 2^-256 (R4);
-// root: L_c = sum_r P(gamma_r) pi' p (Eq. 3) -> logL tile partial.
+// post-order level: one CTA per (tile, node of the level, category r).
+// u_k[r] = (u_a o u_b) P_k' (Eq. 2), children rescaled on load; root:
+// P(gamma_r) pi' p (Eq. 3) per pattern -> Lpart.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT) codon_post_kernel(const CodonArgs a, int level_off) {
     extern __shared__ __align__(16) unsigned char smem_c[];
     double *As = reinterpret_cast<double *>(smem_c);      // A tile (p)
     double *Ts = As + TILE;                                 // child b tile
-    int *pmax = reinterpret_cast<int *>(Ts + TILE);         // [T]
-    double *Lsum = reinterpret_cast<double *>(pmax + T);    // [T]
-    const int tile = blockIdx.x;
+    double *sc = Ts + TILE;                                 // [2][T] child scales
+    const int tile = blockIdx.x, r = blockIdx.z;
     const int k = a.levels[level_off + blockIdx.y];
     const int ca = a.child_a[k], cb = a.child_b[k];
     const int root = 2 * a.N - 2;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x < T) { pmax[threadIdx.x] = 0; Lsum[threadIdx.x] = 0.0; }
-    for (int r = 0; r < a.R; ++r) {
-        double b[16];
-        if (k != root) load_bfrag(b, a.PBpost + ((size_t)k * a.R + r) * MAT, w, lane);
-        load_child(As, a, ca, r, tile);
-        load_child(Ts, a, cb, r, tile);
-        __syncthreads();
-        for (int i = threadIdx.x; i < TILE; i += NT) As[i] *= Ts[i];
-        __syncthreads();
-        if (k == root) {
-            // thread -> (pattern m = tid/8, 8 states); deterministic shuffle sum
-            const int m = threadIdx.x >> 3, j = threadIdx.x & 7;
-            double s = 0.0;
-            for (int kk = j; kk < SP; kk += 8) s = fma(a.pi[kk], As[apos(m, kk)], s);
-            s += __shfl_xor_sync(0xffffffffu, s, 1);
-            s += __shfl_xor_sync(0xffffffffu, s, 2);
-            s += __shfl_xor_sync(0xffffffffu, s, 4);
-            if (j == 0) Lsum[m] += a.cat_w[r] * s;
-        } else {
-            double acc[4][2];
-            gemm_tile(acc, As, b, lane);
-            double *out = a.u + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE;
-#pragma unroll
-            for (int mt = 0; mt < 4; ++mt) {
-                const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-                *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
-                const int f = max(__double2hiint(acc[mt][0]) >> 20, __double2hiint(acc[mt][1]) >> 20);
-                atomicMax(pmax + m, f);
-            }
-        }
-        __syncthreads();
-    }
     const int pat0 = tile * T;
+    double b[16];
+    if (k != root) load_bfrag(b, a.PBpost + ((size_t)k * a.R + r) * MAT, w, lane);
+    child_scale(sc, a, ca, a.fmax, pat0);
+    child_scale(sc + T, a, cb, a.fmax, pat0);
+    if (r == 0 && threadIdx.x < T) {     // cumulative exponent inside u_k (and at the root)
+        const int m = threadIdx.x;
+        int Ek = 0;
+        if (ca >= a.N) Ek += a.E[(size_t)(ca - a.N) * a.Cpad + pat0 + m] + lazy_exp(a.fmax[(size_t)(ca - a.N) * a.Cpad + pat0 + m]);
+        if (cb >= a.N) Ek += a.E[(size_t)(cb - a.N) * a.Cpad + pat0 + m] + lazy_exp(a.fmax[(size_t)(cb - a.N) * a.Cpad + pat0 + m]);
+        a.E[(size_t)(k - a.N) * a.Cpad + pat0 + m] = Ek;
+    }
+    load_child(As, a, ca, r, tile);
+    load_child(Ts, a, cb, r, tile);
+    __syncthreads();
+    for (int i = threadIdx.x; i < TILE; i += NT) {
+        int m, kk;
+        apos_inv(i, m, kk);
+        As[i] *= Ts[i] * (sc[m] * sc[T + m]);
+    }
+    __syncthreads();
     if (k == root) {
-        if (threadIdx.x < 32) {
-            const int m = threadIdx.x, c = pat0 + m;
-            const int E = a.E[(size_t)(k - a.N) * a.Cpad + c];
-            const double L = Lsum[m];
-            double v = 0.0;
-            if (c < a.C) {
-                if (!(L > 0.0) || !isfinite(L)) atomicMin(a.status, c);
-                v = a.pat_w[c] * (log(L) + (double)E * 0.69314718055994530942);
-            }
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (threadIdx.x == 0) a.logl_part[tile] = v;
-        }
+        // thread -> (pattern m = tid/8, 8 states); deterministic shuffle sum
+        const int m = threadIdx.x >> 3, j = threadIdx.x & 7;
+        double sum = 0.0;
+        for (int kk = j; kk < SP; kk += 8) sum = fma(a.pi[kk], As[apos(m, kk)], sum);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+        if (j == 0) a.Lpart[(size_t)r * a.Cpad + pat0 + m] = a.cat_w[r] * sum;
         return;
     }
-    // lazy exact rescale of the R stored tiles + cumulative exponents
-    __shared__ int need;
-    if (threadIdx.x == 0) need = 0;
-    __syncthreads();
-    if (threadIdx.x < T && pmax[threadIdx.x] < 1023 - 256) need = 1;
-    __syncthreads();
-    int *Ek = a.E + (size_t)(k - a.N) * a.Cpad + pat0;
-    if (threadIdx.x < T) {
-        const int m = threadIdx.x;
-        const int e = need ? min(max(pmax[m] - 1022, -1021), 1022) : 0;
-        pmax[m] = e;
-        const int Ea = ca >= a.N ? a.E[(size_t)(ca - a.N) * a.Cpad + pat0 + m] : 0;
-        const int Eb = cb >= a.N ? a.E[(size_t)(cb - a.N) * a.Cpad + pat0 + m] : 0;
-        Ek[m] = e + Ea + Eb;
-    }
-    if (!need) return;
-    __syncthreads();
-    for (int r = 0; r < a.R; ++r) {
-        double *out = a.u + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE;
-        for (int idx = threadIdx.x; idx < TILE; idx += NT) {
-            int m, kk;
-            apos_inv(idx, m, kk);
-            out[idx] *= __longlong_as_double((long long)(1023 - pmax[m]) << 52);
-        }
+    double acc[4][2];
+    gemm_tile(acc, As, b, lane);
+    double *out = a.u + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE;
+    int *fm = a.fmax + (size_t)(k - a.N) * a.Cpad + pat0;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+        const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+        *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
+        int f = max(__double2hiint(acc[mt][0]) >> 20, __double2hiint(acc[mt][1]) >> 20);
+        f = max(f, __shfl_xor_sync(0xffffffffu, f, 1));
+        f = max(f, __shfl_xor_sync(0xffffffffu, f, 2));
+        if ((lane & 3) == 0) atomicMax(fm + m, f);
     }
 }
 
 // ---------------------------------------------------------------------------
-// pre-order level: one CTA per (tile, parent of the level), all categories.
+// pre-order level: one CTA per (tile, parent of the level, category r).
 // x_c = q_k o u_sibling; q_c = x_c P_c (Eq. 4) for internal children;
 // Eq. 8 terms num_r = gamma_r P(gamma_r) x_c'Q u_c (internal: Qu = u Q' on the
-// tensor path; tip: D' row gather), den_r = P(gamma_r) x_c'u_c; per pattern
-// ratio, weighted (Eq. 6), summed over the tile -> grad_part.
+// tensor path; tip: D' row gather), den_r = P(gamma_r) x_c'u_c per pattern ->
+// numden[child][r][pattern]; the ratio over categories is formed afterwards.
+// All inputs use the same per-pattern scales in every category, so the
+// category sums stay consistent (the ratio itself is scale invariant).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int level_off) {
     extern __shared__ __align__(16) unsigned char smem_c[];
     double *Qs = reinterpret_cast<double *>(smem_c);
     double *Us[2] = {Qs + TILE, Qs + 2 * TILE};
     double *part = Qs + 3 * TILE;                            // [2 (num,den)][NW][T]
-    double *numden = part + 2 * NW * T;                      // [2 child][2][T]
-    int *pmax = reinterpret_cast<int *>(numden + 4 * T);     // [2][T]
-    const int tile = blockIdx.x;
+    double *sc = part + 2 * NW * T;                          // [3][T]: q_k, u_a, u_b scales
+    const int tile = blockIdx.x, r = blockIdx.z;
     const int k = a.levels[level_off + blockIdx.y];
     const int root = 2 * a.N - 2;
     const int ch[2] = {a.child_a[k], a.child_b[k]};
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int pat0 = tile * T;
-    if (threadIdx.x < 4 * T) numden[threadIdx.x] = 0.0;
-    if (threadIdx.x < 2 * T) pmax[threadIdx.x] = 0;
-    for (int r = 0; r < a.R; ++r) {
-        if (k == root) {
-            for (int idx = threadIdx.x; idx < TILE; idx += NT) {
-                int m, kk;
-                apos_inv(idx, m, kk);
-                Qs[idx] = a.pi[kk];
-            }
-        } else {
-            load_block(Qs, a.q + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE, TILE);
+    if (threadIdx.x < T)
+        sc[threadIdx.x] = k == root ? 1.0 : pow2neg(lazy_exp(a.qmax[(size_t)(k - a.N) * a.Cpad + pat0 + threadIdx.x]));
+    child_scale(sc + T, a, ch[0], a.fmax, pat0);
+    child_scale(sc + 2 * T, a, ch[1], a.fmax, pat0);
+    if (k == root) {
+        for (int idx = threadIdx.x; idx < TILE; idx += NT) {
+            int m, kk;
+            apos_inv(idx, m, kk);
+            Qs[idx] = a.pi[kk];
         }
-        load_child(Us[0], a, ch[0], r, tile);
-        load_child(Us[1], a, ch[1], r, tile);
-        __syncthreads();
-        const double wr = a.cat_w[r], gr = a.cat_g[r];
-        for (int c = 0; c < 2; ++c) {
-            const int node = ch[c];
-            const size_t br = (size_t)node * a.R + r;
-            // --- Eq. 8 terms ------------------------------------------------
-            double acc[4][2];
-            double scale;
-            if (node >= a.N) {
-                double b[16];
-                load_bfrag(b, a.QB, w, lane);
-                gemm_tile(acc, Us[c], b, lane);
-                scale = gr * wr;
-            } else {
-                // tip: (Q u)[s] gamma = D[s][state]; missing data: D 1 = gamma Q 1 = 0
-#pragma unroll
-                for (int mt = 0; mt < 4; ++mt) {
-                    const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-                    if (a.tip_is_partial[node]) {
-                        double s0 = 0.0, s1 = 0.0;     // D p = sum_t D[s][t] p[t]
-                        const double *p = a.tip_partials + ((size_t)node * a.Cpad + pat0 + m) * SP;
-                        const double *DT = a.DT + br * MAT;
-                        for (int t = 0; t < SP; ++t) {
-                            s0 = fma(__ldg(DT + t * SP + n), __ldg(p + t), s0);
-                            s1 = fma(__ldg(DT + t * SP + n + 1), __ldg(p + t), s1);
-                        }
-                        acc[mt][0] = s0;
-                        acc[mt][1] = s1;
-                    } else {
-                        const int s = a.tip_states[(size_t)node * a.Cpad + pat0 + m];
-                        if (s < a.S) {
-                            const double2 v = __ldg(reinterpret_cast<const double2 *>(a.DT + br * MAT + s * SP + n));
-                            acc[mt][0] = v.x;
-                            acc[mt][1] = v.y;
-                        } else {
-                            acc[mt][0] = acc[mt][1] = 0.0;
-                        }
-                    }
-                }
-                scale = wr;
-            }
-            double pn[4], pd[4];
+    } else {
+        load_block(Qs, a.q + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE, TILE);
+    }
+    load_child(Us[0], a, ch[0], r, tile);
+    load_child(Us[1], a, ch[1], r, tile);
+    __syncthreads();
+    for (int i = threadIdx.x; i < TILE; i += NT) {
+        int m, kk;
+        apos_inv(i, m, kk);
+        Qs[i] *= sc[m];
+        Us[0][i] *= sc[T + m];
+        Us[1][i] *= sc[2 * T + m];
+    }
+    __syncthreads();
+    const double wr = a.cat_w[r], gr = a.cat_g[r];
+    for (int c = 0; c < 2; ++c) {
+        const int node = ch[c];
+        const size_t br = (size_t)node * a.R + r;
+        double bq[16];
+        if (node >= a.N) load_bfrag(bq, a.PBpre + br * MAT, w, lane);     // issued early
+        // --- Eq. 8 terms ------------------------------------------------
+        double acc[4][2];
+        double scale;
+        if (node >= a.N) {
+            double b[16];
+            load_bfrag(b, a.QB, w, lane);
+            gemm_tile(acc, Us[c], b, lane);
+            scale = gr * wr;
+        } else {
+            // tip: gamma (Q u)[s] = D[s][state]; missing data: D 1 = gamma Q 1 = 0
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
                 const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-                const int p = apos(m, n);
-                const double2 q2 = *reinterpret_cast<const double2 *>(Qs + p);
-                const double2 o2 = *reinterpret_cast<const double2 *>(Us[1 - c] + p);
-                const double2 u2 = *reinterpret_cast<const double2 *>(Us[c] + p);
-                const double x0 = q2.x * o2.x, x1 = q2.y * o2.y;     // x_c = q_k o u_sibling
-                double sn = x0 * acc[mt][0] + x1 * acc[mt][1];
-                double sd = x0 * u2.x + x1 * u2.y;
-                sn += __shfl_xor_sync(0xffffffffu, sn, 1);
-                sd += __shfl_xor_sync(0xffffffffu, sd, 1);
-                sn += __shfl_xor_sync(0xffffffffu, sn, 2);
-                sd += __shfl_xor_sync(0xffffffffu, sd, 2);
-                pn[mt] = sn;
-                pd[mt] = sd;
-            }
-            if ((lane & 3) == 0) {
-#pragma unroll
-                for (int mt = 0; mt < 4; ++mt) {
-                    const int m = mt * 8 + (lane >> 2);
-                    part[(0 * NW + w) * T + m] = pn[mt];
-                    part[(1 * NW + w) * T + m] = pd[mt];
+                if (a.tip_is_partial[node]) {
+                    double s0 = 0.0, s1 = 0.0;     // D p = sum_t D[s][t] p[t]
+                    const double *p = a.tip_partials + ((size_t)node * a.Cpad + pat0 + m) * SP;
+                    const double *DT = a.DT + br * MAT;
+                    for (int t = 0; t < SP; ++t) {
+                        s0 = fma(__ldg(DT + t * SP + n), __ldg(p + t), s0);
+                        s1 = fma(__ldg(DT + t * SP + n + 1), __ldg(p + t), s1);
+                    }
+                    acc[mt][0] = s0;
+                    acc[mt][1] = s1;
+                } else {
+                    const int s = a.tip_states[(size_t)node * a.Cpad + pat0 + m];
+                    if (s < a.S) {
+                        const double2 v = __ldg(reinterpret_cast<const double2 *>(a.DT + br * MAT + s * SP + n));
+                        acc[mt][0] = v.x;
+                        acc[mt][1] = v.y;
+                    } else {
+                        acc[mt][0] = acc[mt][1] = 0.0;
+                    }
                 }
             }
-            __syncthreads();
-            if (threadIdx.x < T) {                // fixed-order sum over the 8 warps
-                const int m = threadIdx.x;
-                double sn = 0.0, sd = 0.0;
-                for (int ww = 0; ww < NW; ++ww) { sn += part[ww * T + m]; sd += part[(NW + ww) * T + m]; }
-                numden[(c * 2 + 0) * T + m] += scale * sn;
-                numden[(c * 2 + 1) * T + m] += wr * sd;
-            }
-            // --- q_c = x_c P_c (Eq. 4) for internal children ------------------
-            if (node >= a.N) {
-                double b[16];
-                load_bfrag(b, a.PBpre + br * MAT, w, lane);
-                gemm_tile2(acc, Qs, Us[1 - c], b, lane);
-                double *out = a.q + (((size_t)(node - a.N) * a.R + r) * a.ntiles + tile) * TILE;
+            scale = wr;
+        }
+        double pn[4], pd[4];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) {
-                    const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-                    *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
-                    atomicMax(pmax + c * T + m, max(__double2hiint(acc[mt][0]) >> 20, __double2hiint(acc[mt][1]) >> 20));
-                }
-            }
-            __syncthreads();
+        for (int mt = 0; mt < 4; ++mt) {
+            const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+            const int p = apos(m, n);
+            const double2 q2 = *reinterpret_cast<const double2 *>(Qs + p);
+            const double2 o2 = *reinterpret_cast<const double2 *>(Us[1 - c] + p);
+            const double2 u2 = *reinterpret_cast<const double2 *>(Us[c] + p);
+            const double x0 = q2.x * o2.x, x1 = q2.y * o2.y;     // x_c = q_k o u_sibling
+            double sn = x0 * acc[mt][0] + x1 * acc[mt][1];
+            double sd = x0 * u2.x + x1 * u2.y;
+            sn += __shfl_xor_sync(0xffffffffu, sn, 1);
+            sd += __shfl_xor_sync(0xffffffffu, sd, 1);
+            sn += __shfl_xor_sync(0xffffffffu, sn, 2);
+            sd += __shfl_xor_sync(0xffffffffu, sd, 2);
+            pn[mt] = sn;
+            pd[mt] = sd;
         }
-    }
-    // Eq. 8 ratio per pattern, weighted, summed over the tile (fixed order)
-    if (threadIdx.x < 64) {
-        const int c = threadIdx.x >> 5, m = threadIdx.x & 31, pat = pat0 + m;
-        const double wc = a.pat_w[pat];
-        double d = wc != 0.0 ? wc * (numden[(c * 2) * T + m] / numden[(c * 2 + 1) * T + m]) : 0.0;
-        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-        if (m == 0) a.grad_part[(size_t)ch[c] * a.ntiles + tile] = d;
-    }
-    // lazy exact rescale of the stored q tiles (shared across categories)
-    __shared__ int need[2];
-    if (threadIdx.x < 2) need[threadIdx.x] = 0;
-    __syncthreads();
-    if (threadIdx.x < 2 * T && ch[threadIdx.x / T] >= a.N && pmax[threadIdx.x] < 1023 - 256) need[threadIdx.x / T] = 1;
-    __syncthreads();
-    for (int c = 0; c < 2; ++c) {
-        if (!need[c]) continue;
-        for (int r = 0; r < a.R; ++r) {
-            double *out = a.q + (((size_t)(ch[c] - a.N) * a.R + r) * a.ntiles + tile) * TILE;
-            for (int idx = threadIdx.x; idx < TILE; idx += NT) {
-                int m, kk;
-                apos_inv(idx, m, kk);
-                const int e = min(max(pmax[c * T + m] - 1022, -1021), 1022);
-                out[idx] *= __longlong_as_double((long long)(1023 - e) << 52);
+        if ((lane & 3) == 0) {
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int m = mt * 8 + (lane >> 2);
+                part[(0 * NW + w) * T + m] = pn[mt];
+                part[(1 * NW + w) * T + m] = pd[mt];
             }
         }
+        // --- q_c = x_c P_c (Eq. 4) for internal children ------------------
+        if (node >= a.N) {
+            gemm_tile2(acc, Qs, Us[1 - c], bq, lane);
+            double *out = a.q + (((size_t)(node - a.N) * a.R + r) * a.ntiles + tile) * TILE;
+            int *qm = a.qmax + (size_t)(node - a.N) * a.Cpad + pat0;
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
+                int f = max(__double2hiint(acc[mt][0]) >> 20, __double2hiint(acc[mt][1]) >> 20);
+                f = max(f, __shfl_xor_sync(0xffffffffu, f, 1));
+                f = max(f, __shfl_xor_sync(0xffffffffu, f, 2));
+                if ((lane & 3) == 0) atomicMax(qm + m, f);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < T) {                // fixed-order sum over the 8 warps
+            const int m = threadIdx.x;
+            double sn = 0.0, sd = 0.0;
+            for (int ww = 0; ww < NW; ++ww) { sn += part[ww * T + m]; sd += part[(NW + ww) * T + m]; }
+            double2 *dst = reinterpret_cast<double2 *>(a.numden) + (br * a.Cpad + pat0 + m);
+            *dst = make_double2(scale * sn, wr * sd);
+        }
+        __syncthreads();
     }
 }
 
-constexpr size_t post_smem() { return (size_t)(2 * TILE) * 8 + T * 4 + T * 8; }
-constexpr size_t pre_smem() { return (size_t)(3 * TILE) * 8 + (2 * NW * T + 4 * T) * 8 + 2 * T * 4; }
+// ---------------------------------------------------------------------------
+// Eq. 6-8 ratio over categories, weighted by w_c, summed over patterns in a
+// fixed order (block b < B: branch b); block B: logL from the root terms.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) codon_ratio_kernel(const CodonArgs a, double *out) {
+    __shared__ double sh[256];
+    const int b = blockIdx.x, B = 2 * a.N - 2, root = 2 * a.N - 2;
+    double acc = 0.0;
+    for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
+        const double wc = a.pat_w[c];
+        if (b < B) {
+            double num = 0.0, den = 0.0;
+            for (int r = 0; r < a.R; ++r) {
+                const double2 v = reinterpret_cast<const double2 *>(a.numden)[((size_t)b * a.R + r) * a.Cpad + c];
+                num += v.x;
+                den += v.y;
+            }
+            if (wc != 0.0) acc += wc * (num / den);
+        } else {
+            double L = 0.0;
+            for (int r = 0; r < a.R; ++r) L += a.Lpart[(size_t)r * a.Cpad + c];
+            if (!(L > 0.0) || !isfinite(L)) atomicMin(a.status, c);
+            acc += wc * (log(L) + (double)a.E[(size_t)(root - a.N) * a.Cpad + c] * 0.69314718055994530942);
+        }
+    }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[b < B ? 1 + b : 0] = sh[0];
+}
+
+constexpr size_t post_smem() { return (size_t)(2 * TILE + 2 * T) * 8; }
+constexpr size_t pre_smem() { return (size_t)(3 * TILE + 2 * NW * T + 3 * T) * 8; }
 
 // ---------------------------------------------------------------------------
 // A1 for this path: per (branch, category) P and D = gamma Q P from the
