@@ -107,16 +107,22 @@ __device__ __forceinline__ void load_block(double *dst, const double *src, int n
         reinterpret_cast<double2 *>(dst)[i] = __ldg(reinterpret_cast<const double2 *>(src) + i);
 }
 
-// Fill a tile with child vectors for category r: internal (u from HBM) or tip.
-__device__ void load_child(double *dst, const CodonArgs &a, int child, int r, int tile) {
+// pattern index of fragment-order position idx
+__device__ __forceinline__ int apos_m(int idx) { return ((idx >> 9) << 3) + ((idx & 31) >> 2); }
+
+// Fill a tile with child vectors for category r: internal (u from HBM) or tip
+// (rows of P' picked by the pattern's state: u_tip[s] = P[s][state]).  Flat
+// position loop (conflict-free smem stores), two states per 16-B load.
+// `stbuf` (>= T ints of smem) receives the tile's tip states.
+__device__ void load_child(double *dst, const CodonArgs &a, int child, int r, int tile, int *stbuf) {
     if (child >= a.N) {
         load_block(dst, a.u + (((size_t)(child - a.N) * a.R + r) * a.ntiles + tile) * TILE, TILE);
         return;
     }
     const size_t br = (size_t)child * a.R + r;
     const int pat0 = tile * T;
-    if (a.tip_is_partial[child]) {
-        const double *PT = a.PT + br * MAT;   // u[s] = sum_t P[s][t] p[t] = sum_t PT[t][s] p[t]
+    const double *PT = a.PT + br * MAT;
+    if (a.tip_is_partial[child]) {          // u[s] = sum_t P[s][t] p[t] = sum_t PT[t][s] p[t]
         for (int idx = threadIdx.x; idx < TILE; idx += blockDim.x) {
             int m, k;
             apos_inv(idx, m, k);
@@ -127,17 +133,18 @@ __device__ void load_child(double *dst, const CodonArgs &a, int child, int r, in
         }
         return;
     }
-    const double *PT = a.PT + br * MAT;
+    if (threadIdx.x < T) stbuf[threadIdx.x] = a.tip_states[(size_t)child * a.Cpad + pat0 + threadIdx.x];
+    __syncthreads();
     const double *ONE = a.PONE + br * SP;
-    const uint8_t *st = a.tip_states + (size_t)child * a.Cpad + pat0;
-    for (int idx = threadIdx.x; idx < TILE; idx += blockDim.x) {
+    for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += blockDim.x) {
+        const int idx = 2 * i2;
         int m, k;
         apos_inv(idx, m, k);
-        const int s = st[m];
-        dst[idx] = s < a.S ? __ldg(PT + s * SP + k) : __ldg(ONE + k);
+        const int s = stbuf[m];
+        const double2 v = __ldg(reinterpret_cast<const double2 *>(s < a.S ? PT + s * SP + k : ONE + k));
+        reinterpret_cast<double2 *>(dst)[i2] = v;
     }
 }
-
 
 // Lazy exact rescaling across categories (R4).  Categories of a node run in
 // different CTAs, so the stored u / q tiles are unscaled; every CTA atomically
@@ -164,6 +171,7 @@ __global__ void __launch_bounds__(NT) codon_post_kernel(const CodonArgs a, int l
     double *As = reinterpret_cast<double *>(smem_c);      // A tile (p)
     double *Ts = As + TILE;                                 // child b tile
     double *sc = Ts + TILE;                                 // [2][T] child scales
+    int *stb = reinterpret_cast<int *>(sc + 2 * T);         // [2][T] tip states
     const int tile = blockIdx.x, r = blockIdx.z;
     const int k = a.levels[level_off + blockIdx.y];
     const int ca = a.child_a[k], cb = a.child_b[k];
@@ -181,12 +189,11 @@ __global__ void __launch_bounds__(NT) codon_post_kernel(const CodonArgs a, int l
         if (cb >= a.N) Ek += a.E[(size_t)(cb - a.N) * a.Cpad + pat0 + m] + lazy_exp(a.fmax[(size_t)(cb - a.N) * a.Cpad + pat0 + m]);
         a.E[(size_t)(k - a.N) * a.Cpad + pat0 + m] = Ek;
     }
-    load_child(As, a, ca, r, tile);
-    load_child(Ts, a, cb, r, tile);
+    load_child(As, a, ca, r, tile, stb);
+    load_child(Ts, a, cb, r, tile, stb + T);
     __syncthreads();
     for (int i = threadIdx.x; i < TILE; i += NT) {
-        int m, kk;
-        apos_inv(i, m, kk);
+        const int m = apos_m(i);
         As[i] *= Ts[i] * (sc[m] * sc[T + m]);
     }
     __syncthreads();
@@ -231,6 +238,7 @@ __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int le
     double *Us[2] = {Qs + TILE, Qs + 2 * TILE};
     double *part = Qs + 3 * TILE;                            // [2 (num,den)][NW][T]
     double *sc = part + 2 * NW * T;                          // [3][T]: q_k, u_a, u_b scales
+    int *stb = reinterpret_cast<int *>(sc + 3 * T);          // [2][T] tip states
     const int tile = blockIdx.x, r = blockIdx.z;
     const int k = a.levels[level_off + blockIdx.y];
     const int root = 2 * a.N - 2;
@@ -242,20 +250,15 @@ __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int le
     child_scale(sc + T, a, ch[0], a.fmax, pat0);
     child_scale(sc + 2 * T, a, ch[1], a.fmax, pat0);
     if (k == root) {
-        for (int idx = threadIdx.x; idx < TILE; idx += NT) {
-            int m, kk;
-            apos_inv(idx, m, kk);
-            Qs[idx] = a.pi[kk];
-        }
+        for (int idx = threadIdx.x; idx < TILE; idx += NT) Qs[idx] = a.pi[((idx >> 5) & 15) * 4 + (idx & 3)];
     } else {
         load_block(Qs, a.q + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE, TILE);
     }
-    load_child(Us[0], a, ch[0], r, tile);
-    load_child(Us[1], a, ch[1], r, tile);
+    load_child(Us[0], a, ch[0], r, tile, stb);
+    load_child(Us[1], a, ch[1], r, tile, stb + T);
     __syncthreads();
     for (int i = threadIdx.x; i < TILE; i += NT) {
-        int m, kk;
-        apos_inv(i, m, kk);
+        const int m = apos_m(i);
         Qs[i] *= sc[m];
         Us[0][i] *= sc[T + m];
         Us[1][i] *= sc[2 * T + m];
@@ -390,8 +393,8 @@ __global__ void __launch_bounds__(256) codon_ratio_kernel(const CodonArgs a, dou
     if (threadIdx.x == 0) out[b < B ? 1 + b : 0] = sh[0];
 }
 
-constexpr size_t post_smem() { return (size_t)(2 * TILE + 2 * T) * 8; }
-constexpr size_t pre_smem() { return (size_t)(3 * TILE + 2 * NW * T + 3 * T) * 8; }
+constexpr size_t post_smem() { return (size_t)(2 * TILE + 2 * T) * 8 + 2 * T * 4; }
+constexpr size_t pre_smem() { return (size_t)(3 * TILE + 2 * NW * T + 3 * T) * 8 + 2 * T * 4; }
 
 // ---------------------------------------------------------------------------
 // A1 for this path: per (branch, category) P and D = gamma Q P from the
