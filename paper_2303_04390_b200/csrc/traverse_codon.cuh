@@ -192,31 +192,31 @@ __global__ void __launch_bounds__(NT) codon_post_kernel(const CodonArgs a, int l
     load_child(As, a, ca, r, tile, stb);
     load_child(Ts, a, cb, r, tile, stb + T);
     __syncthreads();
-    for (int i = threadIdx.x; i < TILE; i += NT) {
-        const int m = apos_m(i);
-        As[i] *= Ts[i] * (sc[m] * sc[T + m]);
-    }
-    __syncthreads();
     if (k == root) {
         // thread -> (pattern m = tid/8, 8 states); deterministic shuffle sum
         const int m = threadIdx.x >> 3, j = threadIdx.x & 7;
         double sum = 0.0;
-        for (int kk = j; kk < SP; kk += 8) sum = fma(a.pi[kk], As[apos(m, kk)], sum);
+        for (int kk = j; kk < SP; kk += 8) {
+            const int p = apos(m, kk);
+            sum = fma(a.pi[kk], As[p] * Ts[p], sum);
+        }
         sum += __shfl_xor_sync(0xffffffffu, sum, 1);
         sum += __shfl_xor_sync(0xffffffffu, sum, 2);
         sum += __shfl_xor_sync(0xffffffffu, sum, 4);
-        if (j == 0) a.Lpart[(size_t)r * a.Cpad + pat0 + m] = a.cat_w[r] * sum;
+        if (j == 0) a.Lpart[(size_t)r * a.Cpad + pat0 + m] = a.cat_w[r] * sum * (sc[m] * sc[T + m]);
         return;
     }
     double acc[4][2];
-    gemm_tile(acc, As, b, lane);
+    gemm_tile2(acc, As, Ts, b, lane);           // p = u_a o u_b formed on the fly
     double *out = a.u + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE;
     int *fm = a.fmax + (size_t)(k - a.N) * a.Cpad + pat0;
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
         const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-        *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
-        int f = max(__double2hiint(acc[mt][0]) >> 20, __double2hiint(acc[mt][1]) >> 20);
+        const double f2 = sc[m] * sc[T + m];             // children's scales, per pattern row
+        const double c0 = acc[mt][0] * f2, c1 = acc[mt][1] * f2;
+        *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(c0, c1);
+        int f = max(__double2hiint(c0) >> 20, __double2hiint(c1) >> 20);
         f = max(f, __shfl_xor_sync(0xffffffffu, f, 1));
         f = max(f, __shfl_xor_sync(0xffffffffu, f, 2));
         if ((lane & 3) == 0) atomicMax(fm + m, f);
@@ -257,13 +257,9 @@ __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int le
     load_child(Us[0], a, ch[0], r, tile, stb);
     load_child(Us[1], a, ch[1], r, tile, stb + T);
     __syncthreads();
-    for (int i = threadIdx.x; i < TILE; i += NT) {
-        const int m = apos_m(i);
-        Qs[i] *= sc[m];
-        Us[0][i] *= sc[T + m];
-        Us[1][i] *= sc[2 * T + m];
-    }
-    __syncthreads();
+    // Tiles stay unscaled: the Eq. 8 terms of a pattern carry the same factor
+    // sc_q sc_a sc_b in numerator and denominator of every category (cancels);
+    // the stored q_c rows are multiplied by sc_q sc_sibling below.
     const double wr = a.cat_w[r], gr = a.cat_g[r];
     for (int c = 0; c < 2; ++c) {
         const int node = ch[c];
@@ -340,6 +336,9 @@ __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int le
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
                 const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                const double f2 = sc[m] * sc[(2 - c) * T + m];   // q_k and sibling scales
+                acc[mt][0] *= f2;
+                acc[mt][1] *= f2;
                 *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
                 int f = max(__double2hiint(acc[mt][0]) >> 20, __double2hiint(acc[mt][1]) >> 20);
                 f = max(f, __shfl_xor_sync(0xffffffffu, f, 1));
