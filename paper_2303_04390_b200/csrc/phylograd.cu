@@ -38,7 +38,7 @@ struct Layout {
         off_post, off_pre, total;
     // codon (variant 2) extras
     size_t off_PBpre = 0, off_DT = 0, off_PONE = 0, off_QB = 0, off_q = 0, off_E = 0, off_child = 0,
-           off_levels = 0, off_tipmode = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0;
+           off_levels = 0, off_tipmode = 0, off_VA = 0, off_ViB = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0;
 };
 
 int padded_states(int S) {
@@ -102,6 +102,8 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         L->off_DT = take(mats);
         L->off_PONE = take((size_t)L->B * R * SP * 8);
         L->off_QB = take((size_t)SP * SP * 8);
+        L->off_VA = take((size_t)SP * SP * 8);
+        L->off_ViB = take((size_t)SP * SP * 8);
     }
     L->off_Q = take((size_t)SP * SP * L->real);
     L->off_QT = take((size_t)SP * SP * L->real);
@@ -390,6 +392,20 @@ int pg_set_eigen(pg_instance *inst, const double *evec, const double *ievec, con
             QB[idx] = Q[(size_t)(nt * 8 + (lane >> 2)) * SP + kt * 4 + (lane & 3)];
         }
         if ((rc = upload_doubles(inst, inst->L.off_QB, QB.data(), QB.size()))) return rc;
+        // V as A fragments (element (m,k) at apos(m,k), 64 rows) and V^{-1} as B fragments
+        std::vector<double> VA((size_t)SP * SP, 0.0), ViB((size_t)SP * SP, 0.0);
+        for (int m = 0; m < S; ++m)
+            for (int k = 0; k < S; ++k) {
+                const int pos = (((m >> 3) * 16 + (k >> 2)) << 5) + ((m & 7) << 2) + (k & 3);
+                VA[pos] = evec[m * S + k];
+            }
+        for (int idx = 0; idx < SP * SP; ++idx) {
+            const int lane = idx & 31, kt = (idx >> 5) & 15, nt = idx >> 9;
+            const int kk = kt * 4 + (lane & 3), nn = nt * 8 + (lane >> 2);
+            ViB[idx] = (kk < S && nn < S) ? ievec[kk * S + nn] : 0.0;
+        }
+        if ((rc = upload_doubles(inst, inst->L.off_VA, VA.data(), VA.size()))) return rc;
+        if ((rc = upload_doubles(inst, inst->L.off_ViB, ViB.data(), ViB.size()))) return rc;
     }
     inst->have_eigen = true;
     return PG_OK;
@@ -671,7 +687,8 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
     if (L.variant == 2) {
         double *PBpost = inst->at<double>(L.off_P), *PBpre = inst->at<double>(L.off_PBpre),
                *PT = inst->at<double>(L.off_PT), *DT = inst->at<double>(L.off_DT), *PONE = inst->at<double>(L.off_PONE);
-        void *args[] = {&V, &Vi, &lam, &rates, &bl, &S, (void *)&R, &PBpost, &PBpre, &PT, &DT, &PONE};
+        const double *VA = inst->at<double>(L.off_VA), *ViB = inst->at<double>(L.off_ViB);
+        void *args[] = {&VA, &ViB, &lam, &rates, &bl, &S, (void *)&R, &PBpost, &PBpre, &PT, &DT, &PONE};
         CK(cudaLaunchKernel((void *)pg::codon::codon_pmat_kernel, dim3(L.B * R), dim3(256), args,
                             pg::codon::pmat_smem(), inst->stream), "codon pmat launch");
     } else {

@@ -166,7 +166,7 @@ __device__ __forceinline__ void child_scale(double *sc, const CodonArgs &a, int 
 // u_k[r] = (u_a o u_b) P_k' (Eq. 2), children rescaled on load; root:
 // P(gamma_r) pi' p (Eq. 3) per pattern -> Lpart.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) codon_post_kernel(const CodonArgs a, int level_off) {
+__global__ void __launch_bounds__(NT, 5) codon_post_kernel(const CodonArgs a, int level_off) {
     extern __shared__ __align__(16) unsigned char smem_c[];
     double *As = reinterpret_cast<double *>(smem_c);      // A tile (p)
     double *Ts = As + TILE;                                 // child b tile
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(NT) codon_post_kernel(const CodonArgs a, int l
 // All inputs use the same per-pattern scales in every category, so the
 // category sums stay consistent (the ratio itself is scale invariant).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int level_off) {
+__global__ void __launch_bounds__(NT, 4) codon_pre_kernel(const CodonArgs a, int level_off) {
     extern __shared__ __align__(16) unsigned char smem_c[];
     double *Qs = reinterpret_cast<double *>(smem_c);
     double *Us[2] = {Qs + TILE, Qs + 2 * TILE};
@@ -264,8 +264,6 @@ __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int le
     for (int c = 0; c < 2; ++c) {
         const int node = ch[c];
         const size_t br = (size_t)node * a.R + r;
-        double bq[16];
-        if (node >= a.N) load_bfrag(bq, a.PBpre + br * MAT, w, lane);     // issued early
         // --- Eq. 8 terms ------------------------------------------------
         double acc[4][2];
         double scale;
@@ -330,6 +328,8 @@ __global__ void __launch_bounds__(NT) codon_pre_kernel(const CodonArgs a, int le
         }
         // --- q_c = x_c P_c (Eq. 4) for internal children ------------------
         if (node >= a.N) {
+            double bq[16];
+            load_bfrag(bq, a.PBpre + br * MAT, w, lane);
             gemm_tile2(acc, Qs, Us[1 - c], bq, lane);
             double *out = a.q + (((size_t)(node - a.N) * a.R + r) * a.ntiles + tile) * TILE;
             int *qm = a.qmax + (size_t)(node - a.N) * a.Cpad + pat0;
@@ -396,10 +396,14 @@ constexpr size_t post_smem() { return (size_t)(2 * TILE + 2 * T) * 8 + 2 * T * 4
 constexpr size_t pre_smem() { return (size_t)(3 * TILE + 2 * NW * T + 3 * T) * 8 + 2 * T * 4; }
 
 // ---------------------------------------------------------------------------
-// A1 for this path: per (branch, category) P and D = gamma Q P from the
-// eigensystem (Eq. 1; Eq. 8's factor), written as PBpost, PBpre, P', D', P 1.
+// A1 for this path: per (branch, category) P = (V diag(e)) V^{-1} and
+// D = gamma Q P = (V diag(gamma lambda e)) V^{-1} (Eq. 1; Eq. 8's factor),
+// e = exp(gamma b lambda), as two 64^3 products on the FP64 tensor path
+// (V pre-arranged as A fragments, V^{-1} as B fragments at set_eigen); the
+// results are written as PBpost, PBpre, P', D', P 1.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restrict__ V, const double *__restrict__ Vi,
+__global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restrict__ VA,
+                                                         const double *__restrict__ ViB,
                                                          const double *__restrict__ lam,
                                                          const double *__restrict__ rates,
                                                          const double *__restrict__ bl, int S, int R,
@@ -410,40 +414,57 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
     double *Ds = Ps + SP * (SP + 1);
     __shared__ double e[SP], de[SP];
     const int br = blockIdx.x, r = br % R, b = br / R;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double g = rates[r], t = g * bl[b];
     for (int k = threadIdx.x; k < SP; k += blockDim.x) {
         const double ex = k < S ? exp(lam[k] * t) : 0.0;
         e[k] = ex;
         de[k] = k < S ? g * lam[k] * ex : 0.0;
     }
+    double bfr[16];
+    load_bfrag(bfr, ViB, w, lane);
     __syncthreads();
-    for (int idx = threadIdx.x; idx < SP * SP; idx += blockDim.x) {
-        const int s = idx / SP, u = idx % SP;
-        double p = 0.0, d = 0.0;
-        if (s < S && u < S)
-            for (int k = 0; k < S; ++k) {
-                const double vv = V[s * S + k] * Vi[k * S + u];
-                p = fma(vv, e[k], p);
-                d = fma(vv, de[k], d);
+    double ek[16], dk[16];
+#pragma unroll
+    for (int kt = 0; kt < 16; ++kt) { ek[kt] = e[kt * 4 + (lane & 3)]; dk[kt] = de[kt * 4 + (lane & 3)]; }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {              // rows 32h .. 32h+31
+        double ap[4][2], ad[4][2];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) ap[mt][0] = ap[mt][1] = ad[mt][0] = ad[mt][1] = 0.0;
+        const double *A = VA + h * TILE + lane;
+#pragma unroll
+        for (int kt = 0; kt < 16; ++kt)
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const double v = __ldg(A + (mt * 16 + kt) * 32);
+                dmma(ap[mt], v * ek[kt], bfr[kt]);
+                dmma(ad[mt], v * dk[kt], bfr[kt]);
             }
-        Ps[s * (SP + 1) + u] = p;
-        Ds[s * (SP + 1) + u] = d;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            const int m = h * 32 + mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+            Ps[m * (SP + 1) + n] = ap[mt][0];
+            Ps[m * (SP + 1) + n + 1] = ap[mt][1];
+            Ds[m * (SP + 1) + n] = ad[mt][0];
+            Ds[m * (SP + 1) + n + 1] = ad[mt][1];
+        }
     }
     __syncthreads();
     const size_t base = (size_t)br * MAT;
     for (int idx = threadIdx.x; idx < MAT; idx += blockDim.x) {
-        const int lane = idx & 31, kt = (idx >> 5) & 15, nt = idx >> 9;
-        const int kk = kt * 4 + (lane & 3), nn = nt * 8 + (lane >> 2);
+        const int ln = idx & 31, kt = (idx >> 5) & 15, nt = idx >> 9;
+        const int kk = kt * 4 + (ln & 3), nn = nt * 8 + (ln >> 2);
         PBpost[base + idx] = Ps[nn * (SP + 1) + kk];    // B[k=t][n=s] = P[s][t]
         PBpre[base + idx] = Ps[kk * (SP + 1) + nn];     // B[k=s][n=t] = P[s][t]
         const int row = idx / SP, col = idx % SP;
         PT[base + idx] = Ps[col * (SP + 1) + row];      // P'[t][s] = P[s][t]
         DT[base + idx] = Ds[col * (SP + 1) + row];
     }
-    for (int s = threadIdx.x; s < SP; s += blockDim.x) {
+    for (int s2 = threadIdx.x; s2 < SP; s2 += blockDim.x) {
         double acc = 0.0;
-        for (int u = 0; u < SP; ++u) acc += Ps[s * (SP + 1) + u];
-        PONE[(size_t)br * SP + s] = acc;
+        for (int u = 0; u < SP; ++u) acc += Ps[s2 * (SP + 1) + u];
+        PONE[(size_t)br * SP + s2] = acc;
     }
 }
 constexpr size_t pmat_smem() { return (size_t)2 * SP * (SP + 1) * 8; }
