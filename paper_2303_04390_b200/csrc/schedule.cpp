@@ -164,152 +164,6 @@ int build_plan(int32_t N, const int32_t *ops, int32_t n_ops, Plan *out, std::str
     return PG_OK;
 }
 
-namespace {
-
-// Slot allocator over a step schedule.  Each value (a node's u in post, q in
-// pre) is produced in one step and consumed in a later one; inputs of a step
-// are freed before its outputs are allocated (reads precede writes).
-struct SlotAlloc {
-    std::vector<int32_t> slot_of;     // by node
-    std::vector<int32_t> free_list;
-    int32_t used = 0;
-    explicit SlotAlloc(int32_t nn) : slot_of(nn, -1) {}
-    void release(int32_t node) {
-        if (node >= 0 && slot_of[node] >= 0) free_list.push_back(slot_of[node]);
-    }
-    int32_t take(int32_t node) {
-        int32_t s;
-        if (!free_list.empty()) {
-            auto it = std::min_element(free_list.begin(), free_list.end());
-            s = *it;
-            free_list.erase(it);
-        } else {
-            s = used++;
-        }
-        slot_of[node] = s;
-        return s;
-    }
-};
-
-}  // namespace
-
-void build_paired(Plan *plan, int32_t max_slots) {
-    const int32_t N = plan->N, nn = 2 * N - 1, root = 2 * N - 2;
-    const auto &ca = plan->child_a, &cb = plan->child_b;
-    constexpr int WINDOW = 24;
-    // ------------------------------------------------------------ post ----
-    {
-        std::vector<int32_t> order;
-        for (const auto &o : plan->post) order.push_back(o.x);
-        auto schedule = [&](bool pair) {
-            std::vector<std::pair<int32_t, int32_t>> steps;
-            std::vector<char> done(nn, 0), taken(nn, 0);
-            for (int32_t v = 0; v < N; ++v) done[v] = 1;
-            size_t head = 0;
-            while (head < order.size()) {
-                while (head < order.size() && taken[order[head]]) ++head;
-                if (head >= order.size()) break;
-                const int32_t a = order[head];
-                taken[a] = 1;
-                int32_t b = -1;
-                if (pair && a != root)
-                    for (size_t j = head + 1, seen = 0; j < order.size() && seen < WINDOW; ++j) {
-                        const int32_t c = order[j];
-                        if (taken[c]) continue;
-                        ++seen;
-                        if (c != root && done[ca[c]] && done[cb[c]]) { b = c; break; }
-                    }
-                if (b >= 0) taken[b] = 1;
-                steps.push_back({a, b});
-                done[a] = 1;
-                if (b >= 0) done[b] = 1;
-            }
-            return steps;
-        };
-        for (int pass = 0; pass < 2; ++pass) {
-            const auto steps = schedule(pass == 0);
-            SlotAlloc al(nn);
-            std::vector<Op4> prog;
-            for (const auto &st : steps) {
-                const int32_t ks[2] = {st.first, st.second};
-                for (int32_t k : ks)
-                    if (k >= 0) { al.release(ca[k]); al.release(cb[k]); }
-                for (int32_t k : ks) {
-                    if (k < 0) { prog.push_back({kNoOp, 0, 0, 0}); continue; }
-                    auto code = [&](int32_t c) { return c >= N ? -(al.slot_of[c] + 1) : c; };
-                    const int32_t y = code(ca[k]), z = code(cb[k]);
-                    const int32_t w = (k == root) ? 0 : al.take(k);
-                    prog.push_back({k, y, z, w});
-                }
-            }
-            if (pass == 0 && al.used > max_slots) continue;     // too deep: unpaired
-            plan->post2 = std::move(prog);
-            plan->post2_depth = std::max(al.used, 1);
-            break;
-        }
-    }
-    // ------------------------------------------------------------- pre ----
-    {
-        std::vector<int32_t> order, parent(nn, -1);
-        // parents of pre ops: op k consumes q_k produced by parent(k)'s op
-        for (int32_t v = N; v < nn; ++v) {
-            if (ca[v] >= 0) parent[ca[v]] = v;
-            if (cb[v] >= 0) parent[cb[v]] = v;
-        }
-        // recover node order of the pre program (op.y/op.z are children of the op's node)
-        for (const auto &o : plan->pre) {
-            const int32_t c = o.y & ~kTipPartialBit;
-            order.push_back(parent[c]);
-        }
-        auto schedule = [&](bool pair) {
-            std::vector<std::pair<int32_t, int32_t>> steps;
-            std::vector<char> done(nn, 0), taken(nn, 0);
-            size_t head = 0;
-            while (head < order.size()) {
-                while (head < order.size() && taken[order[head]]) ++head;
-                if (head >= order.size()) break;
-                const int32_t a = order[head];
-                taken[a] = 1;
-                int32_t b = -1;
-                if (pair)
-                    for (size_t j = head + 1, seen = 0; j < order.size() && seen < WINDOW; ++j) {
-                        const int32_t c = order[j];
-                        if (taken[c]) continue;
-                        ++seen;
-                        if (c != root && done[parent[c]]) { b = c; break; }
-                    }
-                if (b >= 0) taken[b] = 1;
-                steps.push_back({a, b});
-                done[a] = 1;
-                if (b >= 0) done[b] = 1;
-            }
-            return steps;
-        };
-        for (int pass = 0; pass < 2; ++pass) {
-            const auto steps = schedule(pass == 0);
-            SlotAlloc al(nn);
-            std::vector<Op4> prog;
-            for (const auto &st : steps) {
-                const int32_t ks[2] = {st.first, st.second};
-                int32_t qslot[2] = {-1, -1};
-                for (int i = 0; i < 2; ++i)
-                    if (ks[i] >= 0 && ks[i] != root) { qslot[i] = al.slot_of[ks[i]]; al.release(ks[i]); }
-                for (int i = 0; i < 2; ++i) {
-                    const int32_t k = ks[i];
-                    if (k < 0) { prog.push_back({kNoOp, 0, 0, 0}); continue; }
-                    const int32_t a = ca[k], b = cb[k];
-                    const int32_t sa = a >= N ? al.take(a) : -1, sb = b >= N ? al.take(b) : -1;
-                    prog.push_back({qslot[i], a, b, (sa + 1) | ((sb + 1) << 16)});
-                }
-            }
-            if (pass == 0 && al.used > max_slots) continue;
-            plan->pre2 = std::move(prog);
-            plan->pre2_depth = std::max(al.used, 1);
-            break;
-        }
-    }
-}
-
 void encode_tip_modes(Plan *plan, const std::vector<uint8_t> &tip_is_partial) {
     auto enc = [&](int32_t c) {
         if (c >= 0) {
@@ -320,18 +174,7 @@ void encode_tip_modes(Plan *plan, const std::vector<uint8_t> &tip_is_partial) {
         return c;
     };
     for (auto &o : plan->post) { o.y = enc(o.y); o.z = enc(o.z); }
-    for (auto &o : plan->post2)
-        if (o.x != kNoOp) { o.y = enc(o.y); o.z = enc(o.z); }
     for (auto &o : plan->pre) {
-        auto enc_pre = [&](int32_t c) {
-            int32_t node = c & ~kTipPartialBit;
-            return (node < plan->N && tip_is_partial[node]) ? (node | kTipPartialBit) : node;
-        };
-        o.y = enc_pre(o.y);
-        o.z = enc_pre(o.z);
-    }
-    for (auto &o : plan->pre2) {
-        if (o.x == kNoOp) continue;
         auto enc_pre = [&](int32_t c) {
             int32_t node = c & ~kTipPartialBit;
             return (node < plan->N && tip_is_partial[node]) ? (node | kTipPartialBit) : node;

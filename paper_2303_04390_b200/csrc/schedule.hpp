@@ -41,21 +41,7 @@ struct Plan {
     // (post, tips = 0) and by depth (pre, root = 0); level i of each is
     // level_nodes[off[i] .. off[i+1])
     std::vector<int32_t> level_nodes, post_off, pre_off;
-    // paired programs (small-S kernel): step i executes post2[2i] and
-    // post2[2i+1] (x == kNoOp => single op) -- two ops with no dependence
-    // between them, so their instruction streams interleave.  Slots are
-    // re-allocated for the paired schedule (inputs are read before outputs
-    // are written within a step).
-    std::vector<Op4> post2, pre2;
-    int32_t post2_depth = 0, pre2_depth = 0;
 };
-
-constexpr int32_t kNoOp = -0x40000000;
-
-// Build post2/pre2 from a valid plan (greedy pairing inside a lookahead
-// window, then interval slot allocation; pairing is skipped when it would
-// raise the slot count above `max_slots`).
-void build_paired(Plan *plan, int32_t max_slots);
 
 // Returns 0 on success, else a PG_ERR_* code with *err filled.
 int build_plan(int32_t N, const int32_t *ops, int32_t n_ops, Plan *out, std::string *err);
