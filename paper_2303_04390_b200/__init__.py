@@ -22,7 +22,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libphylograd.so")
+LIB_PATH = os.environ.get("PHYLOGRAD_LIB", os.path.join(_HERE, "lib", "libphylograd.so"))
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "phylograd.h")
 
 if not os.path.exists(LIB_PATH):

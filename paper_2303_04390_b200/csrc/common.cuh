@@ -26,7 +26,21 @@ struct TravArgs {
     double *logl_part;          // [n_tiles] per-tile logL partial sums
     int *status;                // first zero-likelihood pattern (INT_MAX = none)
     int N, S, R, Cpad, C, n_tiles, depth, prefetch;
+    int prog_smem_off;          // > 0: byte offset of the staged op programs in dynamic smem
+    long long *trace;           // PG_TRACE builds only: clock64 samples of CTA 0
 };
+
+// ---- optional phase timing (compiled in only with -DPG_TRACE) --------------
+#ifdef PG_TRACE
+#define PG_TSTAMP(slot, dep)                                                             \
+    do {                                                                                 \
+        long long _c;                                                                    \
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(_c) : "r"(__double2hiint((double)(dep))) : "memory"); \
+        if (a.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0) a.trace[(slot)] = _c;  \
+    } while (0)
+#else
+#define PG_TSTAMP(slot, dep) do { } while (0)
+#endif
 
 // ---- cp.async (LDGSTS) ----------------------------------------------------
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {

@@ -175,12 +175,13 @@ struct pg_instance {
     int *status_pinned = nullptr;
     bool bl_host_pending = false;
     // launch configuration
-    int prefetch = 4, smem = 0, grid = 0, block = 0, tiles_per_cta = 1;
+    int prefetch = 4, smem = 0, grid = 0, block = 0, tiles_per_cta = 1, prog_smem_off = 0;
     cudaGraphExec_t gexec = nullptr;
     double *gexec_out = nullptr;
     bool timing = false;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     std::string err;
+    long long *trace = nullptr;         // PG_TRACE builds: [2(N-1)][8] clock samples
 
     template <typename T> T *at(size_t off) { return reinterpret_cast<T *>(ws + off); }
     int fail(int code, const std::string &msg) { err = msg; return code; }
@@ -558,6 +559,14 @@ static int configure(pg_instance *inst) {
         inst->prefetch = (L.SP <= 8) ? 4 : 2;
         inst->smem = (int)small_smem(L, R, K, depth);
         if (inst->smem > 227 * 1024) return inst->fail(PG_ERR_UNSUPPORTED, "traversal does not fit in shared memory");
+        // stage both op programs in smem when they fit (producer/consumers never read ops from HBM)
+        const int prog_bytes = 2 * (inst->cfg.tips - 1) * (int)sizeof(Op4);
+        const int off = (inst->smem + 15) / 16 * 16;
+        inst->prog_smem_off = 0;
+        if (off + prog_bytes <= 227 * 1024) {
+            inst->prog_smem_off = off;
+            inst->smem = off + prog_bytes;
+        }
     } else if (L.variant == 2) {
         inst->block = pg::codon::NT;
         inst->prefetch = 0;
@@ -632,6 +641,8 @@ static pg::TravArgs trav_args(pg_instance *inst) {
     a.n_tiles = L.n_tiles;
     a.depth = std::max(inst->plan.post_depth, inst->plan.pre_depth);
     a.prefetch = inst->prefetch;
+    a.prog_smem_off = inst->prog_smem_off;
+    a.trace = inst->trace;
     return a;
 }
 
@@ -764,6 +775,12 @@ static int prepare(pg_instance *inst) {
 static int launch_eval(pg_instance *inst, double *d_out) {
     if (!inst->gexec || inst->gexec_out != d_out) {
         if (inst->gexec) { cudaGraphExecDestroy(inst->gexec); inst->gexec = nullptr; }
+#ifdef PG_TRACE
+        if (!inst->trace) {   // allocation is illegal inside stream capture
+            cudaMalloc((void **)&inst->trace, sizeof(long long) * 16 * 2 * (size_t)inst->cfg.tips);
+            cudaMemset(inst->trace, 0, sizeof(long long) * 16 * 2 * (size_t)inst->cfg.tips);
+        }
+#endif
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(inst->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
         int rc = enqueue_eval(inst, d_out);
@@ -850,6 +867,16 @@ int pg_get_kernel_times(pg_instance *inst, float *ms) {
     for (int k = 0; k < 3; ++k) CK(cudaEventElapsedTime(&ms[k], inst->ev[k], inst->ev[k + 1]), "elapsed");
     return PG_OK;
 }
+
+#ifdef PG_TRACE
+// trace builds only: copy the clock64 samples of the last evaluation
+extern "C" int pg_trace_copy(pg_instance *inst, long long *host, int n) {
+    if (!inst || !inst->trace) return PG_ERR_SEQUENCE;
+    cudaStreamSynchronize(inst->stream);
+    cudaMemcpy(host, inst->trace, sizeof(long long) * n, cudaMemcpyDeviceToHost);
+    return PG_OK;
+}
+#endif
 
 int pg_kernels_per_eval(const pg_instance *inst, int32_t *n) {
     if (!inst || !n) return PG_ERR_ARG;

@@ -40,6 +40,10 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef PG_SMALL_W
+#define PG_SMALL_W 2
+#endif
+
 namespace pg {
 
 // ---- shape of one CTA's work ----------------------------------------------
@@ -53,12 +57,13 @@ struct SmallCfg {
     static constexpr int TP = 32 / RP;                        // patterns per warp tile
     static constexpr int D = (SP <= 8) ? 4 : 2;                // stage ring depth
     static constexpr int PF = 16;                              // L2 prefetch distance (steps)
-    static constexpr int W = 2;                                // gradient window (steps)
+    static constexpr int W = PG_SMALL_W;                       // gradient window (steps)
     static constexpr int VB = SP * (int)sizeof(Real);          // vector bytes
     static constexpr int MATB = SP * SP * (int)sizeof(Real);   // one category's matrix
     static constexpr int CS = MATB + (RP > 1 ? 16 : 0);        // padded category stride
     static constexpr int ND = W * 2 * 32 * 16;                 // (num, den) window per warp
-    static constexpr int BARS = 128;                           // mbarrier area
+    static constexpr int QOFF = 128;                           // Q (SP > 4 only; SP <= 4 keeps it in registers)
+    static constexpr int BARS = QOFF + (SP > 4 ? SP * SP * (int)sizeof(Real) : 0);   // barriers + Q
     static __host__ __device__ int mat_slot(int R) { return R * CS; }
     static __host__ __device__ int vslot(int R, int K) {       // one child's vectors for K warps
         int a = K * TP * R * VB, b = K * TP * VB, c = (15 + K * TP + 15) / 16 * 16;
@@ -190,6 +195,19 @@ __device__ __forceinline__ double cat_sum(double v) {
     for (int o = 1; o < RP; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
+// n / d for the Eq. 8 ratio, branch-free: hardware reciprocal estimate, two
+// Newton steps and one residual correction (faithful to <= 1 ulp; d is a
+// normal positive number: vectors are rescaled long before denormals).
+__device__ __forceinline__ double ratio(double n, double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    const double q = n * r;
+    return fma(fma(-d, q, n), r, q);
+}
 // Rescale v (exactly) if any vector of the warp fell below the threshold;
 // returns the exponent removed (shared by the categories of a pattern).
 template <typename Real, int SP, int RP>
@@ -230,12 +248,34 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
     const uint8_t *__restrict__ tipS = a.tip_states;
     char *__restrict__ Ub = static_cast<char *>(a.u);
 
+    // both traversal programs staged once in shared memory (when they fit), so
+    // neither the producer nor the consumers read ops from global memory
+    uint64_t *prog_bar = post_done + 1;
+    const Op4 *post_prog = a.post, *pre_prog = a.pre;
+    if (a.prog_smem_off > 0) {
+        post_prog = reinterpret_cast<const Op4 *>(smem + a.prog_smem_off);
+        pre_prog = post_prog + (N - 1);
+    }
     if (threadIdx.x == 0) {
         for (int i = 0; i < D; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, K); }
         mbar_init(post_done, K);
+        mbar_init(prog_bar, 1);
         fence_mbar_init();
+        if (a.prog_smem_off > 0) {
+            const unsigned pb = (unsigned)(N - 1) * 16u;
+            mbar_arrive_expect_tx(prog_bar, 2 * pb);
+            bulk_g2s(smem + a.prog_smem_off, a.post, pb, prog_bar);
+            bulk_g2s(smem + a.prog_smem_off + pb, a.pre, pb, prog_bar);
+        } else {
+            mbar_arrive_expect_tx(prog_bar, 0);
+        }
+    }
+    if constexpr (SP > 4) {
+        Real *Qs = reinterpret_cast<Real *>(smem + Cfg::QOFF);
+        for (int i = threadIdx.x; i < SP * SP; i += blockDim.x) Qs[i] = static_cast<const Real *>(a.Q)[i];
     }
     __syncthreads();
+    mbar_wait(prog_bar, 0u);
 
     // =============================== producer ===================================
     if (warp == K) {
@@ -254,12 +294,15 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
         for (int t = 0; t < 2 * nops; ++t) {
             const bool pre = t >= nops;
             const int m = pre ? t - nops : t;
+            PG_TSTAMP((size_t)t * 16 + 0, t);
             if (t == nops) mbar_wait(post_done, 0);       // u of every tile stored + fenced
             if (t >= D) mbar_wait(empty + t % D, (uint32_t)(t / D + 1) & 1u);
+            PG_TSTAMP((size_t)t * 16 + 1, t);
             if (lane == 0) {
                 unsigned char *st = stages + (t % D) * ST;
                 uint64_t *bar = full + t % D;
-                const Op4 *prog = pre ? a.pre : a.post;
+                const Op4 *gprog = pre ? a.pre : a.post;           // global copy (bulk source)
+                const Op4 *prog = pre ? pre_prog : post_prog;       // smem copy when staged
                 const Op4 op = prog[m];
                 fence_proxy_async_smem();
                 if (!pre) {
@@ -267,7 +310,7 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
                     const unsigned bytes = 16 + (op.x != root ? MS : 0) + (op.y >= 0 ? MS + tip_bytes(op.y) : 0) +
                                            (op.z >= 0 ? MS + tip_bytes(op.z) : 0);
                     mbar_arrive_expect_tx(bar, bytes);
-                    bulk_g2s(st, prog + m, 16, bar);
+                    bulk_g2s(st, gprog + m, 16, bar);
                     if (op.x != root) bulk_g2s(st + 16, Pb + (size_t)op.x * MS, MS, bar);
                     if (op.y >= 0) {
                         bulk_g2s(st + 16 + MS, Pb + (size_t)(op.y & ~kTipPartialBit) * MS, MS, bar);
@@ -283,7 +326,7 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
                     const unsigned bytes = 16 + 2 * MS + (na >= N ? u_bytes : tip_bytes(op.y)) +
                                            (nb >= N ? u_bytes : tip_bytes(op.z));
                     mbar_arrive_expect_tx(bar, bytes);
-                    bulk_g2s(st, prog + m, 16, bar);
+                    bulk_g2s(st, gprog + m, 16, bar);
                     bulk_g2s(st + 16, Pb + (size_t)na * MS, MS, bar);
                     bulk_g2s(st + 16 + MS, Pb + (size_t)nb * MS, MS, bar);
                     if (na >= N) bulk_g2s(st + 16 + 3 * MS, u_src(na), u_bytes, bar);
@@ -298,6 +341,7 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
                     }
                 }
             }
+            PG_TSTAMP((size_t)t * 16 + 2, t);
             __syncwarp();
         }
         return;
@@ -347,18 +391,48 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
     };
 
     // ------------------------- post program (Eq. 2, Eq. 3) -----------------------
+    // The next op is decoded while the current step computes, and the u just
+    // pushed is forwarded through registers when the next op consumes it
+    // (the common case in a depth-first order): no STS -> LDS round trip.
     int E = 0;                    // post-order exponents removed from this pattern
     double logl_local = 0.0;
+    int prev_slot = -1;
+    Real prev_u[SP];
+    Op4 op_next = {0, 0, 0, 0};
+    if (active && nops > 0) {
+        mbar_wait(full, 0u);
+        op_next = *reinterpret_cast<const Op4 *>(stages);
+    }
+    auto stack_or_fwd = [&](Real (&u)[SP], int code) {
+        const int sl = -code - 1;
+        if (sl == prev_slot) {
+#pragma unroll
+            for (int s = 0; s < SP; ++s) u[s] = prev_u[s];
+        } else {
+            lds_vec<Real, SP>(u, stack_at(sl));
+        }
+    };
     for (int t = 0; t < nops; ++t) {
-        mbar_wait(full + t % D, (uint32_t)(t / D) & 1u);
-        if (!active) { release(t); continue; }
+        if (!active) {
+            mbar_wait(full + t % D, (uint32_t)(t / D) & 1u);
+            release(t);
+            continue;
+        }
         const unsigned char *st = stages + (t % D) * ST;
-        const Op4 op = *reinterpret_cast<const Op4 *>(st);
+        const Op4 op = op_next;
+        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 3, op.x);
         Real ua[SP], ub[SP];
-        if (op.y < 0) lds_vec<Real, SP>(ua, stack_at(-op.y - 1));
+        if (op.y < 0) stack_or_fwd(ua, op.y);
         else child_tip(ua, st + 16 + MS, st + 16 + 3 * MS, op.y);
-        if (op.z < 0) lds_vec<Real, SP>(ub, stack_at(-op.z - 1));
+        if (op.z < 0) stack_or_fwd(ub, op.z);
         else child_tip(ub, st + 16 + 2 * MS, st + 16 + 3 * MS + VS, op.z);
+        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 4, ua[0] + ub[SP - 1]);
+        if (t + 1 < nops) {
+            const int t1 = t + 1;
+            mbar_wait(full + t1 % D, (uint32_t)(t1 / D) & 1u);
+            op_next = *reinterpret_cast<const Op4 *>(stages + (t1 % D) * ST);
+        }
+        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 5, op_next.x);
         Real p[SP];
 #pragma unroll
         for (int s = 0; s < SP; ++s) p[s] = ua[s] * ub[s];
@@ -374,11 +448,16 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
             }
         } else {
             E += maybe_rescale<Real, SP, RP>(p);
+            if (warp == 0) PG_TSTAMP((size_t)t * 16 + 6, p[0]);
             Real u[SP];
             mv<Real, SP>(u, reinterpret_cast<const Real *>(st + 16 + mat_lane), p);
+            if (warp == 0) PG_TSTAMP((size_t)t * 16 + 7, u[0] + u[SP - 1]);
             release(t);
-            if (live) stg_vec<Real, SP>(Ub + (size_t)(op.x - N) * u_node + u_lane, u);
+            stg_vec<Real, SP>(Ub + (size_t)(op.x - N) * u_node + u_lane, u);   // shadow lanes: same value
             sts_vec<Real, SP>(stack_at(op.w), u);
+#pragma unroll
+            for (int s = 0; s < SP; ++s) prev_u[s] = u[s];
+            prev_slot = op.w;
         }
     }
     if (active) {
@@ -399,17 +478,36 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
 #pragma unroll
             for (int t = 0; t < SP; ++t) Qr[s][t] = static_cast<const Real *>(a.Q)[s * SP + t];
     }
-    const Real *Qg = static_cast<const Real *>(a.Q);
+    const Real *Qs = reinterpret_cast<const Real *>(smem + Cfg::QOFF);
+    // next op decoded early; the q's pushed by the previous step are
+    // forwarded through registers when this step pops one of them
+    int fslot[2] = {-1, -1};
+    Real fq[2][SP];
+    Op4 opn = {0, 0, 0, 0};
+    if (active && nops > 0) {
+        mbar_wait(full + nops % D, (uint32_t)(nops / D) & 1u);
+        opn = *reinterpret_cast<const Op4 *>(stages + (nops % D) * ST);
+    }
     for (int n = 0; n < nops; ++n) {
         const int t = nops + n;
-        mbar_wait(full + t % D, (uint32_t)(t / D) & 1u);
-        if (!active) { release(t); continue; }
+        if (!active) {
+            mbar_wait(full + t % D, (uint32_t)(t / D) & 1u);
+            release(t);
+            continue;
+        }
         const unsigned char *st = stages + (t % D) * ST;
-        const Op4 op = *reinterpret_cast<const Op4 *>(st);
+        const Op4 op = opn;
+        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 3, op.x);
         Real q[SP];
         if (op.x < 0) {
 #pragma unroll
             for (int s = 0; s < SP; ++s) q[s] = pi[s];
+        } else if (op.x == fslot[0]) {
+#pragma unroll
+            for (int s = 0; s < SP; ++s) q[s] = fq[0][s];
+        } else if (op.x == fslot[1]) {
+#pragma unroll
+            for (int s = 0; s < SP; ++s) q[s] = fq[1][s];
         } else {
             lds_vec<Real, SP>(q, stack_at(op.x));
         }
@@ -422,6 +520,13 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
             if ((cs[c] & ~kTipPartialBit) >= N) lds_vec<Real, SP>(uc[c], vs + u_vec);
             else child_tip(uc[c], st + 16 + c * MS, vs, cs[c]);
         }
+        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 4, q[0] + uc[0][0] + uc[1][SP - 1]);
+        if (n + 1 < nops) {
+            const int t1 = t + 1;
+            mbar_wait(full + t1 % D, (uint32_t)(t1 / D) & 1u);
+            opn = *reinterpret_cast<const Op4 *>(stages + (t1 % D) * ST);
+        }
+        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 5, opn.x);
         Real qc[2][SP];
 #pragma unroll
         for (int c = 0; c < 2; ++c)
@@ -431,6 +536,7 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
                 for (int s = 0; s < SP; ++s) x[s] = q[s] * uc[1 - c][s];
                 mvt<Real, SP>(qc[c], reinterpret_cast<const Real *>(st + 16 + c * MS + mat_lane), x);
             }
+        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 6, qc[0][0] + qc[1][0]);
         release(t);                                 // stage no longer needed
         double2 *ndw = nd + (n % W) * 64 + lane;
 #pragma unroll
@@ -446,9 +552,11 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
 #pragma unroll
                     for (int t2 = 1; t2 < SP; ++t2) Qu = fma(Qr[s][t2], uc[c][t2], Qu);
                 } else {
-                    Qu = __ldg(Qg + s * SP) * uc[c][0];
+                    Real row[SP];
+                    lds_vec<Real, SP>(row, Qs + s * SP);
+                    Qu = row[0] * uc[c][0];
 #pragma unroll
-                    for (int t2 = 1; t2 < SP; ++t2) Qu = fma(__ldg(Qg + s * SP + t2), uc[c][t2], Qu);
+                    for (int t2 = 1; t2 < SP; ++t2) Qu = fma(row[t2], uc[c][t2], Qu);
                 }
                 num = fma(xs, Qu, num);
                 den = fma(xs, uc[c][s], den);
@@ -459,6 +567,18 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
                 sts_vec<Real, SP>(stack_at(slots[c]), qc[c]);
             }
         }
+        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 7, qc[0][0] + qc[1][0]);
+        // registers now hold the latest values of these slots
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            fslot[c] = slots[c];
+#pragma unroll
+            for (int s = 0; s < SP; ++s) fq[c][s] = qc[c][s];
+        }
+        // a slot written by this step but not re-pushed keeps its smem value; slots
+        // that were forwarded earlier but overwritten now are no longer valid
+        if (fslot[0] == fslot[1]) fslot[1] = -1;
+        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 8, fq[0][0] + fq[1][0]);
         if (n % W == W - 1 || n == nops - 1) {
             // W steps of (num_r, den_r) -> Eq. 8 ratio per pattern, weighted (Eq. 6),
             // summed over the tile's patterns; all 32 lanes busy.
@@ -477,13 +597,18 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
 #pragma unroll
                     for (int q2 = 0; q2 < RP; ++q2) { const double2 v = src[q2]; num += v.x; den += v.y; }
                     const double w = wbuf[p];
+#ifdef PG_SLOWDIV
                     acc += (w != 0.0) ? w * (num / den) : 0.0;
+#else
+                    acc = fma(w, ratio(num, (w != 0.0) ? den : 1.0), acc);   // w = 0: padding
+#endif
                 }
             }
 #pragma unroll
             for (int o = 1; o < LPP; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             if (sub == 0 && n2 <= n) a.grad_part[(size_t)nodes_w[wstep * 2 + c] * a.n_tiles + tile] = acc;
             __syncwarp();
+            if (warp == 0) PG_TSTAMP((size_t)t * 16 + 9, acc);
         }
     }
 }
