@@ -77,7 +77,7 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         }
         int Rp = 1;
         while (Rp < R) Rp <<= 1;
-        L->tpl = 32 / Rp;      // patterns per warp tile (lane = pattern x category)
+        L->tpl = 32 / (Rp * pg::small_lanes_per_vector(SP));   // patterns per warp tile (lane = pattern x category x state group)
     } else if (L->variant == 2) {
         if (R > 16) { if (err) *err = "too many rate categories (max 16)"; return PG_ERR_UNSUPPORTED; }
         L->tpl = pg::codon::T;

@@ -46,6 +46,14 @@
 
 namespace pg {
 
+// lanes per (pattern, category) vector: each lane holds VL = SP / LV states.
+// SP = 4 keeps a whole vector per lane; S = 8 and 16 split it over 2 and 4
+// lanes so a warp's 32 lanes hold 8 patterns x R categories at any S (more
+// resident warps, a quarter of the per-lane matvec work for S = 16).
+// (Splitting S = 4 over 2 lanes as well was measured 2x slower on the dengue
+// workload: twice the warps, the same per-step control work.)
+__host__ __device__ constexpr int small_lanes_per_vector(int SP) { return SP / 4; }
+
 // ---- shape of one CTA's work ----------------------------------------------
 // A CTA = K consumer warps (one pattern tile each) + 1 producer warp.  Global
 // layout of the transition matrices for this kernel: per branch, R category
@@ -54,14 +62,19 @@ namespace pg {
 // matrices are one contiguous bulk copy.
 template <typename Real, int SP, int RP>
 struct SmallCfg {
-    static constexpr int TP = 32 / RP;                        // patterns per warp tile
+    static constexpr int LV = small_lanes_per_vector(SP);     // lanes per vector
+    static constexpr int VL = SP / LV;                         // states per lane
+    static constexpr int TP = 32 / (RP * LV);                  // patterns per warp tile
     static constexpr int D = (SP <= 8) ? 4 : 2;                // stage ring depth
     static constexpr int PF = 16;                              // L2 prefetch distance (steps)
     static constexpr int W = PG_SMALL_W;                       // gradient window (steps)
     static constexpr int VB = SP * (int)sizeof(Real);          // vector bytes
+    static constexpr int VBL = VL * (int)sizeof(Real);         // one lane's part of a vector
     static constexpr int MATB = SP * SP * (int)sizeof(Real);   // one category's matrix
     static constexpr int CS = MATB + (RP > 1 ? 16 : 0);        // padded category stride
     static constexpr int ND = W * 2 * 32 * 16;                 // (num, den) window per warp
+    static constexpr int XGS = VB + 16;                        // exchange stride per lane group (bank skew)
+    static constexpr int XB = LV > 1 ? (32 / LV) * XGS : 0;    // full-vector exchange buffer per warp
     static constexpr int QOFF = 128;                           // Q (SP > 4 only; SP <= 4 keeps it in registers)
     static constexpr int BARS = QOFF + (SP > 4 ? SP * SP * (int)sizeof(Real) : 0);   // barriers + Q
     static __host__ __device__ int mat_slot(int R) { return R * CS; }
@@ -72,88 +85,126 @@ struct SmallCfg {
         return (m + 15) / 16 * 16;
     }
     static __host__ __device__ int stage(int R, int K) { return 16 + 3 * mat_slot(R) + 2 * vslot(R, K); }
-    static __host__ __device__ int warp_bytes(int depth) { return (depth * 32 * VB + ND + TP * 8 + W * 2 * 4 + 8 + 15) / 16 * 16; }
+    // stack: depth slots + one holding pi (the root's q)
+    static __host__ __device__ int warp_bytes(int depth) {
+        return ((depth + 1) * 32 * VBL + ND + XB + TP * 8 + W * 2 * 4 + 8 + 15) / 16 * 16;
+    }
     static __host__ __device__ size_t smem(int R, int K, int depth) {
         return (size_t)BARS + (size_t)D * stage(R, K) + (size_t)K * warp_bytes(depth);
     }
 };
 
-// ---- vector access helpers ------------------------------------------------
-template <typename Real, int SP>
-__device__ __forceinline__ void lds_vec(Real (&d)[SP], const void *src) {
+// ---- vector access helpers (n values, 16-byte chunks where possible) -------
+template <typename Real, int n>
+__device__ __forceinline__ void lds_vec(Real (&d)[n], const void *src) {
     if constexpr (sizeof(Real) == 8) {
 #pragma unroll
-        for (int i = 0; i < SP / 2; ++i) {
+        for (int i = 0; i < n / 2; ++i) {
             const double2 t = reinterpret_cast<const double2 *>(src)[i];
             d[2 * i] = t.x;
             d[2 * i + 1] = t.y;
         }
-    } else {
+        if constexpr (n % 2) d[n - 1] = reinterpret_cast<const double *>(src)[n - 1];
+    } else if constexpr (n % 4 == 0) {
 #pragma unroll
-        for (int i = 0; i < SP / 4; ++i) {
+        for (int i = 0; i < n / 4; ++i) {
             const float4 t = reinterpret_cast<const float4 *>(src)[i];
             d[4 * i] = t.x; d[4 * i + 1] = t.y; d[4 * i + 2] = t.z; d[4 * i + 3] = t.w;
         }
-    }
-}
-template <typename Real, int SP>
-__device__ __forceinline__ void sts_vec(void *dst, const Real (&d)[SP]) {
-    if constexpr (sizeof(Real) == 8) {
-#pragma unroll
-        for (int i = 0; i < SP / 2; ++i) reinterpret_cast<double2 *>(dst)[i] = make_double2(d[2 * i], d[2 * i + 1]);
     } else {
 #pragma unroll
-        for (int i = 0; i < SP / 4; ++i)
+        for (int i = 0; i < n; ++i) d[i] = reinterpret_cast<const float *>(src)[i];
+    }
+}
+template <typename Real, int n>
+__device__ __forceinline__ void sts_vec(void *dst, const Real (&d)[n]) {
+    if constexpr (sizeof(Real) == 8) {
+#pragma unroll
+        for (int i = 0; i < n / 2; ++i) reinterpret_cast<double2 *>(dst)[i] = make_double2(d[2 * i], d[2 * i + 1]);
+        if constexpr (n % 2) reinterpret_cast<double *>(dst)[n - 1] = d[n - 1];
+    } else if constexpr (n % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < n / 4; ++i)
             reinterpret_cast<float4 *>(dst)[i] = make_float4(d[4 * i], d[4 * i + 1], d[4 * i + 2], d[4 * i + 3]);
-    }
-}
-template <typename Real, int SP>
-__device__ __forceinline__ void stg_vec(void *dst, const Real (&d)[SP]) {
-    if constexpr (sizeof(Real) == 8) {
-#pragma unroll
-        for (int i = 0; i < SP / 2; ++i) __stcg(reinterpret_cast<double2 *>(dst) + i, make_double2(d[2 * i], d[2 * i + 1]));
     } else {
 #pragma unroll
-        for (int i = 0; i < SP / 4; ++i)
+        for (int i = 0; i < n; ++i) reinterpret_cast<float *>(dst)[i] = d[i];
+    }
+}
+template <typename Real, int n>
+__device__ __forceinline__ void stg_vec(void *dst, const Real (&d)[n]) {
+    if constexpr (sizeof(Real) == 8) {
+#pragma unroll
+        for (int i = 0; i < n / 2; ++i) __stcg(reinterpret_cast<double2 *>(dst) + i, make_double2(d[2 * i], d[2 * i + 1]));
+        if constexpr (n % 2) __stcg(reinterpret_cast<double *>(dst) + n - 1, d[n - 1]);
+    } else if constexpr (n % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < n / 4; ++i)
             __stcg(reinterpret_cast<float4 *>(dst) + i, make_float4(d[4 * i], d[4 * i + 1], d[4 * i + 2], d[4 * i + 3]));
+    } else {
+#pragma unroll
+        for (int i = 0; i < n; ++i) __stcg(reinterpret_cast<float *>(dst) + i, d[i]);
     }
 }
 
-// y = M x (y[s] = sum_t M[s][t] x[t]), M row-major in shared memory
-template <typename Real, int SP>
-__device__ __forceinline__ void mv(Real (&y)[SP], const Real *M, const Real (&x)[SP]) {
+// The lane owns states [h VL, h VL + VL) of a vector.  Whole vectors it
+// gathers are kept ROTATED by h VL (its own block first): x[j] holds state
+// (j + h VL) mod SP.  Walking matrix rows in the same rotated order makes the
+// LV lanes of a group read different shared-memory banks (rows are 32 banks
+// long, so unrotated they would all start on bank 0).  LV = 1: no rotation.
+// y = rows [h VL, +VL) of M x, M row-major SP x SP in shared memory
+template <typename Real, int SP, int VL>
+__device__ __forceinline__ void mv(Real (&y)[VL], const Real *M, const Real (&x)[SP], int h) {
+    constexpr int LV = SP / VL;
 #pragma unroll
-    for (int s = 0; s < SP; ++s) {
-        Real row[SP];
-        lds_vec<Real, SP>(row, M + s * SP);
-        Real acc = row[0] * x[0];
+    for (int i = 0; i < VL; ++i) {
+        const Real *row = M + (h * VL + i) * SP;
+        Real acc = 0;
 #pragma unroll
-        for (int t = 1; t < SP; ++t) acc = fma(row[t], x[t], acc);
-        y[s] = acc;
+        for (int b = 0; b < LV; ++b) {
+            Real blk[VL];
+            lds_vec<Real, VL>(blk, row + ((b + h) & (LV - 1)) * VL);
+#pragma unroll
+            for (int t = 0; t < VL; ++t) acc = (b == 0 && t == 0) ? blk[0] * x[0] : fma(blk[t], x[b * VL + t], acc);
+        }
+        y[i] = acc;
     }
 }
-// y = M' x (y[t] = sum_s M[s][t] x[s])
-template <typename Real, int SP>
-__device__ __forceinline__ void mvt(Real (&y)[SP], const Real *M, const Real (&x)[SP]) {
+// y = entries [h VL, +VL) of M' x (y[i] = sum_s M[s][h VL + i] x[s]), x rotated
+template <typename Real, int SP, int VL>
+__device__ __forceinline__ void mvt(Real (&y)[VL], const Real *M, const Real (&x)[SP], int h) {
 #pragma unroll
-    for (int s = 0; s < SP; ++s) {
-        Real row[SP];
-        lds_vec<Real, SP>(row, M + s * SP);
+    for (int j = 0; j < SP; ++j) {
+        const int s = (j + h * VL) & (SP - 1);
+        Real row[VL];
+        lds_vec<Real, VL>(row, M + s * SP + h * VL);
 #pragma unroll
-        for (int t = 0; t < SP; ++t) y[t] = s == 0 ? row[t] * x[0] : fma(row[t], x[s], y[t]);
+        for (int i = 0; i < VL; ++i) y[i] = j == 0 ? row[i] * x[0] : fma(row[i], x[j], y[i]);
     }
 }
-// u = column s of M (observed tip state) or M 1 (missing, s >= S)
-template <typename Real, int SP>
-__device__ __forceinline__ void mcol(Real (&u)[SP], const Real *M, int s, int S) {
+// rotated whole vector from shared memory (LV blocks of VL)
+template <typename Real, int SP, int VL>
+__device__ __forceinline__ void lds_rot(Real (&x)[SP], const unsigned char *src, int h) {
+    constexpr int LV = SP / VL;
+#pragma unroll
+    for (int b = 0; b < LV; ++b) {
+        Real blk[VL];
+        lds_vec<Real, VL>(blk, src + ((b + h) & (LV - 1)) * VL * (int)sizeof(Real));
+#pragma unroll
+        for (int t = 0; t < VL; ++t) x[b * VL + t] = blk[t];
+    }
+}
+// u = entries [h VL, +VL) of column s of M (observed tip state) or of M 1 (missing, s >= S)
+template <typename Real, int SP, int VL>
+__device__ __forceinline__ void mcol(Real (&u)[VL], const Real *M, int s, int S, int h) {
     if (s < S) {
 #pragma unroll
-        for (int x = 0; x < SP; ++x) u[x] = M[x * SP + s];
+        for (int x = 0; x < VL; ++x) u[x] = M[(h * VL + x) * SP + s];
     } else {
 #pragma unroll
-        for (int x = 0; x < SP; ++x) {
+        for (int x = 0; x < VL; ++x) {
             Real row[SP];
-            lds_vec<Real, SP>(row, M + x * SP);
+            lds_vec<Real, SP>(row, M + (h * VL + x) * SP);
             Real acc = row[0];
 #pragma unroll
             for (int t = 1; t < SP; ++t) acc += row[t];
@@ -163,23 +214,27 @@ __device__ __forceinline__ void mcol(Real (&u)[SP], const Real *M, int s, int S)
 }
 
 // ---- exact power-of-two rescaling -----------------------------------------
-__device__ __forceinline__ int expfield(double x) { return __double2hiint(x) >> 20; }   // x >= 0
-__device__ __forceinline__ int expfield(float x) { return __float_as_int(x) >> 23; }
+// high word of a non-negative value: ordered like the value, exponent field in
+// bits 20 (fp64) / 23 (fp32) and up
+__device__ __forceinline__ int hiword(double x) { return __double2hiint(x); }
+__device__ __forceinline__ int hiword(float x) { return __float_as_int(x); }
 template <typename Real, int SP>
-__device__ __forceinline__ int max_expfield(const Real (&v)[SP]) {
-    int m = expfield(v[0]);
+__device__ __forceinline__ int max_hiword(const Real (&v)[SP]) {
+    int m = hiword(v[0]);
 #pragma unroll
-    for (int i = 1; i < SP; ++i) m = max(m, expfield(v[i]));
+    for (int i = 1; i < SP; ++i) m = max(m, hiword(v[i]));
     return m;
 }
 template <typename Real> struct ScaleTraits;
 template <> struct ScaleTraits<double> {
     static constexpr int THRESH = 1023 - 256;   // rescale once a max drops below 2^-256
+    static constexpr int SHIFT = 20;
     static __device__ __forceinline__ int exponent(int field) { return min(max(field - 1022, -1021), 1022); }
     static __device__ __forceinline__ double factor(int e) { return __longlong_as_double((long long)(1023 - e) << 52); }
 };
 template <> struct ScaleTraits<float> {
     static constexpr int THRESH = 127 - 64;      // 2^-64
+    static constexpr int SHIFT = 23;
     static __device__ __forceinline__ int exponent(int field) { return min(max(field - 126, -125), 126); }
     static __device__ __forceinline__ float factor(int e) { return __int_as_float((127 - e) << 23); }
 };
@@ -210,11 +265,13 @@ __device__ __forceinline__ double ratio(double n, double d) {
 }
 // Rescale v (exactly) if any vector of the warp fell below the threshold;
 // returns the exponent removed (shared by the categories of a pattern).
-template <typename Real, int SP, int RP>
+// G = lanes sharing one pattern (categories x state groups, contiguous)
+template <typename Real, int SP, int G>
 __device__ __forceinline__ int maybe_rescale(Real (&v)[SP]) {
-    const int f = max_expfield<Real, SP>(v);
-    if (!__any_sync(0xffffffffu, f < ScaleTraits<Real>::THRESH)) return 0;
-    const int e = ScaleTraits<Real>::exponent(cat_max<RP>(f));
+    using T = ScaleTraits<Real>;
+    const int h = max_hiword<Real, SP>(v);
+    if (!__any_sync(0xffffffffu, h < (T::THRESH << T::SHIFT))) return 0;
+    const int e = T::exponent(cat_max<G>(h) >> T::SHIFT);
     const Real s = ScaleTraits<Real>::factor(e);
 #pragma unroll
     for (int i = 0; i < SP; ++i) v[i] *= s;
@@ -226,6 +283,7 @@ template <typename Real, int SP, int RP>
 __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a) {
     using Cfg = SmallCfg<Real, SP, RP>;
     constexpr int TP = Cfg::TP, D = Cfg::D, PF = Cfg::PF, W = Cfg::W, VB = Cfg::VB, CS = Cfg::CS;
+    constexpr int LV = Cfg::LV, VL = Cfg::VL, VBL = Cfg::VBL, G = RP * LV;
     extern __shared__ __align__(128) unsigned char smem_s[];
     unsigned char *smem = smem_s;
     const int R = a.R, N = a.N, S = a.S;
@@ -243,6 +301,9 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
     uint64_t *empty = full + D;                                     // [D]
     uint64_t *post_done = empty + D;                                // [1]
     unsigned char *stages = smem + Cfg::BARS;
+    // shared-window addresses of the barriers and stages (loop-invariant bases)
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t full_u = sbase, empty_u = sbase + 8u * D, stages_u = sbase + Cfg::BARS;
     const char *__restrict__ Pb = static_cast<const char *>(a.P);
     const char *__restrict__ tipP = static_cast<const char *>(a.tip_partials);
     const uint8_t *__restrict__ tipS = a.tip_states;
@@ -285,10 +346,10 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
         const int tip_lead = cta_pat0 & 15;
         const unsigned tipw_bytes = (tip_lead + ntile * TP + 15) / 16 * 16;
         auto tip_bytes = [&](int code) -> unsigned { return (code & kTipPartialBit) ? tipp_bytes : tipw_bytes; };
-        auto copy_tip = [&](unsigned char *dst, int code, uint64_t *bar) {
+        auto copy_tip = [&](uint32_t dst, int code, uint32_t bar) {
             const int node = code & ~kTipPartialBit;
-            if (code & kTipPartialBit) bulk_g2s(dst, tipP + ((size_t)node * Cpad + cta_pat0) * VB, tipp_bytes, bar);
-            else bulk_g2s(dst, tipS + ((size_t)node * Cpad + cta_pat0 - tip_lead), tipw_bytes, bar);
+            if (code & kTipPartialBit) bulk_g2s_u32(dst, tipP + ((size_t)node * Cpad + cta_pat0) * VB, tipp_bytes, bar);
+            else bulk_g2s_u32(dst, tipS + ((size_t)node * Cpad + cta_pat0 - tip_lead), tipw_bytes, bar);
         };
         auto u_src = [&](int node) -> const char * { return Ub + (size_t)(node - N) * u_node + u_cta; };
         for (int t = 0; t < 2 * nops; ++t) {
@@ -296,11 +357,11 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
             const int m = pre ? t - nops : t;
             PG_TSTAMP((size_t)t * 16 + 0, t);
             if (t == nops) mbar_wait(post_done, 0);       // u of every tile stored + fenced
-            if (t >= D) mbar_wait(empty + t % D, (uint32_t)(t / D + 1) & 1u);
+            if (t >= D) mbar_wait_u32(empty_u + 8u * (t % D), (uint32_t)(t / D + 1) & 1u);
             PG_TSTAMP((size_t)t * 16 + 1, t);
             if (lane == 0) {
-                unsigned char *st = stages + (t % D) * ST;
-                uint64_t *bar = full + t % D;
+                const uint32_t st = stages_u + (t % D) * ST;
+                const uint32_t bar = full_u + 8u * (t % D);
                 const Op4 *gprog = pre ? a.pre : a.post;           // global copy (bulk source)
                 const Op4 *prog = pre ? pre_prog : post_prog;       // smem copy when staged
                 const Op4 op = prog[m];
@@ -309,15 +370,15 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
                     // [op][P_k][P_a][P_b][tip a][tip b]
                     const unsigned bytes = 16 + (op.x != root ? MS : 0) + (op.y >= 0 ? MS + tip_bytes(op.y) : 0) +
                                            (op.z >= 0 ? MS + tip_bytes(op.z) : 0);
-                    mbar_arrive_expect_tx(bar, bytes);
-                    bulk_g2s(st, gprog + m, 16, bar);
-                    if (op.x != root) bulk_g2s(st + 16, Pb + (size_t)op.x * MS, MS, bar);
+                    mbar_arrive_expect_tx_u32(bar, bytes);
+                    bulk_g2s_u32(st, gprog + m, 16, bar);
+                    if (op.x != root) bulk_g2s_u32(st + 16, Pb + (size_t)op.x * MS, MS, bar);
                     if (op.y >= 0) {
-                        bulk_g2s(st + 16 + MS, Pb + (size_t)(op.y & ~kTipPartialBit) * MS, MS, bar);
+                        bulk_g2s_u32(st + 16 + MS, Pb + (size_t)(op.y & ~kTipPartialBit) * MS, MS, bar);
                         copy_tip(st + 16 + 3 * MS, op.y, bar);
                     }
                     if (op.z >= 0) {
-                        bulk_g2s(st + 16 + 2 * MS, Pb + (size_t)(op.z & ~kTipPartialBit) * MS, MS, bar);
+                        bulk_g2s_u32(st + 16 + 2 * MS, Pb + (size_t)(op.z & ~kTipPartialBit) * MS, MS, bar);
                         copy_tip(st + 16 + 3 * MS + VS, op.z, bar);
                     }
                 } else {
@@ -325,13 +386,13 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
                     const int na = op.y & ~kTipPartialBit, nb = op.z & ~kTipPartialBit;
                     const unsigned bytes = 16 + 2 * MS + (na >= N ? u_bytes : tip_bytes(op.y)) +
                                            (nb >= N ? u_bytes : tip_bytes(op.z));
-                    mbar_arrive_expect_tx(bar, bytes);
-                    bulk_g2s(st, gprog + m, 16, bar);
-                    bulk_g2s(st + 16, Pb + (size_t)na * MS, MS, bar);
-                    bulk_g2s(st + 16 + MS, Pb + (size_t)nb * MS, MS, bar);
-                    if (na >= N) bulk_g2s(st + 16 + 3 * MS, u_src(na), u_bytes, bar);
+                    mbar_arrive_expect_tx_u32(bar, bytes);
+                    bulk_g2s_u32(st, gprog + m, 16, bar);
+                    bulk_g2s_u32(st + 16, Pb + (size_t)na * MS, MS, bar);
+                    bulk_g2s_u32(st + 16 + MS, Pb + (size_t)nb * MS, MS, bar);
+                    if (na >= N) bulk_g2s_u32(st + 16 + 3 * MS, u_src(na), u_bytes, bar);
                     else copy_tip(st + 16 + 3 * MS, op.y, bar);
-                    if (nb >= N) bulk_g2s(st + 16 + 3 * MS + VS, u_src(nb), u_bytes, bar);
+                    if (nb >= N) bulk_g2s_u32(st + 16 + 3 * MS + VS, u_src(nb), u_bytes, bar);
                     else copy_tip(st + 16 + 3 * MS + VS, op.z, bar);
                     if (m + PF < nops) {                         // pull later u chunks into L2
                         const Op4 o2 = prog[m + PF];
@@ -348,45 +409,63 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
     }
 
     // =============================== consumers ==================================
+    // lane = (pattern pl, category cat, state group h), h fastest; the G = RP LV
+    // lanes of one pattern are contiguous.
     const int tile = cta_tile0 + warp;
     const bool active = warp < ntile;
-    const int cat = lane & (RP - 1);
+    const int h = lane & (LV - 1);
+    const int cat = (lane / LV) & (RP - 1);
     const int r = min(cat, R - 1);                  // shadow lanes reuse category R-1
     const bool live = cat < R;
-    const int pl = lane / RP;
+    const int pl = lane / G;
     const int pat0 = tile * TP;
     const int pat = pat0 + pl;
     unsigned char *wsm = stages + D * ST + (size_t)warp * Cfg::warp_bytes(a.depth);
     unsigned char *stackb = wsm;
-    double2 *nd = reinterpret_cast<double2 *>(wsm + a.depth * 32 * VB);          // [W][2][32]
-    double *wbuf = reinterpret_cast<double *>(wsm + a.depth * 32 * VB + Cfg::ND); // [TP]
-    int *nodes_w = reinterpret_cast<int *>(wbuf + TP);                            // [W][2] branch ids
+    const int pi_slot = a.depth;
+    double2 *nd = reinterpret_cast<double2 *>(wsm + (a.depth + 1) * 32 * VBL);     // [W][2][32]
+    unsigned char *xb = wsm + (a.depth + 1) * 32 * VBL + Cfg::ND;                  // exchange [32/LV][XGS]
+    double *wbuf = reinterpret_cast<double *>(xb + Cfg::XB);                        // [TP]
+    int *nodes_w = reinterpret_cast<int *>(wbuf + TP);                              // [W][2] branch ids
     const double wr = live ? a.cat_w[r] : 0.0;
     const double gwr = wr * a.cat_g[r];
-    Real pi[SP];
+    Real pi[VL];
 #pragma unroll
-    for (int s = 0; s < SP; ++s) pi[s] = static_cast<const Real *>(a.pi)[s];
+    for (int s = 0; s < VL; ++s) pi[s] = static_cast<const Real *>(a.pi)[h * VL + s];
     if (active && lane < TP) wbuf[lane] = a.pat_w[pat0 + lane];
     __syncwarp();
 
     const unsigned mat_lane = r * CS;
-    const unsigned u_vec = ((warp * TP + pl) * R + r) * VB;        // my vector inside a CTA u chunk
+    const unsigned u_vec = ((warp * TP + pl) * R + r) * VB + h * VBL;   // my part inside a CTA u chunk
     const int tip_idx = (cta_pat0 & 15) + warp * TP + pl;          // my code inside a tip window
-    const unsigned tipp_vec = (warp * TP + pl) * VB;               // my tip partial vector
-    const size_t u_lane = (size_t)pat * R * VB + r * VB;
-    auto stack_at = [&](int slot) -> unsigned char * { return stackb + (slot * 32 + lane) * VB; };
+    const unsigned tipp_vec = (warp * TP + pl) * VB;               // my tip partial vector (whole)
+    const size_t u_lane = (size_t)pat * R * VB + r * VB + h * VBL;
+    unsigned char *xg = xb + (lane / LV) * Cfg::XGS;               // my group's exchange row
+    auto stack_at = [&](int slot) -> unsigned char * { return stackb + (slot * 32 + lane) * VBL; };
     auto release = [&](int t) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(empty + t % D);
+        if (lane == 0) mbar_arrive_u32(empty_u + 8u * (t % D));
     };
-    auto child_tip = [&](Real (&u)[SP], const unsigned char *M_, const unsigned char *vs, int code) {
+    // the whole SP-vector of my (pattern, category) from the lanes' parts, rotated by h VL
+    auto gather = [&](Real (&full)[SP], const Real (&part)[VL]) {
+        if constexpr (LV == 1) {
+#pragma unroll
+            for (int s = 0; s < SP; ++s) full[s] = part[s];
+        } else {
+            __syncwarp();
+            sts_vec<Real, VL>(xg + h * VBL, part);
+            __syncwarp();
+            lds_rot<Real, SP, VL>(full, xg, h);
+        }
+    };
+    auto child_tip = [&](Real (&u)[VL], const unsigned char *M_, const unsigned char *vs, int code) {
         const Real *M = reinterpret_cast<const Real *>(M_ + mat_lane);
         if (code & kTipPartialBit) {
             Real tp[SP];
-            lds_vec<Real, SP>(tp, vs + tipp_vec);
-            mv<Real, SP>(u, M, tp);
+            lds_rot<Real, SP, VL>(tp, vs + tipp_vec, h);
+            mv<Real, SP, VL>(u, M, tp, h);
         } else {
-            mcol<Real, SP>(u, M, vs[tip_idx], S);
+            mcol<Real, SP, VL>(u, M, vs[tip_idx], S, h);
         }
     };
 
@@ -397,66 +476,68 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
     int E = 0;                    // post-order exponents removed from this pattern
     double logl_local = 0.0;
     int prev_slot = -1;
-    Real prev_u[SP];
+    Real prev_u[VL];
     Op4 op_next = {0, 0, 0, 0};
     if (active && nops > 0) {
         mbar_wait(full, 0u);
         op_next = *reinterpret_cast<const Op4 *>(stages);
     }
-    auto stack_or_fwd = [&](Real (&u)[SP], int code) {
+    auto stack_or_fwd = [&](Real (&u)[VL], int code) {
         const int sl = -code - 1;
         if (sl == prev_slot) {
 #pragma unroll
-            for (int s = 0; s < SP; ++s) u[s] = prev_u[s];
+            for (int s = 0; s < VL; ++s) u[s] = prev_u[s];
         } else {
-            lds_vec<Real, SP>(u, stack_at(sl));
+            lds_vec<Real, VL>(u, stack_at(sl));
         }
     };
     for (int t = 0; t < nops; ++t) {
         if (!active) {
-            mbar_wait(full + t % D, (uint32_t)(t / D) & 1u);
+            mbar_wait_u32(full_u + 8u * (t % D), (uint32_t)(t / D) & 1u);
             release(t);
             continue;
         }
         const unsigned char *st = stages + (t % D) * ST;
         const Op4 op = op_next;
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 3, op.x);
-        Real ua[SP], ub[SP];
+        Real ua[VL], ub[VL];
         if (op.y < 0) stack_or_fwd(ua, op.y);
         else child_tip(ua, st + 16 + MS, st + 16 + 3 * MS, op.y);
         if (op.z < 0) stack_or_fwd(ub, op.z);
         else child_tip(ub, st + 16 + 2 * MS, st + 16 + 3 * MS + VS, op.z);
-        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 4, ua[0] + ub[SP - 1]);
+        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 4, ua[0] + ub[VL - 1]);
         if (t + 1 < nops) {
             const int t1 = t + 1;
-            mbar_wait(full + t1 % D, (uint32_t)(t1 / D) & 1u);
+            mbar_wait_u32(full_u + 8u * (t1 % D), (uint32_t)(t1 / D) & 1u);
             op_next = *reinterpret_cast<const Op4 *>(stages + (t1 % D) * ST);
         }
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 5, op_next.x);
-        Real p[SP];
+        Real p[VL];
 #pragma unroll
-        for (int s = 0; s < SP; ++s) p[s] = ua[s] * ub[s];
+        for (int s = 0; s < VL; ++s) p[s] = ua[s] * ub[s];
         if (op.x == root) {
             release(t);
             double L = 0.0;
 #pragma unroll
-            for (int s = 0; s < SP; ++s) L = fma((double)pi[s], (double)p[s], L);
-            L = cat_sum<RP>(wr * L);
-            if (cat == 0 && pat < a.C) {
+            for (int s = 0; s < VL; ++s) L = fma((double)pi[s], (double)p[s], L);
+            L = cat_sum<G>(wr * L);
+            if (cat == 0 && h == 0 && pat < a.C) {
                 if (!(L > 0.0) || !isfinite(L)) atomicMin(a.status, pat);
                 logl_local = wbuf[pl] * (log(L) + (double)E * 0.69314718055994530942);
             }
         } else {
-            E += maybe_rescale<Real, SP, RP>(p);
+            E += maybe_rescale<Real, VL, G>(p);
             if (warp == 0) PG_TSTAMP((size_t)t * 16 + 6, p[0]);
-            Real u[SP];
-            mv<Real, SP>(u, reinterpret_cast<const Real *>(st + 16 + mat_lane), p);
-            if (warp == 0) PG_TSTAMP((size_t)t * 16 + 7, u[0] + u[SP - 1]);
+            Real pf[SP];
+            gather(pf, p);
+            Real u[VL];
+            mv<Real, SP, VL>(u, reinterpret_cast<const Real *>(st + 16 + mat_lane), pf, h);
+            if (warp == 0) PG_TSTAMP((size_t)t * 16 + 7, u[0] + u[VL - 1]);
             release(t);
-            stg_vec<Real, SP>(Ub + (size_t)(op.x - N) * u_node + u_lane, u);   // shadow lanes: same value
-            sts_vec<Real, SP>(stack_at(op.w), u);
+            stg_vec<Real, VL>(Ub + (size_t)(op.x - N) * u_node + u_lane, u);   // shadow lanes: same value
+            sts_vec<Real, VL>(stack_at(op.w), u);
 #pragma unroll
-            for (int s = 0; s < SP; ++s) prev_u[s] = u[s];
+            for (int s = 0; s < VL; ++s) prev_u[s] = u[s];
             prev_slot = op.w;
         }
     }
@@ -471,18 +552,20 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
     if (lane == 0) mbar_arrive(post_done);
 
     // -------------------- pre program (Eq. 4) + gradient (Eq. 6-8) ---------------
-    Real Qr[SP][SP <= 4 ? SP : 1];
+    // Q rows [h VL, +VL): registers when SP = 4, else shared memory
+    Real Qr[SP <= 4 ? VL : 1][SP <= 4 ? SP : 1];
     if constexpr (SP <= 4) {
 #pragma unroll
-        for (int s = 0; s < SP; ++s)
+        for (int s = 0; s < VL; ++s)
 #pragma unroll
-            for (int t = 0; t < SP; ++t) Qr[s][t] = static_cast<const Real *>(a.Q)[s * SP + t];
+            for (int t = 0; t < SP; ++t) Qr[s][t] = static_cast<const Real *>(a.Q)[(h * VL + s) * SP + t];
     }
     const Real *Qs = reinterpret_cast<const Real *>(smem + Cfg::QOFF);
     // next op decoded early; the q's pushed by the previous step are
     // forwarded through registers when this step pops one of them
+    sts_vec<Real, VL>(stack_at(pi_slot), pi);
     int fslot[2] = {-1, -1};
-    Real fq[2][SP];
+    Real fq[2][VL];
     Op4 opn = {0, 0, 0, 0};
     if (active && nops > 0) {
         mbar_wait(full + nops % D, (uint32_t)(nops / D) & 1u);
@@ -491,50 +574,55 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
     for (int n = 0; n < nops; ++n) {
         const int t = nops + n;
         if (!active) {
-            mbar_wait(full + t % D, (uint32_t)(t / D) & 1u);
+            mbar_wait_u32(full_u + 8u * (t % D), (uint32_t)(t / D) & 1u);
             release(t);
             continue;
         }
         const unsigned char *st = stages + (t % D) * ST;
         const Op4 op = opn;
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 3, op.x);
-        Real q[SP];
+        Real q[VL];
         if (op.x < 0) {
 #pragma unroll
-            for (int s = 0; s < SP; ++s) q[s] = pi[s];
+            for (int s = 0; s < VL; ++s) q[s] = pi[s];
         } else if (op.x == fslot[0]) {
 #pragma unroll
-            for (int s = 0; s < SP; ++s) q[s] = fq[0][s];
+            for (int s = 0; s < VL; ++s) q[s] = fq[0][s];
         } else if (op.x == fslot[1]) {
 #pragma unroll
-            for (int s = 0; s < SP; ++s) q[s] = fq[1][s];
+            for (int s = 0; s < VL; ++s) q[s] = fq[1][s];
         } else {
-            lds_vec<Real, SP>(q, stack_at(op.x));
+            lds_vec<Real, VL>(q, stack_at(op.x));
         }
         const int cs[2] = {op.y, op.z};
         const int slots[2] = {(op.w & 0xffff) - 1, (op.w >> 16) - 1};
-        Real uc[2][SP];
+        Real uc[2][VL];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             const unsigned char *vs = st + 16 + 3 * MS + c * VS;
-            if ((cs[c] & ~kTipPartialBit) >= N) lds_vec<Real, SP>(uc[c], vs + u_vec);
+            if ((cs[c] & ~kTipPartialBit) >= N) lds_vec<Real, VL>(uc[c], vs + u_vec);
             else child_tip(uc[c], st + 16 + c * MS, vs, cs[c]);
         }
-        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 4, q[0] + uc[0][0] + uc[1][SP - 1]);
+        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 4, q[0] + uc[0][0] + uc[1][VL - 1]);
         if (n + 1 < nops) {
             const int t1 = t + 1;
-            mbar_wait(full + t1 % D, (uint32_t)(t1 / D) & 1u);
+            mbar_wait_u32(full_u + 8u * (t1 % D), (uint32_t)(t1 / D) & 1u);
             opn = *reinterpret_cast<const Op4 *>(stages + (t1 % D) * ST);
         }
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 5, opn.x);
-        Real qc[2][SP];
+        // x_c = q o u_sibling (my states); q_c = P_c' x_c for internal children
+        Real x[2][VL];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int s = 0; s < VL; ++s) x[c][s] = q[s] * uc[1 - c][s];
+        Real qc[2][VL];
 #pragma unroll
         for (int c = 0; c < 2; ++c)
             if (slots[c] >= 0) {
-                Real x[SP];
-#pragma unroll
-                for (int s = 0; s < SP; ++s) x[s] = q[s] * uc[1 - c][s];
-                mvt<Real, SP>(qc[c], reinterpret_cast<const Real *>(st + 16 + c * MS + mat_lane), x);
+                Real xf[SP];
+                gather(xf, x[c]);
+                mvt<Real, SP, VL>(qc[c], reinterpret_cast<const Real *>(st + 16 + c * MS + mat_lane), xf, h);
             }
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 6, qc[0][0] + qc[1][0]);
         release(t);                                 // stage no longer needed
@@ -542,29 +630,32 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             if (lane == 0) nodes_w[(n % W) * 2 + c] = cs[c] & ~kTipPartialBit;
+            // my states' share of num = x' Q u_c and den = x' u_c (summed over
+            // the pattern's lanes in the window flush)
+            Real ucf[SP];
+            gather(ucf, uc[c]);
             Real num = 0, den = 0;
 #pragma unroll
-            for (int s = 0; s < SP; ++s) {
-                const Real xs = q[s] * uc[1 - c][s];
+            for (int s = 0; s < VL; ++s) {
                 Real Qu;
                 if constexpr (SP <= 4) {
-                    Qu = Qr[s][0] * uc[c][0];
+                    Qu = Qr[s][0] * ucf[0];
 #pragma unroll
-                    for (int t2 = 1; t2 < SP; ++t2) Qu = fma(Qr[s][t2], uc[c][t2], Qu);
+                    for (int t2 = 1; t2 < SP; ++t2) Qu = fma(Qr[s][t2], ucf[t2], Qu);
                 } else {
                     Real row[SP];
-                    lds_vec<Real, SP>(row, Qs + s * SP);
-                    Qu = row[0] * uc[c][0];
+                    lds_rot<Real, SP, VL>(row, reinterpret_cast<const unsigned char *>(Qs + (h * VL + s) * SP), h);
+                    Qu = row[0] * ucf[0];
 #pragma unroll
-                    for (int t2 = 1; t2 < SP; ++t2) Qu = fma(row[t2], uc[c][t2], Qu);
+                    for (int t2 = 1; t2 < SP; ++t2) Qu = fma(row[t2], ucf[t2], Qu);
                 }
-                num = fma(xs, Qu, num);
-                den = fma(xs, uc[c][s], den);
+                num = fma(x[c][s], Qu, num);
+                den = fma(x[c][s], uc[c][s], den);
             }
             ndw[c * 32] = make_double2(gwr * (double)num, wr * (double)den);
             if (slots[c] >= 0) {
-                maybe_rescale<Real, SP, RP>(qc[c]);
-                sts_vec<Real, SP>(stack_at(slots[c]), qc[c]);
+                maybe_rescale<Real, VL, G>(qc[c]);
+                sts_vec<Real, VL>(stack_at(slots[c]), qc[c]);
             }
         }
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 7, qc[0][0] + qc[1][0]);
@@ -573,15 +664,15 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
         for (int c = 0; c < 2; ++c) {
             fslot[c] = slots[c];
 #pragma unroll
-            for (int s = 0; s < SP; ++s) fq[c][s] = qc[c][s];
+            for (int s = 0; s < VL; ++s) fq[c][s] = qc[c][s];
         }
         // a slot written by this step but not re-pushed keeps its smem value; slots
         // that were forwarded earlier but overwritten now are no longer valid
         if (fslot[0] == fslot[1]) fslot[1] = -1;
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 8, fq[0][0] + fq[1][0]);
         if (n % W == W - 1 || n == nops - 1) {
-            // W steps of (num_r, den_r) -> Eq. 8 ratio per pattern, weighted (Eq. 6),
-            // summed over the tile's patterns; all 32 lanes busy.
+            // W steps of (num, den) lane shares -> Eq. 8 ratio per pattern, weighted
+            // (Eq. 6), summed over the tile's patterns; all 32 lanes busy.
             __syncwarp();
             constexpr int PAIRS = 2 * W, LPP = 32 / PAIRS, PPL = TP / LPP > 0 ? TP / LPP : 1;
             const int pair = lane / LPP, sub = lane % LPP;
@@ -592,10 +683,10 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
 #pragma unroll
                 for (int k = 0; k < PPL; ++k) {
                     const int p = sub * PPL + k;
-                    const double2 *src = nd + ((wstep * 2 + c) * 32 + p * RP);
+                    const double2 *src = nd + ((wstep * 2 + c) * 32 + p * G);
                     double num = 0.0, den = 0.0;
 #pragma unroll
-                    for (int q2 = 0; q2 < RP; ++q2) { const double2 v = src[q2]; num += v.x; den += v.y; }
+                    for (int q2 = 0; q2 < G; ++q2) { const double2 v = src[q2]; num += v.x; den += v.y; }
                     const double w = wbuf[p];
 #ifdef PG_SLOWDIV
                     acc += (w != 0.0) ? w * (num / den) : 0.0;
