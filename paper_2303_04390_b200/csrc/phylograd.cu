@@ -563,7 +563,11 @@ static int configure(pg_instance *inst) {
         const int prog_bytes = 2 * (inst->cfg.tips - 1) * (int)sizeof(Op4);
         const int off = (inst->smem + 15) / 16 * 16;
         inst->prog_smem_off = 0;
+#ifdef PG_NO_PROG_SMEM
+        if (false) {
+#else
         if (off + prog_bytes <= 227 * 1024) {
+#endif
             inst->prog_smem_off = off;
             inst->smem = off + prog_bytes;
         }

@@ -65,7 +65,11 @@ struct SmallCfg {
     static constexpr int LV = small_lanes_per_vector(SP);     // lanes per vector
     static constexpr int VL = SP / LV;                         // states per lane
     static constexpr int TP = 32 / (RP * LV);                  // patterns per warp tile
+#ifndef PG_STAGES
     static constexpr int D = (SP <= 8) ? 4 : 2;                // stage ring depth
+#else
+    static constexpr int D = PG_STAGES;
+#endif
     static constexpr int PF = 16;                              // L2 prefetch distance (steps)
     static constexpr int W = PG_SMALL_W;                       // gradient window (steps)
     static constexpr int VB = SP * (int)sizeof(Real);          // vector bytes
@@ -561,11 +565,8 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
             for (int t = 0; t < SP; ++t) Qr[s][t] = static_cast<const Real *>(a.Q)[(h * VL + s) * SP + t];
     }
     const Real *Qs = reinterpret_cast<const Real *>(smem + Cfg::QOFF);
-    // next op decoded early; the q's pushed by the previous step are
-    // forwarded through registers when this step pops one of them
+    // next op decoded early
     sts_vec<Real, VL>(stack_at(pi_slot), pi);
-    int fslot[2] = {-1, -1};
-    Real fq[2][VL];
     Op4 opn = {0, 0, 0, 0};
     if (active && nops > 0) {
         mbar_wait(full + nops % D, (uint32_t)(nops / D) & 1u);
@@ -581,19 +582,11 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
         const unsigned char *st = stages + (t % D) * ST;
         const Op4 op = opn;
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 3, op.x);
+        // q_k from its stack slot (pi for the root): forwarding the previous
+        // step's pushes through registers measured slower here (more
+        // instructions than the shared-memory round trip it saves)
         Real q[VL];
-        if (op.x < 0) {
-#pragma unroll
-            for (int s = 0; s < VL; ++s) q[s] = pi[s];
-        } else if (op.x == fslot[0]) {
-#pragma unroll
-            for (int s = 0; s < VL; ++s) q[s] = fq[0][s];
-        } else if (op.x == fslot[1]) {
-#pragma unroll
-            for (int s = 0; s < VL; ++s) q[s] = fq[1][s];
-        } else {
-            lds_vec<Real, VL>(q, stack_at(op.x));
-        }
+        lds_vec<Real, VL>(q, stack_at(op.x < 0 ? pi_slot : op.x));
         const int cs[2] = {op.y, op.z};
         const int slots[2] = {(op.w & 0xffff) - 1, (op.w >> 16) - 1};
         Real uc[2][VL];
@@ -659,17 +652,7 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
             }
         }
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 7, qc[0][0] + qc[1][0]);
-        // registers now hold the latest values of these slots
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            fslot[c] = slots[c];
-#pragma unroll
-            for (int s = 0; s < VL; ++s) fq[c][s] = qc[c][s];
-        }
-        // a slot written by this step but not re-pushed keeps its smem value; slots
-        // that were forwarded earlier but overwritten now are no longer valid
-        if (fslot[0] == fslot[1]) fslot[1] = -1;
-        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 8, fq[0][0] + fq[1][0]);
+        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 8, qc[0][0] + qc[1][0]);
         if (n % W == W - 1 || n == nops - 1) {
             // W steps of (num, den) lane shares -> Eq. 8 ratio per pattern, weighted
             // (Eq. 6), summed over the tile's patterns; all 32 lanes busy.
