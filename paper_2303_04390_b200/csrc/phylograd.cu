@@ -551,7 +551,7 @@ static int configure(pg_instance *inst) {
     if (L.variant == 0) {
         // CTA = K tile warps + 1 producer warp; K = tiles / SMs (one wave), at
         // most 9 (launch bounds) and within the shared-memory budget.
-        int K = std::max(1, std::min(9, (L.n_tiles + inst->sm_count - 1) / inst->sm_count));
+        int K = std::max(1, std::min(pg::small_max_consumers(L.SP), (L.n_tiles + inst->sm_count - 1) / inst->sm_count));
         while (K > 1 && small_smem(L, R, K, depth) > 227 * 1024) --K;
         inst->tiles_per_cta = K;
         inst->block = 32 * (K + 1);

@@ -52,7 +52,12 @@ namespace pg {
 // resident warps, a quarter of the per-lane matvec work for S = 16).
 // (Splitting S = 4 over 2 lanes as well was measured 2x slower on the dengue
 // workload: twice the warps, the same per-step control work.)
-__host__ __device__ constexpr int small_lanes_per_vector(int SP) { return SP / 4; }
+#ifndef PG_SP4_LV
+#define PG_SP4_LV 1
+#endif
+__host__ __device__ constexpr int small_lanes_per_vector(int SP) { return SP == 4 ? PG_SP4_LV : SP / 4; }
+// consumer warps per CTA at most (launch bounds: + 1 producer warp)
+__host__ __device__ constexpr int small_max_consumers(int SP) { return small_lanes_per_vector(SP) * 4 / SP >= 2 ? 17 : 9; }
 
 // ---- shape of one CTA's work ----------------------------------------------
 // A CTA = K consumer warps (one pattern tile each) + 1 producer warp.  Global
@@ -284,7 +289,7 @@ __device__ __forceinline__ int maybe_rescale(Real (&v)[SP]) {
 
 
 template <typename Real, int SP, int RP>
-__global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a) {
+__global__ void __launch_bounds__(32 * (small_max_consumers(SP) + 1), 1) traverse_small_kernel(const TravArgs a) {
     using Cfg = SmallCfg<Real, SP, RP>;
     constexpr int TP = Cfg::TP, D = Cfg::D, PF = Cfg::PF, W = Cfg::W, VB = Cfg::VB, CS = Cfg::CS;
     constexpr int LV = Cfg::LV, VL = Cfg::VL, VBL = Cfg::VBL, G = RP * LV;
@@ -562,7 +567,8 @@ __global__ void __launch_bounds__(320, 1) traverse_small_kernel(const TravArgs a
 #pragma unroll
         for (int s = 0; s < VL; ++s)
 #pragma unroll
-            for (int t = 0; t < SP; ++t) Qr[s][t] = static_cast<const Real *>(a.Q)[(h * VL + s) * SP + t];
+            for (int t = 0; t < SP; ++t)       // columns rotated like gathered vectors
+                Qr[s][t] = static_cast<const Real *>(a.Q)[(h * VL + s) * SP + ((t + h * VL) & (SP - 1))];
     }
     const Real *Qs = reinterpret_cast<const Real *>(smem + Cfg::QOFF);
     // next op decoded early
