@@ -576,7 +576,7 @@ static int configure(pg_instance *inst) {
         inst->prefetch = 0;
         inst->smem = (int)pg::codon::pre_smem();
         CK(cudaFuncSetAttribute((void *)pg::codon::codon_post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)pg::codon::post_smem()), "smem attr");
+                                (int)(pg::codon::post_smem() + 16 * (size_t)inst->cfg.tips)), "smem attr");
         CK(cudaFuncSetAttribute((void *)pg::codon::codon_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)pg::codon::pre_smem()), "smem attr");
         CK(cudaFuncSetAttribute((void *)pg::codon::codon_pmat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -722,9 +722,11 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         CK(cudaMemsetAsync(inst->ws + L.off_fmax, 0, (size_t)(2 * N - 3) * L.Cpad * 4, inst->stream), "fmax reset");
         for (size_t i = 0; i + 1 < pl.post_off.size(); ++i) {
             int off = pl.post_off[i], cnt = pl.post_off[i + 1] - off;
-            void *args[] = {&c, &off};
-            CK(cudaLaunchKernel((void *)pg::codon::codon_post_kernel, dim3(L.n_tiles, cnt, R), dim3(pg::codon::NT), args,
-                                pg::codon::post_smem(), inst->stream), "codon post launch");
+            const int items = L.n_tiles * cnt * R;      // persistent: 3 CTAs per SM walk the level's items
+            void *args[] = {&c, &off, &cnt};
+            CK(cudaLaunchKernel((void *)pg::codon::codon_post_kernel, dim3(std::min(items, 3 * inst->sm_count)),
+                                dim3(pg::codon::NT), args, pg::codon::post_smem() + 16 * (size_t)cnt, inst->stream),
+               "codon post launch");
         }
         for (size_t i = 0; i + 1 < pl.pre_off.size(); ++i) {
             int off = pl.pre_off[i], cnt = pl.pre_off[i + 1] - off;

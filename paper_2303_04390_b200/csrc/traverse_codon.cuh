@@ -162,65 +162,202 @@ __device__ __forceinline__ void child_scale(double *sc, const CodonArgs &a, int 
 }
 
 // ---------------------------------------------------------------------------
-// post-order level: one CTA per (tile, node of the level, category r).
-// u_k[r] = (u_a o u_b) P_k' (Eq. 2), children rescaled on load; root:
-// P(gamma_r) pi' p (Eq. 3) per pattern -> Lpart.
+// post-order level, persistent: each CTA walks a contiguous range of the
+// level's work items (node, category r, tile), tile fastest, so the B
+// fragments of P_k (registers) are reloaded only when (node, r) changes.
+// Child tiles stream into a PST-stage shared-memory ring with cp.async
+// (internal u tiles: contiguous 16 KB; tips: rows of P' picked by the
+// pattern's state), issued PST-1 items ahead of the tensor-core GEMM.
+// u_k[r] = (u_a o u_b) P_k' (Eq. 2), children rescaled in the epilogue;
+// root: P(gamma_r) pi' p (Eq. 3) per pattern -> Lpart.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT, 5) codon_post_kernel(const CodonArgs a, int level_off) {
-    extern __shared__ __align__(16) unsigned char smem_c[];
-    double *As = reinterpret_cast<double *>(smem_c);      // A tile (p)
-    double *Ts = As + TILE;                                 // child b tile
-    double *sc = Ts + TILE;                                 // [2][T] child scales
-    int *stb = reinterpret_cast<int *>(sc + 2 * T);         // [2][T] tip states
-    const int tile = blockIdx.x, r = blockIdx.z;
-    const int k = a.levels[level_off + blockIdx.y];
-    const int ca = a.child_a[k], cb = a.child_b[k];
-    const int root = 2 * a.N - 2;
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int pat0 = tile * T;
-    double b[16];
-    if (k != root) load_bfrag(b, a.PBpost + ((size_t)k * a.R + r) * MAT, w, lane);
-    child_scale(sc, a, ca, a.fmax, pat0);
-    child_scale(sc + T, a, cb, a.fmax, pat0);
-    if (r == 0 && threadIdx.x < T) {     // cumulative exponent inside u_k (and at the root)
-        const int m = threadIdx.x;
-        int Ek = 0;
-        if (ca >= a.N) Ek += a.E[(size_t)(ca - a.N) * a.Cpad + pat0 + m] + lazy_exp(a.fmax[(size_t)(ca - a.N) * a.Cpad + pat0 + m]);
-        if (cb >= a.N) Ek += a.E[(size_t)(cb - a.N) * a.Cpad + pat0 + m] + lazy_exp(a.fmax[(size_t)(cb - a.N) * a.Cpad + pat0 + m]);
-        a.E[(size_t)(k - a.N) * a.Cpad + pat0 + m] = Ek;
+constexpr int PST = 2;                                           // post data stages
+constexpr int PSTAGE = 2 * TILE * 8 + 2 * T * 4;                 // A, B tiles + children's fmax
+constexpr int PSS = 3;                                           // state-code slots (2 children x 32 B)
+constexpr size_t post_smem() { return (size_t)PST * PSTAGE + PSS * 2 * T; }
+
+// The level's nodes and their children, staged in shared memory at kernel
+// start: {k, child a, child b, kinds}, kind = 0 internal, 1 tip states,
+// 2 tip partials (child a in bits 0-1, child b in bits 2-3).
+struct Item { int k, r, tile, ca, cb, kinds; };
+__device__ __forceinline__ int child_kind(const CodonArgs &a, int c) {
+    return c >= a.N ? 0 : (a.tip_is_partial[c] ? 2 : 1);
+}
+__device__ __forceinline__ void stage_level(int4 *tab, const CodonArgs &a, int level_off, int cnt) {
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        const int k = a.levels[level_off + i], ca = a.child_a[k], cb = a.child_b[k];
+        tab[i] = make_int4(k, ca, cb, child_kind(a, ca) | (child_kind(a, cb) << 2));
     }
-    load_child(As, a, ca, r, tile, stb);
-    load_child(Ts, a, cb, r, tile, stb + T);
-    __syncthreads();
-    if (k == root) {
-        // thread -> (pattern m = tid/8, 8 states); deterministic shuffle sum
-        const int m = threadIdx.x >> 3, j = threadIdx.x & 7;
-        double sum = 0.0;
-        for (int kk = j; kk < SP; kk += 8) {
-            const int p = apos(m, kk);
-            sum = fma(a.pi[kk], As[p] * Ts[p], sum);
-        }
-        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 4);
-        if (j == 0) a.Lpart[(size_t)r * a.Cpad + pat0 + m] = a.cat_w[r] * sum * (sc[m] * sc[T + m]);
+}
+__device__ __forceinline__ Item level_item(const CodonArgs &a, const int4 *tab, int item) {
+    Item it;
+    it.tile = item % a.ntiles;
+    const int nr = item / a.ntiles;
+    it.r = nr % a.R;
+    const int4 e = tab[nr / a.R];
+    it.k = e.x;
+    it.ca = e.y;
+    it.cb = e.z;
+    it.kinds = e.w;
+    return it;
+}
+// Start the copy of child tile `child` (category r) into dst; fmax of an
+// internal child's patterns into fm.  A tip's state codes for the tile (32
+// bytes) were staged in shared memory one item earlier (`st`), so the
+// gather addresses need no global round trip.  Tip partials (rare) are
+// computed here.
+__device__ __forceinline__ void issue_child(double *dst, int *fm, const unsigned char *st, const CodonArgs &a,
+                                            int child, int kind, int r, int tile) {
+    const int tid = threadIdx.x;
+    if (kind == 0) {
+        const double *src = a.u + (((size_t)(child - a.N) * a.R + r) * a.ntiles + tile) * TILE;
+#pragma unroll
+        for (int j = 0; j < TILE / 2 / NT; ++j) cp_async16(dst + 2 * (tid + j * NT), src + 2 * (tid + j * NT));
+        if (tid < T / 4) cp_async16(fm + 4 * tid, a.fmax + (size_t)(child - a.N) * a.Cpad + tile * T + 4 * tid);
         return;
     }
-    double acc[4][2];
-    gemm_tile2(acc, As, Ts, b, lane);           // p = u_a o u_b formed on the fly
-    double *out = a.u + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE;
-    int *fm = a.fmax + (size_t)(k - a.N) * a.Cpad + pat0;
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-        const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-        const double f2 = sc[m] * sc[T + m];             // children's scales, per pattern row
-        const double c0 = acc[mt][0] * f2, c1 = acc[mt][1] * f2;
-        *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(c0, c1);
-        int f = max(__double2hiint(c0) >> 20, __double2hiint(c1) >> 20);
-        f = max(f, __shfl_xor_sync(0xffffffffu, f, 1));
-        f = max(f, __shfl_xor_sync(0xffffffffu, f, 2));
-        if ((lane & 3) == 0) atomicMax(fm + m, f);
+    const size_t br = (size_t)child * a.R + r;
+    const double *PT = a.PT + br * MAT;
+    if (kind == 2) {                        // u[s] = sum_t P[s][t] p[t] = sum_t PT[t][s] p[t]
+        for (int idx = tid; idx < TILE; idx += NT) {
+            int m, k;
+            apos_inv(idx, m, k);
+            const double *p = a.tip_partials + ((size_t)child * a.Cpad + tile * T + m) * SP;
+            double acc = 0.0;
+            for (int t = 0; t < SP; ++t) acc = fma(__ldg(PT + t * SP + k), __ldg(p + t), acc);
+            dst[idx] = acc;
+        }
+        return;
     }
+    // thread tid needs patterns m = 8j + c, c = (tid & 15) / 2 (fragment order)
+    const int c = (tid & 15) >> 1;
+    const double *ONE = a.PONE + br * SP;
+#pragma unroll
+    for (int j = 0; j < TILE / 2 / NT; ++j) {
+        int m, k;
+        apos_inv(2 * (tid + j * NT), m, k);
+        const int s = st[8 * j + c];
+        cp_async16(dst + 2 * (tid + j * NT), s < a.S ? PT + s * SP + k : ONE + k);
+    }
+}
+// stage a tip child's 32 state codes of the tile (2 x 16 B)
+__device__ __forceinline__ void issue_states(unsigned char *st, const CodonArgs &a, int child, int kind, int tile) {
+    if (kind == 1 && threadIdx.x < 2)
+        cp_async16(st + 16 * threadIdx.x, a.tip_states + (size_t)child * a.Cpad + tile * T + 16 * threadIdx.x);
+}
+__device__ __forceinline__ double child_sc(const CodonArgs &a, int child, const int *fm, int m) {
+    return child >= a.N ? pow2neg(lazy_exp(fm[m])) : 1.0;
+}
+
+__global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, int level_off, int cnt) {
+    extern __shared__ __align__(16) unsigned char smem_c[];
+    const int nitems = cnt * a.R * a.ntiles;
+    int4 *tab = reinterpret_cast<int4 *>(smem_c + post_smem());
+    stage_level(tab, a, level_off, cnt);
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int root = 2 * a.N - 2;
+    const int per = (nitems + gridDim.x - 1) / gridDim.x;
+    const int beg = blockIdx.x * per, end = min(nitems, beg + per);
+    auto stage_A = [&](int s) { return reinterpret_cast<double *>(smem_c + (size_t)s * PSTAGE); };
+    auto stage_B = [&](int s) { return reinterpret_cast<double *>(smem_c + (size_t)s * PSTAGE) + TILE; };
+    auto stage_F = [&](int s) { return reinterpret_cast<int *>(smem_c + (size_t)s * PSTAGE + 2 * TILE * 8); };
+    auto stage_S = [&](int item) { return smem_c + (size_t)PST * PSTAGE + ((item - beg) % PSS) * 2 * T; };
+    // data of `item` into stage s (its states are staged); states of `item2`
+    auto issue = [&](int item, int s, int item2) {
+        if (item < end) {
+            const Item it = level_item(a, tab, item);
+            const unsigned char *st = stage_S(item);
+            issue_child(stage_A(s), stage_F(s), st, a, it.ca, it.kinds & 3, it.r, it.tile);
+            issue_child(stage_B(s), stage_F(s) + T, st + T, a, it.cb, it.kinds >> 2, it.r, it.tile);
+        }
+        if (item2 < end) {
+            const Item it = level_item(a, tab, item2);
+            unsigned char *st = stage_S(item2);
+            issue_states(st, a, it.ca, it.kinds & 3, it.tile);
+            issue_states(st + T, a, it.cb, it.kinds >> 2, it.tile);
+        }
+        cp_async_commit();
+    };
+    // prologue: states of items beg, beg+1; data of beg
+    if (beg < end) {
+        const Item it = level_item(a, tab, beg);
+        issue_states(stage_S(beg), a, it.ca, it.kinds & 3, it.tile);
+        issue_states(stage_S(beg) + T, a, it.cb, it.kinds >> 2, it.tile);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    issue(beg, 0, beg + 1);
+    double b[16];
+    int cur = -1;                            // (node, r) whose B fragments are in b
+    for (int i = beg; i < end; ++i) {
+        cp_async_wait<0>();                  // item i's data and item i+1's states (own thread) landed
+        __syncthreads();                     // ... everyone's; stage of item i-1 is free
+        issue(i + 1, (i + 1 - beg) % PST, i + 2);
+        const int s = (i - beg) % PST;
+        const Item it = level_item(a, tab, i);
+        const int k = it.k, r = it.r, ca = it.ca, cb = it.cb;
+        const int pat0 = it.tile * T;
+        const double *As = stage_A(s), *Ts = stage_B(s);
+        const int *fa = stage_F(s), *fb = fa + T;
+        if (r == 0 && threadIdx.x < T) {     // cumulative exponent inside u_k (and at the root)
+            const int m = threadIdx.x;
+            int Ek = 0;
+            if (ca >= a.N) Ek += a.E[(size_t)(ca - a.N) * a.Cpad + pat0 + m] + lazy_exp(fa[m]);
+            if (cb >= a.N) Ek += a.E[(size_t)(cb - a.N) * a.Cpad + pat0 + m] + lazy_exp(fb[m]);
+            a.E[(size_t)(k - a.N) * a.Cpad + pat0 + m] = Ek;
+        }
+        if (k == root) {
+            // thread -> (pattern m = tid/8, 8 states); deterministic shuffle sum
+            const int m = threadIdx.x >> 3, j = threadIdx.x & 7;
+            double sum = 0.0;
+            for (int kk = j; kk < SP; kk += 8) {
+                const int p = apos(m, kk);
+                sum = fma(a.pi[kk], As[p] * Ts[p], sum);
+            }
+            sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+            sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+            sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+            if (j == 0)
+                a.Lpart[(size_t)r * a.Cpad + pat0 + m] = a.cat_w[r] * sum * (child_sc(a, ca, fa, m) * child_sc(a, cb, fb, m));
+            continue;
+        }
+        const int kr = k * a.R + r;
+        if (kr != cur) {
+            load_bfrag(b, a.PBpost + (size_t)kr * MAT, w, lane);
+            cur = kr;
+        }
+        // p = u_a o u_b in place (one A operand for the GEMM: half the
+        // shared-memory traffic per DMMA of forming it on the fly)
+        double *Pm = stage_A(s);
+#pragma unroll
+        for (int j = 0; j < TILE / 2 / NT; ++j) {
+            double2 *pa = reinterpret_cast<double2 *>(Pm) + threadIdx.x + j * NT;
+            const double2 tb = reinterpret_cast<const double2 *>(Ts)[threadIdx.x + j * NT];
+            double2 v = *pa;
+            v.x *= tb.x;
+            v.y *= tb.y;
+            *pa = v;
+        }
+        __syncthreads();
+        double acc[4][2];
+        gemm_tile(acc, Pm, b, lane);
+        double *out = a.u + (((size_t)(k - a.N) * a.R + r) * a.ntiles + it.tile) * TILE;
+        int *fm = a.fmax + (size_t)(k - a.N) * a.Cpad + pat0;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+            const double f2 = child_sc(a, ca, fa, m) * child_sc(a, cb, fb, m);   // children's scales
+            const double c0 = acc[mt][0] * f2, c1 = acc[mt][1] * f2;
+            *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(c0, c1);
+            int f = max(__double2hiint(c0) >> 20, __double2hiint(c1) >> 20);
+            f = max(f, __shfl_xor_sync(0xffffffffu, f, 1));
+            f = max(f, __shfl_xor_sync(0xffffffffu, f, 2));
+            if ((lane & 3) == 0) atomicMax(fm + m, f);
+        }
+    }
+    cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -392,7 +529,6 @@ __global__ void __launch_bounds__(256) codon_ratio_kernel(const CodonArgs a, dou
     if (threadIdx.x == 0) out[b < B ? 1 + b : 0] = sh[0];
 }
 
-constexpr size_t post_smem() { return (size_t)(2 * TILE + 2 * T) * 8 + 2 * T * 4; }
 constexpr size_t pre_smem() { return (size_t)(3 * TILE + 2 * NW * T + 3 * T) * 8 + 2 * T * 4; }
 
 // ---------------------------------------------------------------------------
