@@ -386,13 +386,44 @@ __global__ void __launch_bounds__(NT, 4) codon_pre_kernel(const CodonArgs a, int
         sc[threadIdx.x] = k == root ? 1.0 : pow2neg(lazy_exp(a.qmax[(size_t)(k - a.N) * a.Cpad + pat0 + threadIdx.x]));
     child_scale(sc + T, a, ch[0], a.fmax, pat0);
     child_scale(sc + 2 * T, a, ch[1], a.fmax, pat0);
+    // tip state codes of both children (one pass), then every tile copy in
+    // flight at once with cp.async (16-B pieces; tips: rows of P' by state)
+    if (threadIdx.x < 2 * T) {
+        const int c = threadIdx.x / T, m = threadIdx.x % T, node = ch[c];
+        stb[threadIdx.x] = (node < a.N) ? a.tip_states[(size_t)node * a.Cpad + pat0 + m] : 0;
+    }
+    __syncthreads();
     if (k == root) {
         for (int idx = threadIdx.x; idx < TILE; idx += NT) Qs[idx] = a.pi[((idx >> 5) & 15) * 4 + (idx & 3)];
     } else {
-        load_block(Qs, a.q + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE, TILE);
+        const double *src = a.q + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE;
+#pragma unroll
+        for (int j = 0; j < TILE / 2 / NT; ++j) cp_async16(Qs + 2 * (threadIdx.x + j * NT), src + 2 * (threadIdx.x + j * NT));
     }
-    load_child(Us[0], a, ch[0], r, tile, stb);
-    load_child(Us[1], a, ch[1], r, tile, stb + T);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int node = ch[c];
+        double *dst = Us[c];
+        if (node >= a.N) {
+            const double *src = a.u + (((size_t)(node - a.N) * a.R + r) * a.ntiles + tile) * TILE;
+#pragma unroll
+            for (int j = 0; j < TILE / 2 / NT; ++j) cp_async16(dst + 2 * (threadIdx.x + j * NT), src + 2 * (threadIdx.x + j * NT));
+        } else if (a.tip_is_partial[node]) {
+            load_child(dst, a, node, r, tile, stb + c * T);
+        } else {
+            const size_t br = (size_t)node * a.R + r;
+            const double *PT = a.PT + br * MAT, *ONE = a.PONE + br * SP;
+#pragma unroll
+            for (int j = 0; j < TILE / 2 / NT; ++j) {
+                int m, kk;
+                apos_inv(2 * (threadIdx.x + j * NT), m, kk);
+                const int st = stb[c * T + m];
+                cp_async16(dst + 2 * (threadIdx.x + j * NT), st < a.S ? PT + st * SP + kk : ONE + kk);
+            }
+        }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     // Tiles stay unscaled: the Eq. 8 terms of a pattern carry the same factor
     // sc_q sc_a sc_b in numerator and denominator of every category (cancels);
@@ -425,7 +456,7 @@ __global__ void __launch_bounds__(NT, 4) codon_pre_kernel(const CodonArgs a, int
                     acc[mt][0] = s0;
                     acc[mt][1] = s1;
                 } else {
-                    const int s = a.tip_states[(size_t)node * a.Cpad + pat0 + m];
+                    const int s = stb[c * T + m];              // staged above
                     if (s < a.S) {
                         const double2 v = __ldg(reinterpret_cast<const double2 *>(a.DT + br * MAT + s * SP + n));
                         acc[mt][0] = v.x;
