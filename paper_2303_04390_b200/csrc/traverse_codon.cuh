@@ -174,7 +174,7 @@ __device__ __forceinline__ void child_scale(double *sc, const CodonArgs &a, int 
 constexpr int PST = 2;                                           // post data stages
 constexpr int PSTAGE = 2 * TILE * 8 + 2 * T * 4;                 // A, B tiles + children's fmax
 constexpr int PSS = 3;                                           // state-code slots (2 children x 32 B)
-constexpr size_t post_smem() { return (size_t)PST * PSTAGE + PSS * 2 * T; }
+constexpr size_t post_smem() { return (size_t)PST * PSTAGE + PSS * 2 * T + T * 8; }   // + row scales
 
 // The level's nodes and their children, staged in shared memory at kernel
 // start: {k, child a, child b, kinds}, kind = 0 internal, 1 tip states,
@@ -331,6 +331,8 @@ __global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, in
         // p = u_a o u_b in place (one A operand for the GEMM: half the
         // shared-memory traffic per DMMA of forming it on the fly)
         double *Pm = stage_A(s);
+        double *f2s = reinterpret_cast<double *>(smem_c + (size_t)PST * PSTAGE + PSS * 2 * T);
+        if (threadIdx.x < T) f2s[threadIdx.x] = child_sc(a, ca, fa, threadIdx.x) * child_sc(a, cb, fb, threadIdx.x);
 #pragma unroll
         for (int j = 0; j < TILE / 2 / NT; ++j) {
             double2 *pa = reinterpret_cast<double2 *>(Pm) + threadIdx.x + j * NT;
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, in
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) {
             const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-            const double f2 = child_sc(a, ca, fa, m) * child_sc(a, cb, fb, m);   // children's scales
+            const double f2 = f2s[m];                         // children's scales (row)
             const double c0 = acc[mt][0] * f2, c1 = acc[mt][1] * f2;
             *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(c0, c1);
             int f = max(__double2hiint(c0) >> 20, __double2hiint(c1) >> 20);
