@@ -38,7 +38,7 @@ struct Layout {
         off_post, off_pre, total;
     // codon (variant 2) extras
     size_t off_PBpre = 0, off_DT = 0, off_PONE = 0, off_QB = 0, off_q = 0, off_E = 0, off_child = 0,
-           off_levels = 0, off_tipmode = 0, off_VA = 0, off_ViB = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0;
+           off_levels = 0, off_lev4 = 0, off_tipmode = 0, off_VA = 0, off_ViB = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0;
 };
 
 int padded_states(int S) {
@@ -133,6 +133,7 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         L->off_Lpart = take((size_t)R * L->Cpad * 8);
         L->off_child = take((size_t)2 * (2 * N - 1) * 4);
         L->off_levels = take((size_t)2 * (N - 1) * 4);
+        L->off_lev4 = take((size_t)2 * (N - 1) * 16);
         L->off_tipmode = take((size_t)N);
     }
     L->total = o;
@@ -609,6 +610,18 @@ static int refresh_plan(pg_instance *inst) {
                            cudaMemcpyHostToDevice, inst->stream), "levels upload");
         CK(cudaMemcpyAsync(inst->ws + inst->L.off_tipmode, inst->tip_is_partial.data(), N, cudaMemcpyHostToDevice,
                            inst->stream), "tip modes upload");
+        // per level entry: {node, child a, child b, kinds}; kind 0 internal, 1 tip states, 2 tip partials
+        auto kind = [&](int c) { return c >= N ? 0 : (inst->tip_is_partial[c] ? 2 : 1); };
+        std::vector<int32_t> l4(4 * inst->plan.level_nodes.size());
+        for (size_t i = 0; i < inst->plan.level_nodes.size(); ++i) {
+            const int k = inst->plan.level_nodes[i], ca = inst->plan.child_a[k], cb = inst->plan.child_b[k];
+            l4[4 * i] = k;
+            l4[4 * i + 1] = ca;
+            l4[4 * i + 2] = cb;
+            l4[4 * i + 3] = kind(ca) | (kind(cb) << 2);
+        }
+        CK(cudaMemcpyAsync(inst->ws + inst->L.off_lev4, l4.data(), l4.size() * 4, cudaMemcpyHostToDevice, inst->stream),
+           "level table upload");
     }
     CK(cudaStreamSynchronize(inst->stream), "plan upload sync");
     int rc = configure(inst);
@@ -657,6 +670,7 @@ static pg::codon::CodonArgs codon_args(pg_instance *inst) {
     c.child_a = inst->at<int>(L.off_child);
     c.child_b = c.child_a + (2 * N - 1);
     c.levels = inst->at<int>(L.off_levels);
+    c.lev4 = reinterpret_cast<const int4 *>(inst->ws + L.off_lev4);
     c.PBpost = inst->at<double>(L.off_P);
     c.PBpre = inst->at<double>(L.off_PBpre);
     c.PT = inst->at<double>(L.off_PT);

@@ -40,6 +40,7 @@ __device__ __forceinline__ void apos_inv(int idx, int &m, int &k) {
 struct CodonArgs {
     const int *child_a, *child_b;     // [2N-1] children of internal nodes (-1 for tips)
     const int *levels;                // node lists of all levels
+    const int4 *lev4;                 // per level entry {node, child a, child b, kinds} (host-built)
     const double *PBpost, *PBpre;     // [B][R][MAT] fragment-ordered B operands
     const double *PT, *DT;            // [B][R][SP][SP]  P' and (gamma Q P)' row-major
     const double *PONE;               // [B][R][SP]      P 1 (missing-data tips)
@@ -184,10 +185,7 @@ __device__ __forceinline__ int child_kind(const CodonArgs &a, int c) {
     return c >= a.N ? 0 : (a.tip_is_partial[c] ? 2 : 1);
 }
 __device__ __forceinline__ void stage_level(int4 *tab, const CodonArgs &a, int level_off, int cnt) {
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-        const int k = a.levels[level_off + i], ca = a.child_a[k], cb = a.child_b[k];
-        tab[i] = make_int4(k, ca, cb, child_kind(a, ca) | (child_kind(a, cb) << 2));
-    }
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) tab[i] = a.lev4[level_off + i];
 }
 __device__ __forceinline__ Item level_item(const CodonArgs &a, const int4 *tab, int item) {
     Item it;
@@ -379,9 +377,11 @@ __global__ void __launch_bounds__(NT, 4) codon_pre_kernel(const CodonArgs a, int
     double *sc = part + 2 * NW * T;                          // [3][T]: q_k, u_a, u_b scales
     int *stb = reinterpret_cast<int *>(sc + 3 * T);          // [2][T] tip states
     const int tile = blockIdx.x, r = blockIdx.z;
-    const int k = a.levels[level_off + blockIdx.y];
+    const int4 lv = a.lev4[level_off + blockIdx.y];        // {node, children, kinds}: one load
+    const int k = lv.x;
     const int root = 2 * a.N - 2;
-    const int ch[2] = {a.child_a[k], a.child_b[k]};
+    const int ch[2] = {lv.y, lv.z};
+    const int kinds = lv.w;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int pat0 = tile * T;
     if (threadIdx.x < T)
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(NT, 4) codon_pre_kernel(const CodonArgs a, int
             const double *src = a.u + (((size_t)(node - a.N) * a.R + r) * a.ntiles + tile) * TILE;
 #pragma unroll
             for (int j = 0; j < TILE / 2 / NT; ++j) cp_async16(dst + 2 * (threadIdx.x + j * NT), src + 2 * (threadIdx.x + j * NT));
-        } else if (a.tip_is_partial[node]) {
+        } else if (((kinds >> (2 * c)) & 3) == 2) {
             load_child(dst, a, node, r, tile, stb + c * T);
         } else {
             const size_t br = (size_t)node * a.R + r;
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(NT, 4) codon_pre_kernel(const CodonArgs a, int
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
                 const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-                if (a.tip_is_partial[node]) {
+                if (((kinds >> (2 * c)) & 3) == 2) {
                     double s0 = 0.0, s1 = 0.0;     // D p = sum_t D[s][t] p[t]
                     const double *p = a.tip_partials + ((size_t)node * a.Cpad + pat0 + m) * SP;
                     const double *DT = a.DT + br * MAT;
