@@ -373,8 +373,8 @@ __global__ void __launch_bounds__(NT, 4) codon_pre_kernel(const CodonArgs a, int
     extern __shared__ __align__(16) unsigned char smem_c[];
     double *Qs = reinterpret_cast<double *>(smem_c);
     double *Us[2] = {Qs + TILE, Qs + 2 * TILE};
-    double *part = Qs + 3 * TILE;                            // [2 (num,den)][NW][T]
-    double *sc = part + 2 * NW * T;                          // [3][T]: q_k, u_a, u_b scales
+    double *part = Qs + 3 * TILE;                            // [3: num a, num b, den][NW][T]
+    double *sc = part + 3 * NW * T;                          // [3][T]: q_k, u_a, u_b scales
     int *stb = reinterpret_cast<int *>(sc + 3 * T);          // [2][T] tip states
     const int tile = blockIdx.x, r = blockIdx.z;
     const int4 lv = a.lev4[level_off + blockIdx.y];        // {node, children, kinds}: one load
@@ -431,17 +431,18 @@ __global__ void __launch_bounds__(NT, 4) codon_pre_kernel(const CodonArgs a, int
     // sc_q sc_a sc_b in numerator and denominator of every category (cancels);
     // the stored q_c rows are multiplied by sc_q sc_sibling below.
     const double wr = a.cat_w[r], gr = a.cat_g[r];
+    // --- phase 1: Eq. 8 terms of both children --------------------------
+    // num_c = x_c'(Q u_c) with x_c = q_k o u_sibling; den = x_c'u_c is the
+    // same for both children (q_k o u_a o u_b, Eq. 5).
+#pragma unroll 1
     for (int c = 0; c < 2; ++c) {
         const int node = ch[c];
         const size_t br = (size_t)node * a.R + r;
-        // --- Eq. 8 terms ------------------------------------------------
         double acc[4][2];
-        double scale;
         if (node >= a.N) {
             double b[16];
             load_bfrag(b, a.QB, w, lane);
             gemm_tile(acc, Us[c], b, lane);
-            scale = gr * wr;
         } else {
             // tip: gamma (Q u)[s] = D[s][state]; missing data: D 1 = gamma Q 1 = 0
 #pragma unroll
@@ -468,63 +469,77 @@ __global__ void __launch_bounds__(NT, 4) codon_pre_kernel(const CodonArgs a, int
                     }
                 }
             }
-            scale = wr;
         }
-        double pn[4], pd[4];
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) {
             const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
             const int p = apos(m, n);
             const double2 q2 = *reinterpret_cast<const double2 *>(Qs + p);
             const double2 o2 = *reinterpret_cast<const double2 *>(Us[1 - c] + p);
-            const double2 u2 = *reinterpret_cast<const double2 *>(Us[c] + p);
             const double x0 = q2.x * o2.x, x1 = q2.y * o2.y;     // x_c = q_k o u_sibling
             double sn = x0 * acc[mt][0] + x1 * acc[mt][1];
-            double sd = x0 * u2.x + x1 * u2.y;
             sn += __shfl_xor_sync(0xffffffffu, sn, 1);
-            sd += __shfl_xor_sync(0xffffffffu, sd, 1);
             sn += __shfl_xor_sync(0xffffffffu, sn, 2);
-            sd += __shfl_xor_sync(0xffffffffu, sd, 2);
-            pn[mt] = sn;
-            pd[mt] = sd;
-        }
-        if ((lane & 3) == 0) {
-#pragma unroll
-            for (int mt = 0; mt < 4; ++mt) {
-                const int m = mt * 8 + (lane >> 2);
-                part[(0 * NW + w) * T + m] = pn[mt];
-                part[(1 * NW + w) * T + m] = pd[mt];
+            if ((lane & 3) == 0) part[(c * NW + w) * T + m] = sn;
+            if (c == 0) {
+                const double2 u2 = *reinterpret_cast<const double2 *>(Us[0] + p);
+                double sd = x0 * u2.x + x1 * u2.y;
+                sd += __shfl_xor_sync(0xffffffffu, sd, 1);
+                sd += __shfl_xor_sync(0xffffffffu, sd, 2);
+                if ((lane & 3) == 0) part[(2 * NW + w) * T + m] = sd;
             }
         }
-        // --- q_c = x_c P_c (Eq. 4) for internal children ------------------
-        if (node >= a.N) {
-            double bq[16];
-            load_bfrag(bq, a.PBpre + br * MAT, w, lane);
-            gemm_tile2(acc, Qs, Us[1 - c], bq, lane);
-            double *out = a.q + (((size_t)(node - a.N) * a.R + r) * a.ntiles + tile) * TILE;
-            int *qm = a.qmax + (size_t)(node - a.N) * a.Cpad + pat0;
+    }
+    __syncthreads();
+    // --- phase 2: x_0 = q o u_b into u_b's tile, x_1 = q o u_a into u_a's
+    // (in place: the u tiles are not needed any more) ---------------------
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt) {
-                const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-                const double f2 = sc[m] * sc[(2 - c) * T + m];   // q_k and sibling scales
-                acc[mt][0] *= f2;
-                acc[mt][1] *= f2;
-                *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
-                int f = max(__double2hiint(acc[mt][0]) >> 20, __double2hiint(acc[mt][1]) >> 20);
-                f = max(f, __shfl_xor_sync(0xffffffffu, f, 1));
-                f = max(f, __shfl_xor_sync(0xffffffffu, f, 2));
-                if ((lane & 3) == 0) atomicMax(qm + m, f);
-            }
+    for (int j = 0; j < TILE / 2 / NT; ++j) {
+        const int i2 = threadIdx.x + j * NT;
+        const double2 q2 = reinterpret_cast<const double2 *>(Qs)[i2];
+        const double2 u0 = reinterpret_cast<const double2 *>(Us[0])[i2];
+        const double2 u1 = reinterpret_cast<const double2 *>(Us[1])[i2];
+        reinterpret_cast<double2 *>(Us[1])[i2] = make_double2(q2.x * u1.x, q2.y * u1.y);
+        reinterpret_cast<double2 *>(Us[0])[i2] = make_double2(q2.x * u0.x, q2.y * u0.y);
+    }
+    if (threadIdx.x < T) {                    // fixed-order sums over the 8 warps
+        const int m = threadIdx.x;
+        double sd = 0.0, sn0 = 0.0, sn1 = 0.0;
+        for (int ww = 0; ww < NW; ++ww) {
+            sn0 += part[ww * T + m];
+            sn1 += part[(NW + ww) * T + m];
+            sd += part[(2 * NW + ww) * T + m];
         }
-        __syncthreads();
-        if (threadIdx.x < T) {                // fixed-order sum over the 8 warps
-            const int m = threadIdx.x;
-            double sn = 0.0, sd = 0.0;
-            for (int ww = 0; ww < NW; ++ww) { sn += part[ww * T + m]; sd += part[(NW + ww) * T + m]; }
-            double2 *dst = reinterpret_cast<double2 *>(a.numden) + (br * a.Cpad + pat0 + m);
-            *dst = make_double2(scale * sn, wr * sd);
+        double2 *nd = reinterpret_cast<double2 *>(a.numden);
+        // internal children: Q u (times gamma_r here); tips: D u already carries gamma_r
+        const double s0 = ch[0] >= a.N ? gr * wr : wr, s1 = ch[1] >= a.N ? gr * wr : wr;
+        nd[((size_t)ch[0] * a.R + r) * a.Cpad + pat0 + m] = make_double2(s0 * sn0, wr * sd);
+        nd[((size_t)ch[1] * a.R + r) * a.Cpad + pat0 + m] = make_double2(s1 * sn1, wr * sd);
+    }
+    __syncthreads();
+    // --- phase 3: q_c = x_c P_c (Eq. 4) for internal children ---------------
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+        const int node = ch[c];
+        if (node < a.N) continue;
+        const size_t br = (size_t)node * a.R + r;
+        double bq[16], acc[4][2];
+        load_bfrag(bq, a.PBpre + br * MAT, w, lane);
+        gemm_tile(acc, Us[1 - c], bq, lane);          // x_c lives in the sibling's tile
+        double *out = a.q + (((size_t)(node - a.N) * a.R + r) * a.ntiles + tile) * TILE;
+        int *qm = a.qmax + (size_t)(node - a.N) * a.Cpad + pat0;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+            const double f2 = sc[m] * sc[(2 - c) * T + m];   // q_k and sibling scales
+            acc[mt][0] *= f2;
+            acc[mt][1] *= f2;
+            *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
+            int f = max(__double2hiint(acc[mt][0]) >> 20, __double2hiint(acc[mt][1]) >> 20);
+            f = max(f, __shfl_xor_sync(0xffffffffu, f, 1));
+            f = max(f, __shfl_xor_sync(0xffffffffu, f, 2));
+            if ((lane & 3) == 0) atomicMax(qm + m, f);
         }
-        __syncthreads();
     }
 }
 
@@ -562,7 +577,7 @@ __global__ void __launch_bounds__(256) codon_ratio_kernel(const CodonArgs a, dou
     if (threadIdx.x == 0) out[b < B ? 1 + b : 0] = sh[0];
 }
 
-constexpr size_t pre_smem() { return (size_t)(3 * TILE + 2 * NW * T + 3 * T) * 8 + 2 * T * 4; }
+constexpr size_t pre_smem() { return (size_t)(3 * TILE + 3 * NW * T + 3 * T) * 8 + 2 * T * 4; }
 
 // ---------------------------------------------------------------------------
 // A1 for this path: per (branch, category) P = (V diag(e)) V^{-1} and
