@@ -576,8 +576,9 @@ static int configure(pg_instance *inst) {
         inst->block = pg::codon::NT;
         inst->prefetch = 0;
         inst->smem = (int)pg::codon::pre_smem();
-        CK(cudaFuncSetAttribute((void *)pg::codon::codon_post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(pg::codon::post_smem() + 16 * (size_t)inst->cfg.tips)), "smem attr");
+        for (void *fn : {(void *)pg::codon::codon_post_kernel<4>, (void *)pg::codon::codon_post_kernel<2>})
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(pg::codon::post_smem() + 16 * (size_t)inst->cfg.tips)), "smem attr");
         CK(cudaFuncSetAttribute((void *)pg::codon::codon_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)pg::codon::pre_smem()), "smem attr");
         CK(cudaFuncSetAttribute((void *)pg::codon::codon_pmat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -736,10 +737,14 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         CK(cudaMemsetAsync(inst->ws + L.off_fmax, 0, (size_t)(2 * N - 3) * L.Cpad * 4, inst->stream), "fmax reset");
         for (size_t i = 0; i + 1 < pl.post_off.size(); ++i) {
             int off = pl.post_off[i], cnt = pl.post_off[i + 1] - off;
-            const int items = L.n_tiles * cnt * R;      // persistent: 3 CTAs per SM walk the level's items
+            // persistent: 3 CTAs per SM walk the level's items; narrow levels
+            // (fewer full-tile items than ~2 waves) use half-tile items
+            const bool narrow = L.n_tiles * cnt * R < 6 * inst->sm_count;
+            const int items = L.n_tiles * cnt * R * (narrow ? 2 : 1);
+            void *fn = narrow ? (void *)pg::codon::codon_post_kernel<2> : (void *)pg::codon::codon_post_kernel<4>;
             void *args[] = {&c, &off, &cnt};
-            CK(cudaLaunchKernel((void *)pg::codon::codon_post_kernel, dim3(std::min(items, 3 * inst->sm_count)),
-                                dim3(pg::codon::NT), args, pg::codon::post_smem() + 16 * (size_t)cnt, inst->stream),
+            CK(cudaLaunchKernel(fn, dim3(std::min(items, 3 * inst->sm_count)), dim3(pg::codon::NT), args,
+                                pg::codon::post_smem() + 16 * (size_t)cnt, inst->stream),
                "codon post launch");
         }
         for (size_t i = 0; i + 1 < pl.pre_off.size(); ++i) {

@@ -79,13 +79,14 @@ __device__ __forceinline__ void load_bfrag(double (&b)[16], const double *__rest
 }
 
 // acc[mt] (rows mt*8 + lane/4, cols w*8 + 2*(lane%4) + {0,1}) = A(32x64) * B(64x64)[:, 8w..8w+7]
-__device__ __forceinline__ void gemm_tile(double (&acc)[4][2], const double *As, const double (&b)[16], int lane) {
+template <int MT = 4>
+__device__ __forceinline__ void gemm_tile(double (&acc)[MT][2], const double *As, const double (&b)[16], int lane) {
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+    for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
 #pragma unroll
     for (int kt = 0; kt < 16; ++kt)
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) dmma(acc[mt], As[(mt * 16 + kt) * 32 + lane], b[kt]);
+        for (int mt = 0; mt < MT; ++mt) dmma(acc[mt], As[(mt * 16 + kt) * 32 + lane], b[kt]);
 }
 
 // same with A = A1 o A2 (element-wise, e.g. x = q o u_sibling), formed on the fly
@@ -180,17 +181,24 @@ constexpr size_t post_smem() { return (size_t)PST * PSTAGE + PSS * 2 * T + T * 8
 // The level's nodes and their children, staged in shared memory at kernel
 // start: {k, child a, child b, kinds}, kind = 0 internal, 1 tip states,
 // 2 tip partials (child a in bits 0-1, child b in bits 2-3).
-struct Item { int k, r, tile, ca, cb, kinds; };
+struct Item { int k, r, tile, ro, ca, cb, kinds; };
 __device__ __forceinline__ int child_kind(const CodonArgs &a, int c) {
     return c >= a.N ? 0 : (a.tip_is_partial[c] ? 2 : 1);
 }
 __device__ __forceinline__ void stage_level(int4 *tab, const CodonArgs &a, int level_off, int cnt) {
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) tab[i] = a.lev4[level_off + i];
 }
+// Items are (node, r, tile, row block), row block fastest: MH m-tiles (8 MH
+// patterns) of a 32-pattern tile.  Narrow levels use MH = 2 (twice the items,
+// half the latency each); rows of a tile are contiguous in fragment order.
+template <int MH>
 __device__ __forceinline__ Item level_item(const CodonArgs &a, const int4 *tab, int item) {
+    constexpr int HALF = 4 / MH;
     Item it;
-    it.tile = item % a.ntiles;
-    const int nr = item / a.ntiles;
+    const int sub = item % (a.ntiles * HALF);
+    it.tile = sub / HALF;
+    it.ro = (sub % HALF) * 8 * MH;
+    const int nr = item / (a.ntiles * HALF);
     it.r = nr % a.R;
     const int4 e = tab[nr / a.R];
     it.k = e.x;
@@ -204,23 +212,24 @@ __device__ __forceinline__ Item level_item(const CodonArgs &a, const int4 *tab, 
 // bytes) were staged in shared memory one item earlier (`st`), so the
 // gather addresses need no global round trip.  Tip partials (rare) are
 // computed here.
+template <int MH>
 __device__ __forceinline__ void issue_child(double *dst, int *fm, const unsigned char *st, const CodonArgs &a,
-                                            int child, int kind, int r, int tile) {
+                                            int child, int kind, int r, int tile, int ro) {
     const int tid = threadIdx.x;
     if (kind == 0) {
-        const double *src = a.u + (((size_t)(child - a.N) * a.R + r) * a.ntiles + tile) * TILE;
+        const double *src = a.u + (((size_t)(child - a.N) * a.R + r) * a.ntiles + tile) * TILE + ro * SP;
 #pragma unroll
-        for (int j = 0; j < TILE / 2 / NT; ++j) cp_async16(dst + 2 * (tid + j * NT), src + 2 * (tid + j * NT));
-        if (tid < T / 4) cp_async16(fm + 4 * tid, a.fmax + (size_t)(child - a.N) * a.Cpad + tile * T + 4 * tid);
+        for (int j = 0; j < MH; ++j) cp_async16(dst + 2 * (tid + j * NT), src + 2 * (tid + j * NT));
+        if (tid < 2 * MH) cp_async16(fm + 4 * tid, a.fmax + (size_t)(child - a.N) * a.Cpad + tile * T + ro + 4 * tid);
         return;
     }
     const size_t br = (size_t)child * a.R + r;
     const double *PT = a.PT + br * MAT;
     if (kind == 2) {                        // u[s] = sum_t P[s][t] p[t] = sum_t PT[t][s] p[t]
-        for (int idx = tid; idx < TILE; idx += NT) {
+        for (int idx = tid; idx < MH * 8 * SP; idx += NT) {
             int m, k;
             apos_inv(idx, m, k);
-            const double *p = a.tip_partials + ((size_t)child * a.Cpad + tile * T + m) * SP;
+            const double *p = a.tip_partials + ((size_t)child * a.Cpad + tile * T + ro + m) * SP;
             double acc = 0.0;
             for (int t = 0; t < SP; ++t) acc = fma(__ldg(PT + t * SP + k), __ldg(p + t), acc);
             dst[idx] = acc;
@@ -231,25 +240,28 @@ __device__ __forceinline__ void issue_child(double *dst, int *fm, const unsigned
     const int c = (tid & 15) >> 1;
     const double *ONE = a.PONE + br * SP;
 #pragma unroll
-    for (int j = 0; j < TILE / 2 / NT; ++j) {
+    for (int j = 0; j < MH; ++j) {
         int m, k;
         apos_inv(2 * (tid + j * NT), m, k);
         const int s = st[8 * j + c];
         cp_async16(dst + 2 * (tid + j * NT), s < a.S ? PT + s * SP + k : ONE + k);
     }
 }
-// stage a tip child's 32 state codes of the tile (2 x 16 B)
-__device__ __forceinline__ void issue_states(unsigned char *st, const CodonArgs &a, int child, int kind, int tile) {
-    if (kind == 1 && threadIdx.x < 2)
-        cp_async16(st + 16 * threadIdx.x, a.tip_states + (size_t)child * a.Cpad + tile * T + 16 * threadIdx.x);
+// stage a tip child's 8 MH state codes of the row block (16-B pieces)
+template <int MH>
+__device__ __forceinline__ void issue_states(unsigned char *st, const CodonArgs &a, int child, int kind, int tile, int ro) {
+    if (kind == 1 && threadIdx.x < MH / 2)
+        cp_async16(st + 16 * threadIdx.x, a.tip_states + (size_t)child * a.Cpad + tile * T + ro + 16 * threadIdx.x);
 }
 __device__ __forceinline__ double child_sc(const CodonArgs &a, int child, const int *fm, int m) {
     return child >= a.N ? pow2neg(lazy_exp(fm[m])) : 1.0;
 }
 
+template <int MH>
 __global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, int level_off, int cnt) {
+    constexpr int TI = 8 * MH;               // patterns per item
     extern __shared__ __align__(16) unsigned char smem_c[];
-    const int nitems = cnt * a.R * a.ntiles;
+    const int nitems = cnt * a.R * a.ntiles * (4 / MH);
     int4 *tab = reinterpret_cast<int4 *>(smem_c + post_smem());
     stage_level(tab, a, level_off, cnt);
     __syncthreads();
@@ -264,24 +276,24 @@ __global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, in
     // data of `item` into stage s (its states are staged); states of `item2`
     auto issue = [&](int item, int s, int item2) {
         if (item < end) {
-            const Item it = level_item(a, tab, item);
+            const Item it = level_item<MH>(a, tab, item);
             const unsigned char *st = stage_S(item);
-            issue_child(stage_A(s), stage_F(s), st, a, it.ca, it.kinds & 3, it.r, it.tile);
-            issue_child(stage_B(s), stage_F(s) + T, st + T, a, it.cb, it.kinds >> 2, it.r, it.tile);
+            issue_child<MH>(stage_A(s), stage_F(s), st, a, it.ca, it.kinds & 3, it.r, it.tile, it.ro);
+            issue_child<MH>(stage_B(s), stage_F(s) + T, st + T, a, it.cb, it.kinds >> 2, it.r, it.tile, it.ro);
         }
         if (item2 < end) {
-            const Item it = level_item(a, tab, item2);
+            const Item it = level_item<MH>(a, tab, item2);
             unsigned char *st = stage_S(item2);
-            issue_states(st, a, it.ca, it.kinds & 3, it.tile);
-            issue_states(st + T, a, it.cb, it.kinds >> 2, it.tile);
+            issue_states<MH>(st, a, it.ca, it.kinds & 3, it.tile, it.ro);
+            issue_states<MH>(st + T, a, it.cb, it.kinds >> 2, it.tile, it.ro);
         }
         cp_async_commit();
     };
     // prologue: states of items beg, beg+1; data of beg
     if (beg < end) {
-        const Item it = level_item(a, tab, beg);
-        issue_states(stage_S(beg), a, it.ca, it.kinds & 3, it.tile);
-        issue_states(stage_S(beg) + T, a, it.cb, it.kinds >> 2, it.tile);
+        const Item it = level_item<MH>(a, tab, beg);
+        issue_states<MH>(stage_S(beg), a, it.ca, it.kinds & 3, it.tile, it.ro);
+        issue_states<MH>(stage_S(beg) + T, a, it.cb, it.kinds >> 2, it.tile, it.ro);
     }
     cp_async_commit();
     cp_async_wait<0>();
@@ -294,12 +306,12 @@ __global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, in
         __syncthreads();                     // ... everyone's; stage of item i-1 is free
         issue(i + 1, (i + 1 - beg) % PST, i + 2);
         const int s = (i - beg) % PST;
-        const Item it = level_item(a, tab, i);
+        const Item it = level_item<MH>(a, tab, i);
         const int k = it.k, r = it.r, ca = it.ca, cb = it.cb;
-        const int pat0 = it.tile * T;
+        const int pat0 = it.tile * T + it.ro;     // first pattern of the item
         const double *As = stage_A(s), *Ts = stage_B(s);
         const int *fa = stage_F(s), *fb = fa + T;
-        if (r == 0 && threadIdx.x < T) {     // cumulative exponent inside u_k (and at the root)
+        if (r == 0 && threadIdx.x < TI) {    // cumulative exponent inside u_k (and at the root)
             const int m = threadIdx.x;
             int Ek = 0;
             if (ca >= a.N) Ek += a.E[(size_t)(ca - a.N) * a.Cpad + pat0 + m] + lazy_exp(fa[m]);
@@ -310,14 +322,15 @@ __global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, in
             // thread -> (pattern m = tid/8, 8 states); deterministic shuffle sum
             const int m = threadIdx.x >> 3, j = threadIdx.x & 7;
             double sum = 0.0;
-            for (int kk = j; kk < SP; kk += 8) {
-                const int p = apos(m, kk);
-                sum = fma(a.pi[kk], As[p] * Ts[p], sum);
-            }
+            if (m < TI)
+                for (int kk = j; kk < SP; kk += 8) {
+                    const int p = apos(m, kk);
+                    sum = fma(a.pi[kk], As[p] * Ts[p], sum);
+                }
             sum += __shfl_xor_sync(0xffffffffu, sum, 1);
             sum += __shfl_xor_sync(0xffffffffu, sum, 2);
             sum += __shfl_xor_sync(0xffffffffu, sum, 4);
-            if (j == 0)
+            if (j == 0 && m < TI)
                 a.Lpart[(size_t)r * a.Cpad + pat0 + m] = a.cat_w[r] * sum * (child_sc(a, ca, fa, m) * child_sc(a, cb, fb, m));
             continue;
         }
@@ -330,9 +343,9 @@ __global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, in
         // shared-memory traffic per DMMA of forming it on the fly)
         double *Pm = stage_A(s);
         double *f2s = reinterpret_cast<double *>(smem_c + (size_t)PST * PSTAGE + PSS * 2 * T);
-        if (threadIdx.x < T) f2s[threadIdx.x] = child_sc(a, ca, fa, threadIdx.x) * child_sc(a, cb, fb, threadIdx.x);
+        if (threadIdx.x < TI) f2s[threadIdx.x] = child_sc(a, ca, fa, threadIdx.x) * child_sc(a, cb, fb, threadIdx.x);
 #pragma unroll
-        for (int j = 0; j < TILE / 2 / NT; ++j) {
+        for (int j = 0; j < MH; ++j) {
             double2 *pa = reinterpret_cast<double2 *>(Pm) + threadIdx.x + j * NT;
             const double2 tb = reinterpret_cast<const double2 *>(Ts)[threadIdx.x + j * NT];
             double2 v = *pa;
@@ -341,12 +354,12 @@ __global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, in
             *pa = v;
         }
         __syncthreads();
-        double acc[4][2];
-        gemm_tile(acc, Pm, b, lane);
-        double *out = a.u + (((size_t)(k - a.N) * a.R + r) * a.ntiles + it.tile) * TILE;
+        double acc[MH][2];
+        gemm_tile<MH>(acc, Pm, b, lane);
+        double *out = a.u + (((size_t)(k - a.N) * a.R + r) * a.ntiles + it.tile) * TILE + it.ro * SP;
         int *fm = a.fmax + (size_t)(k - a.N) * a.Cpad + pat0;
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
+        for (int mt = 0; mt < MH; ++mt) {
             const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
             const double f2 = f2s[m];                         // children's scales (row)
             const double c0 = acc[mt][0] * f2, c1 = acc[mt][1] * f2;
