@@ -77,7 +77,7 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         }
         int Rp = 1;
         while (Rp < R) Rp <<= 1;
-        L->tpl = 32 / (Rp * pg::small_lanes_per_vector(SP));   // patterns per warp tile (lane = pattern x category x state group)
+        L->tpl = 32 / (Rp * pg::small_lanes_per_vector(SP, Rp));   // patterns per warp tile (lane = pattern x category x state group)
     } else if (L->variant == 2) {
         if (R > 16) { if (err) *err = "too many rate categories (max 16)"; return PG_ERR_UNSUPPORTED; }
         L->tpl = pg::codon::T;
@@ -552,7 +552,8 @@ static int configure(pg_instance *inst) {
     if (L.variant == 0) {
         // CTA = K tile warps + 1 producer warp; K = tiles / SMs (one wave), at
         // most 9 (launch bounds) and within the shared-memory budget.
-        int K = std::max(1, std::min(pg::small_max_consumers(L.SP), (L.n_tiles + inst->sm_count - 1) / inst->sm_count));
+        int K = std::max(1, std::min(pg::small_max_consumers(L.SP, pad_categories(R)),
+                                     (L.n_tiles + inst->sm_count - 1) / inst->sm_count));
         while (K > 1 && small_smem(L, R, K, depth) > 227 * 1024) --K;
         inst->tiles_per_cta = K;
         inst->block = 32 * (K + 1);

@@ -55,9 +55,14 @@ namespace pg {
 #ifndef PG_SP4_LV
 #define PG_SP4_LV 1
 #endif
-__host__ __device__ constexpr int small_lanes_per_vector(int SP) { return SP == 4 ? PG_SP4_LV : SP / 4; }
+#ifndef PG_SP16_LV
+#define PG_SP16_LV 4
+#endif
+__host__ __device__ constexpr int small_lanes_per_vector(int SP, int RP) {
+    return SP == 4 ? PG_SP4_LV : SP == 16 ? (PG_SP16_LV < 32 / RP ? PG_SP16_LV : 32 / RP) : SP / 4;
+}
 // consumer warps per CTA at most (launch bounds: + 1 producer warp)
-__host__ __device__ constexpr int small_max_consumers(int SP) { return small_lanes_per_vector(SP) * 4 / SP >= 2 ? 17 : 9; }
+__host__ __device__ constexpr int small_max_consumers(int SP, int RP) { return small_lanes_per_vector(SP, RP) * 4 / SP >= 2 ? 17 : 9; }
 
 // ---- shape of one CTA's work ----------------------------------------------
 // A CTA = K consumer warps (one pattern tile each) + 1 producer warp.  Global
@@ -67,7 +72,7 @@ __host__ __device__ constexpr int small_max_consumers(int SP) { return small_lan
 // matrices are one contiguous bulk copy.
 template <typename Real, int SP, int RP>
 struct SmallCfg {
-    static constexpr int LV = small_lanes_per_vector(SP);     // lanes per vector
+    static constexpr int LV = small_lanes_per_vector(SP, RP); // lanes per vector
     static constexpr int VL = SP / LV;                         // states per lane
     static constexpr int TP = 32 / (RP * LV);                  // patterns per warp tile
 #ifndef PG_STAGES
@@ -289,7 +294,7 @@ __device__ __forceinline__ int maybe_rescale(Real (&v)[SP]) {
 
 
 template <typename Real, int SP, int RP>
-__global__ void __launch_bounds__(32 * (small_max_consumers(SP) + 1), 1) traverse_small_kernel(const TravArgs a) {
+__global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) traverse_small_kernel(const TravArgs a) {
     using Cfg = SmallCfg<Real, SP, RP>;
     constexpr int TP = Cfg::TP, D = Cfg::D, PF = Cfg::PF, W = Cfg::W, VB = Cfg::VB, CS = Cfg::CS;
     constexpr int LV = Cfg::LV, VL = Cfg::VL, VBL = Cfg::VBL, G = RP * LV;
