@@ -44,6 +44,7 @@
 #define PG_SMALL_W 2
 #endif
 
+
 namespace pg {
 
 // lanes per (pattern, category) vector: each lane holds VL = SP / LV states.
@@ -103,8 +104,18 @@ struct SmallCfg {
     static __host__ __device__ int warp_bytes(int depth) {
         return ((depth + 1) * 32 * VBL + ND + XB + TP * 8 + W * 2 * 4 + 8 + 15) / 16 * 16;
     }
+    // OPS consecutive ops share one ring stage (one full/empty barrier pair),
+    // DS stages in the ring.  Pairing halves the barrier traffic but lets the
+    // producer refill only after both ops: measured +5 % for S = 16 (whose
+    // ring grows to 4 ops), 24 % slower for S = 4 (same smem, less lookahead).
+#ifdef PG_OPS
+    static constexpr int OPS = PG_OPS;
+#else
+    static constexpr int OPS = SP == 16 ? 2 : 1;
+#endif
+    static constexpr int DS = D / OPS < 2 ? 2 : D / OPS;
     static __host__ __device__ size_t smem(int R, int K, int depth) {
-        return (size_t)BARS + (size_t)D * stage(R, K) + (size_t)K * warp_bytes(depth);
+        return (size_t)BARS + (size_t)DS * OPS * stage(R, K) + (size_t)K * warp_bytes(depth);
     }
 };
 
@@ -296,8 +307,9 @@ __device__ __forceinline__ int maybe_rescale(Real (&v)[SP]) {
 template <typename Real, int SP, int RP>
 __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) traverse_small_kernel(const TravArgs a) {
     using Cfg = SmallCfg<Real, SP, RP>;
-    constexpr int TP = Cfg::TP, D = Cfg::D, PF = Cfg::PF, W = Cfg::W, VB = Cfg::VB, CS = Cfg::CS;
+    constexpr int TP = Cfg::TP, PF = Cfg::PF, W = Cfg::W, VB = Cfg::VB, CS = Cfg::CS;
     constexpr int LV = Cfg::LV, VL = Cfg::VL, VBL = Cfg::VBL, G = RP * LV;
+    constexpr int OPS = Cfg::OPS, DS = Cfg::DS;
     extern __shared__ __align__(128) unsigned char smem_s[];
     unsigned char *smem = smem_s;
     const int R = a.R, N = a.N, S = a.S;
@@ -312,12 +324,20 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     const size_t u_node = Cpad * R * VB;                           // one node's u block (bytes)
 
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);            // [D]
-    uint64_t *empty = full + D;                                     // [D]
-    uint64_t *post_done = empty + D;                                // [1]
+    uint64_t *empty = full + DS;                                    // [DS]
+    uint64_t *post_done = empty + DS;                               // [1]
     unsigned char *stages = smem + Cfg::BARS;
     // shared-window addresses of the barriers and stages (loop-invariant bases)
     const uint32_t sbase = smem_u32(smem);
-    const uint32_t full_u = sbase, empty_u = sbase + 8u * D, stages_u = sbase + Cfg::BARS;
+    const uint32_t full_u = sbase, empty_u = sbase + 8u * DS, stages_u = sbase + Cfg::BARS;
+    // step t (post 0..nops-1, pre nops..2nops-1) -> ring stage and slot; the
+    // pre program starts on a fresh stage
+    const int GP = (nops + OPS - 1) / OPS;
+    auto stg = [&](int t) { return t < nops ? t / OPS : GP + (t - nops) / OPS; };
+    auto slot = [&](int t) { return t < nops ? t % OPS : (t - nops) % OPS; };
+    auto sub_off = [&](int t) { return (stg(t) % DS) * (OPS * ST) + slot(t) * ST; };
+    auto last_in_stage = [&](int t) { return slot(t) == OPS - 1 || t == nops - 1 || t == 2 * nops - 1; };
+    auto wait_full = [&](int t) { const int g = stg(t); mbar_wait_u32(full_u + 8u * (g % DS), (uint32_t)(g / DS) & 1u); };
     const char *__restrict__ Pb = static_cast<const char *>(a.P);
     const char *__restrict__ tipP = static_cast<const char *>(a.tip_partials);
     const uint8_t *__restrict__ tipS = a.tip_states;
@@ -332,7 +352,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
         pre_prog = post_prog + (N - 1);
     }
     if (threadIdx.x == 0) {
-        for (int i = 0; i < D; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, K); }
+        for (int i = 0; i < DS; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, K); }
         mbar_init(post_done, K);
         mbar_init(prog_bar, 1);
         fence_mbar_init();
@@ -366,57 +386,66 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             else bulk_g2s_u32(dst, tipS + ((size_t)node * Cpad + cta_pat0 - tip_lead), tipw_bytes, bar);
         };
         auto u_src = [&](int node) -> const char * { return Ub + (size_t)(node - N) * u_node + u_cta; };
-        for (int t = 0; t < 2 * nops; ++t) {
+        // bytes and copies of step t's sub-stage:
+        //   post [op][P_k][P_a][P_b][tip a][tip b];  pre [op][P_a][P_b][-][vec a][vec b]
+        auto op_bytes = [&](int t) -> unsigned {
             const bool pre = t >= nops;
             const int m = pre ? t - nops : t;
-            PG_TSTAMP((size_t)t * 16 + 0, t);
-            if (t == nops) mbar_wait(post_done, 0);       // u of every tile stored + fenced
-            if (t >= D) mbar_wait_u32(empty_u + 8u * (t % D), (uint32_t)(t / D + 1) & 1u);
-            PG_TSTAMP((size_t)t * 16 + 1, t);
-            if (lane == 0) {
-                const uint32_t st = stages_u + (t % D) * ST;
-                const uint32_t bar = full_u + 8u * (t % D);
-                const Op4 *gprog = pre ? a.pre : a.post;           // global copy (bulk source)
-                const Op4 *prog = pre ? pre_prog : post_prog;       // smem copy when staged
-                const Op4 op = prog[m];
-                fence_proxy_async_smem();
-                if (!pre) {
-                    // [op][P_k][P_a][P_b][tip a][tip b]
-                    const unsigned bytes = 16 + (op.x != root ? MS : 0) + (op.y >= 0 ? MS + tip_bytes(op.y) : 0) +
-                                           (op.z >= 0 ? MS + tip_bytes(op.z) : 0);
-                    mbar_arrive_expect_tx_u32(bar, bytes);
-                    bulk_g2s_u32(st, gprog + m, 16, bar);
-                    if (op.x != root) bulk_g2s_u32(st + 16, Pb + (size_t)op.x * MS, MS, bar);
-                    if (op.y >= 0) {
-                        bulk_g2s_u32(st + 16 + MS, Pb + (size_t)(op.y & ~kTipPartialBit) * MS, MS, bar);
-                        copy_tip(st + 16 + 3 * MS, op.y, bar);
-                    }
-                    if (op.z >= 0) {
-                        bulk_g2s_u32(st + 16 + 2 * MS, Pb + (size_t)(op.z & ~kTipPartialBit) * MS, MS, bar);
-                        copy_tip(st + 16 + 3 * MS + VS, op.z, bar);
-                    }
-                } else {
-                    // [op][P_a][P_b][-][vec a][vec b]
-                    const int na = op.y & ~kTipPartialBit, nb = op.z & ~kTipPartialBit;
-                    const unsigned bytes = 16 + 2 * MS + (na >= N ? u_bytes : tip_bytes(op.y)) +
-                                           (nb >= N ? u_bytes : tip_bytes(op.z));
-                    mbar_arrive_expect_tx_u32(bar, bytes);
-                    bulk_g2s_u32(st, gprog + m, 16, bar);
-                    bulk_g2s_u32(st + 16, Pb + (size_t)na * MS, MS, bar);
-                    bulk_g2s_u32(st + 16 + MS, Pb + (size_t)nb * MS, MS, bar);
-                    if (na >= N) bulk_g2s_u32(st + 16 + 3 * MS, u_src(na), u_bytes, bar);
-                    else copy_tip(st + 16 + 3 * MS, op.y, bar);
-                    if (nb >= N) bulk_g2s_u32(st + 16 + 3 * MS + VS, u_src(nb), u_bytes, bar);
-                    else copy_tip(st + 16 + 3 * MS + VS, op.z, bar);
-                    if (m + PF < nops) {                         // pull later u chunks into L2
-                        const Op4 o2 = prog[m + PF];
-                        const int pa = o2.y & ~kTipPartialBit, pb = o2.z & ~kTipPartialBit;
-                        if (pa >= N) prefetch_l2(u_src(pa), u_bytes);
-                        if (pb >= N) prefetch_l2(u_src(pb), u_bytes);
-                    }
+            const Op4 op = (pre ? pre_prog : post_prog)[m];
+            if (!pre)
+                return 16 + (op.x != root ? MS : 0) + (op.y >= 0 ? MS + tip_bytes(op.y) : 0) +
+                       (op.z >= 0 ? MS + tip_bytes(op.z) : 0);
+            const int na = op.y & ~kTipPartialBit, nb = op.z & ~kTipPartialBit;
+            return 16 + 2 * MS + (na >= N ? u_bytes : tip_bytes(op.y)) + (nb >= N ? u_bytes : tip_bytes(op.z));
+        };
+        auto op_issue = [&](int t, uint32_t st, uint32_t bar) {
+            const bool pre = t >= nops;
+            const int m = pre ? t - nops : t;
+            const Op4 *gprog = pre ? a.pre : a.post;           // global copy (bulk source)
+            const Op4 *prog = pre ? pre_prog : post_prog;       // smem copy when staged
+            const Op4 op = prog[m];
+            bulk_g2s_u32(st, gprog + m, 16, bar);
+            if (!pre) {
+                if (op.x != root) bulk_g2s_u32(st + 16, Pb + (size_t)op.x * MS, MS, bar);
+                if (op.y >= 0) {
+                    bulk_g2s_u32(st + 16 + MS, Pb + (size_t)(op.y & ~kTipPartialBit) * MS, MS, bar);
+                    copy_tip(st + 16 + 3 * MS, op.y, bar);
+                }
+                if (op.z >= 0) {
+                    bulk_g2s_u32(st + 16 + 2 * MS, Pb + (size_t)(op.z & ~kTipPartialBit) * MS, MS, bar);
+                    copy_tip(st + 16 + 3 * MS + VS, op.z, bar);
+                }
+            } else {
+                const int na = op.y & ~kTipPartialBit, nb = op.z & ~kTipPartialBit;
+                bulk_g2s_u32(st + 16, Pb + (size_t)na * MS, MS, bar);
+                bulk_g2s_u32(st + 16 + MS, Pb + (size_t)nb * MS, MS, bar);
+                if (na >= N) bulk_g2s_u32(st + 16 + 3 * MS, u_src(na), u_bytes, bar);
+                else copy_tip(st + 16 + 3 * MS, op.y, bar);
+                if (nb >= N) bulk_g2s_u32(st + 16 + 3 * MS + VS, u_src(nb), u_bytes, bar);
+                else copy_tip(st + 16 + 3 * MS + VS, op.z, bar);
+                if (m + PF < nops) {                         // pull later u chunks into L2
+                    const Op4 o2 = prog[m + PF];
+                    const int pa = o2.y & ~kTipPartialBit, pb = o2.z & ~kTipPartialBit;
+                    if (pa >= N) prefetch_l2(u_src(pa), u_bytes);
+                    if (pb >= N) prefetch_l2(u_src(pb), u_bytes);
                 }
             }
-            PG_TSTAMP((size_t)t * 16 + 2, t);
+        };
+        const int NG = GP + (nops + OPS - 1) / OPS;
+        for (int g = 0; g < NG; ++g) {
+            const bool pre = g >= GP;
+            const int t0 = pre ? nops + (g - GP) * OPS : g * OPS;
+            const int t1 = min(t0 + OPS, pre ? 2 * nops : nops);
+            if (g == GP) mbar_wait(post_done, 0);            // u of every tile stored + fenced
+            if (g >= DS) mbar_wait_u32(empty_u + 8u * (g % DS), (uint32_t)(g / DS + 1) & 1u);
+            if (lane == 0) {
+                const uint32_t bar = full_u + 8u * (g % DS);
+                unsigned total = 0;
+                for (int t = t0; t < t1; ++t) total += op_bytes(t);
+                fence_proxy_async_smem();
+                mbar_arrive_expect_tx_u32(bar, total);
+                for (int t = t0; t < t1; ++t) op_issue(t, stages_u + sub_off(t), bar);
+            }
             __syncwarp();
         }
         return;
@@ -434,7 +463,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     const int pl = lane / G;
     const int pat0 = tile * TP;
     const int pat = pat0 + pl;
-    unsigned char *wsm = stages + D * ST + (size_t)warp * Cfg::warp_bytes(a.depth);
+    unsigned char *wsm = stages + DS * OPS * ST + (size_t)warp * Cfg::warp_bytes(a.depth);
     unsigned char *stackb = wsm;
     const int pi_slot = a.depth;
     double2 *nd = reinterpret_cast<double2 *>(wsm + (a.depth + 1) * 32 * VBL);     // [W][2][32]
@@ -456,9 +485,10 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     const size_t u_lane = (size_t)pat * R * VB + r * VB + h * VBL;
     unsigned char *xg = xb + (lane / LV) * Cfg::XGS;               // my group's exchange row
     auto stack_at = [&](int slot) -> unsigned char * { return stackb + (slot * 32 + lane) * VBL; };
-    auto release = [&](int t) {
+    auto release = [&](int t) {                      // after step t's last use of its stage
+        if (!last_in_stage(t)) return;
         __syncwarp();
-        if (lane == 0) mbar_arrive_u32(empty_u + 8u * (t % D));
+        if (lane == 0) mbar_arrive_u32(empty_u + 8u * (stg(t) % DS));
     };
     // the whole SP-vector of my (pattern, category) from the lanes' parts, rotated by h VL
     auto gather = [&](Real (&full)[SP], const Real (&part)[VL]) {
@@ -493,8 +523,8 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     Real prev_u[VL];
     Op4 op_next = {0, 0, 0, 0};
     if (active && nops > 0) {
-        mbar_wait(full, 0u);
-        op_next = *reinterpret_cast<const Op4 *>(stages);
+        wait_full(0);
+        op_next = *reinterpret_cast<const Op4 *>(stages + sub_off(0));
     }
     auto stack_or_fwd = [&](Real (&u)[VL], int code) {
         const int sl = -code - 1;
@@ -507,11 +537,11 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     };
     for (int t = 0; t < nops; ++t) {
         if (!active) {
-            mbar_wait_u32(full_u + 8u * (t % D), (uint32_t)(t / D) & 1u);
+            if (slot(t) == 0) wait_full(t);
             release(t);
             continue;
         }
-        const unsigned char *st = stages + (t % D) * ST;
+        const unsigned char *st = stages + sub_off(t);
         const Op4 op = op_next;
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 3, op.x);
         Real ua[VL], ub[VL];
@@ -522,8 +552,8 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 4, ua[0] + ub[VL - 1]);
         if (t + 1 < nops) {
             const int t1 = t + 1;
-            mbar_wait_u32(full_u + 8u * (t1 % D), (uint32_t)(t1 / D) & 1u);
-            op_next = *reinterpret_cast<const Op4 *>(stages + (t1 % D) * ST);
+            if (slot(t1) == 0) wait_full(t1);
+            op_next = *reinterpret_cast<const Op4 *>(stages + sub_off(t1));
         }
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 5, op_next.x);
         Real p[VL];
@@ -580,17 +610,17 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     sts_vec<Real, VL>(stack_at(pi_slot), pi);
     Op4 opn = {0, 0, 0, 0};
     if (active && nops > 0) {
-        mbar_wait(full + nops % D, (uint32_t)(nops / D) & 1u);
-        opn = *reinterpret_cast<const Op4 *>(stages + (nops % D) * ST);
+        wait_full(nops);
+        opn = *reinterpret_cast<const Op4 *>(stages + sub_off(nops));
     }
     for (int n = 0; n < nops; ++n) {
         const int t = nops + n;
         if (!active) {
-            mbar_wait_u32(full_u + 8u * (t % D), (uint32_t)(t / D) & 1u);
+            if (slot(t) == 0) wait_full(t);
             release(t);
             continue;
         }
-        const unsigned char *st = stages + (t % D) * ST;
+        const unsigned char *st = stages + sub_off(t);
         const Op4 op = opn;
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 3, op.x);
         // q_k from its stack slot (pi for the root): forwarding the previous
@@ -610,8 +640,8 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 4, q[0] + uc[0][0] + uc[1][VL - 1]);
         if (n + 1 < nops) {
             const int t1 = t + 1;
-            mbar_wait_u32(full_u + 8u * (t1 % D), (uint32_t)(t1 / D) & 1u);
-            opn = *reinterpret_cast<const Op4 *>(stages + (t1 % D) * ST);
+            if (slot(t1) == 0) wait_full(t1);
+            opn = *reinterpret_cast<const Op4 *>(stages + sub_off(t1));
         }
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 5, opn.x);
         // x_c = q o u_sibling (my states); q_c = P_c' x_c for internal children
