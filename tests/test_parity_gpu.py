@@ -107,6 +107,14 @@ def test_small_shapes(model, N, R, C):
     _compare(pb)
 
 
+@pytest.mark.parametrize("model,R", [("mmm4", 8), ("mmm2", 16), ("hky", 16)])
+def test_max_categories(model, R):
+    # lane maps at their limits: S = 16 with 8 categories (4 lanes per vector x 8
+    # categories = one pattern per warp), S = 8 / 4 with 16 categories
+    pb = ps.small_problem(21, model, R=R, C=45, seed=R, missing=0.1, simulate=True)
+    _compare(pb)
+
+
 @pytest.mark.parametrize("model", ["hky", "mmm4", "codon"])
 def test_tip_partials_nonstationary_root(model):
     pb = ps.small_problem(10, model, R=2, C=37, seed=5, partial_tips=True, stationary_root=False,
