@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between timed steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the baseline sample")
+    ap.add_argument("--virtual-shard", type=int, default=0, metavar="G",
+                    help="evidence runs only: time rank 0's pattern shard of a G-GPU run on this one GPU "
+                         "(value = that shard's evals/s; not a bench line)")
     return ap.parse_args()
 
 
@@ -217,6 +220,9 @@ def run_ours(args):
     pb = make_problem(args.config, args.precision)
     C = pb.patterns
     lo, hi = pg.shard_range(C, world, rank)
+    if args.virtual_shard > 1:
+        assert world == 1, "--virtual-shard is a single-process emulation"
+        lo, hi = pg.shard_range(C, args.virtual_shard, 0)
     inst = pg.from_problem(pb, precision=args.precision, device=local, lo=lo, hi=hi)
     stream = inst.stream
     B = 2 * pb.n_tips - 2
@@ -317,7 +323,8 @@ def run_ours(args):
                        "states": pb.states, "categories": len(pb.cat_rates),
                        "precision": args.precision,
                        "l2": "flushed (256 MiB write) between timed steps" if flush is not None else "not flushed",
-                       "parallelism": f"pattern-shard x{world}",
+                       "parallelism": f"pattern-shard x{world}" if args.virtual_shard <= 1 else
+                                      f"virtual: rank 0's shard [{lo},{hi}) of x{args.virtual_shard}, on 1 GPU",
                        "branch_lengths": "seeded +-1% jitter per step, device resident"},
             "e2e": {"value": round(e2e_rate, 3), "unit": UNIT, "h2d_bytes_per_step": 8 * B,
                     "d2h_bytes_per_step": 8 * (B + 1) + (4 if world == 1 else 0)},
@@ -333,7 +340,8 @@ def run_ours(args):
                           "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
                           "frac": round(algorithmic_flops(pb, Cl) / (trav_ms * 1e-3) / 1e12 / peaks["fp64_tflops"], 4),
                           "traffic": traffic,
-                          "kernel": "codon_post_kernel + codon_pre_kernel (all levels of one evaluation)",
+                          "kernel": ("codon_flow_kernel (post + pre order, one launch)" if info.get("flow_tiles", 0) > 0
+                                     else "codon_post_kernel + codon_pre_kernel (all levels of one evaluation)"),
                           "algorithmic_flops_per_eval": algorithmic_flops(pb, Cl), "kernel_ms": round(trav_ms, 5),
                           "hbm_algorithmic_bytes": abytes, "peak_source": peaks["fp64_src"],
                           "dtype_note": "fp64 on the FP64 tensor path (DMMA)"}),

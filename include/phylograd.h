@@ -151,6 +151,45 @@ int pg_compute(pg_instance *inst, double *log_likelihood, double *gradient);
  * Errors: PG_ERR_SEQUENCE, PG_ERR_CUDA. */
 int pg_compute_device(pg_instance *inst, double *d_out /*[2N-1]*/);
 
+/* ---- Time-tree ("clock") parameterisation of the branch lengths ----------
+ * a branch length "can ... be the difference between the
+ * parent and child node heights measured in time-units multiplied by a
+ * (possibly branch-specific) evolutionary rate scalar":
+ *     b_i = rho_i * tau_i,   tau_i = h_parent(i) - h_i,   i = 0..2N-3.
+ * The gradient w.r.t. these parameters is the chain rule on g = dlogL/db
+ * (HMC over rate scalars and node heights,
+ * P:967-968; strict clock "reduce the partial derivatives across a set of
+ * branches").  Node numbering and parents come from the operation
+ * list (pg_set_operations must have been called).
+ *
+ * pg_set_node_heights: host heights [2N-1] (tips may be non-zero: serially
+ * sampled data) and rate scalars [2N-2] (NULL = all 1), validated
+ * (h_parent >= h_child, rho >= 0, finite; else PG_ERR_DOMAIN), copied, and
+ * b is formed on the device inside the next compute.
+ * pg_set_node_heights_device: the same from DEVICE pointers, stream-ordered,
+ * no validation (a child above its parent yields b < 0: undefined results).
+ * Both replace any branch lengths set before. */
+int pg_set_node_heights(pg_instance *inst, const double *heights /*[2N-1]*/, const double *rates /*[2N-2]*/);
+int pg_set_node_heights_device(pg_instance *inst, const double *d_heights, const double *d_rates);
+
+/* Branch sets for clock-rate sums: set_of_branch[i] in -1..n_sets-1 (-1 = in
+ * no set), 1 <= n_sets <= 2N-2.  Default (never called): one set holding
+ * every branch, i.e. the strict clock b_i = r tau_i.  Errors: PG_ERR_ARG. */
+int pg_set_branch_sets(pg_instance *inst, const int32_t *set_of_branch /*[2N-2]*/, int32_t n_sets);
+
+/* Chain rule on the device, on the instance stream, from d_out = [logL, g]
+ * as written by pg_compute_device (after any allreduce), using the heights
+ * and rates of the last pg_set_node_heights[_device]:
+ *   d_grad_rates[i]   = dlogL/drho_i = tau_i g_i                    [2N-2]
+ *   d_grad_heights[k] = dlogL/dh_k   = sum_{c: parent(c) = k} rho_c g_c
+ *                                      - [k != root] rho_k g_k       [2N-1]
+ *   d_set_sums[s]     = sum_{i in set s} tau_i g_i   (= dlogL/dr for
+ *                       b_i = r tau_i on the set, fixed-order sum)  [n_sets]
+ * Any output may be NULL (skipped).  Device pointers, caller-owned.
+ * Errors: PG_ERR_ARG, PG_ERR_SEQUENCE (no heights set), PG_ERR_CUDA. */
+int pg_clock_gradient_device(pg_instance *inst, const double *d_out, double *d_grad_rates,
+                             double *d_grad_heights, double *d_set_sums);
+
 /* Synchronise the stream and report the first zero-likelihood pattern of the
  * most recent evaluation (-1 if none).  Returns PG_ERR_ZERO_LIKELIHOOD if
  * one occurred. */
@@ -176,7 +215,11 @@ typedef struct {
     int32_t smem_bytes;              /* dynamic shared memory per CTA      */
     int32_t prefetch_depth;          /* pre-order prefetch ring stages     */
     int32_t padded_patterns;         /* C rounded up to the CTA tile       */
-    int32_t kernel_variant;          /* 0 = small-S, 1 = large-S           */
+    int32_t kernel_variant;          /* 0 = small-S, 1 = large-S SIMT,
+                                        2 = codon FP64 tensor path        */
+    int32_t flow_tiles;              /* codon: 32-pattern tiles per item of
+                                        the one-launch dataflow schedule;
+                                        0 = one launch per tree level     */
 } pg_plan_info;
 int pg_get_plan_info(const pg_instance *inst, pg_plan_info *info);
 

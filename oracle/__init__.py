@@ -176,3 +176,75 @@ def grad_quadratic(pb, lo: int = 0, hi: int | None = None):
     if rc < 0:
         raise ValueError(f"oracle_grad_quadratic failed ({rc})")
     return g
+
+
+# ---------------------------------------------------------------------------
+# Time-tree ("clock") parameterisation, SURVEY §8(f) NEXT-1 and C23.
+# "Each branch length b_i ... can ... be the difference
+# between the parent and child node heights measured in time-units multiplied
+# by a (possibly branch-specific) evolutionary rate scalar":
+#     b_i = rho_i * (h_parent(i) - h_i).
+# for a strict clock "further reduce the partial derivatives across
+# a set of branches and report a single value".  The gradients below are the
+# chain rule written out term by term; pinned in tests/test_oracle_pins.py by
+# central finite differences of logL in h, rho and a global clock rate, and
+# by the scaling identity sum_k h_k dlogL/dh_k = sum_i b_i g_i.
+# ---------------------------------------------------------------------------
+
+def parents(N: int, ops) -> np.ndarray:
+    """parent[v] of every node (-1 for the root) from the post-order op list."""
+    par = np.full(2 * N - 1, -1, dtype=np.int64)
+    for d, a, b in np.asarray(ops).reshape(-1, 3):
+        par[a] = d
+        par[b] = d
+    return par
+
+
+def clock_branch_lengths(N: int, ops, heights, rates=None) -> np.ndarray:
+    """b_i = rho_i (h_parent(i) - h_i), i = 0..2N-3 (P:199-200)."""
+    par = parents(N, ops)
+    B = 2 * N - 2
+    b = np.zeros(B)
+    for i in range(B):
+        rho = 1.0 if rates is None else rates[i]
+        b[i] = rho * (heights[par[i]] - heights[i])
+    return b
+
+
+def clock_gradient(N: int, ops, heights, rates, g, set_of_branch=None, n_sets: int = 1):
+    """Chain rule of logL(b(h, rho)) from g = dlogL/db:
+      dlogL/drho_i = (h_parent(i) - h_i) g_i
+      dlogL/dh_k   = sum over children c of k: rho_c g_c   (b_c grows with h_k)
+                     - rho_k g_k if k is not the root      (b_k shrinks)
+      set sums     = sum over branches i of set s of (h_parent(i) - h_i) g_i
+                     (= dlogL/dr for b_i = r tau_i on that set).
+    Also returns the condition-aware magnitudes (same sums of |terms|, with
+    `g_abs` in place of g when given via g=(g, g_abs))."""
+    g_abs = None
+    if isinstance(g, tuple):
+        g, g_abs = g
+    par = parents(N, ops)
+    B = 2 * N - 2
+    rho = np.ones(B) if rates is None else np.asarray(rates, float)
+    sets = np.zeros(B, dtype=np.int64) if set_of_branch is None else np.asarray(set_of_branch)
+    d_rho = np.zeros(B)
+    d_h = np.zeros(2 * N - 1)
+    s_sum = np.zeros(n_sets)
+    a_rho, a_h, a_s = np.zeros(B), np.zeros(2 * N - 1), np.zeros(n_sets)
+    for i in range(B):
+        tau = heights[par[i]] - heights[i]
+        d_rho[i] = tau * g[i]
+        d_h[par[i]] += rho[i] * g[i]
+        d_h[i] -= rho[i] * g[i]
+        if sets[i] >= 0:
+            s_sum[sets[i]] += tau * g[i]
+        if g_abs is not None:
+            a_rho[i] = abs(tau) * g_abs[i]
+            a_h[par[i]] += abs(rho[i]) * g_abs[i]
+            a_h[i] += abs(rho[i]) * g_abs[i]
+            if sets[i] >= 0:
+                a_s[sets[i]] += abs(tau) * g_abs[i]
+    out = dict(grad_rates=d_rho, grad_heights=d_h, set_sums=s_sum)
+    if g_abs is not None:
+        out.update(abs_rates=a_rho, abs_heights=a_h, abs_sets=a_s)
+    return out

@@ -47,7 +47,8 @@ class PgConfig(ctypes.Structure):
 
 class PgPlanInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("post_depth", "pre_depth", "grid", "block", "smem_bytes",
-                                              "prefetch_depth", "padded_patterns", "kernel_variant")]
+                                              "prefetch_depth", "padded_patterns", "kernel_variant",
+                                              "flow_tiles")]
 
 
 _vp = ctypes.c_void_p
@@ -69,6 +70,10 @@ _SIGS = {
     "pg_set_operations": ([_vp, _ip, ctypes.c_int32], ctypes.c_int),
     "pg_set_branch_lengths": ([_vp, _dp], ctypes.c_int),
     "pg_set_branch_lengths_device": ([_vp, _vp], ctypes.c_int),
+    "pg_set_node_heights": ([_vp, _dp, _dp], ctypes.c_int),
+    "pg_set_node_heights_device": ([_vp, _vp, _vp], ctypes.c_int),
+    "pg_set_branch_sets": ([_vp, _ip, ctypes.c_int32], ctypes.c_int),
+    "pg_clock_gradient_device": ([_vp, _vp, _vp, _vp, _vp], ctypes.c_int),
     "pg_compute": ([_vp, _dp, _dp], ctypes.c_int),
     "pg_compute_device": ([_vp, _vp], ctypes.c_int),
     "pg_check_status": ([_vp, _ip], ctypes.c_int),
@@ -212,6 +217,56 @@ class Instance:
         """t: a CUDA float64 tensor of 2N-2 branch lengths (stream-ordered copy)."""
         assert t.dtype == self.torch.float64 and t.is_cuda and t.numel() == self.n_branches
         self._check(_lib.pg_set_branch_lengths_device(self._h, _vp(t.data_ptr())), "set_branch_lengths_device")
+
+    # -- time-tree parameterisation (include/phylograd.h, P:199-200) --------
+    def set_node_heights(self, heights, rates=None):
+        """b_i = rho_i (h_parent(i) - h_i) from host heights [2N-1] and rate
+        scalars [2N-2] (None = all 1); validated and copied."""
+        r = None if rates is None else _f64(rates)
+        self._check(_lib.pg_set_node_heights(self._h, _dptr(_f64(heights)), _dptr(r) if r is not None else None),
+                    "set_node_heights")
+
+    def set_node_heights_device(self, h, rates=None):
+        """Same from CUDA float64 tensors (stream-ordered, not validated)."""
+        assert h.dtype == self.torch.float64 and h.is_cuda and h.numel() == self.n_branches + 1
+        if rates is not None:
+            assert rates.dtype == self.torch.float64 and rates.is_cuda and rates.numel() == self.n_branches
+        self._check(_lib.pg_set_node_heights_device(self._h, _vp(h.data_ptr()),
+                                                    _vp(rates.data_ptr()) if rates is not None else None),
+                    "set_node_heights_device")
+
+    def set_branch_sets(self, set_of_branch, n_sets: int):
+        s = np.ascontiguousarray(set_of_branch, dtype=np.int32)
+        self._check(_lib.pg_set_branch_sets(self._h, s.ctypes.data_as(_ip), int(n_sets)), "set_branch_sets")
+
+    def clock_gradient_device(self, out, grad_rates=None, grad_heights=None, set_sums=None):
+        """Chain rule on the device from out = [logL, g] (compute_device's
+        output): dlogL/drho [2N-2], dlogL/dh [2N-1], branch-set sums; any
+        output tensor may be None."""
+        def ptr(t):
+            return None if t is None else _vp(t.data_ptr())
+        self._check(_lib.pg_clock_gradient_device(self._h, _vp(out.data_ptr()), ptr(grad_rates),
+                                                  ptr(grad_heights), ptr(set_sums)), "clock_gradient_device")
+
+    def clock_gradient(self, n_sets: int = 1):
+        """Synchronous evaluation in the time-tree parameterisation: returns
+        (logL, g, dlogL/drho, dlogL/dh, set sums) as host arrays."""
+        torch = self.torch
+        dev = torch.device("cuda", self.device)
+        B = self.n_branches
+        out = torch.empty(B + 1, dtype=torch.float64, device=dev)
+        gr = torch.empty(B, dtype=torch.float64, device=dev)
+        gh = torch.empty(B + 1, dtype=torch.float64, device=dev)
+        ss = torch.empty(n_sets, dtype=torch.float64, device=dev)
+        with torch.cuda.stream(self.stream):
+            self.compute_device(out)
+            self.clock_gradient_device(out, gr, gh, ss)
+        self.stream.synchronize()
+        zp = self.check_status()
+        if zp >= 0:
+            raise PhyloGradError(PG_ERR_ZERO_LIKELIHOOD, f"zero likelihood at pattern {zp}")
+        o = out.cpu().numpy()
+        return o[0], o[1:], gr.cpu().numpy(), gh.cpu().numpy(), ss.cpu().numpy()
 
     # -- evaluation ----------------------------------------------------------
     def compute(self, gradient: bool = True):

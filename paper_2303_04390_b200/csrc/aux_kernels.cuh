@@ -56,3 +56,68 @@ __global__ void __launch_bounds__(256) reduce_kernel(const double *__restrict__ 
 }
 
 }  // namespace pg
+
+namespace pg {
+
+// ---- time-tree (clock) parameterisation, SURVEY §8(f) NEXT-1 / C23 ---------
+// b_i = rho_i (h_parent(i) - h_i).  One thread per node: copies
+// the heights and rate scalars into the instance (src may equal dst; rho_src
+// NULL = all 1) and forms b for the 2N-2 branches.
+__global__ void __launch_bounds__(256) clock_bl_kernel(const int *__restrict__ parent, const double *h_src,
+                                                       const double *rho_src, int N, double *h_dst,
+                                                       double *rho_dst, double *__restrict__ bl) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int B = 2 * N - 2;
+    if (i > B) return;
+    const double hi = h_src[i];
+    if (i < B) {
+        const double r = rho_src ? rho_src[i] : 1.0;
+        const double tau = h_src[parent[i]] - hi;
+        bl[i] = r * tau;
+        rho_dst[i] = r;
+    }
+    h_dst[i] = hi;
+}
+
+// Chain rule on g = out[1..2N-2] (out[0] = logL), one thread per node k:
+//   dlogL/drho_k = tau_k g_k;
+//   dlogL/dh_k   = sum over children c of rho_c g_c (tau_c grows with h_k)
+//                  - rho_k g_k (tau_k shrinks), the root having no branch.
+__global__ void __launch_bounds__(256) clock_grad_kernel(const int *__restrict__ parent, const int *__restrict__ ca,
+                                                         const int *__restrict__ cb, const double *__restrict__ h,
+                                                         const double *__restrict__ rho, int N,
+                                                         const double *__restrict__ out, double *grad_rho,
+                                                         double *grad_h) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int B = 2 * N - 2;
+    if (k > B) return;
+    const double *g = out + 1;
+    const double own = k < B ? rho[k] * g[k] : 0.0;
+    if (grad_rho && k < B) grad_rho[k] = (h[parent[k]] - h[k]) * g[k];
+    if (grad_h) {
+        double d = 0.0;
+        if (k >= N) d = rho[ca[k]] * g[ca[k]] + rho[cb[k]] * g[cb[k]];
+        grad_h[k] = d - own;
+    }
+}
+
+// Set sums sum_{i in set s} tau_i g_i: one CTA per set, fixed-order strided
+// sums then a fixed shared-memory tree (deterministic, no atomics).
+__global__ void __launch_bounds__(256) clock_set_kernel(const int *__restrict__ parent, const double *__restrict__ h,
+                                                        const int *__restrict__ bset, int N,
+                                                        const double *__restrict__ out, double *set_sums) {
+    __shared__ double sh[256];
+    const int s = blockIdx.x, B = 2 * N - 2;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < B; i += blockDim.x)
+        if (bset[i] == s) acc += (h[parent[i]] - h[i]) * out[1 + i];
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) set_sums[s] = sh[0];
+}
+
+}  // namespace pg

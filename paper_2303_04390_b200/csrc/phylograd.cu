@@ -11,6 +11,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -38,7 +39,10 @@ struct Layout {
         off_post, off_pre, total;
     // codon (variant 2) extras
     size_t off_PBpre = 0, off_DT = 0, off_PONE = 0, off_QB = 0, off_q = 0, off_E = 0, off_child = 0,
-           off_levels = 0, off_lev4 = 0, off_tipmode = 0, off_VA = 0, off_ViB = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0;
+           off_levels = 0, off_lev4 = 0, off_tipmode = 0, off_VA = 0, off_ViB = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0,
+           off_flow = 0, flow_bytes = 0, reset_bytes = 0;
+    // time-tree parameterisation: parent/child_a/child_b [3][2N-1], heights, rate scalars, branch sets
+    size_t off_tree = 0, off_h = 0, off_rho = 0, off_bset = 0;
 };
 
 int padded_states(int S) {
@@ -124,11 +128,20 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
     L->off_status = take(sizeof(int) * 4);
     L->off_post = take((size_t)(N - 1) * sizeof(Op4));
     L->off_pre = take((size_t)(N - 1) * sizeof(Op4));
+    L->off_tree = take((size_t)3 * (2 * N - 1) * 4);
+    L->off_h = take((size_t)(2 * N - 1) * 8);
+    L->off_rho = take((size_t)(2 * N - 2) * 8);
+    L->off_bset = take((size_t)(2 * N - 2) * 4);     // zeroed at create: one set (strict clock)
     if (L->variant == 2) {
         L->off_q = take((size_t)(N - 2) * R * L->Cpad * SP * 8);
         L->off_E = take((size_t)(N - 1) * L->Cpad * 4);
-        L->off_fmax = take((size_t)(2 * N - 3) * L->Cpad * 4);     // fmax [N-1] then qmax [N-2] (one memset)
+        // fmax [N-1], qmax [N-2], then the flow schedule's counters
+        // {item counter, rpost [N-1][<= ntiles], rpre [N-1][<= ntiles]}: one memset
+        L->flow_bytes = ((size_t)32 + (size_t)2 * (N - 1) * L->n_tiles) * 4;
+        L->reset_bytes = (size_t)(2 * N - 3) * L->Cpad * 4 + L->flow_bytes;
+        L->off_fmax = take(L->reset_bytes);
         L->off_qmax = L->off_fmax + (size_t)(N - 1) * L->Cpad * 4;
+        L->off_flow = L->off_qmax + (size_t)(N - 2) * L->Cpad * 4;
         L->off_numden = take((size_t)L->B * R * L->Cpad * 16);
         L->off_Lpart = take((size_t)R * L->Cpad * 8);
         L->off_child = take((size_t)2 * (2 * N - 1) * 4);
@@ -175,8 +188,12 @@ struct pg_instance {
     double *bl_pinned = nullptr, *out_pinned = nullptr;
     int *status_pinned = nullptr;
     bool bl_host_pending = false;
+    double *clock_pinned = nullptr;     // [2N-1] heights then [2N-2] rate scalars
+    bool clock_host_pending = false, have_heights = false;
+    int n_sets = 1;
     // launch configuration
     int prefetch = 4, smem = 0, grid = 0, block = 0, tiles_per_cta = 1, prog_smem_off = 0;
+    int flow_tch = 0;                   // codon: tiles per flow item (0 = level-by-level kernels)
     cudaGraphExec_t gexec = nullptr;
     double *gexec_out = nullptr;
     bool timing = false;
@@ -257,7 +274,8 @@ int pg_create(const pg_config *cfg, void *cuda_stream, void *dev_workspace, size
     }
     if (cudaMallocHost((void **)&inst->bl_pinned, sizeof(double) * L.B) != cudaSuccess ||
         cudaMallocHost((void **)&inst->out_pinned, sizeof(double) * (L.B + 1)) != cudaSuccess ||
-        cudaMallocHost((void **)&inst->status_pinned, sizeof(int) * 4) != cudaSuccess)
+        cudaMallocHost((void **)&inst->status_pinned, sizeof(int) * 4) != cudaSuccess ||
+        cudaMallocHost((void **)&inst->clock_pinned, sizeof(double) * (2 * L.B + 1)) != cudaSuccess)
         return bail(PG_ERR_MEMORY);
     const int N = cfg->tips;
     inst->tips_h.assign((size_t)N * L.Cpad, (uint8_t)cfg->states);   // all missing
@@ -276,6 +294,7 @@ int pg_destroy(pg_instance *inst) {
     for (auto &e : inst->ev) if (e) cudaEventDestroy(e);
     if (inst->own_ws && inst->ws) cudaFree(inst->ws);
     if (inst->bl_pinned) cudaFreeHost(inst->bl_pinned);
+    if (inst->clock_pinned) cudaFreeHost(inst->clock_pinned);
     if (inst->out_pinned) cudaFreeHost(inst->out_pinned);
     if (inst->status_pinned) cudaFreeHost(inst->status_pinned);
     if (inst->own_stream && inst->stream) cudaStreamDestroy(inst->stream);
@@ -442,6 +461,109 @@ int pg_set_operations(pg_instance *inst, const int32_t *ops, int32_t n_ops) {
     inst->plan = std::move(p);
     inst->have_ops = true;
     inst->plan_dirty = true;
+    // parent / children of every node for the time-tree parameterisation
+    const int N = inst->cfg.tips, nn = 2 * N - 1;
+    std::vector<int32_t> tree(3 * (size_t)nn, -1);
+    for (int v = N; v < nn; ++v) {
+        const int a = inst->plan.child_a[v], b = inst->plan.child_b[v];
+        tree[nn + v] = a;
+        tree[2 * nn + v] = b;
+        tree[a] = v;
+        tree[b] = v;
+    }
+    CK(cudaMemcpyAsync(inst->ws + inst->L.off_tree, tree.data(), tree.size() * 4, cudaMemcpyHostToDevice, inst->stream),
+       "tree upload");
+    CK(cudaStreamSynchronize(inst->stream), "tree upload sync");
+    inst->have_heights = false;
+    return PG_OK;
+}
+
+// ---- time-tree parameterisation (b_i = rho_i (h_parent(i) - h_i))
+static int launch_clock_bl(pg_instance *inst, const double *h_src, const double *rho_src) {
+    const Layout &L = inst->L;
+    const int N = inst->cfg.tips;
+    const int *parent = inst->at<int>(L.off_tree);
+    double *h = inst->at<double>(L.off_h), *rho = inst->at<double>(L.off_rho), *bl = inst->at<double>(L.off_bl);
+    pg::clock_bl_kernel<<<(2 * N - 1 + 255) / 256, 256, 0, inst->stream>>>(parent, h_src, rho_src, N, h, rho, bl);
+    CK(cudaGetLastError(), "clock_bl launch");
+    return PG_OK;
+}
+
+int pg_set_node_heights(pg_instance *inst, const double *heights, const double *rates) {
+    if (!inst || !heights) return PG_ERR_ARG;
+    if (!inst->have_ops) return inst->fail(PG_ERR_SEQUENCE, "operations not set (node parents unknown)");
+    const int N = inst->cfg.tips, B = inst->L.B;
+    if (!finite_all(heights, 2 * N - 1)) return inst->fail(PG_ERR_DOMAIN, "node heights must be finite");
+    for (int v = N; v < 2 * N - 1; ++v)
+        for (int c : {inst->plan.child_a[v], inst->plan.child_b[v]})
+            if (!(heights[v] >= heights[c]))
+                return inst->fail(PG_ERR_DOMAIN, "node " + std::to_string(c) + " is above its parent " + std::to_string(v));
+    if (rates)
+        for (int i = 0; i < B; ++i)
+            if (!(rates[i] >= 0.0) || !std::isfinite(rates[i]))
+                return inst->fail(PG_ERR_DOMAIN, "rate scalar " + std::to_string(i) + " is negative or not finite");
+    std::memcpy(inst->clock_pinned, heights, sizeof(double) * (2 * N - 1));
+    for (int i = 0; i < B; ++i) inst->clock_pinned[2 * N - 1 + i] = rates ? rates[i] : 1.0;
+    inst->clock_host_pending = true;
+    inst->bl_host_pending = false;
+    inst->have_bl = inst->have_heights = true;
+    return PG_OK;
+}
+
+int pg_set_node_heights_device(pg_instance *inst, const double *d_heights, const double *d_rates) {
+    if (!inst || !d_heights) return PG_ERR_ARG;
+    if (!inst->have_ops) return inst->fail(PG_ERR_SEQUENCE, "operations not set (node parents unknown)");
+    int rc = launch_clock_bl(inst, d_heights, d_rates);
+    if (rc) return rc;
+    inst->clock_host_pending = inst->bl_host_pending = false;
+    inst->have_bl = inst->have_heights = true;
+    return PG_OK;
+}
+
+// host heights/rates staged by pg_set_node_heights -> device, then b (stream-ordered)
+static int flush_clock_host(pg_instance *inst) {
+    if (!inst->clock_host_pending) return PG_OK;
+    const Layout &L = inst->L;
+    const int N = inst->cfg.tips;
+    CK(cudaMemcpyAsync(inst->ws + L.off_h, inst->clock_pinned, sizeof(double) * (2 * N - 1), cudaMemcpyHostToDevice,
+                       inst->stream), "heights H2D");
+    CK(cudaMemcpyAsync(inst->ws + L.off_rho, inst->clock_pinned + 2 * N - 1, sizeof(double) * L.B,
+                       cudaMemcpyHostToDevice, inst->stream), "rates H2D");
+    return launch_clock_bl(inst, inst->at<double>(L.off_h), inst->at<double>(L.off_rho));
+}
+
+int pg_set_branch_sets(pg_instance *inst, const int32_t *set_of_branch, int32_t n_sets) {
+    if (!inst || !set_of_branch) return PG_ERR_ARG;
+    const int B = inst->L.B;
+    if (n_sets < 1 || n_sets > B) return inst->fail(PG_ERR_ARG, "n_sets must be in 1..2N-2");
+    for (int i = 0; i < B; ++i)
+        if (set_of_branch[i] < -1 || set_of_branch[i] >= n_sets)
+            return inst->fail(PG_ERR_ARG, "branch " + std::to_string(i) + ": set id out of range");
+    CK(cudaMemcpyAsync(inst->ws + inst->L.off_bset, set_of_branch, sizeof(int32_t) * B, cudaMemcpyHostToDevice,
+                       inst->stream), "branch sets upload");
+    CK(cudaStreamSynchronize(inst->stream), "branch sets sync");
+    inst->n_sets = n_sets;
+    return PG_OK;
+}
+
+int pg_clock_gradient_device(pg_instance *inst, const double *d_out, double *d_grad_rates, double *d_grad_heights,
+                             double *d_set_sums) {
+    if (!inst || !d_out) return PG_ERR_ARG;
+    if (!inst->have_heights) return inst->fail(PG_ERR_SEQUENCE, "node heights not set");
+    const Layout &L = inst->L;
+    const int N = inst->cfg.tips;
+    const int *tree = inst->at<int>(L.off_tree);
+    const double *h = inst->at<double>(L.off_h), *rho = inst->at<double>(L.off_rho);
+    if (d_grad_rates || d_grad_heights) {
+        pg::clock_grad_kernel<<<(2 * N - 1 + 255) / 256, 256, 0, inst->stream>>>(
+            tree, tree + (2 * N - 1), tree + 2 * (2 * N - 1), h, rho, N, d_out, d_grad_rates, d_grad_heights);
+        CK(cudaGetLastError(), "clock_grad launch");
+    }
+    if (d_set_sums) {
+        pg::clock_set_kernel<<<inst->n_sets, 256, 0, inst->stream>>>(tree, h, inst->at<int>(L.off_bset), N, d_out,
+                                                                     d_set_sums);
+        CK(cudaGetLastError(), "clock_set launch");
+    }
     return PG_OK;
 }
 
@@ -453,6 +575,7 @@ int pg_set_branch_lengths(pg_instance *inst, const double *b) {
             return inst->fail(PG_ERR_DOMAIN, "branch length " + std::to_string(i) + " is negative or not finite");
     std::memcpy(inst->bl_pinned, b, sizeof(double) * B);
     inst->bl_host_pending = true;
+    inst->clock_host_pending = false;
     inst->have_bl = true;
     return PG_OK;
 }
@@ -461,7 +584,7 @@ int pg_set_branch_lengths_device(pg_instance *inst, const double *d_b) {
     if (!inst || !d_b) return PG_ERR_ARG;
     CK(cudaMemcpyAsync(inst->ws + inst->L.off_bl, d_b, sizeof(double) * inst->L.B, cudaMemcpyDeviceToDevice,
                        inst->stream), "branch lengths D2D");
-    inst->bl_host_pending = false;
+    inst->bl_host_pending = inst->clock_host_pending = false;
     inst->have_bl = true;
     return PG_OK;
 }
@@ -584,6 +707,22 @@ static int configure(pg_instance *inst) {
                                 (int)pg::codon::pre_smem()), "smem attr");
         CK(cudaFuncSetAttribute((void *)pg::codon::codon_pmat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)pg::codon::pmat_smem()), "smem attr");
+        CK(cudaFuncSetAttribute((void *)pg::codon::codon_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pg::codon::flow_smem()), "smem attr");
+        // flow schedule (default): chunks of TCH tiles per item, enough items
+        // per node that a level of a few nodes still fills the 3 CTAs/SM
+        const char *fe = getenv("PG_CODON_FLOW"), *te = getenv("PG_FLOW_TCH");
+        if (fe && atoi(fe) == 0) {
+            inst->flow_tch = 0;
+        } else if (te && atoi(te) > 0) {
+            inst->flow_tch = std::min(atoi(te), L.n_tiles);
+        } else {
+            // measured (profiles/r01/flow_sweep.jsonl): 2 tiles per item once a
+            // node alone fills the CTA slots (WNV 2.47 -> 2.38 ms), else 1
+            // (8-way shards: yeast 0.288 -> 0.261 ms, WNV 0.714 -> 0.702 ms)
+            const int slots = 3 * inst->sm_count;
+            inst->flow_tch = L.n_tiles * R >= slots ? 2 : 1;
+        }
         return PG_OK;
     } else {
         inst->block = L.tpl * R * (L.SP / 4);
@@ -735,8 +874,23 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         pg::codon::CodonArgs c = codon_args(inst);
         const auto &pl = inst->plan;
         const int N = inst->cfg.tips;
-        CK(cudaMemsetAsync(inst->ws + L.off_fmax, 0, (size_t)(2 * N - 3) * L.Cpad * 4, inst->stream), "fmax reset");
-        for (size_t i = 0; i + 1 < pl.post_off.size(); ++i) {
+        CK(cudaMemsetAsync(inst->ws + L.off_fmax, 0, L.reset_bytes, inst->stream), "fmax/flow reset");
+        if (inst->flow_tch > 0) {
+            pg::codon::FlowArgs f{};
+            f.ctr = inst->at<int>(L.off_flow);
+            f.tch = inst->flow_tch;
+            f.nch = (L.n_tiles + f.tch - 1) / f.tch;
+            f.rpost = f.ctr + 32;
+            f.rpre = f.rpost + (size_t)(N - 1) * f.nch;
+            f.npost = pl.post_off.back();
+            f.ntask = (int)pl.level_nodes.size();
+            void *args[] = {&c, &f};
+            const int items = f.ntask * R * f.nch;
+            CK(cudaLaunchKernel((void *)pg::codon::codon_flow_kernel, dim3(std::min(items, 3 * inst->sm_count)),
+                                dim3(pg::codon::NT), args, pg::codon::flow_smem(), inst->stream),
+               "codon flow launch");
+        }
+        for (size_t i = 0; inst->flow_tch == 0 && i + 1 < pl.post_off.size(); ++i) {
             int off = pl.post_off[i], cnt = pl.post_off[i + 1] - off;
             // persistent: 3 CTAs per SM walk the level's items; narrow levels
             // (fewer full-tile items than ~2 waves) use half-tile items
@@ -748,7 +902,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
                                 pg::codon::post_smem() + 16 * (size_t)cnt, inst->stream),
                "codon post launch");
         }
-        for (size_t i = 0; i + 1 < pl.pre_off.size(); ++i) {
+        for (size_t i = 0; inst->flow_tch == 0 && i + 1 < pl.pre_off.size(); ++i) {
             int off = pl.pre_off[i], cnt = pl.pre_off[i + 1] - off;
             void *args[] = {&c, &off};
             CK(cudaLaunchKernel((void *)pg::codon::codon_pre_kernel, dim3(L.n_tiles, cnt, R), dim3(pg::codon::NT), args,
@@ -831,6 +985,8 @@ int pg_compute_device(pg_instance *inst, double *d_out) {
                            cudaMemcpyHostToDevice, inst->stream), "branch lengths H2D");
         inst->bl_host_pending = false;
     }
+    if ((rc = flush_clock_host(inst))) return rc;
+    inst->clock_host_pending = false;
     return launch_eval(inst, d_out);
 }
 
@@ -844,6 +1000,7 @@ int pg_compute(pg_instance *inst, double *log_likelihood, double *gradient) {
                            inst->stream), "branch lengths H2D");
         // host branch lengths stay "pending": every pg_compute re-uploads them
     }
+    if ((rc = flush_clock_host(inst))) return rc;      // likewise host heights / rate scalars
     double *d_out = inst->at<double>(L.off_out);
     if ((rc = launch_eval(inst, d_out))) return rc;
     CK(cudaMemcpyAsync(inst->out_pinned, d_out, sizeof(double) * (L.B + 1), cudaMemcpyDeviceToHost, inst->stream),
@@ -907,8 +1064,8 @@ extern "C" int pg_trace_copy(pg_instance *inst, long long *host, int n) {
 int pg_kernels_per_eval(const pg_instance *inst, int32_t *n) {
     if (!inst || !n) return PG_ERR_ARG;
     *n = 3;   // pmat, traverse, reduce
-    if (inst->L.variant == 2)   // pmat + one launch per post level + per pre level + reduce
-        *n = 2 + (int32_t)(inst->plan.post_off.size() - 1) + (int32_t)(inst->plan.pre_off.size() - 1);
+    if (inst->L.variant == 2)   // pmat + (one flow launch | one launch per post level + per pre level) + reduce
+        *n = 2 + (inst->flow_tch > 0 ? 1 : (int32_t)(inst->plan.post_off.size() - 1) + (int32_t)(inst->plan.pre_off.size() - 1));
     return PG_OK;
 }
 
@@ -922,5 +1079,11 @@ int pg_get_plan_info(const pg_instance *inst, pg_plan_info *info) {
     info->prefetch_depth = inst->prefetch;
     info->padded_patterns = inst->L.Cpad;
     info->kernel_variant = inst->L.variant;
+    info->flow_tiles = inst->flow_tch;
+    if (inst->L.variant == 2 && inst->flow_tch > 0) {
+        const int nch = (inst->L.n_tiles + inst->flow_tch - 1) / inst->flow_tch;
+        info->grid = std::min((int)inst->plan.level_nodes.size() * inst->cfg.categories * nch, 3 * inst->sm_count);
+        info->smem_bytes = (int)pg::codon::flow_smem();
+    }
     return PG_OK;
 }

@@ -160,7 +160,7 @@ __device__ __forceinline__ double pow2neg(int e) { return __longlong_as_double((
 
 // per-pattern scale of a child tile (1 for tips)
 __device__ __forceinline__ void child_scale(double *sc, const CodonArgs &a, int child, const int *mx, int pat0) {
-    if (threadIdx.x < T) sc[threadIdx.x] = child >= a.N ? pow2neg(lazy_exp(mx[(size_t)(child - a.N) * a.Cpad + pat0 + threadIdx.x])) : 1.0;
+    if (threadIdx.x < T) sc[threadIdx.x] = child >= a.N ? pow2neg(lazy_exp(__ldcg(mx + (size_t)(child - a.N) * a.Cpad + pat0 + threadIdx.x))) : 1.0;
 }
 
 // ---------------------------------------------------------------------------
@@ -257,18 +257,12 @@ __device__ __forceinline__ double child_sc(const CodonArgs &a, int child, const 
     return child >= a.N ? pow2neg(lazy_exp(fm[m])) : 1.0;
 }
 
+// Items [beg, end) of a level whose node table `tab` is in shared memory.
 template <int MH>
-__global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, int level_off, int cnt) {
+__device__ __forceinline__ void post_range(const CodonArgs &a, const int4 *tab, int beg, int end, unsigned char *smem_c) {
     constexpr int TI = 8 * MH;               // patterns per item
-    extern __shared__ __align__(16) unsigned char smem_c[];
-    const int nitems = cnt * a.R * a.ntiles * (4 / MH);
-    int4 *tab = reinterpret_cast<int4 *>(smem_c + post_smem());
-    stage_level(tab, a, level_off, cnt);
-    __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int root = 2 * a.N - 2;
-    const int per = (nitems + gridDim.x - 1) / gridDim.x;
-    const int beg = blockIdx.x * per, end = min(nitems, beg + per);
     auto stage_A = [&](int s) { return reinterpret_cast<double *>(smem_c + (size_t)s * PSTAGE); };
     auto stage_B = [&](int s) { return reinterpret_cast<double *>(smem_c + (size_t)s * PSTAGE) + TILE; };
     auto stage_F = [&](int s) { return reinterpret_cast<int *>(smem_c + (size_t)s * PSTAGE + 2 * TILE * 8); };
@@ -314,8 +308,8 @@ __global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, in
         if (r == 0 && threadIdx.x < TI) {    // cumulative exponent inside u_k (and at the root)
             const int m = threadIdx.x;
             int Ek = 0;
-            if (ca >= a.N) Ek += a.E[(size_t)(ca - a.N) * a.Cpad + pat0 + m] + lazy_exp(fa[m]);
-            if (cb >= a.N) Ek += a.E[(size_t)(cb - a.N) * a.Cpad + pat0 + m] + lazy_exp(fb[m]);
+            if (ca >= a.N) Ek += __ldcg(a.E + (size_t)(ca - a.N) * a.Cpad + pat0 + m) + lazy_exp(fa[m]);
+            if (cb >= a.N) Ek += __ldcg(a.E + (size_t)(cb - a.N) * a.Cpad + pat0 + m) + lazy_exp(fb[m]);
             a.E[(size_t)(k - a.N) * a.Cpad + pat0 + m] = Ek;
         }
         if (k == root) {
@@ -373,6 +367,18 @@ __global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, in
     cp_async_wait<0>();
 }
 
+template <int MH>
+__global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, int level_off, int cnt) {
+    extern __shared__ __align__(16) unsigned char smem_c[];
+    const int nitems = cnt * a.R * a.ntiles * (4 / MH);
+    int4 *tab = reinterpret_cast<int4 *>(smem_c + post_smem());
+    stage_level(tab, a, level_off, cnt);
+    __syncthreads();
+    const int per = (nitems + gridDim.x - 1) / gridDim.x;
+    const int beg = blockIdx.x * per, end = min(nitems, beg + per);
+    post_range<MH>(a, tab, beg, end, smem_c);
+}
+
 // ---------------------------------------------------------------------------
 // pre-order level: one CTA per (tile, parent of the level, category r).
 // x_c = q_k o u_sibling; q_c = x_c P_c (Eq. 4) for internal children;
@@ -382,15 +388,12 @@ __global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, in
 // All inputs use the same per-pattern scales in every category, so the
 // category sums stay consistent (the ratio itself is scale invariant).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT, 4) codon_pre_kernel(const CodonArgs a, int level_off) {
-    extern __shared__ __align__(16) unsigned char smem_c[];
+__device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int r, int tile, unsigned char *smem_c) {
     double *Qs = reinterpret_cast<double *>(smem_c);
     double *Us[2] = {Qs + TILE, Qs + 2 * TILE};
     double *part = Qs + 3 * TILE;                            // [3: num a, num b, den][NW][T]
     double *sc = part + 3 * NW * T;                          // [3][T]: q_k, u_a, u_b scales
     int *stb = reinterpret_cast<int *>(sc + 3 * T);          // [2][T] tip states
-    const int tile = blockIdx.x, r = blockIdx.z;
-    const int4 lv = a.lev4[level_off + blockIdx.y];        // {node, children, kinds}: one load
     const int k = lv.x;
     const int root = 2 * a.N - 2;
     const int ch[2] = {lv.y, lv.z};
@@ -398,7 +401,7 @@ __global__ void __launch_bounds__(NT, 4) codon_pre_kernel(const CodonArgs a, int
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int pat0 = tile * T;
     if (threadIdx.x < T)
-        sc[threadIdx.x] = k == root ? 1.0 : pow2neg(lazy_exp(a.qmax[(size_t)(k - a.N) * a.Cpad + pat0 + threadIdx.x]));
+        sc[threadIdx.x] = k == root ? 1.0 : pow2neg(lazy_exp(__ldcg(a.qmax + (size_t)(k - a.N) * a.Cpad + pat0 + threadIdx.x)));
     child_scale(sc + T, a, ch[0], a.fmax, pat0);
     child_scale(sc + 2 * T, a, ch[1], a.fmax, pat0);
     // tip state codes of both children (one pass), then every tile copy in
@@ -555,6 +558,11 @@ __global__ void __launch_bounds__(NT, 4) codon_pre_kernel(const CodonArgs a, int
         }
     }
 }
+__global__ void __launch_bounds__(NT, 4) codon_pre_kernel(const CodonArgs a, int level_off) {
+    extern __shared__ __align__(16) unsigned char smem_c[];
+    // one CTA per (tile, parent of the level, category): {node, children, kinds} in one load
+    pre_tile(a, a.lev4[level_off + blockIdx.y], blockIdx.z, blockIdx.x, smem_c);
+}
 
 // ---------------------------------------------------------------------------
 // Eq. 6-8 ratio over categories, weighted by w_c, summed over patterns in a
@@ -591,6 +599,90 @@ __global__ void __launch_bounds__(256) codon_ratio_kernel(const CodonArgs a, dou
 }
 
 constexpr size_t pre_smem() { return (size_t)(3 * TILE + 3 * NW * T + 3 * T) * 8 + 2 * T * 4; }
+
+// ---------------------------------------------------------------------------
+// Dataflow ("flow") schedule: the post-order and pre-order items of every
+// level in ONE persistent launch.  Work items are (task, category r, chunk of
+// TCH tiles), task = entry of the level table (post levels by height, then pre
+// levels by depth), chunk fastest; CTAs take items in that (topological) order
+// from a global counter, wait until the item's inputs are complete, run it and
+// publish completion:
+//   post (k, r, chunk)  needs u of internal children, all R categories
+//                       (rpost[child][chunk] == R: the children's fmax are final);
+//   pre  (k, r, chunk)  needs q_k, all R categories (rpre[k][chunk] == R); at
+//                       the root, u of both children instead.  Completion of
+//                       pre(k) publishes q of its internal children.
+// An item only waits on items taken earlier by running CTAs, so the schedule
+// cannot deadlock; a node starts as soon as ITS inputs exist (not when its
+// whole level is done), and no level pays a launch + tail.  Cross-item data
+// is read through L2 only (cp.async.cg, ld.cg) after an acquire by thread 0
+// and a CTA barrier; results are published by a CTA barrier, a device fence
+// and an atomic increment by thread 0.
+// ---------------------------------------------------------------------------
+struct FlowArgs {
+    int *ctr;          // item counter (reset per evaluation)
+    int *rpost;        // [N-1][nch] completed post items per (internal node, chunk)
+    int *rpre;         // [N-1][nch] completed q writes per (internal node, chunk)
+    int npost, ntask, tch, nch;
+};
+constexpr size_t flow_smem() {
+    return (post_smem() + 16) > pre_smem() ? (post_smem() + 16) : pre_smem();
+}
+__device__ __forceinline__ void wait_count(const int *p, int v) {
+    int x;
+    for (long long spin = 0;; ++spin) {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
+        if (x >= v) return;
+        if (spin > (1ll << 27)) __trap();     // a schedule bug must fail loudly, not hang the GPU
+        __nanosleep(40);
+    }
+}
+__global__ void __launch_bounds__(NT, 3) codon_flow_kernel(const CodonArgs a, const FlowArgs f) {
+    extern __shared__ __align__(16) unsigned char smem_c[];
+    __shared__ int s_item;
+    int4 *tab = reinterpret_cast<int4 *>(smem_c + post_smem());
+    const int per_task = a.R * f.nch, nitems = f.ntask * per_task;
+    const int root = 2 * a.N - 2;
+    for (;;) {
+        if (threadIdx.x == 0) s_item = atomicAdd(f.ctr, 1);
+        __syncthreads();
+        const int item = s_item;
+        if (item >= nitems) return;
+        const int task = item / per_task, rem = item - task * per_task;
+        const int r = rem / f.nch, ch = rem - r * f.nch;
+        const int4 e = a.lev4[task];
+        const int t0 = ch * f.tch, t1 = min(a.ntiles, t0 + f.tch);
+        const bool post = task < f.npost;
+        if (threadIdx.x == 0) {
+            if (post || e.x == root) {
+                if (e.y >= a.N) wait_count(f.rpost + (size_t)(e.y - a.N) * f.nch + ch, a.R);
+                if (e.z >= a.N) wait_count(f.rpost + (size_t)(e.z - a.N) * f.nch + ch, a.R);
+            } else {
+                wait_count(f.rpre + (size_t)(e.x - a.N) * f.nch + ch, a.R);
+            }
+            if (post) tab[0] = e;
+        }
+        __syncthreads();
+        if (post) {
+            post_range<4>(a, tab, r * a.ntiles + t0, r * a.ntiles + t1, smem_c);
+        } else {
+            for (int tile = t0; tile < t1; ++tile) {
+                pre_tile(a, e, r, tile, smem_c);
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (post) {
+                atomicAdd(f.rpost + (size_t)(e.x - a.N) * f.nch + ch, 1);
+            } else {
+                if (e.y >= a.N) atomicAdd(f.rpre + (size_t)(e.y - a.N) * f.nch + ch, 1);
+                if (e.z >= a.N) atomicAdd(f.rpre + (size_t)(e.z - a.N) * f.nch + ch, 1);
+            }
+        }
+    }
+}
 
 // ---------------------------------------------------------------------------
 // A1 for this path: per (branch, category) P = (V diag(e)) V^{-1} and

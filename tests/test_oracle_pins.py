@@ -253,3 +253,102 @@ def test_pattern_range_partial_sums():
     assert np.max(np.abs(sum(p["grad"] for p in parts) - full["grad"])) < 1e-10
     thr = oracle.loglik_grad(pb, threads=3, block=8)
     assert abs(thr["logL"] - full["logL"]) < 1e-12 * abs(full["logL"])
+
+
+# ------------------------------------------- time-tree parameterisation ----
+# b_i = rho_i (h_parent(i) - h_i).
+
+def _time_tree(N, model="hky", R=2, C=8, seed=31):
+    """small problem with serially sampled tips (non-zero tip heights) and
+    lognormal branch rate scalars"""
+    pb = ps.small_problem(N, model, R=R, C=C, seed=seed)
+    rng = np.random.default_rng(seed + 1)
+    par = oracle.parents(N, pb.ops)
+    # heights: root at 1.0, every child strictly below its parent
+    h = np.zeros(2 * N - 1)
+    h[2 * N - 2] = 1.0
+    for d, a, b in pb.ops[::-1]:
+        for c in (a, b):
+            h[c] = h[d] * rng.uniform(0.4, 0.9)
+    rho = rng.lognormal(0.0, 0.3, size=2 * N - 2)
+    assert np.all(h[par[:-1]] > h[:-1])
+    return pb, h, rho
+
+
+def _logl_at(pb, N, h, rho):
+    pb.branch_lengths[:] = oracle.clock_branch_lengths(N, pb.ops, h, rho)
+    return oracle.loglik_grad(pb)["logL"]
+
+
+def test_clock_branch_lengths_hand_example():
+    """3 taxa, ops (3: 0,1), (4: 3,2): b_i = rho_i (h_parent - h_i) by hand."""
+    ops = np.array([[3, 0, 1], [4, 3, 2]])
+    h = np.array([0.0, 0.1, 0.2, 0.5, 0.9])
+    rho = np.array([1.0, 2.0, 3.0, 4.0])
+    b = oracle.clock_branch_lengths(3, ops, h, rho)
+    assert np.allclose(b, [0.5, 0.8, 2.1, 1.6], rtol=0, atol=1e-15)
+
+
+def test_clock_gradient_finite_differences():
+    """dlogL/drho_i and dlogL/dh_k against central differences of logL(b(h, rho))."""
+    N = 7
+    pb, h, rho = _time_tree(N)
+    pb.branch_lengths[:] = oracle.clock_branch_lengths(N, pb.ops, h, rho)
+    g = oracle.loglik_grad(pb)["grad"]
+    cg = oracle.clock_gradient(N, pb.ops, h, rho, g)
+    eps = 1e-6
+    for i in range(2 * N - 2):
+        rp, rm = rho.copy(), rho.copy()
+        rp[i] += eps
+        rm[i] -= eps
+        fd = (_logl_at(pb, N, h, rp) - _logl_at(pb, N, h, rm)) / (2 * eps)
+        assert abs(fd - cg["grad_rates"][i]) < 1e-6 * max(1.0, abs(fd)), i
+    for k in range(2 * N - 1):
+        hp, hm = h.copy(), h.copy()
+        hp[k] += eps
+        hm[k] -= eps
+        fd = (_logl_at(pb, N, hp, rho) - _logl_at(pb, N, hm, rho)) / (2 * eps)
+        assert abs(fd - cg["grad_heights"][k]) < 1e-6 * max(1.0, abs(fd)), k
+
+
+def test_clock_set_sums_are_local_clock_rate_derivatives():
+    """Branch-set sums = d/dr logL when the rates of one set are scaled by r
+    (strict clock: one set holding every branch)."""
+    N = 8
+    pb, h, rho = _time_tree(N, "gtr", R=3, seed=41)
+    rng = np.random.default_rng(5)
+    sets = rng.integers(-1, 3, size=2 * N - 2)
+    eps = 1e-6
+    for s in range(3):
+        m = sets == s
+        # the set sum is sum_set tau_i g_i = d/dr logL with rho_i = r on the set, at r = 1
+        rho1 = np.where(m, 1.0, rho)
+        lp = _logl_at(pb, N, h, np.where(m, 1 + eps, rho))
+        lm = _logl_at(pb, N, h, np.where(m, 1 - eps, rho))
+        fd_unit = (lp - lm) / (2 * eps)
+        pb.branch_lengths[:] = oracle.clock_branch_lengths(N, pb.ops, h, rho1)
+        g1 = oracle.loglik_grad(pb)["grad"]
+        s1 = oracle.clock_gradient(N, pb.ops, h, rho1, g1, sets, 3)["set_sums"][s]
+        assert abs(fd_unit - s1) < 1e-6 * max(1.0, abs(fd_unit)), s
+    # strict clock: every branch in one set
+    lp = _logl_at(pb, N, h, np.full(2 * N - 2, 1 + eps))
+    lm = _logl_at(pb, N, h, np.full(2 * N - 2, 1 - eps))
+    pb.branch_lengths[:] = oracle.clock_branch_lengths(N, pb.ops, h, None)
+    g1 = oracle.loglik_grad(pb)["grad"]
+    s1 = oracle.clock_gradient(N, pb.ops, h, None, g1)["set_sums"][0]
+    assert abs((lp - lm) / (2 * eps) - s1) < 1e-6 * max(1.0, abs(s1))
+
+
+def test_clock_height_identities():
+    """Translating every height (tips included) leaves b unchanged: sum_k
+    dlogL/dh_k = 0; scaling every height by alpha scales b by alpha:
+    sum_k h_k dlogL/dh_k = d/dalpha logL(alpha h) (central difference)."""
+    N = 9
+    pb, h, rho = _time_tree(N, "hky", R=4, seed=53)
+    pb.branch_lengths[:] = oracle.clock_branch_lengths(N, pb.ops, h, rho)
+    g = oracle.loglik_grad(pb)["grad"]
+    gh = oracle.clock_gradient(N, pb.ops, h, rho, g)["grad_heights"]
+    assert abs(gh.sum()) < 1e-12 * np.abs(gh).sum()
+    eps = 1e-6
+    fd = (_logl_at(pb, N, h * (1 + eps), rho) - _logl_at(pb, N, h * (1 - eps), rho)) / (2 * eps)
+    assert abs(np.dot(h, gh) - fd) < 1e-6 * abs(fd)

@@ -246,3 +246,79 @@ def test_caller_owned_stream_and_virtual_sharding():
     assert abs(lt - l0) <= 1e-13 * abs(l0)
     ref = oracle.loglik_grad(pb, threads=8)
     assert np.max(np.abs(gt - g0) / ref["grad_abs"]) < 1e-13
+
+
+# ------------------------------------------- time-tree parameterisation ----
+
+@pytest.mark.parametrize("model,N,R,C", [("hky", 40, 4, 75), ("mmm4", 20, 1, 40), ("codon", 14, 2, 37)])
+def test_clock_gradient_parity(model, N, R, C):
+    """b = rho (h_parent - h) formed on the device, and dlogL/drho, dlogL/dh
+    and branch-set sums (include/phylograd.h) vs the oracle's chain rule on
+    the oracle's g; C17-style scale: sums of |terms| with sum_c w_c |d_c|."""
+    pg = _pg()
+    import torch
+    pb = ps.small_problem(N, model, R=R, C=C, seed=N + C)
+    rng = np.random.default_rng(N)
+    h = np.zeros(2 * N - 1)
+    h[2 * N - 2] = 0.8
+    for d, a, b in pb.ops[::-1]:
+        for c in (a, b):
+            h[c] = h[d] * rng.uniform(0.3, 0.95)
+    rho = rng.lognormal(0.0, 0.3, size=2 * N - 2)
+    sets = rng.integers(-1, 4, size=2 * N - 2)
+    pb.branch_lengths[:] = oracle.clock_branch_lengths(N, pb.ops, h, rho)
+    ref = oracle.loglik_grad(pb, threads=4)
+    cref = oracle.clock_gradient(N, pb.ops, h, rho, (ref["grad"], ref["grad_abs"]), sets, 4)
+    inst = pg.from_problem(pb)
+    inst.set_branch_lengths(np.full(2 * N - 2, 0.123))       # replaced by the heights below
+    inst.set_node_heights(h, rho)
+    inst.set_branch_sets(sets, 4)
+    logl, g, gr, gh, ss = inst.clock_gradient(n_sets=4)
+    assert abs(logl - ref["logL"]) <= 1e-10 * abs(ref["logL"])
+    for got, key, akey in ((gr, "grad_rates", "abs_rates"), (gh, "grad_heights", "abs_heights"),
+                           (ss, "set_sums", "abs_sets")):
+        scale = np.maximum(np.abs(cref[key]), cref[akey])
+        err = np.abs(got - cref[key]) / np.where(scale > 0, scale, 1.0)
+        assert err.max() <= 1e-10, (key, int(np.argmax(err)), err.max())
+    # device-pointer path (rates NULL = all 1) and host path agree
+    dev = torch.device("cuda", 0)
+    pb.branch_lengths[:] = oracle.clock_branch_lengths(N, pb.ops, h, None)
+    ref1 = oracle.loglik_grad(pb, threads=4)
+    inst.set_node_heights_device(torch.tensor(h, device=dev))
+    out = torch.empty(2 * N - 1, dtype=torch.float64, device=dev)
+    gh1 = torch.empty(2 * N - 1, dtype=torch.float64, device=dev)
+    with torch.cuda.stream(inst.stream):
+        inst.compute_device(out)
+        inst.clock_gradient_device(out, grad_heights=gh1)
+    inst.stream.synchronize()
+    c1 = oracle.clock_gradient(N, pb.ops, h, None, (ref1["grad"], ref1["grad_abs"]))
+    scale = np.maximum(np.abs(c1["grad_heights"]), c1["abs_heights"])
+    assert np.max(np.abs(gh1.cpu().numpy() - c1["grad_heights"]) / scale) <= 1e-10
+    assert abs(out[0].item() - ref1["logL"]) <= 1e-10 * abs(ref1["logL"])
+    inst.close()
+
+
+def test_clock_errors():
+    pg = _pg()
+    pb = ps.small_problem(6, "hky", R=1, C=5, seed=3)
+    inst = pg.from_problem(pb)
+    N = 6
+    h = np.linspace(0, 1, 2 * N - 1)
+    h[:N] = 0.0
+    bad = h.copy()
+    bad[0] = 5.0                                           # tip above its parent
+    with pytest.raises(pg.PhyloGradError) as e:
+        inst.set_node_heights(bad)
+    assert e.value.code == pg.PG_ERR_DOMAIN
+    with pytest.raises(pg.PhyloGradError) as e:
+        inst.set_node_heights(h, -np.ones(2 * N - 2))
+    assert e.value.code == pg.PG_ERR_DOMAIN
+    with pytest.raises(pg.PhyloGradError) as e:
+        inst.set_branch_sets(np.full(2 * N - 2, 3), 2)
+    assert e.value.code == pg.PG_ERR_ARG
+    import torch
+    out = torch.zeros(2 * N - 1, dtype=torch.float64, device="cuda")
+    with pytest.raises(pg.PhyloGradError) as e:             # heights never set
+        inst.clock_gradient_device(out, grad_rates=out)
+    assert e.value.code == pg.PG_ERR_SEQUENCE
+    inst.close()
