@@ -53,11 +53,21 @@ def parse():
     ap.add_argument("--virtual-shard", type=int, default=0, metavar="G",
                     help="evidence runs only: time rank 0's pattern shard of a G-GPU run on this one GPU "
                          "(value = that shard's evals/s; not a bench line)")
+    ap.add_argument("--patterns", type=int, default=0, metavar="C",
+                    help="evidence runs only (pattern-count sweep, SURVEY §8(f) NEXT-3): the config's "
+                         "workload with C unique patterns instead of its default; not a bench line")
     return ap.parse_args()
 
 
-def make_problem(cfg: int, precision: str):
+def workload_name(cfg: int, C: int) -> str:
+    base = CONFIG_NAMES[cfg]
+    return base if cfg == 0 else base[:base.rfind("_c")] + f"_c{C}"
+
+
+def make_problem(cfg: int, precision: str, patterns: int = 0):
     kw = {"precision": precision} if cfg in (1, 2, 3, 4) else {}
+    if patterns > 0:
+        kw["C"] = patterns
     return ps.make_config(cfg, **kw)
 
 
@@ -217,7 +227,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    pb = make_problem(args.config, args.precision)
+    pb = make_problem(args.config, args.precision, args.patterns)
     C = pb.patterns
     lo, hi = pg.shard_range(C, world, rank)
     if args.virtual_shard > 1:
@@ -319,7 +329,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": dtype_name(args.precision), "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES[args.config], "tips": pb.n_tips, "patterns": C,
+            "config": {"workload": workload_name(args.config, C), "tips": pb.n_tips, "patterns": C,
                        "states": pb.states, "categories": len(pb.cat_rates),
                        "precision": args.precision,
                        "l2": "flushed (256 MiB write) between timed steps" if flush is not None else "not flushed",
@@ -361,7 +371,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    pb = make_problem(args.config, args.precision)
+    pb = make_problem(args.config, args.precision, args.patterns)
     C = pb.patterns
     threads = os.cpu_count() or 1
     # size the per-step sample so the whole run takes ~2-3 minutes
@@ -385,7 +395,7 @@ def run_reference(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1000.0 / value, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES[args.config], "tips": pb.n_tips, "patterns": C,
+            "config": {"workload": workload_name(args.config, C), "tips": pb.n_tips, "patterns": C,
                        "states": pb.states, "categories": len(pb.cat_rates), "precision": "fp64"},
             "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": threads,
                              "kind": "oracle", "sample": sample},

@@ -194,6 +194,8 @@ struct pg_instance {
     // launch configuration
     int prefetch = 4, smem = 0, grid = 0, block = 0, tiles_per_cta = 1, prog_smem_off = 0;
     int flow_tch = 0;                   // codon: tiles per flow item (0 = level-by-level kernels)
+    unsigned long long *flow_trace = nullptr;   // PG_FLOW_TRACE=<file>: per-item timestamps (diagnostics)
+    size_t flow_trace_n = 0;
     cudaGraphExec_t gexec = nullptr;
     double *gexec_out = nullptr;
     bool timing = false;
@@ -293,6 +295,7 @@ int pg_destroy(pg_instance *inst) {
     if (inst->gexec) cudaGraphExecDestroy(inst->gexec);
     for (auto &e : inst->ev) if (e) cudaEventDestroy(e);
     if (inst->own_ws && inst->ws) cudaFree(inst->ws);
+    if (inst->flow_trace) cudaFree(inst->flow_trace);
     if (inst->bl_pinned) cudaFreeHost(inst->bl_pinned);
     if (inst->clock_pinned) cudaFreeHost(inst->clock_pinned);
     if (inst->out_pinned) cudaFreeHost(inst->out_pinned);
@@ -723,6 +726,14 @@ static int configure(pg_instance *inst) {
             const int slots = 3 * inst->sm_count;
             inst->flow_tch = L.n_tiles * R >= slots ? 2 : 1;
         }
+        if (getenv("PG_FLOW_TRACE") && inst->flow_tch > 0) {    // diagnostics buffer (allocated before capture)
+            const size_t items = inst->plan.level_nodes.size() * (size_t)R *
+                                 ((L.n_tiles + inst->flow_tch - 1) / inst->flow_tch);
+            if (inst->flow_trace) cudaFree(inst->flow_trace);
+            CK(cudaMalloc(&inst->flow_trace, sizeof(unsigned long long) * pg::codon::TRW * items), "trace alloc");
+            CK(cudaMemset(inst->flow_trace, 0, sizeof(unsigned long long) * pg::codon::TRW * items), "trace clear");
+            inst->flow_trace_n = items;
+        }
         return PG_OK;
     } else {
         inst->block = L.tpl * R * (L.SP / 4);
@@ -884,8 +895,9 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
             f.rpre = f.rpost + (size_t)(N - 1) * f.nch;
             f.npost = pl.post_off.back();
             f.ntask = (int)pl.level_nodes.size();
-            void *args[] = {&c, &f};
             const int items = f.ntask * R * f.nch;
+            f.trace = inst->flow_trace_n == (size_t)items ? inst->flow_trace : nullptr;
+            void *args[] = {&c, &f};
             CK(cudaLaunchKernel((void *)pg::codon::codon_flow_kernel, dim3(std::min(items, 3 * inst->sm_count)),
                                 dim3(pg::codon::NT), args, pg::codon::flow_smem(), inst->stream),
                "codon flow launch");
@@ -1015,6 +1027,14 @@ int pg_compute(pg_instance *inst, double *log_likelihood, double *gradient) {
     }
     *log_likelihood = inst->out_pinned[0];
     if (gradient) std::memcpy(gradient, inst->out_pinned + 1, sizeof(double) * L.B);
+    if (inst->flow_trace) {                          // diagnostics: dump the last evaluation's item trace
+        std::vector<unsigned long long> h(pg::codon::TRW * inst->flow_trace_n);
+        CK(cudaMemcpy(h.data(), inst->flow_trace, h.size() * 8, cudaMemcpyDeviceToHost), "trace D2H");
+        if (FILE *fp = fopen(getenv("PG_FLOW_TRACE"), "wb")) {
+            fwrite(h.data(), 8, h.size(), fp);
+            fclose(fp);
+        }
+    }
     return PG_OK;
 }
 

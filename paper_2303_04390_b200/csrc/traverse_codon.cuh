@@ -64,6 +64,14 @@ struct CodonArgs {
     int N, S, R, Cpad, C, ntiles;
 };
 
+// flow-schedule diagnostics (PG_FLOW_TRACE): u64 words per item, device clock
+constexpr int TRW = 8;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c[0]), "+d"(c[1])
@@ -259,7 +267,8 @@ __device__ __forceinline__ double child_sc(const CodonArgs &a, int child, const 
 
 // Items [beg, end) of a level whose node table `tab` is in shared memory.
 template <int MH>
-__device__ __forceinline__ void post_range(const CodonArgs &a, const int4 *tab, int beg, int end, unsigned char *smem_c) {
+__device__ __forceinline__ void post_range(const CodonArgs &a, const int4 *tab, int beg, int end, unsigned char *smem_c,
+                                           unsigned long long *stamp = nullptr) {
     constexpr int TI = 8 * MH;               // patterns per item
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int root = 2 * a.N - 2;
@@ -298,6 +307,7 @@ __device__ __forceinline__ void post_range(const CodonArgs &a, const int4 *tab, 
     for (int i = beg; i < end; ++i) {
         cp_async_wait<0>();                  // item i's data and item i+1's states (own thread) landed
         __syncthreads();                     // ... everyone's; stage of item i-1 is free
+        if (stamp && threadIdx.x == 0) stamp[0] = gtimer();
         issue(i + 1, (i + 1 - beg) % PST, i + 2);
         const int s = (i - beg) % PST;
         const Item it = level_item<MH>(a, tab, i);
@@ -305,14 +315,22 @@ __device__ __forceinline__ void post_range(const CodonArgs &a, const int4 *tab, 
         const int pat0 = it.tile * T + it.ro;     // first pattern of the item
         const double *As = stage_A(s), *Ts = stage_B(s);
         const int *fa = stage_F(s), *fb = fa + T;
-        if (r == 0 && threadIdx.x < TI) {    // cumulative exponent inside u_k (and at the root)
+        // cumulative exponent inside u_k (and at the root): the children's E
+        // loads are issued here and consumed after the GEMM (off the chain)
+        const bool doE = r == 0 && threadIdx.x < TI;
+        int Ea = 0, Eb = 0;
+        if (doE) {
             const int m = threadIdx.x;
-            int Ek = 0;
-            if (ca >= a.N) Ek += __ldcg(a.E + (size_t)(ca - a.N) * a.Cpad + pat0 + m) + lazy_exp(fa[m]);
-            if (cb >= a.N) Ek += __ldcg(a.E + (size_t)(cb - a.N) * a.Cpad + pat0 + m) + lazy_exp(fb[m]);
-            a.E[(size_t)(k - a.N) * a.Cpad + pat0 + m] = Ek;
+            if (ca >= a.N) Ea = __ldcg(a.E + (size_t)(ca - a.N) * a.Cpad + pat0 + m);
+            if (cb >= a.N) Eb = __ldcg(a.E + (size_t)(cb - a.N) * a.Cpad + pat0 + m);
         }
+        auto storeE = [&]() {
+            const int m = threadIdx.x;
+            const int Ek = Ea + Eb + (ca >= a.N ? lazy_exp(fa[m]) : 0) + (cb >= a.N ? lazy_exp(fb[m]) : 0);
+            a.E[(size_t)(k - a.N) * a.Cpad + pat0 + m] = Ek;
+        };
         if (k == root) {
+            if (doE) storeE();
             // thread -> (pattern m = tid/8, 8 states); deterministic shuffle sum
             const int m = threadIdx.x >> 3, j = threadIdx.x & 7;
             double sum = 0.0;
@@ -350,6 +368,8 @@ __device__ __forceinline__ void post_range(const CodonArgs &a, const int4 *tab, 
         __syncthreads();
         double acc[MH][2];
         gemm_tile<MH>(acc, Pm, b, lane);
+        if (stamp && threadIdx.x == 0) stamp[1] = gtimer();
+        if (doE) storeE();
         double *out = a.u + (((size_t)(k - a.N) * a.R + r) * a.ntiles + it.tile) * TILE + it.ro * SP;
         int *fm = a.fmax + (size_t)(k - a.N) * a.Cpad + pat0;
 #pragma unroll
@@ -379,6 +399,14 @@ __global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, in
     post_range<MH>(a, tab, beg, end, smem_c);
 }
 
+struct FlowArgs {
+    int *ctr;          // item counter (reset per evaluation)
+    int *rpost;        // [N-1][nch] completed post items per (internal node, chunk)
+    int *rpre;         // [N-1][nch] completed q writes per (internal node, chunk)
+    int npost, ntask, tch, nch;
+    unsigned long long *trace;   // diagnostics (PG_FLOW_TRACE): [item][TRW] = {smid, t_take, t_ready, t_done, phase stamps}
+};
+
 // ---------------------------------------------------------------------------
 // pre-order level: one CTA per (tile, parent of the level, category r).
 // x_c = q_k o u_sibling; q_c = x_c P_c (Eq. 4) for internal children;
@@ -388,10 +416,13 @@ __global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, in
 // All inputs use the same per-pattern scales in every category, so the
 // category sums stay consistent (the ratio itself is scale invariant).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int r, int tile, unsigned char *smem_c) {
+__device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int r, int tile, unsigned char *smem_c,
+                                        unsigned long long *stamp = nullptr, const FlowArgs *fl = nullptr,
+                                        int fch = 0) {
     double *Qs = reinterpret_cast<double *>(smem_c);
     double *Us[2] = {Qs + TILE, Qs + 2 * TILE};
-    double *part = Qs + 3 * TILE;                            // [3: num a, num b, den][NW][T]
+    double *X = Qs + 3 * TILE;                               // x_c = q_k o u_sibling
+    double *part = Qs + 4 * TILE;                            // [3: num a, num b, den][NW][T]
     double *sc = part + 3 * NW * T;                          // [3][T]: q_k, u_a, u_b scales
     int *stb = reinterpret_cast<int *>(sc + 3 * T);          // [2][T] tip states
     const int k = lv.x;
@@ -443,11 +474,56 @@ __device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int 
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
+    if (stamp && threadIdx.x == 0) stamp[0] = gtimer();
     // Tiles stay unscaled: the Eq. 8 terms of a pattern carry the same factor
     // sc_q sc_a sc_b in numerator and denominator of every category (cancels);
     // the stored q_c rows are multiplied by sc_q sc_sibling below.
     const double wr = a.cat_w[r], gr = a.cat_g[r];
-    // --- phase 1: Eq. 8 terms of both children --------------------------
+    // --- phase A (the pre-order chain): q_c = x_c P_c (Eq. 4) for internal
+    // children, x_c = q_k o u_sibling formed in X; published (flow schedule)
+    // before the Eq. 8 terms, which no later item waits for ---------------
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+        const int node = ch[c];
+        if (node < a.N) continue;
+        const size_t br = (size_t)node * a.R + r;
+        double bq[16], acc[4][2];
+        load_bfrag(bq, a.PBpre + br * MAT, w, lane);
+        __syncthreads();                                  // X free (previous child's GEMM done)
+#pragma unroll
+        for (int j = 0; j < TILE / 2 / NT; ++j) {
+            const int i2 = threadIdx.x + j * NT;
+            const double2 q2 = reinterpret_cast<const double2 *>(Qs)[i2];
+            const double2 us = reinterpret_cast<const double2 *>(Us[1 - c])[i2];
+            reinterpret_cast<double2 *>(X)[i2] = make_double2(q2.x * us.x, q2.y * us.y);
+        }
+        __syncthreads();
+        gemm_tile(acc, X, bq, lane);
+        double *out = a.q + (((size_t)(node - a.N) * a.R + r) * a.ntiles + tile) * TILE;
+        int *qm = a.qmax + (size_t)(node - a.N) * a.Cpad + pat0;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+            const double f2 = sc[m] * sc[(2 - c) * T + m];   // q_k and sibling scales
+            acc[mt][0] *= f2;
+            acc[mt][1] *= f2;
+            *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
+            int f = max(__double2hiint(acc[mt][0]) >> 20, __double2hiint(acc[mt][1]) >> 20);
+            f = max(f, __shfl_xor_sync(0xffffffffu, f, 1));
+            f = max(f, __shfl_xor_sync(0xffffffffu, f, 2));
+            if ((lane & 3) == 0) atomicMax(qm + m, f);
+        }
+    }
+    if (stamp && threadIdx.x == 0) stamp[1] = gtimer();
+    if (fl) {                                             // q of the internal children complete
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (ch[0] >= a.N) atomicAdd(fl->rpre + (size_t)(ch[0] - a.N) * fl->nch + fch, 1);
+            if (ch[1] >= a.N) atomicAdd(fl->rpre + (size_t)(ch[1] - a.N) * fl->nch + fch, 1);
+        }
+    }
+    // --- phase B: Eq. 8 terms of both children ---------------------------
     // num_c = x_c'(Q u_c) with x_c = q_k o u_sibling; den = x_c'u_c is the
     // same for both children (q_k o u_a o u_b, Eq. 5).
 #pragma unroll 1
@@ -507,17 +583,7 @@ __device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int 
         }
     }
     __syncthreads();
-    // --- phase 2: x_0 = q o u_b into u_b's tile, x_1 = q o u_a into u_a's
-    // (in place: the u tiles are not needed any more) ---------------------
-#pragma unroll
-    for (int j = 0; j < TILE / 2 / NT; ++j) {
-        const int i2 = threadIdx.x + j * NT;
-        const double2 q2 = reinterpret_cast<const double2 *>(Qs)[i2];
-        const double2 u0 = reinterpret_cast<const double2 *>(Us[0])[i2];
-        const double2 u1 = reinterpret_cast<const double2 *>(Us[1])[i2];
-        reinterpret_cast<double2 *>(Us[1])[i2] = make_double2(q2.x * u1.x, q2.y * u1.y);
-        reinterpret_cast<double2 *>(Us[0])[i2] = make_double2(q2.x * u0.x, q2.y * u0.y);
-    }
+    if (stamp && threadIdx.x == 0) stamp[2] = gtimer();
     if (threadIdx.x < T) {                    // fixed-order sums over the 8 warps
         const int m = threadIdx.x;
         double sd = 0.0, sn0 = 0.0, sn1 = 0.0;
@@ -532,33 +598,9 @@ __device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int 
         nd[((size_t)ch[0] * a.R + r) * a.Cpad + pat0 + m] = make_double2(s0 * sn0, wr * sd);
         nd[((size_t)ch[1] * a.R + r) * a.Cpad + pat0 + m] = make_double2(s1 * sn1, wr * sd);
     }
-    __syncthreads();
-    // --- phase 3: q_c = x_c P_c (Eq. 4) for internal children ---------------
-#pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
-        const int node = ch[c];
-        if (node < a.N) continue;
-        const size_t br = (size_t)node * a.R + r;
-        double bq[16], acc[4][2];
-        load_bfrag(bq, a.PBpre + br * MAT, w, lane);
-        gemm_tile(acc, Us[1 - c], bq, lane);          // x_c lives in the sibling's tile
-        double *out = a.q + (((size_t)(node - a.N) * a.R + r) * a.ntiles + tile) * TILE;
-        int *qm = a.qmax + (size_t)(node - a.N) * a.Cpad + pat0;
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-            const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-            const double f2 = sc[m] * sc[(2 - c) * T + m];   // q_k and sibling scales
-            acc[mt][0] *= f2;
-            acc[mt][1] *= f2;
-            *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
-            int f = max(__double2hiint(acc[mt][0]) >> 20, __double2hiint(acc[mt][1]) >> 20);
-            f = max(f, __shfl_xor_sync(0xffffffffu, f, 1));
-            f = max(f, __shfl_xor_sync(0xffffffffu, f, 2));
-            if ((lane & 3) == 0) atomicMax(qm + m, f);
-        }
-    }
+
 }
-__global__ void __launch_bounds__(NT, 4) codon_pre_kernel(const CodonArgs a, int level_off) {
+__global__ void __launch_bounds__(NT, 3) codon_pre_kernel(const CodonArgs a, int level_off) {
     extern __shared__ __align__(16) unsigned char smem_c[];
     // one CTA per (tile, parent of the level, category): {node, children, kinds} in one load
     pre_tile(a, a.lev4[level_off + blockIdx.y], blockIdx.z, blockIdx.x, smem_c);
@@ -598,7 +640,7 @@ __global__ void __launch_bounds__(256) codon_ratio_kernel(const CodonArgs a, dou
     if (threadIdx.x == 0) out[b < B ? 1 + b : 0] = sh[0];
 }
 
-constexpr size_t pre_smem() { return (size_t)(3 * TILE + 3 * NW * T + 3 * T) * 8 + 2 * T * 4; }
+constexpr size_t pre_smem() { return (size_t)(4 * TILE + 3 * NW * T + 3 * T) * 8 + 2 * T * 4; }
 
 // ---------------------------------------------------------------------------
 // Dataflow ("flow") schedule: the post-order and pre-order items of every
@@ -610,8 +652,9 @@ constexpr size_t pre_smem() { return (size_t)(3 * TILE + 3 * NW * T + 3 * T) * 8
 //   post (k, r, chunk)  needs u of internal children, all R categories
 //                       (rpost[child][chunk] == R: the children's fmax are final);
 //   pre  (k, r, chunk)  needs q_k, all R categories (rpre[k][chunk] == R); at
-//                       the root, u of both children instead.  Completion of
-//                       pre(k) publishes q of its internal children.
+//                       the root, u of both children instead.  pre(k)
+//                       publishes q of its internal children as soon as their
+//                       q GEMMs are stored, before its Eq. 8 terms.
 // An item only waits on items taken earlier by running CTAs, so the schedule
 // cannot deadlock; a node starts as soon as ITS inputs exist (not when its
 // whole level is done), and no level pays a launch + tail.  Cross-item data
@@ -619,12 +662,7 @@ constexpr size_t pre_smem() { return (size_t)(3 * TILE + 3 * NW * T + 3 * T) * 8
 // and a CTA barrier; results are published by a CTA barrier, a device fence
 // and an atomic increment by thread 0.
 // ---------------------------------------------------------------------------
-struct FlowArgs {
-    int *ctr;          // item counter (reset per evaluation)
-    int *rpost;        // [N-1][nch] completed post items per (internal node, chunk)
-    int *rpre;         // [N-1][nch] completed q writes per (internal node, chunk)
-    int npost, ntask, tch, nch;
-};
+
 constexpr size_t flow_smem() {
     return (post_smem() + 16) > pre_smem() ? (post_smem() + 16) : pre_smem();
 }
@@ -653,6 +691,23 @@ __global__ void __launch_bounds__(NT, 3) codon_flow_kernel(const CodonArgs a, co
         const int4 e = a.lev4[task];
         const int t0 = ch * f.tch, t1 = min(a.ntiles, t0 + f.tch);
         const bool post = task < f.npost;
+        unsigned long long t_take = 0;
+        if (f.trace && threadIdx.x == 0) t_take = gtimer();
+        {   // B operands depend only on A1, not on earlier items: pull this
+            // warp's fragments into L1 while thread 0 waits for the inputs
+            const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            auto pf = [&](const double *Bg) {
+                const double *Bw = Bg + w * 16 * 32 + lane;
+#pragma unroll
+                for (int kt = 0; kt < 16; ++kt) asm volatile("prefetch.global.L1 [%0];" ::"l"(Bw + kt * 32));
+            };
+            if (post) {
+                if (e.x != root) pf(a.PBpost + ((size_t)e.x * a.R + r) * MAT);
+            } else {
+                if (e.y >= a.N) pf(a.PBpre + ((size_t)e.y * a.R + r) * MAT);
+                if (e.z >= a.N) pf(a.PBpre + ((size_t)e.z * a.R + r) * MAT);
+            }
+        }
         if (threadIdx.x == 0) {
             if (post || e.x == root) {
                 if (e.y >= a.N) wait_count(f.rpost + (size_t)(e.y - a.N) * f.nch + ch, a.R);
@@ -661,25 +716,33 @@ __global__ void __launch_bounds__(NT, 3) codon_flow_kernel(const CodonArgs a, co
                 wait_count(f.rpre + (size_t)(e.x - a.N) * f.nch + ch, a.R);
             }
             if (post) tab[0] = e;
+            if (f.trace) {
+                unsigned smid;
+                asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+                f.trace[TRW * (size_t)item] = smid;
+                f.trace[TRW * (size_t)item + 1] = t_take;
+                f.trace[TRW * (size_t)item + 2] = gtimer();
+            }
         }
         __syncthreads();
         if (post) {
-            post_range<4>(a, tab, r * a.ntiles + t0, r * a.ntiles + t1, smem_c);
+            post_range<4>(a, tab, r * a.ntiles + t0, r * a.ntiles + t1, smem_c,
+                          f.trace ? f.trace + TRW * (size_t)item + 4 : nullptr);
         } else {
+            // q of the chunk is published inside the last tile, after its
+            // q GEMMs and before its Eq. 8 terms (earlier tiles are complete)
             for (int tile = t0; tile < t1; ++tile) {
-                pre_tile(a, e, r, tile, smem_c);
+                pre_tile(a, e, r, tile, smem_c, f.trace ? f.trace + TRW * (size_t)item + 4 : nullptr,
+                         tile == t1 - 1 ? &f : nullptr, ch);
                 __syncthreads();
             }
         }
         __syncthreads();
+        if (f.trace && threadIdx.x == 0) f.trace[TRW * (size_t)item + 7] = gtimer();
         if (threadIdx.x == 0) {
             __threadfence();
-            if (post) {
-                atomicAdd(f.rpost + (size_t)(e.x - a.N) * f.nch + ch, 1);
-            } else {
-                if (e.y >= a.N) atomicAdd(f.rpre + (size_t)(e.y - a.N) * f.nch + ch, 1);
-                if (e.z >= a.N) atomicAdd(f.rpre + (size_t)(e.z - a.N) * f.nch + ch, 1);
-            }
+            if (post) atomicAdd(f.rpost + (size_t)(e.x - a.N) * f.nch + ch, 1);
+            if (f.trace) f.trace[TRW * (size_t)item + 3] = gtimer();
         }
     }
 }
@@ -701,9 +764,15 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
     extern __shared__ __align__(16) unsigned char smem_p[];
     double *Ps = reinterpret_cast<double *>(smem_p);     // [SP][SP+1]
     double *Ds = Ps + SP * (SP + 1);
+    double *Vs = Ds + SP * (SP + 1);                     // V in A-fragment order (staged)
     __shared__ double e[SP], de[SP];
     const int br = blockIdx.x, r = br % R, b = br / R;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // V's fragments are read by all 8 warps: one cp.async pass into shared
+    // memory (all 16-B copies in flight together) instead of dependent L2
+    // loads inside the DMMA loop
+    for (int i = threadIdx.x; i < MAT / 2; i += blockDim.x) cp_async16(Vs + 2 * i, VA + 2 * i);
+    cp_async_commit();
     const double g = rates[r], t = g * bl[b];
     for (int k = threadIdx.x; k < SP; k += blockDim.x) {
         const double ex = k < S ? exp(lam[k] * t) : 0.0;
@@ -712,6 +781,7 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
     }
     double bfr[16];
     load_bfrag(bfr, ViB, w, lane);
+    cp_async_wait<0>();
     __syncthreads();
     double ek[16], dk[16];
 #pragma unroll
@@ -721,12 +791,12 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
         double ap[4][2], ad[4][2];
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) ap[mt][0] = ap[mt][1] = ad[mt][0] = ad[mt][1] = 0.0;
-        const double *A = VA + h * TILE + lane;
+        const double *A = Vs + h * TILE + lane;
 #pragma unroll
         for (int kt = 0; kt < 16; ++kt)
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
-                const double v = __ldg(A + (mt * 16 + kt) * 32);
+                const double v = A[(mt * 16 + kt) * 32];
                 dmma(ap[mt], v * ek[kt], bfr[kt]);
                 dmma(ad[mt], v * dk[kt], bfr[kt]);
             }
@@ -756,7 +826,7 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
         PONE[(size_t)br * SP + s2] = acc;
     }
 }
-constexpr size_t pmat_smem() { return (size_t)2 * SP * (SP + 1) * 8; }
+constexpr size_t pmat_smem() { return (size_t)2 * SP * (SP + 1) * 8 + (size_t)MAT * 8; }
 
 }  // namespace codon
 }  // namespace pg
