@@ -36,7 +36,8 @@ import phylo_synth as ps  # noqa: E402
 METRIC = "full BLS-gradient evals/sec"
 UNIT = "evals/s"
 CONFIG_NAMES = {0: "jc5_c200", 1: "dengue997_hky_g4_c10000", 2: "carnivore62_mmm16_c5000",
-                3: "yeast49_gy94_g4_c4000", 4: "wnv104_gy94_g4_ucld_c3700"}
+                3: "yeast49_gy94_g4_c4000", 4: "wnv104_gy94_g4_ucld_c3700",
+                5: "yeast49_mmm2x61_c4000"}
 
 
 def parse():
@@ -65,7 +66,7 @@ def workload_name(cfg: int, C: int) -> str:
 
 
 def make_problem(cfg: int, precision: str, patterns: int = 0):
-    kw = {"precision": precision} if cfg in (1, 2, 3, 4) else {}
+    kw = {"precision": precision} if cfg in (1, 2, 3, 4, 5) else {}
     if patterns > 0:
         kw["C"] = patterns
     return ps.make_config(cfg, **kw)
@@ -142,7 +143,7 @@ def algorithmic_bytes(pb, C: int, precision: str) -> int:
     (pre): 2 (N-2) R C SP w; tip codes read once per pass: 2 N C; pattern
     weights 8 C.  SP = padded states."""
     N, S, R = pb.n_tips, pb.states, len(pb.cat_rates)
-    SP = 4 if S <= 4 else 8 if S <= 8 else 16 if S <= 16 else 32 if S <= 32 else 64
+    SP = 4 if S <= 4 else 8 if S <= 8 else 16 if S <= 16 else 32 if S <= 32 else 64 if S <= 64 else 128
     w = 8 if precision == "fp64" else 4
     tips = 2 * N * C if pb.tip_partials is None else 2 * N * C * SP * w
     return 2 * (N - 2) * R * C * SP * w + tips + 8 * C
@@ -153,6 +154,20 @@ def algorithmic_flops(pb, C: int) -> int:
     2 S^2 per (pattern, category) with unpadded S."""
     N, S, R = pb.n_tips, pb.states, len(pb.cat_rates)
     return 3 * (N - 2) * 2 * S * S * R * C
+
+
+def alu_roofline(pb, C, trav_ms, peaks, precision, abytes, traffic):
+    """S > 64 (and fp32 S > 16): the SIMT large-state kernel is bound by plain
+    FP64 (FP32) FMA throughput, not HBM: achieved = minimal flops / launch time
+    against the measured DFMA peak (derived FFMA peak for fp32)."""
+    fl = algorithmic_flops(pb, C)
+    ach = fl / (trav_ms * 1e-3) / 1e12
+    pk, src = ((peaks["dfma_tflops"], peaks["dfma_src"]) if precision == "fp64"
+               else (peaks["ffma_tflops"], peaks["ffma_src"]))
+    return {"bound": "alu", "achieved": round(ach, 3), "peak": round(pk, 2), "unit": "TFLOP/s",
+            "frac": round(ach / pk, 4), "traffic": traffic, "kernel": "traverse_large_kernel (SIMT)",
+            "algorithmic_flops_per_eval": fl, "kernel_ms": round(trav_ms, 5), "hbm_algorithmic_bytes": abytes,
+            "peak_source": src}
 
 
 def load_peaks():
@@ -171,6 +186,14 @@ def load_peaks():
                    fp64_src="measured (mma.sync f64 DMMA microbenchmark, profiles/r01/fp64_peak.json)")
     except Exception:
         out.update(fp64_tflops=37.0, fp64_src="fallback (B200 datasheet FP64 tensor ~37-40 TF/s)")
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01", "fp64_peak.json")))
+        out.update(dfma_tflops=float(d["dfma_tflops"]),
+                   dfma_src="measured (DFMA microbenchmark, profiles/r01/fp64_peak.json)")
+    except Exception:
+        out.update(dfma_tflops=36.0, dfma_src="fallback (B200 FP64 ~37 TF/s)")
+    # FP32 FFMA: 148 SMs x 128 lanes x 2 flops x 1.965 GHz (guide unit counts, max clock)
+    out.update(ffma_tflops=148 * 128 * 2 * 1.965e9 / 1e12, ffma_src="derived: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz")
     return out
 
 
@@ -339,7 +362,9 @@ def run_ours(args):
             "e2e": {"value": round(e2e_rate, 3), "unit": UNIT, "h2d_bytes_per_step": 8 * B,
                     "d2h_bytes_per_step": 8 * (B + 1) + (4 if world == 1 else 0)},
             "gpu_launches": args.steps * inst.kernels_per_eval(),
-            "roofline": ({"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
+            "roofline": alu_roofline(pb, Cl, trav_ms, peaks, args.precision, abytes, traffic)
+            if info["kernel_variant"] == 1 else
+            ({"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
                           "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
                           "traffic": traffic,
                           "kernel": "traverse_small_kernel" if info["kernel_variant"] == 0 else "traverse_large_kernel",

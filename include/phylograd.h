@@ -64,7 +64,7 @@ typedef struct pg_instance pg_instance;
 typedef struct {
     int32_t tips;        /* N >= 2                                              */
     int32_t patterns;    /* C >= 1 unique site patterns             */
-    int32_t states;      /* S, 2 <= S <= 64 in this build (4, <=16, <=64 paths) */
+    int32_t states;      /* S, 2 <= S <= 128 (4, <=16, <=64, <=128 paths)      */
     int32_t categories;  /* R, 1 <= R <= 16 rate categories         */
     int32_t precision;   /* PG_FP64 or PG_FP32                                  */
     int32_t device;      /* CUDA device ordinal                                 */

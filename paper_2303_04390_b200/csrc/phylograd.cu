@@ -51,6 +51,7 @@ int padded_states(int S) {
     if (S <= 16) return 16;
     if (S <= 32) return 32;
     if (S <= 64) return 64;
+    if (S <= 128) return 128;          // S = 122: MMM of two codon models (NEXT-2)
     return 0;
 }
 
@@ -65,9 +66,10 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         return PG_ERR_ARG;
     }
     int SP = padded_states(c->states);
-    if (!SP) { if (err) *err = "states > 64 are not supported by this build"; return PG_ERR_UNSUPPORTED; }
-    // fp64 with S > 16: level-batched FP64 tensor-core path, states padded to 64
-    const bool codon = SP > 16 && c->precision == PG_FP64;
+    if (!SP) { if (err) *err = "states > 128 are not supported by this build"; return PG_ERR_UNSUPPORTED; }
+    // fp64 with 16 < S <= 64: level-batched FP64 tensor-core path, states
+    // padded to 64; S > 64 (padded to 128) runs on the SIMT large-state kernel
+    const bool codon = SP > 16 && SP <= 64 && c->precision == PG_FP64;
     if (codon) SP = 64;
     if (c->states > 254) { if (err) *err = "states > 254"; return PG_ERR_UNSUPPORTED; }
     const int R = c->categories;
@@ -86,9 +88,13 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         if (R > 16) { if (err) *err = "too many rate categories (max 16)"; return PG_ERR_UNSUPPORTED; }
         L->tpl = pg::codon::T;
     } else {
-        if (R > 16) { if (err) *err = "too many rate categories (max 16)"; return PG_ERR_UNSUPPORTED; }
+        if (R > (SP == 128 ? 8 : 16)) {
+            if (err) *err = "too many rate categories (max 16; 8 for S > 64)";
+            return PG_ERR_UNSUPPORTED;
+        }
         L->tpl = (L->real == 8) ? pg::LargeCfg<double, 64>::tpl(R) : pg::LargeCfg<float, 64>::tpl(R);
         if (SP == 32) L->tpl = (L->real == 8) ? pg::LargeCfg<double, 32>::tpl(R) : pg::LargeCfg<float, 32>::tpl(R);
+        if (SP == 128) L->tpl = (L->real == 8) ? pg::LargeCfg<double, 128>::tpl(R) : pg::LargeCfg<float, 128>::tpl(R);
     }
     const long long N = c->tips, C = c->patterns;
     L->Cpad = (int)((C + 31) / 32 * 32);
@@ -629,6 +635,7 @@ static void *traverse_fn(const Layout &L, int R) {
         case 16: return d ? small_by_rp<double, 16>(RP) : small_by_rp<float, 16>(RP);
         case 32: return d ? large_kernel<double, 32>() : large_kernel<float, 32>();
         case 64: return d ? large_kernel<double, 64>() : large_kernel<float, 64>();
+        case 128: return d ? large_kernel<double, 128>() : large_kernel<float, 128>();
     }
     return nullptr;
 }
@@ -640,6 +647,7 @@ static void *pmat_kernel_fn(const Layout &L) {
         case 16: return d ? pmat_fn<double, 16>() : pmat_fn<float, 16>();
         case 32: return d ? pmat_fn<double, 32>() : pmat_fn<float, 32>();
         case 64: return d ? pmat_fn<double, 64>() : pmat_fn<float, 64>();
+        case 128: return d ? pmat_fn<double, 128>() : pmat_fn<float, 128>();
     }
     return nullptr;
 }

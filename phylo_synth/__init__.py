@@ -509,12 +509,39 @@ def config4_wnv(N: int = 104, C: int = 3_700, precision: str = "fp64",
                    rate_scalars=rho * clock, branch_times=tau)
 
 
+def config5_yeast_mmm(N: int = 49, C: int = 4_000, precision: str = "fp64",
+                      seed: Optional[int] = None) -> Problem:
+    """the paper's state-space test, a
+    Markov-modulated model of two GY94 codon models (2 x 61 = 122 states,
+    padded to 128) on the yeast-shaped tree; hidden class unobserved at the
+    tips (partials with 1 on both copies of the observed codon)."""
+    rng = np.random.default_rng(MASTER_SEED + 5 if seed is None else seed)
+    tree = coalescent_tree(N, rng, root_height=1.0)
+    pib = _codon_freqs(rng)
+    Qb = gy94(2.5, 0.1, pib)
+    K = 2
+    Q, pi = markov_modulated(Qb, pib, np.array([0.4, 1.6]), 0.5)
+    rates, cw = np.ones(1), np.ones(1)
+    hidden = _simulate_until(tree, Q, pi, rates, cw, C, rng, start=int(1.3 * C),
+                             project=lambda a: a // K)
+    obs = hidden // K
+    pats, w = compress_patterns(obs, C)
+    S = 61 * K
+    part = np.zeros((N, C, S))
+    for n in range(N):
+        for k in range(K):
+            part[n, np.arange(C), pats[n] * K + k] = 1.0
+    return _finish(f"yeastmmm{N}", tree, Q, pi, rates, cw, pats, w, S,
+                   tip_partials=part, precision=precision)
+
+
 CONFIGS = {
     0: config0_jc5,
     1: config1_dengue,
     2: config2_mmm,
     3: config3_yeast,
     4: config4_wnv,
+    5: config5_yeast_mmm,
 }
 
 
@@ -552,7 +579,8 @@ def small_problem(N: int = 5, model: str = "hky", R: int = 1, C: int = 7,
                   simulate: bool = False) -> Problem:
     """Small random instance for pins and parity tests.
 
-    model: 'jc' | 'hky' | 'gtr' | 'mmm2' (S=8) | 'mmm4' (S=16) | 'codon' (S=61).
+    model: 'jc' | 'hky' | 'gtr' | 'mmm2' (S=8) | 'mmm4' (S=16) | 'codon' (S=61)
+           | 'codon2' (S=122, two-class codon MMM).
     Tip states are uniform random (or simulated when `simulate`), with a
     `missing` fraction of state code S; `partial_tips` gives random masks.
     """
@@ -569,6 +597,9 @@ def small_problem(N: int = 5, model: str = "hky", R: int = 1, C: int = 7,
     elif model == "codon":
         pi = _codon_freqs(rng)
         Q = gy94(2.5, 0.2, pi)
+    elif model == "codon2":                   # 2-class codon MMM, S = 122
+        pib = _codon_freqs(rng)
+        Q, pi = markov_modulated(gy94(2.5, 0.2, pib), pib, np.array([0.4, 1.6]), 0.5)
     else:
         raise ValueError(model)
     S = Q.shape[0]

@@ -73,6 +73,13 @@ def test_workspace_bytes(pg):
     with pytest.raises(pg.PhyloGradError) as ei:
         pg.workspace_bytes(10, 10, 300, 1)
     assert ei.value.code == pg.PG_ERR_UNSUPPORTED
+    # S = 122 (two-class codon MMM) pads to 128 on the large-state kernel
+    b122 = pg.workspace_bytes(49, 4000, 122, 1)
+    assert (49 - 2) * 4000 * 128 * 8 < b122
+    for S, R in ((129, 1), (122, 9)):
+        with pytest.raises(pg.PhyloGradError) as ei:
+            pg.workspace_bytes(10, 10, S, R)
+        assert ei.value.code == pg.PG_ERR_UNSUPPORTED
 
 
 def test_shard_range_covers_patterns(pg):

@@ -114,7 +114,7 @@ def test_all_missing_pattern_has_unit_likelihood():
 # ------------------------------------------------------- brute force ----
 
 BRUTE = [("jc", 3, 1), ("hky", 4, 2), ("gtr", 5, 4), ("hky", 6, 2), ("mmm2", 4, 2),
-         ("mmm4", 4, 1), ("codon", 3, 2)]
+         ("mmm4", 4, 1), ("codon", 3, 2), ("codon2", 3, 1)]
 
 
 @pytest.mark.parametrize("model,N,R", BRUTE)
@@ -143,7 +143,7 @@ def test_brute_force_tip_partials_and_nonstationary_root():
 
 # ---------------------------------------------------- invariants ----
 
-@pytest.mark.parametrize("model,N,R", [("hky", 12, 4), ("mmm4", 9, 1), ("codon", 7, 2)])
+@pytest.mark.parametrize("model,N,R", [("hky", 12, 4), ("mmm4", 9, 1), ("codon", 7, 2), ("codon2", 6, 2)])
 def test_node_invariance_eq5(model, N, R):
     """sum_r P(gamma_r) p_i'q_i = L_c at every node (Eq. 5)."""
     pb = ps.small_problem(N, model, R=R, C=9, seed=4, missing=0.1)
@@ -153,7 +153,7 @@ def test_node_invariance_eq5(model, N, R):
 
 
 @pytest.mark.parametrize("model,N,R", [("hky", 16, 4), ("gtr", 32, 2), ("mmm4", 8, 2),
-                                       ("codon", 8, 2), ("hky", 64, 1)])
+                                       ("codon", 8, 2), ("codon2", 6, 1), ("hky", 64, 1)])
 def test_quadratic_reprune_matches_eq8(model, N, R):
     pb = ps.small_problem(N, model, R=R, C=6, seed=N, missing=0.05, simulate=True)
     r = oracle.loglik_grad(pb)

@@ -71,6 +71,12 @@ def test_codon_fp32_reduced():
     _compare(ps.config3_yeast(N=16, C=50, precision="fp32"), "fp32")
 
 
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_codon_mmm122_reduced(precision):
+    # NEXT-2: two-class codon MMM, S = 122 padded to 128, tip partials
+    _compare(ps.config5_yeast_mmm(N=12, C=45, precision=precision), precision)
+
+
 @pytest.mark.slow
 def test_dengue_full_fp64():
     """BJ:configs[1] at full size in the bench launch configuration."""
@@ -93,6 +99,11 @@ def test_yeast_full():
 
 
 @pytest.mark.slow
+def test_codon_mmm122_full():
+    _compare(ps.config5_yeast_mmm(), threads=16)
+
+
+@pytest.mark.slow
 def test_wnv_full():
     _compare(ps.config4_wnv(), threads=16)
 
@@ -101,7 +112,8 @@ def test_wnv_full():
 
 @pytest.mark.parametrize("model,N,R,C", [("jc", 2, 1, 1), ("hky", 3, 4, 31), ("gtr", 17, 3, 33),
                                          ("hky", 64, 2, 95), ("mmm2", 9, 3, 40), ("mmm4", 12, 2, 64),
-                                         ("codon", 5, 1, 9), ("codon", 9, 4, 20)])
+                                         ("codon", 5, 1, 9), ("codon", 9, 4, 20), ("codon2", 7, 2, 33),
+                                         ("codon2", 5, 8, 9)])
 def test_small_shapes(model, N, R, C):
     pb = ps.small_problem(N, model, R=R, C=C, seed=N + C, missing=0.1, simulate=True)
     _compare(pb)
