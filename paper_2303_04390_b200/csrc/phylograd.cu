@@ -39,7 +39,7 @@ struct Layout {
         off_post, off_pre, total;
     // codon (variant 2) extras
     size_t off_PBpre = 0, off_DT = 0, off_PONE = 0, off_QB = 0, off_q = 0, off_E = 0, off_child = 0,
-           off_levels = 0, off_lev4 = 0, off_tipmode = 0, off_VA = 0, off_ViB = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0,
+           off_levels = 0, off_lev4 = 0, off_tipmode = 0, off_utip = 0, off_VA = 0, off_ViB = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0,
            off_flow = 0, flow_bytes = 0, reset_bytes = 0;
     // time-tree parameterisation: parent/child_a/child_b [3][2N-1], heights, rate scalars, branch sets
     size_t off_tree = 0, off_h = 0, off_rho = 0, off_bset = 0;
@@ -67,10 +67,10 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
     }
     int SP = padded_states(c->states);
     if (!SP) { if (err) *err = "states > 128 are not supported by this build"; return PG_ERR_UNSUPPORTED; }
-    // fp64 with 16 < S <= 64: level-batched FP64 tensor-core path, states
-    // padded to 64; S > 64 (padded to 128) runs on the SIMT large-state kernel
-    const bool codon = SP > 16 && SP <= 64 && c->precision == PG_FP64;
-    if (codon) SP = 64;
+    // fp64 with S > 16: FP64 tensor-core path, states padded to 64 (codon) or
+    // 128 (S = 122, two-class codon MMM); fp32 S > 16: SIMT large-state kernel
+    const bool codon = SP > 16 && c->precision == PG_FP64;
+    if (codon) SP = SP <= 64 ? 64 : 128;
     if (c->states > 254) { if (err) *err = "states > 254"; return PG_ERR_UNSUPPORTED; }
     const int R = c->categories;
     L->SP = SP;
@@ -140,6 +140,8 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
     L->off_bset = take((size_t)(2 * N - 2) * 4);     // zeroed at create: one set (strict clock)
     if (L->variant == 2) {
         L->off_q = take((size_t)(N - 2) * R * L->Cpad * SP * 8);
+        // u = P p of partial tips (formed once per evaluation by codon_tipu_kernel)
+        L->off_utip = take((c->flags & PG_FLAG_TIP_PARTIALS) ? (size_t)N * R * L->Cpad * SP * 8 : 0);
         L->off_E = take((size_t)(N - 1) * L->Cpad * 4);
         // fmax [N-1], qmax [N-2], then the flow schedule's counters
         // {item counter, rpost [N-1][<= ntiles], rpre [N-1][<= ntiles]}: one memset
@@ -417,8 +419,9 @@ int pg_set_eigen(pg_instance *inst, const double *evec, const double *ievec, con
     if ((rc = upload_real(inst, inst->L.off_QT, QT))) return rc;
     if (inst->L.variant == 2) {      // Q as the fragment-ordered B operand of Qu = u Q'
         std::vector<double> QB((size_t)SP * SP);
+        const int KT = SP / 4;           // B fragments: [nt SP/8][kt SP/4][lane 32]
         for (int idx = 0; idx < SP * SP; ++idx) {
-            const int lane = idx & 31, kt = (idx >> 5) & 15, nt = idx >> 9;
+            const int lane = idx & 31, kt = (idx >> 5) & (KT - 1), nt = idx / (32 * KT);
             QB[idx] = Q[(size_t)(nt * 8 + (lane >> 2)) * SP + kt * 4 + (lane & 3)];
         }
         if ((rc = upload_doubles(inst, inst->L.off_QB, QB.data(), QB.size()))) return rc;
@@ -426,11 +429,11 @@ int pg_set_eigen(pg_instance *inst, const double *evec, const double *ievec, con
         std::vector<double> VA((size_t)SP * SP, 0.0), ViB((size_t)SP * SP, 0.0);
         for (int m = 0; m < S; ++m)
             for (int k = 0; k < S; ++k) {
-                const int pos = (((m >> 3) * 16 + (k >> 2)) << 5) + ((m & 7) << 2) + (k & 3);
+                const int pos = (((m >> 3) * KT + (k >> 2)) << 5) + ((m & 7) << 2) + (k & 3);
                 VA[pos] = evec[m * S + k];
             }
         for (int idx = 0; idx < SP * SP; ++idx) {
-            const int lane = idx & 31, kt = (idx >> 5) & 15, nt = idx >> 9;
+            const int lane = idx & 31, kt = (idx >> 5) & (KT - 1), nt = idx / (32 * KT);
             const int kk = kt * 4 + (lane & 3), nn = nt * 8 + (lane >> 2);
             ViB[idx] = (kk < S && nn < S) ? ievec[kk * S + nn] : 0.0;
         }
@@ -609,6 +612,22 @@ static void *large_kernel() { return (void *)pg::traverse_large_kernel<Real, SP>
 template <typename Real, int SP>
 static void *pmat_fn() { return (void *)pg::pmat_kernel<Real, SP>; }
 
+// kernels and launch geometry of the FP64 tensor-core path for SP = 64 / 128
+struct CodonFns {
+    void *post4, *post2, *pre, *pmat, *flow, *tipu;
+    int threads, ctas_per_sm;
+    size_t post_smem, pre_smem, pmat_smem, flow_smem, tipu_smem;
+};
+template <int SP>
+static CodonFns codon_fns_t() {
+    namespace c = pg::codon;
+    return {(void *)c::codon_post_kernel<SP, 4>, (void *)c::codon_post_kernel<SP, 2>, (void *)c::codon_pre_kernel<SP>,
+            (void *)c::codon_pmat_kernel<SP>, (void *)c::codon_flow_kernel<SP>,
+            (void *)c::codon_tipu_kernel<SP>, c::codon_threads<SP>(), c::codon_ctas_per_sm<SP>(), c::post_smem<SP>(),
+            c::pre_smem<SP>(), c::pmat_smem<SP>(), c::flow_smem<SP>(), c::tipu_smem<SP>()};
+}
+static CodonFns codon_fns(int SP) { return SP == 128 ? codon_fns_t<128>() : codon_fns_t<64>(); }
+
 static int pad_categories(int R) {
     int p = 1;
     while (p < R) p <<= 1;
@@ -708,18 +727,16 @@ static int configure(pg_instance *inst) {
             inst->smem = off + prog_bytes;
         }
     } else if (L.variant == 2) {
-        inst->block = pg::codon::NT;
+        const CodonFns cf = codon_fns(L.SP);
+        inst->block = cf.threads;
         inst->prefetch = 0;
-        inst->smem = (int)pg::codon::pre_smem();
-        for (void *fn : {(void *)pg::codon::codon_post_kernel<4>, (void *)pg::codon::codon_post_kernel<2>})
+        inst->smem = (int)cf.pre_smem;
+        for (void *fn : {cf.post4, cf.post2})
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(pg::codon::post_smem() + 16 * (size_t)inst->cfg.tips)), "smem attr");
-        CK(cudaFuncSetAttribute((void *)pg::codon::codon_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)pg::codon::pre_smem()), "smem attr");
-        CK(cudaFuncSetAttribute((void *)pg::codon::codon_pmat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)pg::codon::pmat_smem()), "smem attr");
-        CK(cudaFuncSetAttribute((void *)pg::codon::codon_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)pg::codon::flow_smem()), "smem attr");
+                                    (int)(cf.post_smem + 16 * (size_t)inst->cfg.tips)), "smem attr");
+        CK(cudaFuncSetAttribute(cf.pre, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.pre_smem), "smem attr");
+        CK(cudaFuncSetAttribute(cf.pmat, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.pmat_smem), "smem attr");
+        CK(cudaFuncSetAttribute(cf.flow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.flow_smem), "smem attr");
         // flow schedule (default): chunks of TCH tiles per item, enough items
         // per node that a level of a few nodes still fills the 3 CTAs/SM
         const char *fe = getenv("PG_CODON_FLOW"), *te = getenv("PG_FLOW_TCH");
@@ -731,7 +748,7 @@ static int configure(pg_instance *inst) {
             // measured (profiles/r01/flow_sweep.jsonl): 2 tiles per item once a
             // node alone fills the CTA slots (WNV 2.47 -> 2.38 ms), else 1
             // (8-way shards: yeast 0.288 -> 0.261 ms, WNV 0.714 -> 0.702 ms)
-            const int slots = 3 * inst->sm_count;
+            const int slots = cf.ctas_per_sm * inst->sm_count;
             inst->flow_tch = L.n_tiles * R >= slots ? 2 : 1;
         }
         if (getenv("PG_FLOW_TRACE") && inst->flow_tch > 0) {    // diagnostics buffer (allocated before capture)
@@ -844,6 +861,7 @@ static pg::codon::CodonArgs codon_args(pg_instance *inst) {
     c.tip_states = inst->at<uint8_t>(L.off_tips);
     c.tip_partials = (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? inst->at<double>(L.off_tipp) : nullptr;
     c.tip_is_partial = inst->at<uint8_t>(L.off_tipmode);
+    c.utip = (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? inst->at<double>(L.off_utip) : nullptr;
     c.u = inst->at<double>(L.off_u);
     c.q = inst->at<double>(L.off_q);
     c.E = inst->at<int>(L.off_E);
@@ -878,8 +896,14 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
                *PT = inst->at<double>(L.off_PT), *DT = inst->at<double>(L.off_DT), *PONE = inst->at<double>(L.off_PONE);
         const double *VA = inst->at<double>(L.off_VA), *ViB = inst->at<double>(L.off_ViB);
         void *args[] = {&VA, &ViB, &lam, &rates, &bl, &S, (void *)&R, &PBpost, &PBpre, &PT, &DT, &PONE};
-        CK(cudaLaunchKernel((void *)pg::codon::codon_pmat_kernel, dim3(L.B * R), dim3(256), args,
-                            pg::codon::pmat_smem(), inst->stream), "codon pmat launch");
+        const CodonFns cf = codon_fns(L.SP);
+        CK(cudaLaunchKernel(cf.pmat, dim3(L.B * R), dim3(256), args, cf.pmat_smem, inst->stream), "codon pmat launch");
+        if (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) {     // u = P p of partial tips (A2's tip step)
+            pg::codon::CodonArgs c = codon_args(inst);
+            void *targs[] = {&c};
+            CK(cudaLaunchKernel(cf.tipu, dim3(L.n_tiles, inst->cfg.tips, R), dim3(cf.threads), targs, cf.tipu_smem,
+                                inst->stream), "codon tip-partials launch");
+        }
     } else {
         void *fn = pmat_kernel_fn(L);
         void *P = inst->ws + L.off_P;
@@ -891,6 +915,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[1], inst->stream, cudaEventRecordExternal), "event");
     if (L.variant == 2) {
         pg::codon::CodonArgs c = codon_args(inst);
+        const CodonFns cf = codon_fns(L.SP);
         const auto &pl = inst->plan;
         const int N = inst->cfg.tips;
         CK(cudaMemsetAsync(inst->ws + L.off_fmax, 0, L.reset_bytes, inst->stream), "fmax/flow reset");
@@ -906,27 +931,27 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
             const int items = f.ntask * R * f.nch;
             f.trace = inst->flow_trace_n == (size_t)items ? inst->flow_trace : nullptr;
             void *args[] = {&c, &f};
-            CK(cudaLaunchKernel((void *)pg::codon::codon_flow_kernel, dim3(std::min(items, 3 * inst->sm_count)),
-                                dim3(pg::codon::NT), args, pg::codon::flow_smem(), inst->stream),
+            CK(cudaLaunchKernel(cf.flow, dim3(std::min(items, cf.ctas_per_sm * inst->sm_count)),
+                                dim3(cf.threads), args, cf.flow_smem, inst->stream),
                "codon flow launch");
         }
         for (size_t i = 0; inst->flow_tch == 0 && i + 1 < pl.post_off.size(); ++i) {
             int off = pl.post_off[i], cnt = pl.post_off[i + 1] - off;
             // persistent: 3 CTAs per SM walk the level's items; narrow levels
             // (fewer full-tile items than ~2 waves) use half-tile items
-            const bool narrow = L.n_tiles * cnt * R < 6 * inst->sm_count;
+            const bool narrow = L.n_tiles * cnt * R < 2 * cf.ctas_per_sm * inst->sm_count;
             const int items = L.n_tiles * cnt * R * (narrow ? 2 : 1);
-            void *fn = narrow ? (void *)pg::codon::codon_post_kernel<2> : (void *)pg::codon::codon_post_kernel<4>;
+            void *fn = narrow ? cf.post2 : cf.post4;
             void *args[] = {&c, &off, &cnt};
-            CK(cudaLaunchKernel(fn, dim3(std::min(items, 3 * inst->sm_count)), dim3(pg::codon::NT), args,
-                                pg::codon::post_smem() + 16 * (size_t)cnt, inst->stream),
+            CK(cudaLaunchKernel(fn, dim3(std::min(items, cf.ctas_per_sm * inst->sm_count)), dim3(cf.threads), args,
+                                cf.post_smem + 16 * (size_t)cnt, inst->stream),
                "codon post launch");
         }
         for (size_t i = 0; inst->flow_tch == 0 && i + 1 < pl.pre_off.size(); ++i) {
             int off = pl.pre_off[i], cnt = pl.pre_off[i + 1] - off;
             void *args[] = {&c, &off};
-            CK(cudaLaunchKernel((void *)pg::codon::codon_pre_kernel, dim3(L.n_tiles, cnt, R), dim3(pg::codon::NT), args,
-                                pg::codon::pre_smem(), inst->stream), "codon pre launch");
+            CK(cudaLaunchKernel(cf.pre, dim3(L.n_tiles, cnt, R), dim3(cf.threads), args, cf.pre_smem, inst->stream),
+               "codon pre launch");
         }
     } else {
         pg::TravArgs a = trav_args(inst);
@@ -1093,7 +1118,8 @@ int pg_kernels_per_eval(const pg_instance *inst, int32_t *n) {
     if (!inst || !n) return PG_ERR_ARG;
     *n = 3;   // pmat, traverse, reduce
     if (inst->L.variant == 2)   // pmat + (one flow launch | one launch per post level + per pre level) + reduce
-        *n = 2 + (inst->flow_tch > 0 ? 1 : (int32_t)(inst->plan.post_off.size() - 1) + (int32_t)(inst->plan.pre_off.size() - 1));
+        *n = 2 + ((inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? 1 : 0) +
+             (inst->flow_tch > 0 ? 1 : (int32_t)(inst->plan.post_off.size() - 1) + (int32_t)(inst->plan.pre_off.size() - 1));
     return PG_OK;
 }
 
@@ -1110,8 +1136,9 @@ int pg_get_plan_info(const pg_instance *inst, pg_plan_info *info) {
     info->flow_tiles = inst->flow_tch;
     if (inst->L.variant == 2 && inst->flow_tch > 0) {
         const int nch = (inst->L.n_tiles + inst->flow_tch - 1) / inst->flow_tch;
-        info->grid = std::min((int)inst->plan.level_nodes.size() * inst->cfg.categories * nch, 3 * inst->sm_count);
-        info->smem_bytes = (int)pg::codon::flow_smem();
+        const CodonFns cf = codon_fns(inst->L.SP);
+        info->grid = std::min((int)inst->plan.level_nodes.size() * inst->cfg.categories * nch, cf.ctas_per_sm * inst->sm_count);
+        info->smem_bytes = (int)cf.flow_smem;
     }
     return PG_OK;
 }

@@ -6,7 +6,7 @@
 // Layout ("fragment order").  A 32-pattern x 64-state tile of partials is
 // stored as [mt 4][kt 16][lane 32] doubles so that the m8n8k4 A fragment of
 // (mt, kt) is 32 consecutive doubles: element (m, k) lives at
-//     apos(m, k) = ((m/8)*16 + k/4)*32 + (m%8)*4 + k%4.
+//     apos<SP>(m, k) = ((m/8)*16 + k/4)*32 + (m%8)*4 + k%4.
 // u and q are stored per (node, category, tile) in this order in HBM, so a
 // tile is one contiguous 16 KB block, and element-wise products (Eq. 2's
 // u_a o u_b, Eq. 4's q o u) are plain position-wise products.  B operands
@@ -24,15 +24,26 @@
 namespace pg {
 namespace codon {
 
-constexpr int SP = 64, T = 32, TILE = T * SP, NW = 8, NT = NW * 32;
-constexpr int MAT = SP * SP;
+// Geometry of the SP-state path, SP = 64 (codon, 61 states) or 128 (two-class
+// codon MMM, 122 states): a 32-pattern tile is
+// [mt 4][kt SP/4][lane 32]; NW = SP/8 warps, warp w owns output columns
+// 8w..8w+7 (B fragments of KT = SP/4 doubles per lane in registers).
+constexpr int T = 32;
+#define CODON_GEO                                                              \
+    constexpr int TILE = T * SP, NW = SP / 8, NT = NW * 32, KT = SP / 4;       \
+    constexpr size_t MAT = (size_t)SP * SP;                                    \
+    (void)TILE; (void)NW; (void)NT; (void)KT; (void)MAT
+template <int SP> constexpr int codon_threads() { return SP / 8 * 32; }
+template <int SP> constexpr int codon_ctas_per_sm() { return SP == 64 ? 3 : 1; }
 
+template <int SP>
 __host__ __device__ __forceinline__ int apos(int m, int k) {
-    return (((m >> 3) * 16 + (k >> 2)) << 5) + ((m & 7) << 2) + (k & 3);
+    return (((m >> 3) * (SP / 4) + (k >> 2)) << 5) + ((m & 7) << 2) + (k & 3);
 }
 // inverse of apos
+template <int SP>
 __device__ __forceinline__ void apos_inv(int idx, int &m, int &k) {
-    const int lane = idx & 31, kt = (idx >> 5) & 15, mt = idx >> 9;
+    const int lane = idx & 31, kt = (idx >> 5) & (SP / 4 - 1), mt = (int)((unsigned)idx / (8u * SP));
     m = mt * 8 + (lane >> 2);
     k = kt * 4 + (lane & 3);
 }
@@ -51,6 +62,7 @@ struct CodonArgs {
     const uint8_t *tip_states;        // [N][Cpad]
     const double *tip_partials;       // [N][Cpad][SP] or null
     const uint8_t *tip_is_partial;    // [N]
+    double *utip;                     // [N][R][ntiles][TILE] u = P p of partial tips (codon_tipu_kernel)
     double *u;                        // [N-2][R][ntiles][TILE]
     double *q;                        // [N-2][R][ntiles][TILE]
     int *E;                           // [N-1][Cpad] cumulative exponent inside the stored u (internal + root)
@@ -80,35 +92,23 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 
 // B fragments of warp w (output columns 8w..8w+7) straight from L2 into
 // registers: 16 independent coalesced 256-B loads per warp.
-__device__ __forceinline__ void load_bfrag(double (&b)[16], const double *__restrict__ Bg, int w, int lane) {
-    const double *Bw = Bg + w * 16 * 32 + lane;
+template <int SP>
+__device__ __forceinline__ void load_bfrag(double (&b)[SP / 4], const double *__restrict__ Bg, int w, int lane) {
+    const double *Bw = Bg + w * (SP / 4) * 32 + lane;
 #pragma unroll
-    for (int kt = 0; kt < 16; ++kt) b[kt] = __ldg(Bw + kt * 32);
+    for (int kt = 0; kt < SP / 4; ++kt) b[kt] = __ldg(Bw + kt * 32);
 }
 
 // acc[mt] (rows mt*8 + lane/4, cols w*8 + 2*(lane%4) + {0,1}) = A(32x64) * B(64x64)[:, 8w..8w+7]
-template <int MT = 4>
-__device__ __forceinline__ void gemm_tile(double (&acc)[MT][2], const double *As, const double (&b)[16], int lane) {
+template <int SP, int MT = 4>
+__device__ __forceinline__ void gemm_tile(double (&acc)[MT][2], const double *As, const double (&b)[SP / 4], int lane) {
+    constexpr int KT = SP / 4;
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
 #pragma unroll
-    for (int kt = 0; kt < 16; ++kt)
+    for (int kt = 0; kt < KT; ++kt)
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) dmma(acc[mt], As[(mt * 16 + kt) * 32 + lane], b[kt]);
-}
-
-// same with A = A1 o A2 (element-wise, e.g. x = q o u_sibling), formed on the fly
-__device__ __forceinline__ void gemm_tile2(double (&acc)[4][2], const double *A1, const double *A2,
-                                           const double (&b)[16], int lane) {
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
-#pragma unroll
-    for (int kt = 0; kt < 16; ++kt)
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-            const int i = (mt * 16 + kt) * 32 + lane;
-            dmma(acc[mt], A1[i] * A2[i], b[kt]);
-        }
+        for (int mt = 0; mt < MT; ++mt) dmma(acc[mt], As[(mt * KT + kt) * 32 + lane], b[kt]);
 }
 
 // copy n doubles (n % 2 == 0, 16-B aligned) global -> shared with all threads
@@ -118,13 +118,16 @@ __device__ __forceinline__ void load_block(double *dst, const double *src, int n
 }
 
 // pattern index of fragment-order position idx
-__device__ __forceinline__ int apos_m(int idx) { return ((idx >> 9) << 3) + ((idx & 31) >> 2); }
+template <int SP>
+__device__ __forceinline__ int apos_m(int idx) { return (int)((unsigned)idx / (8u * SP)) * 8 + ((idx & 31) >> 2); }
 
 // Fill a tile with child vectors for category r: internal (u from HBM) or tip
 // (rows of P' picked by the pattern's state: u_tip[s] = P[s][state]).  Flat
 // position loop (conflict-free smem stores), two states per 16-B load.
 // `stbuf` (>= T ints of smem) receives the tile's tip states.
+template <int SP>
 __device__ void load_child(double *dst, const CodonArgs &a, int child, int r, int tile, int *stbuf) {
+    CODON_GEO;
     if (child >= a.N) {
         load_block(dst, a.u + (((size_t)(child - a.N) * a.R + r) * a.ntiles + tile) * TILE, TILE);
         return;
@@ -132,15 +135,8 @@ __device__ void load_child(double *dst, const CodonArgs &a, int child, int r, in
     const size_t br = (size_t)child * a.R + r;
     const int pat0 = tile * T;
     const double *PT = a.PT + br * MAT;
-    if (a.tip_is_partial[child]) {          // u[s] = sum_t P[s][t] p[t] = sum_t PT[t][s] p[t]
-        for (int idx = threadIdx.x; idx < TILE; idx += blockDim.x) {
-            int m, k;
-            apos_inv(idx, m, k);
-            const double *p = a.tip_partials + ((size_t)child * a.Cpad + pat0 + m) * SP;
-            double acc = 0.0;
-            for (int t = 0; t < SP; ++t) acc = fma(__ldg(PT + t * SP + k), __ldg(p + t), acc);
-            dst[idx] = acc;
-        }
+    if (a.tip_is_partial[child]) {          // u = P p, formed once per evaluation (codon_tipu_kernel)
+        load_block(dst, a.utip + (((size_t)child * a.R + r) * a.ntiles + tile) * TILE, TILE);
         return;
     }
     if (threadIdx.x < T) stbuf[threadIdx.x] = a.tip_states[(size_t)child * a.Cpad + pat0 + threadIdx.x];
@@ -149,7 +145,7 @@ __device__ void load_child(double *dst, const CodonArgs &a, int child, int r, in
     for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += blockDim.x) {
         const int idx = 2 * i2;
         int m, k;
-        apos_inv(idx, m, k);
+        apos_inv<SP>(idx, m, k);
         const int s = stbuf[m];
         const double2 v = __ldg(reinterpret_cast<const double2 *>(s < a.S ? PT + s * SP + k : ONE + k));
         reinterpret_cast<double2 *>(dst)[i2] = v;
@@ -182,9 +178,9 @@ __device__ __forceinline__ void child_scale(double *sc, const CodonArgs &a, int 
 // root: P(gamma_r) pi' p (Eq. 3) per pattern -> Lpart.
 // ---------------------------------------------------------------------------
 constexpr int PST = 2;                                           // post data stages
-constexpr int PSTAGE = 2 * TILE * 8 + 2 * T * 4;                 // A, B tiles + children's fmax
+template <int SP> constexpr int pstage() { return 2 * T * SP * 8 + 2 * T * 4; }   // A, B tiles + children's fmax
 constexpr int PSS = 3;                                           // state-code slots (2 children x 32 B)
-constexpr size_t post_smem() { return (size_t)PST * PSTAGE + PSS * 2 * T + T * 8; }   // + row scales
+template <int SP> constexpr size_t post_smem() { return (size_t)PST * pstage<SP>() + PSS * 2 * T + T * 8; }   // + row scales
 
 // The level's nodes and their children, staged in shared memory at kernel
 // start: {k, child a, child b, kinds}, kind = 0 internal, 1 tip states,
@@ -220,9 +216,10 @@ __device__ __forceinline__ Item level_item(const CodonArgs &a, const int4 *tab, 
 // bytes) were staged in shared memory one item earlier (`st`), so the
 // gather addresses need no global round trip.  Tip partials (rare) are
 // computed here.
-template <int MH>
+template <int SP, int MH>
 __device__ __forceinline__ void issue_child(double *dst, int *fm, const unsigned char *st, const CodonArgs &a,
                                             int child, int kind, int r, int tile, int ro) {
+    CODON_GEO;
     const int tid = threadIdx.x;
     if (kind == 0) {
         const double *src = a.u + (((size_t)(child - a.N) * a.R + r) * a.ntiles + tile) * TILE + ro * SP;
@@ -233,24 +230,19 @@ __device__ __forceinline__ void issue_child(double *dst, int *fm, const unsigned
     }
     const size_t br = (size_t)child * a.R + r;
     const double *PT = a.PT + br * MAT;
-    if (kind == 2) {                        // u[s] = sum_t P[s][t] p[t] = sum_t PT[t][s] p[t]
-        for (int idx = tid; idx < MH * 8 * SP; idx += NT) {
-            int m, k;
-            apos_inv(idx, m, k);
-            const double *p = a.tip_partials + ((size_t)child * a.Cpad + tile * T + ro + m) * SP;
-            double acc = 0.0;
-            for (int t = 0; t < SP; ++t) acc = fma(__ldg(PT + t * SP + k), __ldg(p + t), acc);
-            dst[idx] = acc;
-        }
+    if (kind == 2) {                        // u = P p of a partial tip (codon_tipu_kernel)
+        const double *src = a.utip + ((br * a.ntiles + tile) * TILE + ro * SP);
+#pragma unroll
+        for (int j = 0; j < MH; ++j) cp_async16(dst + 2 * (tid + j * NT), src + 2 * (tid + j * NT));
         return;
     }
-    // thread tid needs patterns m = 8j + c, c = (tid & 15) / 2 (fragment order)
+    // thread tid needs patterns m = 8j + c, c = (tid & 15) / 2 (fragment order, any SP)
     const int c = (tid & 15) >> 1;
     const double *ONE = a.PONE + br * SP;
 #pragma unroll
     for (int j = 0; j < MH; ++j) {
         int m, k;
-        apos_inv(2 * (tid + j * NT), m, k);
+        apos_inv<SP>(2 * (tid + j * NT), m, k);
         const int s = st[8 * j + c];
         cp_async16(dst + 2 * (tid + j * NT), s < a.S ? PT + s * SP + k : ONE + k);
     }
@@ -266,9 +258,14 @@ __device__ __forceinline__ double child_sc(const CodonArgs &a, int child, const 
 }
 
 // Items [beg, end) of a level whose node table `tab` is in shared memory.
-template <int MH>
+// CACHE_B: keep P_k's B fragments in registers across consecutive items of
+// the same (node, category) (persistent level kernel); the flow kernel runs
+// one or two items per call and reloads them (fewer live registers)
+template <int SP, int MH, bool CACHE_B = true>
 __device__ __forceinline__ void post_range(const CodonArgs &a, const int4 *tab, int beg, int end, unsigned char *smem_c,
                                            unsigned long long *stamp = nullptr) {
+    CODON_GEO;
+    constexpr int PSTAGE = pstage<SP>();
     constexpr int TI = 8 * MH;               // patterns per item
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int root = 2 * a.N - 2;
@@ -281,8 +278,8 @@ __device__ __forceinline__ void post_range(const CodonArgs &a, const int4 *tab, 
         if (item < end) {
             const Item it = level_item<MH>(a, tab, item);
             const unsigned char *st = stage_S(item);
-            issue_child<MH>(stage_A(s), stage_F(s), st, a, it.ca, it.kinds & 3, it.r, it.tile, it.ro);
-            issue_child<MH>(stage_B(s), stage_F(s) + T, st + T, a, it.cb, it.kinds >> 2, it.r, it.tile, it.ro);
+            issue_child<SP, MH>(stage_A(s), stage_F(s), st, a, it.ca, it.kinds & 3, it.r, it.tile, it.ro);
+            issue_child<SP, MH>(stage_B(s), stage_F(s) + T, st + T, a, it.cb, it.kinds >> 2, it.r, it.tile, it.ro);
         }
         if (item2 < end) {
             const Item it = level_item<MH>(a, tab, item2);
@@ -302,8 +299,8 @@ __device__ __forceinline__ void post_range(const CodonArgs &a, const int4 *tab, 
     cp_async_wait<0>();
     __syncthreads();
     issue(beg, 0, beg + 1);
-    double b[16];
-    int cur = -1;                            // (node, r) whose B fragments are in b
+    double bc[CACHE_B ? SP / 4 : 1];
+    int cur = -1;                            // (node, r) whose B fragments are in bc
     for (int i = beg; i < end; ++i) {
         cp_async_wait<0>();                  // item i's data and item i+1's states (own thread) landed
         __syncthreads();                     // ... everyone's; stage of item i-1 is free
@@ -336,7 +333,7 @@ __device__ __forceinline__ void post_range(const CodonArgs &a, const int4 *tab, 
             double sum = 0.0;
             if (m < TI)
                 for (int kk = j; kk < SP; kk += 8) {
-                    const int p = apos(m, kk);
+                    const int p = apos<SP>(m, kk);
                     sum = fma(a.pi[kk], As[p] * Ts[p], sum);
                 }
             sum += __shfl_xor_sync(0xffffffffu, sum, 1);
@@ -347,9 +344,14 @@ __device__ __forceinline__ void post_range(const CodonArgs &a, const int4 *tab, 
             continue;
         }
         const int kr = k * a.R + r;
-        if (kr != cur) {
-            load_bfrag(b, a.PBpost + (size_t)kr * MAT, w, lane);
-            cur = kr;
+        double bl[CACHE_B ? 1 : SP / 4];
+        if constexpr (CACHE_B) {
+            if (kr != cur) {
+                load_bfrag<SP>(bc, a.PBpost + (size_t)kr * MAT, w, lane);
+                cur = kr;
+            }
+        } else {
+            load_bfrag<SP>(bl, a.PBpost + (size_t)kr * MAT, w, lane);
         }
         // p = u_a o u_b in place (one A operand for the GEMM: half the
         // shared-memory traffic per DMMA of forming it on the fly)
@@ -367,7 +369,8 @@ __device__ __forceinline__ void post_range(const CodonArgs &a, const int4 *tab, 
         }
         __syncthreads();
         double acc[MH][2];
-        gemm_tile<MH>(acc, Pm, b, lane);
+        if constexpr (CACHE_B) gemm_tile<SP, MH>(acc, Pm, bc, lane);
+        else gemm_tile<SP, MH>(acc, Pm, bl, lane);
         if (stamp && threadIdx.x == 0) stamp[1] = gtimer();
         if (doE) storeE();
         double *out = a.u + (((size_t)(k - a.N) * a.R + r) * a.ntiles + it.tile) * TILE + it.ro * SP;
@@ -377,7 +380,7 @@ __device__ __forceinline__ void post_range(const CodonArgs &a, const int4 *tab, 
             const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
             const double f2 = f2s[m];                         // children's scales (row)
             const double c0 = acc[mt][0] * f2, c1 = acc[mt][1] * f2;
-            *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(c0, c1);
+            *reinterpret_cast<double2 *>(out + apos<SP>(m, n)) = make_double2(c0, c1);
             int f = max(__double2hiint(c0) >> 20, __double2hiint(c1) >> 20);
             f = max(f, __shfl_xor_sync(0xffffffffu, f, 1));
             f = max(f, __shfl_xor_sync(0xffffffffu, f, 2));
@@ -387,16 +390,16 @@ __device__ __forceinline__ void post_range(const CodonArgs &a, const int4 *tab, 
     cp_async_wait<0>();
 }
 
-template <int MH>
-__global__ void __launch_bounds__(NT, 3) codon_post_kernel(const CodonArgs a, int level_off, int cnt) {
+template <int SP, int MH>
+__global__ void __launch_bounds__(codon_threads<SP>(), codon_ctas_per_sm<SP>()) codon_post_kernel(const CodonArgs a, int level_off, int cnt) {
     extern __shared__ __align__(16) unsigned char smem_c[];
     const int nitems = cnt * a.R * a.ntiles * (4 / MH);
-    int4 *tab = reinterpret_cast<int4 *>(smem_c + post_smem());
+    int4 *tab = reinterpret_cast<int4 *>(smem_c + post_smem<SP>());
     stage_level(tab, a, level_off, cnt);
     __syncthreads();
     const int per = (nitems + gridDim.x - 1) / gridDim.x;
     const int beg = blockIdx.x * per, end = min(nitems, beg + per);
-    post_range<MH>(a, tab, beg, end, smem_c);
+    post_range<SP, MH>(a, tab, beg, end, smem_c);
 }
 
 struct FlowArgs {
@@ -416,9 +419,11 @@ struct FlowArgs {
 // All inputs use the same per-pattern scales in every category, so the
 // category sums stay consistent (the ratio itself is scale invariant).
 // ---------------------------------------------------------------------------
+template <int SP>
 __device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int r, int tile, unsigned char *smem_c,
                                         unsigned long long *stamp = nullptr, const FlowArgs *fl = nullptr,
                                         int fch = 0) {
+    CODON_GEO;
     double *Qs = reinterpret_cast<double *>(smem_c);
     double *Us[2] = {Qs + TILE, Qs + 2 * TILE};
     double *X = Qs + 3 * TILE;                               // x_c = q_k o u_sibling
@@ -443,7 +448,7 @@ __device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int 
     }
     __syncthreads();
     if (k == root) {
-        for (int idx = threadIdx.x; idx < TILE; idx += NT) Qs[idx] = a.pi[((idx >> 5) & 15) * 4 + (idx & 3)];
+        for (int idx = threadIdx.x; idx < TILE; idx += NT) Qs[idx] = a.pi[((idx >> 5) & (KT - 1)) * 4 + (idx & 3)];
     } else {
         const double *src = a.q + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE;
 #pragma unroll
@@ -458,14 +463,14 @@ __device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int 
 #pragma unroll
             for (int j = 0; j < TILE / 2 / NT; ++j) cp_async16(dst + 2 * (threadIdx.x + j * NT), src + 2 * (threadIdx.x + j * NT));
         } else if (((kinds >> (2 * c)) & 3) == 2) {
-            load_child(dst, a, node, r, tile, stb + c * T);
+            load_child<SP>(dst, a, node, r, tile, stb + c * T);
         } else {
             const size_t br = (size_t)node * a.R + r;
             const double *PT = a.PT + br * MAT, *ONE = a.PONE + br * SP;
 #pragma unroll
             for (int j = 0; j < TILE / 2 / NT; ++j) {
                 int m, kk;
-                apos_inv(2 * (threadIdx.x + j * NT), m, kk);
+                apos_inv<SP>(2 * (threadIdx.x + j * NT), m, kk);
                 const int st = stb[c * T + m];
                 cp_async16(dst + 2 * (threadIdx.x + j * NT), st < a.S ? PT + st * SP + kk : ONE + kk);
             }
@@ -487,8 +492,8 @@ __device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int 
         const int node = ch[c];
         if (node < a.N) continue;
         const size_t br = (size_t)node * a.R + r;
-        double bq[16], acc[4][2];
-        load_bfrag(bq, a.PBpre + br * MAT, w, lane);
+        double bq[SP / 4], acc[4][2];
+        load_bfrag<SP>(bq, a.PBpre + br * MAT, w, lane);
         __syncthreads();                                  // X free (previous child's GEMM done)
 #pragma unroll
         for (int j = 0; j < TILE / 2 / NT; ++j) {
@@ -498,7 +503,7 @@ __device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int 
             reinterpret_cast<double2 *>(X)[i2] = make_double2(q2.x * us.x, q2.y * us.y);
         }
         __syncthreads();
-        gemm_tile(acc, X, bq, lane);
+        gemm_tile<SP>(acc, X, bq, lane);
         double *out = a.q + (((size_t)(node - a.N) * a.R + r) * a.ntiles + tile) * TILE;
         int *qm = a.qmax + (size_t)(node - a.N) * a.Cpad + pat0;
 #pragma unroll
@@ -507,7 +512,7 @@ __device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int 
             const double f2 = sc[m] * sc[(2 - c) * T + m];   // q_k and sibling scales
             acc[mt][0] *= f2;
             acc[mt][1] *= f2;
-            *reinterpret_cast<double2 *>(out + apos(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
+            *reinterpret_cast<double2 *>(out + apos<SP>(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
             int f = max(__double2hiint(acc[mt][0]) >> 20, __double2hiint(acc[mt][1]) >> 20);
             f = max(f, __shfl_xor_sync(0xffffffffu, f, 1));
             f = max(f, __shfl_xor_sync(0xffffffffu, f, 2));
@@ -531,26 +536,17 @@ __device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int 
         const int node = ch[c];
         const size_t br = (size_t)node * a.R + r;
         double acc[4][2];
-        if (node >= a.N) {
-            double b[16];
-            load_bfrag(b, a.QB, w, lane);
-            gemm_tile(acc, Us[c], b, lane);
+        if (node >= a.N || ((kinds >> (2 * c)) & 3) == 2) {
+            // internal child or partial tip (u tile in smem): Q u on the tensor path
+            double b[SP / 4];
+            load_bfrag<SP>(b, a.QB, w, lane);
+            gemm_tile<SP>(acc, Us[c], b, lane);
         } else {
             // tip: gamma (Q u)[s] = D[s][state]; missing data: D 1 = gamma Q 1 = 0
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
                 const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-                if (((kinds >> (2 * c)) & 3) == 2) {
-                    double s0 = 0.0, s1 = 0.0;     // D p = sum_t D[s][t] p[t]
-                    const double *p = a.tip_partials + ((size_t)node * a.Cpad + pat0 + m) * SP;
-                    const double *DT = a.DT + br * MAT;
-                    for (int t = 0; t < SP; ++t) {
-                        s0 = fma(__ldg(DT + t * SP + n), __ldg(p + t), s0);
-                        s1 = fma(__ldg(DT + t * SP + n + 1), __ldg(p + t), s1);
-                    }
-                    acc[mt][0] = s0;
-                    acc[mt][1] = s1;
-                } else {
+                {
                     const int s = stb[c * T + m];              // staged above
                     if (s < a.S) {
                         const double2 v = __ldg(reinterpret_cast<const double2 *>(a.DT + br * MAT + s * SP + n));
@@ -565,7 +561,7 @@ __device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int 
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) {
             const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-            const int p = apos(m, n);
+            const int p = apos<SP>(m, n);
             const double2 q2 = *reinterpret_cast<const double2 *>(Qs + p);
             const double2 o2 = *reinterpret_cast<const double2 *>(Us[1 - c] + p);
             const double x0 = q2.x * o2.x, x1 = q2.y * o2.y;     // x_c = q_k o u_sibling
@@ -593,17 +589,20 @@ __device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int 
             sd += part[(2 * NW + ww) * T + m];
         }
         double2 *nd = reinterpret_cast<double2 *>(a.numden);
-        // internal children: Q u (times gamma_r here); tips: D u already carries gamma_r
-        const double s0 = ch[0] >= a.N ? gr * wr : wr, s1 = ch[1] >= a.N ? gr * wr : wr;
+        // internal children and partial tips: Q u (times gamma_r here); state
+        // tips: the D' row already carries gamma_r
+        const bool qa = ch[0] >= a.N || (kinds & 3) == 2, qb = ch[1] >= a.N || ((kinds >> 2) & 3) == 2;
+        const double s0 = qa ? gr * wr : wr, s1 = qb ? gr * wr : wr;
         nd[((size_t)ch[0] * a.R + r) * a.Cpad + pat0 + m] = make_double2(s0 * sn0, wr * sd);
         nd[((size_t)ch[1] * a.R + r) * a.Cpad + pat0 + m] = make_double2(s1 * sn1, wr * sd);
     }
 
 }
-__global__ void __launch_bounds__(NT, 3) codon_pre_kernel(const CodonArgs a, int level_off) {
+template <int SP>
+__global__ void __launch_bounds__(codon_threads<SP>(), codon_ctas_per_sm<SP>()) codon_pre_kernel(const CodonArgs a, int level_off) {
     extern __shared__ __align__(16) unsigned char smem_c[];
     // one CTA per (tile, parent of the level, category): {node, children, kinds} in one load
-    pre_tile(a, a.lev4[level_off + blockIdx.y], blockIdx.z, blockIdx.x, smem_c);
+    pre_tile<SP>(a, a.lev4[level_off + blockIdx.y], blockIdx.z, blockIdx.x, smem_c);
 }
 
 // ---------------------------------------------------------------------------
@@ -640,7 +639,8 @@ __global__ void __launch_bounds__(256) codon_ratio_kernel(const CodonArgs a, dou
     if (threadIdx.x == 0) out[b < B ? 1 + b : 0] = sh[0];
 }
 
-constexpr size_t pre_smem() { return (size_t)(4 * TILE + 3 * NW * T + 3 * T) * 8 + 2 * T * 4; }
+template <int SP>
+constexpr size_t pre_smem() { return (size_t)(4 * T * SP + 3 * (SP / 8) * T + 3 * T) * 8 + 2 * T * 4; }
 
 // ---------------------------------------------------------------------------
 // Dataflow ("flow") schedule: the post-order and pre-order items of every
@@ -663,8 +663,9 @@ constexpr size_t pre_smem() { return (size_t)(4 * TILE + 3 * NW * T + 3 * T) * 8
 // and an atomic increment by thread 0.
 // ---------------------------------------------------------------------------
 
+template <int SP>
 constexpr size_t flow_smem() {
-    return (post_smem() + 16) > pre_smem() ? (post_smem() + 16) : pre_smem();
+    return (post_smem<SP>() + 16) > pre_smem<SP>() ? (post_smem<SP>() + 16) : pre_smem<SP>();
 }
 __device__ __forceinline__ void wait_count(const int *p, int v) {
     int x;
@@ -675,10 +676,12 @@ __device__ __forceinline__ void wait_count(const int *p, int v) {
         __nanosleep(40);
     }
 }
-__global__ void __launch_bounds__(NT, 3) codon_flow_kernel(const CodonArgs a, const FlowArgs f) {
+template <int SP>
+__global__ void __launch_bounds__(codon_threads<SP>(), codon_ctas_per_sm<SP>()) codon_flow_kernel(const CodonArgs a, const FlowArgs f) {
+    CODON_GEO;
     extern __shared__ __align__(16) unsigned char smem_c[];
     __shared__ int s_item;
-    int4 *tab = reinterpret_cast<int4 *>(smem_c + post_smem());
+    int4 *tab = reinterpret_cast<int4 *>(smem_c + post_smem<SP>());
     const int per_task = a.R * f.nch, nitems = f.ntask * per_task;
     const int root = 2 * a.N - 2;
     for (;;) {
@@ -697,9 +700,9 @@ __global__ void __launch_bounds__(NT, 3) codon_flow_kernel(const CodonArgs a, co
             // warp's fragments into L1 while thread 0 waits for the inputs
             const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
             auto pf = [&](const double *Bg) {
-                const double *Bw = Bg + w * 16 * 32 + lane;
+                const double *Bw = Bg + w * KT * 32 + lane;
 #pragma unroll
-                for (int kt = 0; kt < 16; ++kt) asm volatile("prefetch.global.L1 [%0];" ::"l"(Bw + kt * 32));
+                for (int kt = 0; kt < KT; ++kt) asm volatile("prefetch.global.L1 [%0];" ::"l"(Bw + kt * 32));
             };
             if (post) {
                 if (e.x != root) pf(a.PBpost + ((size_t)e.x * a.R + r) * MAT);
@@ -726,13 +729,13 @@ __global__ void __launch_bounds__(NT, 3) codon_flow_kernel(const CodonArgs a, co
         }
         __syncthreads();
         if (post) {
-            post_range<4>(a, tab, r * a.ntiles + t0, r * a.ntiles + t1, smem_c,
+            post_range<SP, 4, false>(a, tab, r * a.ntiles + t0, r * a.ntiles + t1, smem_c,
                           f.trace ? f.trace + TRW * (size_t)item + 4 : nullptr);
         } else {
             // q of the chunk is published inside the last tile, after its
             // q GEMMs and before its Eq. 8 terms (earlier tiles are complete)
             for (int tile = t0; tile < t1; ++tile) {
-                pre_tile(a, e, r, tile, smem_c, f.trace ? f.trace + TRW * (size_t)item + 4 : nullptr,
+                pre_tile<SP>(a, e, r, tile, smem_c, f.trace ? f.trace + TRW * (size_t)item + 4 : nullptr,
                          tile == t1 - 1 ? &f : nullptr, ch);
                 __syncthreads();
             }
@@ -748,12 +751,46 @@ __global__ void __launch_bounds__(NT, 3) codon_flow_kernel(const CodonArgs a, co
 }
 
 // ---------------------------------------------------------------------------
+// Tips given as partial vectors (MMM hidden states, ambiguity codes; P:613-614
+// generalised, R6): u_tip = P_tip p_tip, once per evaluation, as a
+// GEMM per (tile, tip, category) on the tensor path -- afterwards these tips
+// are read like internal u tiles (post: child tiles; pre: Q u by GEMM).
+// ---------------------------------------------------------------------------
+template <int SP>
+__global__ void __launch_bounds__(codon_threads<SP>(), 1) codon_tipu_kernel(const CodonArgs a) {
+    CODON_GEO;
+    extern __shared__ __align__(16) unsigned char smem_c[];
+    const int tile = blockIdx.x, tip = blockIdx.y, r = blockIdx.z;
+    if (!a.tip_is_partial[tip]) return;
+    double *As = reinterpret_cast<double *>(smem_c);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double *src = a.tip_partials + ((size_t)tip * a.Cpad + (size_t)tile * T) * SP;   // [32][SP] row-major
+    for (int i = threadIdx.x; i < TILE; i += NT) {
+        const int m = i / SP, k = i % SP;
+        As[apos<SP>(m, k)] = __ldg(src + i);
+    }
+    double b[SP / 4], acc[4][2];
+    load_bfrag<SP>(b, a.PBpost + ((size_t)tip * a.R + r) * MAT, w, lane);
+    __syncthreads();
+    gemm_tile<SP>(acc, As, b, lane);
+    double *out = a.utip + (((size_t)tip * a.R + r) * a.ntiles + tile) * TILE;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+        const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+        *reinterpret_cast<double2 *>(out + apos<SP>(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
+    }
+}
+template <int SP>
+constexpr size_t tipu_smem() { return (size_t)T * SP * 8; }
+
+// ---------------------------------------------------------------------------
 // A1 for this path: per (branch, category) P = (V diag(e)) V^{-1} and
 // D = gamma Q P = (V diag(gamma lambda e)) V^{-1} (Eq. 1; Eq. 8's factor),
 // e = exp(gamma b lambda), as two 64^3 products on the FP64 tensor path
 // (V pre-arranged as A fragments, V^{-1} as B fragments at set_eigen); the
 // results are written as PBpost, PBpre, P', D', P 1.
 // ---------------------------------------------------------------------------
+template <int SP>
 __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restrict__ VA,
                                                          const double *__restrict__ ViB,
                                                          const double *__restrict__ lam,
@@ -761,72 +798,73 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
                                                          const double *__restrict__ bl, int S, int R,
                                                          double *PBpost, double *PBpre, double *PT, double *DT,
                                                          double *PONE) {
+    CODON_GEO;
     extern __shared__ __align__(16) unsigned char smem_p[];
-    double *Ps = reinterpret_cast<double *>(smem_p);     // [SP][SP+1]
-    double *Ds = Ps + SP * (SP + 1);
-    double *Vs = Ds + SP * (SP + 1);                     // V in A-fragment order (staged)
-    __shared__ double e[SP], de[SP];
+    double *Ps = reinterpret_cast<double *>(smem_p);     // [SP][SP+1]: P, then D
+    double *e = Ps + SP * (SP + 1), *de = e + SP;        // [SP] each
     const int br = blockIdx.x, r = br % R, b = br / R;
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // V's fragments are read by all 8 warps: one cp.async pass into shared
-    // memory (all 16-B copies in flight together) instead of dependent L2
-    // loads inside the DMMA loop
-    for (int i = threadIdx.x; i < MAT / 2; i += blockDim.x) cp_async16(Vs + 2 * i, VA + 2 * i);
-    cp_async_commit();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const double g = rates[r], t = g * bl[b];
     for (int k = threadIdx.x; k < SP; k += blockDim.x) {
         const double ex = k < S ? exp(lam[k] * t) : 0.0;
         e[k] = ex;
         de[k] = k < S ? g * lam[k] * ex : 0.0;
     }
-    double bfr[16];
-    load_bfrag(bfr, ViB, w, lane);
-    cp_async_wait<0>();
-    __syncthreads();
-    double ek[16], dk[16];
-#pragma unroll
-    for (int kt = 0; kt < 16; ++kt) { ek[kt] = e[kt * 4 + (lane & 3)]; dk[kt] = de[kt * 4 + (lane & 3)]; }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {              // rows 32h .. 32h+31
-        double ap[4][2], ad[4][2];
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) ap[mt][0] = ap[mt][1] = ad[mt][0] = ad[mt][1] = 0.0;
-        const double *A = Vs + h * TILE + lane;
-#pragma unroll
-        for (int kt = 0; kt < 16; ++kt)
-#pragma unroll
-            for (int mt = 0; mt < 4; ++mt) {
-                const double v = A[(mt * 16 + kt) * 32];
-                dmma(ap[mt], v * ek[kt], bfr[kt]);
-                dmma(ad[mt], v * dk[kt], bfr[kt]);
-            }
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-            const int m = h * 32 + mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-            Ps[m * (SP + 1) + n] = ap[mt][0];
-            Ps[m * (SP + 1) + n + 1] = ap[mt][1];
-            Ds[m * (SP + 1) + n] = ad[mt][0];
-            Ds[m * (SP + 1) + n + 1] = ad[mt][1];
-        }
-    }
     __syncthreads();
     const size_t base = (size_t)br * MAT;
-    for (int idx = threadIdx.x; idx < MAT; idx += blockDim.x) {
-        const int ln = idx & 31, kt = (idx >> 5) & 15, nt = idx >> 9;
-        const int kk = kt * 4 + (ln & 3), nn = nt * 8 + (ln >> 2);
-        PBpost[base + idx] = Ps[nn * (SP + 1) + kk];    // B[k=t][n=s] = P[s][t]
-        PBpre[base + idx] = Ps[kk * (SP + 1) + nn];     // B[k=s][n=t] = P[s][t]
-        const int row = idx / SP, col = idx % SP;
-        PT[base + idx] = Ps[col * (SP + 1) + row];      // P'[t][s] = P[s][t]
-        DT[base + idx] = Ds[col * (SP + 1) + row];
-    }
-    for (int s2 = threadIdx.x; s2 < SP; s2 += blockDim.x) {
-        double acc = 0.0;
-        for (int u = 0; u < SP; ++u) acc += Ps[s2 * (SP + 1) + u];
-        PONE[(size_t)br * SP + s2] = acc;
+    // pass 0: P = V diag(e) V^-1; pass 1: D = V diag(gamma lambda e) V^-1.
+    // Warp w computes column strips 8 cs .. 8 cs + 7, cs = w, w + nw, ...
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        const double *ev = pass ? de : e;
+#pragma unroll 1
+        for (int cs = w; cs < NW; cs += nw) {
+            double bfr[KT];
+            load_bfrag<SP>(bfr, ViB, cs, lane);
+#pragma unroll 1
+            for (int h = 0; h < SP / 32; ++h) {      // rows 32h .. 32h+31
+                double ap[4][2];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) ap[mt][0] = ap[mt][1] = 0.0;
+                const double *A = VA + h * TILE + lane;
+#pragma unroll
+                for (int kt = 0; kt < KT; ++kt) {
+                    const double ek = ev[kt * 4 + (lane & 3)];
+#pragma unroll
+                    for (int mt = 0; mt < 4; ++mt) dmma(ap[mt], __ldg(A + (mt * KT + kt) * 32) * ek, bfr[kt]);
+                }
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) {
+                    const int m = h * 32 + mt * 8 + (lane >> 2), n = cs * 8 + 2 * (lane & 3);
+                    Ps[m * (SP + 1) + n] = ap[mt][0];
+                    Ps[m * (SP + 1) + n + 1] = ap[mt][1];
+                }
+            }
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < (int)MAT; idx += blockDim.x) {
+            const int row = idx / SP, col = idx % SP;
+            if (pass == 0) {
+                const int ln = idx & 31, kt = (idx >> 5) & (KT - 1), nt = idx / (32 * KT);
+                const int kk = kt * 4 + (ln & 3), nn = nt * 8 + (ln >> 2);
+                PBpost[base + idx] = Ps[nn * (SP + 1) + kk];    // B[k=t][n=s] = P[s][t]
+                PBpre[base + idx] = Ps[kk * (SP + 1) + nn];     // B[k=s][n=t] = P[s][t]
+                PT[base + idx] = Ps[col * (SP + 1) + row];      // P'[t][s] = P[s][t]
+            } else {
+                DT[base + idx] = Ps[col * (SP + 1) + row];      // D'
+            }
+        }
+        if (pass == 0)
+            for (int s2 = threadIdx.x; s2 < SP; s2 += blockDim.x) {
+                double acc = 0.0;
+                for (int u = 0; u < SP; ++u) acc += Ps[s2 * (SP + 1) + u];
+                PONE[(size_t)br * SP + s2] = acc;
+            }
+        __syncthreads();
     }
 }
-constexpr size_t pmat_smem() { return (size_t)2 * SP * (SP + 1) * 8 + (size_t)MAT * 8; }
+template <int SP>
+constexpr size_t pmat_smem() { return ((size_t)SP * (SP + 1) + 2 * SP) * 8; }
 
 }  // namespace codon
 }  // namespace pg

@@ -46,7 +46,7 @@ def launches(fn):
 
 
 fn = os.path.join(out_dir, "launches_yeast.csv")
-if os.path.exists(fn):
+if os.path.exists(fn) and not os.path.exists(os.path.join(out_dir, "prof_flow.ncu-rep")):
     items = launches(fn)
     starts = [i for i, e in enumerate(items) if "pmat" in e["k"]]
     ends = [i for i, e in enumerate(items) if "ratio" in e["k"]]
@@ -55,6 +55,16 @@ if os.path.exists(fn):
     tot = sum(to_bytes(*e["dram__bytes_read.sum"]) + to_bytes(*e["dram__bytes_write.sum"]) for e in items[s:t + 1])
     d["config3_fp64"] = {"bytes": tot, "kernel": f"codon pmat + level kernels + ratio ({t - s + 1} launches, one evaluation)",
                          "source": "profiles/r01/ncu_launches_yeast.csv"}
+# codon flow kernel (the dominant launch since the one-launch schedule): ncu --set full captures
+for cfg, name in ((3, "prof_flow"), (4, "prof_flow_wnv"), (5, "prof_flow_s122")):
+    rep = os.path.join(out_dir, name + ".ncu-rep")
+    if os.path.exists(rep):
+        v, u = raw_metrics(rep)
+        rd = to_bytes(v["dram__bytes_read.sum"], u["dram__bytes_read.sum"])
+        wr = to_bytes(v["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
+        d[f"config{cfg}_fp64"] = {"bytes": rd + wr, "read": rd, "write": wr,
+                                  "kernel": v.get("Kernel Name", "codon_flow_kernel"),
+                                  "source": f"profiles/r01/ncu_flow_config{cfg}.txt (ncu --set full)"}
 fn = os.path.join(out_dir, "launches_mmm.csv")
 if os.path.exists(fn):
     tr = [e for e in launches(fn) if "traverse" in e["k"]][-1]

@@ -76,9 +76,9 @@ def test_workspace_bytes(pg):
     # S = 122 (two-class codon MMM) pads to 128 on the large-state kernel
     b122 = pg.workspace_bytes(49, 4000, 122, 1)
     assert (49 - 2) * 4000 * 128 * 8 < b122
-    for S, R in ((129, 1), (122, 9)):
+    for S, R, prec in ((129, 1, "fp64"), (122, 9, "fp32"), (122, 17, "fp64")):
         with pytest.raises(pg.PhyloGradError) as ei:
-            pg.workspace_bytes(10, 10, S, R)
+            pg.workspace_bytes(10, 10, S, R, prec)
         assert ei.value.code == pg.PG_ERR_UNSUPPORTED
 
 
