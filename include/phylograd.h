@@ -190,6 +190,25 @@ int pg_set_branch_sets(pg_instance *inst, const int32_t *set_of_branch /*[2N-2]*
 int pg_clock_gradient_device(pg_instance *inst, const double *d_out, double *d_grad_rates,
                              double *d_grad_heights, double *d_set_sums);
 
+/* Device-resident HMC leapfrog over theta = log b (the
+ * paper's use of the BLS gradient).  Target
+ *   log pi(theta) = logL(b = exp(theta)) + sum_i theta_i
+ * (logL of Eq. 3 plus the log-Jacobian of b = e^theta; flat prior on b), so
+ *   grad_i = b_i dlogL/db_i + 1.
+ * Runs n_steps >= 0 leapfrog steps of size eps with diagonal inverse mass:
+ *   p += eps/2 grad; repeat { theta += eps M^-1 p; p += eps grad } ... with the
+ * last kick eps/2 -- n_steps + 1 full evaluations (each the captured graph),
+ * all on the instance stream, no host synchronisation.  In/out: d_theta,
+ * d_p [2N-2]; d_inv_mass [2N-2] or NULL (identity).  Out: d_out [2N-1] =
+ * [logL, dlogL/db] at the final position; d_grad_theta [2N-2] (or NULL) =
+ * grad of log pi at the final position.  Device pointers, caller-owned; the
+ * instance's branch lengths become exp(theta_final).  The log-likelihood of
+ * a zero-likelihood pattern makes the trajectory meaningless: check with
+ * pg_check_status afterwards.  Errors: PG_ERR_ARG (NULL, n_steps < 0,
+ * eps not finite), PG_ERR_SEQUENCE, PG_ERR_CUDA. */
+int pg_hmc_leapfrog(pg_instance *inst, double *d_theta, double *d_p, const double *d_inv_mass, double eps,
+                    int32_t n_steps, double *d_out, double *d_grad_theta);
+
 /* Synchronise the stream and report the first zero-likelihood pattern of the
  * most recent evaluation (-1 if none).  Returns PG_ERR_ZERO_LIKELIHOOD if
  * one occurred. */

@@ -74,6 +74,7 @@ _SIGS = {
     "pg_set_node_heights_device": ([_vp, _vp, _vp], ctypes.c_int),
     "pg_set_branch_sets": ([_vp, _ip, ctypes.c_int32], ctypes.c_int),
     "pg_clock_gradient_device": ([_vp, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "pg_hmc_leapfrog": ([_vp, _vp, _vp, _vp, ctypes.c_double, ctypes.c_int32, _vp, _vp], ctypes.c_int),
     "pg_compute": ([_vp, _dp, _dp], ctypes.c_int),
     "pg_compute_device": ([_vp, _vp], ctypes.c_int),
     "pg_check_status": ([_vp, _ip], ctypes.c_int),
@@ -282,6 +283,20 @@ class Instance:
         [logL, g_0..g_{2N-3}] (this instance's partial sums), on self.stream."""
         assert out.dtype == self.torch.float64 and out.is_cuda and out.numel() >= self.n_branches + 1
         self._check(_lib.pg_compute_device(self._h, _vp(out.data_ptr())), "compute_device")
+
+    def hmc_leapfrog(self, theta, p, eps: float, n_steps: int, out, inv_mass=None, grad_theta=None):
+        """n_steps leapfrog steps over theta = log b on the device (NEXT-4,
+        include/phylograd.h pg_hmc_leapfrog): theta, p (float64 CUDA tensors,
+        [2N-2]) are updated in place; out [2N-1] receives [logL, dlogL/db] and
+        grad_theta (optional) the gradient of logL + sum(theta) at the end."""
+        t = self.torch
+        for x in (theta, p, out) + tuple(y for y in (inv_mass, grad_theta) if y is not None):
+            assert x.dtype == t.float64 and x.is_cuda and x.is_contiguous()
+
+        def ptr(x):
+            return None if x is None else _vp(x.data_ptr())
+        self._check(_lib.pg_hmc_leapfrog(self._h, ptr(theta), ptr(p), ptr(inv_mass), float(eps), int(n_steps),
+                                         ptr(out), ptr(grad_theta)), "hmc_leapfrog")
 
     def check_status(self) -> int:
         zp = ctypes.c_int32(-1)

@@ -55,6 +55,26 @@ __global__ void __launch_bounds__(256) reduce_kernel(const double *__restrict__ 
     if (threadIdx.x == 0) out[b < B ? 1 + b : 0] = sh[0];
 }
 
+// NEXT-4: leapfrog pieces over theta = log b (include/phylograd.h pg_hmc_leapfrog)
+// drift: theta += eps M^-1 p, b = exp(theta) into the instance's branch lengths
+__global__ void hmc_drift_kernel(double *__restrict__ theta, const double *__restrict__ p,
+                                 const double *__restrict__ inv_mass, double eps, double *__restrict__ bl, int B) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B) return;
+    const double th = theta[i] + eps * (inv_mass ? inv_mass[i] : 1.0) * p[i];
+    theta[i] = th;
+    bl[i] = exp(th);
+}
+// kick: grad = b o dlogL/db + 1 (from out = [logL, g]); p += coef grad
+__global__ void hmc_kick_kernel(const double *__restrict__ bl, const double *__restrict__ out, double coef,
+                                double *__restrict__ p, double *__restrict__ grad_theta, int B) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B) return;
+    const double g = bl[i] * out[1 + i] + 1.0;
+    if (grad_theta) grad_theta[i] = g;
+    p[i] += coef * g;
+}
+
 }  // namespace pg
 
 namespace pg {

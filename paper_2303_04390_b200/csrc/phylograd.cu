@@ -362,8 +362,17 @@ int pg_set_tip_partials(pg_instance *inst, int32_t tip, const double *partials) 
         if (!(partials[i] >= 0.0) || !std::isfinite(partials[i]))
             return inst->fail(PG_ERR_DOMAIN, "tip partials must be finite and >= 0");
     std::vector<double> v((size_t)Cp * SP, 0.0);
+    const int KT = SP / 4;
     for (int p = 0; p < Cp; ++p)
-        for (int s = 0; s < S; ++s) v[(size_t)p * SP + s] = p < c.patterns ? partials[(size_t)p * S + s] : 1.0;
+        for (int s = 0; s < S; ++s) {
+            const double x = p < c.patterns ? partials[(size_t)p * S + s] : 1.0;
+            if (inst->L.variant == 2) {      // 32-pattern tiles in A-fragment order (codon_tipu_kernel)
+                const int m = p & 31;
+                v[(size_t)(p >> 5) * 32 * SP + ((((m >> 3) * KT + (s >> 2)) << 5) + ((m & 7) << 2) + (s & 3))] = x;
+            } else {
+                v[(size_t)p * SP + s] = x;
+            }
+        }
     int rc = upload_real(inst, inst->L.off_tipp + (size_t)tip * Cp * SP * inst->L.real, v);
     if (rc) return rc;
     if (!inst->tip_is_partial[tip]) { inst->tip_is_partial[tip] = 1; inst->partial_modes_dirty = true; }
@@ -737,6 +746,7 @@ static int configure(pg_instance *inst) {
         CK(cudaFuncSetAttribute(cf.pre, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.pre_smem), "smem attr");
         CK(cudaFuncSetAttribute(cf.pmat, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.pmat_smem), "smem attr");
         CK(cudaFuncSetAttribute(cf.flow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.flow_smem), "smem attr");
+        CK(cudaFuncSetAttribute(cf.tipu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.tipu_smem), "smem attr");
         // flow schedule (default): chunks of TCH tiles per item, enough items
         // per node that a level of a few nodes still fills the 3 CTAs/SM
         const char *fe = getenv("PG_CODON_FLOW"), *te = getenv("PG_FLOW_TCH");
@@ -901,8 +911,9 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         if (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) {     // u = P p of partial tips (A2's tip step)
             pg::codon::CodonArgs c = codon_args(inst);
             void *targs[] = {&c};
-            CK(cudaLaunchKernel(cf.tipu, dim3(L.n_tiles, inst->cfg.tips, R), dim3(cf.threads), targs, cf.tipu_smem,
-                                inst->stream), "codon tip-partials launch");
+            CK(cudaLaunchKernel(cf.tipu, dim3((L.n_tiles + pg::codon::TIPU_TILES - 1) / pg::codon::TIPU_TILES,
+                                              inst->cfg.tips, R),
+                                dim3(cf.threads), targs, cf.tipu_smem, inst->stream), "codon tip-partials launch");
         }
     } else {
         void *fn = pmat_kernel_fn(L);
@@ -1067,6 +1078,37 @@ int pg_compute(pg_instance *inst, double *log_likelihood, double *gradient) {
             fwrite(h.data(), 8, h.size(), fp);
             fclose(fp);
         }
+    }
+    return PG_OK;
+}
+
+int pg_hmc_leapfrog(pg_instance *inst, double *d_theta, double *d_p, const double *d_inv_mass, double eps,
+                    int32_t n_steps, double *d_out, double *d_grad_theta) {
+    if (!inst) return PG_ERR_ARG;
+    if (!d_theta || !d_p || !d_out || n_steps < 0 || !std::isfinite(eps))
+        return inst->fail(PG_ERR_ARG, "NULL pointer, n_steps < 0 or non-finite eps");
+    const int B = inst->L.B;
+    double *bl = inst->at<double>(inst->L.off_bl);
+    // the branch lengths now come from theta: drop pending host uploads
+    inst->bl_host_pending = inst->clock_host_pending = false;
+    inst->have_bl = true;
+    int rc = prepare(inst);
+    if (rc) return rc;
+    const dim3 grid((B + 127) / 128), block(128);
+    auto drift = [&](double e) -> int {
+        pg::hmc_drift_kernel<<<grid, block, 0, inst->stream>>>(d_theta, d_p, d_inv_mass, e, bl, B);
+        CK(cudaGetLastError(), "hmc drift launch");
+        return PG_OK;
+    };
+    auto kick = [&](double coef) -> int {
+        pg::hmc_kick_kernel<<<grid, block, 0, inst->stream>>>(bl, d_out, coef, d_p, d_grad_theta, B);
+        CK(cudaGetLastError(), "hmc kick launch");
+        return PG_OK;
+    };
+    if ((rc = drift(0.0)) || (rc = launch_eval(inst, d_out)) || (rc = kick(n_steps > 0 ? 0.5 * eps : 0.0))) return rc;
+    for (int s = 0; s < n_steps; ++s) {
+        if ((rc = drift(eps)) || (rc = launch_eval(inst, d_out))) return rc;
+        if ((rc = kick(s + 1 < n_steps ? eps : 0.5 * eps))) return rc;
     }
     return PG_OK;
 }

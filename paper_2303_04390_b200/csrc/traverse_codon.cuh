@@ -673,7 +673,10 @@ __device__ __forceinline__ void wait_count(const int *p, int v) {
         asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
         if (x >= v) return;
         if (spin > (1ll << 27)) __trap();     // a schedule bug must fail loudly, not hang the GPU
-        __nanosleep(40);
+#ifndef PG_FLOW_SLEEP
+#define PG_FLOW_SLEEP 40
+#endif
+        if (PG_FLOW_SLEEP > 0) __nanosleep(PG_FLOW_SLEEP);
     }
 }
 template <int SP>
@@ -756,32 +759,47 @@ __global__ void __launch_bounds__(codon_threads<SP>(), codon_ctas_per_sm<SP>()) 
 // GEMM per (tile, tip, category) on the tensor path -- afterwards these tips
 // are read like internal u tiles (post: child tiles; pre: Q u by GEMM).
 // ---------------------------------------------------------------------------
+constexpr int TIPU_TILES = 4;            // tiles per CTA (B fragments loaded once)
 template <int SP>
 __global__ void __launch_bounds__(codon_threads<SP>(), 1) codon_tipu_kernel(const CodonArgs a) {
     CODON_GEO;
     extern __shared__ __align__(16) unsigned char smem_c[];
-    const int tile = blockIdx.x, tip = blockIdx.y, r = blockIdx.z;
+    const int tip = blockIdx.y, r = blockIdx.z;
     if (!a.tip_is_partial[tip]) return;
-    double *As = reinterpret_cast<double *>(smem_c);
+    const int t0 = blockIdx.x * TIPU_TILES, t1 = min(a.ntiles, t0 + TIPU_TILES);
+    double *buf[2] = {reinterpret_cast<double *>(smem_c), reinterpret_cast<double *>(smem_c) + TILE};
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const double *src = a.tip_partials + ((size_t)tip * a.Cpad + (size_t)tile * T) * SP;   // [32][SP] row-major
-    for (int i = threadIdx.x; i < TILE; i += NT) {
-        const int m = i / SP, k = i % SP;
-        As[apos<SP>(m, k)] = __ldg(src + i);
-    }
+    // tip partials are stored in A-fragment order per tile (pg_set_tip_partials)
+    auto issue = [&](int tile, double *dst) {
+        const double *src = a.tip_partials + ((size_t)tip * a.Cpad + (size_t)tile * T) * SP;
+#pragma unroll
+        for (int j = 0; j < TILE / 2 / NT; ++j) cp_async16(dst + 2 * (threadIdx.x + j * NT), src + 2 * (threadIdx.x + j * NT));
+        cp_async_commit();
+    };
+    issue(t0, buf[0]);
     double b[SP / 4], acc[4][2];
     load_bfrag<SP>(b, a.PBpost + ((size_t)tip * a.R + r) * MAT, w, lane);
-    __syncthreads();
-    gemm_tile<SP>(acc, As, b, lane);
-    double *out = a.utip + (((size_t)tip * a.R + r) * a.ntiles + tile) * TILE;
+    for (int tile = t0; tile < t1; ++tile) {
+        const int s = (tile - t0) & 1;
+        if (tile + 1 < t1) {
+            issue(tile + 1, buf[s ^ 1]);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        gemm_tile<SP>(acc, buf[s], b, lane);
+        double *out = a.utip + (((size_t)tip * a.R + r) * a.ntiles + tile) * TILE;
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-        const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-        *reinterpret_cast<double2 *>(out + apos<SP>(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
+        for (int mt = 0; mt < 4; ++mt) {
+            const int m = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+            *reinterpret_cast<double2 *>(out + apos<SP>(m, n)) = make_double2(acc[mt][0], acc[mt][1]);
+        }
+        __syncthreads();                     // buf[s] is refilled two tiles later
     }
 }
 template <int SP>
-constexpr size_t tipu_smem() { return (size_t)T * SP * 8; }
+constexpr size_t tipu_smem() { return (size_t)2 * T * SP * 8; }
 
 // ---------------------------------------------------------------------------
 // A1 for this path: per (branch, category) P = (V diag(e)) V^{-1} and

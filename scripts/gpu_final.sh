@@ -31,4 +31,11 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:codo
 for r in prof_trav prof_flow prof_flow_wnv prof_flow_s122 prof_flow8; do
   [ -f gpurun_out/$r.ncu-rep ] && python scripts/ncu_summary.py gpurun_out/$r.ncu-rep > gpurun_out/$r.txt
 done
+python scripts/ncu_lines.py gpurun_out/prof_flow.ncu-rep codon_flow 60 > gpurun_out/prof_flow_lines.txt 2>&1
+python scripts/ncu_lines.py gpurun_out/prof_trav.ncu-rep traverse 60 > gpurun_out/prof_trav_lines.txt 2>&1
+python scripts/update_traffic.py gpurun_out > gpurun_out/traffic.json 2>&1
+# keep the copy-back under 64 MiB: only the yeast flow report stays as .ncu-rep
+rm -f gpurun_out/prof_flow_wnv.ncu-rep gpurun_out/prof_flow_s122.ncu-rep gpurun_out/prof_flow8.ncu-rep gpurun_out/prof_trav.ncu-rep
+cp profiles/ncu_traffic.json gpurun_out/ncu_traffic.json
+timeout 300 python scripts/hmc_bench.py 1 3 > gpurun_out/hmc_bench.jsonl 2>&1; cat gpurun_out/hmc_bench.jsonl
 timeout 300 python scripts/flow_trace.py 3 8 > gpurun_out/flow_trace_yeast8.txt 2>&1

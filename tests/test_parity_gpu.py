@@ -348,3 +348,59 @@ def test_clock_errors():
         inst.clock_gradient_device(out, grad_rates=out)
     assert e.value.code == pg.PG_ERR_SEQUENCE
     inst.close()
+
+
+# ------------------------------------------------------- HMC (NEXT-4) ----
+
+def _leapfrog_oracle(pb, theta, p, eps, n_steps):
+    """Reference leapfrog over theta = log b with the oracle's gradient
+    (target logL(e^theta) + sum(theta); include/phylograd.h pg_hmc_leapfrog)."""
+    def grad(th):
+        pb.branch_lengths[:] = np.exp(th)
+        r = oracle.loglik_grad(pb, threads=4)
+        return r["logL"], np.exp(th) * r["grad"] + 1.0
+    th, pp = theta.copy(), p.copy()
+    lg, g = grad(th)
+    if n_steps > 0:
+        pp += 0.5 * eps * g
+    for s in range(n_steps):
+        th += eps * pp
+        lg, g = grad(th)
+        pp += (eps if s + 1 < n_steps else 0.5 * eps) * g
+    return th, pp, lg, g
+
+
+@pytest.mark.parametrize("model,N,R,C", [("hky", 12, 4, 40), ("codon", 7, 2, 15)])
+def test_hmc_leapfrog_matches_oracle_trajectory(model, N, R, C):
+    import torch
+    pg = _pg()
+    pb = ps.small_problem(N, model, R=R, C=C, seed=3, simulate=True)
+    rng = np.random.default_rng(7)
+    theta0 = np.log(pb.branch_lengths.copy())
+    p0 = rng.standard_normal(2 * N - 2)
+    eps, L = 0.02, 6
+    th_ref, p_ref, lg_ref, g_ref = _leapfrog_oracle(pb, theta0, p0, eps, L)
+    inst = pg.from_problem(pb)
+    dev = torch.device("cuda", 0)
+    th = torch.tensor(theta0, device=dev)
+    pm = torch.tensor(p0, device=dev)
+    out = torch.empty(2 * N - 1, dtype=torch.float64, device=dev)
+    gt = torch.empty(2 * N - 2, dtype=torch.float64, device=dev)
+    with torch.cuda.stream(inst.stream):
+        inst.hmc_leapfrog(th, pm, eps, L, out, grad_theta=gt)
+    inst.stream.synchronize()
+    assert inst.check_status() == -1
+    # the trajectory only propagates gradient rounding (~1e-12 relative)
+    scale = np.maximum(np.abs(p_ref), 1.0)
+    assert np.max(np.abs(th.cpu().numpy() - th_ref)) < 1e-10
+    assert np.max(np.abs(pm.cpu().numpy() - p_ref) / scale) < 1e-10
+    assert abs(out[0].item() - lg_ref) <= 1e-10 * abs(lg_ref)
+    assert np.max(np.abs(gt.cpu().numpy() - g_ref) / np.maximum(np.abs(g_ref), 1.0)) < 1e-9
+    # zero steps: one evaluation at the current position, momenta unchanged
+    p_before = pm.clone()
+    with torch.cuda.stream(inst.stream):
+        inst.hmc_leapfrog(th, pm, eps, 0, out)
+    inst.stream.synchronize()
+    assert torch.equal(pm, p_before)
+    assert abs(out[0].item() - lg_ref) <= 1e-10 * abs(lg_ref)
+    inst.close()
