@@ -39,7 +39,7 @@ struct Layout {
         off_post, off_pre, total;
     // codon (variant 2) extras
     size_t off_PBpre = 0, off_DT = 0, off_PONE = 0, off_QB = 0, off_q = 0, off_E = 0, off_child = 0,
-           off_levels = 0, off_lev4 = 0, off_tipmode = 0, off_utip = 0, off_VA = 0, off_ViB = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0,
+           off_levels = 0, off_lev4 = 0, off_tipmode = 0, off_utip = 0, off_tipmask = 0, off_tipmasked = 0, off_VA = 0, off_ViB = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0,
            off_flow = 0, flow_bytes = 0, reset_bytes = 0;
     // time-tree parameterisation: parent/child_a/child_b [3][2N-1], heights, rate scalars, branch sets
     size_t off_tree = 0, off_h = 0, off_rho = 0, off_bset = 0;
@@ -142,6 +142,9 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         L->off_q = take((size_t)(N - 2) * R * L->Cpad * SP * 8);
         // u = P p of partial tips (formed once per evaluation by codon_tipu_kernel)
         L->off_utip = take((c->flags & PG_FLAG_TIP_PARTIALS) ? (size_t)N * R * L->Cpad * SP * 8 : 0);
+        // 0/1 mask partials with <= 4 ones (MMM hidden states): state lists, u by gathers
+        L->off_tipmask = take((c->flags & PG_FLAG_TIP_PARTIALS) ? (size_t)N * L->Cpad * 4 : 0);
+        L->off_tipmasked = take((size_t)N);
         L->off_E = take((size_t)(N - 1) * L->Cpad * 4);
         // fmax [N-1], qmax [N-2], then the flow schedule's counters
         // {item counter, rpost [N-1][<= ntiles], rpre [N-1][<= ntiles]}: one memset
@@ -188,7 +191,7 @@ struct pg_instance {
     int sm_count = 148;
     // host-side state
     std::vector<uint8_t> tips_h;        // [N][Cpad]
-    std::vector<uint8_t> tip_is_partial, tip_set;
+    std::vector<uint8_t> tip_is_partial, tip_set, tip_masked;
     bool have_ops = false, have_eigen = false, have_pi = false, have_rates = false,
          have_cw = false, have_bl = false, have_patw = false;
     pg::Plan plan;
@@ -290,6 +293,7 @@ int pg_create(const pg_config *cfg, void *cuda_stream, void *dev_workspace, size
     const int N = cfg->tips;
     inst->tips_h.assign((size_t)N * L.Cpad, (uint8_t)cfg->states);   // all missing
     inst->tip_is_partial.assign(N, 0);
+    inst->tip_masked.assign(N, 0);
     inst->tip_set.assign(N, 0);
     // zero padded weights, partials (all-ones for padding is set per tip), Q, pi, matrices
     if (cudaMemsetAsync(inst->ws, 0, L.total, inst->stream) != cudaSuccess) return bail(PG_ERR_CUDA);
@@ -375,6 +379,36 @@ int pg_set_tip_partials(pg_instance *inst, int32_t tip, const double *partials) 
         }
     int rc = upload_real(inst, inst->L.off_tipp + (size_t)tip * Cp * SP * inst->L.real, v);
     if (rc) return rc;
+    if (inst->L.variant == 2) {
+        // a 0/1 mask with 1..4 ones per pattern (e.g. the hidden copies of an
+        // observed state): keep the state list so u = P p is a sum of <= 4
+        // columns of P instead of a GEMM (codon_tipu_kernel)
+        std::vector<uint8_t> idx((size_t)Cp * 4, 255);
+        bool masked = true;
+        for (int p = 0; p < c.patterns && masked; ++p) {
+            int n = 0;
+            for (int s = 0; s < S && masked; ++s) {
+                const double x = partials[(size_t)p * S + s];
+                if (x == 1.0) {
+                    if (n == 4) masked = false;
+                    else idx[(size_t)p * 4 + n++] = (uint8_t)s;
+                } else if (x != 0.0) {
+                    masked = false;
+                }
+            }
+            if (n == 0) masked = false;
+        }
+        for (int p = c.patterns; p < Cp; ++p) idx[(size_t)p * 4] = 0;      // padding: weight 0, any finite u
+        if (masked) {
+            CK(cudaMemcpyAsync(inst->ws + inst->L.off_tipmask + (size_t)tip * Cp * 4, idx.data(), idx.size(),
+                               cudaMemcpyHostToDevice, inst->stream), "tip mask upload");
+            CK(cudaStreamSynchronize(inst->stream), "tip mask sync");
+        }
+        if (inst->tip_masked[tip] != (uint8_t)masked) {
+            inst->tip_masked[tip] = (uint8_t)masked;
+            inst->partial_modes_dirty = true;
+        }
+    }
     if (!inst->tip_is_partial[tip]) { inst->tip_is_partial[tip] = 1; inst->partial_modes_dirty = true; }
     inst->tip_set[tip] = 1;
     return PG_OK;
@@ -623,7 +657,7 @@ static void *pmat_fn() { return (void *)pg::pmat_kernel<Real, SP>; }
 
 // kernels and launch geometry of the FP64 tensor-core path for SP = 64 / 128
 struct CodonFns {
-    void *post4, *post2, *pre, *pmat, *flow, *tipu;
+    void *post4, *post2, *pre, *pmat, *flow, *tipu, *tipmask;
     int threads, ctas_per_sm;
     size_t post_smem, pre_smem, pmat_smem, flow_smem, tipu_smem;
 };
@@ -632,7 +666,7 @@ static CodonFns codon_fns_t() {
     namespace c = pg::codon;
     return {(void *)c::codon_post_kernel<SP, 4>, (void *)c::codon_post_kernel<SP, 2>, (void *)c::codon_pre_kernel<SP>,
             (void *)c::codon_pmat_kernel<SP>, (void *)c::codon_flow_kernel<SP>,
-            (void *)c::codon_tipu_kernel<SP>, c::codon_threads<SP>(), c::codon_ctas_per_sm<SP>(), c::post_smem<SP>(),
+            (void *)c::codon_tipu_kernel<SP>, (void *)c::codon_tipmask_kernel<SP>, c::codon_threads<SP>(), c::codon_ctas_per_sm<SP>(), c::post_smem<SP>(),
             c::pre_smem<SP>(), c::pmat_smem<SP>(), c::flow_smem<SP>(), c::tipu_smem<SP>()};
 }
 static CodonFns codon_fns(int SP) { return SP == 128 ? codon_fns_t<128>() : codon_fns_t<64>(); }
@@ -797,6 +831,8 @@ static int refresh_plan(pg_instance *inst) {
                            cudaMemcpyHostToDevice, inst->stream), "levels upload");
         CK(cudaMemcpyAsync(inst->ws + inst->L.off_tipmode, inst->tip_is_partial.data(), N, cudaMemcpyHostToDevice,
                            inst->stream), "tip modes upload");
+        CK(cudaMemcpyAsync(inst->ws + inst->L.off_tipmasked, inst->tip_masked.data(), N, cudaMemcpyHostToDevice,
+                           inst->stream), "tip mask modes upload");
         // per level entry: {node, child a, child b, kinds}; kind 0 internal, 1 tip states, 2 tip partials
         auto kind = [&](int c) { return c >= N ? 0 : (inst->tip_is_partial[c] ? 2 : 1); };
         std::vector<int32_t> l4(4 * inst->plan.level_nodes.size());
@@ -872,6 +908,8 @@ static pg::codon::CodonArgs codon_args(pg_instance *inst) {
     c.tip_partials = (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? inst->at<double>(L.off_tipp) : nullptr;
     c.tip_is_partial = inst->at<uint8_t>(L.off_tipmode);
     c.utip = (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? inst->at<double>(L.off_utip) : nullptr;
+    c.tip_mask = (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? inst->at<uint8_t>(L.off_tipmask) : nullptr;
+    c.tip_masked = inst->at<uint8_t>(L.off_tipmasked);
     c.u = inst->at<double>(L.off_u);
     c.q = inst->at<double>(L.off_q);
     c.E = inst->at<int>(L.off_E);
@@ -914,6 +952,8 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
             CK(cudaLaunchKernel(cf.tipu, dim3((L.n_tiles + pg::codon::TIPU_TILES - 1) / pg::codon::TIPU_TILES,
                                               inst->cfg.tips, R),
                                 dim3(cf.threads), targs, cf.tipu_smem, inst->stream), "codon tip-partials launch");
+            CK(cudaLaunchKernel(cf.tipmask, dim3(L.n_tiles, inst->cfg.tips, R), dim3(256), targs, 0, inst->stream),
+               "codon tip-mask launch");
         }
     } else {
         void *fn = pmat_kernel_fn(L);
@@ -1160,7 +1200,7 @@ int pg_kernels_per_eval(const pg_instance *inst, int32_t *n) {
     if (!inst || !n) return PG_ERR_ARG;
     *n = 3;   // pmat, traverse, reduce
     if (inst->L.variant == 2)   // pmat + (one flow launch | one launch per post level + per pre level) + reduce
-        *n = 2 + ((inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? 1 : 0) +
+        *n = 2 + ((inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? 2 : 0) +
              (inst->flow_tch > 0 ? 1 : (int32_t)(inst->plan.post_off.size() - 1) + (int32_t)(inst->plan.pre_off.size() - 1));
     return PG_OK;
 }

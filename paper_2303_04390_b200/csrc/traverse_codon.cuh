@@ -63,6 +63,8 @@ struct CodonArgs {
     const double *tip_partials;       // [N][Cpad][SP] or null
     const uint8_t *tip_is_partial;    // [N]
     double *utip;                     // [N][R][ntiles][TILE] u = P p of partial tips (codon_tipu_kernel)
+    const uint8_t *tip_mask;          // [N][Cpad][4] states of 0/1 mask partials (255 = none)
+    const uint8_t *tip_masked;        // [N] 1: the tip's partials are such masks
     double *u;                        // [N-2][R][ntiles][TILE]
     double *q;                        // [N-2][R][ntiles][TILE]
     int *E;                           // [N-1][Cpad] cumulative exponent inside the stored u (internal + root)
@@ -767,6 +769,7 @@ __global__ void __launch_bounds__(codon_threads<SP>(), 1) codon_tipu_kernel(cons
     const int tip = blockIdx.y, r = blockIdx.z;
     if (!a.tip_is_partial[tip]) return;
     const int t0 = blockIdx.x * TIPU_TILES, t1 = min(a.ntiles, t0 + TIPU_TILES);
+    if (a.tip_masked[tip]) return;                 // codon_tipmask_kernel
     double *buf[2] = {reinterpret_cast<double *>(smem_c), reinterpret_cast<double *>(smem_c) + TILE};
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // tip partials are stored in A-fragment order per tile (pg_set_tip_partials)
@@ -798,6 +801,36 @@ __global__ void __launch_bounds__(codon_threads<SP>(), 1) codon_tipu_kernel(cons
         __syncthreads();                     // buf[s] is refilled two tiles later
     }
 }
+// Mask tips (0/1 partials with <= 4 ones, e.g. the hidden copies of an
+// observed codon): u[s] = sum over the pattern's mask states t of P[s][t] =
+// P'[t][s], contiguous rows of P' -- gathers, no GEMM; one CTA per (tile, tip,
+// category), light registers so many CTAs share an SM.
+template <int SP>
+__global__ void __launch_bounds__(256) codon_tipmask_kernel(const CodonArgs a) {
+    constexpr int TILE = T * SP;
+    constexpr size_t MAT = (size_t)SP * SP;
+    const int tile = blockIdx.x, tip = blockIdx.y, r = blockIdx.z;
+    if (!a.tip_masked[tip]) return;
+    const double *PT = a.PT + ((size_t)tip * a.R + r) * MAT;
+    double *out = a.utip + (((size_t)tip * a.R + r) * a.ntiles + tile) * TILE;
+    const uint8_t *mk = a.tip_mask + ((size_t)tip * a.Cpad + (size_t)tile * T) * 4;
+#pragma unroll 4
+    for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += blockDim.x) {
+        int m, k;
+        apos_inv<SP>(2 * i2, m, k);
+        const uchar4 ids = __ldg(reinterpret_cast<const uchar4 *>(mk + 4 * m));
+        const uint8_t id4[4] = {ids.x, ids.y, ids.z, ids.w};
+        double2 u = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (id4[j] != 255) {
+                const double2 v = __ldg(reinterpret_cast<const double2 *>(PT + (size_t)id4[j] * SP + k));
+                u.x += v.x;
+                u.y += v.y;
+            }
+        reinterpret_cast<double2 *>(out)[i2] = u;
+    }
+}
 template <int SP>
 constexpr size_t tipu_smem() { return (size_t)2 * T * SP * 8; }
 
@@ -820,16 +853,27 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
     extern __shared__ __align__(16) unsigned char smem_p[];
     double *Ps = reinterpret_cast<double *>(smem_p);     // [SP][SP+1]: P, then D
     double *e = Ps + SP * (SP + 1), *de = e + SP;        // [SP] each
+    // SP = 64: V's A fragments staged in shared memory once (all copies in
+    // flight together; ncu: L2 loads inside the DMMA loop were the top stall);
+    // SP = 128 reads them from L2 (no room next to the 132 KB output buffer)
+    constexpr bool STAGE_V = SP == 64;
+    double *Vs = de + SP;
     const int br = blockIdx.x, r = br % R, b = br / R;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if constexpr (STAGE_V) {
+        for (int i = threadIdx.x; i < (int)MAT / 2; i += blockDim.x) cp_async16(Vs + 2 * i, VA + 2 * i);
+        cp_async_commit();
+    }
     const double g = rates[r], t = g * bl[b];
     for (int k = threadIdx.x; k < SP; k += blockDim.x) {
         const double ex = k < S ? exp(lam[k] * t) : 0.0;
         e[k] = ex;
         de[k] = k < S ? g * lam[k] * ex : 0.0;
     }
+    if constexpr (STAGE_V) cp_async_wait<0>();
     __syncthreads();
     const size_t base = (size_t)br * MAT;
+    const double *Vsrc = STAGE_V ? Vs : VA;
     // pass 0: P = V diag(e) V^-1; pass 1: D = V diag(gamma lambda e) V^-1.
     // Warp w computes column strips 8 cs .. 8 cs + 7, cs = w, w + nw, ...
 #pragma unroll 1
@@ -844,12 +888,15 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
                 double ap[4][2];
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt) ap[mt][0] = ap[mt][1] = 0.0;
-                const double *A = VA + h * TILE + lane;
+                const double *A = Vsrc + h * TILE + lane;
 #pragma unroll
                 for (int kt = 0; kt < KT; ++kt) {
                     const double ek = ev[kt * 4 + (lane & 3)];
 #pragma unroll
-                    for (int mt = 0; mt < 4; ++mt) dmma(ap[mt], __ldg(A + (mt * KT + kt) * 32) * ek, bfr[kt]);
+                    for (int mt = 0; mt < 4; ++mt) {
+                        const double v = STAGE_V ? A[(mt * KT + kt) * 32] : __ldg(A + (mt * KT + kt) * 32);
+                        dmma(ap[mt], v * ek, bfr[kt]);
+                    }
                 }
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt) {
@@ -882,7 +929,7 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
     }
 }
 template <int SP>
-constexpr size_t pmat_smem() { return ((size_t)SP * (SP + 1) + 2 * SP) * 8; }
+constexpr size_t pmat_smem() { return ((size_t)SP * (SP + 1) + 2 * SP + (SP == 64 ? (size_t)SP * SP : 0)) * 8; }
 
 }  // namespace codon
 }  // namespace pg

@@ -77,7 +77,7 @@ struct SmallCfg {
     static constexpr int VL = SP / LV;                         // states per lane
     static constexpr int TP = 32 / (RP * LV);                  // patterns per warp tile
 #ifndef PG_STAGES
-    static constexpr int D = (SP <= 8) ? 4 : 2;                // stage ring depth
+    static constexpr int D = 4;                                // stage ring depth (steps)
 #else
     static constexpr int D = PG_STAGES;
 #endif
@@ -106,12 +106,13 @@ struct SmallCfg {
     }
     // OPS consecutive ops share one ring stage (one full/empty barrier pair),
     // DS stages in the ring.  Pairing halves the barrier traffic but lets the
-    // producer refill only after both ops: measured +5 % for S = 16 (whose
-    // ring grows to 4 ops), 24 % slower for S = 4 (same smem, less lookahead).
+    // producer refill only after both ops: 24 % slower for S = 4; for S = 16
+    // (MMM) 2 stages x 2 ops vs 4 stages x 1 op measured 0.228 vs 0.222 ms
+    // (scripts/gpu_mmm_stages.sh), so one op per stage everywhere.
 #ifdef PG_OPS
     static constexpr int OPS = PG_OPS;
 #else
-    static constexpr int OPS = SP == 16 ? 2 : 1;
+    static constexpr int OPS = 1;
 #endif
     static constexpr int DS = D / OPS < 2 ? 2 : D / OPS;
     static __host__ __device__ size_t smem(int R, int K, int depth) {
