@@ -751,6 +751,7 @@ static int configure(pg_instance *inst) {
         int K = std::max(1, std::min(pg::small_max_consumers(L.SP, pad_categories(R)),
                                      (L.n_tiles + inst->sm_count - 1) / inst->sm_count));
         while (K > 1 && small_smem(L, R, K, depth) > 227 * 1024) --K;
+        if (const char *ke = getenv("PG_SMALL_K")) K = std::max(1, std::min(K, atoi(ke)));   // experiments
         inst->tiles_per_cta = K;
         inst->block = 32 * (K + 1);
         inst->grid = (L.n_tiles + K - 1) / K;

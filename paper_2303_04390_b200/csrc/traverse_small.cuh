@@ -486,6 +486,39 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     const size_t u_lane = (size_t)pat * R * VB + r * VB + h * VBL;
     unsigned char *xg = xb + (lane / LV) * Cfg::XGS;               // my group's exchange row
     auto stack_at = [&](int slot) -> unsigned char * { return stackb + (slot * 32 + lane) * VBL; };
+    // stack slots as 16-B planes [slot][plane][lane]: a lane's 32-B part at a
+    // 32-B lane stride cost 2-way bank conflicts per 128-bit access (dengue
+    // fp64 traversal 1.493 -> 1.434 ms, scripts/gpu_ss.sh; PG_STACK_INTERLEAVED
+    // restores the old layout)
+    constexpr int NPL = VBL > 16 ? VBL / 16 : 1, PLB = VBL > 16 ? 16 : VBL;
+    auto stk_ld = [&](Real (&v)[VL], int slot) {
+#ifndef PG_STACK_INTERLEAVED
+        constexpr int PE = PLB / (int)sizeof(Real);
+#pragma unroll
+        for (int c = 0; c < NPL; ++c) {
+            Real t[PE];
+            lds_vec<Real, PE>(t, stackb + ((slot * NPL + c) * 32 + lane) * PLB);
+#pragma unroll
+            for (int i = 0; i < PE; ++i) v[c * PE + i] = t[i];
+        }
+#else
+        lds_vec<Real, VL>(v, stack_at(slot));
+#endif
+    };
+    auto stk_st = [&](int slot, const Real (&v)[VL]) {
+#ifndef PG_STACK_INTERLEAVED
+        constexpr int PE = PLB / (int)sizeof(Real);
+#pragma unroll
+        for (int c = 0; c < NPL; ++c) {
+            Real t[PE];
+#pragma unroll
+            for (int i = 0; i < PE; ++i) t[i] = v[c * PE + i];
+            sts_vec<Real, PE>(stackb + ((slot * NPL + c) * 32 + lane) * PLB, t);
+        }
+#else
+        sts_vec<Real, VL>(stack_at(slot), v);
+#endif
+    };
     auto release = [&](int t) {                      // after step t's last use of its stage
         if (!last_in_stage(t)) return;
         __syncwarp();
@@ -533,7 +566,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
 #pragma unroll
             for (int s = 0; s < VL; ++s) u[s] = prev_u[s];
         } else {
-            lds_vec<Real, VL>(u, stack_at(sl));
+            stk_ld(u, sl);
         }
     };
     for (int t = 0; t < nops; ++t) {
@@ -580,7 +613,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             if (warp == 0) PG_TSTAMP((size_t)t * 16 + 7, u[0] + u[VL - 1]);
             release(t);
             stg_vec<Real, VL>(Ub + (size_t)(op.x - N) * u_node + u_lane, u);   // shadow lanes: same value
-            sts_vec<Real, VL>(stack_at(op.w), u);
+            stk_st(op.w, u);
 #pragma unroll
             for (int s = 0; s < VL; ++s) prev_u[s] = u[s];
             prev_slot = op.w;
@@ -608,7 +641,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     }
     const Real *Qs = reinterpret_cast<const Real *>(smem + Cfg::QOFF);
     // next op decoded early
-    sts_vec<Real, VL>(stack_at(pi_slot), pi);
+    stk_st(pi_slot, pi);
     Op4 opn = {0, 0, 0, 0};
     if (active && nops > 0) {
         wait_full(nops);
@@ -628,7 +661,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
         // step's pushes through registers measured slower here (more
         // instructions than the shared-memory round trip it saves)
         Real q[VL];
-        lds_vec<Real, VL>(q, stack_at(op.x < 0 ? pi_slot : op.x));
+        stk_ld(q, op.x < 0 ? pi_slot : op.x);
         const int cs[2] = {op.y, op.z};
         const int slots[2] = {(op.w & 0xffff) - 1, (op.w >> 16) - 1};
         Real uc[2][VL];
@@ -690,7 +723,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             ndw[c * 32] = make_double2(gwr * (double)num, wr * (double)den);
             if (slots[c] >= 0) {
                 maybe_rescale<Real, VL, G>(qc[c]);
-                sts_vec<Real, VL>(stack_at(slots[c]), qc[c]);
+                stk_st(slots[c], qc[c]);
             }
         }
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 7, qc[0][0] + qc[1][0]);

@@ -404,3 +404,14 @@ def test_hmc_leapfrog_matches_oracle_trajectory(model, N, R, C):
     assert torch.equal(pm, p_before)
     assert abs(out[0].item() - lg_ref) <= 1e-10 * abs(lg_ref)
     inst.close()
+
+
+@pytest.mark.parametrize("env", [{"PG_CODON_FLOW": "0"}, {"PG_FLOW_TCH": "3"}, {"PG_FLOW_TCH": "1"}])
+def test_codon_schedules(env, monkeypatch):
+    """The level-by-level codon kernels (PG_CODON_FLOW=0) and other flow chunk
+    sizes give the same parity as the default one-launch schedule (read when
+    the instance plans its launches)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _compare(ps.config3_yeast(N=24, C=150))
+    _compare(ps.config5_yeast_mmm(N=10, C=70))
