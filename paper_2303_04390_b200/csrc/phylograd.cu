@@ -101,7 +101,7 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
     L->n_tiles = L->Cpad / L->tpl;
     L->B = (int)(2 * N - 2);
     // small-S kernels read P with a padded category stride (SmallCfg::CS)
-    L->cat_stride = SP * SP + ((L->variant == 0 && R > 1) ? (int)(16 / L->real) : 0);
+    L->cat_stride = SP * SP + ((L->variant == 0 && R > 1) ? pg::small_cat_pad(L->real, SP) / L->real : 0);
     const size_t mats = (size_t)L->B * R * L->cat_stride * L->real;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t at = o; o = align_up(o + bytes); return at; };

@@ -62,6 +62,18 @@ namespace pg {
 __host__ __device__ constexpr int small_lanes_per_vector(int SP, int RP) {
     return SP == 4 ? PG_SP4_LV : SP == 16 ? (PG_SP16_LV < 32 / RP ? PG_SP16_LV : 32 / RP) : SP / 4;
 }
+// bytes between consecutive category matrices beyond SP*SP Reals (R > 1):
+// shifts each category's matrix to other shared-memory banks so the lanes of
+// different categories reading the same row (matvec) or column (tip gather)
+// do not collide; fp64 S = 4 matrices are exactly 32 banks long and need an
+// 8-bank (32 B) shift for the column reads of tip children
+__host__ __device__ constexpr int small_cat_pad(int real_bytes, int SP) {
+#ifdef PG_CATPAD16
+    return 16;
+#else
+    return (real_bytes == 8 && SP == 4) ? 32 : 16;
+#endif
+}
 // consumer warps per CTA at most (launch bounds: + 1 producer warp)
 __host__ __device__ constexpr int small_max_consumers(int SP, int RP) { return small_lanes_per_vector(SP, RP) * 4 / SP >= 2 ? 17 : 9; }
 
@@ -86,7 +98,7 @@ struct SmallCfg {
     static constexpr int VB = SP * (int)sizeof(Real);          // vector bytes
     static constexpr int VBL = VL * (int)sizeof(Real);         // one lane's part of a vector
     static constexpr int MATB = SP * SP * (int)sizeof(Real);   // one category's matrix
-    static constexpr int CS = MATB + (RP > 1 ? 16 : 0);        // padded category stride
+    static constexpr int CS = MATB + (RP > 1 ? small_cat_pad(sizeof(Real), SP) : 0);   // padded category stride
     static constexpr int ND = W * 2 * 32 * 16;                 // (num, den) window per warp
     static constexpr int XGS = VB + 16;                        // exchange stride per lane group (bank skew)
     static constexpr int XB = LV > 1 ? (32 / LV) * XGS : 0;    // full-vector exchange buffer per warp
