@@ -409,6 +409,7 @@ struct FlowArgs {
     int *rpost;        // [N-1][nch] completed post items per (internal node, chunk)
     int *rpre;         // [N-1][nch] completed q writes per (internal node, chunk)
     int npost, ntask, tch, nch;
+    int defer;         // 1: pre items compute q only; Eq. 8 items (one per pre item) come after all of them
     unsigned long long *trace;   // diagnostics (PG_FLOW_TRACE): [item][TRW] = {smid, t_take, t_ready, t_done, phase stamps}
 };
 
@@ -424,7 +425,9 @@ struct FlowArgs {
 template <int SP>
 __device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int r, int tile, unsigned char *smem_c,
                                         unsigned long long *stamp = nullptr, const FlowArgs *fl = nullptr,
-                                        int fch = 0) {
+                                        int fch = 0, int mode = 0) {
+    // mode 0: q of the children and their Eq. 8 terms; 1: q only (phase A);
+    // 2: Eq. 8 terms only (phase B; q_k read back from HBM)
     CODON_GEO;
     double *Qs = reinterpret_cast<double *>(smem_c);
     double *Us[2] = {Qs + TILE, Qs + 2 * TILE};
@@ -490,7 +493,7 @@ __device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int 
     // children, x_c = q_k o u_sibling formed in X; published (flow schedule)
     // before the Eq. 8 terms, which no later item waits for ---------------
 #pragma unroll 1
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < 2 && mode != 2; ++c) {
         const int node = ch[c];
         if (node < a.N) continue;
         const size_t br = (size_t)node * a.R + r;
@@ -530,6 +533,7 @@ __device__ __forceinline__ void pre_tile(const CodonArgs &a, const int4 lv, int 
             if (ch[1] >= a.N) atomicAdd(fl->rpre + (size_t)(ch[1] - a.N) * fl->nch + fch, 1);
         }
     }
+    if (mode == 1) return;
     // --- phase B: Eq. 8 terms of both children ---------------------------
     // num_c = x_c'(Q u_c) with x_c = q_k o u_sibling; den = x_c'u_c is the
     // same for both children (q_k o u_a o u_b, Eq. 5).
@@ -687,15 +691,19 @@ __global__ void __launch_bounds__(codon_threads<SP>(), codon_ctas_per_sm<SP>()) 
     extern __shared__ __align__(16) unsigned char smem_c[];
     __shared__ int s_item;
     int4 *tab = reinterpret_cast<int4 *>(smem_c + post_smem<SP>());
-    const int per_task = a.R * f.nch, nitems = f.ntask * per_task;
+    const int per_task = a.R * f.nch;
+    const int npre = f.ntask - f.npost;
+    const int nitems = (f.ntask + (f.defer ? npre : 0)) * per_task;
     const int root = 2 * a.N - 2;
     for (;;) {
         if (threadIdx.x == 0) s_item = atomicAdd(f.ctr, 1);
         __syncthreads();
         const int item = s_item;
         if (item >= nitems) return;
-        const int task = item / per_task, rem = item - task * per_task;
+        const int vtask = item / per_task, rem = item - vtask * per_task;
         const int r = rem / f.nch, ch = rem - r * f.nch;
+        const bool grad_item = vtask >= f.ntask;            // deferred Eq. 8 item of pre task vtask - npre
+        const int task = grad_item ? vtask - npre : vtask;
         const int4 e = a.lev4[task];
         const int t0 = ch * f.tch, t1 = min(a.ntiles, t0 + f.tch);
         const bool post = task < f.npost;
@@ -741,7 +749,8 @@ __global__ void __launch_bounds__(codon_threads<SP>(), codon_ctas_per_sm<SP>()) 
             // q GEMMs and before its Eq. 8 terms (earlier tiles are complete)
             for (int tile = t0; tile < t1; ++tile) {
                 pre_tile<SP>(a, e, r, tile, smem_c, f.trace ? f.trace + TRW * (size_t)item + 4 : nullptr,
-                         tile == t1 - 1 ? &f : nullptr, ch);
+                         (tile == t1 - 1 && !grad_item) ? &f : nullptr, ch,
+                         grad_item ? 2 : (f.defer ? 1 : 0));
                 __syncthreads();
             }
         }
