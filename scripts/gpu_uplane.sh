@@ -1,4 +1,4 @@
-# small-S traversal: u stored as 16-B planes (working tree) vs HEAD
+# small-S traversal: working tree vs HEAD
 for rep in 1 2; do
 for f in "" head; do
   if [ -n "$f" ]; then export PHYLOGRAD_LIB=$PWD/paper_2303_04390_b200/lib/libphylograd_$f.so; else unset PHYLOGRAD_LIB; fi
