@@ -206,6 +206,7 @@ struct pg_instance {
     int prefetch = 4, smem = 0, grid = 0, block = 0, tiles_per_cta = 1, prog_smem_off = 0;
     int flow_tch = 0;                   // codon: tiles per flow item (0 = level-by-level kernels)
     int flow_defer = 0;                 // codon flow: Eq. 8 items after all pre items (PG_FLOW_DEFER)
+    int flow_half = 0;                  // codon flow: half-tile post items when tch == 1 (PG_FLOW_HALF)
     unsigned long long *flow_trace = nullptr;   // PG_FLOW_TRACE=<file>: per-item timestamps (diagnostics)
     size_t flow_trace_n = 0;
     cudaGraphExec_t gexec = nullptr;
@@ -799,6 +800,8 @@ static int configure(pg_instance *inst) {
         }
         const char *de = getenv("PG_FLOW_DEFER");
         inst->flow_defer = de ? (atoi(de) != 0) : 0;
+        const char *he = getenv("PG_FLOW_HALF");
+        inst->flow_half = he ? (atoi(he) != 0) : 0;
         if (getenv("PG_FLOW_TRACE") && inst->flow_tch > 0) {    // diagnostics buffer (allocated before capture)
             const size_t items = inst->plan.level_nodes.size() * (size_t)R *
                                  ((L.n_tiles + inst->flow_tch - 1) / inst->flow_tch);
@@ -984,8 +987,9 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
             f.npost = pl.post_off.back();
             f.ntask = (int)pl.level_nodes.size();
             f.defer = inst->flow_defer;
+            f.phalf = (inst->flow_half && f.tch == 1) ? 2 : 1;
             const int npre = f.ntask - f.npost;
-            const int items = (f.ntask + (f.defer ? npre : 0)) * R * f.nch;
+            const int items = f.npost * R * f.nch * f.phalf + (npre + (f.defer ? npre : 0)) * R * f.nch;
             f.trace = inst->flow_trace_n == (size_t)items ? inst->flow_trace : nullptr;
             void *args[] = {&c, &f};
             CK(cudaLaunchKernel(cf.flow, dim3(std::min(items, cf.ctas_per_sm * inst->sm_count)),

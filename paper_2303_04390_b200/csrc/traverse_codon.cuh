@@ -410,6 +410,7 @@ struct FlowArgs {
     int *rpre;         // [N-1][nch] completed q writes per (internal node, chunk)
     int npost, ntask, tch, nch;
     int defer;         // 1: pre items compute q only; Eq. 8 items (one per pre item) come after all of them
+    int phalf;         // 2: post items are half tiles (16 patterns; needs tch == 1): shorter chain links
     unsigned long long *trace;   // diagnostics (PG_FLOW_TRACE): [item][TRW] = {smid, t_take, t_ready, t_done, phase stamps}
 };
 
@@ -691,17 +692,32 @@ __global__ void __launch_bounds__(codon_threads<SP>(), codon_ctas_per_sm<SP>()) 
     extern __shared__ __align__(16) unsigned char smem_c[];
     __shared__ int s_item;
     int4 *tab = reinterpret_cast<int4 *>(smem_c + post_smem<SP>());
-    const int per_task = a.R * f.nch;
+    const int per_task = a.R * f.nch, per_post = per_task * f.phalf;
     const int npre = f.ntask - f.npost;
-    const int nitems = (f.ntask + (f.defer ? npre : 0)) * per_task;
+    const int npost_items = f.npost * per_post;
+    const int nitems = npost_items + (npre + (f.defer ? npre : 0)) * per_task;
+    const int post_full = a.R * f.phalf;                   // completed post items per (node, chunk)
     const int root = 2 * a.N - 2;
     for (;;) {
         if (threadIdx.x == 0) s_item = atomicAdd(f.ctr, 1);
         __syncthreads();
         const int item = s_item;
         if (item >= nitems) return;
-        const int vtask = item / per_task, rem = item - vtask * per_task;
-        const int r = rem / f.nch, ch = rem - r * f.nch;
+        int vtask, r, ch, half = 0;
+        if (item < npost_items) {
+            vtask = item / per_post;
+            const int rem = item - vtask * per_post;
+            r = rem / (f.nch * f.phalf);
+            const int rem2 = rem - r * f.nch * f.phalf;
+            ch = rem2 / f.phalf;
+            half = rem2 - ch * f.phalf;
+        } else {
+            const int i2 = item - npost_items;
+            vtask = f.npost + i2 / per_task;
+            const int rem = i2 - (vtask - f.npost) * per_task;
+            r = rem / f.nch;
+            ch = rem - r * f.nch;
+        }
         const bool grad_item = vtask >= f.ntask;            // deferred Eq. 8 item of pre task vtask - npre
         const int task = grad_item ? vtask - npre : vtask;
         const int4 e = a.lev4[task];
@@ -726,8 +742,8 @@ __global__ void __launch_bounds__(codon_threads<SP>(), codon_ctas_per_sm<SP>()) 
         }
         if (threadIdx.x == 0) {
             if (post || e.x == root) {
-                if (e.y >= a.N) wait_count(f.rpost + (size_t)(e.y - a.N) * f.nch + ch, a.R);
-                if (e.z >= a.N) wait_count(f.rpost + (size_t)(e.z - a.N) * f.nch + ch, a.R);
+                if (e.y >= a.N) wait_count(f.rpost + (size_t)(e.y - a.N) * f.nch + ch, post_full);
+                if (e.z >= a.N) wait_count(f.rpost + (size_t)(e.z - a.N) * f.nch + ch, post_full);
             } else {
                 wait_count(f.rpre + (size_t)(e.x - a.N) * f.nch + ch, a.R);
             }
@@ -741,7 +757,10 @@ __global__ void __launch_bounds__(codon_threads<SP>(), codon_ctas_per_sm<SP>()) 
             }
         }
         __syncthreads();
-        if (post) {
+        if (post && f.phalf == 2) {                   // one 16-pattern half of tile t0 (tch == 1)
+            const int b = (r * a.ntiles + t0) * 2 + half;
+            post_range<SP, 2, false>(a, tab, b, b + 1, smem_c, f.trace ? f.trace + TRW * (size_t)item + 4 : nullptr);
+        } else if (post) {
             post_range<SP, 4, false>(a, tab, r * a.ntiles + t0, r * a.ntiles + t1, smem_c,
                           f.trace ? f.trace + TRW * (size_t)item + 4 : nullptr);
         } else {

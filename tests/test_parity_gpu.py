@@ -407,7 +407,8 @@ def test_hmc_leapfrog_matches_oracle_trajectory(model, N, R, C):
 
 
 @pytest.mark.parametrize("env", [{"PG_CODON_FLOW": "0"}, {"PG_FLOW_TCH": "3"}, {"PG_FLOW_TCH": "1"},
-                                 {"PG_FLOW_DEFER": "1"}, {"PG_FLOW_DEFER": "0"}])
+                                 {"PG_FLOW_DEFER": "1"}, {"PG_FLOW_DEFER": "0"}, {"PG_FLOW_HALF": "1"},
+                                 {"PG_FLOW_HALF": "1", "PG_FLOW_DEFER": "1"}])
 def test_codon_schedules(env, monkeypatch):
     """The level-by-level codon kernels (PG_CODON_FLOW=0) and other flow chunk
     sizes give the same parity as the default one-launch schedule (read when
