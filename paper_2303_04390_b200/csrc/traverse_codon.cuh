@@ -119,9 +119,6 @@ __device__ __forceinline__ void load_block(double *dst, const double *src, int n
         reinterpret_cast<double2 *>(dst)[i] = __ldg(reinterpret_cast<const double2 *>(src) + i);
 }
 
-// pattern index of fragment-order position idx
-template <int SP>
-__device__ __forceinline__ int apos_m(int idx) { return (int)((unsigned)idx / (8u * SP)) * 8 + ((idx & 31) >> 2); }
 
 // Fill a tile with child vectors for category r: internal (u from HBM) or tip
 // (rows of P' picked by the pattern's state: u_tip[s] = P[s][state]).  Flat
