@@ -93,7 +93,11 @@ struct SmallCfg {
 #else
     static constexpr int D = PG_STAGES;
 #endif
-    static constexpr int PF = 16;                              // L2 prefetch distance (steps)
+#ifdef PG_PF
+    static constexpr int PF = PG_PF;
+#else
+    static constexpr int PF = 32;                              // L2 prefetch distance (steps; 16: +0.4 %, scripts/gpu_pf.sh)
+#endif
     static constexpr int W = PG_SMALL_W;                       // gradient window (steps)
     static constexpr int VB = SP * (int)sizeof(Real);          // vector bytes
     static constexpr int VBL = VL * (int)sizeof(Real);         // one lane's part of a vector
