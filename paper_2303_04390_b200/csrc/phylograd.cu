@@ -753,7 +753,15 @@ static int configure(pg_instance *inst) {
         int K = std::max(1, std::min(pg::small_max_consumers(L.SP, pad_categories(R)),
                                      (L.n_tiles + inst->sm_count - 1) / inst->sm_count));
         while (K > 1 && small_smem(L, R, K, depth) > 227 * 1024) --K;
-        if (const char *ke = getenv("PG_SMALL_K")) K = std::max(1, std::min(K, atoi(ke)));   // experiments
+        // fp32 S = 4: three CTAs of K = 3 per SM (three producers) beat one
+        // CTA of K = 9 when all tiles still fit in one wave (dengue fp32
+        // 1.293 -> 1.268 ms, scripts/gpu_smallk.sh)
+        const char *ke = getenv("PG_SMALL_K");                      // experiments (ignored unless > 0)
+        if (ke && atoi(ke) > 0)
+            K = std::min(K, atoi(ke));
+        else if (L.real == 4 && L.SP == 4 && K > 3 && 3 * (small_smem(L, R, 3, depth) + 1024) <= 228 * 1024 &&
+                 (L.n_tiles + 2) / 3 <= 3 * inst->sm_count)
+            K = 3;
         inst->tiles_per_cta = K;
         inst->block = 32 * (K + 1);
         inst->grid = (L.n_tiles + K - 1) / K;
