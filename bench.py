@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
     ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between timed steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra-configs", action="store_true",
+                    help="skip the codon / MMM workloads timed beside the default dengue line")
+    ap.add_argument("--no-fp64-probe", action="store_true", help="skip the in-run FP64 peak measurement")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the baseline sample")
     ap.add_argument("--virtual-shard", type=int, default=0, metavar="G",
                     help="evidence runs only: time rank 0's pattern shard of a G-GPU run on this one GPU "
@@ -137,43 +140,42 @@ class ClockSampler:
 
 # ----------------------------------------------------------- roofline ----
 
-def algorithmic_bytes(pb, C: int, precision: str) -> int:
-    """Compulsory HBM bytes of one traversal launch:
-    u = P p of every internal non-root node written once (post) and read once
-    (pre): 2 (N-2) R C SP w; tip codes read once per pass: 2 N C; pattern
-    weights 8 C.  SP = padded states."""
+def padded_states(S: int) -> int:
+    return 4 if S <= 4 else 8 if S <= 8 else 16 if S <= 16 else 32 if S <= 32 else 64 if S <= 64 else 128
+
+
+def hbm_counts(pb, C: int, precision: str) -> dict:
+    """Byte counts of one evaluation over C patterns; V = R C Sp w
+    is one node's partials.
+      b_min     5 (N-2) V + tips + 8 (N-1) C: the roofline basis (u written once
+                and read twice, q written and read once, tip codes read twice,
+                int32 scale exponents written and read); tips = 2 N C (int8
+                codes) or 2 N C Sp w (partial tips, MMM);
+      schedule  what this build's one-launch walk must move: 2 (N-2) V (u
+                written once, read once; q never leaves the chip) + tips + 8 C;
+      paper     (10N - 13) V, the paper-literal per-node schedule."""
     N, S, R = pb.n_tips, pb.states, len(pb.cat_rates)
-    SP = 4 if S <= 4 else 8 if S <= 8 else 16 if S <= 16 else 32 if S <= 32 else 64 if S <= 64 else 128
+    Sp = padded_states(S)
     w = 8 if precision == "fp64" else 4
-    tips = 2 * N * C if pb.tip_partials is None else 2 * N * C * SP * w
-    return 2 * (N - 2) * R * C * SP * w + tips + 8 * C
+    V = R * C * Sp * w
+    tips = 2 * N * C if pb.tip_partials is None else 2 * N * C * Sp * w
+    return {"b_min": 5 * (N - 2) * V + tips + 8 * (N - 1) * C,
+            "schedule": 2 * (N - 2) * V + tips + 8 * C,
+            "paper": (10 * N - 13) * V}
 
 
-def algorithmic_flops(pb, C: int) -> int:
-    """Minimal flops of one evaluation: 3 (N-2) matvecs of
-    2 S^2 per (pattern, category) with unpadded S."""
+def flop_counts(pb, C: int) -> dict:
+    """f_min = 3 (N-2) 2 S^2 R C (unpadded S); paper-literal
+    (6N - 8) 2 Sp^2 R C."""
     N, S, R = pb.n_tips, pb.states, len(pb.cat_rates)
-    return 3 * (N - 2) * 2 * S * S * R * C
-
-
-def alu_roofline(pb, C, trav_ms, peaks, precision, abytes, traffic):
-    """S > 64 (and fp32 S > 16): the SIMT large-state kernel is bound by plain
-    FP64 (FP32) FMA throughput, not HBM: achieved = minimal flops / launch time
-    against the measured DFMA peak (derived FFMA peak for fp32)."""
-    fl = algorithmic_flops(pb, C)
-    ach = fl / (trav_ms * 1e-3) / 1e12
-    pk, src = ((peaks["dfma_tflops"], peaks["dfma_src"]) if precision == "fp64"
-               else (peaks["ffma_tflops"], peaks["ffma_src"]))
-    return {"bound": "alu", "achieved": round(ach, 3), "peak": round(pk, 2), "unit": "TFLOP/s",
-            "frac": round(ach / pk, 4), "traffic": traffic, "kernel": "traverse_large_kernel (SIMT)",
-            "algorithmic_flops_per_eval": fl, "kernel_ms": round(trav_ms, 5), "hbm_algorithmic_bytes": abytes,
-            "peak_source": src}
+    Sp = 64 if S <= 64 else 128
+    return {"f_min": 3 * (N - 2) * 2 * S * S * R * C, "paper": (6 * N - 8) * 2 * Sp * Sp * R * C}
 
 
 def load_peaks():
-    """HBM: MEASURED_PEAKS.json (driver-written copy bandwidth).  FP64 tensor:
-    our DMMA microbenchmark on this pool's B200 (scripts/fp64_peak.cu ->
-    profiles/r01/fp64_peak.json); MEASURED_PEAKS.json has no FP64 entry."""
+    """HBM: MEASURED_PEAKS.json (driver-written copy bandwidth).  FP64: measured
+    inside this bench run (probe_fp64, below) when it ran, else our committed
+    microbenchmark (profiles/r01/fp64_peak.json)."""
     out = {}
     try:
         d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -182,41 +184,112 @@ def load_peaks():
         out.update(hbm_gbs=6650.0, hbm_src="fallback (B200_PROFILING.md)")
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "r01", "fp64_peak.json")))
-        out.update(fp64_tflops=float(d["dmma_tflops"]),
-                   fp64_src="measured (mma.sync f64 DMMA microbenchmark, profiles/r01/fp64_peak.json)")
+        out.update(fp64_tflops=float(d["dmma_tflops"]), dfma_tflops=float(d["dfma_tflops"]),
+                   fp64_src="committed DMMA microbenchmark (profiles/r01/fp64_peak.json)",
+                   dfma_src="committed DFMA microbenchmark (profiles/r01/fp64_peak.json)")
     except Exception:
-        out.update(fp64_tflops=37.0, fp64_src="fallback (B200 datasheet FP64 tensor ~37-40 TF/s)")
-    try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r01", "fp64_peak.json")))
-        out.update(dfma_tflops=float(d["dfma_tflops"]),
-                   dfma_src="measured (DFMA microbenchmark, profiles/r01/fp64_peak.json)")
-    except Exception:
-        out.update(dfma_tflops=36.0, dfma_src="fallback (B200 FP64 ~37 TF/s)")
+        out.update(fp64_tflops=37.0, dfma_tflops=36.0, fp64_src="fallback (~37 TF/s)", dfma_src="fallback")
     # FP32 FFMA: 148 SMs x 128 lanes x 2 flops x 1.965 GHz (guide unit counts, max clock)
     out.update(ffma_tflops=148 * 128 * 2 * 1.965e9 / 1e12, ffma_src="derived: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz")
     return out
 
 
-def load_traffic(cfg: int, precision: str):
-    """DRAM bytes per traversal launch from a committed ncu --set full capture
+def probe_fp64(peaks, device: int):
+    """FP64 DMMA / DFMA peaks measured now, on this GPU, with clocks sampled
+    during the probe (lib/libpgprobe.so, csrc/probe.cu)."""
+    import ctypes
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_2303_04390_b200", "lib", "libpgprobe.so"))
+    dm, df, n = ctypes.c_double(0), ctypes.c_double(0), ctypes.c_int(0)
+    with ClockSampler(device) as clk:
+        rc = lib.pgprobe_fp64_peak(int(device), ctypes.c_float(1500.0), ctypes.byref(dm), ctypes.byref(df),
+                                   ctypes.byref(n))
+    if rc != 0:
+        return {"error": f"probe rc {rc}"}
+    peaks.update(fp64_tflops=dm.value, dfma_tflops=df.value,
+                 fp64_src="measured in this run (mma.sync m8n8k4 f64 DMMA probe, csrc/probe.cu)",
+                 dfma_src="measured in this run (DFMA probe, csrc/probe.cu)")
+    return {"dmma_tflops": round(dm.value, 3), "dfma_tflops": round(df.value, 3), "launches": n.value,
+            "how": "best launch of 592 CTAs x 8 warps, ~1.5 s per probe", "clocks": clk.summary()}
+
+
+def traffic_key(cfg: int, precision: str, shard: int = 1, patterns: int = 0) -> str:
+    k = f"config{cfg}_{precision}"
+    if shard > 1:
+        k += f"_shard{shard}"
+    if patterns > 0:
+        k += f"_C{patterns}"
+    return k
+
+
+def load_traffic(key: str):
+    """DRAM bytes (read + write) per launch of the dominant kernel from a
+    committed ncu --set full capture of exactly this workload
     (profiles/ncu_traffic.json), or None."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        d = json.load(open(p)).get(f"config{cfg}_{precision}")
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(key)
         return None if d is None else d["bytes"]
     except Exception:
         return None
 
 
+def roofline(pb, C: int, variant: int, precision: str, kms: dict, peaks: dict, traffic, flow: bool) -> dict:
+    """Roofline object of the dominant kernel (the traversal) on SURVEY §8(d)'s
+    algorithmic basis: B_min for the HBM-bound S <= 16 paths, F_min for the
+    FP64 tensor path; the schedule / paper-literal / ncu-DRAM figures beside."""
+    t = kms["traverse"] * 1e-3
+    ev = (kms["pmat"] + kms["traverse"] + kms["reduce"]) * 1e-3
+    if variant == 2 or variant == 1:
+        fl = flop_counts(pb, C)
+        hb = hbm_counts(pb, C, precision)
+        if variant == 2:
+            pk, unit, bound, src = peaks["fp64_tflops"], "TFLOP/s", "tensor", peaks["fp64_src"]
+            kname = ("codon_flow_kernel (post + pre order, one launch)" if flow
+                     else "codon_post_kernel + codon_pre_kernel (all levels of one evaluation)")
+        else:
+            pk, src = ((peaks["dfma_tflops"], peaks["dfma_src"]) if precision == "fp64"
+                       else (peaks["ffma_tflops"], peaks["ffma_src"]))
+            unit, bound, kname = "TFLOP/s", "alu", "traverse_large_kernel (SIMT)"
+        ach = fl["f_min"] / t / 1e12
+        r = {"bound": bound, "achieved": round(ach, 3), "peak": round(pk, 3), "unit": unit,
+             "frac": round(ach / pk, 4), "traffic": traffic, "kernel": kname,
+             "basis": "SURVEY §8(d) F_min = 3(N-2) 2 S^2 R C (unpadded S) per launch",
+             "algorithmic_flops_per_launch": fl["f_min"], "kernel_ms": round(kms["traverse"], 5),
+             "eval_ms": round(ev * 1e3, 5), "eval_frac": round(fl["f_min"] / ev / 1e12 / pk, 4),
+             "paper_literal": {"flops": fl["paper"], "frac": round(fl["paper"] / t / 1e12 / pk, 4)},
+             "peak_source": src}
+        if traffic:
+            r["dram_frac_ncu"] = round(traffic / t / 1e9 / peaks["hbm_gbs"], 4)
+            r["hbm_b_min_frac"] = round(hb["b_min"] / t / 1e9 / peaks["hbm_gbs"], 4)
+        return r
+    hb = hbm_counts(pb, C, precision)
+    ach = hb["b_min"] / t / 1e9
+    pk = peaks["hbm_gbs"]
+    r = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk, "unit": "GB/s", "frac": round(ach / pk, 4),
+         "traffic": traffic, "kernel": "traverse_small_kernel",
+         "basis": "SURVEY §8(d) B_min = 5(N-2)V + 2NC + 8(N-1)C, V = R C Sp w (per launch)",
+         "algorithmic_bytes_per_launch": hb["b_min"], "kernel_ms": round(kms["traverse"], 5),
+         "eval_ms": round(ev * 1e3, 5), "eval_frac": round(hb["b_min"] / ev / 1e9 / pk, 4),
+         "schedule_bytes_per_launch": hb["schedule"],
+         "schedule_frac": round(hb["schedule"] / t / 1e9 / pk, 4),
+         "paper_literal": {"bytes": hb["paper"], "frac": round(hb["paper"] / t / 1e9 / pk, 4)},
+         "peak_source": peaks["hbm_src"]}
+    if traffic:
+        r["dram_frac_ncu"] = round(traffic / t / 1e9 / pk, 4)
+    return r
+
+
+def pct(xs, q):
+    return float(np.percentile(np.asarray(xs), q))
+
+
 # ------------------------------------------------------------ CPU oracle ----
 
-def cpu_oracle_rate(pb, seconds: float):
-    """Oracle evals/s on a bounded pattern sample, all host cores."""
+def cpu_oracle_rate(pb, seconds: float, threads: int):
+    """Oracle evals/s on a bounded pattern sample with `threads` host threads
+    (pattern blocks run concurrently, the paper's CPU parallelisation P:78)."""
     import oracle
-    threads = os.cpu_count() or 1
     C = pb.patterns
-    # calibrate on a small sample, then size the sample to ~`seconds`
-    m0 = min(C, max(threads * 4, 64))
+    m0 = min(C, max(threads * 4, 16))
     t0 = time.perf_counter()
     oracle.loglik_grad(pb, 0, m0, threads=threads, block=max(1, m0 // threads))
     dt0 = time.perf_counter() - t0
@@ -232,7 +305,71 @@ def cpu_oracle_rate(pb, seconds: float):
             "sample": f"patterns [0,{m}) of {C} (full tree) x {reps} evaluation(s), {dt:.1f} s, scaled by C/{m}"}
 
 
+def workload_config(args, pb, C, world, lo=0, hi=None, flushed=True, shard=0):
+    """The `config` object (identical in both arms)."""
+    return {"workload": workload_name(args.config, C), "tips": pb.n_tips, "patterns": C,
+            "states": pb.states, "categories": len(pb.cat_rates), "precision": args.precision,
+            "l2": "flushed (256 MiB write) between timed steps" if flushed else "not flushed",
+            "parallelism": (f"pattern-shard x{world}" if shard <= 1 else
+                            f"virtual: rank 0's shard [{lo},{hi}) of x{shard}, on 1 GPU"),
+            "branch_lengths": "seeded +-1% jitter per step"}
+
+
 # ------------------------------------------------------------------ ours ----
+
+def time_steps(step, stream, steps, warmup, flush, inst=None, sample_every=16):
+    """Warm-up, then `steps` steps each bracketed by CUDA events on `stream`
+    (L2 flushed outside the events); per-kernel split from the instance's
+    in-graph events on a sample of steps."""
+    import torch
+    with torch.cuda.stream(stream):
+        for i in range(warmup):
+            step(i)
+        stream.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        kt = {"pmat": 0.0, "traverse": 0.0, "reduce": 0.0}
+        ns = 0
+        for k in range(steps):
+            if flush is not None:
+                flush.zero_()
+            evs[k][0].record(stream)
+            step(warmup + k)
+            evs[k][1].record(stream)
+            if inst is not None and (k % sample_every == 0 or k == steps - 1):
+                t = inst.kernel_times()
+                for n in kt:
+                    kt[n] += t[n]
+                ns += 1
+        stream.synchronize()
+    ms = [a.elapsed_time(b) for a, b in evs]
+    return ms, {n: v / max(ns, 1) for n, v in kt.items()}
+
+
+def bench_instance(pb, precision, device, lo, hi, steps, warmup, flush, seed_off=99):
+    """Single-process timing of one (shard of a) workload; returns stats."""
+    import torch
+    import paper_2303_04390_b200 as pg
+    dev = torch.device("cuda", device)
+    inst = pg.from_problem(pb, precision=precision, device=device, lo=lo, hi=hi)
+    B = 2 * pb.n_tips - 2
+    out = torch.zeros(B + 1, dtype=torch.float64, device=dev)
+    rng = np.random.default_rng(ps.MASTER_SEED + seed_off)
+    bls = pb.branch_lengths[None, :] * rng.uniform(0.99, 1.01, size=(warmup + steps, B))
+    bl_dev = torch.tensor(bls, dtype=torch.float64, device=dev)
+
+    def step(i):
+        inst.set_branch_lengths_device(bl_dev[i])
+        inst.compute_device(out)
+
+    inst.set_kernel_timing(True)
+    ms, kt = time_steps(step, inst.stream, steps, warmup, flush, inst)
+    zp = inst.check_status()
+    assert zp < 0, f"zero likelihood at pattern {zp}"
+    info = inst.plan_info()
+    nk = inst.kernels_per_eval()
+    inst.set_kernel_timing(False)
+    return inst, ms, kt, info, nk, bls
+
 
 def run_ours(args):
     import torch
@@ -250,147 +387,146 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
+    peaks = load_peaks()
+    fp64_probe = None
+    if rank == 0 and world == 1 and not args.no_fp64_probe:
+        fp64_probe = probe_fp64(peaks, local)
+
     pb = make_problem(args.config, args.precision, args.patterns)
     C = pb.patterns
-    lo, hi = pg.shard_range(C, world, rank)
-    if args.virtual_shard > 1:
-        assert world == 1, "--virtual-shard is a single-process emulation"
-        lo, hi = pg.shard_range(C, args.virtual_shard, 0)
-    inst = pg.from_problem(pb, precision=args.precision, device=local, lo=lo, hi=hi)
-    stream = inst.stream
     B = 2 * pb.n_tips - 2
-    out = torch.zeros(B + 1, dtype=torch.float64, device=dev)
+    flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    shard = args.virtual_shard if args.virtual_shard > 1 else 0
+    if shard:
+        assert world == 1, "--virtual-shard is a single-process emulation"
+        lo, hi = pg.shard_range(C, shard, 0)
+    else:
+        lo, hi = pg.shard_range(C, world, rank)
 
-    # seeded +-1% branch-length jitter per step, resident on the device
     rng = np.random.default_rng(ps.MASTER_SEED + 99)
     nvar = args.warmup + args.steps
     bls = pb.branch_lengths[None, :] * rng.uniform(0.99, 1.01, size=(nvar, B))
     bl_dev = torch.tensor(bls, dtype=torch.float64, device=dev)
-    flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    # one CUDA graph per step: [branch lengths D2D, evaluation kernels, allreduce]
+    # at N > 1 (the library enqueues into the caller's capture)
+    ev = pg.ShardEvaluation(pb, rank=0 if shard else rank, world=shard or world, device=local,
+                            precision=args.precision, capture=world > 1, timing=True)
+    inst = ev.inst
 
     def step(i):
-        inst.set_branch_lengths_device(bl_dev[i])
-        inst.compute_device(out)
-        if world > 1:
-            pg.allreduce_evaluation(out)
+        with torch.cuda.stream(ev.stream):
+            ev.bl.copy_(bl_dev[i], non_blocking=True)
+        ev.evaluate()
 
-    inst.set_kernel_timing(True)
-    with torch.cuda.stream(stream):
-        for i in range(args.warmup):
-            step(i)
-        stream.synchronize()
-        zp = inst.check_status()
-        assert zp < 0, f"zero likelihood at pattern {zp}"
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)]
-        ktimes = {"pmat": 0.0, "traverse": 0.0, "reduce": 0.0}
-        with ClockSampler(local) as clk:
-            for k in range(args.steps):
-                if flush is not None:
-                    flush.zero_()
-                evs[k][0].record(stream)
-                step(args.warmup + k)
-                evs[k][1].record(stream)
-                if k % 16 == 0 or k == args.steps - 1:     # per-kernel split on a sample of steps
-                    t = inst.kernel_times()
-                    for n in ktimes:
-                        ktimes[n] += t[n]
-            stream.synchronize()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-    nsamp = len([k for k in range(args.steps) if k % 16 == 0 or k == args.steps - 1])
-    dev_ms = sum(a.elapsed_time(b) for a, b in evs)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms, kt = time_steps(step, ev.stream, args.steps, args.warmup, flush, inst)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    zp = ev.zero_pattern()
+    assert zp < 0, f"zero likelihood at pattern {zp}"
+    dev_ms = sum(ms)
     t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dev_ms = float(t.item())
     ms_per_step = dev_ms / args.steps
     value = 1000.0 / ms_per_step            # whole-job evaluations per second
-    kavg = {n: v / nsamp for n, v in ktimes.items()}
 
     # ---- end to end through the public API with host buffers ---------------
-    inst.set_kernel_timing(False)
     e2e_steps = max(10, min(args.steps, 200))
     host_out = torch.empty(B + 1, dtype=torch.float64, pin_memory=True)
+    host_bl = torch.empty(B, dtype=torch.float64, pin_memory=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for k in range(e2e_steps):
-        inst.set_branch_lengths(bls[k % nvar])
-        if world == 1:
-            logl, g = inst.compute()
+        if world == 1 and inst is not None:
+            inst.set_branch_lengths(bls[k % nvar])           # pg_set_branch_lengths (pinned staging)
+            logl, g = inst.compute()                           # pg_compute: H2D, graph, D2H, sync
         else:
-            with torch.cuda.stream(stream):
-                inst.compute_device(out)
-                pg.allreduce_evaluation(out)
-                host_out.copy_(out, non_blocking=True)
-            stream.synchronize()
+            host_bl.copy_(torch.from_numpy(bls[k % nvar]))
+            with torch.cuda.stream(ev.stream):
+                ev.bl.copy_(host_bl, non_blocking=True)
+                ev.evaluate()
+                host_out.copy_(ev.out, non_blocking=True)
+            ev.stream.synchronize()
     e2e_s = time.perf_counter() - t0
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_rate = e2e_steps / float(te.item())
 
-    # ---- parity spot check of this run's last evaluation (rank 0, N = 1) -----
     result = None
     if rank == 0:
-        peaks = load_peaks()
+        info = inst.plan_info() if inst is not None else {}
+        nk = inst.kernels_per_eval() if inst is not None else 0
+        variant = info.get("kernel_variant", 0)
         Cl = hi - lo
-        abytes = algorithmic_bytes(pb, Cl, args.precision)
-        trav_ms = kavg["traverse"]
-        achieved = abytes / (trav_ms * 1e-3) / 1e9
-        traffic = load_traffic(args.config, args.precision)
-        info = inst.plan_info()
-        tensor = info["kernel_variant"] == 2
+        traffic = load_traffic(traffic_key(args.config, args.precision, shard, args.patterns))
         result = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
+            "ms_step_p10_p50_p90": [round(pct(ms, 10), 5), round(pct(ms, 50), 5), round(pct(ms, 90), 5)],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": dtype_name(args.precision), "data": "synthetic",
-            "config": {"workload": workload_name(args.config, C), "tips": pb.n_tips, "patterns": C,
-                       "states": pb.states, "categories": len(pb.cat_rates),
-                       "precision": args.precision,
-                       "l2": "flushed (256 MiB write) between timed steps" if flush is not None else "not flushed",
-                       "parallelism": f"pattern-shard x{world}" if args.virtual_shard <= 1 else
-                                      f"virtual: rank 0's shard [{lo},{hi}) of x{args.virtual_shard}, on 1 GPU",
-                       "branch_lengths": "seeded +-1% jitter per step, device resident"},
+            "config": workload_config(args, pb, C, world, lo, hi, flush is not None, shard),
             "e2e": {"value": round(e2e_rate, 3), "unit": UNIT, "h2d_bytes_per_step": 8 * B,
-                    "d2h_bytes_per_step": 8 * (B + 1) + (4 if world == 1 else 0)},
-            "gpu_launches": args.steps * inst.kernels_per_eval(),
-            "roofline": alu_roofline(pb, Cl, trav_ms, peaks, args.precision, abytes, traffic)
-            if info["kernel_variant"] == 1 else
-            ({"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
-                          "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
-                          "traffic": traffic,
-                          "kernel": "traverse_small_kernel" if info["kernel_variant"] == 0 else "traverse_large_kernel",
-                          "algorithmic_bytes_per_launch": abytes, "kernel_ms": round(trav_ms, 5),
-                          "peak_source": peaks["hbm_src"]} if not tensor else
-                         {"bound": "tensor",
-                          "achieved": round(algorithmic_flops(pb, Cl) / (trav_ms * 1e-3) / 1e12, 3),
-                          "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
-                          "frac": round(algorithmic_flops(pb, Cl) / (trav_ms * 1e-3) / 1e12 / peaks["fp64_tflops"], 4),
-                          "traffic": traffic,
-                          "kernel": ("codon_flow_kernel (post + pre order, one launch)" if info.get("flow_tiles", 0) > 0
-                                     else "codon_post_kernel + codon_pre_kernel (all levels of one evaluation)"),
-                          "algorithmic_flops_per_eval": algorithmic_flops(pb, Cl), "kernel_ms": round(trav_ms, 5),
-                          "hbm_algorithmic_bytes": abytes, "peak_source": peaks["fp64_src"],
-                          "dtype_note": "fp64 on the FP64 tensor path (DMMA)"}),
-            "kernel_ms": {k: round(v, 5) for k, v in kavg.items()},
+                    "d2h_bytes_per_step": 8 * (B + 1) + (4 if world == 1 else 0),
+                    "path": ("pg_set_branch_lengths + pg_compute (host buffers)" if world == 1 else
+                             "pinned H2D of b, captured [b, evaluation, NCCL allreduce] graph, D2H of [logL, g]")},
+            "gpu_launches": args.steps * nk,
+            "roofline": roofline(pb, Cl, variant, args.precision, kt, peaks, traffic, info.get("flow_tiles", 0) > 0),
+            "kernel_ms": {k: round(v, 5) for k, v in kt.items()},
             "plan": info,
             "clocks": clk.summary(),
         }
-
-    inst.close()
+        if world > 1:
+            result["allreduce"] = "NCCL allreduce of 2N-1 doubles captured in the per-step CUDA graph"
+        if fp64_probe is not None:
+            result["fp64_peak_probe"] = fp64_probe
+    ev.close()
     return result, pb
 
 
+def run_extra_configs(args, peaks):
+    """The codon (FP64 tensor) workloads beside the headline line, each timed
+    on this GPU with the same protocol (BJ:configs[3], [4], and rank 0's
+    shard of the 8-GPU yeast run)."""
+    import torch
+    dev = torch.device("cuda", 0)
+    flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    out = {}
+    steps, warmup = min(args.steps, 200), max(3, min(args.warmup, 20))
+    import paper_2303_04390_b200 as pg
+    for cfg, shard in ((3, 0), (4, 0), (3, 8), (2, 0), (5, 0)):
+        pb = make_problem(cfg, "fp64")
+        C = pb.patterns
+        lo, hi = pg.shard_range(C, shard, 0) if shard else (0, C)
+        inst, ms, kt, info, nk, _ = bench_instance(pb, "fp64", 0, lo, hi, steps, warmup, flush, 100 + cfg)
+        inst.close()
+        name = workload_name(cfg, C) + (f"_shard0of{shard}" if shard else "")
+        mps = sum(ms) / len(ms)
+        out[name] = {"value": round(1000.0 / mps, 3), "unit": UNIT, "ms_per_step": round(mps, 5),
+                     "ms_step_p10_p50_p90": [round(pct(ms, 10), 5), round(pct(ms, 50), 5), round(pct(ms, 90), 5)],
+                     "patterns_timed": hi - lo, "steps": steps, "warmup": warmup,
+                     "kernel_ms": {k: round(v, 5) for k, v in kt.items()},
+                     "roofline": roofline(pb, hi - lo, info["kernel_variant"], "fp64", kt, peaks,
+                                          load_traffic(traffic_key(cfg, "fp64", shard)), info.get("flow_tiles", 0) > 0)}
+        if shard:
+            out[name]["note"] = (f"one GPU timing rank 0's pattern shard [{lo},{hi}) of a {shard}-GPU run "
+                                 "(the per-GPU work of that run; the allreduce of 2N-1 doubles is not included)")
+    return out
+
 def run_reference(args):
-    """The CPU oracle as the reference arm, on our arm's config and metric."""
+    """The CPU oracle as the reference arm (this tier has no installable
+    reference: /root/reference holds only the paper), on our arm's config,
+    metric and unit; rank 0 alone runs it."""
     import oracle
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -416,12 +552,12 @@ def run_reference(args):
     step_s = sum(times) / len(times)
     value = (m / C) / step_s
     sample = f"patterns [0,{m}) of {C} per step (full tree), scaled by C/{m}"
+    cfg = workload_config(args, pb, C, world, flushed=not args.no_flush)
+    cfg["l2"] = "n/a (host oracle)"
     return {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1000.0 / value, 3), "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(args.config, C), "tips": pb.n_tips, "patterns": C,
-                       "states": pb.states, "categories": len(pb.cat_rates), "precision": "fp64"},
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
             "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": threads,
                              "kind": "oracle", "sample": sample},
             "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -439,8 +575,18 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank == 0:
+        if world == 1 and not args.no_extra_configs and args.config == 1 and args.patterns == 0 \
+                and args.virtual_shard <= 1:
+            peaks = load_peaks()
+            if "fp64_peak_probe" in res and "dmma_tflops" in res["fp64_peak_probe"]:
+                peaks.update(fp64_tflops=res["fp64_peak_probe"]["dmma_tflops"],
+                             dfma_tflops=res["fp64_peak_probe"]["dfma_tflops"],
+                             fp64_src="measured in this run (DMMA probe, csrc/probe.cu)",
+                             dfma_src="measured in this run (DFMA probe, csrc/probe.cu)")
+            res["configs"] = run_extra_configs(args, peaks)
         if world == 1 and not args.no_cpu_baseline:
-            res["cpu_baseline"] = cpu_oracle_rate(pb, args.cpu_seconds)
+            res["cpu_baseline"] = cpu_oracle_rate(pb, args.cpu_seconds, os.cpu_count() or 1)
+            res["cpu_baseline_1thread"] = cpu_oracle_rate(pb, args.cpu_seconds / 2, 1)
         print(json.dumps(res), flush=True)
     if world > 1:
         import torch.distributed as dist

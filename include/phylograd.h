@@ -21,7 +21,9 @@
  *  - Every host input is COPIED at the set_* call; the library keeps no
  *    pointer to caller memory.  Outputs are written to caller buffers.
  *  - One instance is bound to one CUDA device and one stream and is not
- *    thread-safe.  All device work is ordered on that stream.
+ *    thread-safe.  All device work is ordered on that stream.  Every call
+ *    switches to the instance's device and restores the caller's current
+ *    device before returning.
  *  - Errors: every call returns PG_OK (0) or a PG_ERR_* code; the message of
  *    the last failure is pg_last_error(instance).  A failed call leaves the
  *    instance's previous state unchanged.
@@ -127,8 +129,11 @@ int pg_set_operations(pg_instance *inst, const int32_t *ops /*[n_ops][3]*/, int3
 
 /* Branch lengths b_i >= 0 indexed by child node, i = 0..2N-3.  May
  * change between computes (the HMC use case).  The host copy goes through a
- * pinned staging buffer and is uploaded inside the next pg_compute.
- * Errors: PG_ERR_ARG, PG_ERR_DOMAIN. */
+ * pinned staging buffer and is uploaded inside the next pg_compute /
+ * pg_compute_device.  If a previous pg_compute_device's upload from that
+ * buffer is still queued on the stream, this call first waits for it (so an
+ * evaluation always sees the values set before it).
+ * Errors: PG_ERR_ARG, PG_ERR_DOMAIN, PG_ERR_CUDA. */
 int pg_set_branch_lengths(pg_instance *inst, const double *b /*[2N-2]*/);
 
 /* Same, from DEVICE memory: a stream-ordered device-to-device copy (no
@@ -136,7 +141,8 @@ int pg_set_branch_lengths(pg_instance *inst, const double *b /*[2N-2]*/);
  * GPU (device-resident HMC, benchmarks). */
 int pg_set_branch_lengths_device(pg_instance *inst, const double *d_b /*[2N-2]*/);
 
-/* Evaluate logL and the gradient; synchronous, host outputs.
+/* Evaluate logL and the gradient; synchronous, host outputs (not allowed
+ * while the instance stream is being captured: PG_ERR_SEQUENCE).
  *   gradient  [2N-2] or NULL (logL only is still a full evaluation).
  * On PG_ERR_ZERO_LIKELIHOOD *log_likelihood = -inf, the gradient is not
  * written, and pg_last_error names the first such pattern.
@@ -146,8 +152,17 @@ int pg_compute(pg_instance *inst, double *log_likelihood, double *gradient);
 /* Asynchronous evaluation into DEVICE memory: d_out[0] = this instance's
  * logL, d_out[1 + i] = gradient entry i (2N-1 doubles), stream-ordered, no
  * host synchronisation.  These are the partial sums over this instance's
- * patterns, ready for an allreduce(sum) across pattern shards.  Zero
- * likelihoods are recorded on the device; read them with pg_check_status.
+ * patterns (Eq. 6 is a sum over patterns), ready for an
+ * allreduce(sum) across pattern shards.  Zero likelihoods are
+ * recorded on the device; read them with pg_check_status.
+ * Stream capture: normally the evaluation is replayed from a CUDA graph the
+ * library captured itself.  If the CALLER is capturing the instance stream
+ * (cudaStreamBeginCapture), the kernels are enqueued straight into the
+ * caller's graph instead, so one graph can hold [pg_set_branch_lengths_device,
+ * pg_compute_device, ncclAllReduce].  Under capture the call must not need
+ * host uploads: run one evaluation outside capture first (else
+ * PG_ERR_SEQUENCE); host-staged branch lengths become memcpy nodes that
+ * re-read the pinned staging buffer at every replay.
  * Errors: PG_ERR_SEQUENCE, PG_ERR_CUDA. */
 int pg_compute_device(pg_instance *inst, double *d_out /*[2N-1]*/);
 

@@ -112,8 +112,21 @@ def _dptr(a: np.ndarray):
     return a.ctypes.data_as(_dp)
 
 
-def _f64(a) -> np.ndarray:
-    return np.ascontiguousarray(a, dtype=np.float64)
+def _f64(a, n: Optional[int] = None, what: str = "array") -> np.ndarray:
+    """C-contiguous float64 copy/view of `a`; with `n`, its size must be n (the
+    C side reads exactly that many values: a short array would be a heap
+    over-read, a long one a silent truncation)."""
+    x = np.ascontiguousarray(a, dtype=np.float64)
+    if n is not None and x.size != n:
+        raise ValueError(f"{what}: expected {n} values, got {x.size} (shape {np.shape(a)})")
+    return x
+
+
+def _i32(a, n: int, what: str) -> np.ndarray:
+    x = np.ascontiguousarray(a, dtype=np.int32)
+    if x.size != n:
+        raise ValueError(f"{what}: expected {n} values, got {x.size} (shape {np.shape(a)})")
+    return x
 
 
 def plan_check(tips: int, ops) -> tuple[int, int]:
@@ -182,37 +195,43 @@ class Instance:
         except Exception:
             pass
 
-    # -- setters (copied at call time) ------------------------------------
+    # -- setters (copied at call time; sizes checked here) -------
     def set_tip_states(self, tip: int, states):
-        s = np.ascontiguousarray(states, dtype=np.int32)
+        s = _i32(states, self.patterns, "tip states [C]")
         self._check(_lib.pg_set_tip_states(self._h, int(tip), s.ctypes.data_as(_ip)), "set_tip_states")
 
     def set_tip_partials(self, tip: int, partials):
-        p = _f64(partials)
+        p = _f64(partials, self.patterns * self.states, "tip partials [C][S]")
         self._check(_lib.pg_set_tip_partials(self._h, int(tip), _dptr(p)), "set_tip_partials")
 
     def set_pattern_weights(self, w):
-        self._check(_lib.pg_set_pattern_weights(self._h, _dptr(_f64(w))), "set_pattern_weights")
+        self._check(_lib.pg_set_pattern_weights(self._h, _dptr(_f64(w, self.patterns, "pattern weights [C]"))),
+                    "set_pattern_weights")
 
     def set_state_frequencies(self, pi):
-        self._check(_lib.pg_set_state_frequencies(self._h, _dptr(_f64(pi))), "set_state_frequencies")
+        self._check(_lib.pg_set_state_frequencies(self._h, _dptr(_f64(pi, self.states, "pi [S]"))),
+                    "set_state_frequencies")
 
     def set_eigen(self, evec, ievec, evals):
-        V, Vi, lam = _f64(evec), _f64(ievec), _f64(evals)
+        S = self.states
+        V, Vi, lam = _f64(evec, S * S, "evec [S][S]"), _f64(ievec, S * S, "ievec [S][S]"), _f64(evals, S, "eval [S]")
         self._check(_lib.pg_set_eigen(self._h, _dptr(V), _dptr(Vi), _dptr(lam)), "set_eigen")
 
     def set_category_rates(self, rates):
-        self._check(_lib.pg_set_category_rates(self._h, _dptr(_f64(rates))), "set_category_rates")
+        self._check(_lib.pg_set_category_rates(self._h, _dptr(_f64(rates, self.categories, "category rates [R]"))),
+                    "set_category_rates")
 
     def set_category_weights(self, w):
-        self._check(_lib.pg_set_category_weights(self._h, _dptr(_f64(w))), "set_category_weights")
+        self._check(_lib.pg_set_category_weights(self._h, _dptr(_f64(w, self.categories, "category weights [R]"))),
+                    "set_category_weights")
 
     def set_operations(self, ops):
         o = np.ascontiguousarray(ops, dtype=np.int32).reshape(-1, 3)
         self._check(_lib.pg_set_operations(self._h, o.ctypes.data_as(_ip), int(o.shape[0])), "set_operations")
 
     def set_branch_lengths(self, b):
-        self._check(_lib.pg_set_branch_lengths(self._h, _dptr(_f64(b))), "set_branch_lengths")
+        self._check(_lib.pg_set_branch_lengths(self._h, _dptr(_f64(b, self.n_branches, "branch lengths [2N-2]"))),
+                    "set_branch_lengths")
 
     def set_branch_lengths_device(self, t):
         """t: a CUDA float64 tensor of 2N-2 branch lengths (stream-ordered copy)."""
@@ -223,8 +242,9 @@ class Instance:
     def set_node_heights(self, heights, rates=None):
         """b_i = rho_i (h_parent(i) - h_i) from host heights [2N-1] and rate
         scalars [2N-2] (None = all 1); validated and copied."""
-        r = None if rates is None else _f64(rates)
-        self._check(_lib.pg_set_node_heights(self._h, _dptr(_f64(heights)), _dptr(r) if r is not None else None),
+        r = None if rates is None else _f64(rates, self.n_branches, "rate scalars [2N-2]")
+        h = _f64(heights, self.n_branches + 1, "node heights [2N-1]")
+        self._check(_lib.pg_set_node_heights(self._h, _dptr(h), _dptr(r) if r is not None else None),
                     "set_node_heights")
 
     def set_node_heights_device(self, h, rates=None):
@@ -237,7 +257,7 @@ class Instance:
                     "set_node_heights_device")
 
     def set_branch_sets(self, set_of_branch, n_sets: int):
-        s = np.ascontiguousarray(set_of_branch, dtype=np.int32)
+        s = _i32(set_of_branch, self.n_branches, "branch set ids [2N-2]")
         self._check(_lib.pg_set_branch_sets(self._h, s.ctypes.data_as(_ip), int(n_sets)), "set_branch_sets")
 
     def clock_gradient_device(self, out, grad_rates=None, grad_heights=None, set_sums=None):
@@ -351,16 +371,89 @@ def from_problem(pb, precision: Optional[str] = None, device: int = 0, stream=No
 def shard_range(C: int, world: int, rank: int) -> tuple[int, int]:
     """Contiguous pattern shard [lo, hi) of `rank`: patterns
     are conditionally independent, so logL and every gradient
-    entry are sums of per-shard partial sums."""
-    per = -(-C // world)
-    lo = min(C, rank * per)
-    return lo, min(C, lo + per)
+    entry are sums of per-shard partial sums (Eq. 6).  Balanced
+    split: shard sizes differ by at most one; a shard is empty only when
+    C < world (then that rank contributes zeros to the allreduce)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world {world}")
+    return rank * C // world, (rank + 1) * C // world
 
 
 def allreduce_evaluation(out, group=None):
-    """A7: sum the per-shard [logL, g] vector across ranks (one NCCL
-    allreduce per evaluation, on the current stream)."""
+    """A7: sum the per-shard [logL, g] vector across ranks (one allreduce per
+    evaluation, on the current stream; NCCL on GPUs).  It may be captured in
+    the same CUDA graph as pg_compute_device (see `capture_evaluation`)."""
     import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    if dist.is_available() and dist.is_initialized():      # world size 1 too: the same collective path
         dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
     return out
+
+
+class ShardEvaluation:
+    """One rank's side of a pattern-sharded evaluation.
+
+    `pb` is a phylo_synth.Problem (the whole alignment); this rank evaluates
+    patterns shard_range(C, world, rank) through the C ABI and the per-shard
+    [logL, g] vectors are summed with one allreduce.  A rank whose shard is
+    empty (C < world) creates no instance and contributes zeros.
+
+    capture=True records [set_branch_lengths_device, compute_device,
+    allreduce] as ONE CUDA graph on the instance stream (the library enqueues
+    into the caller's capture) and replays it per evaluation.
+    """
+
+    def __init__(self, pb, rank: int = 0, world: int = 1, device: int = 0, precision: Optional[str] = None,
+                 group=None, capture: bool = False, timing: bool = False):
+        import torch
+        self.torch = torch
+        self.group = group
+        self.lo, self.hi = shard_range(pb.patterns, world, rank)
+        self.n_branches = 2 * pb.n_tips - 2
+        self.dev = torch.device("cuda", device)
+        self.inst = from_problem(pb, precision=precision, device=device, lo=self.lo, hi=self.hi) \
+            if self.hi > self.lo else None
+        self.stream = self.inst.stream if self.inst is not None else torch.cuda.Stream(device=self.dev)
+        self.out = torch.zeros(self.n_branches + 1, dtype=torch.float64, device=self.dev)
+        self.bl = torch.tensor(np.asarray(pb.branch_lengths[:self.n_branches], dtype=np.float64), device=self.dev)
+        self.graph = None
+        if timing and self.inst is not None:          # per-kernel events (recorded inside the graph too)
+            self.inst.set_kernel_timing(True)
+        if capture:
+            with torch.cuda.stream(self.stream):
+                self._enqueue()                       # uploads + plan outside the capture
+            self.stream.synchronize()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=self.stream):
+                self._enqueue()
+
+    def _enqueue(self):
+        if self.inst is not None:
+            self.inst.set_branch_lengths_device(self.bl)
+            self.inst.compute_device(self.out)
+        else:
+            self.out.zero_()
+        allreduce_evaluation(self.out, self.group)
+
+    def evaluate(self, branch_lengths=None):
+        """[logL, g] summed over all ranks' shards (device tensor, stream-ordered)."""
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
+            if branch_lengths is not None:
+                self.bl.copy_(torch.as_tensor(np.asarray(branch_lengths, dtype=np.float64)), non_blocking=False)
+            if self.graph is not None:
+                self.graph.replay()
+            else:
+                self._enqueue()
+        return self.out
+
+    def zero_pattern(self) -> int:
+        """First zero-likelihood pattern of this shard (global index) or -1."""
+        if self.inst is None:
+            return -1
+        zp = self.inst.check_status()
+        return zp + self.lo if zp >= 0 else -1
+
+    def close(self):
+        if self.inst is not None:
+            self.inst.close()
+            self.inst = None

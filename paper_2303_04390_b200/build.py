@@ -13,6 +13,9 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIB_DIR, "libphylograd.so")
 SOURCES = ["phylograd.cu", "schedule.cpp"]
+# measurement helper for bench.py (FP64 peak probe; not the hot path, not the ABI)
+PROBE = os.path.join(LIB_DIR, "libpgprobe.so")
+PROBE_SOURCES = ["probe.cu"]
 HEADER_GLOBS = ("*.cuh", "*.hpp", "*.h")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -30,10 +33,10 @@ def _inputs():
 
 
 def _stale() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(PROBE):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(f) > t for f in _inputs())
+    t = min(os.path.getmtime(LIB), os.path.getmtime(PROBE))
+    return any(os.path.getmtime(f) > t for f in _inputs() + [os.path.join(CSRC, f) for f in PROBE_SOURCES])
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -44,7 +47,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [nvcc, *NVCC_FLAGS, "-o", LIB, *[os.path.join(CSRC, f) for f in SOURCES]]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
-    subprocess.check_call(cmd)
+    probe = [nvcc, *NVCC_FLAGS, "-o", PROBE, *[os.path.join(CSRC, f) for f in PROBE_SOURCES]]
+    procs = [subprocess.Popen(c) for c in (cmd, probe)]
+    for p, c in zip(procs, (cmd, probe)):
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, c)
     return LIB
 
 

@@ -9,9 +9,14 @@ namespace pg {
 // SP x SP (category blocks `cs` Reals apart).  One CTA per (branch, category): the S exponentials go to shared
 // memory, then every thread forms entries of P and (optionally) P'.  Padded
 // rows/columns are exactly 0.  The work is ~2% of an evaluation.
+// Evaluated as P = M0 + V diag(expm1(gamma_r b_i lambda)) V^{-1} with
+// M0 = V V^{-1} formed once on the host (equal to Eq. 1 in exact arithmetic;
+// the summed terms shrink with |gamma b lambda|, so short branches lose less
+// to cancellation, R15b).
 template <typename Real, int SP>
 __global__ void __launch_bounds__(256) pmat_kernel(const double *__restrict__ V,
                                                    const double *__restrict__ Vi,
+                                                   const double *__restrict__ M0,
                                                    const double *__restrict__ lam,
                                                    const double *__restrict__ rates,
                                                    const double *__restrict__ bl, int S, int R,
@@ -20,15 +25,17 @@ __global__ void __launch_bounds__(256) pmat_kernel(const double *__restrict__ V,
     const int br = blockIdx.x;          // branch * R + r
     const int r = br % R, b = br / R;
     const double t = rates[r] * bl[b];
-    for (int k = threadIdx.x; k < SP; k += blockDim.x) e[k] = k < S ? exp(lam[k] * t) : 0.0;
+    for (int k = threadIdx.x; k < SP; k += blockDim.x) e[k] = k < S ? expm1(lam[k] * t) : 0.0;
     __syncthreads();
     Real *Pm = P + (size_t)br * cs;     // cs = category stride (>= SP*SP, zero padded)
     Real *PTm = PT ? PT + (size_t)br * SP * SP : nullptr;
     for (int idx = threadIdx.x; idx < SP * SP; idx += blockDim.x) {
         const int s = idx / SP, u = idx % SP;
         double acc = 0.0;
-        if (s < S && u < S)
+        if (s < S && u < S) {
             for (int k = 0; k < S; ++k) acc += V[s * S + k] * e[k] * Vi[k * S + u];
+            acc += M0[idx];
+        }
         Pm[idx] = (Real)acc;
         if (PTm) PTm[u * SP + s] = (Real)acc;
     }

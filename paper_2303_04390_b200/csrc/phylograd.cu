@@ -34,7 +34,7 @@ size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
 struct Layout {
     int SP = 0, variant = 0, Cpad = 0, n_tiles = 0, B = 0, tpl = 32, cat_stride = 0;
     size_t real = 8;
-    size_t off_P, off_PT, off_Q, off_QT, off_pi, off_V, off_Vi, off_lam, off_rates, off_cw,
+    size_t off_P, off_PT, off_M0, off_Q, off_QT, off_pi, off_V, off_Vi, off_lam, off_rates, off_cw,
         off_bl, off_patw, off_tips, off_tipp, off_u, off_gpart, off_lpart, off_out, off_status,
         off_post, off_pre, total;
     // codon (variant 2) extras
@@ -115,6 +115,7 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         L->off_VA = take((size_t)SP * SP * 8);
         L->off_ViB = take((size_t)SP * SP * 8);
     }
+    L->off_M0 = take((size_t)SP * SP * 8);     // V V^-1 (A1's identity term, host long double)
     L->off_Q = take((size_t)SP * SP * L->real);
     L->off_QT = take((size_t)SP * SP * L->real);
     L->off_pi = take((size_t)SP * L->real);
@@ -201,6 +202,8 @@ struct pg_instance {
     bool bl_host_pending = false;
     double *clock_pinned = nullptr;     // [2N-1] heights then [2N-2] rate scalars
     bool clock_host_pending = false, have_heights = false;
+    cudaEvent_t staged_ev = nullptr;    // recorded after the H2D copies that read the pinned staging buffers
+    bool staged_pending = false;
     int n_sets = 1;
     // launch configuration
     int prefetch = 4, smem = 0, grid = 0, block = 0, tiles_per_cta = 1, prog_smem_off = 0;
@@ -229,6 +232,40 @@ struct pg_instance {
         cudaError_t _e = (call);                                  \
         if (_e != cudaSuccess) return inst->cuda_fail(_e, what);  \
     } while (0)
+
+// Every entry point that touches the GPU runs on the instance's device and
+// restores the caller's current device on return (an instance is
+// bound to one device; torch's current device must not change under it).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        int cur = -1;
+        if (dev < 0 || cudaGetDevice(&cur) != cudaSuccess || cur == dev) return;
+        if (cudaSetDevice(dev) == cudaSuccess) prev = cur;
+    }
+    explicit DeviceGuard(const pg_instance *inst) : DeviceGuard(inst ? inst->cfg.device : -1) {}
+    ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+// Host staging buffers (bl_pinned, clock_pinned) are read by stream-ordered
+// H2D copies that may still be queued when the caller sets new values
+// (pg_compute_device returns without synchronising): wait for the copy that
+// last read them before overwriting.
+static int wait_staging(pg_instance *inst) {
+    if (!inst->staged_pending) return PG_OK;
+    CK(cudaEventSynchronize(inst->staged_ev), "staging buffer wait");
+    inst->staged_pending = false;
+    return PG_OK;
+}
+static int mark_staging(pg_instance *inst) {
+    CK(cudaEventRecord(inst->staged_ev, inst->stream), "staging event");
+    inst->staged_pending = true;
+    return PG_OK;
+}
+static bool capturing(const pg_instance *inst) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(inst->stream, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone;
+}
 
 // Exported functions get C linkage from their declarations in phylograd.h.
 
@@ -269,7 +306,10 @@ int pg_create(const pg_config *cfg, void *cuda_stream, void *dev_workspace, size
     inst->cfg = *cfg;
     inst->L = L;
     auto bail = [&](int code) { pg_destroy(inst); return code; };
-    cudaError_t e = cudaSetDevice(cfg->device);
+    DeviceGuard dg(cfg->device);         // restores the caller's current device on return
+    int cur = -1;
+    cudaError_t e = cudaGetDevice(&cur);
+    if (e == cudaSuccess && cur != cfg->device) e = cudaErrorInvalidDevice;
     if (e != cudaSuccess) { inst->cuda_fail(e, "cudaSetDevice"); return bail(PG_ERR_CUDA); }
     int dev_sms = 0;
     if (cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device) == cudaSuccess && dev_sms > 0)
@@ -292,6 +332,7 @@ int pg_create(const pg_config *cfg, void *cuda_stream, void *dev_workspace, size
         cudaMallocHost((void **)&inst->status_pinned, sizeof(int) * 4) != cudaSuccess ||
         cudaMallocHost((void **)&inst->clock_pinned, sizeof(double) * (2 * L.B + 1)) != cudaSuccess)
         return bail(PG_ERR_MEMORY);
+    if (cudaEventCreateWithFlags(&inst->staged_ev, cudaEventDisableTiming) != cudaSuccess) return bail(PG_ERR_CUDA);
     const int N = cfg->tips;
     inst->tips_h.assign((size_t)N * L.Cpad, (uint8_t)cfg->states);   // all missing
     inst->tip_is_partial.assign(N, 0);
@@ -304,10 +345,12 @@ int pg_create(const pg_config *cfg, void *cuda_stream, void *dev_workspace, size
 }
 
 int pg_destroy(pg_instance *inst) {
+    DeviceGuard dg(inst);
     if (!inst) return PG_OK;
     if (inst->stream) cudaStreamSynchronize(inst->stream);
     if (inst->gexec) cudaGraphExecDestroy(inst->gexec);
     for (auto &e : inst->ev) if (e) cudaEventDestroy(e);
+    if (inst->staged_ev) cudaEventDestroy(inst->staged_ev);
     if (inst->own_ws && inst->ws) cudaFree(inst->ws);
     if (inst->flow_trace) cudaFree(inst->flow_trace);
     if (inst->bl_pinned) cudaFreeHost(inst->bl_pinned);
@@ -358,6 +401,7 @@ int pg_set_tip_states(pg_instance *inst, int32_t tip, const int32_t *states) {
 }
 
 int pg_set_tip_partials(pg_instance *inst, int32_t tip, const double *partials) {
+    DeviceGuard dg(inst);
     if (!inst) return PG_ERR_ARG;
     const pg_config &c = inst->cfg;
     if (!(c.flags & PG_FLAG_TIP_PARTIALS))
@@ -417,6 +461,7 @@ int pg_set_tip_partials(pg_instance *inst, int32_t tip, const double *partials) 
 }
 
 int pg_set_pattern_weights(pg_instance *inst, const double *w) {
+    DeviceGuard dg(inst);
     if (!inst || !w) return PG_ERR_ARG;
     const int C = inst->cfg.patterns;
     for (int i = 0; i < C; ++i)
@@ -430,6 +475,7 @@ int pg_set_pattern_weights(pg_instance *inst, const double *w) {
 }
 
 int pg_set_state_frequencies(pg_instance *inst, const double *pi) {
+    DeviceGuard dg(inst);
     if (!inst || !pi) return PG_ERR_ARG;
     const int S = inst->cfg.states, SP = inst->L.SP;
     for (int s = 0; s < S; ++s)
@@ -443,6 +489,7 @@ int pg_set_state_frequencies(pg_instance *inst, const double *pi) {
 }
 
 int pg_set_eigen(pg_instance *inst, const double *evec, const double *ievec, const double *eval) {
+    DeviceGuard dg(inst);
     if (!inst || !evec || !ievec || !eval) return PG_ERR_ARG;
     const int S = inst->cfg.states, SP = inst->L.SP;
     if (!finite_all(evec, (size_t)S * S) || !finite_all(ievec, (size_t)S * S) || !finite_all(eval, S))
@@ -451,15 +498,27 @@ int pg_set_eigen(pg_instance *inst, const double *evec, const double *ievec, con
     if ((rc = upload_doubles(inst, inst->L.off_V, evec, (size_t)S * S))) return rc;
     if ((rc = upload_doubles(inst, inst->L.off_Vi, ievec, (size_t)S * S))) return rc;
     if ((rc = upload_doubles(inst, inst->L.off_lam, eval, S))) return rc;
-    // Q = V diag(lambda) V^{-1} (host, double), padded; and Q'
-    std::vector<double> Q((size_t)SP * SP, 0.0), QT((size_t)SP * SP, 0.0);
+    // Q = V diag(lambda) V^{-1} and M0 = V V^{-1} (host, long double sums,
+    // rounded once), padded; and Q'.  A1 evaluates Eq. 1 as
+    //   P = V diag(e) V^-1 = M0 + V diag(e - 1) V^-1,   e - 1 = expm1(gamma b lambda),
+    //   D = gamma V diag(lambda e) V^-1 = gamma (Q + V diag(lambda (e - 1)) V^-1):
+    // identical in exact arithmetic, but the summed terms are smaller by |gamma
+    // b lambda| on short branches, so the cancellation that forms P's tiny
+    // entries (multi-nucleotide codon changes) loses far less (R15b)
+    std::vector<double> Q((size_t)SP * SP, 0.0), QT((size_t)SP * SP, 0.0), M0((size_t)SP * SP, 0.0);
     for (int s = 0; s < S; ++s)
         for (int t = 0; t < S; ++t) {
-            double acc = 0.0;
-            for (int k = 0; k < S; ++k) acc += evec[s * S + k] * eval[k] * ievec[k * S + t];
-            Q[(size_t)s * SP + t] = acc;
-            QT[(size_t)t * SP + s] = acc;
+            long double acc = 0.0L, acc0 = 0.0L;
+            for (int k = 0; k < S; ++k) {
+                const long double vv = (long double)evec[s * S + k] * (long double)ievec[k * S + t];
+                acc += vv * (long double)eval[k];
+                acc0 += vv;
+            }
+            Q[(size_t)s * SP + t] = (double)acc;
+            QT[(size_t)t * SP + s] = (double)acc;
+            M0[(size_t)s * SP + t] = (double)acc0;
         }
+    if ((rc = upload_doubles(inst, inst->L.off_M0, M0.data(), M0.size()))) return rc;
     if ((rc = upload_real(inst, inst->L.off_Q, Q))) return rc;
     if ((rc = upload_real(inst, inst->L.off_QT, QT))) return rc;
     if (inst->L.variant == 2) {      // Q as the fragment-ordered B operand of Qu = u Q'
@@ -490,6 +549,7 @@ int pg_set_eigen(pg_instance *inst, const double *evec, const double *ievec, con
 }
 
 int pg_set_category_rates(pg_instance *inst, const double *rates) {
+    DeviceGuard dg(inst);
     if (!inst || !rates) return PG_ERR_ARG;
     for (int r = 0; r < inst->cfg.categories; ++r)
         if (!(rates[r] > 0.0) || !std::isfinite(rates[r])) return inst->fail(PG_ERR_DOMAIN, "category rates must be > 0");
@@ -500,6 +560,7 @@ int pg_set_category_rates(pg_instance *inst, const double *rates) {
 }
 
 int pg_set_category_weights(pg_instance *inst, const double *w) {
+    DeviceGuard dg(inst);
     if (!inst || !w) return PG_ERR_ARG;
     for (int r = 0; r < inst->cfg.categories; ++r)
         if (!(w[r] >= 0.0) || !std::isfinite(w[r])) return inst->fail(PG_ERR_DOMAIN, "category weights must be >= 0");
@@ -510,6 +571,7 @@ int pg_set_category_weights(pg_instance *inst, const double *w) {
 }
 
 int pg_set_operations(pg_instance *inst, const int32_t *ops, int32_t n_ops) {
+    DeviceGuard dg(inst);
     if (!inst) return PG_ERR_ARG;
     pg::Plan p;
     std::string e;
@@ -547,6 +609,7 @@ static int launch_clock_bl(pg_instance *inst, const double *h_src, const double 
 }
 
 int pg_set_node_heights(pg_instance *inst, const double *heights, const double *rates) {
+    DeviceGuard dg(inst);
     if (!inst || !heights) return PG_ERR_ARG;
     if (!inst->have_ops) return inst->fail(PG_ERR_SEQUENCE, "operations not set (node parents unknown)");
     const int N = inst->cfg.tips, B = inst->L.B;
@@ -559,6 +622,8 @@ int pg_set_node_heights(pg_instance *inst, const double *heights, const double *
         for (int i = 0; i < B; ++i)
             if (!(rates[i] >= 0.0) || !std::isfinite(rates[i]))
                 return inst->fail(PG_ERR_DOMAIN, "rate scalar " + std::to_string(i) + " is negative or not finite");
+    int rc = wait_staging(inst);
+    if (rc) return rc;
     std::memcpy(inst->clock_pinned, heights, sizeof(double) * (2 * N - 1));
     for (int i = 0; i < B; ++i) inst->clock_pinned[2 * N - 1 + i] = rates ? rates[i] : 1.0;
     inst->clock_host_pending = true;
@@ -568,6 +633,7 @@ int pg_set_node_heights(pg_instance *inst, const double *heights, const double *
 }
 
 int pg_set_node_heights_device(pg_instance *inst, const double *d_heights, const double *d_rates) {
+    DeviceGuard dg(inst);
     if (!inst || !d_heights) return PG_ERR_ARG;
     if (!inst->have_ops) return inst->fail(PG_ERR_SEQUENCE, "operations not set (node parents unknown)");
     int rc = launch_clock_bl(inst, d_heights, d_rates);
@@ -590,6 +656,7 @@ static int flush_clock_host(pg_instance *inst) {
 }
 
 int pg_set_branch_sets(pg_instance *inst, const int32_t *set_of_branch, int32_t n_sets) {
+    DeviceGuard dg(inst);
     if (!inst || !set_of_branch) return PG_ERR_ARG;
     const int B = inst->L.B;
     if (n_sets < 1 || n_sets > B) return inst->fail(PG_ERR_ARG, "n_sets must be in 1..2N-2");
@@ -605,6 +672,7 @@ int pg_set_branch_sets(pg_instance *inst, const int32_t *set_of_branch, int32_t 
 
 int pg_clock_gradient_device(pg_instance *inst, const double *d_out, double *d_grad_rates, double *d_grad_heights,
                              double *d_set_sums) {
+    DeviceGuard dg(inst);
     if (!inst || !d_out) return PG_ERR_ARG;
     if (!inst->have_heights) return inst->fail(PG_ERR_SEQUENCE, "node heights not set");
     const Layout &L = inst->L;
@@ -625,11 +693,14 @@ int pg_clock_gradient_device(pg_instance *inst, const double *d_out, double *d_g
 }
 
 int pg_set_branch_lengths(pg_instance *inst, const double *b) {
+    DeviceGuard dg(inst);
     if (!inst || !b) return PG_ERR_ARG;
     const int B = inst->L.B;
     for (int i = 0; i < B; ++i)
         if (!(b[i] >= 0.0) || !std::isfinite(b[i]))
             return inst->fail(PG_ERR_DOMAIN, "branch length " + std::to_string(i) + " is negative or not finite");
+    int rc = wait_staging(inst);
+    if (rc) return rc;
     std::memcpy(inst->bl_pinned, b, sizeof(double) * B);
     inst->bl_host_pending = true;
     inst->clock_host_pending = false;
@@ -638,6 +709,7 @@ int pg_set_branch_lengths(pg_instance *inst, const double *b) {
 }
 
 int pg_set_branch_lengths_device(pg_instance *inst, const double *d_b) {
+    DeviceGuard dg(inst);
     if (!inst || !d_b) return PG_ERR_ARG;
     CK(cudaMemcpyAsync(inst->ws + inst->L.off_bl, d_b, sizeof(double) * inst->L.B, cudaMemcpyDeviceToDevice,
                        inst->stream), "branch lengths D2D");
@@ -785,9 +857,6 @@ static int configure(pg_instance *inst) {
         inst->block = cf.threads;
         inst->prefetch = 0;
         inst->smem = (int)cf.pre_smem;
-        for (void *fn : {cf.post4, cf.post2})
-            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(cf.post_smem + 16 * (size_t)inst->cfg.tips)), "smem attr");
         CK(cudaFuncSetAttribute(cf.pre, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.pre_smem), "smem attr");
         CK(cudaFuncSetAttribute(cf.pmat, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.pmat_smem), "smem attr");
         CK(cudaFuncSetAttribute(cf.flow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.flow_smem), "smem attr");
@@ -805,6 +874,20 @@ static int configure(pg_instance *inst) {
             // (8-way shards: yeast 0.288 -> 0.261 ms, WNV 0.714 -> 0.702 ms)
             const int slots = cf.ctas_per_sm * inst->sm_count;
             inst->flow_tch = L.n_tiles * R >= slots ? 2 : 1;
+        }
+        if (inst->flow_tch == 0) {
+            // level-by-level kernels: post levels stage their node table (16 B
+            // per node) after the ring; size the attribute for the widest level
+            const auto &po = inst->plan.post_off;
+            int widest = 1;
+            for (size_t i = 0; i + 1 < po.size(); ++i) widest = std::max(widest, po[i + 1] - po[i]);
+            const size_t need = cf.post_smem + 16 * (size_t)widest;
+            if (need > 227 * 1024)
+                return inst->fail(PG_ERR_UNSUPPORTED, "a post-order level of " + std::to_string(widest) +
+                                                          " nodes does not fit the level kernel's shared memory; "
+                                                          "use the flow schedule (PG_CODON_FLOW unset)");
+            for (void *fn : {cf.post4, cf.post2})
+                CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need), "smem attr");
         }
         const char *de = getenv("PG_FLOW_DEFER");
         inst->flow_defer = de ? (atoi(de) != 0) : 0;
@@ -958,7 +1041,8 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         double *PBpost = inst->at<double>(L.off_P), *PBpre = inst->at<double>(L.off_PBpre),
                *PT = inst->at<double>(L.off_PT), *DT = inst->at<double>(L.off_DT), *PONE = inst->at<double>(L.off_PONE);
         const double *VA = inst->at<double>(L.off_VA), *ViB = inst->at<double>(L.off_ViB);
-        void *args[] = {&VA, &ViB, &lam, &rates, &bl, &S, (void *)&R, &PBpost, &PBpre, &PT, &DT, &PONE};
+        const double *M0 = inst->at<double>(L.off_M0), *Qd = inst->at<double>(L.off_Q);
+        void *args[] = {&VA, &ViB, &M0, &Qd, &lam, &rates, &bl, &S, (void *)&R, &PBpost, &PBpre, &PT, &DT, &PONE};
         const CodonFns cf = codon_fns(L.SP);
         CK(cudaLaunchKernel(cf.pmat, dim3(L.B * R), dim3(256), args, cf.pmat_smem, inst->stream), "codon pmat launch");
         if (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) {     // u = P p of partial tips (A2's tip step)
@@ -975,7 +1059,8 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         void *P = inst->ws + L.off_P;
         void *PT = L.variant == 1 ? inst->ws + L.off_PT : nullptr;
         int cs = L.cat_stride;
-        void *args[] = {&V, &Vi, &lam, &rates, &bl, &S, (void *)&R, &cs, &P, &PT};
+        const double *M0 = inst->at<double>(L.off_M0);
+        void *args[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, (void *)&R, &cs, &P, &PT};
         CK(cudaLaunchKernel(fn, dim3(L.B * R), dim3(std::min(256, L.SP * L.SP)), args, 0, inst->stream), "pmat launch");
     }
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[1], inst->stream, cudaEventRecordExternal), "event");
@@ -1045,7 +1130,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
     return PG_OK;
 }
 
-static int prepare(pg_instance *inst) {
+static int prepare(pg_instance *inst, bool captured = false) {
     if (!inst->have_ops) return inst->fail(PG_ERR_SEQUENCE, "operations not set");
     if (!inst->have_eigen) return inst->fail(PG_ERR_SEQUENCE, "eigensystem not set");
     if (!inst->have_pi) return inst->fail(PG_ERR_SEQUENCE, "state frequencies not set");
@@ -1054,6 +1139,14 @@ static int prepare(pg_instance *inst) {
     if (!inst->have_bl) return inst->fail(PG_ERR_SEQUENCE, "branch lengths not set");
     for (int t = 0; t < inst->cfg.tips; ++t)
         if (!inst->tip_set[t]) return inst->fail(PG_ERR_SEQUENCE, "tip " + std::to_string(t) + " has no data");
+    if (captured) {
+        // inside the caller's stream capture nothing may synchronise: the
+        // plan, launch configuration and tip data must already be on the device
+        if (inst->plan_dirty || inst->partial_modes_dirty || inst->tips_dirty)
+            return inst->fail(PG_ERR_SEQUENCE, "pending uploads (operations, tips or launch plan): run one evaluation "
+                                               "outside stream capture before capturing pg_compute_device");
+        return PG_OK;
+    }
     int rc = refresh_plan(inst);
     if (rc) return rc;
     if (inst->tips_dirty) {
@@ -1065,8 +1158,12 @@ static int prepare(pg_instance *inst) {
     return PG_OK;
 }
 
-// one evaluation via a cached CUDA graph (captured per output pointer)
-static int launch_eval(pg_instance *inst, double *d_out) {
+// one evaluation via a cached CUDA graph (captured per output pointer); when
+// the caller is itself capturing the stream, the kernels are enqueued into
+// the caller's graph instead (a caller can then capture [branch lengths,
+// evaluation, allreduce] as one graph)
+static int launch_eval(pg_instance *inst, double *d_out, bool captured = false) {
+    if (captured) return enqueue_eval(inst, d_out);
     if (!inst->gexec || inst->gexec_out != d_out) {
         if (inst->gexec) { cudaGraphExecDestroy(inst->gexec); inst->gexec = nullptr; }
 #ifdef PG_TRACE
@@ -1092,20 +1189,31 @@ static int launch_eval(pg_instance *inst, double *d_out) {
 
 int pg_compute_device(pg_instance *inst, double *d_out) {
     if (!inst || !d_out) return PG_ERR_ARG;
-    int rc = prepare(inst);
+    DeviceGuard dg(inst);
+    const bool cap = capturing(inst);
+    int rc = prepare(inst, cap);
     if (rc) return rc;
+    // host-staged inputs: stream-ordered copies from the pinned buffers.  In a
+    // caller's capture they become memcpy nodes that re-read the buffers at
+    // every replay (the pending flags are left as they are)
+    const bool staged = inst->bl_host_pending || inst->clock_host_pending;
     if (inst->bl_host_pending) {
         CK(cudaMemcpyAsync(inst->ws + inst->L.off_bl, inst->bl_pinned, sizeof(double) * inst->L.B,
                            cudaMemcpyHostToDevice, inst->stream), "branch lengths H2D");
-        inst->bl_host_pending = false;
+        if (!cap) inst->bl_host_pending = false;
     }
     if ((rc = flush_clock_host(inst))) return rc;
-    inst->clock_host_pending = false;
-    return launch_eval(inst, d_out);
+    if (!cap) {
+        inst->clock_host_pending = false;
+        if (staged && (rc = mark_staging(inst))) return rc;
+    }
+    return launch_eval(inst, d_out, cap);
 }
 
 int pg_compute(pg_instance *inst, double *log_likelihood, double *gradient) {
+    DeviceGuard dg(inst);
     if (!inst || !log_likelihood) return PG_ERR_ARG;
+    if (capturing(inst)) return inst->fail(PG_ERR_SEQUENCE, "pg_compute synchronises: use pg_compute_device under stream capture");
     int rc = prepare(inst);
     if (rc) return rc;
     const Layout &L = inst->L;
@@ -1122,6 +1230,7 @@ int pg_compute(pg_instance *inst, double *log_likelihood, double *gradient) {
     CK(cudaMemcpyAsync(inst->status_pinned, inst->at<int>(L.off_status), sizeof(int), cudaMemcpyDeviceToHost,
                        inst->stream), "status D2H");
     CK(cudaStreamSynchronize(inst->stream), "compute sync");
+    inst->staged_pending = false;
     const int zp = inst->status_pinned[0];
     if (zp != 0x7f7f7f7f) {
         *log_likelihood = -INFINITY;
@@ -1142,6 +1251,7 @@ int pg_compute(pg_instance *inst, double *log_likelihood, double *gradient) {
 
 int pg_hmc_leapfrog(pg_instance *inst, double *d_theta, double *d_p, const double *d_inv_mass, double eps,
                     int32_t n_steps, double *d_out, double *d_grad_theta) {
+    DeviceGuard dg(inst);
     if (!inst) return PG_ERR_ARG;
     if (!d_theta || !d_p || !d_out || n_steps < 0 || !std::isfinite(eps))
         return inst->fail(PG_ERR_ARG, "NULL pointer, n_steps < 0 or non-finite eps");
@@ -1150,7 +1260,8 @@ int pg_hmc_leapfrog(pg_instance *inst, double *d_theta, double *d_p, const doubl
     // the branch lengths now come from theta: drop pending host uploads
     inst->bl_host_pending = inst->clock_host_pending = false;
     inst->have_bl = true;
-    int rc = prepare(inst);
+    const bool cap = capturing(inst);
+    int rc = prepare(inst, cap);
     if (rc) return rc;
     const dim3 grid((B + 127) / 128), block(128);
     auto drift = [&](double e) -> int {
@@ -1163,15 +1274,16 @@ int pg_hmc_leapfrog(pg_instance *inst, double *d_theta, double *d_p, const doubl
         CK(cudaGetLastError(), "hmc kick launch");
         return PG_OK;
     };
-    if ((rc = drift(0.0)) || (rc = launch_eval(inst, d_out)) || (rc = kick(n_steps > 0 ? 0.5 * eps : 0.0))) return rc;
+    if ((rc = drift(0.0)) || (rc = launch_eval(inst, d_out, cap)) || (rc = kick(n_steps > 0 ? 0.5 * eps : 0.0))) return rc;
     for (int s = 0; s < n_steps; ++s) {
-        if ((rc = drift(eps)) || (rc = launch_eval(inst, d_out))) return rc;
+        if ((rc = drift(eps)) || (rc = launch_eval(inst, d_out, cap))) return rc;
         if ((rc = kick(s + 1 < n_steps ? eps : 0.5 * eps))) return rc;
     }
     return PG_OK;
 }
 
 int pg_check_status(pg_instance *inst, int32_t *zero_pattern) {
+    DeviceGuard dg(inst);
     if (!inst) return PG_ERR_ARG;
     int v = 0;
     CK(cudaMemcpyAsync(inst->status_pinned, inst->at<int>(inst->L.off_status), sizeof(int), cudaMemcpyDeviceToHost,
@@ -1185,6 +1297,7 @@ int pg_check_status(pg_instance *inst, int32_t *zero_pattern) {
 }
 
 int pg_set_kernel_timing(pg_instance *inst, int enable) {
+    DeviceGuard dg(inst);
     if (!inst) return PG_ERR_ARG;
     if (enable && !inst->ev[0])
         for (auto &e : inst->ev) CK(cudaEventCreate(&e), "event create");
@@ -1197,6 +1310,7 @@ int pg_set_kernel_timing(pg_instance *inst, int enable) {
 }
 
 int pg_get_kernel_times(pg_instance *inst, float *ms) {
+    DeviceGuard dg(inst);
     if (!inst || !ms) return PG_ERR_ARG;
     if (!inst->timing) return inst->fail(PG_ERR_SEQUENCE, "kernel timing is not enabled");
     CK(cudaEventSynchronize(inst->ev[3]), "event sync");

@@ -869,6 +869,8 @@ constexpr size_t tipu_smem() { return (size_t)2 * T * SP * 8; }
 template <int SP>
 __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restrict__ VA,
                                                          const double *__restrict__ ViB,
+                                                         const double *__restrict__ M0,
+                                                         const double *__restrict__ Qd,
                                                          const double *__restrict__ lam,
                                                          const double *__restrict__ rates,
                                                          const double *__restrict__ bl, int S, int R,
@@ -890,10 +892,12 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
         cp_async_commit();
     }
     const double g = rates[r], t = g * bl[b];
+    // P = M0 + V diag(e - 1) V^-1, D = gamma (Q + V diag(lambda (e - 1)) V^-1)
+    // (M0 = V V^-1, Q formed once on the host; R15b)
     for (int k = threadIdx.x; k < SP; k += blockDim.x) {
-        const double ex = k < S ? exp(lam[k] * t) : 0.0;
-        e[k] = ex;
-        de[k] = k < S ? g * lam[k] * ex : 0.0;
+        const double em1 = k < S ? expm1(lam[k] * t) : 0.0;
+        e[k] = em1;
+        de[k] = k < S ? g * lam[k] * em1 : 0.0;
     }
     if constexpr (STAGE_V) cp_async_wait<0>();
     __syncthreads();
@@ -926,8 +930,10 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt) {
                     const int m = h * 32 + mt * 8 + (lane >> 2), n = cs * 8 + 2 * (lane & 3);
-                    Ps[m * (SP + 1) + n] = ap[mt][0];
-                    Ps[m * (SP + 1) + n + 1] = ap[mt][1];
+                    const double2 z = *reinterpret_cast<const double2 *>((pass ? Qd : M0) + m * SP + n);
+                    const double zs = pass ? g : 1.0;
+                    Ps[m * (SP + 1) + n] = fma(zs, z.x, ap[mt][0]);
+                    Ps[m * (SP + 1) + n + 1] = fma(zs, z.y, ap[mt][1]);
                 }
             }
         }

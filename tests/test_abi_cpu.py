@@ -87,3 +87,19 @@ def test_shard_range_covers_patterns(pg):
         spans = [pg.shard_range(C, w, r) for r in range(w)]
         assert spans[0][0] == 0 and spans[-1][1] == C
         assert all(spans[i][1] == spans[i + 1][0] for i in range(w - 1))
+    # balanced: sizes differ by at most one; C < world leaves some shards empty
+    for C, w in ((9, 8), (10000, 8), (3, 8), (1, 2)):
+        sizes = [hi - lo for lo, hi in (pg.shard_range(C, w, r) for r in range(w))]
+        assert sum(sizes) == C and max(sizes) - min(sizes) <= 1
+
+
+def test_setters_check_array_sizes(pg):
+    """Short or long host arrays raise before the C call (the C side reads
+    fixed counts: 2N-2, C, C*S, S*S, R)."""
+    import numpy as np
+    sig = pg._f64
+    with pytest.raises(ValueError):
+        sig(np.zeros(5), 6, "x")
+    with pytest.raises(ValueError):
+        pg._i32(np.zeros(7), 6, "y")
+    assert sig(np.zeros((2, 3)), 6, "z").shape == (2, 3)
