@@ -5,6 +5,8 @@
 //                    -> reduce_kernel (A6)
 // A7 (the cross-GPU allreduce) is the caller's, on the same stream, over the
 // 2N-1 doubles pg_compute_device leaves in device memory.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -21,6 +23,7 @@
 #include "common.cuh"
 #include "schedule.hpp"
 #include "traverse_codon.cuh"
+#include "traverse_codon2.cuh"
 #include "traverse_large.cuh"
 #include "traverse_small.cuh"
 
@@ -208,6 +211,8 @@ struct pg_instance {
     // launch configuration
     int prefetch = 4, smem = 0, grid = 0, block = 0, tiles_per_cta = 1, prog_smem_off = 0;
     int flow_tch = 0;                   // codon: tiles per flow item (0 = level-by-level kernels)
+    int flow_ver = 2;                   // codon flow kernel: 2 = warp-specialised TMA ring (codon_flow2_kernel), 1 = round-1 kernel
+    pg::codon::TmaMaps tmaps{};         // TMA tensor maps of u, q, utip (codon_flow2_kernel)
     int flow_defer = 0;                 // codon flow: Eq. 8 items after all pre items (PG_FLOW_DEFER)
     int flow_half = 0;                  // codon flow: half-tile post items when tch == 1 (PG_FLOW_HALF)
     unsigned long long *flow_trace = nullptr;   // PG_FLOW_TRACE=<file>: per-item timestamps (diagnostics)
@@ -731,17 +736,19 @@ static void *pmat_fn() { return (void *)pg::pmat_kernel<Real, SP>; }
 
 // kernels and launch geometry of the FP64 tensor-core path for SP = 64 / 128
 struct CodonFns {
-    void *post4, *post2, *pre, *pmat, *flow, *tipu, *tipmask;
-    int threads, ctas_per_sm;
-    size_t post_smem, pre_smem, pmat_smem, flow_smem, tipu_smem;
+    void *post4, *post2, *pre, *pmat, *flow, *tipu, *tipmask, *flow2;
+    int threads, ctas_per_sm, flow2_threads, flow2_ctas;
+    size_t post_smem, pre_smem, pmat_smem, flow_smem, tipu_smem, flow2_smem;
 };
 template <int SP>
 static CodonFns codon_fns_t() {
     namespace c = pg::codon;
     return {(void *)c::codon_post_kernel<SP, 4>, (void *)c::codon_post_kernel<SP, 2>, (void *)c::codon_pre_kernel<SP>,
             (void *)c::codon_pmat_kernel<SP>, (void *)c::codon_flow_kernel<SP>,
-            (void *)c::codon_tipu_kernel<SP>, (void *)c::codon_tipmask_kernel<SP>, c::codon_threads<SP>(), c::codon_ctas_per_sm<SP>(), c::post_smem<SP>(),
-            c::pre_smem<SP>(), c::pmat_smem<SP>(), c::flow_smem<SP>(), c::tipu_smem<SP>()};
+            (void *)c::codon_tipu_kernel<SP>, (void *)c::codon_tipmask_kernel<SP>, (void *)c::codon_flow2_kernel<SP>,
+            c::codon_threads<SP>(), c::codon_ctas_per_sm<SP>(), c::flow2_threads<SP>(), c::flow2_ctas<SP>(),
+            c::post_smem<SP>(), c::pre_smem<SP>(), c::pmat_smem<SP>(), c::flow_smem<SP>(), c::tipu_smem<SP>(),
+            c::flow2_smem<SP>()};
 }
 static CodonFns codon_fns(int SP) { return SP == 128 ? codon_fns_t<128>() : codon_fns_t<64>(); }
 
@@ -813,6 +820,40 @@ static size_t large_smem(const Layout &L, int R, int depth) {
     return (5 + (size_t)depth) * vb + nvec * (4 * 8 + 2 * 4) + (size_t)L.tpl * 16;
 }
 
+// TMA tensor maps over the fragment-ordered tile arrays u, q, utip
+// ([tiles][TILE] doubles viewed as rows of 256 doubles; one box = one tile)
+static int make_tile_maps(pg_instance *inst) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return inst->fail(PG_ERR_CUDA, "cuTensorMapEncodeTiled is not available from the driver");
+        encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    const Layout &L = inst->L;
+    const int N = inst->cfg.tips, R = inst->cfg.categories;
+    const cuuint32_t rows = (cuuint32_t)(pg::codon::T * L.SP / 256);
+    auto enc = [&](CUtensorMap *m, size_t off, size_t tiles) -> int {
+        cuuint64_t dims[2] = {256, (cuuint64_t)std::max<size_t>(tiles, 1) * rows};
+        cuuint64_t strides[1] = {256 * 8};
+        cuuint32_t box[2] = {256, rows};
+        cuuint32_t es[2] = {1, 1};
+        CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, inst->ws + off, dims, strides, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return inst->fail(PG_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+        return PG_OK;
+    };
+    int rc;
+    const size_t t_int = (size_t)std::max(N - 2, 0) * R * L.n_tiles;
+    if ((rc = enc(&inst->tmaps.u, L.off_u, t_int))) return rc;
+    if ((rc = enc(&inst->tmaps.q, L.off_q, t_int))) return rc;
+    const bool tp = inst->cfg.flags & PG_FLAG_TIP_PARTIALS;
+    return enc(&inst->tmaps.utip, tp ? L.off_utip : L.off_u, tp ? (size_t)N * R * L.n_tiles : t_int);
+}
+
 static int configure(pg_instance *inst) {
     const Layout &L = inst->L;
     const int R = inst->cfg.categories;
@@ -864,8 +905,15 @@ static int configure(pg_instance *inst) {
         // flow schedule (default): chunks of TCH tiles per item, enough items
         // per node that a level of a few nodes still fills the 3 CTAs/SM
         const char *fe = getenv("PG_CODON_FLOW"), *te = getenv("PG_FLOW_TCH");
+        inst->flow_ver = (fe && atoi(fe) == 1) ? 1 : 2;
         if (fe && atoi(fe) == 0) {
             inst->flow_tch = 0;
+        } else if (inst->flow_ver == 2) {
+            // warp-specialised TMA kernel: one tile per item (loads overlap compute)
+            inst->flow_tch = 1;
+            CK(cudaFuncSetAttribute(cf.flow2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.flow2_smem), "smem attr");
+            int rc = make_tile_maps(inst);
+            if (rc) return rc;
         } else if (te && atoi(te) > 0) {
             inst->flow_tch = std::min(atoi(te), L.n_tiles);
         } else {
@@ -1032,6 +1080,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
     const Layout &L = inst->L;
     const int R = inst->cfg.categories;
     CK(cudaMemsetAsync(inst->at<int>(L.off_status), 0x7f, sizeof(int), inst->stream), "status reset");
+    CK(cudaMemsetAsync(inst->at<int>(L.off_status) + 1, 0, sizeof(int), inst->stream), "stall flag reset");
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[0], inst->stream, cudaEventRecordExternal), "event");
     const double *V = inst->at<double>(L.off_V), *Vi = inst->at<double>(L.off_Vi),
                  *lam = inst->at<double>(L.off_lam), *rates = inst->at<double>(L.off_rates),
@@ -1084,10 +1133,18 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
             const int npre = f.ntask - f.npost;
             const int items = f.npost * R * f.nch * f.phalf + (npre + (f.defer ? npre : 0)) * R * f.nch;
             f.trace = inst->flow_trace_n == (size_t)items ? inst->flow_trace : nullptr;
-            void *args[] = {&c, &f};
-            CK(cudaLaunchKernel(cf.flow, dim3(std::min(items, cf.ctas_per_sm * inst->sm_count)),
-                                dim3(cf.threads), args, cf.flow_smem, inst->stream),
-               "codon flow launch");
+            if (inst->flow_ver == 2) {
+                const int items2 = f.ntask * R * L.n_tiles;
+                void *args2[] = {&c, &f, &inst->tmaps};
+                CK(cudaLaunchKernel(cf.flow2, dim3(std::min(items2, cf.flow2_ctas * inst->sm_count)),
+                                    dim3(cf.flow2_threads), args2, cf.flow2_smem, inst->stream),
+                   "codon flow2 launch");
+            } else {
+                void *args[] = {&c, &f};
+                CK(cudaLaunchKernel(cf.flow, dim3(std::min(items, cf.ctas_per_sm * inst->sm_count)),
+                                    dim3(cf.threads), args, cf.flow_smem, inst->stream),
+                   "codon flow launch");
+            }
         }
         for (size_t i = 0; inst->flow_tch == 0 && i + 1 < pl.post_off.size(); ++i) {
             int off = pl.post_off[i], cnt = pl.post_off[i + 1] - off;
@@ -1227,10 +1284,11 @@ int pg_compute(pg_instance *inst, double *log_likelihood, double *gradient) {
     if ((rc = launch_eval(inst, d_out))) return rc;
     CK(cudaMemcpyAsync(inst->out_pinned, d_out, sizeof(double) * (L.B + 1), cudaMemcpyDeviceToHost, inst->stream),
        "result D2H");
-    CK(cudaMemcpyAsync(inst->status_pinned, inst->at<int>(L.off_status), sizeof(int), cudaMemcpyDeviceToHost,
+    CK(cudaMemcpyAsync(inst->status_pinned, inst->at<int>(L.off_status), 2 * sizeof(int), cudaMemcpyDeviceToHost,
                        inst->stream), "status D2H");
     CK(cudaStreamSynchronize(inst->stream), "compute sync");
     inst->staged_pending = false;
+    if (inst->status_pinned[1]) return inst->fail(PG_ERR_CUDA, "codon flow schedule stalled (> 20 s waiting for an input)");
     const int zp = inst->status_pinned[0];
     if (zp != 0x7f7f7f7f) {
         *log_likelihood = -INFINITY;
@@ -1286,9 +1344,10 @@ int pg_check_status(pg_instance *inst, int32_t *zero_pattern) {
     DeviceGuard dg(inst);
     if (!inst) return PG_ERR_ARG;
     int v = 0;
-    CK(cudaMemcpyAsync(inst->status_pinned, inst->at<int>(inst->L.off_status), sizeof(int), cudaMemcpyDeviceToHost,
+    CK(cudaMemcpyAsync(inst->status_pinned, inst->at<int>(inst->L.off_status), 2 * sizeof(int), cudaMemcpyDeviceToHost,
                        inst->stream), "status D2H");
     CK(cudaStreamSynchronize(inst->stream), "status sync");
+    if (inst->status_pinned[1]) return inst->fail(PG_ERR_CUDA, "codon flow schedule stalled (> 20 s waiting for an input)");
     v = inst->status_pinned[0];
     const bool bad = v != 0x7f7f7f7f;
     if (zero_pattern) *zero_pattern = bad ? v : -1;

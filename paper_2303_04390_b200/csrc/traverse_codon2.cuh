@@ -1,0 +1,437 @@
+// traverse_codon2.cuh -- codon path (fp64, S > 16 padded to SP = 64 / 128),
+// one-launch dataflow schedule, warp-specialised with TMA staging.
+//
+// Same work items, data layout (fragment order, traverse_codon.cuh) and
+// dependency counters as codon_flow_kernel; what changes is how a CTA runs
+// them.  A CTA is NW consumer warps (warp w owns output columns 8w..8w+7 of
+// every [32 x SP] x [SP x SP] product) plus ONE PRODUCER warp, joined by an
+// NST-stage shared-memory ring (mbarriers "full" / "empty"):
+//   producer  claims the next item (global counter, topological order),
+//             prefetches the item's B operands (P, Q fragments) into L1,
+//             waits (acquire) until the item's inputs are published, then
+//             stages them: the partial-likelihood TILES (u of internal
+//             children, q of the parent, u of partial tips) with TMA tensor
+//             loads (cp.async.bulk.tensor, SASS UTMALDG; 16 KB per tile, one
+//             instruction), state-tip tiles as row gathers of P' (cp.async,
+//             completion tracked by the same mbarrier), and the per-pattern
+//             rescaling exponents and tip states;
+//   consumers wait on "full", run the item's GEMMs on the FP64 tensor path
+//             (mma.sync m8n8k4 f64, SASS DMMA), store results, publish
+//             completion (fence + atomic counter) and release the stage.
+// While the consumers compute item i, the producer is already waiting for /
+// loading item i+1 (and i+2 with three stages), so dependency waits and tile
+// loads leave the tensor pipe's critical path.
+//   post item (node k, category r, tile): p = u_a o u_b formed in place,
+//             u_k = p P_k' (Eq. 2), rows scaled by the children's exponents;
+//             at the root the Eq. 3 terms P(gamma_r) pi' p.
+//   pre item  (parent k, category r, tile): q_c = (q_k o u_sib) P_c (Eq. 4)
+//             for internal children -- the A operand formed on the fly --
+//             published before the Eq. 8 terms num_c = x_c'(Q u_c),
+//             den = x_c'u_c (Eq. 6-8; state tips: rows of D').
+// Paper: Eq. 2, Eq. 3, Eq. 4, Eq. 6-8
+// P:274-365; Alg. 1/2's prefetch of partials into shared memory P:385-389,
+// P:633-634 (here: TMA).
+#pragma once
+#include <cuda.h>
+
+#include "traverse_codon.cuh"
+
+namespace pg {
+namespace codon {
+
+struct TmaMaps {
+    CUtensorMap u;      // u    as [rows][256] doubles, one tile = TILE/256 rows
+    CUtensorMap q;      // q    (same geometry)
+    CUtensorMap utip;   // utip (same geometry; partial tips)
+};
+
+__device__ __forceinline__ void tma_load_tile(uint32_t dst, const CUtensorMap *map, int row, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(row), "r"(bar)
+        : "memory");
+}
+// arrive on `bar` when this thread's prior cp.async copies have landed
+// (pending count incremented now, decremented at completion)
+__device__ __forceinline__ void cp_async_mbar_arrive(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+    asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+// Poll a completion counter (acquire) until >= v.  A stall longer than
+// ~20 s (a schedule bug, or a neighbour that never lets a CTA run) is
+// reported through status[1] instead of trapping, and the wait gives up so
+// the launch terminates; pg_check_status / pg_compute turn it into an error.
+__device__ __forceinline__ void wait_count2(const int *p, int v, int *status) {
+    int x;
+    const unsigned long long t0 = gtimer();
+    for (unsigned it = 0;; ++it) {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
+        if (x >= v) return;
+        if ((it & 1023u) == 1023u && gtimer() - t0 > 20000000000ull) {
+            atomicExch(status + 1, 1);
+            return;
+        }
+        __nanosleep(32);
+    }
+}
+
+// Per-stage metadata written by the producer (generic stores, ordered before
+// its arrive on "full").
+struct alignas(16) Meta2 {
+    int item, task, r, tile;
+    int4 lev;                 // {k, child a, child b, kinds}
+    int fa[T], fb[T];         // children's fmax (IEEE exponent fields), internal children
+    int fq[T];                // qmax of the parent (pre, non-root)
+    int Ea[T], Eb[T];         // children's cumulative exponents (post, r == 0)
+    uint8_t sa[T], sb[T];     // state codes of state-tip children
+};
+
+template <int SP> constexpr int flow2_nst() { return 2; }
+template <int SP> constexpr int flow2_ctas() { return SP == 64 ? 2 : 1; }
+template <int SP> constexpr int flow2_threads() { return (SP / 8 + 1) * 32; }
+template <int SP> constexpr size_t flow2_stage() { return (size_t)3 * T * SP * 8 + ((sizeof(Meta2) + 127) / 128) * 128; }
+template <int SP>
+constexpr size_t flow2_smem() {
+    return 128 + (size_t)flow2_nst<SP>() * flow2_stage<SP>() + (size_t)3 * (SP / 8) * T * 8;   // barriers, ring, Eq. 8 partials
+}
+
+template <int SP>
+__global__ void __launch_bounds__(flow2_threads<SP>(), flow2_ctas<SP>())
+    codon_flow2_kernel(const CodonArgs a, const FlowArgs f, const __grid_constant__ TmaMaps tm) {
+    CODON_GEO;
+    constexpr int NST = flow2_nst<SP>();
+    constexpr size_t STG = flow2_stage<SP>();
+    constexpr int ROWS = TILE / 256;                       // tensor-map rows per tile
+    constexpr unsigned TILE_B = (unsigned)TILE * 8u;
+    extern __shared__ __align__(128) unsigned char smem2[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem2);
+    uint64_t *empty = full + NST;
+    unsigned char *ring = smem2 + 128;
+    double *part = reinterpret_cast<double *>(ring + NST * STG);          // [3][NW][T]
+    const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int R = a.R, ntiles = a.ntiles, N = a.N;
+    const int root = 2 * N - 2;
+    const int nitems = f.ntask * R * ntiles;
+    auto tileA = [&](int s) { return reinterpret_cast<double *>(ring + s * STG); };
+    auto meta = [&](int s) { return reinterpret_cast<Meta2 *>(ring + s * STG + 3 * (size_t)TILE * 8); };
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NST; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // ================================ producer ================================
+    if (warp == NW) {
+        for (int g = 0;; ++g) {
+            const int s = g % NST;
+            if (g >= NST) mbar_wait_u32(empty_u + 8u * s, (uint32_t)(g / NST + 1) & 1u);
+            int item = 0;
+            if (lane == 0) item = atomicAdd(f.ctr, 1);
+            item = __shfl_sync(0xffffffffu, item, 0);
+            Meta2 *m = meta(s);
+            const uint32_t bar = full_u + 8u * s;
+            if (item >= nitems) {
+                if (lane == 0) {
+                    m->item = -1;
+                    mbar_arrive_u32(bar);
+                }
+                return;
+            }
+            const int task = item / (R * ntiles);
+            const int rem = item - task * R * ntiles;
+            const int r = rem / ntiles, tile = rem - r * ntiles;
+            const int4 e = a.lev4[task];
+            const int k = e.x, ca = e.y, cb = e.z, kinds = e.w;
+            const bool post = task < f.npost;
+            // B operands of the item's products into this SM's L1 while we wait
+            {
+                auto pf = [&](const double *Bg) {
+                    for (int i = lane; i < (int)MAT / 16; i += 32) prefetch_l1(Bg + 16 * i);
+                };
+                if (post) {
+                    if (k != root) pf(a.PBpost + ((size_t)k * R + r) * MAT);
+                } else {
+                    if (ca >= N) pf(a.PBpre + ((size_t)ca * R + r) * MAT);
+                    if (cb >= N) pf(a.PBpre + ((size_t)cb * R + r) * MAT);
+                }
+            }
+            if (lane == 0) {
+                if (post || k == root) {
+                    if (ca >= N) wait_count2(f.rpost + (size_t)(ca - N) * ntiles + tile, R, a.status);
+                    if (cb >= N) wait_count2(f.rpost + (size_t)(cb - N) * ntiles + tile, R, a.status);
+                } else {
+                    wait_count2(f.rpre + (size_t)(k - N) * ntiles + tile, R, a.status);
+                }
+                fence_proxy_async_global();          // published generic stores -> our async-proxy reads
+                m->item = item;
+                m->task = task;
+                m->r = r;
+                m->tile = tile;
+                m->lev = e;
+            }
+            __syncwarp();
+            const int pat = tile * T + lane;
+            const int kc[2] = {kinds & 3, (kinds >> 2) & 3};
+            const int cc[2] = {ca, cb};
+            // per-pattern metadata (lane = pattern of the tile)
+            m->fa[lane] = ca >= N ? __ldcg(a.fmax + (size_t)(ca - N) * a.Cpad + pat) : 0;
+            m->fb[lane] = cb >= N ? __ldcg(a.fmax + (size_t)(cb - N) * a.Cpad + pat) : 0;
+            if (!post) m->fq[lane] = k != root ? __ldcg(a.qmax + (size_t)(k - N) * a.Cpad + pat) : 0;
+            if (post && r == 0 && k != root) {
+                m->Ea[lane] = ca >= N ? __ldcg(a.E + (size_t)(ca - N) * a.Cpad + pat) : 0;
+                m->Eb[lane] = cb >= N ? __ldcg(a.E + (size_t)(cb - N) * a.Cpad + pat) : 0;
+            }
+            if (post && r == 0 && k == root) {
+                m->Ea[lane] = ca >= N ? __ldcg(a.E + (size_t)(ca - N) * a.Cpad + pat) : 0;
+                m->Eb[lane] = cb >= N ? __ldcg(a.E + (size_t)(cb - N) * a.Cpad + pat) : 0;
+            }
+            int st2[2];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                st2[c] = (cc[c] < N && kc[c] == 1) ? a.tip_states[(size_t)cc[c] * a.Cpad + pat] : 0;
+                (c ? m->sb : m->sa)[lane] = (uint8_t)st2[c];
+            }
+            // state-tip tiles: rows of P' picked by state (u_tip[s] = P[s][state];
+            // missing data: P 1), gathered in fragment order with cp.async
+            bool gathered = false;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                if (cc[c] >= N || kc[c] != 1) continue;
+                const size_t br = (size_t)cc[c] * R + r;
+                const double *PT = a.PT + br * MAT, *ONE = a.PONE + br * SP;
+                double *dst = tileA(s) + (size_t)c * TILE;
+                for (int i2 = lane; i2 < TILE / 2; i2 += 32) {
+                    int mm, kk;
+                    apos_inv<SP>(2 * i2, mm, kk);
+                    const int sv = __shfl_sync(0xffffffffu, st2[c], mm);
+                    cp_async16(dst + 2 * i2, sv < a.S ? PT + (size_t)sv * SP + kk : ONE + kk);
+                }
+                gathered = true;
+            }
+            // root of the pre-order: q = pi (generic stores into the Q tile)
+            if (!post && k == root) {
+                double *Qs = tileA(s) + 2 * (size_t)TILE;
+                for (int idx = lane; idx < TILE; idx += 32) Qs[idx] = a.pi[((idx >> 5) & (KT - 1)) * 4 + (idx & 3)];
+            }
+            if (gathered) cp_async_mbar_arrive(bar);
+            __syncwarp();
+            if (lane == 0) {
+                unsigned bytes = 0;
+                for (int c = 0; c < 2; ++c)
+                    if (cc[c] >= N || kc[c] == 2) bytes += TILE_B;
+                if (!post && k != root) bytes += TILE_B;
+                fence_proxy_async_smem();            // earlier generic accesses of this stage -> TMA writes
+                mbar_arrive_expect_tx_u32(bar, bytes);
+                const uint32_t st_u = smem_u32(tileA(s));
+                for (int c = 0; c < 2; ++c) {
+                    if (cc[c] >= N)
+                        tma_load_tile(st_u + c * TILE_B, &tm.u, (int)((((size_t)(cc[c] - N) * R + r) * ntiles + tile) * ROWS), bar);
+                    else if (kc[c] == 2)
+                        tma_load_tile(st_u + c * TILE_B, &tm.utip, (int)((((size_t)cc[c] * R + r) * ntiles + tile) * ROWS), bar);
+                }
+                if (!post && k != root)
+                    tma_load_tile(st_u + 2 * TILE_B, &tm.q, (int)((((size_t)(k - N) * R + r) * ntiles + tile) * ROWS), bar);
+            }
+        }
+    }
+
+    // ================================ consumers ===============================
+    const int w = warp;
+    for (int g = 0;; ++g) {
+        const int s = g % NST;
+        mbar_wait_u32(full_u + 8u * s, (uint32_t)(g / NST) & 1u);
+        const Meta2 *m = meta(s);
+        const int item = m->item;
+        if (item < 0) break;
+        const int r = m->r, tile = m->tile;
+        const int k = m->lev.x, ca = m->lev.y, cb = m->lev.z, kinds = m->lev.w;
+        const int pat0 = tile * T;
+        double *As = tileA(s), *Bs = As + TILE, *Qs = As + 2 * (size_t)TILE;
+        const bool post = m->task < f.npost;
+        if (post) {
+            auto scA = [&](int mm) { return ca >= N ? pow2neg(lazy_exp(m->fa[mm])) : 1.0; };
+            auto scB = [&](int mm) { return cb >= N ? pow2neg(lazy_exp(m->fb[mm])) : 1.0; };
+            auto storeE = [&]() {
+                const int mm = threadIdx.x;
+                const int Ek = m->Ea[mm] + m->Eb[mm] + (ca >= N ? lazy_exp(m->fa[mm]) : 0) +
+                               (cb >= N ? lazy_exp(m->fb[mm]) : 0);
+                a.E[(size_t)(k - N) * a.Cpad + pat0 + mm] = Ek;
+            };
+            if (k == root) {
+                if (r == 0 && threadIdx.x < T) storeE();
+                // Eq. 3 terms: thread -> (pattern mm = tid/8, states j, j+8, ...)
+                const int mm = threadIdx.x >> 3, j = threadIdx.x & 7;
+                double sum = 0.0;
+                if (mm < T)
+                    for (int kk = j; kk < SP; kk += 8) {
+                        const int p = apos<SP>(mm, kk);
+                        sum = fma(a.pi[kk], As[p] * Bs[p], sum);
+                    }
+                sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+                sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+                sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+                if (j == 0 && mm < T) a.Lpart[(size_t)r * a.Cpad + pat0 + mm] = a.cat_w[r] * sum * (scA(mm) * scB(mm));
+            } else {
+                double bfr[KT];
+                load_bfrag<SP>(bfr, a.PBpost + ((size_t)k * R + r) * MAT, w, lane);
+                // p = u_a o u_b in place (one A operand for the GEMM)
+                for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += NT) {
+                    double2 *pa = reinterpret_cast<double2 *>(As) + i2;
+                    const double2 tb = reinterpret_cast<const double2 *>(Bs)[i2];
+                    double2 v = *pa;
+                    v.x *= tb.x;
+                    v.y *= tb.y;
+                    *pa = v;
+                }
+                consumer_sync(NT);
+                double acc[4][2];
+                gemm_tile<SP>(acc, As, bfr, lane);
+                if (r == 0 && threadIdx.x < T) storeE();
+                double *out = a.u + (((size_t)(k - N) * R + r) * ntiles + tile) * TILE;
+                int *fm = a.fmax + (size_t)(k - N) * a.Cpad + pat0;
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) {
+                    const int mm = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                    const double f2 = scA(mm) * scB(mm);
+                    const double c0 = acc[mt][0] * f2, c1 = acc[mt][1] * f2;
+                    *reinterpret_cast<double2 *>(out + apos<SP>(mm, n)) = make_double2(c0, c1);
+                    int fx = max(__double2hiint(c0) >> 20, __double2hiint(c1) >> 20);
+                    fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 1));
+                    fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 2));
+                    if ((lane & 3) == 0) atomicMax(fm + mm, fx);
+                }
+            }
+            fence_proxy_async_global();              // our generic stores -> later TMA reads (other CTAs)
+            consumer_sync(NT);                       // stage consumed, outputs issued
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(f.rpost + (size_t)(k - N) * ntiles + tile, 1);
+                mbar_arrive_u32(empty_u + 8u * s);
+            }
+            continue;
+        }
+        // ------------------------------- pre item ------------------------------
+        const int ch[2] = {ca, cb};
+        auto scQ = [&](int mm) { return k == root ? 1.0 : pow2neg(lazy_exp(m->fq[mm])); };
+        auto scC = [&](int c, int mm) {
+            return ch[c] >= N ? pow2neg(lazy_exp(c ? m->fb[mm] : m->fa[mm])) : 1.0;
+        };
+        double *Us[2] = {As, Bs};
+        // phase A (the pre-order chain): q_c = x_c P_c, x_c = q_k o u_sib formed
+        // in the A-fragment loads; rows scaled by the q_k and sibling exponents
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int node = ch[c];
+            if (node < N) continue;
+            double bq[KT], acc[4][2];
+            load_bfrag<SP>(bq, a.PBpre + ((size_t)node * R + r) * MAT, w, lane);
+            const double *Ub = Us[1 - c];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+#pragma unroll
+            for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) {
+                    const int p = (mt * KT + kt) * 32 + lane;
+                    dmma(acc[mt], Qs[p] * Ub[p], bq[kt]);
+                }
+            double *out = a.q + (((size_t)(node - N) * R + r) * ntiles + tile) * TILE;
+            int *qm = a.qmax + (size_t)(node - N) * a.Cpad + pat0;
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int mm = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                const double f2 = scQ(mm) * scC(1 - c, mm);
+                const double c0 = acc[mt][0] * f2, c1 = acc[mt][1] * f2;
+                *reinterpret_cast<double2 *>(out + apos<SP>(mm, n)) = make_double2(c0, c1);
+                int fx = max(__double2hiint(c0) >> 20, __double2hiint(c1) >> 20);
+                fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 1));
+                fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 2));
+                if ((lane & 3) == 0) atomicMax(qm + mm, fx);
+            }
+        }
+        if (ca >= N || cb >= N) {                    // publish q of the internal children
+            fence_proxy_async_global();
+            consumer_sync(NT);
+            if (threadIdx.x == 0) {
+                __threadfence();
+                if (ca >= N) atomicAdd(f.rpre + (size_t)(ca - N) * ntiles + tile, 1);
+                if (cb >= N) atomicAdd(f.rpre + (size_t)(cb - N) * ntiles + tile, 1);
+            }
+        }
+        // phase B: Eq. 8 terms; den = x_c'u_c is the same for both children
+        // (q_k o u_a o u_b, Eq. 5).  Tiles are unscaled: the factors cancel in
+        // the ratio, which is formed over categories afterwards.
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int node = ch[c];
+            const size_t br = (size_t)node * R + r;
+            const int kind = (kinds >> (2 * c)) & 3;
+            double acc[4][2];
+            if (node >= N || kind == 2) {
+                double b[KT];
+                load_bfrag<SP>(b, a.QB, w, lane);
+                gemm_tile<SP>(acc, Us[c], b, lane);
+            } else {
+                const uint8_t *stc = c ? m->sb : m->sa;
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) {
+                    const int mm = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                    const int sv = stc[mm];
+                    if (sv < a.S) {
+                        const double2 v = __ldg(reinterpret_cast<const double2 *>(a.DT + br * MAT + (size_t)sv * SP + n));
+                        acc[mt][0] = v.x;
+                        acc[mt][1] = v.y;
+                    } else {
+                        acc[mt][0] = acc[mt][1] = 0.0;
+                    }
+                }
+            }
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int mm = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                const int p = apos<SP>(mm, n);
+                const double2 q2 = *reinterpret_cast<const double2 *>(Qs + p);
+                const double2 o2 = *reinterpret_cast<const double2 *>(Us[1 - c] + p);
+                const double x0 = q2.x * o2.x, x1 = q2.y * o2.y;
+                double sn = x0 * acc[mt][0] + x1 * acc[mt][1];
+                sn += __shfl_xor_sync(0xffffffffu, sn, 1);
+                sn += __shfl_xor_sync(0xffffffffu, sn, 2);
+                if ((lane & 3) == 0) part[(c * NW + w) * T + mm] = sn;
+                if (c == 0) {
+                    const double2 u2 = *reinterpret_cast<const double2 *>(Us[0] + p);
+                    double sd = x0 * u2.x + x1 * u2.y;
+                    sd += __shfl_xor_sync(0xffffffffu, sd, 1);
+                    sd += __shfl_xor_sync(0xffffffffu, sd, 2);
+                    if ((lane & 3) == 0) part[(2 * NW + w) * T + mm] = sd;
+                }
+            }
+        }
+        consumer_sync(NT);                           // stage and partials complete
+        if (threadIdx.x < T) {                       // fixed-order sums over the warps
+            const int mm = threadIdx.x;
+            double sd = 0.0, sn0 = 0.0, sn1 = 0.0;
+            for (int ww = 0; ww < NW; ++ww) {
+                sn0 += part[ww * T + mm];
+                sn1 += part[(NW + ww) * T + mm];
+                sd += part[(2 * NW + ww) * T + mm];
+            }
+            const double wr = a.cat_w[r], gr = a.cat_g[r];
+            double2 *nd = reinterpret_cast<double2 *>(a.numden);
+            const bool qa = ca >= N || (kinds & 3) == 2, qb = cb >= N || ((kinds >> 2) & 3) == 2;
+            const double s0 = qa ? gr * wr : wr, s1 = qb ? gr * wr : wr;
+            nd[((size_t)ca * R + r) * a.Cpad + pat0 + mm] = make_double2(s0 * sn0, wr * sd);
+            nd[((size_t)cb * R + r) * a.Cpad + pat0 + mm] = make_double2(s1 * sn1, wr * sd);
+        }
+        consumer_sync(NT);                           // partials read before the next item writes them
+        if (threadIdx.x == 0) mbar_arrive_u32(empty_u + 8u * s);
+    }
+}
+
+}  // namespace codon
+}  // namespace pg

@@ -416,13 +416,17 @@ def test_hmc_leapfrog_matches_oracle_trajectory(model, N, R, C):
     inst.close()
 
 
-@pytest.mark.parametrize("env", [{"PG_CODON_FLOW": "0"}, {"PG_FLOW_TCH": "3"}, {"PG_FLOW_TCH": "1"},
-                                 {"PG_FLOW_DEFER": "1"}, {"PG_FLOW_DEFER": "0"}, {"PG_FLOW_HALF": "1"},
-                                 {"PG_FLOW_HALF": "1", "PG_FLOW_DEFER": "1"}])
+@pytest.mark.parametrize("env", [{"PG_CODON_FLOW": "0"}, {"PG_CODON_FLOW": "2"}, {"PG_CODON_FLOW": "1"},
+                                 {"PG_CODON_FLOW": "1", "PG_FLOW_TCH": "3"},
+                                 {"PG_CODON_FLOW": "1", "PG_FLOW_TCH": "1"},
+                                 {"PG_CODON_FLOW": "1", "PG_FLOW_DEFER": "1"},
+                                 {"PG_CODON_FLOW": "1", "PG_FLOW_HALF": "1"},
+                                 {"PG_CODON_FLOW": "1", "PG_FLOW_HALF": "1", "PG_FLOW_DEFER": "1"}])
 def test_codon_schedules(env, monkeypatch):
-    """The level-by-level codon kernels (PG_CODON_FLOW=0) and other flow chunk
-    sizes give the same parity as the default one-launch schedule (read when
-    the instance plans its launches)."""
+    """Every codon schedule gives the same parity: the level-by-level kernels
+    (PG_CODON_FLOW=0), the round-1 one-launch flow kernel (=1, with its chunk
+    / deferral / half-tile options) and the default warp-specialised TMA flow
+    kernel (=2) (read when the instance plans its launches)."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     _compare(ps.config3_yeast(N=24, C=150))
