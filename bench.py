@@ -232,12 +232,16 @@ def load_traffic(key: str):
         return None
 
 
-def roofline(pb, C: int, variant: int, precision: str, kms: dict, peaks: dict, traffic, flow: bool) -> dict:
+def roofline(pb, C: int, variant: int, precision: str, kms: dict, peaks: dict, traffic, flow: bool,
+             eval_ms: float) -> dict:
     """Roofline object of the dominant kernel (the traversal) on SURVEY §8(d)'s
     algorithmic basis: B_min for the HBM-bound S <= 16 paths, F_min for the
-    FP64 tensor path; the schedule / paper-literal / ncu-DRAM figures beside."""
+    FP64 tensor path; the schedule / paper-literal / ncu-DRAM figures beside.
+    kernel_ms is the traversal's event-timed duration (separate timing pass);
+    eval_frac uses the whole measured evaluation (A1 + traversal + reduction,
+    as timed per step)."""
     t = kms["traverse"] * 1e-3
-    ev = (kms["pmat"] + kms["traverse"] + kms["reduce"]) * 1e-3
+    ev = eval_ms * 1e-3
     if variant == 2 or variant == 1:
         fl = flop_counts(pb, C)
         hb = hbm_counts(pb, C, precision)
@@ -317,32 +321,40 @@ def workload_config(args, pb, C, world, lo=0, hi=None, flushed=True, shard=0):
 
 # ------------------------------------------------------------------ ours ----
 
-def time_steps(step, stream, steps, warmup, flush, inst=None, sample_every=16):
+def time_steps(step, stream, steps, warmup, flush, inst=None, ksteps=32):
     """Warm-up, then `steps` steps each bracketed by CUDA events on `stream`
-    (L2 flushed outside the events); per-kernel split from the instance's
-    in-graph events on a sample of steps."""
+    (L2 flushed outside the events).  Then, separately, `ksteps` more steps
+    with the instance's in-graph kernel events enabled give the per-kernel
+    split (events between kernels also switch off the A1 -> flow
+    programmatic launch, so the split is not taken from the timed steps)."""
     import torch
+    kt = {"pmat": 0.0, "traverse": 0.0, "reduce": 0.0}
     with torch.cuda.stream(stream):
         for i in range(warmup):
             step(i)
         stream.synchronize()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-        kt = {"pmat": 0.0, "traverse": 0.0, "reduce": 0.0}
-        ns = 0
         for k in range(steps):
             if flush is not None:
                 flush.zero_()
             evs[k][0].record(stream)
             step(warmup + k)
             evs[k][1].record(stream)
-            if inst is not None and (k % sample_every == 0 or k == steps - 1):
-                t = inst.kernel_times()
-                for n in kt:
-                    kt[n] += t[n]
-                ns += 1
         stream.synchronize()
+        if inst is not None and ksteps > 0:
+            inst.set_kernel_timing(True)
+            for k in range(ksteps + 2):
+                if flush is not None:
+                    flush.zero_()
+                step(warmup + k % max(steps, 1))
+                if k >= 2:
+                    t = inst.kernel_times()
+                    for n in kt:
+                        kt[n] += t[n] / ksteps
+            inst.set_kernel_timing(False)
+            stream.synchronize()
     ms = [a.elapsed_time(b) for a, b in evs]
-    return ms, {n: v / max(ns, 1) for n, v in kt.items()}
+    return ms, kt
 
 
 def bench_instance(pb, precision, device, lo, hi, steps, warmup, flush, seed_off=99):
@@ -361,13 +373,11 @@ def bench_instance(pb, precision, device, lo, hi, steps, warmup, flush, seed_off
         inst.set_branch_lengths_device(bl_dev[i])
         inst.compute_device(out)
 
-    inst.set_kernel_timing(True)
     ms, kt = time_steps(step, inst.stream, steps, warmup, flush, inst)
     zp = inst.check_status()
     assert zp < 0, f"zero likelihood at pattern {zp}"
     info = inst.plan_info()
     nk = inst.kernels_per_eval()
-    inst.set_kernel_timing(False)
     return inst, ms, kt, info, nk, bls
 
 
@@ -411,7 +421,7 @@ def run_ours(args):
     # one CUDA graph per step: [branch lengths D2D, evaluation kernels, allreduce]
     # at N > 1 (the library enqueues into the caller's capture)
     ev = pg.ShardEvaluation(pb, rank=0 if shard else rank, world=shard or world, device=local,
-                            precision=args.precision, capture=world > 1, timing=True)
+                            precision=args.precision, capture=world > 1, timing=world > 1)
     inst = ev.inst
 
     def step(i):
@@ -481,8 +491,10 @@ def run_ours(args):
                     "path": ("pg_set_branch_lengths + pg_compute (host buffers)" if world == 1 else
                              "pinned H2D of b, captured [b, evaluation, NCCL allreduce] graph, D2H of [logL, g]")},
             "gpu_launches": args.steps * nk,
-            "roofline": roofline(pb, Cl, variant, args.precision, kt, peaks, traffic, info.get("flow_tiles", 0) > 0),
+            "roofline": roofline(pb, Cl, variant, args.precision, kt, peaks, traffic, info.get("flow_tiles", 0) > 0,
+                                 ms_per_step),
             "kernel_ms": {k: round(v, 5) for k, v in kt.items()},
+            "kernel_ms_note": "per-kernel split from a separate 32-step pass with in-graph events (A1 -> flow PDL off)",
             "plan": info,
             "clocks": clk.summary(),
         }
@@ -517,7 +529,9 @@ def run_extra_configs(args, peaks):
                      "patterns_timed": hi - lo, "steps": steps, "warmup": warmup,
                      "kernel_ms": {k: round(v, 5) for k, v in kt.items()},
                      "roofline": roofline(pb, hi - lo, info["kernel_variant"], "fp64", kt, peaks,
-                                          load_traffic(traffic_key(cfg, "fp64", shard)), info.get("flow_tiles", 0) > 0)}
+                                          load_traffic(traffic_key(cfg, "fp64", shard)), info.get("flow_tiles", 0) > 0,
+                                          mps),
+                     "plan": info}
         if shard:
             out[name]["note"] = (f"one GPU timing rank 0's pattern shard [{lo},{hi}) of a {shard}-GPU run "
                                  "(the per-GPU work of that run; the allreduce of 2N-1 doubles is not included)")

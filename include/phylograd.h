@@ -254,6 +254,11 @@ typedef struct {
     int32_t flow_tiles;              /* codon: 32-pattern tiles per item of
                                         the one-launch dataflow schedule;
                                         0 = one launch per tree level     */
+    int32_t flow_version;            /* codon: 2 = warp-specialised TMA ring,
+                                        1 = round-1 flow kernel            */
+    int32_t flow_stages;             /* codon flow v2: ring stages (1 or 2) */
+    int32_t flow_pdl;                /* codon flow v2: launched behind A1
+                                        with programmatic dependent launch */
 } pg_plan_info;
 int pg_get_plan_info(const pg_instance *inst, pg_plan_info *info);
 

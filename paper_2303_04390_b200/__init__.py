@@ -48,7 +48,7 @@ class PgConfig(ctypes.Structure):
 class PgPlanInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("post_depth", "pre_depth", "grid", "block", "smem_bytes",
                                               "prefetch_depth", "padded_patterns", "kernel_variant",
-                                              "flow_tiles")]
+                                              "flow_tiles", "flow_version", "flow_stages", "flow_pdl")]
 
 
 _vp = ctypes.c_void_p

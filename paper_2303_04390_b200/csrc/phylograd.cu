@@ -152,7 +152,7 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         L->off_E = take((size_t)(N - 1) * L->Cpad * 4);
         // fmax [N-1], qmax [N-2], then the flow schedule's counters
         // {item counter, rpost [N-1][<= ntiles], rpre [N-1][<= ntiles]}: one memset
-        L->flow_bytes = ((size_t)32 + (size_t)2 * (N - 1) * L->n_tiles) * 4;
+        L->flow_bytes = ((size_t)32 + (size_t)2 * (N - 1) * L->n_tiles + (size_t)L->B * R) * 4;   // + A1 done flags
         L->reset_bytes = (size_t)(2 * N - 3) * L->Cpad * 4 + L->flow_bytes;
         L->off_fmax = take(L->reset_bytes);
         L->off_qmax = L->off_fmax + (size_t)(N - 1) * L->Cpad * 4;
@@ -212,6 +212,8 @@ struct pg_instance {
     int prefetch = 4, smem = 0, grid = 0, block = 0, tiles_per_cta = 1, prog_smem_off = 0;
     int flow_tch = 0;                   // codon: tiles per flow item (0 = level-by-level kernels)
     int flow_ver = 2;                   // codon flow kernel: 2 = warp-specialised TMA ring (codon_flow2_kernel), 1 = round-1 kernel
+    int flow_nst = 2;                   // codon_flow2_kernel ring stages (1: latency, 2: throughput)
+    int flow_pdl = 1;                   // A1 -> flow programmatic dependent launch (PG_FLOW_PDL=0 disables)
     pg::codon::TmaMaps tmaps{};         // TMA tensor maps of u, q, utip (codon_flow2_kernel)
     int flow_defer = 0;                 // codon flow: Eq. 8 items after all pre items (PG_FLOW_DEFER)
     int flow_half = 0;                  // codon flow: half-tile post items when tch == 1 (PG_FLOW_HALF)
@@ -736,19 +738,21 @@ static void *pmat_fn() { return (void *)pg::pmat_kernel<Real, SP>; }
 
 // kernels and launch geometry of the FP64 tensor-core path for SP = 64 / 128
 struct CodonFns {
-    void *post4, *post2, *pre, *pmat, *flow, *tipu, *tipmask, *flow2;
-    int threads, ctas_per_sm, flow2_threads, flow2_ctas;
-    size_t post_smem, pre_smem, pmat_smem, flow_smem, tipu_smem, flow2_smem;
+    void *post4, *post2, *pre, *pmat, *flow, *tipu, *tipmask, *flow2[2];     // flow2[NST - 1]
+    int threads, ctas_per_sm, flow2_threads, flow2_ctas[2];
+    size_t post_smem, pre_smem, pmat_smem, flow_smem, tipu_smem, flow2_smem[2];
 };
 template <int SP>
 static CodonFns codon_fns_t() {
     namespace c = pg::codon;
     return {(void *)c::codon_post_kernel<SP, 4>, (void *)c::codon_post_kernel<SP, 2>, (void *)c::codon_pre_kernel<SP>,
             (void *)c::codon_pmat_kernel<SP>, (void *)c::codon_flow_kernel<SP>,
-            (void *)c::codon_tipu_kernel<SP>, (void *)c::codon_tipmask_kernel<SP>, (void *)c::codon_flow2_kernel<SP>,
-            c::codon_threads<SP>(), c::codon_ctas_per_sm<SP>(), c::flow2_threads<SP>(), c::flow2_ctas<SP>(),
+            (void *)c::codon_tipu_kernel<SP>, (void *)c::codon_tipmask_kernel<SP>,
+            {(void *)c::codon_flow2_kernel<SP, 1>, (void *)c::codon_flow2_kernel<SP, 2>},
+            c::codon_threads<SP>(), c::codon_ctas_per_sm<SP>(), c::flow2_threads<SP>(),
+            {c::flow2_ctas<SP, 1>(), c::flow2_ctas<SP, 2>()},
             c::post_smem<SP>(), c::pre_smem<SP>(), c::pmat_smem<SP>(), c::flow_smem<SP>(), c::tipu_smem<SP>(),
-            c::flow2_smem<SP>()};
+            {c::flow2_smem<SP, 1>(), c::flow2_smem<SP, 2>()}};
 }
 static CodonFns codon_fns(int SP) { return SP == 128 ? codon_fns_t<128>() : codon_fns_t<64>(); }
 
@@ -911,7 +915,15 @@ static int configure(pg_instance *inst) {
         } else if (inst->flow_ver == 2) {
             // warp-specialised TMA kernel: one tile per item (loads overlap compute)
             inst->flow_tch = 1;
-            CK(cudaFuncSetAttribute(cf.flow2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.flow2_smem), "smem attr");
+            // ring depth: two stages (claim-ahead) when every task has at
+            // least as many items as the two-stage grid has CTAs, else one
+            const char *ne = getenv("PG_FLOW_NST"), *pe = getenv("PG_FLOW_PDL");
+            inst->flow_nst = (ne && atoi(ne) >= 1 && atoi(ne) <= 2) ? atoi(ne)
+                             : (L.n_tiles * R >= cf.flow2_ctas[1] * inst->sm_count ? 2 : 1);
+            inst->flow_pdl = pe ? (atoi(pe) != 0) : 1;
+            for (int v = 0; v < 2; ++v)
+                CK(cudaFuncSetAttribute(cf.flow2[v], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.flow2_smem[v]),
+                   "smem attr");
             int rc = make_tile_maps(inst);
             if (rc) return rc;
         } else if (te && atoi(te) > 0) {
@@ -1091,7 +1103,10 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
                *PT = inst->at<double>(L.off_PT), *DT = inst->at<double>(L.off_DT), *PONE = inst->at<double>(L.off_PONE);
         const double *VA = inst->at<double>(L.off_VA), *ViB = inst->at<double>(L.off_ViB);
         const double *M0 = inst->at<double>(L.off_M0), *Qd = inst->at<double>(L.off_Q);
-        void *args[] = {&VA, &ViB, &M0, &Qd, &lam, &rates, &bl, &S, (void *)&R, &PBpost, &PBpre, &PT, &DT, &PONE};
+        // per-evaluation counters (rescaling maxima, flow counters, A1 flags)
+        CK(cudaMemsetAsync(inst->ws + L.off_fmax, 0, L.reset_bytes, inst->stream), "fmax/flow reset");
+        int *pready = inst->at<int>(L.off_flow) + 32 + (size_t)2 * (inst->cfg.tips - 1) * L.n_tiles;
+        void *args[] = {&VA, &ViB, &M0, &Qd, &lam, &rates, &bl, &S, (void *)&R, &PBpost, &PBpre, &PT, &DT, &PONE, &pready};
         const CodonFns cf = codon_fns(L.SP);
         CK(cudaLaunchKernel(cf.pmat, dim3(L.B * R), dim3(256), args, cf.pmat_smem, inst->stream), "codon pmat launch");
         if (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) {     // u = P p of partial tips (A2's tip step)
@@ -1118,7 +1133,6 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         const CodonFns cf = codon_fns(L.SP);
         const auto &pl = inst->plan;
         const int N = inst->cfg.tips;
-        CK(cudaMemsetAsync(inst->ws + L.off_fmax, 0, L.reset_bytes, inst->stream), "fmax/flow reset");
         if (inst->flow_tch > 0) {
             pg::codon::FlowArgs f{};
             f.ctr = inst->at<int>(L.off_flow);
@@ -1135,10 +1149,23 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
             f.trace = inst->flow_trace_n == (size_t)items ? inst->flow_trace : nullptr;
             if (inst->flow_ver == 2) {
                 const int items2 = f.ntask * R * L.n_tiles;
+                const int v = inst->flow_nst - 1;
+                // programmatic dependent launch right behind A1 (no partial-tip
+                // kernels or timing events in between): items wait on pready
+                const bool pdl = inst->flow_pdl && !inst->timing && !(inst->cfg.flags & PG_FLAG_TIP_PARTIALS);
+                f.pready = pdl ? inst->at<int>(L.off_flow) + 32 + (size_t)2 * (N - 1) * L.n_tiles : nullptr;
                 void *args2[] = {&c, &f, &inst->tmaps};
-                CK(cudaLaunchKernel(cf.flow2, dim3(std::min(items2, cf.flow2_ctas * inst->sm_count)),
-                                    dim3(cf.flow2_threads), args2, cf.flow2_smem, inst->stream),
-                   "codon flow2 launch");
+                cudaLaunchConfig_t lc{};
+                lc.gridDim = dim3(std::min(items2, cf.flow2_ctas[v] * inst->sm_count));
+                lc.blockDim = dim3(cf.flow2_threads);
+                lc.dynamicSmemBytes = cf.flow2_smem[v];
+                lc.stream = inst->stream;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                at[0].val.programmaticStreamSerializationAllowed = 1;
+                lc.attrs = at;
+                lc.numAttrs = pdl ? 1 : 0;
+                CK(cudaLaunchKernelExC(&lc, cf.flow2[v], args2), "codon flow2 launch");
             } else {
                 void *args[] = {&c, &f};
                 CK(cudaLaunchKernel(cf.flow, dim3(std::min(items, cf.ctas_per_sm * inst->sm_count)),
@@ -1407,11 +1434,18 @@ int pg_get_plan_info(const pg_instance *inst, pg_plan_info *info) {
     info->padded_patterns = inst->L.Cpad;
     info->kernel_variant = inst->L.variant;
     info->flow_tiles = inst->flow_tch;
+    info->flow_version = inst->L.variant == 2 && inst->flow_tch > 0 ? inst->flow_ver : 0;
+    info->flow_stages = info->flow_version == 2 ? inst->flow_nst : 0;
+    info->flow_pdl = info->flow_version == 2 && inst->flow_pdl && !inst->timing &&
+                     !(inst->cfg.flags & PG_FLAG_TIP_PARTIALS);
     if (inst->L.variant == 2 && inst->flow_tch > 0) {
         const int nch = (inst->L.n_tiles + inst->flow_tch - 1) / inst->flow_tch;
         const CodonFns cf = codon_fns(inst->L.SP);
-        info->grid = std::min((int)inst->plan.level_nodes.size() * inst->cfg.categories * nch, cf.ctas_per_sm * inst->sm_count);
-        info->smem_bytes = (int)cf.flow_smem;
+        const int v = inst->flow_nst - 1;
+        const int slots = inst->flow_ver == 2 ? cf.flow2_ctas[v] * inst->sm_count : cf.ctas_per_sm * inst->sm_count;
+        info->grid = std::min((int)inst->plan.level_nodes.size() * inst->cfg.categories * nch, slots);
+        info->smem_bytes = (int)(inst->flow_ver == 2 ? cf.flow2_smem[v] : cf.flow_smem);
+        info->block = inst->flow_ver == 2 ? cf.flow2_threads : cf.threads;
     }
     return PG_OK;
 }

@@ -409,6 +409,7 @@ struct FlowArgs {
     int defer;         // 1: pre items compute q only; Eq. 8 items (one per pre item) come after all of them
     int phalf;         // 2: post items are half tiles (16 patterns; needs tch == 1): shorter chain links
     unsigned long long *trace;   // diagnostics (PG_FLOW_TRACE): [item][TRW] = {smid, t_take, t_ready, t_done, phase stamps}
+    const int *pready;           // codon_flow2_kernel under PDL: [B][R] A1 done flags (null: A1 finished before launch)
 };
 
 // ---------------------------------------------------------------------------
@@ -875,8 +876,11 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
                                                          const double *__restrict__ rates,
                                                          const double *__restrict__ bl, int S, int R,
                                                          double *PBpost, double *PBpre, double *PT, double *DT,
-                                                         double *PONE) {
+                                                         double *PONE, int *pready) {
     CODON_GEO;
+    // programmatic dependent launch: the flow kernel may start now; it reads
+    // this CTA's outputs only after pready[branch][r] is published below
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     extern __shared__ __align__(16) unsigned char smem_p[];
     double *Ps = reinterpret_cast<double *>(smem_p);     // [SP][SP+1]: P, then D
     double *e = Ps + SP * (SP + 1), *de = e + SP;        // [SP] each
@@ -957,6 +961,10 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
                 PONE[(size_t)br * SP + s2] = acc;
             }
         __syncthreads();
+    }
+    if (pready && threadIdx.x == 0) {                    // publish (release) for the flow kernel
+        __threadfence();
+        atomicAdd(pready + br, 1);
     }
 }
 template <int SP>

@@ -91,20 +91,30 @@ struct alignas(16) Meta2 {
     uint8_t sa[T], sb[T];     // state codes of state-tip children
 };
 
-template <int SP> constexpr int flow2_nst() { return 2; }
-template <int SP> constexpr int flow2_ctas() { return SP == 64 ? 2 : 1; }
+// NST = ring stages.  NST = 2: the producer claims and stages item i+1 while
+// the consumers compute item i (throughput: full-size workloads).  NST = 1:
+// an item is claimed only when the consumers are free, so a busy CTA never
+// holds back an item another CTA could start (latency: pattern shards whose
+// levels have fewer items than CTA slots), and three CTAs fit on an SM.
+template <int SP, int NST> constexpr int flow2_ctas() { return SP == 64 ? (NST == 1 ? 3 : 2) : 1; }
 template <int SP> constexpr int flow2_threads() { return (SP / 8 + 1) * 32; }
 template <int SP> constexpr size_t flow2_stage() { return (size_t)3 * T * SP * 8 + ((sizeof(Meta2) + 127) / 128) * 128; }
-template <int SP>
+template <int SP, int NST>
 constexpr size_t flow2_smem() {
-    return 128 + (size_t)flow2_nst<SP>() * flow2_stage<SP>() + (size_t)3 * (SP / 8) * T * 8;   // barriers, ring, Eq. 8 partials
+    return 128 + (size_t)NST * flow2_stage<SP>() + (size_t)3 * (SP / 8) * T * 8;   // barriers, ring, Eq. 8 partials
 }
 
-template <int SP>
-__global__ void __launch_bounds__(flow2_threads<SP>(), flow2_ctas<SP>())
+// A1 -> flow overlap (programmatic dependent launch): the flow kernel may
+// start while codon_pmat_kernel is still running; an item then also waits
+// until the transition matrices it reads are published (pready[branch][r]).
+__device__ __forceinline__ void wait_p(const FlowArgs &f, int node, int r, int R, int root, int *status) {
+    if (f.pready && node != root) wait_count2(f.pready + (size_t)node * R + r, 1, status);
+}
+
+template <int SP, int NST>
+__global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
     codon_flow2_kernel(const CodonArgs a, const FlowArgs f, const __grid_constant__ TmaMaps tm) {
     CODON_GEO;
-    constexpr int NST = flow2_nst<SP>();
     constexpr size_t STG = flow2_stage<SP>();
     constexpr int ROWS = TILE / 256;                       // tensor-map rows per tile
     constexpr unsigned TILE_B = (unsigned)TILE * 8u;
@@ -149,6 +159,12 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), flow2_ctas<SP>())
             const int4 e = a.lev4[task];
             const int k = e.x, ca = e.y, cb = e.z, kinds = e.w;
             const bool post = task < f.npost;
+            if (lane == 0 && f.pready) {             // the item's P, P', D' rows written by A1
+                wait_p(f, k, r, R, root, a.status);
+                wait_p(f, ca, r, R, root, a.status);
+                wait_p(f, cb, r, R, root, a.status);
+            }
+            __syncwarp();
             // B operands of the item's products into this SM's L1 while we wait
             {
                 auto pf = [&](const double *Bg) {
