@@ -213,7 +213,7 @@ struct pg_instance {
     int flow_tch = 0;                   // codon: tiles per flow item (0 = level-by-level kernels)
     int flow_ver = 2;                   // codon flow kernel: 2 = warp-specialised TMA ring (codon_flow2_kernel), 1 = round-1 kernel
     int flow_nst = 2;                   // codon_flow2_kernel ring stages (1: latency, 2: throughput)
-    int flow_pdl = 1;                   // A1 -> flow programmatic dependent launch (PG_FLOW_PDL=0 disables)
+    int flow_pdl = 0;                   // A1 -> flow programmatic dependent launch (PG_FLOW_PDL=1 enables)
     pg::codon::TmaMaps tmaps{};         // TMA tensor maps of u, q, utip (codon_flow2_kernel)
     int flow_defer = 0;                 // codon flow: Eq. 8 items after all pre items (PG_FLOW_DEFER)
     int flow_half = 0;                  // codon flow: half-tile post items when tch == 1 (PG_FLOW_HALF)
@@ -915,12 +915,12 @@ static int configure(pg_instance *inst) {
         } else if (inst->flow_ver == 2) {
             // warp-specialised TMA kernel: one tile per item (loads overlap compute)
             inst->flow_tch = 1;
-            // ring depth: two stages (claim-ahead) when every task has at
-            // least as many items as the two-stage grid has CTAs, else one
+            // ring depth 2 (claim-ahead) measured faster than 1 for every
+            // workload, shards included (scripts/gpu_codon3.sh); the A1 -> flow
+            // programmatic launch measured slower (yeast 1.175 -> 1.203 ms), off
             const char *ne = getenv("PG_FLOW_NST"), *pe = getenv("PG_FLOW_PDL");
-            inst->flow_nst = (ne && atoi(ne) >= 1 && atoi(ne) <= 2) ? atoi(ne)
-                             : (L.n_tiles * R >= cf.flow2_ctas[1] * inst->sm_count ? 2 : 1);
-            inst->flow_pdl = pe ? (atoi(pe) != 0) : 1;
+            inst->flow_nst = (ne && atoi(ne) >= 1 && atoi(ne) <= 2) ? atoi(ne) : 2;
+            inst->flow_pdl = pe ? (atoi(pe) != 0) : 0;
             for (int v = 0; v < 2; ++v)
                 CK(cudaFuncSetAttribute(cf.flow2[v], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.flow2_smem[v]),
                    "smem attr");

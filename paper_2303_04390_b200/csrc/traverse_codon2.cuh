@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
     auto tileA = [&](int s) { return reinterpret_cast<double *>(ring + s * STG); };
     auto meta = [&](int s) { return reinterpret_cast<Meta2 *>(ring + s * STG + 3 * (size_t)TILE * 8); };
     if (threadIdx.x == 0) {
-        for (int i = 0; i < NST; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
+        for (int i = 0; i < NST; ++i) { mbar_init(full + i, 2); mbar_init(empty + i, 1); }
         fence_mbar_init();
     }
     __syncthreads();
@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 if (lane == 0) {
                     m->item = -1;
                     mbar_arrive_u32(bar);
+                    mbar_arrive_u32(bar);
                 }
                 return;
             }
@@ -165,7 +166,10 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 wait_p(f, cb, r, R, root, a.status);
             }
             __syncwarp();
-            // B operands of the item's products into this SM's L1 while we wait
+            // ---- what does not depend on other items, before the wait:
+            // B operands into this SM's L1, tip states, state-tip tile gathers
+            // (rows of P' picked by state: u_tip[s] = P[s][state]; missing data:
+            // P 1) with cp.async, the item header, q = pi at the root
             {
                 auto pf = [&](const double *Bg) {
                     for (int i = lane; i < (int)MAT / 16; i += 32) prefetch_l1(Bg + 16 * i);
@@ -177,45 +181,15 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                     if (cb >= N) pf(a.PBpre + ((size_t)cb * R + r) * MAT);
                 }
             }
-            if (lane == 0) {
-                if (post || k == root) {
-                    if (ca >= N) wait_count2(f.rpost + (size_t)(ca - N) * ntiles + tile, R, a.status);
-                    if (cb >= N) wait_count2(f.rpost + (size_t)(cb - N) * ntiles + tile, R, a.status);
-                } else {
-                    wait_count2(f.rpre + (size_t)(k - N) * ntiles + tile, R, a.status);
-                }
-                fence_proxy_async_global();          // published generic stores -> our async-proxy reads
-                m->item = item;
-                m->task = task;
-                m->r = r;
-                m->tile = tile;
-                m->lev = e;
-            }
-            __syncwarp();
             const int pat = tile * T + lane;
             const int kc[2] = {kinds & 3, (kinds >> 2) & 3};
             const int cc[2] = {ca, cb};
-            // per-pattern metadata (lane = pattern of the tile)
-            m->fa[lane] = ca >= N ? __ldcg(a.fmax + (size_t)(ca - N) * a.Cpad + pat) : 0;
-            m->fb[lane] = cb >= N ? __ldcg(a.fmax + (size_t)(cb - N) * a.Cpad + pat) : 0;
-            if (!post) m->fq[lane] = k != root ? __ldcg(a.qmax + (size_t)(k - N) * a.Cpad + pat) : 0;
-            if (post && r == 0 && k != root) {
-                m->Ea[lane] = ca >= N ? __ldcg(a.E + (size_t)(ca - N) * a.Cpad + pat) : 0;
-                m->Eb[lane] = cb >= N ? __ldcg(a.E + (size_t)(cb - N) * a.Cpad + pat) : 0;
-            }
-            if (post && r == 0 && k == root) {
-                m->Ea[lane] = ca >= N ? __ldcg(a.E + (size_t)(ca - N) * a.Cpad + pat) : 0;
-                m->Eb[lane] = cb >= N ? __ldcg(a.E + (size_t)(cb - N) * a.Cpad + pat) : 0;
-            }
             int st2[2];
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 st2[c] = (cc[c] < N && kc[c] == 1) ? a.tip_states[(size_t)cc[c] * a.Cpad + pat] : 0;
                 (c ? m->sb : m->sa)[lane] = (uint8_t)st2[c];
             }
-            // state-tip tiles: rows of P' picked by state (u_tip[s] = P[s][state];
-            // missing data: P 1), gathered in fragment order with cp.async
-            bool gathered = false;
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 if (cc[c] >= N || kc[c] != 1) continue;
@@ -228,16 +202,27 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                     const int sv = __shfl_sync(0xffffffffu, st2[c], mm);
                     cp_async16(dst + 2 * i2, sv < a.S ? PT + (size_t)sv * SP + kk : ONE + kk);
                 }
-                gathered = true;
             }
-            // root of the pre-order: q = pi (generic stores into the Q tile)
             if (!post && k == root) {
                 double *Qs = tileA(s) + 2 * (size_t)TILE;
                 for (int idx = lane; idx < TILE; idx += 32) Qs[idx] = a.pi[((idx >> 5) & (KT - 1)) * 4 + (idx & 3)];
             }
-            if (gathered) cp_async_mbar_arrive(bar);
-            __syncwarp();
             if (lane == 0) {
+                m->item = item;
+                m->task = task;
+                m->r = r;
+                m->tile = tile;
+                m->lev = e;
+            }
+            // ---- inputs published by other items
+            if (lane == 0) {
+                if (post || k == root) {
+                    if (ca >= N) wait_count2(f.rpost + (size_t)(ca - N) * ntiles + tile, R, a.status);
+                    if (cb >= N) wait_count2(f.rpost + (size_t)(cb - N) * ntiles + tile, R, a.status);
+                } else {
+                    wait_count2(f.rpre + (size_t)(k - N) * ntiles + tile, R, a.status);
+                }
+                fence_proxy_async_global();          // published generic stores -> our async-proxy reads
                 unsigned bytes = 0;
                 for (int c = 0; c < 2; ++c)
                     if (cc[c] >= N || kc[c] == 2) bytes += TILE_B;
@@ -254,6 +239,28 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 if (!post && k != root)
                     tma_load_tile(st_u + 2 * TILE_B, &tm.q, (int)((((size_t)(k - N) * R + r) * ntiles + tile) * ROWS), bar);
             }
+            __syncwarp();
+            // per-pattern rescaling exponents of the inputs (lane = pattern),
+            // 4-byte cp.async into the stage's metadata
+            if (ca >= N) cp_async4(&m->fa[lane], a.fmax + (size_t)(ca - N) * a.Cpad + pat);
+            else m->fa[lane] = 0;
+            if (cb >= N) cp_async4(&m->fb[lane], a.fmax + (size_t)(cb - N) * a.Cpad + pat);
+            else m->fb[lane] = 0;
+            if (!post) {
+                if (k != root) cp_async4(&m->fq[lane], a.qmax + (size_t)(k - N) * a.Cpad + pat);
+                else m->fq[lane] = 0;
+            }
+            if (post && r == 0) {
+                if (ca >= N) cp_async4(&m->Ea[lane], a.E + (size_t)(ca - N) * a.Cpad + pat);
+                else m->Ea[lane] = 0;
+                if (cb >= N) cp_async4(&m->Eb[lane], a.E + (size_t)(cb - N) * a.Cpad + pat);
+                else m->Eb[lane] = 0;
+            }
+            // the stage is complete when the TMA bytes, every lane's cp.async
+            // copies and lane 0's arrive below have all landed
+            cp_async_mbar_arrive(bar);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_u32(bar);
         }
     }
 
