@@ -213,7 +213,7 @@ struct pg_instance {
     int flow_tch = 0;                   // codon: tiles per flow item (0 = level-by-level kernels)
     int flow_ver = 2;                   // codon flow kernel: 2 = warp-specialised TMA ring (codon_flow2_kernel), 1 = round-1 kernel
     int flow_nst = 2;                   // codon_flow2_kernel ring stages (1: latency, 2: throughput)
-    int flow_pdl = 0;                   // A1 -> flow programmatic dependent launch (PG_FLOW_PDL=1 enables)
+    int flow_pdl = 0;                   // A1 -> flow programmatic dependent launch (PG_FLOW_PDL=0/1 overrides)
     pg::codon::TmaMaps tmaps{};         // TMA tensor maps of u, q, utip (codon_flow2_kernel)
     int flow_defer = 0;                 // codon flow: Eq. 8 items after all pre items (PG_FLOW_DEFER)
     int flow_half = 0;                  // codon flow: half-tile post items when tch == 1 (PG_FLOW_HALF)
@@ -916,11 +916,12 @@ static int configure(pg_instance *inst) {
             // warp-specialised TMA kernel: one tile per item (loads overlap compute)
             inst->flow_tch = 1;
             // ring depth 2 (claim-ahead) measured faster than 1 for every
-            // workload, shards included (scripts/gpu_codon3.sh); the A1 -> flow
-            // programmatic launch measured slower (yeast 1.175 -> 1.203 ms), off
+            // workload, shards included (scripts/gpu_codon3.sh)
             const char *ne = getenv("PG_FLOW_NST"), *pe = getenv("PG_FLOW_PDL");
             inst->flow_nst = (ne && atoi(ne) >= 1 && atoi(ne) <= 2) ? atoi(ne) : 2;
-            inst->flow_pdl = pe ? (atoi(pe) != 0) : 0;
+            // PDL: on when a task's items do not fill the grid (latency-bound
+            // shards: yeast x8 0.251 -> 0.239 ms); off at full size (1.175 -> 1.203)
+            inst->flow_pdl = pe ? (atoi(pe) != 0) : (L.n_tiles * R < cf.flow2_ctas[inst->flow_nst - 1] * inst->sm_count);
             for (int v = 0; v < 2; ++v)
                 CK(cudaFuncSetAttribute(cf.flow2[v], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.flow2_smem[v]),
                    "smem attr");
@@ -1106,9 +1107,10 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         // per-evaluation counters (rescaling maxima, flow counters, A1 flags)
         CK(cudaMemsetAsync(inst->ws + L.off_fmax, 0, L.reset_bytes, inst->stream), "fmax/flow reset");
         int *pready = inst->at<int>(L.off_flow) + 32 + (size_t)2 * (inst->cfg.tips - 1) * L.n_tiles;
-        void *args[] = {&VA, &ViB, &M0, &Qd, &lam, &rates, &bl, &S, (void *)&R, &PBpost, &PBpre, &PT, &DT, &PONE, &pready};
+        int Nt = inst->cfg.tips, tipp = (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? 1 : 0;
+        void *args[] = {&VA, &ViB, &M0, &Qd, &lam, &rates, &bl, &S, (void *)&R, &Nt, &tipp, &PBpost, &PBpre, &PT, &DT, &PONE, &pready};
         const CodonFns cf = codon_fns(L.SP);
-        CK(cudaLaunchKernel(cf.pmat, dim3(L.B * R), dim3(256), args, cf.pmat_smem, inst->stream), "codon pmat launch");
+        CK(cudaLaunchKernel(cf.pmat, dim3(L.B * R, 2), dim3(256), args, cf.pmat_smem, inst->stream), "codon pmat launch");
         if (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) {     // u = P p of partial tips (A2's tip step)
             pg::codon::CodonArgs c = codon_args(inst);
             void *targs[] = {&c};

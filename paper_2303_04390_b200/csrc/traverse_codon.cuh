@@ -874,44 +874,47 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
                                                          const double *__restrict__ Qd,
                                                          const double *__restrict__ lam,
                                                          const double *__restrict__ rates,
-                                                         const double *__restrict__ bl, int S, int R,
-                                                         double *PBpost, double *PBpre, double *PT, double *DT,
-                                                         double *PONE, int *pready) {
+                                                         const double *__restrict__ bl, int S, int R, int N,
+                                                         int tip_partials, double *PBpost, double *PBpre, double *PT,
+                                                         double *DT, double *PONE, int *pready) {
     CODON_GEO;
     // programmatic dependent launch: the flow kernel may start now; it reads
     // this CTA's outputs only after pready[branch][r] is published below
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     extern __shared__ __align__(16) unsigned char smem_p[];
-    double *Ps = reinterpret_cast<double *>(smem_p);     // [SP][SP+1]: P, then D
-    double *e = Ps + SP * (SP + 1), *de = e + SP;        // [SP] each
+    double *Ps = reinterpret_cast<double *>(smem_p);     // [SP][SP+1]: P or D
+    double *e = Ps + SP * (SP + 1);                      // [SP]
     // SP = 64: V's A fragments staged in shared memory once (all copies in
     // flight together; ncu: L2 loads inside the DMMA loop were the top stall);
     // SP = 128 reads them from L2 (no room next to the 132 KB output buffer)
     constexpr bool STAGE_V = SP == 64;
-    double *Vs = de + SP;
+    double *Vs = e + 2 * SP;
     const int br = blockIdx.x, r = br % R, b = br / R;
+    // blockIdx.y = 0: P (every branch), 1: D (tips only).  What each branch's
+    // consumers read: internal branches the B fragments of P' (post, u_k =
+    // p P') and P (pre, q_c = x_c P); tips the rows of P' (gathers), P 1
+    // (missing data) and D' (Eq. 8 numerators); partial tips also P'-fragments
+    // (codon_tipu_kernel).  Nothing else is formed or written.
+    const int pass = blockIdx.y;
+    const bool tip = b < N;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    if constexpr (STAGE_V) {
-        for (int i = threadIdx.x; i < (int)MAT / 2; i += blockDim.x) cp_async16(Vs + 2 * i, VA + 2 * i);
-        cp_async_commit();
-    }
-    const double g = rates[r], t = g * bl[b];
-    // P = M0 + V diag(e - 1) V^-1, D = gamma (Q + V diag(lambda (e - 1)) V^-1)
-    // (M0 = V V^-1, Q formed once on the host; R15b)
-    for (int k = threadIdx.x; k < SP; k += blockDim.x) {
-        const double em1 = k < S ? expm1(lam[k] * t) : 0.0;
-        e[k] = em1;
-        de[k] = k < S ? g * lam[k] * em1 : 0.0;
-    }
-    if constexpr (STAGE_V) cp_async_wait<0>();
-    __syncthreads();
-    const size_t base = (size_t)br * MAT;
-    const double *Vsrc = STAGE_V ? Vs : VA;
-    // pass 0: P = V diag(e) V^-1; pass 1: D = V diag(gamma lambda e) V^-1.
-    // Warp w computes column strips 8 cs .. 8 cs + 7, cs = w, w + nw, ...
-#pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {
-        const double *ev = pass ? de : e;
+    if (pass == 0 || tip) {
+        if constexpr (STAGE_V) {
+            for (int i = threadIdx.x; i < (int)MAT / 2; i += blockDim.x) cp_async16(Vs + 2 * i, VA + 2 * i);
+            cp_async_commit();
+        }
+        const double g = rates[r], t = g * bl[b];
+        // P = M0 + V diag(e - 1) V^-1, D = gamma (Q + V diag(lambda (e - 1)) V^-1)
+        // (M0 = V V^-1, Q formed once on the host; R15b)
+        for (int k = threadIdx.x; k < SP; k += blockDim.x) {
+            const double em1 = k < S ? expm1(lam[k] * t) : 0.0;
+            e[k] = pass ? (k < S ? g * lam[k] * em1 : 0.0) : em1;
+        }
+        if constexpr (STAGE_V) cp_async_wait<0>();
+        __syncthreads();
+        const size_t base = (size_t)br * MAT;
+        const double *Vsrc = STAGE_V ? Vs : VA;
+        // Warp w computes column strips 8 cs .. 8 cs + 7, cs = w, w + nw, ...
 #pragma unroll 1
         for (int cs = w; cs < NW; cs += nw) {
             double bfr[KT];
@@ -924,7 +927,7 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
                 const double *A = Vsrc + h * TILE + lane;
 #pragma unroll
                 for (int kt = 0; kt < KT; ++kt) {
-                    const double ek = ev[kt * 4 + (lane & 3)];
+                    const double ek = e[kt * 4 + (lane & 3)];
 #pragma unroll
                     for (int mt = 0; mt < 4; ++mt) {
                         const double v = STAGE_V ? A[(mt * KT + kt) * 32] : __ldg(A + (mt * KT + kt) * 32);
@@ -942,19 +945,20 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
             }
         }
         __syncthreads();
+        const bool frag_post = !tip || tip_partials, frag_pre = !tip;
         for (int idx = threadIdx.x; idx < (int)MAT; idx += blockDim.x) {
             const int row = idx / SP, col = idx % SP;
             if (pass == 0) {
                 const int ln = idx & 31, kt = (idx >> 5) & (KT - 1), nt = idx / (32 * KT);
                 const int kk = kt * 4 + (ln & 3), nn = nt * 8 + (ln >> 2);
-                PBpost[base + idx] = Ps[nn * (SP + 1) + kk];    // B[k=t][n=s] = P[s][t]
-                PBpre[base + idx] = Ps[kk * (SP + 1) + nn];     // B[k=s][n=t] = P[s][t]
-                PT[base + idx] = Ps[col * (SP + 1) + row];      // P'[t][s] = P[s][t]
+                if (frag_post) PBpost[base + idx] = Ps[nn * (SP + 1) + kk];    // B[k=t][n=s] = P[s][t]
+                if (frag_pre) PBpre[base + idx] = Ps[kk * (SP + 1) + nn];      // B[k=s][n=t] = P[s][t]
+                if (tip) PT[base + idx] = Ps[col * (SP + 1) + row];            // P'[t][s] = P[s][t]
             } else {
-                DT[base + idx] = Ps[col * (SP + 1) + row];      // D'
+                DT[base + idx] = Ps[col * (SP + 1) + row];                     // D'
             }
         }
-        if (pass == 0)
+        if (pass == 0 && tip)
             for (int s2 = threadIdx.x; s2 < SP; s2 += blockDim.x) {
                 double acc = 0.0;
                 for (int u = 0; u < SP; ++u) acc += Ps[s2 * (SP + 1) + u];
@@ -962,13 +966,14 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
             }
         __syncthreads();
     }
-    if (pready && threadIdx.x == 0) {                    // publish (release) for the flow kernel
+    if (pready && threadIdx.x == 0) {                    // publish (release): 2 CTAs per (branch, r)
         __threadfence();
         atomicAdd(pready + br, 1);
     }
 }
 template <int SP>
 constexpr size_t pmat_smem() { return ((size_t)SP * (SP + 1) + 2 * SP + (SP == 64 ? (size_t)SP * SP : 0)) * 8; }
+constexpr int PMAT_FLAGS = 2;                            // pready count per (branch, r): the P and D CTAs
 
 }  // namespace codon
 }  // namespace pg
