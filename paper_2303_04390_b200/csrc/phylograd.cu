@@ -1149,6 +1149,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
             const int npre = f.ntask - f.npost;
             const int items = f.npost * R * f.nch * f.phalf + (npre + (f.defer ? npre : 0)) * R * f.nch;
             f.trace = inst->flow_trace_n == (size_t)items ? inst->flow_trace : nullptr;
+            if (inst->flow_ver == 2) f.trace = inst->flow_trace_n == (size_t)f.ntask * R * L.n_tiles ? inst->flow_trace : nullptr;
             if (inst->flow_ver == 2) {
                 const int items2 = f.ntask * R * L.n_tiles;
                 const int v = inst->flow_nst - 1;

@@ -154,6 +154,14 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 }
                 return;
             }
+            unsigned long long *tr = f.trace ? f.trace + TRW * (size_t)item : nullptr;   // PG_FLOW_TRACE
+            if (tr && lane == 0) {
+                unsigned smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                tr[0] = smid;
+                tr[1] = gtimer();
+                tr[7] = blockIdx.x;
+            }
             const int task = item / (R * ntiles);
             const int rem = item - task * R * ntiles;
             const int r = rem / ntiles, tile = rem - r * ntiles;
@@ -222,6 +230,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 } else {
                     wait_count2(f.rpre + (size_t)(k - N) * ntiles + tile, R, a.status);
                 }
+                if (tr) tr[2] = gtimer();
                 fence_proxy_async_global();          // published generic stores -> our async-proxy reads
                 unsigned bytes = 0;
                 for (int c = 0; c < 2; ++c)
@@ -275,6 +284,8 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
         const int r = m->r, tile = m->tile;
         const int k = m->lev.x, ca = m->lev.y, cb = m->lev.z, kinds = m->lev.w;
         const int pat0 = tile * T;
+        unsigned long long *tr = (f.trace && threadIdx.x == 0) ? f.trace + TRW * (size_t)item : nullptr;
+        if (tr) tr[3] = gtimer();
         double *As = tileA(s), *Bs = As + TILE, *Qs = As + 2 * (size_t)TILE;
         const bool post = m->task < f.npost;
         if (post) {
@@ -315,6 +326,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 consumer_sync(NT);
                 double acc[4][2];
                 gemm_tile<SP>(acc, As, bfr, lane);
+                if (tr) tr[4] = gtimer();
                 if (r == 0 && threadIdx.x < T) storeE();
                 double *out = a.u + (((size_t)(k - N) * R + r) * ntiles + tile) * TILE;
                 int *fm = a.fmax + (size_t)(k - N) * a.Cpad + pat0;
@@ -336,6 +348,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 __threadfence();
                 atomicAdd(f.rpost + (size_t)(k - N) * ntiles + tile, 1);
                 mbar_arrive_u32(empty_u + 8u * s);
+                if (tr) tr[5] = tr[6] = gtimer();
             }
             continue;
         }
@@ -378,6 +391,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 if ((lane & 3) == 0) atomicMax(qm + mm, fx);
             }
         }
+        if (tr) tr[4] = gtimer();
         if (ca >= N || cb >= N) {                    // publish q of the internal children
             fence_proxy_async_global();
             consumer_sync(NT);
@@ -387,6 +401,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 if (cb >= N) atomicAdd(f.rpre + (size_t)(cb - N) * ntiles + tile, 1);
             }
         }
+        if (tr) tr[5] = gtimer();
         // phase B: Eq. 8 terms; den = x_c'u_c is the same for both children
         // (q_k o u_a o u_b, Eq. 5).  Tiles are unscaled: the factors cancel in
         // the ratio, which is formed over categories afterwards.
@@ -453,6 +468,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
         }
         consumer_sync(NT);                           // partials read before the next item writes them
         if (threadIdx.x == 0) mbar_arrive_u32(empty_u + 8u * s);
+        if (tr) tr[6] = gtimer();
     }
 }
 
