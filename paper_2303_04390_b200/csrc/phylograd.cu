@@ -214,6 +214,7 @@ struct pg_instance {
     int flow_ver = 2;                   // codon flow kernel: 2 = warp-specialised TMA ring (codon_flow2_kernel), 1 = round-1 kernel
     int flow_nst = 2;                   // codon_flow2_kernel ring stages (1: latency, 2: throughput)
     int flow_pdl = 0;                   // A1 -> flow programmatic dependent launch (PG_FLOW_PDL=0/1 overrides)
+    int flow_split = 0;                 // codon_flow2_kernel: one pre item per child (PG_FLOW_SPLIT=0/1 overrides)
     pg::codon::TmaMaps tmaps{};         // TMA tensor maps of u, q, utip (codon_flow2_kernel)
     int flow_defer = 0;                 // codon flow: Eq. 8 items after all pre items (PG_FLOW_DEFER)
     int flow_half = 0;                  // codon flow: half-tile post items when tch == 1 (PG_FLOW_HALF)
@@ -921,7 +922,10 @@ static int configure(pg_instance *inst) {
             inst->flow_nst = (ne && atoi(ne) >= 1 && atoi(ne) <= 2) ? atoi(ne) : 2;
             // PDL: on when a task's items do not fill the grid (latency-bound
             // shards: yeast x8 0.251 -> 0.239 ms); off at full size (1.175 -> 1.203)
-            inst->flow_pdl = pe ? (atoi(pe) != 0) : (L.n_tiles * R < cf.flow2_ctas[inst->flow_nst - 1] * inst->sm_count);
+            const bool latency = L.n_tiles * R < cf.flow2_ctas[inst->flow_nst - 1] * inst->sm_count;
+            inst->flow_pdl = pe ? (atoi(pe) != 0) : latency;
+            const char *se = getenv("PG_FLOW_SPLIT");
+            inst->flow_split = se ? (atoi(se) != 0) : latency;
             for (int v = 0; v < 2; ++v)
                 CK(cudaFuncSetAttribute(cf.flow2[v], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.flow2_smem[v]),
                    "smem attr");
@@ -955,7 +959,7 @@ static int configure(pg_instance *inst) {
         const char *he = getenv("PG_FLOW_HALF");
         inst->flow_half = he ? (atoi(he) != 0) : 0;
         if (getenv("PG_FLOW_TRACE") && inst->flow_tch > 0) {    // diagnostics buffer (allocated before capture)
-            const size_t items = inst->plan.level_nodes.size() * (size_t)R *
+            const size_t items = 2 * inst->plan.level_nodes.size() * (size_t)R *     // x2: split pre items
                                  ((L.n_tiles + inst->flow_tch - 1) / inst->flow_tch);
             if (inst->flow_trace) cudaFree(inst->flow_trace);
             CK(cudaMalloc(&inst->flow_trace, sizeof(unsigned long long) * pg::codon::TRW * items), "trace alloc");
@@ -1148,10 +1152,13 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
             f.phalf = (inst->flow_half && f.tch == 1) ? 2 : 1;
             const int npre = f.ntask - f.npost;
             const int items = f.npost * R * f.nch * f.phalf + (npre + (f.defer ? npre : 0)) * R * f.nch;
-            f.trace = inst->flow_trace_n == (size_t)items ? inst->flow_trace : nullptr;
-            if (inst->flow_ver == 2) f.trace = inst->flow_trace_n == (size_t)f.ntask * R * L.n_tiles ? inst->flow_trace : nullptr;
+            f.trace = inst->flow_trace_n >= (size_t)items ? inst->flow_trace : nullptr;
+            if (inst->flow_ver == 2)
+                f.trace = inst->flow_trace_n >= (size_t)(f.npost + 2 * (f.ntask - f.npost)) * R * L.n_tiles ? inst->flow_trace
+                                                                                                          : nullptr;
             if (inst->flow_ver == 2) {
-                const int items2 = f.ntask * R * L.n_tiles;
+                f.split = inst->flow_split;
+                const int items2 = (f.npost + (f.ntask - f.npost) * (f.split ? 2 : 1)) * R * L.n_tiles;
                 const int v = inst->flow_nst - 1;
                 // programmatic dependent launch right behind A1 (no partial-tip
                 // kernels or timing events in between): items wait on pready

@@ -410,6 +410,7 @@ struct FlowArgs {
     int phalf;         // 2: post items are half tiles (16 patterns; needs tch == 1): shorter chain links
     unsigned long long *trace;   // diagnostics (PG_FLOW_TRACE): [item][TRW] = {smid, t_take, t_ready, t_done, phase stamps}
     const int *pready;           // codon_flow2_kernel under PDL: [B][R] A1 done flags (null: A1 finished before launch)
+    int split;                   // codon_flow2_kernel: one pre item per child (latency-bound shards)
 };
 
 // ---------------------------------------------------------------------------

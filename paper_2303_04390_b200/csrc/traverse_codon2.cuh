@@ -85,6 +85,7 @@ __device__ __forceinline__ void wait_count2(const int *p, int v, int *status) {
 struct alignas(16) Meta2 {
     int item, task, r, tile;
     int4 lev;                 // {k, child a, child b, kinds}
+    int cs, pad0, pad1, pad2; // pre items: -1 both children, else the one child of a split item
     int fa[T], fb[T];         // children's fmax (IEEE exponent fields), internal children
     int fq[T];                // qmax of the parent (pre, non-root)
     int Ea[T], Eb[T];         // children's cumulative exponents (post, r == 0)
@@ -127,7 +128,11 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int R = a.R, ntiles = a.ntiles, N = a.N;
     const int root = 2 * N - 2;
-    const int nitems = f.ntask * R * ntiles;
+    // items: post (task, r, tile); pre (task, r, tile) for both children, or
+    // with f.split (task, child, r, tile): one child each -- the two q GEMMs
+    // of a parent then run on different CTAs (shorter pre-order chain links)
+    const int npost_items = f.npost * R * ntiles;
+    const int nitems = npost_items + (f.ntask - f.npost) * R * ntiles * (f.split ? 2 : 1);
     auto tileA = [&](int s) { return reinterpret_cast<double *>(ring + s * STG); };
     auto meta = [&](int s) { return reinterpret_cast<Meta2 *>(ring + s * STG + 3 * (size_t)TILE * 8); };
     if (threadIdx.x == 0) {
@@ -162,8 +167,17 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 tr[1] = gtimer();
                 tr[7] = blockIdx.x;
             }
-            const int task = item / (R * ntiles);
-            const int rem = item - task * R * ntiles;
+            int task, cs = -1, rem;
+            if (item < npost_items || !f.split) {
+                task = item / (R * ntiles);
+                rem = item - task * R * ntiles;
+            } else {
+                const int i2 = item - npost_items, per = 2 * R * ntiles;
+                task = f.npost + i2 / per;
+                const int rr = i2 - (task - f.npost) * per;
+                cs = rr / (R * ntiles);
+                rem = rr - cs * R * ntiles;
+            }
             const int r = rem / ntiles, tile = rem - r * ntiles;
             const int4 e = a.lev4[task];
             const int k = e.x, ca = e.y, cb = e.z, kinds = e.w;
@@ -185,8 +199,8 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 if (post) {
                     if (k != root) pf(a.PBpost + ((size_t)k * R + r) * MAT);
                 } else {
-                    if (ca >= N) pf(a.PBpre + ((size_t)ca * R + r) * MAT);
-                    if (cb >= N) pf(a.PBpre + ((size_t)cb * R + r) * MAT);
+                    if (ca >= N && cs != 1) pf(a.PBpre + ((size_t)ca * R + r) * MAT);
+                    if (cb >= N && cs != 0) pf(a.PBpre + ((size_t)cb * R + r) * MAT);
                 }
             }
             const int pat = tile * T + lane;
@@ -221,6 +235,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 m->r = r;
                 m->tile = tile;
                 m->lev = e;
+                m->cs = cs;
             }
             // ---- inputs published by other items
             if (lane == 0) {
@@ -354,6 +369,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
         }
         // ------------------------------- pre item ------------------------------
         const int ch[2] = {ca, cb};
+        const int cs = m->cs, c0 = cs < 0 ? 0 : cs, c1 = cs < 0 ? 1 : cs;   // children of this item
         auto scQ = [&](int mm) { return k == root ? 1.0 : pow2neg(lazy_exp(m->fq[mm])); };
         auto scC = [&](int c, int mm) {
             return ch[c] >= N ? pow2neg(lazy_exp(c ? m->fb[mm] : m->fa[mm])) : 1.0;
@@ -364,7 +380,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             const int node = ch[c];
-            if (node < N) continue;
+            if (node < N || c < c0 || c > c1) continue;
             double bq[KT], acc[4][2];
             load_bfrag<SP>(bq, a.PBpre + ((size_t)node * R + r) * MAT, w, lane);
             const double *Ub = Us[1 - c];
@@ -392,21 +408,23 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
             }
         }
         if (tr) tr[4] = gtimer();
-        if (ca >= N || cb >= N) {                    // publish q of the internal children
+        const bool pa = ca >= N && c0 == 0, pb = cb >= N && c1 == 1;
+        if (pa || pb) {                              // publish q of the internal children
             fence_proxy_async_global();
             consumer_sync(NT);
             if (threadIdx.x == 0) {
                 __threadfence();
-                if (ca >= N) atomicAdd(f.rpre + (size_t)(ca - N) * ntiles + tile, 1);
-                if (cb >= N) atomicAdd(f.rpre + (size_t)(cb - N) * ntiles + tile, 1);
+                if (pa) atomicAdd(f.rpre + (size_t)(ca - N) * ntiles + tile, 1);
+                if (pb) atomicAdd(f.rpre + (size_t)(cb - N) * ntiles + tile, 1);
             }
         }
         if (tr) tr[5] = gtimer();
         // phase B: Eq. 8 terms; den = x_c'u_c is the same for both children
-        // (q_k o u_a o u_b, Eq. 5).  Tiles are unscaled: the factors cancel in
-        // the ratio, which is formed over categories afterwards.
+        // (q_k o u_a o u_b, Eq. 5; formed once per item).  Tiles are unscaled:
+        // the factors cancel in the ratio, formed over categories afterwards.
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
+            if (c < c0 || c > c1) continue;
             const int node = ch[c];
             const size_t br = (size_t)node * R + r;
             const int kind = (kinds >> (2 * c)) & 3;
@@ -441,8 +459,8 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 sn += __shfl_xor_sync(0xffffffffu, sn, 1);
                 sn += __shfl_xor_sync(0xffffffffu, sn, 2);
                 if ((lane & 3) == 0) part[(c * NW + w) * T + mm] = sn;
-                if (c == 0) {
-                    const double2 u2 = *reinterpret_cast<const double2 *>(Us[0] + p);
+                if (c == c0) {
+                    const double2 u2 = *reinterpret_cast<const double2 *>(Us[c] + p);
                     double sd = x0 * u2.x + x1 * u2.y;
                     sd += __shfl_xor_sync(0xffffffffu, sd, 1);
                     sd += __shfl_xor_sync(0xffffffffu, sd, 2);
@@ -455,16 +473,16 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
             const int mm = threadIdx.x;
             double sd = 0.0, sn0 = 0.0, sn1 = 0.0;
             for (int ww = 0; ww < NW; ++ww) {
-                sn0 += part[ww * T + mm];
-                sn1 += part[(NW + ww) * T + mm];
+                if (c0 == 0) sn0 += part[ww * T + mm];
+                if (c1 == 1) sn1 += part[(NW + ww) * T + mm];
                 sd += part[(2 * NW + ww) * T + mm];
             }
             const double wr = a.cat_w[r], gr = a.cat_g[r];
             double2 *nd = reinterpret_cast<double2 *>(a.numden);
             const bool qa = ca >= N || (kinds & 3) == 2, qb = cb >= N || ((kinds >> 2) & 3) == 2;
             const double s0 = qa ? gr * wr : wr, s1 = qb ? gr * wr : wr;
-            nd[((size_t)ca * R + r) * a.Cpad + pat0 + mm] = make_double2(s0 * sn0, wr * sd);
-            nd[((size_t)cb * R + r) * a.Cpad + pat0 + mm] = make_double2(s1 * sn1, wr * sd);
+            if (c0 == 0) nd[((size_t)ca * R + r) * a.Cpad + pat0 + mm] = make_double2(s0 * sn0, wr * sd);
+            if (c1 == 1) nd[((size_t)cb * R + r) * a.Cpad + pat0 + mm] = make_double2(s1 * sn1, wr * sd);
         }
         consumer_sync(NT);                           // partials read before the next item writes them
         if (threadIdx.x == 0) mbar_arrive_u32(empty_u + 8u * s);

@@ -26,8 +26,14 @@ info = inst.plan_info()
 t = np.fromfile(path, dtype=np.uint64).reshape(-1, 8).astype(np.int64)
 R = len(pb.cat_rates)
 ntiles = (hi - lo + 31) // 32
-per_task = R * ntiles
-ntask = len(t) // per_task
+split = os.environ.get("PG_FLOW_SPLIT", "1" if ntiles * R < 296 else "0") != "0"
+npost = pb.n_tips - 1
+n_items = npost * R * ntiles * (3 if split else 2)
+t = t[:n_items]
+# per task rows: post tasks R*ntiles items, pre tasks (2 if split) R*ntiles
+bounds = [k * R * ntiles for k in range(npost + 1)]
+bounds += [bounds[-1] + (k + 1) * R * ntiles * (2 if split else 1) for k in range(npost)]
+ntask = len(bounds) - 1
 t0 = t[:, 1].min()
 claim, ready, full, gemm, pub, end = [(t[:, i] - t0) / 1e3 for i in range(1, 7)]
 print(f"config {cfg} shards {shards}: items {len(t)} tasks {ntask} span {end.max():.1f} us  CTAs {len(np.unique(t[:, 7]))}"
@@ -37,7 +43,7 @@ print(f"mean us: claim->ready {np.mean(ready - claim):.2f}  ready->full {np.mean
       f"full->end {np.mean(end - full):.2f}")
 npost = info.get("npost", None)
 for k in range(ntask):
-    s = slice(k * per_task, (k + 1) * per_task)
+    s = slice(bounds[k], bounds[k + 1])
     print(f"task {k:3d}  claim {claim[s].min():7.1f}  ready {ready[s].min():7.1f}..{ready[s].max():7.1f}  "
           f"full {full[s].min():7.1f}..{full[s].max():7.1f}  pub {pub[s].max():7.1f}  end {end[s].max():7.1f}  "
           f"item {np.mean(end[s] - full[s]):5.2f} (gemm {np.mean(gemm[s] - full[s]):5.2f})")
