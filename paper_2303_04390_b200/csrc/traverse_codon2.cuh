@@ -368,31 +368,19 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
             continue;
         }
         // ------------------------------- pre item ------------------------------
-        const int ch[2] = {ca, cb};
-        const int cs = m->cs, c0 = cs < 0 ? 0 : cs, c1 = cs < 0 ? 1 : cs;   // children of this item
+        const int cs = m->cs;                        // -1: both children, else the one child of a split item
         auto scQ = [&](int mm) { return k == root ? 1.0 : pow2neg(lazy_exp(m->fq[mm])); };
         auto scC = [&](int c, int mm) {
-            return ch[c] >= N ? pow2neg(lazy_exp(c ? m->fb[mm] : m->fa[mm])) : 1.0;
+            return (c ? cb : ca) >= N ? pow2neg(lazy_exp(c ? m->fb[mm] : m->fa[mm])) : 1.0;
         };
-        double *Us[2] = {As, Bs};
-        // phase A (the pre-order chain): q_c = x_c P_c, x_c = q_k o u_sib formed
-        // in the A-fragment loads; rows scaled by the q_k and sibling exponents
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int node = ch[c];
-            if (node < N || c < c0 || c > c1) continue;
+        auto Uc = [&](int c) { return c ? Bs : As; };
+        // q_c = x_c P_c (Eq. 4) from the x_c tile Xs; rows scaled by the q_k
+        // and sibling exponents
+        auto q_gemm = [&](int c, const double *Xs) {
+            const int node = c ? cb : ca;
             double bq[KT], acc[4][2];
             load_bfrag<SP>(bq, a.PBpre + ((size_t)node * R + r) * MAT, w, lane);
-            const double *Ub = Us[1 - c];
-#pragma unroll
-            for (int mt = 0; mt < 4; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
-#pragma unroll
-            for (int kt = 0; kt < KT; ++kt)
-#pragma unroll
-                for (int mt = 0; mt < 4; ++mt) {
-                    const int p = (mt * KT + kt) * 32 + lane;
-                    dmma(acc[mt], Qs[p] * Ub[p], bq[kt]);
-                }
+            gemm_tile<SP>(acc, Xs, bq, lane);
             double *out = a.q + (((size_t)(node - N) * R + r) * ntiles + tile) * TILE;
             int *qm = a.qmax + (size_t)(node - N) * a.Cpad + pat0;
 #pragma unroll
@@ -406,10 +394,9 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 2));
                 if ((lane & 3) == 0) atomicMax(qm + mm, fx);
             }
-        }
-        if (tr) tr[4] = gtimer();
-        const bool pa = ca >= N && c0 == 0, pb = cb >= N && c1 == 1;
-        if (pa || pb) {                              // publish q of the internal children
+        };
+        auto publish_q = [&](bool pa, bool pb) {
+            if (!pa && !pb) return;
             fence_proxy_async_global();
             consumer_sync(NT);
             if (threadIdx.x == 0) {
@@ -417,22 +404,21 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 if (pa) atomicAdd(f.rpre + (size_t)(ca - N) * ntiles + tile, 1);
                 if (pb) atomicAdd(f.rpre + (size_t)(cb - N) * ntiles + tile, 1);
             }
-        }
-        if (tr) tr[5] = gtimer();
-        // phase B: Eq. 8 terms; den = x_c'u_c is the same for both children
-        // (q_k o u_a o u_b, Eq. 5; formed once per item).  Tiles are unscaled:
-        // the factors cancel in the ratio, formed over categories afterwards.
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            if (c < c0 || c > c1) continue;
-            const int node = ch[c];
+        };
+        // Eq. 8 terms of child c: num_c = x_c'(Q u_c) (internal child or partial
+        // tip: Q u on the tensor path; state tip: the D' row, which carries
+        // gamma_r), with x_c at the output positions from xat(p); den = x_c'u_c
+        // (the same for both children, q_k o u_a o u_b, Eq. 5).  Tiles are
+        // unscaled: the factors cancel in the ratio over categories.
+        auto eq8 = [&](int c, bool den, auto xat) {
+            const int node = c ? cb : ca;
             const size_t br = (size_t)node * R + r;
             const int kind = (kinds >> (2 * c)) & 3;
             double acc[4][2];
             if (node >= N || kind == 2) {
                 double b[KT];
                 load_bfrag<SP>(b, a.QB, w, lane);
-                gemm_tile<SP>(acc, Us[c], b, lane);
+                gemm_tile<SP>(acc, Uc(c), b, lane);
             } else {
                 const uint8_t *stc = c ? m->sb : m->sa;
 #pragma unroll
@@ -452,22 +438,70 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
             for (int mt = 0; mt < 4; ++mt) {
                 const int mm = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
                 const int p = apos<SP>(mm, n);
-                const double2 q2 = *reinterpret_cast<const double2 *>(Qs + p);
-                const double2 o2 = *reinterpret_cast<const double2 *>(Us[1 - c] + p);
-                const double x0 = q2.x * o2.x, x1 = q2.y * o2.y;
-                double sn = x0 * acc[mt][0] + x1 * acc[mt][1];
+                const double2 x2 = xat(p);
+                double sn = x2.x * acc[mt][0] + x2.y * acc[mt][1];
                 sn += __shfl_xor_sync(0xffffffffu, sn, 1);
                 sn += __shfl_xor_sync(0xffffffffu, sn, 2);
                 if ((lane & 3) == 0) part[(c * NW + w) * T + mm] = sn;
-                if (c == c0) {
-                    const double2 u2 = *reinterpret_cast<const double2 *>(Us[c] + p);
-                    double sd = x0 * u2.x + x1 * u2.y;
+                if (den) {
+                    const double2 u2 = *reinterpret_cast<const double2 *>(Uc(c) + p);
+                    double sd = x2.x * u2.x + x2.y * u2.y;
                     sd += __shfl_xor_sync(0xffffffffu, sd, 1);
                     sd += __shfl_xor_sync(0xffffffffu, sd, 2);
                     if ((lane & 3) == 0) part[(2 * NW + w) * T + mm] = sd;
                 }
             }
+        };
+        if (cs >= 0) {
+            // split item (latency): x_c = q_k o u_sib formed in place over q_k
+            // (q_k is not needed again), q_c GEMM and publication first, then
+            // child c's Eq. 8 terms from x_c and u_c
+            const int c = cs;
+            const double *Usib = Uc(1 - c);
+            for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += NT) {
+                double2 *px = reinterpret_cast<double2 *>(Qs) + i2;
+                const double2 us = reinterpret_cast<const double2 *>(Usib)[i2];
+                double2 v = *px;
+                v.x *= us.x;
+                v.y *= us.y;
+                *px = v;
+            }
+            consumer_sync(NT);
+            if ((c ? cb : ca) >= N) q_gemm(c, Qs);
+            if (tr) tr[4] = gtimer();
+            publish_q(c == 0 && ca >= N, c == 1 && cb >= N);
+            if (tr) tr[5] = gtimer();
+            eq8(c, true, [&](int p) { return *reinterpret_cast<const double2 *>(Qs + p); });
+        } else {
+            // both children (throughput): Eq. 8 terms from q_k and the u tiles,
+            // then x_a = q o u_b over u_b and x_b = q o u_a over u_a in one pass
+            // (the u tiles are not needed again), then the two q GEMMs
+            auto xq = [&](int c) {
+                return [&, c](int p) {
+                    const double2 q2 = *reinterpret_cast<const double2 *>(Qs + p);
+                    const double2 o2 = *reinterpret_cast<const double2 *>(Uc(1 - c) + p);
+                    return make_double2(q2.x * o2.x, q2.y * o2.y);
+                };
+            };
+            eq8(0, true, xq(0));
+            eq8(1, false, xq(1));
+            consumer_sync(NT);
+            for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += NT) {
+                const double2 q2 = reinterpret_cast<const double2 *>(Qs)[i2];
+                double2 *pa = reinterpret_cast<double2 *>(As) + i2;
+                double2 *pb = reinterpret_cast<double2 *>(Bs) + i2;
+                const double2 ua = *pa, ub = *pb;
+                *pb = make_double2(q2.x * ub.x, q2.y * ub.y);           // x_a (child a's A operand)
+                *pa = make_double2(q2.x * ua.x, q2.y * ua.y);           // x_b
+            }
+            consumer_sync(NT);
+            if (ca >= N) q_gemm(0, Bs);
+            if (cb >= N) q_gemm(1, As);
+            if (tr) tr[4] = gtimer();
+            publish_q(ca >= N, cb >= N);
+            if (tr) tr[5] = gtimer();
         }
+        const int c0 = cs < 0 ? 0 : cs, c1 = cs < 0 ? 1 : cs;
         consumer_sync(NT);                           // stage and partials complete
         if (threadIdx.x < T) {                       // fixed-order sums over the warps
             const int mm = threadIdx.x;
