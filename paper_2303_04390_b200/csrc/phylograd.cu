@@ -924,6 +924,8 @@ static int configure(pg_instance *inst) {
             // shards: yeast x8 0.251 -> 0.239 ms); off at full size (1.175 -> 1.203)
             const bool latency = L.n_tiles * R < cf.flow2_ctas[inst->flow_nst - 1] * inst->sm_count;
             inst->flow_pdl = pe ? (atoi(pe) != 0) : latency;
+            // one pre item per child in the latency regime (S = 122 x8 shard
+            // 0.297 -> 0.206 ms, WNV x8 0.579 -> 0.462 ms; scripts/gpu_codon3.sh)
             const char *se = getenv("PG_FLOW_SPLIT");
             inst->flow_split = se ? (atoi(se) != 0) : latency;
             for (int v = 0; v < 2; ++v)

@@ -61,6 +61,18 @@ __device__ __forceinline__ void consumer_sync(int nthreads) {
     asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
 }
 __device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+// mbarrier phase wait with a suspend-time hint: the waiting warp sleeps until
+// the phase completes (or the hint expires) instead of re-issuing try_wait
+// (ncu: 21 % of the flow kernel's issued instructions were the try_wait loop)
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAITS_%=;\n}\n" ::"r"(bar),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
 
 // Poll a completion counter (acquire) until >= v.  A stall longer than
 // ~20 s (a schedule bug, or a neighbour that never lets a CTA run) is
@@ -145,7 +157,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
     if (warp == NW) {
         for (int g = 0;; ++g) {
             const int s = g % NST;
-            if (g >= NST) mbar_wait_u32(empty_u + 8u * s, (uint32_t)(g / NST + 1) & 1u);
+            if (g >= NST) mbar_wait_sleep(empty_u + 8u * s, (uint32_t)(g / NST + 1) & 1u);
             int item = 0;
             if (lane == 0) item = atomicAdd(f.ctr, 1);
             item = __shfl_sync(0xffffffffu, item, 0);
@@ -292,7 +304,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
     const int w = warp;
     for (int g = 0;; ++g) {
         const int s = g % NST;
-        mbar_wait_u32(full_u + 8u * s, (uint32_t)(g / NST) & 1u);
+        mbar_wait_sleep(full_u + 8u * s, (uint32_t)(g / NST) & 1u);
         const Meta2 *m = meta(s);
         const int item = m->item;
         if (item < 0) break;
