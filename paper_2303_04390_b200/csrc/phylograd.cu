@@ -152,7 +152,8 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         L->off_E = take((size_t)(N - 1) * L->Cpad * 4);
         // fmax [N-1], qmax [N-2], then the flow schedule's counters
         // {item counter, rpost [N-1][<= ntiles], rpre [N-1][<= ntiles]}: one memset
-        L->flow_bytes = ((size_t)32 + (size_t)2 * (N - 1) * L->n_tiles + (size_t)L->B * R) * 4;   // + A1 done flags
+        // {item counter, rpost, rpre, A1 done flags [B][R], ratio slice counters [B+1]}
+        L->flow_bytes = ((size_t)32 + (size_t)2 * (N - 1) * L->n_tiles + (size_t)L->B * R + (L->B + 1)) * 4;
         L->reset_bytes = (size_t)(2 * N - 3) * L->Cpad * 4 + L->flow_bytes;
         L->off_fmax = take(L->reset_bytes);
         L->off_qmax = L->off_fmax + (size_t)(N - 1) * L->Cpad * 4;
@@ -1212,8 +1213,11 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[2], inst->stream, cudaEventRecordExternal), "event");
     if (L.variant == 2) {
         pg::codon::CodonArgs c = codon_args(inst);
-        void *args[] = {&c, &d_out};
-        CK(cudaLaunchKernel((void *)pg::codon::codon_ratio_kernel, dim3(L.B + 1), dim3(256), args, 0, inst->stream),
+        int *cnt = inst->at<int>(L.off_flow) + 32 + (size_t)2 * (inst->cfg.tips - 1) * L.n_tiles + (size_t)L.B * R;
+        double *sp = inst->at<double>(L.off_gpart);      // [B+1][slices] <= [B][n_tiles] + [n_tiles] (codon path)
+        const int ns = std::min(pg::codon::RATIO_SLICES, L.n_tiles);
+        void *args[] = {&c, &d_out, &sp, &cnt};
+        CK(cudaLaunchKernel((void *)pg::codon::codon_ratio_kernel, dim3(L.B + 1, ns), dim3(256), args, 0, inst->stream),
            "codon ratio launch");
     } else {
         const double *gp = inst->at<double>(L.off_gpart), *lp = inst->at<double>(L.off_lpart);

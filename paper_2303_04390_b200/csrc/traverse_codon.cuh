@@ -615,11 +615,19 @@ __global__ void __launch_bounds__(codon_threads<SP>(), codon_ctas_per_sm<SP>()) 
 // Eq. 6-8 ratio over categories, weighted by w_c, summed over patterns in a
 // fixed order (block b < B: branch b); block B: logL from the root terms.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) codon_ratio_kernel(const CodonArgs a, double *out) {
+// Pattern slices per branch: block (b, slice) sums its slice, the last
+// slice to finish (atomic counter) adds the slice sums in slice order, so the
+// result does not depend on which block finished last (deterministic).
+constexpr int RATIO_SLICES = 8;
+__global__ void __launch_bounds__(256) codon_ratio_kernel(const CodonArgs a, double *out, double *slice_part,
+                                                          int *slice_cnt) {
     __shared__ double sh[256];
+    __shared__ bool last;
     const int b = blockIdx.x, B = 2 * a.N - 2, root = 2 * a.N - 2;
+    const int ns = gridDim.y, per = (a.C + ns - 1) / ns;
+    const int c0 = blockIdx.y * per, c1 = min(a.C, c0 + per);
     double acc = 0.0;
-    for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
+    for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
         const double wc = a.pat_w[c];
         if (b < B) {
             double num = 0.0, den = 0.0;
@@ -642,7 +650,18 @@ __global__ void __launch_bounds__(256) codon_ratio_kernel(const CodonArgs a, dou
         if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
         __syncthreads();
     }
-    if (threadIdx.x == 0) out[b < B ? 1 + b : 0] = sh[0];
+    if (threadIdx.x == 0) {
+        slice_part[(size_t)b * ns + blockIdx.y] = sh[0];
+        __threadfence();
+        last = atomicAdd(slice_cnt + b, 1) == ns - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double t = 0.0;
+        for (int k = 0; k < ns; ++k) t += __ldcg(slice_part + (size_t)b * ns + k);
+        out[b < B ? 1 + b : 0] = t;
+    }
 }
 
 template <int SP>
