@@ -41,6 +41,54 @@ __global__ void __launch_bounds__(256) pmat_kernel(const double *__restrict__ V,
     }
 }
 
+// A1 for the FP64 tensor-core S = 16 traversal (traverse_small.cuh,
+// small_mma): P = M0 + V diag(expm1(gamma_r b_i lambda)) V^{-1} as above,
+// written as the branch's three layouts [B of u = P p][B of q = x P][row-major,
+// stride 17, column 16 = P 1] (fragment order: element (kt, nt, lane) at
+// (kt * 2 + nt) * 32 + lane, k = 4 kt + lane % 4, n = 8 nt + lane / 4, output
+// state sigma(n)).  One CTA per branch (R = 1).
+__global__ void __launch_bounds__(256) pmat16_mma_kernel(const double *__restrict__ V, const double *__restrict__ Vi,
+                                                         const double *__restrict__ M0,
+                                                         const double *__restrict__ lam,
+                                                         const double *__restrict__ rates,
+                                                         const double *__restrict__ bl, int S, int rec,
+                                                         double *__restrict__ P) {
+    __shared__ double e[16], Ps[16][17];
+    const int b = blockIdx.x;
+    const double t = rates[0] * bl[b];
+    for (int k = threadIdx.x; k < 16; k += blockDim.x) e[k] = k < S ? expm1(lam[k] * t) : 0.0;
+    __syncthreads();
+    {
+        const int s = threadIdx.x >> 4, u = threadIdx.x & 15;
+        double acc = 0.0;
+        if (s < S && u < S) {
+            for (int k = 0; k < S; ++k) acc += V[s * S + k] * e[k] * Vi[k * S + u];
+            acc += M0[s * 16 + u];
+        }
+        Ps[s][u] = acc;
+    }
+    __syncthreads();
+    double *R0 = P + (size_t)b * rec, *R1 = R0 + 16 * 17, *R2 = R1 + 16 * 17;
+    {
+        const int idx = threadIdx.x, f = idx >> 5, l = idx & 31;
+        const int k = 4 * (f >> 1) + (l & 3), n = 8 * (f & 1) + (l >> 2);
+        const int sg = 4 * (2 * (n >> 3) + (n & 1)) + ((n & 7) >> 1);
+        R0[idx] = Ps[sg][k];
+        R1[idx] = Ps[k][sg];
+    }
+    for (int i = threadIdx.x; i < 16 * 17; i += blockDim.x) {
+        const int row = i / 17, col = i % 17;
+        double v;
+        if (col < 16) {
+            v = Ps[row][col];
+        } else {
+            v = 0.0;
+            for (int c = 0; c < 16; ++c) v += Ps[row][c];
+        }
+        R2[i] = v;
+    }
+}
+
 // A6 -- Eq. 6 column sum, deterministic: block b < B sums the
 // per-tile gradient partials of branch b, block B the per-tile logL partials,
 // in a fixed order (strided serial sums, then a fixed smem tree).  No atomics,

@@ -36,6 +36,7 @@ size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
 
 struct Layout {
     int SP = 0, variant = 0, Cpad = 0, n_tiles = 0, B = 0, tpl = 32, cat_stride = 0;
+    bool mma = false;                   // small-S traversal on the FP64 tensor path (SP = 16, R = 1, fp64)
     size_t real = 8;
     size_t off_P, off_PT, off_M0, off_Q, off_QT, off_pi, off_V, off_Vi, off_lam, off_rates, off_cw,
         off_bl, off_patw, off_tips, off_tipp, off_u, off_gpart, off_lpart, off_out, off_status,
@@ -103,8 +104,11 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
     L->Cpad = (int)((C + 31) / 32 * 32);
     L->n_tiles = L->Cpad / L->tpl;
     L->B = (int)(2 * N - 2);
-    // small-S kernels read P with a padded category stride (SmallCfg::CS)
-    L->cat_stride = SP * SP + ((L->variant == 0 && R > 1) ? pg::small_cat_pad(L->real, SP) / L->real : 0);
+    // small-S kernels read P with a padded category stride (SmallCfg::CS); the
+    // tensor-core S = 16 variant keeps a three-layout record per branch
+    L->mma = L->variant == 0 && pg::small_mma(SP, R == 1 ? 1 : 2, (int)L->real);
+    L->cat_stride = L->mma ? pg::MMA_REC / 8
+                           : SP * SP + ((L->variant == 0 && R > 1) ? pg::small_cat_pad(L->real, SP) / L->real : 0);
     const size_t mats = (size_t)L->B * R * L->cat_stride * L->real;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t at = o; o = align_up(o + bytes); return at; };
@@ -528,7 +532,16 @@ int pg_set_eigen(pg_instance *inst, const double *evec, const double *ievec, con
             M0[(size_t)s * SP + t] = (double)acc0;
         }
     if ((rc = upload_doubles(inst, inst->L.off_M0, M0.data(), M0.size()))) return rc;
-    if ((rc = upload_real(inst, inst->L.off_Q, Q))) return rc;
+    if (inst->L.mma) {                  // Q as the B operand of Q u (small_mma fragment order)
+        std::vector<double> QB((size_t)SP * SP, 0.0);
+        for (int idx = 0; idx < 256; ++idx) {
+            const int f = idx >> 5, l = idx & 31, k = 4 * (f >> 1) + (l & 3), n = 8 * (f & 1) + (l >> 2);
+            QB[idx] = Q[(size_t)pg::mma_sigma(n) * SP + k];
+        }
+        if ((rc = upload_real(inst, inst->L.off_Q, QB))) return rc;
+    } else if ((rc = upload_real(inst, inst->L.off_Q, Q))) {
+        return rc;
+    }
     if ((rc = upload_real(inst, inst->L.off_QT, QT))) return rc;
     if (inst->L.variant == 2) {      // Q as the fragment-ordered B operand of Qu = u Q'
         std::vector<double> QB((size_t)SP * SP);
@@ -1133,8 +1146,15 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         void *PT = L.variant == 1 ? inst->ws + L.off_PT : nullptr;
         int cs = L.cat_stride;
         const double *M0 = inst->at<double>(L.off_M0);
-        void *args[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, (void *)&R, &cs, &P, &PT};
-        CK(cudaLaunchKernel(fn, dim3(L.B * R), dim3(std::min(256, L.SP * L.SP)), args, 0, inst->stream), "pmat launch");
+        if (L.mma) {
+            void *args16[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, &cs, &P};
+            CK(cudaLaunchKernel((void *)pg::pmat16_mma_kernel, dim3(L.B), dim3(256), args16, 0, inst->stream),
+               "pmat16 launch");
+        } else {
+            void *args[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, (void *)&R, &cs, &P, &PT};
+            CK(cudaLaunchKernel(fn, dim3(L.B * R), dim3(std::min(256, L.SP * L.SP)), args, 0, inst->stream),
+               "pmat launch");
+        }
     }
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[1], inst->stream, cudaEventRecordExternal), "event");
     if (L.variant == 2) {

@@ -74,6 +74,31 @@ __host__ __device__ constexpr int small_cat_pad(int real_bytes, int SP) {
     return (real_bytes == 8 && SP == 4) ? 32 : 16;
 #endif
 }
+// FP64 tensor-core variant (SP = 16, one rate category, fp64: the 4 x K
+// Markov-modulated workloads, BJ:configs[2]).  A warp's tile is 8 patterns x
+// 16 states, and every matrix-vector product of a step -- u = P p (Eq. 2),
+// q = x P (Eq. 4), Q u (Eq. 8) -- is one [8 x 16] x [16 x 16] product: 8
+// mma.sync.m8n8k4.f64 (SASS DMMA) instead of 64 DFMA per lane plus a
+// shared-memory exchange of the whole vector.  Lane l holds states
+// {j, 4+j, 8+j, 12+j} (j = l % 4) of pattern l / 4: exactly its A fragments
+// (k = 4 kt + j).  The output columns of the B operands are permuted,
+// n -> sigma(n) = 4 (2 (n / 8) + n % 2) + (n % 8) / 2, so the lane's C
+// fragments are again its own states in the same order: a product's result
+// is the next product's A operand with no data movement.  Each branch's
+// record holds three 16 x 16 layouts (A1 writes them): [P as B of u = P p]
+// [P as B of q = x P] [P row-major, row stride 17, column 16 = P 1].
+__host__ __device__ constexpr bool small_mma(int SP, int RP, int real_bytes) {
+#ifdef PG_NO_SMALL_MMA
+    return false;
+#else
+    return SP == 16 && RP == 1 && real_bytes == 8;
+#endif
+}
+constexpr int MMA_RS = 17;                                       // row stride of the row-major layout
+constexpr int MMA_SLOT = 16 * MMA_RS * 8;                        // bytes per layout (2176)
+constexpr int MMA_REC = 3 * MMA_SLOT;                            // bytes per branch record
+__host__ __device__ constexpr int mma_sigma(int n) { return 4 * (2 * (n >> 3) + (n & 1)) + ((n & 7) >> 1); }
+
 // consumer warps per CTA at most (launch bounds: + 1 producer warp)
 __host__ __device__ constexpr int small_max_consumers(int SP, int RP) { return small_lanes_per_vector(SP, RP) * 4 / SP >= 2 ? 17 : 9; }
 
@@ -105,10 +130,12 @@ struct SmallCfg {
     static constexpr int CS = MATB + (RP > 1 ? small_cat_pad(sizeof(Real), SP) : 0);   // padded category stride
     static constexpr int ND = W * 2 * 32 * 16;                 // (num, den) window per warp
     static constexpr int XGS = VB + 16;                        // exchange stride per lane group (bank skew)
-    static constexpr int XB = LV > 1 ? (32 / LV) * XGS : 0;    // full-vector exchange buffer per warp
+    static constexpr bool MMA = small_mma(SP, RP, (int)sizeof(Real));
+    static constexpr int XB = (LV > 1 && !MMA) ? (32 / LV) * XGS : 0;   // full-vector exchange buffer per warp
     static constexpr int QOFF = 128;                           // Q (SP > 4 only; SP <= 4 keeps it in registers)
     static constexpr int BARS = QOFF + (SP > 4 ? SP * SP * (int)sizeof(Real) : 0);   // barriers + Q
-    static __host__ __device__ int mat_slot(int R) { return R * CS; }
+    static __host__ __device__ int mat_slot(int R) { return MMA ? MMA_SLOT : R * CS; }
+    static __host__ __device__ int mat_rec(int R) { return MMA ? MMA_REC : R * CS; }   // bytes per branch in HBM
     static __host__ __device__ int vslot(int R, int K) {       // one child's vectors for K warps
         int a = K * TP * R * VB, b = K * TP * VB, c = (15 + K * TP + 15) / 16 * 16;
         int m = a > b ? a : b;
@@ -305,6 +332,39 @@ __device__ __forceinline__ double ratio(double n, double d) {
     const double q = n * r;
     return fma(fma(-d, q, n), r, q);
 }
+// [8 patterns x 16] x [16 x 16] on the FP64 tensor path: y (the lane's 4
+// states, slot order) = A (slot order) times the fragment-ordered B operand
+// Bf[(kt * 2 + nt) * 32 + lane]; see small_mma.
+__device__ __forceinline__ void dmma16(double (&y)[4], const double (&A)[4], const double *Bf, int lane) {
+    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+#pragma unroll
+    for (int kt = 0; kt < 4; ++kt) {
+        const double b0 = Bf[(kt * 2) * 32 + lane], b1 = Bf[(kt * 2 + 1) * 32 + lane];
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c0[0]), "+d"(c0[1]) : "d"(A[kt]), "d"(b0));
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c1[0]), "+d"(c1[1]) : "d"(A[kt]), "d"(b1));
+    }
+    y[0] = c0[0];
+    y[1] = c0[1];
+    y[2] = c1[0];
+    y[3] = c1[1];
+}
+__device__ __forceinline__ void dmma16r(double (&y)[4], const double (&A)[4], const double (&B)[8]) {
+    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+#pragma unroll
+    for (int kt = 0; kt < 4; ++kt) {
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c0[0]), "+d"(c0[1]) : "d"(A[kt]), "d"(B[2 * kt]));
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c1[0]), "+d"(c1[1]) : "d"(A[kt]), "d"(B[2 * kt + 1]));
+    }
+    y[0] = c0[0];
+    y[1] = c0[1];
+    y[2] = c1[0];
+    y[3] = c1[1];
+}
+
 // Rescale v (exactly) if any vector of the warp fell below the threshold;
 // returns the exponent removed (shared by the categories of a pattern).
 // G = lanes sharing one pattern (categories x state groups, contiguous)
@@ -334,6 +394,8 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nops = N - 1, root = 2 * N - 2;
     const int MS = Cfg::mat_slot(R), VS = Cfg::vslot(R, K), ST = Cfg::stage(R, K);
+    const int MREC = Cfg::mat_rec(R);
+    constexpr bool MMA = Cfg::MMA;
     const size_t Cpad = (size_t)a.Cpad;
     const int cta_tile0 = blockIdx.x * K;
     const int ntile = min(K, a.n_tiles - cta_tile0);               // live tiles of this CTA
@@ -403,6 +465,17 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             else bulk_g2s_u32(dst, tipS + ((size_t)node * Cpad + cta_pat0 - tip_lead), tipw_bytes, bar);
         };
         auto u_src = [&](int node) -> const char * { return Ub + (size_t)(node - N) * u_node + u_cta; };
+        // the matrix a step reads for node `code` in role `pre` (MMA: which
+        // layout of the branch record; else the branch's R category blocks)
+        auto mat_src = [&](int code, bool pre_child) -> const char * {
+            const int node = code & ~kTipPartialBit;
+            const char *rec = Pb + (size_t)node * MREC;
+            if constexpr (MMA) {
+                const int lay = node >= N ? (pre_child ? 1 : 0) : ((code & kTipPartialBit) ? 0 : 2);
+                return rec + lay * MMA_SLOT;
+            }
+            return rec;
+        };
         // bytes and copies of step t's sub-stage:
         //   post [op][P_k][P_a][P_b][tip a][tip b];  pre [op][P_a][P_b][-][vec a][vec b]
         auto op_bytes = [&](int t) -> unsigned {
@@ -423,19 +496,19 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             const Op4 op = prog[m];
             bulk_g2s_u32(st, gprog + m, 16, bar);
             if (!pre) {
-                if (op.x != root) bulk_g2s_u32(st + 16, Pb + (size_t)op.x * MS, MS, bar);
+                if (op.x != root) bulk_g2s_u32(st + 16, mat_src(op.x, false), MS, bar);
                 if (op.y >= 0) {
-                    bulk_g2s_u32(st + 16 + MS, Pb + (size_t)(op.y & ~kTipPartialBit) * MS, MS, bar);
+                    bulk_g2s_u32(st + 16 + MS, mat_src(op.y, false), MS, bar);
                     copy_tip(st + 16 + 3 * MS, op.y, bar);
                 }
                 if (op.z >= 0) {
-                    bulk_g2s_u32(st + 16 + 2 * MS, Pb + (size_t)(op.z & ~kTipPartialBit) * MS, MS, bar);
+                    bulk_g2s_u32(st + 16 + 2 * MS, mat_src(op.z, false), MS, bar);
                     copy_tip(st + 16 + 3 * MS + VS, op.z, bar);
                 }
             } else {
                 const int na = op.y & ~kTipPartialBit, nb = op.z & ~kTipPartialBit;
-                bulk_g2s_u32(st + 16, Pb + (size_t)na * MS, MS, bar);
-                bulk_g2s_u32(st + 16 + MS, Pb + (size_t)nb * MS, MS, bar);
+                bulk_g2s_u32(st + 16, mat_src(op.y, true), MS, bar);
+                bulk_g2s_u32(st + 16 + MS, mat_src(op.z, true), MS, bar);
                 if (na >= N) bulk_g2s_u32(st + 16 + 3 * MS, u_src(na), u_bytes, bar);
                 else copy_tip(st + 16 + 3 * MS, op.y, bar);
                 if (nb >= N) bulk_g2s_u32(st + 16 + 3 * MS + VS, u_src(nb), u_bytes, bar);
@@ -491,7 +564,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     const double gwr = wr * a.cat_g[r];
     Real pi[VL];
 #pragma unroll
-    for (int s = 0; s < VL; ++s) pi[s] = static_cast<const Real *>(a.pi)[h * VL + s];
+    for (int s = 0; s < VL; ++s) pi[s] = static_cast<const Real *>(a.pi)[MMA ? 4 * s + h : h * VL + s];
     if (active && lane < TP) wbuf[lane] = a.pat_w[pat0 + lane];
     __syncwarp();
 
@@ -554,6 +627,21 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     };
     auto child_tip = [&](Real (&u)[VL], const unsigned char *M_, const unsigned char *vs, int code) {
         const Real *M = reinterpret_cast<const Real *>(M_ + mat_lane);
+        if constexpr (MMA) {
+            if (code & kTipPartialBit) {            // u = P p_tip: the lane's states of p_tip, one product
+                const double *tp = reinterpret_cast<const double *>(vs + tipp_vec);
+                double pa[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) pa[i] = tp[4 * i + h];
+                dmma16(u, pa, M, lane);
+            } else {                                // column `state` of P (column 16 = P 1: missing)
+                const int sv = vs[tip_idx];
+                const int col = sv < S ? sv : 16;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) u[i] = M[(4 * i + h) * MMA_RS + col];
+            }
+            return;
+        }
         if (code & kTipPartialBit) {
             Real tp[SP];
             lds_rot<Real, SP, VL>(tp, vs + tipp_vec, h);
@@ -622,10 +710,14 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
         } else {
             E += maybe_rescale<Real, VL, G>(p);
             if (warp == 0) PG_TSTAMP((size_t)t * 16 + 6, p[0]);
-            Real pf[SP];
-            gather(pf, p);
             Real u[VL];
-            mv<Real, SP, VL>(u, reinterpret_cast<const Real *>(st + 16 + mat_lane), pf, h);
+            if constexpr (MMA) {
+                dmma16(u, p, reinterpret_cast<const double *>(st + 16), lane);
+            } else {
+                Real pf[SP];
+                gather(pf, p);
+                mv<Real, SP, VL>(u, reinterpret_cast<const Real *>(st + 16 + mat_lane), pf, h);
+            }
             if (warp == 0) PG_TSTAMP((size_t)t * 16 + 7, u[0] + u[VL - 1]);
             release(t);
             stg_vec<Real, VL>(Ub + (size_t)(op.x - N) * u_node + u_lane, u);   // shadow lanes: same value
@@ -648,6 +740,11 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     // -------------------- pre program (Eq. 4) + gradient (Eq. 6-8) ---------------
     // Q rows [h VL, +VL): registers when SP = 4, else shared memory
     Real Qr[SP <= 4 ? VL : 1][SP <= 4 ? SP : 1];
+    double QB[MMA ? 8 : 1];                       // MMA: Q as the B operand of Q u (fragment order)
+    if constexpr (MMA) {
+#pragma unroll
+        for (int f = 0; f < 8; ++f) QB[f] = reinterpret_cast<const double *>(smem + Cfg::QOFF)[f * 32 + lane];
+    }
     if constexpr (SP <= 4) {
 #pragma unroll
         for (int s = 0; s < VL; ++s)
@@ -704,9 +801,13 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
 #pragma unroll
         for (int c = 0; c < 2; ++c)
             if (slots[c] >= 0) {
-                Real xf[SP];
-                gather(xf, x[c]);
-                mvt<Real, SP, VL>(qc[c], reinterpret_cast<const Real *>(st + 16 + c * MS + mat_lane), xf, h);
+                if constexpr (MMA) {
+                    dmma16(qc[c], x[c], reinterpret_cast<const double *>(st + 16 + c * MS), lane);
+                } else {
+                    Real xf[SP];
+                    gather(xf, x[c]);
+                    mvt<Real, SP, VL>(qc[c], reinterpret_cast<const Real *>(st + 16 + c * MS + mat_lane), xf, h);
+                }
             }
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 6, qc[0][0] + qc[1][0]);
         release(t);                                 // stage no longer needed
@@ -716,25 +817,36 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             if (lane == 0) nodes_w[(n % W) * 2 + c] = cs[c] & ~kTipPartialBit;
             // my states' share of num = x' Q u_c and den = x' u_c (summed over
             // the pattern's lanes in the window flush)
-            Real ucf[SP];
-            gather(ucf, uc[c]);
             Real num = 0, den = 0;
+            if constexpr (MMA) {
+                double Qu[4];
+                dmma16r(Qu, uc[c], QB);
 #pragma unroll
-            for (int s = 0; s < VL; ++s) {
-                Real Qu;
-                if constexpr (SP <= 4) {
-                    Qu = Qr[s][0] * ucf[0];
-#pragma unroll
-                    for (int t2 = 1; t2 < SP; ++t2) Qu = fma(Qr[s][t2], ucf[t2], Qu);
-                } else {
-                    Real row[SP];
-                    lds_rot<Real, SP, VL>(row, reinterpret_cast<const unsigned char *>(Qs + (h * VL + s) * SP), h);
-                    Qu = row[0] * ucf[0];
-#pragma unroll
-                    for (int t2 = 1; t2 < SP; ++t2) Qu = fma(row[t2], ucf[t2], Qu);
+                for (int s = 0; s < 4; ++s) {
+                    num = fma(x[c][s], Qu[s], num);
+                    den = fma(x[c][s], uc[c][s], den);
                 }
-                num = fma(x[c][s], Qu, num);
-                den = fma(x[c][s], uc[c][s], den);
+            }
+            if constexpr (!MMA) {
+                Real ucf[SP];
+                gather(ucf, uc[c]);
+#pragma unroll
+                for (int s = 0; s < VL; ++s) {
+                    Real Qu;
+                    if constexpr (SP <= 4) {
+                        Qu = Qr[s][0] * ucf[0];
+#pragma unroll
+                        for (int t2 = 1; t2 < SP; ++t2) Qu = fma(Qr[s][t2], ucf[t2], Qu);
+                    } else {
+                        Real row[SP];
+                        lds_rot<Real, SP, VL>(row, reinterpret_cast<const unsigned char *>(Qs + (h * VL + s) * SP), h);
+                        Qu = row[0] * ucf[0];
+#pragma unroll
+                        for (int t2 = 1; t2 < SP; ++t2) Qu = fma(row[t2], ucf[t2], Qu);
+                    }
+                    num = fma(x[c][s], Qu, num);
+                    den = fma(x[c][s], uc[c][s], den);
+                }
             }
             ndw[c * 32] = make_double2(gwr * (double)num, wr * (double)den);
             if (slots[c] >= 0) {
