@@ -43,6 +43,12 @@
 #ifndef PG_SMALL_W
 #define PG_SMALL_W 2
 #endif
+#ifndef PG_MMA_STAGES
+#define PG_MMA_STAGES 8
+#endif
+#ifndef PG_TIPP_PF
+#define PG_TIPP_PF 0
+#endif
 
 
 namespace pg {
@@ -114,7 +120,9 @@ struct SmallCfg {
     static constexpr int VL = SP / LV;                         // states per lane
     static constexpr int TP = 32 / (RP * LV);                  // patterns per warp tile
 #ifndef PG_STAGES
-    static constexpr int D = 4;                                // stage ring depth (steps)
+    // stage ring depth (steps); the tensor-core S = 16 variant's steps are
+    // short enough that 4 stages do not cover the copies' latency
+    static constexpr int D = small_mma(SP, RP, (int)sizeof(Real)) ? PG_MMA_STAGES : 4;
 #else
     static constexpr int D = PG_STAGES;
 #endif
@@ -495,6 +503,13 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             const Op4 *prog = pre ? pre_prog : post_prog;       // smem copy when staged
             const Op4 op = prog[m];
             bulk_g2s_u32(st, gprog + m, 16, bar);
+            if (PG_TIPP_PF && tipP && m + PF < nops) {      // partial-tip chunks into L2 ahead (HBM latency)
+                const Op4 o2 = prog[m + PF];
+                if (o2.y >= 0 && (o2.y & kTipPartialBit))
+                    prefetch_l2(tipP + ((size_t)(o2.y & ~kTipPartialBit) * Cpad + cta_pat0) * VB, tipp_bytes);
+                if (o2.z >= 0 && (o2.z & kTipPartialBit))
+                    prefetch_l2(tipP + ((size_t)(o2.z & ~kTipPartialBit) * Cpad + cta_pat0) * VB, tipp_bytes);
+            }
             if (!pre) {
                 if (op.x != root) bulk_g2s_u32(st + 16, mat_src(op.x, false), MS, bar);
                 if (op.y >= 0) {
