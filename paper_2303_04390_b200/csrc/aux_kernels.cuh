@@ -89,6 +89,32 @@ __global__ void __launch_bounds__(256) pmat16_mma_kernel(const double *__restric
     }
 }
 
+// A1 for the FP64 tensor-core S = 4, R = 4 traversal (traverse_small.cuh,
+// small_tc): thread (category r, lane l) forms the two B-operand entries
+// P_r[(l/4)/2][l%4] (u = P p) and P_r[l%4][(l/4)/2] (q = x P), each as
+// M0 + sum_k V diag(expm1(gamma_r b lambda)) V^{-1}.  One CTA per branch.
+__global__ void __launch_bounds__(128) pmat4_mma_kernel(const double *__restrict__ V, const double *__restrict__ Vi,
+                                                        const double *__restrict__ M0,
+                                                        const double *__restrict__ lam,
+                                                        const double *__restrict__ rates,
+                                                        const double *__restrict__ bl, int S, int rec,
+                                                        double *__restrict__ P) {
+    const int b = blockIdx.x, r = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const double t = rates[r] * bl[b];
+    double e[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) e[k] = k < S ? expm1(lam[k] * t) : 0.0;
+    auto entry = [&](int s, int u) {
+        if (s >= S || u >= S) return 0.0;
+        double acc = 0.0;
+        for (int k = 0; k < S; ++k) acc += V[s * S + k] * e[k] * Vi[k * S + u];
+        return acc + M0[s * 4 + u];
+    };
+    double *R0 = P + (size_t)b * rec;
+    R0[r * 32 + l] = entry((l >> 2) >> 1, l & 3);
+    R0[128 + r * 32 + l] = entry(l & 3, (l >> 2) >> 1);
+}
+
 // A6 -- Eq. 6 column sum, deterministic: block b < B sums the
 // per-tile gradient partials of branch b, block B the per-tile logL partials,
 // in a fixed order (strided serial sums, then a fixed smem tree).  No atomics,

@@ -106,8 +106,8 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
     L->B = (int)(2 * N - 2);
     // small-S kernels read P with a padded category stride (SmallCfg::CS); the
     // tensor-core S = 16 variant keeps a three-layout record per branch
-    L->mma = L->variant == 0 && pg::small_mma(SP, R == 1 ? 1 : 2, (int)L->real);
-    L->cat_stride = L->mma ? pg::MMA_REC / 8
+    L->mma = L->variant == 0 && pg::small_tc(SP, R, (int)L->real);
+    L->cat_stride = L->mma ? (SP == 16 ? pg::MMA_REC / 8 : 2 * pg::MMA4_SLOT / 8 / R)   // per category (x R = record)
                            : SP * SP + ((L->variant == 0 && R > 1) ? pg::small_cat_pad(L->real, SP) / L->real : 0);
     const size_t mats = (size_t)L->B * R * L->cat_stride * L->real;
     size_t o = 0;
@@ -123,7 +123,7 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         L->off_ViB = take((size_t)SP * SP * 8);
     }
     L->off_M0 = take((size_t)SP * SP * 8);     // V V^-1 (A1's identity term, host long double)
-    L->off_Q = take((size_t)SP * SP * L->real);
+    L->off_Q = take((size_t)std::max(SP * SP, 32) * L->real);   // (S = 4 tensor-core variant: 32 fragment values)
     L->off_QT = take((size_t)SP * SP * L->real);
     L->off_pi = take((size_t)SP * L->real);
     L->off_V = take((size_t)c->states * c->states * 8);
@@ -532,7 +532,11 @@ int pg_set_eigen(pg_instance *inst, const double *evec, const double *ievec, con
             M0[(size_t)s * SP + t] = (double)acc0;
         }
     if ((rc = upload_doubles(inst, inst->L.off_M0, M0.data(), M0.size()))) return rc;
-    if (inst->L.mma) {                  // Q as the B operand of Q u (small_mma fragment order)
+    if (inst->L.mma && SP == 4) {       // Q as the B operand of Q u (S = 4 variant: Q[n/2][k])
+        std::vector<double> QB(32, 0.0);
+        for (int l = 0; l < 32; ++l) QB[l] = Q[(size_t)((l >> 2) >> 1) * SP + (l & 3)];
+        if ((rc = upload_real(inst, inst->L.off_Q, QB))) return rc;
+    } else if (inst->L.mma) {           // Q as the B operand of Q u (S = 16 variant fragment order)
         std::vector<double> QB((size_t)SP * SP, 0.0);
         for (int idx = 0; idx < 256; ++idx) {
             const int f = idx >> 5, l = idx & 31, k = 4 * (f >> 1) + (l & 3), n = 8 * (f & 1) + (l >> 2);
@@ -744,8 +748,8 @@ int pg_set_branch_lengths_device(pg_instance *inst, const double *d_b) {
 // launch configuration
 // -------------------------------------------------------------------------
 
-template <typename Real, int SP, int RP>
-static void *small_kernel() { return (void *)pg::traverse_small_kernel<Real, SP, RP>; }
+template <typename Real, int SP, int RP, int TC = 0>
+static void *small_kernel() { return (void *)pg::traverse_small_kernel<Real, SP, RP, TC>; }
 template <typename Real, int SP>
 static void *large_kernel() { return (void *)pg::traverse_large_kernel<Real, SP>; }
 template <typename Real, int SP>
@@ -791,6 +795,7 @@ static void *small_by_rp(int RP) {
 static void *traverse_fn(const Layout &L, int R) {
     const bool d = L.real == 8;
     const int RP = pad_categories(R);
+    if (L.mma) return L.SP == 16 ? small_kernel<double, 16, 1, 1>() : small_kernel<double, 4, 4, 1>();
     switch (L.SP) {
         case 4: return d ? small_by_rp<double, 4>(RP) : small_by_rp<float, 4>(RP);
         case 8: return d ? small_by_rp<double, 8>(RP) : small_by_rp<float, 8>(RP);
@@ -827,6 +832,8 @@ static size_t small_smem_t(int RP, int R, int K, int depth) {
 static size_t small_smem(const Layout &L, int R, int K, int depth) {
     const bool d = L.real == 8;
     const int RP = pad_categories(R);
+    if (L.mma)
+        return L.SP == 16 ? pg::SmallCfg<double, 16, 1, 1>::smem(R, K, depth) : pg::SmallCfg<double, 4, 4, 1>::smem(R, K, depth);
     switch (L.SP) {
         case 4: return d ? small_smem_t<double, 4>(RP, R, K, depth) : small_smem_t<float, 4>(RP, R, K, depth);
         case 8: return d ? small_smem_t<double, 8>(RP, R, K, depth) : small_smem_t<float, 8>(RP, R, K, depth);
@@ -1147,9 +1154,14 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         int cs = L.cat_stride;
         const double *M0 = inst->at<double>(L.off_M0);
         if (L.mma) {
-            void *args16[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, &cs, &P};
-            CK(cudaLaunchKernel((void *)pg::pmat16_mma_kernel, dim3(L.B), dim3(256), args16, 0, inst->stream),
-               "pmat16 launch");
+            int rec = cs * R;                            // doubles per branch record
+            void *args16[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, &rec, &P};
+            if (L.SP == 16)
+                CK(cudaLaunchKernel((void *)pg::pmat16_mma_kernel, dim3(L.B), dim3(256), args16, 0, inst->stream),
+                   "pmat16 launch");
+            else
+                CK(cudaLaunchKernel((void *)pg::pmat4_mma_kernel, dim3(L.B), dim3(128), args16, 0, inst->stream),
+                   "pmat4 launch");
         } else {
             void *args[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, (void *)&R, &cs, &P, &PT};
             CK(cudaLaunchKernel(fn, dim3(L.B * R), dim3(std::min(256, L.SP * L.SP)), args, 0, inst->stream),

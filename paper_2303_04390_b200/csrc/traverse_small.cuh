@@ -93,13 +93,21 @@ __host__ __device__ constexpr int small_cat_pad(int real_bytes, int SP) {
 // is the next product's A operand with no data movement.  Each branch's
 // record holds three 16 x 16 layouts (A1 writes them): [P as B of u = P p]
 // [P as B of q = x P] [P row-major, row stride 17, column 16 = P 1].
-__host__ __device__ constexpr bool small_mma(int SP, int RP, int real_bytes) {
+// The S = 4 (nucleotide) variant with four rate categories: lane l holds
+// state j = l % 4 of pattern l / 4 for the four categories (one register
+// each); per category the product is one m8n8k4 DMMA whose B operand repeats
+// every output column twice (n -> state n / 2), so lane l's first C element
+// is exactly state j of its pattern: [8 x 4] x [4 x 8] per category, the
+// result again in the A layout.  Branch record: [P as B of u = P p][P as B
+// of q = x P], each [4 categories][32 lanes] doubles.
+__host__ __device__ constexpr bool small_tc(int SP, int R, int real_bytes) {
 #ifdef PG_NO_SMALL_MMA
     return false;
 #else
-    return SP == 16 && RP == 1 && real_bytes == 8;
+    return real_bytes == 8 && ((SP == 16 && R == 1) || (SP == 4 && R == 4));
 #endif
 }
+constexpr int MMA4_SLOT = 4 * 32 * 8;                            // bytes per layout (1 KB)
 constexpr int MMA_RS = 17;                                       // row stride of the row-major layout
 constexpr int MMA_SLOT = 16 * MMA_RS * 8;                        // bytes per layout (2176)
 constexpr int MMA_REC = 3 * MMA_SLOT;                            // bytes per branch record
@@ -114,15 +122,17 @@ __host__ __device__ constexpr int small_max_consumers(int SP, int RP) { return s
 // blocks of SP*SP Reals padded to CS bytes (16 extra bytes when R > 1 so the
 // categories of a warp hit distinct shared-memory banks): one branch's
 // matrices are one contiguous bulk copy.
-template <typename Real, int SP, int RP>
+template <typename Real, int SP, int RP, int TC = 0>
 struct SmallCfg {
+    static constexpr bool MMA = TC && SP == 16;                 // tensor-core S = 16, R = 1
+    static constexpr bool MMA4 = TC && SP == 4;                 // tensor-core S = 4, R = 4
     static constexpr int LV = small_lanes_per_vector(SP, RP); // lanes per vector
     static constexpr int VL = SP / LV;                         // states per lane
     static constexpr int TP = 32 / (RP * LV);                  // patterns per warp tile
 #ifndef PG_STAGES
     // stage ring depth (steps); the tensor-core S = 16 variant's steps are
     // short enough that 4 stages do not cover the copies' latency
-    static constexpr int D = small_mma(SP, RP, (int)sizeof(Real)) ? PG_MMA_STAGES : 4;
+    static constexpr int D = MMA ? PG_MMA_STAGES : 4;
 #else
     static constexpr int D = PG_STAGES;
 #endif
@@ -138,12 +148,11 @@ struct SmallCfg {
     static constexpr int CS = MATB + (RP > 1 ? small_cat_pad(sizeof(Real), SP) : 0);   // padded category stride
     static constexpr int ND = W * 2 * 32 * 16;                 // (num, den) window per warp
     static constexpr int XGS = VB + 16;                        // exchange stride per lane group (bank skew)
-    static constexpr bool MMA = small_mma(SP, RP, (int)sizeof(Real));
     static constexpr int XB = (LV > 1 && !MMA) ? (32 / LV) * XGS : 0;   // full-vector exchange buffer per warp
     static constexpr int QOFF = 128;                           // Q (SP > 4 only; SP <= 4 keeps it in registers)
     static constexpr int BARS = QOFF + (SP > 4 ? SP * SP * (int)sizeof(Real) : 0);   // barriers + Q
-    static __host__ __device__ int mat_slot(int R) { return MMA ? MMA_SLOT : R * CS; }
-    static __host__ __device__ int mat_rec(int R) { return MMA ? MMA_REC : R * CS; }   // bytes per branch in HBM
+    static __host__ __device__ int mat_slot(int R) { return MMA ? MMA_SLOT : MMA4 ? MMA4_SLOT : R * CS; }
+    static __host__ __device__ int mat_rec(int R) { return MMA ? MMA_REC : MMA4 ? 2 * MMA4_SLOT : R * CS; }   // bytes per branch in HBM
     static __host__ __device__ int vslot(int R, int K) {       // one child's vectors for K warps
         int a = K * TP * R * VB, b = K * TP * VB, c = (15 + K * TP + 15) / 16 * 16;
         int m = a > b ? a : b;
@@ -358,6 +367,14 @@ __device__ __forceinline__ void dmma16(double (&y)[4], const double (&A)[4], con
     y[2] = c1[0];
     y[3] = c1[1];
 }
+// one category of the S = 4 variant: C = A (8 x 4) B (4 x 8); the lane's
+// first C element is state (lane % 4) of its pattern (see small_tc)
+__device__ __forceinline__ double dmma4(double a, double b) {
+    double c0 = 0.0, c1 = 0.0;
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+    return c0;
+}
 __device__ __forceinline__ void dmma16r(double (&y)[4], const double (&A)[4], const double (&B)[8]) {
     double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
 #pragma unroll
@@ -389,9 +406,9 @@ __device__ __forceinline__ int maybe_rescale(Real (&v)[SP]) {
 }
 
 
-template <typename Real, int SP, int RP>
+template <typename Real, int SP, int RP, int TC = 0>
 __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) traverse_small_kernel(const TravArgs a) {
-    using Cfg = SmallCfg<Real, SP, RP>;
+    using Cfg = SmallCfg<Real, SP, RP, TC>;
     constexpr int TP = Cfg::TP, PF = Cfg::PF, W = Cfg::W, VB = Cfg::VB, CS = Cfg::CS;
     constexpr int LV = Cfg::LV, VL = Cfg::VL, VBL = Cfg::VBL, G = RP * LV;
     constexpr int OPS = Cfg::OPS, DS = Cfg::DS;
@@ -403,7 +420,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     const int nops = N - 1, root = 2 * N - 2;
     const int MS = Cfg::mat_slot(R), VS = Cfg::vslot(R, K), ST = Cfg::stage(R, K);
     const int MREC = Cfg::mat_rec(R);
-    constexpr bool MMA = Cfg::MMA;
+    constexpr bool MMA = Cfg::MMA, MMA4 = Cfg::MMA4;
     const size_t Cpad = (size_t)a.Cpad;
     const int cta_tile0 = blockIdx.x * K;
     const int ntile = min(K, a.n_tiles - cta_tile0);               // live tiles of this CTA
@@ -482,6 +499,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
                 const int lay = node >= N ? (pre_child ? 1 : 0) : ((code & kTipPartialBit) ? 0 : 2);
                 return rec + lay * MMA_SLOT;
             }
+            if constexpr (MMA4) return rec + ((node >= N && pre_child) ? MMA4_SLOT : 0);
             return rec;
         };
         // bytes and copies of step t's sub-stage:
@@ -577,9 +595,18 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     int *nodes_w = reinterpret_cast<int *>(wbuf + TP);                              // [W][2] branch ids
     const double wr = live ? a.cat_w[r] : 0.0;
     const double gwr = wr * a.cat_g[r];
+    // MMA4: the lane's registers are the four categories of state j = cat
+    double wR[MMA4 ? 4 : 1], gwR[MMA4 ? 4 : 1];
+    if constexpr (MMA4) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            wR[q] = a.cat_w[q];
+            gwR[q] = wR[q] * a.cat_g[q];
+        }
+    }
     Real pi[VL];
 #pragma unroll
-    for (int s = 0; s < VL; ++s) pi[s] = static_cast<const Real *>(a.pi)[MMA ? 4 * s + h : h * VL + s];
+    for (int s = 0; s < VL; ++s) pi[s] = static_cast<const Real *>(a.pi)[MMA ? 4 * s + h : MMA4 ? cat : h * VL + s];
     if (active && lane < TP) wbuf[lane] = a.pat_w[pat0 + lane];
     __syncwarp();
 
@@ -642,6 +669,22 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     };
     auto child_tip = [&](Real (&u)[VL], const unsigned char *M_, const unsigned char *vs, int code) {
         const Real *M = reinterpret_cast<const Real *>(M_ + mat_lane);
+        if constexpr (MMA4) {
+            const double *Bf = reinterpret_cast<const double *>(M_);     // [4 categories][32] (u = P p layout)
+            if (code & kTipPartialBit) {
+                const double pt = reinterpret_cast<const double *>(vs + tipp_vec)[cat];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) u[q] = dmma4(pt, Bf[q * 32 + lane]);
+            } else {                                // P[j][state] sits at lane 8 j + state
+                const int sv = vs[tip_idx];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double *row = Bf + q * 32 + 8 * cat;
+                    u[q] = sv < S ? row[sv] : (row[0] + row[1]) + (row[2] + row[3]);
+                }
+            }
+            return;
+        }
         if constexpr (MMA) {
             if (code & kTipPartialBit) {            // u = P p_tip: the lane's states of p_tip, one product
                 const double *tp = reinterpret_cast<const double *>(vs + tipp_vec);
@@ -715,9 +758,15 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
         if (op.x == root) {
             release(t);
             double L = 0.0;
+            if constexpr (MMA4) {
 #pragma unroll
-            for (int s = 0; s < VL; ++s) L = fma((double)pi[s], (double)p[s], L);
-            L = cat_sum<G>(wr * L);
+                for (int s = 0; s < VL; ++s) L = fma(wR[s] * (double)pi[s], (double)p[s], L);
+                L = cat_sum<G>(L);
+            } else {
+#pragma unroll
+                for (int s = 0; s < VL; ++s) L = fma((double)pi[s], (double)p[s], L);
+                L = cat_sum<G>(wr * L);
+            }
             if (cat == 0 && h == 0 && pat < a.C) {
                 if (!(L > 0.0) || !isfinite(L)) atomicMin(a.status, pat);
                 logl_local = wbuf[pl] * (log(L) + (double)E * 0.69314718055994530942);
@@ -728,6 +777,10 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             Real u[VL];
             if constexpr (MMA) {
                 dmma16(u, p, reinterpret_cast<const double *>(st + 16), lane);
+            } else if constexpr (MMA4) {
+                const double *Bf = reinterpret_cast<const double *>(st + 16);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) u[q] = dmma4(p[q], Bf[q * 32 + lane]);
             } else {
                 Real pf[SP];
                 gather(pf, p);
@@ -756,11 +809,12 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     // Q rows [h VL, +VL): registers when SP = 4, else shared memory
     Real Qr[SP <= 4 ? VL : 1][SP <= 4 ? SP : 1];
     double QB[MMA ? 8 : 1];                       // MMA: Q as the B operand of Q u (fragment order)
+    if constexpr (MMA4) QB[0] = static_cast<const double *>(a.Q)[lane];
     if constexpr (MMA) {
 #pragma unroll
         for (int f = 0; f < 8; ++f) QB[f] = reinterpret_cast<const double *>(smem + Cfg::QOFF)[f * 32 + lane];
     }
-    if constexpr (SP <= 4) {
+    if constexpr (SP <= 4 && !MMA4) {
 #pragma unroll
         for (int s = 0; s < VL; ++s)
 #pragma unroll
@@ -818,6 +872,10 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             if (slots[c] >= 0) {
                 if constexpr (MMA) {
                     dmma16(qc[c], x[c], reinterpret_cast<const double *>(st + 16 + c * MS), lane);
+                } else if constexpr (MMA4) {
+                    const double *Bf = reinterpret_cast<const double *>(st + 16 + c * MS);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) qc[c][q] = dmma4(x[c][q], Bf[q * 32 + lane]);
                 } else {
                     Real xf[SP];
                     gather(xf, x[c]);
@@ -833,6 +891,14 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             // my states' share of num = x' Q u_c and den = x' u_c (summed over
             // the pattern's lanes in the window flush)
             Real num = 0, den = 0;
+            if constexpr (MMA4) {                  // weighted over the lane's categories here
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double Qu = dmma4(uc[c][q], QB[0]);
+                    num = fma(gwR[q] * x[c][q], Qu, num);
+                    den = fma(wR[q] * x[c][q], uc[c][q], den);
+                }
+            }
             if constexpr (MMA) {
                 double Qu[4];
                 dmma16r(Qu, uc[c], QB);
@@ -842,7 +908,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
                     den = fma(x[c][s], uc[c][s], den);
                 }
             }
-            if constexpr (!MMA) {
+            if constexpr (!MMA && !MMA4) {
                 Real ucf[SP];
                 gather(ucf, uc[c]);
 #pragma unroll
@@ -863,7 +929,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
                     den = fma(x[c][s], uc[c][s], den);
                 }
             }
-            ndw[c * 32] = make_double2(gwr * (double)num, wr * (double)den);
+            ndw[c * 32] = MMA4 ? make_double2((double)num, (double)den) : make_double2(gwr * (double)num, wr * (double)den);
             if (slots[c] >= 0) {
                 maybe_rescale<Real, VL, G>(qc[c]);
                 stk_st(slots[c], qc[c]);
