@@ -795,7 +795,11 @@ static void *small_by_rp(int RP) {
 static void *traverse_fn(const Layout &L, int R) {
     const bool d = L.real == 8;
     const int RP = pad_categories(R);
+#ifdef PG_SMALL_MMA4
     if (L.mma) return L.SP == 16 ? small_kernel<double, 16, 1, 1>() : small_kernel<double, 4, 4, 1>();
+#else
+    if (L.mma) return small_kernel<double, 16, 1, 1>();
+#endif
     switch (L.SP) {
         case 4: return d ? small_by_rp<double, 4>(RP) : small_by_rp<float, 4>(RP);
         case 8: return d ? small_by_rp<double, 8>(RP) : small_by_rp<float, 8>(RP);
@@ -832,8 +836,7 @@ static size_t small_smem_t(int RP, int R, int K, int depth) {
 static size_t small_smem(const Layout &L, int R, int K, int depth) {
     const bool d = L.real == 8;
     const int RP = pad_categories(R);
-    if (L.mma)
-        return L.SP == 16 ? pg::SmallCfg<double, 16, 1, 1>::smem(R, K, depth) : pg::SmallCfg<double, 4, 4, 1>::smem(R, K, depth);
+    if (L.mma) return L.SP == 16 ? pg::SmallCfg<double, 16, 1, 1>::smem(R, K, depth) : pg::SmallCfg<double, 4, 4, 1>::smem(R, K, depth);
     switch (L.SP) {
         case 4: return d ? small_smem_t<double, 4>(RP, R, K, depth) : small_smem_t<float, 4>(RP, R, K, depth);
         case 8: return d ? small_smem_t<double, 8>(RP, R, K, depth) : small_smem_t<float, 8>(RP, R, K, depth);

@@ -100,11 +100,18 @@ __host__ __device__ constexpr int small_cat_pad(int real_bytes, int SP) {
 // is exactly state j of its pattern: [8 x 4] x [4 x 8] per category, the
 // result again in the A layout.  Branch record: [P as B of u = P p][P as B
 // of q = x P], each [4 categories][32 lanes] doubles.
+// Measured (scripts/gpu_mma4.sh, dengue fp64): the S = 4 variant is slower
+// than the SIMT kernel (traversal 1.577 vs 1.427 ms: a DMMA per category
+// spends 4x the FP64-pipe time of the 16 DFMA it replaces and its latency sits
+// on the step chain), so it is built only with -DPG_SMALL_MMA4 (parity-tested
+// there); S = 16 gains 2x (MMM traversal 0.219 -> 0.109 ms).
 __host__ __device__ constexpr bool small_tc(int SP, int R, int real_bytes) {
 #ifdef PG_NO_SMALL_MMA
     return false;
-#else
+#elif defined(PG_SMALL_MMA4)
     return real_bytes == 8 && ((SP == 16 && R == 1) || (SP == 4 && R == 4));
+#else
+    return real_bytes == 8 && SP == 16 && R == 1;
 #endif
 }
 constexpr int MMA4_SLOT = 4 * 32 * 8;                            // bytes per layout (1 KB)
