@@ -37,7 +37,7 @@ METRIC = "full BLS-gradient evals/sec"
 UNIT = "evals/s"
 CONFIG_NAMES = {0: "jc5_c200", 1: "dengue997_hky_g4_c10000", 2: "carnivore62_mmm16_c5000",
                 3: "yeast49_gy94_g4_c4000", 4: "wnv104_gy94_g4_ucld_c3700",
-                5: "yeast49_mmm2x61_c4000"}
+                5: "yeast49_mmm2x61_c4000", 6: "codonmmm4x61_10001_c256"}
 
 
 def parse():
@@ -69,7 +69,7 @@ def workload_name(cfg: int, C: int) -> str:
 
 
 def make_problem(cfg: int, precision: str, patterns: int = 0):
-    kw = {"precision": precision} if cfg in (1, 2, 3, 4, 5) else {}
+    kw = {"precision": precision} if cfg in (1, 2, 3, 4, 5, 6) else {}
     if patterns > 0:
         kw["C"] = patterns
     return ps.make_config(cfg, **kw)
@@ -141,7 +141,7 @@ class ClockSampler:
 # ----------------------------------------------------------- roofline ----
 
 def padded_states(S: int) -> int:
-    return 4 if S <= 4 else 8 if S <= 8 else 16 if S <= 16 else 32 if S <= 32 else 64 if S <= 64 else 128
+    return 4 if S <= 4 else 8 if S <= 8 else 16 if S <= 16 else 32 if S <= 32 else 64 if S <= 64 else 128 if S <= 128 else 256
 
 
 def hbm_counts(pb, C: int, precision: str) -> dict:
@@ -158,7 +158,7 @@ def hbm_counts(pb, C: int, precision: str) -> dict:
     Sp = padded_states(S)
     w = 8 if precision == "fp64" else 4
     V = R * C * Sp * w
-    tips = 2 * N * C if pb.tip_partials is None else 2 * N * C * Sp * w
+    tips = 2 * N * C if not pb.has_partials else 2 * N * C * Sp * w
     return {"b_min": 5 * (N - 2) * V + tips + 8 * (N - 1) * C,
             "schedule": 2 * (N - 2) * V + tips + 8 * C,
             "paper": (10 * N - 13) * V}
@@ -168,7 +168,7 @@ def flop_counts(pb, C: int) -> dict:
     """f_min = 3 (N-2) 2 S^2 R C (unpadded S); paper-literal
     (6N - 8) 2 Sp^2 R C."""
     N, S, R = pb.n_tips, pb.states, len(pb.cat_rates)
-    Sp = 64 if S <= 64 else 128
+    Sp = 64 if S <= 64 else 128 if S <= 128 else 256
     return {"f_min": 3 * (N - 2) * 2 * S * S * R * C, "paper": (6 * N - 8) * 2 * Sp * Sp * R * C}
 
 
@@ -242,12 +242,13 @@ def roofline(pb, C: int, variant: int, precision: str, kms: dict, peaks: dict, t
     as timed per step)."""
     t = kms["traverse"] * 1e-3
     ev = eval_ms * 1e-3
-    if variant == 2 or variant == 1:
+    if variant in (1, 2, 3):
         fl = flop_counts(pb, C)
         hb = hbm_counts(pb, C, precision)
-        if variant == 2:
+        if variant >= 2:
             pk, unit, bound, src = peaks["fp64_tflops"], "TFLOP/s", "tensor", peaks["fp64_src"]
-            kname = ("codon_flow_kernel (post + pre order, one launch)" if flow
+            kname = ("big_post_kernel + big_pre_kernel (S = 256 class, transpose-free, all levels)" if variant == 3
+                     else "codon_flow2_kernel (post + pre order, one launch, TMA ring)" if flow
                      else "codon_post_kernel + codon_pre_kernel (all levels of one evaluation)")
         else:
             pk, src = ((peaks["dfma_tflops"], peaks["dfma_src"]) if precision == "fp64"

@@ -350,12 +350,12 @@ def from_problem(pb, precision: Optional[str] = None, device: int = 0, stream=No
     """Instance loaded with a phylo_synth.Problem (optionally a pattern shard)."""
     hi = pb.patterns if hi is None else hi
     C = hi - lo
-    part = pb.tip_partials is not None
+    part = pb.has_partials
     inst = Instance(pb.n_tips, C, pb.states, len(pb.cat_rates),
                     precision=precision or pb.precision, device=device, tip_partials=part, stream=stream)
     for n in range(pb.n_tips):
         if part:
-            inst.set_tip_partials(n, pb.tip_partials[n, lo:hi])
+            inst.set_tip_partials(n, pb.tip_partial_rows(n, lo, hi))
         else:
             inst.set_tip_states(n, pb.tip_states[n, lo:hi])
     inst.set_pattern_weights(pb.pattern_weights[lo:hi])

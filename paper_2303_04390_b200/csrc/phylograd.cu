@@ -24,6 +24,7 @@
 #include "schedule.hpp"
 #include "traverse_codon.cuh"
 #include "traverse_codon2.cuh"
+#include "traverse_big.cuh"
 #include "traverse_large.cuh"
 #include "traverse_small.cuh"
 
@@ -42,7 +43,7 @@ struct Layout {
         off_bl, off_patw, off_tips, off_tipp, off_u, off_gpart, off_lpart, off_out, off_status,
         off_post, off_pre, total;
     // codon (variant 2) extras
-    size_t off_PBpre = 0, off_DT = 0, off_PONE = 0, off_QB = 0, off_q = 0, off_E = 0, off_child = 0,
+    size_t off_M0one = 0, off_PBpre = 0, off_DT = 0, off_PONE = 0, off_QB = 0, off_q = 0, off_E = 0, off_child = 0,
            off_levels = 0, off_lev4 = 0, off_tipmode = 0, off_utip = 0, off_tipmask = 0, off_tipmasked = 0, off_VA = 0, off_ViB = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0,
            off_flow = 0, flow_bytes = 0, reset_bytes = 0;
     // time-tree parameterisation: parent/child_a/child_b [3][2N-1], heights, rate scalars, branch sets
@@ -56,6 +57,7 @@ int padded_states(int S) {
     if (S <= 32) return 32;
     if (S <= 64) return 64;
     if (S <= 128) return 128;          // S = 122: MMM of two codon models (NEXT-2)
+    if (S <= 256) return 256;          // S = 256 class (NEXT-2): fp64 only
     return 0;
 }
 
@@ -70,15 +72,17 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         return PG_ERR_ARG;
     }
     int SP = padded_states(c->states);
-    if (!SP) { if (err) *err = "states > 128 are not supported by this build"; return PG_ERR_UNSUPPORTED; }
-    // fp64 with S > 16: FP64 tensor-core path, states padded to 64 (codon) or
-    // 128 (S = 122, two-class codon MMM); fp32 S > 16: SIMT large-state kernel
+    if (!SP) { if (err) *err = "states > 256 are not supported by this build"; return PG_ERR_UNSUPPORTED; }
+    // fp64 with S > 16: FP64 tensor-core path, states padded to 64 (codon),
+    // 128 (S = 122, two-class codon MMM) or 256 (transpose-free level kernels,
+    // traverse_big.cuh); fp32 S > 16: SIMT large-state kernel (S <= 128)
     const bool codon = SP > 16 && c->precision == PG_FP64;
-    if (codon) SP = SP <= 64 ? 64 : 128;
+    if (codon) SP = SP <= 64 ? 64 : SP <= 128 ? 128 : 256;
+    if (SP == 256 && !codon) { if (err) *err = "states > 128 need PG_FP64"; return PG_ERR_UNSUPPORTED; }
     if (c->states > 254) { if (err) *err = "states > 254"; return PG_ERR_UNSUPPORTED; }
     const int R = c->categories;
     L->SP = SP;
-    L->variant = SP <= 16 ? 0 : (codon ? 2 : 1);
+    L->variant = SP <= 16 ? 0 : (codon ? (SP == 256 ? 3 : 2) : 1);
     L->real = c->precision == PG_FP64 ? 8 : 4;
     if (L->variant == 0) {
         if (R > (SP == 16 ? 8 : 16)) {
@@ -88,7 +92,7 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         int Rp = 1;
         while (Rp < R) Rp <<= 1;
         L->tpl = 32 / (Rp * pg::small_lanes_per_vector(SP, Rp));   // patterns per warp tile (lane = pattern x category x state group)
-    } else if (L->variant == 2) {
+    } else if (L->variant >= 2) {
         if (R > 16) { if (err) *err = "too many rate categories (max 16)"; return PG_ERR_UNSUPPORTED; }
         L->tpl = pg::codon::T;
     } else {
@@ -113,14 +117,17 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t at = o; o = align_up(o + bytes); return at; };
     L->off_P = take(mats);
-    L->off_PT = take(L->variant >= 1 ? (size_t)L->B * R * SP * SP * L->real : 0);
-    if (L->variant == 2) {
-        L->off_PBpre = take(mats);
-        L->off_DT = take(mats);
+    // variant 3 keeps ONE matrix per (branch, category), W = P' in off_P
+    // (transpose-free, traverse_big.cuh); variants 1-2 keep P' beside it
+    L->off_PT = take((L->variant == 1 || L->variant == 2) ? (size_t)L->B * R * SP * SP * L->real : 0);
+    if (L->variant >= 2) {
+        L->off_PBpre = take(L->variant == 2 ? mats : 0);
+        L->off_DT = take(L->variant == 2 ? mats : 0);
         L->off_PONE = take((size_t)L->B * R * SP * 8);
-        L->off_QB = take((size_t)SP * SP * 8);
-        L->off_VA = take((size_t)SP * SP * 8);
-        L->off_ViB = take((size_t)SP * SP * 8);
+        L->off_QB = take((size_t)SP * SP * 8);      // variant 3: Q row-major
+        L->off_VA = take((size_t)SP * SP * 8);      // variant 3: (V^-1)' as A fragments
+        L->off_ViB = take((size_t)SP * SP * 8);     // variant 3: V' as B fragments
+        L->off_M0one = take((size_t)SP * 8 * 2);    // variant 3: M0 1 and V^-1 1
     }
     L->off_M0 = take((size_t)SP * SP * 8);     // V V^-1 (A1's identity term, host long double)
     L->off_Q = take((size_t)std::max(SP * SP, 32) * L->real);   // (S = 4 tensor-core variant: 32 fragment values)
@@ -134,7 +141,8 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
     L->off_bl = take((size_t)L->B * 8);
     L->off_patw = take((size_t)L->Cpad * 8);
     L->off_tips = take((size_t)N * L->Cpad);
-    L->off_tipp = take((c->flags & PG_FLAG_TIP_PARTIALS) ? (size_t)N * L->Cpad * SP * L->real : 0);
+    // (variant 3 takes partial tips only as 0/1 masks: no dense copy)
+    L->off_tipp = take((c->flags & PG_FLAG_TIP_PARTIALS) && L->variant != 3 ? (size_t)N * L->Cpad * SP * L->real : 0);
     L->off_u = take((size_t)(N - 2) * R * L->Cpad * SP * L->real);
     L->off_gpart = take((size_t)L->B * L->n_tiles * 8);
     L->off_lpart = take((size_t)L->n_tiles * 8);
@@ -146,7 +154,7 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
     L->off_h = take((size_t)(2 * N - 1) * 8);
     L->off_rho = take((size_t)(2 * N - 2) * 8);
     L->off_bset = take((size_t)(2 * N - 2) * 4);     // zeroed at create: one set (strict clock)
-    if (L->variant == 2) {
+    if (L->variant >= 2) {
         L->off_q = take((size_t)(N - 2) * R * L->Cpad * SP * 8);
         // u = P p of partial tips (formed once per evaluation by codon_tipu_kernel)
         L->off_utip = take((c->flags & PG_FLAG_TIP_PARTIALS) ? (size_t)N * R * L->Cpad * SP * 8 : 0);
@@ -424,9 +432,9 @@ int pg_set_tip_partials(pg_instance *inst, int32_t tip, const double *partials) 
     for (size_t i = 0; i < (size_t)c.patterns * S; ++i)
         if (!(partials[i] >= 0.0) || !std::isfinite(partials[i]))
             return inst->fail(PG_ERR_DOMAIN, "tip partials must be finite and >= 0");
-    std::vector<double> v((size_t)Cp * SP, 0.0);
+    std::vector<double> v(inst->L.variant == 3 ? 0 : (size_t)Cp * SP, 0.0);
     const int KT = SP / 4;
-    for (int p = 0; p < Cp; ++p)
+    for (int p = 0; p < (inst->L.variant == 3 ? 0 : Cp); ++p)
         for (int s = 0; s < S; ++s) {
             const double x = p < c.patterns ? partials[(size_t)p * S + s] : 1.0;
             if (inst->L.variant == 2) {      // 32-pattern tiles in A-fragment order (codon_tipu_kernel)
@@ -436,9 +444,9 @@ int pg_set_tip_partials(pg_instance *inst, int32_t tip, const double *partials) 
                 v[(size_t)p * SP + s] = x;
             }
         }
-    int rc = upload_real(inst, inst->L.off_tipp + (size_t)tip * Cp * SP * inst->L.real, v);
+    int rc = inst->L.variant == 3 ? PG_OK : upload_real(inst, inst->L.off_tipp + (size_t)tip * Cp * SP * inst->L.real, v);
     if (rc) return rc;
-    if (inst->L.variant == 2) {
+    if (inst->L.variant >= 2) {
         // a 0/1 mask with 1..4 ones per pattern (e.g. the hidden copies of an
         // observed state): keep the state list so u = P p is a sum of <= 4
         // columns of P instead of a GEMM (codon_tipu_kernel)
@@ -463,6 +471,8 @@ int pg_set_tip_partials(pg_instance *inst, int32_t tip, const double *partials) 
                                cudaMemcpyHostToDevice, inst->stream), "tip mask upload");
             CK(cudaStreamSynchronize(inst->stream), "tip mask sync");
         }
+        if (!masked && inst->L.variant == 3)
+            return inst->fail(PG_ERR_UNSUPPORTED, "S > 128: tip partials must be 0/1 masks with 1..4 ones per pattern");
         if (inst->tip_masked[tip] != (uint8_t)masked) {
             inst->tip_masked[tip] = (uint8_t)masked;
             inst->partial_modes_dirty = true;
@@ -547,6 +557,27 @@ int pg_set_eigen(pg_instance *inst, const double *evec, const double *ievec, con
         return rc;
     }
     if ((rc = upload_real(inst, inst->L.off_QT, QT))) return rc;
+    if (inst->L.variant == 3) {      // traverse_big.cuh: Q row-major; A1 operands in fragment order
+        const int KT = SP / 4;
+        std::vector<double> ViTA((size_t)SP * SP, 0.0), VTB((size_t)SP * SP, 0.0), ones(2 * (size_t)SP, 0.0);
+        for (int idx = 0; idx < SP * SP; ++idx) {
+            const int lane = idx & 31, kt = (idx >> 5) & (KT - 1), mt = idx / (32 * KT);
+            const int t = mt * 8 + (lane >> 2), k = kt * 4 + (lane & 3);          // A[t][k] = V^-1[k][t]
+            ViTA[idx] = (t < S && k < S) ? ievec[(size_t)k * S + t] : 0.0;
+            const int sn = mt * 8 + (lane >> 2);                                  // B[k][s] = V[s][k] (nt = mt)
+            VTB[idx] = (sn < S && k < S) ? evec[(size_t)sn * S + k] : 0.0;
+        }
+        for (int r0 = 0; r0 < S; ++r0) {
+            long double a = 0.0L, b = 0.0L;
+            for (int t = 0; t < S; ++t) { a += M0[(size_t)r0 * SP + t]; b += ievec[(size_t)r0 * S + t]; }
+            ones[r0] = (double)a;            // M0 1
+            ones[SP + r0] = (double)b;       // V^-1 1
+        }
+        if ((rc = upload_doubles(inst, inst->L.off_QB, Q.data(), Q.size()))) return rc;
+        if ((rc = upload_doubles(inst, inst->L.off_VA, ViTA.data(), ViTA.size()))) return rc;
+        if ((rc = upload_doubles(inst, inst->L.off_ViB, VTB.data(), VTB.size()))) return rc;
+        if ((rc = upload_doubles(inst, inst->L.off_M0one, ones.data(), ones.size()))) return rc;
+    }
     if (inst->L.variant == 2) {      // Q as the fragment-ordered B operand of Qu = u Q'
         std::vector<double> QB((size_t)SP * SP);
         const int KT = SP / 4;           // B fragments: [nt SP/8][kt SP/4][lane 32]
@@ -922,6 +953,16 @@ static int configure(pg_instance *inst) {
             inst->prog_smem_off = off;
             inst->smem = off + prog_bytes;
         }
+    } else if (L.variant == 3) {
+        inst->block = pg::big::NTB;
+        inst->prefetch = 0;
+        inst->flow_tch = 0;                    // level-by-level launches
+        inst->smem = (int)pg::big::pre_smem();
+        CK(cudaFuncSetAttribute((void *)pg::big::big_post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pg::big::post_smem()), "smem attr");
+        CK(cudaFuncSetAttribute((void *)pg::big::big_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pg::big::pre_smem()), "smem attr");
+        return PG_OK;
     } else if (L.variant == 2) {
         const CodonFns cf = codon_fns(L.SP);
         inst->block = cf.threads;
@@ -1011,7 +1052,7 @@ static int refresh_plan(pg_instance *inst) {
                        cudaMemcpyHostToDevice, inst->stream), "plan upload");
     CK(cudaMemcpyAsync(inst->ws + inst->L.off_pre, inst->plan.pre.data(), sizeof(Op4) * (N - 1),
                        cudaMemcpyHostToDevice, inst->stream), "plan upload");
-    if (inst->L.variant == 2) {
+    if (inst->L.variant >= 2) {
         std::vector<int32_t> ch(2 * (2 * N - 1));
         for (int v = 0; v < 2 * N - 1; ++v) { ch[v] = inst->plan.child_a[v]; ch[2 * N - 1 + v] = inst->plan.child_b[v]; }
         CK(cudaMemcpyAsync(inst->ws + inst->L.off_child, ch.data(), ch.size() * 4, cudaMemcpyHostToDevice, inst->stream),
@@ -1085,7 +1126,7 @@ static pg::codon::CodonArgs codon_args(pg_instance *inst) {
     c.lev4 = reinterpret_cast<const int4 *>(inst->ws + L.off_lev4);
     c.PBpost = inst->at<double>(L.off_P);
     c.PBpre = inst->at<double>(L.off_PBpre);
-    c.PT = inst->at<double>(L.off_PT);
+    c.PT = inst->at<double>(L.variant == 3 ? L.off_P : L.off_PT);     // variant 3: W = P' (the only copy)
     c.DT = inst->at<double>(L.off_DT);
     c.PONE = inst->at<double>(L.off_PONE);
     c.QB = inst->at<double>(L.off_QB);
@@ -1129,7 +1170,23 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
                  *lam = inst->at<double>(L.off_lam), *rates = inst->at<double>(L.off_rates),
                  *bl = inst->at<double>(L.off_bl);
     int S = inst->cfg.states;
-    if (L.variant == 2) {
+    if (L.variant == 3) {
+        // A1: W = P' per (branch, category), 8 row blocks each; masked tips' u
+        CK(cudaMemsetAsync(inst->ws + L.off_fmax, 0, L.reset_bytes, inst->stream), "fmax/counters reset");
+        const double *ViTA = inst->at<double>(L.off_VA), *VTB = inst->at<double>(L.off_ViB);
+        const double *M0 = inst->at<double>(L.off_M0), *M0one = inst->at<double>(L.off_M0one),
+                     *Vione = M0one + L.SP;
+        double *W = inst->at<double>(L.off_P), *PONE = inst->at<double>(L.off_PONE);
+        void *args[] = {&ViTA, &VTB, &M0, &M0one, &V, &Vione, &lam, &rates, &bl, &S, (void *)&R, &W, &PONE};
+        CK(cudaLaunchKernel((void *)pg::big::big_pmat_kernel, dim3(L.B * R, 8), dim3(256), args, 0, inst->stream),
+           "big pmat launch");
+        if (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) {
+            pg::codon::CodonArgs c = codon_args(inst);
+            void *targs[] = {&c};
+            CK(cudaLaunchKernel((void *)pg::big::big_tipmask_kernel, dim3(L.n_tiles, inst->cfg.tips, R), dim3(256),
+                                targs, 0, inst->stream), "big tip-mask launch");
+        }
+    } else if (L.variant == 2) {
         double *PBpost = inst->at<double>(L.off_P), *PBpre = inst->at<double>(L.off_PBpre),
                *PT = inst->at<double>(L.off_PT), *DT = inst->at<double>(L.off_DT), *PONE = inst->at<double>(L.off_PONE);
         const double *VA = inst->at<double>(L.off_VA), *ViB = inst->at<double>(L.off_ViB);
@@ -1172,7 +1229,22 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         }
     }
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[1], inst->stream, cudaEventRecordExternal), "event");
-    if (L.variant == 2) {
+    if (L.variant == 3) {
+        pg::codon::CodonArgs c = codon_args(inst);
+        const auto &pl = inst->plan;
+        for (size_t i = 0; i + 1 < pl.post_off.size(); ++i) {
+            int off = pl.post_off[i], cnt = pl.post_off[i + 1] - off;
+            void *args[] = {&c, &off};
+            CK(cudaLaunchKernel((void *)pg::big::big_post_kernel, dim3(L.n_tiles, cnt, R), dim3(pg::big::NTB), args,
+                                pg::big::post_smem(), inst->stream), "big post launch");
+        }
+        for (size_t i = 0; i + 1 < pl.pre_off.size(); ++i) {
+            int off = pl.pre_off[i], cnt = pl.pre_off[i + 1] - off;
+            void *args[] = {&c, &off};
+            CK(cudaLaunchKernel((void *)pg::big::big_pre_kernel, dim3(L.n_tiles, cnt, R), dim3(pg::big::NTB), args,
+                                pg::big::pre_smem(), inst->stream), "big pre launch");
+        }
+    } else if (L.variant == 2) {
         pg::codon::CodonArgs c = codon_args(inst);
         const CodonFns cf = codon_fns(L.SP);
         const auto &pl = inst->plan;
@@ -1246,7 +1318,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
            "traverse launch");
     }
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[2], inst->stream, cudaEventRecordExternal), "event");
-    if (L.variant == 2) {
+    if (L.variant >= 2) {
         pg::codon::CodonArgs c = codon_args(inst);
         int *cnt = inst->at<int>(L.off_flow) + 32 + (size_t)2 * (inst->cfg.tips - 1) * L.n_tiles + (size_t)L.B * R;
         double *sp = inst->at<double>(L.off_gpart);      // [B+1][slices] <= [B][n_tiles] + [n_tiles] (codon path)
@@ -1468,7 +1540,10 @@ extern "C" int pg_trace_copy(pg_instance *inst, long long *host, int n) {
 int pg_kernels_per_eval(const pg_instance *inst, int32_t *n) {
     if (!inst || !n) return PG_ERR_ARG;
     *n = 3;   // pmat, traverse, reduce
-    if (inst->L.variant == 2)   // pmat + (one flow launch | one launch per post level + per pre level) + reduce
+    if (inst->L.variant == 3)   // pmat + [masked tips] + one launch per post level + per pre level + ratio
+        *n = 2 + ((inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? 1 : 0) + (int32_t)(inst->plan.post_off.size() - 1) +
+             (int32_t)(inst->plan.pre_off.size() - 1);
+    else if (inst->L.variant == 2)   // pmat + (one flow launch | one launch per post level + per pre level) + reduce
         *n = 2 + ((inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? 2 : 0) +
              (inst->flow_tch > 0 ? 1 : (int32_t)(inst->plan.post_off.size() - 1) + (int32_t)(inst->plan.pre_off.size() - 1));
     return PG_OK;

@@ -344,10 +344,43 @@ class Problem:
     precision: str = "fp64"
     rate_scalars: Optional[np.ndarray] = None  # relaxed clock rho [2N-2]
     branch_times: Optional[np.ndarray] = None  # tau [2N-2]
+    # Markov-modulated models with the hidden class unobserved at the tips:
+    # tip (n, c) is the 0/1 mask with ones on the mask_K hidden copies
+    # mask_K * obs + k of the observed base state obs = tip_obs[n, c]
+    # (kept implicit: a dense [N, C, S] array is ~5 GB at S = 244, N = 10^4)
+    tip_obs: Optional[np.ndarray] = None       # int32 [N, C]
+    mask_K: int = 0
 
     @property
     def patterns(self) -> int:
         return int(self.pattern_weights.shape[0])
+
+    @property
+    def has_partials(self) -> bool:
+        return self.tip_partials is not None or self.mask_K > 0
+
+    def tip_partial_rows(self, n: int, lo: int = 0, hi: Optional[int] = None) -> np.ndarray:
+        """Dense partials [hi-lo, S] of tip n (explicit, or the hidden-copy mask)."""
+        hi = self.patterns if hi is None else hi
+        if self.tip_partials is not None:
+            return self.tip_partials[n, lo:hi]
+        obs = self.tip_obs[n, lo:hi]
+        part = np.zeros((hi - lo, self.states))
+        for k in range(self.mask_K):
+            part[np.arange(hi - lo), obs * self.mask_K + k] = 1.0
+        return part
+
+    def subset(self, lo: int, hi: int) -> "Problem":
+        """The same tree and model on patterns [lo, hi), tips materialised
+        (explicit partials for mask problems: oracle input)."""
+        import dataclasses
+        kw = dict(pattern_weights=self.pattern_weights[lo:hi].copy(), name=f"{self.name}_p{lo}_{hi}")
+        if self.has_partials:
+            kw.update(tip_partials=np.stack([self.tip_partial_rows(n, lo, hi) for n in range(self.n_tips)]),
+                      tip_states=None, tip_obs=None, mask_K=0)
+        else:
+            kw.update(tip_states=self.tip_states[:, lo:hi].copy())
+        return dataclasses.replace(self, **kw)
 
     @property
     def categories(self) -> int:
@@ -366,6 +399,8 @@ class Problem:
         """[N, C, S] partials; a state code S (missing) becomes all-ones."""
         if self.tip_partials is not None:
             return self.tip_partials
+        if self.mask_K > 0:
+            return np.stack([self.tip_partial_rows(n) for n in range(self.n_tips)])
         N, C, S = self.n_tips, self.patterns, self.states
         out = np.zeros((N, C, S))
         st = self.tip_states
@@ -535,6 +570,26 @@ def config5_yeast_mmm(N: int = 49, C: int = 4_000, precision: str = "fp64",
                    tip_partials=part, precision=precision)
 
 
+def config6_codon_mmm4(N: int = 10_001, C: int = 256, precision: str = "fp64",
+                       seed: Optional[int] = None) -> Problem:
+    """SURVEY §8(f) NEXT-2, the S = 256 class with over 20,000 branch lengths
+    (P:1022-1024): a Markov-modulated model of four GY94 codon classes (4 x 61
+    = 244 states, padded to 256) on a 10,001-tip Kingman tree (20,000
+    branches); the hidden class is unobserved at the tips (0/1 masks on the 4
+    copies of the observed codon, kept implicit: `tip_obs`, `mask_K`)."""
+    rng = np.random.default_rng(MASTER_SEED + 6 if seed is None else seed)
+    tree = coalescent_tree(N, rng, root_height=1.0)
+    pib = _codon_freqs(rng)
+    K = 4
+    Q, pi = markov_modulated(gy94(2.5, 0.1, pib), pib, np.array([0.25, 0.75, 1.25, 1.75]), 0.5)
+    rates, cw = np.ones(1), np.ones(1)
+    hidden = _simulate_until(tree, Q, pi, rates, cw, C, rng, start=int(1.2 * C),
+                             project=lambda a: a // K)
+    pats, w = compress_patterns(hidden // K, C)
+    return _finish(f"codonmmm4_{N}", tree, Q, pi, rates, cw, pats, w, 61 * K,
+                   tip_obs=pats.astype(np.int32), mask_K=K, precision=precision)
+
+
 CONFIGS = {
     0: config0_jc5,
     1: config1_dengue,
@@ -542,6 +597,7 @@ CONFIGS = {
     3: config3_yeast,
     4: config4_wnv,
     5: config5_yeast_mmm,
+    6: config6_codon_mmm4,
 }
 
 
@@ -576,7 +632,7 @@ def subset_patterns(pb: Problem, lo: int, hi: int) -> Problem:
 def small_problem(N: int = 5, model: str = "hky", R: int = 1, C: int = 7,
                   seed: int = 0, missing: float = 0.0, partial_tips: bool = False,
                   root_height: float = 0.5, stationary_root: bool = True,
-                  simulate: bool = False) -> Problem:
+                  simulate: bool = False, hidden_masks: int = 0) -> Problem:
     """Small random instance for pins and parity tests.
 
     model: 'jc' | 'hky' | 'gtr' | 'mmm2' (S=8) | 'mmm4' (S=16) | 'codon' (S=61)
@@ -600,6 +656,9 @@ def small_problem(N: int = 5, model: str = "hky", R: int = 1, C: int = 7,
     elif model == "codon2":                   # 2-class codon MMM, S = 122
         pib = _codon_freqs(rng)
         Q, pi = markov_modulated(gy94(2.5, 0.2, pib), pib, np.array([0.4, 1.6]), 0.5)
+    elif model == "codon4":                   # 4-class codon MMM, S = 244 (padded to 256)
+        pib = _codon_freqs(rng)
+        Q, pi = markov_modulated(gy94(2.5, 0.2, pib), pib, np.array([0.25, 0.75, 1.25, 1.75]), 0.5)
     else:
         raise ValueError(model)
     S = Q.shape[0]
@@ -618,7 +677,14 @@ def small_problem(N: int = 5, model: str = "hky", R: int = 1, C: int = 7,
     root_pi = pi if stationary_root else rng.dirichlet(np.full(S, 2.0))
     V, Vi, lam = eigen_reversible(Q, pi)
     kw = dict(tip_states=states)
-    if partial_tips:
+    if hidden_masks:                          # MMM: 0/1 masks on the K hidden copies of an observed state
+        K = hidden_masks
+        obs = np.minimum(states, S - 1) // K
+        part = np.zeros((N, C, S))
+        for k in range(K):
+            part[np.arange(N)[:, None], np.arange(C)[None, :], obs * K + k] = 1.0
+        kw = dict(tip_partials=part)
+    elif partial_tips:
         part = (rng.random((N, C, S)) < 0.4).astype(np.float64)
         part[np.arange(N)[:, None], np.arange(C)[None, :], states % S] = 1.0
         kw = dict(tip_partials=part)

@@ -76,10 +76,29 @@ def test_workspace_bytes(pg):
     # S = 122 (two-class codon MMM) pads to 128 on the large-state kernel
     b122 = pg.workspace_bytes(49, 4000, 122, 1)
     assert (49 - 2) * 4000 * 128 * 8 < b122
-    for S, R, prec in ((129, 1, "fp64"), (122, 9, "fp32"), (122, 17, "fp64")):
+    for S, R, prec in ((129, 1, "fp32"), (255, 1, "fp64"), (122, 9, "fp32"), (122, 17, "fp64")):
         with pytest.raises(pg.PhyloGradError) as ei:
             pg.workspace_bytes(10, 10, S, R, prec)
         assert ei.value.code == pg.PG_ERR_UNSUPPORTED
+
+
+def test_s256_workspace_fits_without_stored_transposes(pg):
+    """NEXT-2: 244 states padded to 256, 10,001 tips = 20,000
+    branches.  The paper keeps P and its transpose for every branch (~10 GB of
+    transposes alone); this build keeps ONE matrix per (branch, category),
+    W = P' (traverse_big.cuh), so the matrices take B R 256^2 8 bytes once."""
+    N, C, S = 10_001, 256, 244
+    B, SP = 2 * N - 2, 256
+    one_copy = B * SP * SP * 8                          # 10.5 GB
+    for R in (1, 2):
+        ws = pg.workspace_bytes(N, C, S, R, "fp64", tip_partials=True)
+        mats = R * one_copy
+        # u, q (N-2 internal nodes) and u of the partial tips, [R][C][256] each
+        vecs = (2 * (N - 2) + N) * R * C * SP * 8
+        assert ws >= mats + vecs
+        assert ws < mats + vecs + R * one_copy // 4     # no second matrix layout
+        assert ws < 180e9 / 2                           # fits a B200 with room to spare
+
 
 
 def test_shard_range_covers_patterns(pg):

@@ -42,7 +42,7 @@ def test_jc69_transition_closed_form():
         assert np.max(np.abs(P - ref)) < 2e-14   # eigh rounding ~ S * eps
 
 
-@pytest.mark.parametrize("model", ["hky", "gtr", "mmm4", "codon"])
+@pytest.mark.parametrize("model", ["hky", "gtr", "mmm4", "codon", "codon4"])
 def test_transition_matches_pade_expm(model):
     pb = ps.small_problem(4, model, seed=3)
     for t in (1e-4, 0.1, 1.0, 10.0):
@@ -114,7 +114,7 @@ def test_all_missing_pattern_has_unit_likelihood():
 # ------------------------------------------------------- brute force ----
 
 BRUTE = [("jc", 3, 1), ("hky", 4, 2), ("gtr", 5, 4), ("hky", 6, 2), ("mmm2", 4, 2),
-         ("mmm4", 4, 1), ("codon", 3, 2), ("codon2", 3, 1)]
+         ("mmm4", 4, 1), ("codon", 3, 2), ("codon2", 3, 1), ("codon4", 3, 1)]
 
 
 @pytest.mark.parametrize("model,N,R", BRUTE)
@@ -132,6 +132,27 @@ def test_brute_force_loglik_and_gradient(model, N, R):
     assert np.all(np.abs(gq - gb) <= 1e-11 * scale + 1e-14)
 
 
+def test_brute_force_hidden_class_masks_s244():
+    """S = 244 (four-class codon MMM, NEXT-2) with the hidden class unobserved:
+    tips are 0/1 masks on the 4 copies of the observed codon."""
+    pb = ps.small_problem(3, "codon4", R=1, C=3, seed=8, simulate=True, hidden_masks=4)
+    lb, gb = bruteforce.loglik_grad(pb)
+    r = oracle.loglik_grad(pb)
+    assert abs(r["logL"] - lb) <= 1e-12 * abs(lb)
+    assert np.all(np.abs(r["grad"] - gb) <= 1e-11 * np.maximum(np.abs(gb), r["grad_abs"]))
+
+
+def test_mask_problem_subset_is_explicit():
+    """The implicit hidden-copy masks of config 6 equal explicit partials."""
+    pb = ps.config6_codon_mmm4(N=20, C=12)
+    sub = pb.subset(2, 7)
+    assert sub.tip_partials.shape == (20, 5, 244)
+    assert np.all(sub.tip_partials.sum(axis=2) == 4)
+    obs = pb.tip_obs[:, 2:7]
+    for k in range(4):
+        assert np.all(sub.tip_partials[np.arange(20)[:, None], np.arange(5)[None, :], 4 * obs + k] == 1.0)
+
+
 def test_brute_force_tip_partials_and_nonstationary_root():
     pb = ps.small_problem(5, "mmm2", R=2, C=4, seed=11, partial_tips=True,
                           stationary_root=False)
@@ -143,7 +164,8 @@ def test_brute_force_tip_partials_and_nonstationary_root():
 
 # ---------------------------------------------------- invariants ----
 
-@pytest.mark.parametrize("model,N,R", [("hky", 12, 4), ("mmm4", 9, 1), ("codon", 7, 2), ("codon2", 6, 2)])
+@pytest.mark.parametrize("model,N,R", [("hky", 12, 4), ("mmm4", 9, 1), ("codon", 7, 2), ("codon2", 6, 2),
+                                       ("codon4", 6, 1)])
 def test_node_invariance_eq5(model, N, R):
     """sum_r P(gamma_r) p_i'q_i = L_c at every node (Eq. 5)."""
     pb = ps.small_problem(N, model, R=R, C=9, seed=4, missing=0.1)
@@ -153,7 +175,7 @@ def test_node_invariance_eq5(model, N, R):
 
 
 @pytest.mark.parametrize("model,N,R", [("hky", 16, 4), ("gtr", 32, 2), ("mmm4", 8, 2),
-                                       ("codon", 8, 2), ("codon2", 6, 1), ("hky", 64, 1)])
+                                       ("codon", 8, 2), ("codon2", 6, 1), ("hky", 64, 1), ("codon4", 6, 2)])
 def test_quadratic_reprune_matches_eq8(model, N, R):
     pb = ps.small_problem(N, model, R=R, C=6, seed=N, missing=0.05, simulate=True)
     r = oracle.loglik_grad(pb)
