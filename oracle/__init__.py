@@ -78,14 +78,16 @@ class _Bound:
     """A Problem marshalled into C arrays (kept alive with the struct)."""
 
     def __init__(self, pb):
+        # implicit hidden-copy masks (phylo_synth config 6) as explicit partials
+        tp = pb.tip_partials_dense() if getattr(pb, "mask_K", 0) else pb.tip_partials
         self.arrs = dict(
             ops=_c(pb.ops, np.int32), bl=_c(pb.branch_lengths, np.float64),
             V=_c(pb.evec, np.float64), Vi=_c(pb.ievec, np.float64),
             lam=_c(pb.evals, np.float64), pi=_c(pb.pi, np.float64),
             g=_c(pb.cat_rates, np.float64), cw=_c(pb.cat_weights, np.float64),
             w=_c(pb.pattern_weights, np.float64),
-            ts=_c(pb.tip_states, np.int32) if pb.tip_partials is None else None,
-            tp=_c(pb.tip_partials, np.float64))
+            ts=_c(pb.tip_states, np.int32) if tp is None else None,
+            tp=_c(tp, np.float64))
         a = self.arrs
         self.S = int(pb.states)
         self.N = int(pb.n_tips)
