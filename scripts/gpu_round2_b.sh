@@ -1,0 +1,18 @@
+#!/bin/bash
+# consolidated evidence: all GPU tests (+ parity log), smoke, default bench,
+# ncu launch list of the default bench, ncu --set full of the top kernels
+set -u
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out/r2b
+O=gpurun_out/r2b
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/gpu.txt
+PG_PARITY_LOG=$O/parity.jsonl timeout 2400 python -m pytest tests -m gpu -q -rf > $O/gpu_tests.log 2>&1
+echo "tests exit $?" >> $O/gpu_tests.log; tail -3 $O/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
+timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo "bench exit $?" >> $O/bench_default.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 200 -c 60 --csv --log-file $O/launches_dengue.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-fp64-probe --no-extra-configs > /dev/null 2>&1
+for cfg in 3 2; do
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 100 -c 60 --csv --log-file $O/launches_c$cfg.csv python bench.py --config $cfg --steps 20 --warmup 3 --no-cpu-baseline --no-fp64-probe > /dev/null 2>&1
+done
+CFGS="1 2" bash scripts/gpu_ncu_small.sh > $O/ncu_small.out 2>&1
+bash scripts/gpu_ncu_flow.sh > $O/ncu_flow.out 2>&1
