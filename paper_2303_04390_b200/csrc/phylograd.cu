@@ -25,6 +25,7 @@
 #include "traverse_codon.cuh"
 #include "traverse_codon2.cuh"
 #include "traverse_big.cuh"
+#include "traverse_tc.cuh"
 #include "traverse_large.cuh"
 #include "traverse_small.cuh"
 
@@ -83,6 +84,13 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
     const int R = c->categories;
     L->SP = SP;
     L->variant = SP <= 16 ? 0 : (codon ? (SP == 256 ? 3 : 2) : 1);
+    // fp32, 16 < S <= 64, state tips: tcgen05 (kind::tf32, 3xTF32) level kernels
+    // (traverse_tc.cuh); PG_NO_TC=1 keeps the SIMT kernel
+    const char *ntc = getenv("PG_NO_TC");
+    if (L->variant == 1 && SP <= 64 && c->states > 16 && !(c->flags & PG_FLAG_TIP_PARTIALS) && !(ntc && atoi(ntc))) {
+        L->variant = 4;
+        L->SP = SP = 64;
+    }
     L->real = c->precision == PG_FP64 ? 8 : 4;
     if (L->variant == 0) {
         if (R > (SP == 16 ? 8 : 16)) {
@@ -94,7 +102,7 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         L->tpl = 32 / (Rp * pg::small_lanes_per_vector(SP, Rp));   // patterns per warp tile (lane = pattern x category x state group)
     } else if (L->variant >= 2) {
         if (R > 16) { if (err) *err = "too many rate categories (max 16)"; return PG_ERR_UNSUPPORTED; }
-        L->tpl = pg::codon::T;
+        L->tpl = L->variant == 4 ? pg::tcp::TM : pg::codon::T;
     } else {
         if (R > (SP == 128 ? 8 : 16)) {
             if (err) *err = "too many rate categories (max 16; 8 for S > 64)";
@@ -105,13 +113,15 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         if (SP == 128) L->tpl = (L->real == 8) ? pg::LargeCfg<double, 128>::tpl(R) : pg::LargeCfg<float, 128>::tpl(R);
     }
     const long long N = c->tips, C = c->patterns;
-    L->Cpad = (int)((C + 31) / 32 * 32);
+    L->Cpad = (int)((C + L->tpl - 1) / L->tpl * L->tpl);      // whole tiles (32; 128 for variant 4)
+    if (L->Cpad % 32) L->Cpad = (L->Cpad + 31) / 32 * 32;
     L->n_tiles = L->Cpad / L->tpl;
     L->B = (int)(2 * N - 2);
     // small-S kernels read P with a padded category stride (SmallCfg::CS); the
     // tensor-core S = 16 variant keeps a three-layout record per branch
     L->mma = L->variant == 0 && pg::small_tc(SP, R, (int)L->real);
     L->cat_stride = L->mma ? (SP == 16 ? pg::MMA_REC / 8 : 2 * pg::MMA4_SLOT / 8 / R)   // per category (x R = record)
+                  : L->variant == 4 ? (int)pg::tcp::BREC                                      // 4 TF32 B images
                            : SP * SP + ((L->variant == 0 && R > 1) ? pg::small_cat_pad(L->real, SP) / L->real : 0);
     const size_t mats = (size_t)L->B * R * L->cat_stride * L->real;
     size_t o = 0;
@@ -155,7 +165,7 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
     L->off_rho = take((size_t)(2 * N - 2) * 8);
     L->off_bset = take((size_t)(2 * N - 2) * 4);     // zeroed at create: one set (strict clock)
     if (L->variant >= 2) {
-        L->off_q = take((size_t)(N - 2) * R * L->Cpad * SP * 8);
+        L->off_q = take((size_t)(N - 2) * R * L->Cpad * SP * (L->variant == 4 ? 4 : 8));
         // u = P p of partial tips (formed once per evaluation by codon_tipu_kernel)
         L->off_utip = take((c->flags & PG_FLAG_TIP_PARTIALS) ? (size_t)N * R * L->Cpad * SP * 8 : 0);
         // 0/1 mask partials with <= 4 ones (MMM hidden states): state lists, u by gathers
@@ -557,6 +567,19 @@ int pg_set_eigen(pg_instance *inst, const double *evec, const double *ievec, con
         return rc;
     }
     if ((rc = upload_real(inst, inst->L.off_QT, QT))) return rc;
+    if (inst->L.variant == 4) {      // traverse_tc.cuh: Q' as the TF32 hi/lo B images of y = x Q
+        std::vector<float> BQ(2 * (size_t)SP * SP, 0.f);
+        for (int n = 0; n < SP; ++n)
+            for (int kk = 0; kk < SP; ++kk) {
+                const float v = (float)Q[(size_t)kk * SP + n], h = pg::tc::tf32_hi(v);   // image (n, k) = Q[k][n]
+                const uint32_t off = pg::tc::kmajor_off(n, kk, SP) / 4;
+                BQ[off] = h;
+                BQ[(size_t)SP * SP + off] = v - h;
+            }
+        CK(cudaMemcpyAsync(inst->ws + inst->L.off_QB, BQ.data(), BQ.size() * 4, cudaMemcpyHostToDevice, inst->stream),
+           "BQ upload");
+        CK(cudaStreamSynchronize(inst->stream), "BQ sync");
+    }
     if (inst->L.variant == 3) {      // traverse_big.cuh: Q row-major; A1 operands in fragment order
         const int KT = SP / 4;
         std::vector<double> ViTA((size_t)SP * SP, 0.0), VTB((size_t)SP * SP, 0.0), ones(2 * (size_t)SP, 0.0);
@@ -953,6 +976,16 @@ static int configure(pg_instance *inst) {
             inst->prog_smem_off = off;
             inst->smem = off + prog_bytes;
         }
+    } else if (L.variant == 4) {
+        inst->block = pg::tcp::TM;
+        inst->prefetch = 0;
+        inst->flow_tch = 0;
+        inst->smem = (int)pg::tcp::pre_smem();
+        CK(cudaFuncSetAttribute((void *)pg::tcp::tc_post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pg::tcp::post_smem()), "smem attr");
+        CK(cudaFuncSetAttribute((void *)pg::tcp::tc_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pg::tcp::pre_smem()), "smem attr");
+        return PG_OK;
     } else if (L.variant == 3) {
         inst->block = pg::big::NTB;
         inst->prefetch = 0;
@@ -1159,6 +1192,19 @@ static pg::codon::CodonArgs codon_args(pg_instance *inst) {
     return c;
 }
 
+static pg::tcp::TcArgs tc_args(pg_instance *inst) {
+    const Layout &L = inst->L;
+    pg::tcp::TcArgs t{};
+    t.c = codon_args(inst);
+    t.B = inst->at<float>(L.off_P);
+    t.BQ = inst->at<float>(L.off_QB);
+    t.ONE = inst->at<float>(L.off_PONE);
+    t.pi = inst->at<float>(L.off_pi);
+    t.u = inst->at<float>(L.off_u);
+    t.q = inst->at<float>(L.off_q);
+    return t;
+}
+
 // enqueue one evaluation (no host sync) writing [logL, g] to d_out
 static int enqueue_eval(pg_instance *inst, double *d_out) {
     const Layout &L = inst->L;
@@ -1170,7 +1216,14 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
                  *lam = inst->at<double>(L.off_lam), *rates = inst->at<double>(L.off_rates),
                  *bl = inst->at<double>(L.off_bl);
     int S = inst->cfg.states;
-    if (L.variant == 3) {
+    if (L.variant == 4) {
+        CK(cudaMemsetAsync(inst->ws + L.off_fmax, 0, L.reset_bytes, inst->stream), "fmax/counters reset");
+        const double *M0 = inst->at<double>(L.off_M0);
+        float *Bm = inst->at<float>(L.off_P), *ONE = inst->at<float>(L.off_PONE);
+        void *args[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, (void *)&R, &Bm, &ONE};
+        CK(cudaLaunchKernel((void *)pg::tcp::tc_pmat_kernel, dim3(L.B * R), dim3(256), args, 0, inst->stream),
+           "tc pmat launch");
+    } else if (L.variant == 3) {
         // A1: W = P' per (branch, category), 8 row blocks each; masked tips' u
         CK(cudaMemsetAsync(inst->ws + L.off_fmax, 0, L.reset_bytes, inst->stream), "fmax/counters reset");
         const double *ViTA = inst->at<double>(L.off_VA), *VTB = inst->at<double>(L.off_ViB);
@@ -1229,7 +1282,22 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         }
     }
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[1], inst->stream, cudaEventRecordExternal), "event");
-    if (L.variant == 3) {
+    if (L.variant == 4) {
+        pg::tcp::TcArgs t = tc_args(inst);
+        const auto &pl = inst->plan;
+        for (size_t i = 0; i + 1 < pl.post_off.size(); ++i) {
+            int off = pl.post_off[i], cnt = pl.post_off[i + 1] - off;
+            void *args[] = {&t, &off};
+            CK(cudaLaunchKernel((void *)pg::tcp::tc_post_kernel, dim3(L.n_tiles, cnt, R), dim3(pg::tcp::TM), args,
+                                pg::tcp::post_smem(), inst->stream), "tc post launch");
+        }
+        for (size_t i = 0; i + 1 < pl.pre_off.size(); ++i) {
+            int off = pl.pre_off[i], cnt = pl.pre_off[i + 1] - off;
+            void *args[] = {&t, &off};
+            CK(cudaLaunchKernel((void *)pg::tcp::tc_pre_kernel, dim3(L.n_tiles, cnt, R), dim3(pg::tcp::TM), args,
+                                pg::tcp::pre_smem(), inst->stream), "tc pre launch");
+        }
+    } else if (L.variant == 3) {
         pg::codon::CodonArgs c = codon_args(inst);
         const auto &pl = inst->plan;
         for (size_t i = 0; i + 1 < pl.post_off.size(); ++i) {
@@ -1540,7 +1608,9 @@ extern "C" int pg_trace_copy(pg_instance *inst, long long *host, int n) {
 int pg_kernels_per_eval(const pg_instance *inst, int32_t *n) {
     if (!inst || !n) return PG_ERR_ARG;
     *n = 3;   // pmat, traverse, reduce
-    if (inst->L.variant == 3)   // pmat + [masked tips] + one launch per post level + per pre level + ratio
+    if (inst->L.variant == 4)   // pmat + one launch per post level + per pre level + ratio
+        *n = 2 + (int32_t)(inst->plan.post_off.size() - 1) + (int32_t)(inst->plan.pre_off.size() - 1);
+    else if (inst->L.variant == 3)   // pmat + [masked tips] + one launch per post level + per pre level + ratio
         *n = 2 + ((inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? 1 : 0) + (int32_t)(inst->plan.post_off.size() - 1) +
              (int32_t)(inst->plan.pre_off.size() - 1);
     else if (inst->L.variant == 2)   // pmat + (one flow launch | one launch per post level + per pre level) + reduce
