@@ -89,6 +89,32 @@ def test_codon_fp32_reduced():
     _compare(ps.config3_yeast(N=16, C=50, precision="fp32"), "fp32")
 
 
+@pytest.mark.parametrize("N,R,C,missing,stationary", [(3, 1, 5, 0.1, True), (5, 1, 130, 0.1, True),
+                                                      (9, 2, 200, 0.0, False), (20, 4, 300, 0.05, True),
+                                                      (40, 3, 257, 0.02, False)])
+def test_codon_fp32_tensor_core_shapes(N, R, C, missing, stationary):
+    """fp32 codon on tcgen05 (kind::tf32, 3xTF32; kernel variant 4): ragged
+    128-pattern tiles, missing data, several categories, non-stationary root."""
+    pb = ps.small_problem(N, "codon", R=R, C=C, seed=N + C, missing=missing, simulate=True,
+                          stationary_root=stationary)
+    pb.precision = "fp32"
+    inst = _pg().from_problem(pb, precision="fp32")
+    assert inst.plan_info()["kernel_variant"] == 4
+    _compare(pb, "fp32", inst=inst)
+    inst.close()
+
+
+@pytest.mark.slow
+def test_codon_fp32_full():
+    """BJ:configs[3] in fp32 at full size on the tcgen05 path, 1e-4 (BJ:north_star)."""
+    _compare(ps.config3_yeast(precision="fp32"), "fp32", threads=16)
+
+
+@pytest.mark.slow
+def test_wnv_fp32_full():
+    _compare(ps.config4_wnv(precision="fp32"), "fp32", threads=16)
+
+
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 def test_codon_mmm122_reduced(precision):
     # NEXT-2: two-class codon MMM, S = 122 padded to 128, tip partials (P:910)
