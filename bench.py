@@ -172,6 +172,12 @@ def flop_counts(pb, C: int) -> dict:
     return {"f_min": 3 * (N - 2) * 2 * S * S * R * C, "paper": (6 * N - 8) * 2 * Sp * Sp * R * C}
 
 
+def tf32_peak(peaks):
+    """Dense TF32 tensor peak: the measured bf16 burst peak x the guide's
+    nominal tf32 / bf16 ratio (1.1 / 2.25 PFLOP/s, B200_PROFILING.md)."""
+    return peaks.get("bf16_tflops", 1590.0) * 1.1 / 2.25
+
+
 def load_peaks():
     """HBM: MEASURED_PEAKS.json (driver-written copy bandwidth).  FP64: measured
     inside this bench run (probe_fp64, below) when it ran, else our committed
@@ -179,9 +185,10 @@ def load_peaks():
     out = {}
     try:
         d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        out.update(hbm_gbs=float(d["hbm_gbs"]), hbm_src="measured (MEASURED_PEAKS.json hbm_gbs)")
+        out.update(hbm_gbs=float(d["hbm_gbs"]), hbm_src="measured (MEASURED_PEAKS.json hbm_gbs)",
+                   bf16_tflops=float(d["bf16_tflops"]))
     except Exception:
-        out.update(hbm_gbs=6650.0, hbm_src="fallback (B200_PROFILING.md)")
+        out.update(hbm_gbs=6650.0, hbm_src="fallback (B200_PROFILING.md)", bf16_tflops=1590.0)
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "r01", "fp64_peak.json")))
         out.update(fp64_tflops=float(d["dmma_tflops"]), dfma_tflops=float(d["dfma_tflops"]),
@@ -242,10 +249,15 @@ def roofline(pb, C: int, variant: int, precision: str, kms: dict, peaks: dict, t
     as timed per step)."""
     t = kms["traverse"] * 1e-3
     ev = eval_ms * 1e-3
-    if variant in (1, 2, 3):
+    if variant in (1, 2, 3, 4):
         fl = flop_counts(pb, C)
         hb = hbm_counts(pb, C, precision)
-        if variant >= 2:
+        if variant == 4:
+            pk, unit, bound = tf32_peak(peaks), "TFLOP/s", "tensor"
+            src = ("dense TF32 = measured bf16 burst peak (MEASURED_PEAKS.json) x nominal 1.1/2.25; "
+                   "each product issues 3 TF32 MMAs (3xTF32), so 1/3 of this is the fp32-accurate ceiling")
+            kname = "tc_post_kernel + tc_pre_kernel (tcgen05 kind::tf32, 3xTF32, all levels)"
+        elif variant >= 2:
             pk, unit, bound, src = peaks["fp64_tflops"], "TFLOP/s", "tensor", peaks["fp64_src"]
             kname = ("big_post_kernel + big_pre_kernel (S = 256 class, transpose-free, all levels)" if variant == 3
                      else "codon_flow2_kernel (post + pre order, one launch, TMA ring)" if flow

@@ -601,14 +601,14 @@ int pg_set_eigen(pg_instance *inst, const double *evec, const double *ievec, con
         if ((rc = upload_doubles(inst, inst->L.off_ViB, VTB.data(), VTB.size()))) return rc;
         if ((rc = upload_doubles(inst, inst->L.off_M0one, ones.data(), ones.size()))) return rc;
     }
-    if (inst->L.variant == 2) {      // Q as the fragment-ordered B operand of Qu = u Q'
+    if (inst->L.variant == 2 || inst->L.variant == 4) {      // (variant 4: V, V^-1 fragments for A1)
         std::vector<double> QB((size_t)SP * SP);
         const int KT = SP / 4;           // B fragments: [nt SP/8][kt SP/4][lane 32]
         for (int idx = 0; idx < SP * SP; ++idx) {
             const int lane = idx & 31, kt = (idx >> 5) & (KT - 1), nt = idx / (32 * KT);
             QB[idx] = Q[(size_t)(nt * 8 + (lane >> 2)) * SP + kt * 4 + (lane & 3)];
         }
-        if ((rc = upload_doubles(inst, inst->L.off_QB, QB.data(), QB.size()))) return rc;
+        if (inst->L.variant == 2 && (rc = upload_doubles(inst, inst->L.off_QB, QB.data(), QB.size()))) return rc;
         // V as A fragments (element (m,k) at apos(m,k), 64 rows) and V^{-1} as B fragments
         std::vector<double> VA((size_t)SP * SP, 0.0), ViB((size_t)SP * SP, 0.0);
         for (int m = 0; m < S; ++m)
@@ -985,6 +985,8 @@ static int configure(pg_instance *inst) {
                                 (int)pg::tcp::post_smem()), "smem attr");
         CK(cudaFuncSetAttribute((void *)pg::tcp::tc_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)pg::tcp::pre_smem()), "smem attr");
+        CK(cudaFuncSetAttribute((void *)pg::tcp::tc_pmat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pg::tcp::pmat_smem()), "smem attr");
         return PG_OK;
     } else if (L.variant == 3) {
         inst->block = pg::big::NTB;
@@ -1219,10 +1221,11 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
     if (L.variant == 4) {
         CK(cudaMemsetAsync(inst->ws + L.off_fmax, 0, L.reset_bytes, inst->stream), "fmax/counters reset");
         const double *M0 = inst->at<double>(L.off_M0);
+        const double *VA = inst->at<double>(L.off_VA), *ViB = inst->at<double>(L.off_ViB);
         float *Bm = inst->at<float>(L.off_P), *ONE = inst->at<float>(L.off_PONE);
-        void *args[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, (void *)&R, &Bm, &ONE};
-        CK(cudaLaunchKernel((void *)pg::tcp::tc_pmat_kernel, dim3(L.B * R), dim3(256), args, 0, inst->stream),
-           "tc pmat launch");
+        void *args[] = {&VA, &ViB, &M0, &lam, &rates, &bl, &S, (void *)&R, &Bm, &ONE};
+        CK(cudaLaunchKernel((void *)pg::tcp::tc_pmat_kernel, dim3(L.B * R), dim3(256), args, pg::tcp::pmat_smem(),
+                            inst->stream), "tc pmat launch");
     } else if (L.variant == 3) {
         // A1: W = P' per (branch, category), 8 row blocks each; masked tips' u
         CK(cudaMemsetAsync(inst->ws + L.off_fmax, 0, L.reset_bytes, inst->stream), "fmax/counters reset");

@@ -318,33 +318,58 @@ __global__ void __launch_bounds__(TM, 1) tc_pre_kernel(const TcArgs t, int level
     if (warp == 0) tc::tmem_free<128>(d);
 }
 
-// A1 for this path: P = M0 + V diag(expm1(gamma b lambda)) V^-1 (fp64, SIMT:
-// one CTA per (branch, category), 64 x 64 entries), written as the hi/lo
-// TF32 images of the two B operands (P for u = p P', P' for q = x P) and P 1
-__global__ void __launch_bounds__(256) tc_pmat_kernel(const double *__restrict__ V, const double *__restrict__ Vi,
+// A1 for this path: P = M0 + V diag(expm1(gamma b lambda)) V^-1 in fp64 on
+// the FP64 tensor path (one 64^3 DMMA product per (branch, category), V and
+// V^-1 pre-arranged as fragments at pg_set_eigen, as codon_pmat_kernel),
+// written as the hi/lo TF32 images of the two B operands (P for u = p P',
+// P' for q = x P) and P 1
+__global__ void __launch_bounds__(256) tc_pmat_kernel(const double *__restrict__ VA, const double *__restrict__ ViB,
                                                       const double *__restrict__ M0, const double *__restrict__ lam,
                                                       const double *__restrict__ rates, const double *__restrict__ bl,
                                                       int S, int R, float *B, float *ONE) {
-    __shared__ double e[SP], Ps[SP][SP + 1];
+    constexpr int KT = SP / 4, NW = SP / 8;
+    extern __shared__ __align__(16) unsigned char smp[];
+    double *Ps = reinterpret_cast<double *>(smp);            // [SP][SP+1]
+    double *e = Ps + SP * (SP + 1);                          // [SP]
+    double *Vs = e + SP;                                     // V's A fragments [SP*SP]
     const int br = blockIdx.x, r = br % R, b = br / R;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int i = threadIdx.x; i < SP * SP / 2; i += blockDim.x) cp_async16(Vs + 2 * i, VA + 2 * i);
+    cp_async_commit();
     const double t = rates[r] * bl[b];
     for (int k = threadIdx.x; k < SP; k += blockDim.x) e[k] = k < S ? expm1(lam[k] * t) : 0.0;
+    cp_async_wait<0>();
     __syncthreads();
-    for (int idx = threadIdx.x; idx < SP * SP; idx += blockDim.x) {
-        const int s = idx / SP, u = idx % SP;
-        double acc = 0.0;
-        if (s < S && u < S) {
-            for (int k = 0; k < S; ++k) acc += V[s * S + k] * e[k] * Vi[k * S + u];
-            acc += M0[s * SP + u];
+#pragma unroll 1
+    for (int cs = w; cs < NW; cs += nw) {
+        double bfr[KT];
+        codon::load_bfrag<SP>(bfr, ViB, cs, lane);
+#pragma unroll 1
+        for (int h = 0; h < SP / 32; ++h) {
+            double ap[4][2];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) ap[mt][0] = ap[mt][1] = 0.0;
+            const double *A = Vs + h * 32 * SP + lane;
+#pragma unroll
+            for (int kt = 0; kt < KT; ++kt) {
+                const double ek = e[kt * 4 + (lane & 3)];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) codon::dmma(ap[mt], A[(mt * KT + kt) * 32] * ek, bfr[kt]);
+            }
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int m = h * 32 + mt * 8 + (lane >> 2), n = cs * 8 + 2 * (lane & 3);
+                Ps[m * (SP + 1) + n] = ap[mt][0] + M0[m * SP + n];
+                Ps[m * (SP + 1) + n + 1] = ap[mt][1] + M0[m * SP + n + 1];
+            }
         }
-        Ps[s][u] = acc;
     }
     __syncthreads();
     float *rec = B + (size_t)br * BREC;
     for (int idx = threadIdx.x; idx < SP * SP; idx += blockDim.x) {
         const int n = idx / SP, kk = idx % SP;
         const uint32_t off = tc::kmajor_off(n, kk, SP) / 4;
-        const float p = (float)Ps[n][kk], pt = (float)Ps[kk][n];       // image (n, k): P[n][k] | P'[n][k]
+        const float p = (float)Ps[n * (SP + 1) + kk], pt = (float)Ps[kk * (SP + 1) + n];   // image (n, k): P | P'
         const float ph = tc::tf32_hi(p), pth = tc::tf32_hi(pt);
         rec[off] = ph;
         rec[SP * SP + off] = p - ph;
@@ -353,10 +378,11 @@ __global__ void __launch_bounds__(256) tc_pmat_kernel(const double *__restrict__
     }
     for (int s = threadIdx.x; s < SP; s += blockDim.x) {
         double acc = 0.0;
-        for (int u = 0; u < SP; ++u) acc += Ps[s][u];
+        for (int u = 0; u < SP; ++u) acc += Ps[s * (SP + 1) + u];
         ONE[(size_t)br * SP + s] = (float)acc;
     }
 }
+constexpr size_t pmat_smem() { return ((size_t)SP * (SP + 1) + SP + (size_t)SP * SP) * 8; }
 
 }  // namespace tcp
 }  // namespace pg
