@@ -238,6 +238,7 @@ struct pg_instance {
     int flow_nst = 2;                   // codon_flow2_kernel ring stages (1: latency, 2: throughput)
     int flow_pdl = 0;                   // A1 -> flow programmatic dependent launch (PG_FLOW_PDL=0/1 overrides)
     int flow_split = 0;                 // codon_flow2_kernel: one pre item per child (PG_FLOW_SPLIT=0/1 overrides)
+    int flow_rs = 1;                    // codon_flow2_kernel: rows of a product split over 2x the warps (PG_FLOW_RS)
     pg::codon::TmaMaps tmaps{};         // TMA tensor maps of u, q, utip (codon_flow2_kernel)
     int flow_defer = 0;                 // codon flow: Eq. 8 items after all pre items (PG_FLOW_DEFER)
     int flow_half = 0;                  // codon flow: half-tile post items when tch == 1 (PG_FLOW_HALF)
@@ -814,6 +815,8 @@ struct CodonFns {
     void *post4, *post2, *pre, *pmat, *flow, *tipu, *tipmask, *flow2[2];     // flow2[NST - 1]
     int threads, ctas_per_sm, flow2_threads, flow2_ctas[2];
     size_t post_smem, pre_smem, pmat_smem, flow_smem, tipu_smem, flow2_smem[2];
+    void *flow2rs;                      // NST = 2 with the rows split over 2x the consumer warps (SP = 64)
+    int flow2rs_threads;
 };
 template <int SP>
 static CodonFns codon_fns_t() {
@@ -825,7 +828,8 @@ static CodonFns codon_fns_t() {
             c::codon_threads<SP>(), c::codon_ctas_per_sm<SP>(), c::flow2_threads<SP>(),
             {c::flow2_ctas<SP, 1>(), c::flow2_ctas<SP, 2>()},
             c::post_smem<SP>(), c::pre_smem<SP>(), c::pmat_smem<SP>(), c::flow_smem<SP>(), c::tipu_smem<SP>(),
-            {c::flow2_smem<SP, 1>(), c::flow2_smem<SP, 2>()}};
+            {c::flow2_smem<SP, 1>(), c::flow2_smem<SP, 2>()},
+            SP == 64 ? (void *)c::codon_flow2_kernel<64, 2, 2> : nullptr, c::flow2_threads<SP, 2>()};
 }
 static CodonFns codon_fns(int SP) { return SP == 128 ? codon_fns_t<128>() : codon_fns_t<64>(); }
 
@@ -1028,6 +1032,11 @@ static int configure(pg_instance *inst) {
             // 0.297 -> 0.206 ms, WNV x8 0.579 -> 0.462 ms; scripts/gpu_codon3.sh)
             const char *se = getenv("PG_FLOW_SPLIT");
             inst->flow_split = se ? (atoi(se) != 0) : latency;
+            const char *re = getenv("PG_FLOW_RS");
+            inst->flow_rs = (L.SP == 64 && inst->flow_nst == 2 && re && atoi(re) == 2) ? 2 : 1;
+            if (cf.flow2rs)
+                CK(cudaFuncSetAttribute(cf.flow2rs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.flow2_smem[1]),
+                   "smem attr");
             for (int v = 0; v < 2; ++v)
                 CK(cudaFuncSetAttribute(cf.flow2[v], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cf.flow2_smem[v]),
                    "smem attr");
@@ -1347,8 +1356,9 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
                 f.pready = pdl ? inst->at<int>(L.off_flow) + 32 + (size_t)2 * (N - 1) * L.n_tiles : nullptr;
                 void *args2[] = {&c, &f, &inst->tmaps};
                 cudaLaunchConfig_t lc{};
-                lc.gridDim = dim3(std::min(items2, cf.flow2_ctas[v] * inst->sm_count));
-                lc.blockDim = dim3(cf.flow2_threads);
+                const bool rs = inst->flow_rs == 2;
+                lc.gridDim = dim3(std::min(items2, (rs ? 1 : cf.flow2_ctas[v]) * inst->sm_count));
+                lc.blockDim = dim3(rs ? cf.flow2rs_threads : cf.flow2_threads);
                 lc.dynamicSmemBytes = cf.flow2_smem[v];
                 lc.stream = inst->stream;
                 cudaLaunchAttribute at[1];
@@ -1356,7 +1366,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
                 at[0].val.programmaticStreamSerializationAllowed = 1;
                 lc.attrs = at;
                 lc.numAttrs = pdl ? 1 : 0;
-                CK(cudaLaunchKernelExC(&lc, cf.flow2[v], args2), "codon flow2 launch");
+                CK(cudaLaunchKernelExC(&lc, rs ? cf.flow2rs : cf.flow2[v], args2), "codon flow2 launch");
             } else {
                 void *args[] = {&c, &f};
                 CK(cudaLaunchKernel(cf.flow, dim3(std::min(items, cf.ctas_per_sm * inst->sm_count)),

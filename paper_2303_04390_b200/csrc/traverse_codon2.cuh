@@ -109,8 +109,11 @@ struct alignas(16) Meta2 {
 // an item is claimed only when the consumers are free, so a busy CTA never
 // holds back an item another CTA could start (latency: pattern shards whose
 // levels have fewer items than CTA slots), and three CTAs fit on an SM.
-template <int SP, int NST> constexpr int flow2_ctas() { return SP == 64 ? (NST == 1 ? 3 : 2) : 1; }
-template <int SP> constexpr int flow2_threads() { return (SP / 8 + 1) * 32; }
+// RS = 2 splits every product's rows over twice the consumer warps (warp
+// 8 h + w: output columns 8w..8w+7, row blocks 2h, 2h+1): half the DMMA chain
+// per warp on the latency-bound shards (SP = 64 only: 16 + 1 warps)
+template <int SP, int NST, int RS = 1> constexpr int flow2_ctas() { return RS == 2 ? 1 : SP == 64 ? (NST == 1 ? 3 : 2) : 1; }
+template <int SP, int RS = 1> constexpr int flow2_threads() { return (SP / 8 * RS + 1) * 32; }
 template <int SP> constexpr size_t flow2_stage() { return (size_t)3 * T * SP * 8 + ((sizeof(Meta2) + 127) / 128) * 128; }
 template <int SP, int NST>
 constexpr size_t flow2_smem() {
@@ -124,10 +127,11 @@ __device__ __forceinline__ void wait_p(const FlowArgs &f, int node, int r, int R
     if (f.pready && node != root) wait_count2(f.pready + (size_t)node * R + r, PMAT_FLAGS, status);
 }
 
-template <int SP, int NST>
-__global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
+template <int SP, int NST, int RS = 1>
+__global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, RS>()))
     codon_flow2_kernel(const CodonArgs a, const FlowArgs f, const __grid_constant__ TmaMaps tm) {
     CODON_GEO;
+    constexpr int NWC = NW * RS, NTC = NWC * 32, MTW = 4 / RS;     // consumer warps / threads, row blocks per warp
     constexpr size_t STG = flow2_stage<SP>();
     constexpr int ROWS = TILE / 256;                       // tensor-map rows per tile
     constexpr unsigned TILE_B = (unsigned)TILE * 8u;
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
     __syncthreads();
 
     // ================================ producer ================================
-    if (warp == NW) {
+    if (warp == NWC) {
         for (int g = 0;; ++g) {
             const int s = g % NST;
             if (g >= NST) mbar_wait_sleep(empty_u + 8u * s, (uint32_t)(g / NST + 1) & 1u);
@@ -301,7 +305,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
     }
 
     // ================================ consumers ===============================
-    const int w = warp;
+    const int w = warp % NW, mt0 = (warp / NW) * MTW;              // column strip, first row block
     for (int g = 0;; ++g) {
         const int s = g % NST;
         mbar_wait_sleep(full_u + 8u * s, (uint32_t)(g / NST) & 1u);
@@ -326,23 +330,23 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
             };
             if (k == root) {
                 if (r == 0 && threadIdx.x < T) storeE();
-                // Eq. 3 terms: thread -> (pattern mm = tid/8, states j, j+8, ...)
-                const int mm = threadIdx.x >> 3, j = threadIdx.x & 7;
+                // Eq. 3 terms: thread -> (pattern mm, states j, j+TPP, ...)
+                constexpr int TPP = NTC / T;
+                const int mm = threadIdx.x / TPP, j = threadIdx.x % TPP;
                 double sum = 0.0;
                 if (mm < T)
-                    for (int kk = j; kk < SP; kk += 8) {
+                    for (int kk = j; kk < SP; kk += TPP) {
                         const int p = apos<SP>(mm, kk);
                         sum = fma(a.pi[kk], As[p] * Bs[p], sum);
                     }
-                sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-                sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-                sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+#pragma unroll
+                for (int o = 1; o < TPP; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
                 if (j == 0 && mm < T) a.Lpart[(size_t)r * a.Cpad + pat0 + mm] = a.cat_w[r] * sum * (scA(mm) * scB(mm));
             } else {
                 double bfr[KT];
                 load_bfrag<SP>(bfr, a.PBpost + ((size_t)k * R + r) * MAT, w, lane);
                 // p = u_a o u_b in place (one A operand for the GEMM)
-                for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += NT) {
+                for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += NTC) {
                     double2 *pa = reinterpret_cast<double2 *>(As) + i2;
                     const double2 tb = reinterpret_cast<const double2 *>(Bs)[i2];
                     double2 v = *pa;
@@ -350,18 +354,18 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                     v.y *= tb.y;
                     *pa = v;
                 }
-                consumer_sync(NT);
-                double acc[4][2];
-                gemm_tile<SP>(acc, As, bfr, lane);
+                consumer_sync(NTC);
+                double acc[MTW][2];
+                gemm_tile<SP, MTW>(acc, As + mt0 * KT * 32, bfr, lane);
                 if (tr) tr[4] = gtimer();
                 if (r == 0 && threadIdx.x < T) storeE();
                 double *out = a.u + (((size_t)(k - N) * R + r) * ntiles + tile) * TILE;
                 int *fm = a.fmax + (size_t)(k - N) * a.Cpad + pat0;
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) {
-                    const int mm = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                for (int ml = 0; ml < MTW; ++ml) {
+                    const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
                     const double f2 = scA(mm) * scB(mm);
-                    const double c0 = acc[mt][0] * f2, c1 = acc[mt][1] * f2;
+                    const double c0 = acc[ml][0] * f2, c1 = acc[ml][1] * f2;
                     *reinterpret_cast<double2 *>(out + apos<SP>(mm, n)) = make_double2(c0, c1);
                     int fx = max(__double2hiint(c0) >> 20, __double2hiint(c1) >> 20);
                     fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 1));
@@ -370,7 +374,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 }
             }
             fence_proxy_async_global();              // our generic stores -> later TMA reads (other CTAs)
-            consumer_sync(NT);                       // stage consumed, outputs issued
+            consumer_sync(NTC);                      // stage consumed, outputs issued
             if (threadIdx.x == 0) {
                 __threadfence();
                 atomicAdd(f.rpost + (size_t)(k - N) * ntiles + tile, 1);
@@ -390,16 +394,16 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
         // and sibling exponents
         auto q_gemm = [&](int c, const double *Xs) {
             const int node = c ? cb : ca;
-            double bq[KT], acc[4][2];
+            double bq[KT], acc[MTW][2];
             load_bfrag<SP>(bq, a.PBpre + ((size_t)node * R + r) * MAT, w, lane);
-            gemm_tile<SP>(acc, Xs, bq, lane);
+            gemm_tile<SP, MTW>(acc, Xs + mt0 * KT * 32, bq, lane);
             double *out = a.q + (((size_t)(node - N) * R + r) * ntiles + tile) * TILE;
             int *qm = a.qmax + (size_t)(node - N) * a.Cpad + pat0;
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt) {
-                const int mm = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+            for (int ml = 0; ml < MTW; ++ml) {
+                const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
                 const double f2 = scQ(mm) * scC(1 - c, mm);
-                const double c0 = acc[mt][0] * f2, c1 = acc[mt][1] * f2;
+                const double c0 = acc[ml][0] * f2, c1 = acc[ml][1] * f2;
                 *reinterpret_cast<double2 *>(out + apos<SP>(mm, n)) = make_double2(c0, c1);
                 int fx = max(__double2hiint(c0) >> 20, __double2hiint(c1) >> 20);
                 fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 1));
@@ -410,7 +414,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
         auto publish_q = [&](bool pa, bool pb) {
             if (!pa && !pb) return;
             fence_proxy_async_global();
-            consumer_sync(NT);
+            consumer_sync(NTC);
             if (threadIdx.x == 0) {
                 __threadfence();
                 if (pa) atomicAdd(f.rpre + (size_t)(ca - N) * ntiles + tile, 1);
@@ -426,32 +430,32 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
             const int node = c ? cb : ca;
             const size_t br = (size_t)node * R + r;
             const int kind = (kinds >> (2 * c)) & 3;
-            double acc[4][2];
+            double acc[MTW][2];
             if (node >= N || kind == 2) {
                 double b[KT];
                 load_bfrag<SP>(b, a.QB, w, lane);
-                gemm_tile<SP>(acc, Uc(c), b, lane);
+                gemm_tile<SP, MTW>(acc, Uc(c) + mt0 * KT * 32, b, lane);
             } else {
                 const uint8_t *stc = c ? m->sb : m->sa;
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) {
-                    const int mm = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                for (int ml = 0; ml < MTW; ++ml) {
+                    const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
                     const int sv = stc[mm];
                     if (sv < a.S) {
                         const double2 v = __ldg(reinterpret_cast<const double2 *>(a.DT + br * MAT + (size_t)sv * SP + n));
-                        acc[mt][0] = v.x;
-                        acc[mt][1] = v.y;
+                        acc[ml][0] = v.x;
+                        acc[ml][1] = v.y;
                     } else {
-                        acc[mt][0] = acc[mt][1] = 0.0;
+                        acc[ml][0] = acc[ml][1] = 0.0;
                     }
                 }
             }
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt) {
-                const int mm = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+            for (int ml = 0; ml < MTW; ++ml) {
+                const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
                 const int p = apos<SP>(mm, n);
                 const double2 x2 = xat(p);
-                double sn = x2.x * acc[mt][0] + x2.y * acc[mt][1];
+                double sn = x2.x * acc[ml][0] + x2.y * acc[ml][1];
                 sn += __shfl_xor_sync(0xffffffffu, sn, 1);
                 sn += __shfl_xor_sync(0xffffffffu, sn, 2);
                 if ((lane & 3) == 0) part[(c * NW + w) * T + mm] = sn;
@@ -470,7 +474,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
             // child c's Eq. 8 terms from x_c and u_c
             const int c = cs;
             const double *Usib = Uc(1 - c);
-            for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += NT) {
+            for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += NTC) {
                 double2 *px = reinterpret_cast<double2 *>(Qs) + i2;
                 const double2 us = reinterpret_cast<const double2 *>(Usib)[i2];
                 double2 v = *px;
@@ -478,7 +482,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
                 v.y *= us.y;
                 *px = v;
             }
-            consumer_sync(NT);
+            consumer_sync(NTC);
             if ((c ? cb : ca) >= N) q_gemm(c, Qs);
             if (tr) tr[4] = gtimer();
             publish_q(c == 0 && ca >= N, c == 1 && cb >= N);
@@ -494,25 +498,25 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
             for (int c = 0; c < 2; ++c) {
                 const int node = c ? cb : ca;
                 if (node < N) continue;
-                double bq[KT], acc[4][2];
+                double bq[KT], acc[MTW][2];
                 load_bfrag<SP>(bq, a.PBpre + ((size_t)node * R + r) * MAT, w, lane);
                 const double *Ub = Uc(1 - c);
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+                for (int ml = 0; ml < MTW; ++ml) acc[ml][0] = acc[ml][1] = 0.0;
 #pragma unroll
                 for (int kt = 0; kt < KT; ++kt)
 #pragma unroll
-                    for (int mt = 0; mt < 4; ++mt) {
-                        const int p = (mt * KT + kt) * 32 + lane;
-                        dmma(acc[mt], Qs[p] * Ub[p], bq[kt]);
+                    for (int ml = 0; ml < MTW; ++ml) {
+                        const int p = ((mt0 + ml) * KT + kt) * 32 + lane;
+                        dmma(acc[ml], Qs[p] * Ub[p], bq[kt]);
                     }
                 double *out = a.q + (((size_t)(node - N) * R + r) * ntiles + tile) * TILE;
                 int *qm = a.qmax + (size_t)(node - N) * a.Cpad + pat0;
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) {
-                    const int mm = mt * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                for (int ml = 0; ml < MTW; ++ml) {
+                    const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
                     const double f2 = scQ(mm) * scC(1 - c, mm);
-                    const double c0 = acc[mt][0] * f2, c1 = acc[mt][1] * f2;
+                    const double c0 = acc[ml][0] * f2, c1 = acc[ml][1] * f2;
                     *reinterpret_cast<double2 *>(out + apos<SP>(mm, n)) = make_double2(c0, c1);
                     int fx = max(__double2hiint(c0) >> 20, __double2hiint(c1) >> 20);
                     fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 1));
@@ -534,7 +538,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
             eq8(1, false, xq(1));
         }
         const int c0 = cs < 0 ? 0 : cs, c1 = cs < 0 ? 1 : cs;
-        consumer_sync(NT);                           // stage and partials complete
+        consumer_sync(NTC);                          // stage and partials complete
         if (threadIdx.x < T) {                       // fixed-order sums over the warps
             const int mm = threadIdx.x;
             double sd = 0.0, sn0 = 0.0, sn1 = 0.0;
@@ -550,7 +554,7 @@ __global__ void __launch_bounds__(flow2_threads<SP>(), (flow2_ctas<SP, NST>()))
             if (c0 == 0) nd[((size_t)ca * R + r) * a.Cpad + pat0 + mm] = make_double2(s0 * sn0, wr * sd);
             if (c1 == 1) nd[((size_t)cb * R + r) * a.Cpad + pat0 + mm] = make_double2(s1 * sn1, wr * sd);
         }
-        consumer_sync(NT);                           // partials read before the next item writes them
+        consumer_sync(NTC);                          // partials read before the next item writes them
         if (threadIdx.x == 0) mbar_arrive_u32(empty_u + 8u * s);
         if (tr) tr[6] = gtimer();
     }

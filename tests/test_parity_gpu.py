@@ -445,6 +445,8 @@ def test_hmc_leapfrog_matches_oracle_trajectory(model, N, R, C):
 @pytest.mark.parametrize("env", [{"PG_CODON_FLOW": "0"}, {"PG_CODON_FLOW": "2"}, {"PG_CODON_FLOW": "1"},
                                  {"PG_FLOW_NST": "1"}, {"PG_FLOW_NST": "2"}, {"PG_FLOW_PDL": "1"},
                                  {"PG_FLOW_NST": "1", "PG_FLOW_PDL": "1"}, {"PG_FLOW_SPLIT": "1"},
+                                 {"PG_FLOW_RS": "2"}, {"PG_FLOW_RS": "2", "PG_FLOW_SPLIT": "1"},
+                                 {"PG_FLOW_RS": "2", "PG_FLOW_SPLIT": "0"},
                                  {"PG_FLOW_SPLIT": "0", "PG_FLOW_PDL": "1"}, {"PG_FLOW_SPLIT": "1", "PG_FLOW_NST": "1"},
                                  {"PG_CODON_FLOW": "1", "PG_FLOW_TCH": "3"},
                                  {"PG_CODON_FLOW": "1", "PG_FLOW_TCH": "1"},
