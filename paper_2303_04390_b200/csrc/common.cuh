@@ -54,28 +54,6 @@ __device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-__device__ __forceinline__ void cp_async_wait_dyn(int n) {
-    switch (n) {
-        case 0: cp_async_wait<0>(); break;
-        case 1: cp_async_wait<1>(); break;
-        case 2: cp_async_wait<2>(); break;
-        case 3: cp_async_wait<3>(); break;
-        case 4: cp_async_wait<4>(); break;
-        case 5: cp_async_wait<5>(); break;
-        case 6: cp_async_wait<6>(); break;
-        default: cp_async_wait<7>(); break;
-    }
-}
-
-// Copy `bytes` (multiple of 16, 16-B aligned) with 16-B cp.async.
-template <int BYTES>
-__device__ __forceinline__ void cp_async_vec(void *smem, const void *gmem) {
-    static_assert(BYTES % 16 == 0, "vector copies are 16-B granular");
-#pragma unroll
-    for (int i = 0; i < BYTES / 16; ++i)
-        cp_async16((char *)smem + 16 * i, (const char *)gmem + 16 * i);
-}
-
 // ---- exact power-of-two rescaling (reading R4) --------
 // exponent e with m = f * 2^e, f in [0.5, 1); 0 for m == 0.
 __device__ __forceinline__ int exponent_of(double m) {
@@ -91,8 +69,6 @@ __device__ __forceinline__ int exponent_of(float m) {
 __device__ __forceinline__ double scale_pow2(double x, int k) { return ldexp(x, k); }
 __device__ __forceinline__ float scale_pow2(float x, int k) { return ldexpf(x, k); }
 
-template <typename Real>
-__device__ __forceinline__ Real ldg(const Real *p) { return __ldg(p); }
 
 }  // namespace pg
 

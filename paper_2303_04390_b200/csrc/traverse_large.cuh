@@ -7,8 +7,10 @@
 // whole input vector:  u = P p reads the transposed copy P' (so each thread's
 // 4 outputs are 4 consecutive words for every input state t), q = P' x reads
 // P row-major, Q u reads Q'.  A CTA owns TPL patterns x R categories.
-// Round-1 version: SIMT FP64 FMA with CTA barriers between phases; the
-// tensor-core (DMMA) formulation is the planned next step.
+// SIMT FMA with CTA barriers between phases.  Used only where no tensor-core
+// variant applies: fp32 with partial tips, or fp32 with
+// 64 < S <= 128; fp64 codon runs on DMMA (traverse_codon2.cuh), fp32 codon
+// with state tips on tcgen05 TF32 (traverse_tc.cuh).
 #pragma once
 #include "common.cuh"
 
