@@ -426,14 +426,15 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
         // gamma_r), with x_c at the output positions from xat(p); den = x_c'u_c
         // (the same for both children, q_k o u_a o u_b, Eq. 5).  Tiles are
         // unscaled: the factors cancel in the ratio over categories.
-        double bq[KT];                               // B fragments of the item's products (Q's for eq8)
         auto eq8 = [&](int c, bool den, auto xat) {
             const int node = c ? cb : ca;
             const size_t br = (size_t)node * R + r;
             const int kind = (kinds >> (2 * c)) & 3;
             double acc[MTW][2];
             if (node >= N || kind == 2) {
-                gemm_tile<SP, MTW>(acc, Uc(c) + mt0 * KT * 32, bq, lane);
+                double b[KT];
+                load_bfrag<SP>(b, a.QB, w, lane);
+                gemm_tile<SP, MTW>(acc, Uc(c) + mt0 * KT * 32, b, lane);
             } else {
                 const uint8_t *stc = c ? m->sb : m->sa;
 #pragma unroll
@@ -483,7 +484,6 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
             }
             consumer_sync(NTC);
             if ((c ? cb : ca) >= N) q_gemm(c, Qs);
-            load_bfrag<SP>(bq, a.QB, w, lane);
             if (tr) tr[4] = gtimer();
             publish_q(c == 0 && ca >= N, c == 1 && cb >= N);
             if (tr) tr[5] = gtimer();
@@ -494,17 +494,12 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
             // before the Eq. 8 terms (measured faster than forming x in place
             // after the Eq. 8 GEMMs: yeast 1.155 -> 1.106 ms, the pre-order
             // chain link is shorter)
-            // B fragments software-pipelined across the item's products: the
-            // next product's B is in flight while this one's epilogue runs,
-            // and Q's fragments serve both Eq. 8 products
-            if (ca >= N) load_bfrag<SP>(bq, a.PBpre + ((size_t)ca * R + r) * MAT, w, lane);
-            else if (cb >= N) load_bfrag<SP>(bq, a.PBpre + ((size_t)cb * R + r) * MAT, w, lane);
-            else load_bfrag<SP>(bq, a.QB, w, lane);
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 const int node = c ? cb : ca;
                 if (node < N) continue;
-                double acc[MTW][2];
+                double bq[KT], acc[MTW][2];
+                load_bfrag<SP>(bq, a.PBpre + ((size_t)node * R + r) * MAT, w, lane);
                 const double *Ub = Uc(1 - c);
 #pragma unroll
                 for (int ml = 0; ml < MTW; ++ml) acc[ml][0] = acc[ml][1] = 0.0;
@@ -515,9 +510,6 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
                         const int p = ((mt0 + ml) * KT + kt) * 32 + lane;
                         dmma(acc[ml], Qs[p] * Ub[p], bq[kt]);
                     }
-                // next product's B: child b's P after child a's, then Q
-                if (c == 0 && cb >= N) load_bfrag<SP>(bq, a.PBpre + ((size_t)cb * R + r) * MAT, w, lane);
-                else load_bfrag<SP>(bq, a.QB, w, lane);
                 double *out = a.q + (((size_t)(node - N) * R + r) * ntiles + tile) * TILE;
                 int *qm = a.qmax + (size_t)(node - N) * a.Cpad + pat0;
 #pragma unroll
@@ -542,7 +534,7 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
                     return make_double2(q2.x * o2.x, q2.y * o2.y);
                 };
             };
-            eq8(0, true, xq(0));                     // bq = Q's fragments here
+            eq8(0, true, xq(0));
             eq8(1, false, xq(1));
         }
         const int c0 = cs < 0 ? 0 : cs, c1 = cs < 0 ? 1 : cs;

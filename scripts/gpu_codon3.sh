@@ -19,7 +19,7 @@ except Exception as e:
 PY
 }
 for cfg in "--config 3" "--config 3 --virtual-shard 8" "--config 4" "--config 4 --virtual-shard 8" "--config 5" "--config 5 --virtual-shard 8"; do
-  for e in "PG_CODON_FLOW=2"; do
+  for e in "PG_CODON_FLOW=2" "PG_FLOW_RS=2"; do
     run "$e" "$cfg"
   done
 done 2>&1 | tee gpurun_out/codon3_bench.txt
