@@ -1262,8 +1262,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         int Nt = inst->cfg.tips, tipp = (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? 1 : 0;
         void *args[] = {&VA, &ViB, &M0, &Qd, &lam, &rates, &bl, &S, (void *)&R, &Nt, &tipp, &PBpost, &PBpre, &PT, &DT, &PONE, &pready};
         const CodonFns cf = codon_fns(L.SP);
-        CK(cudaLaunchKernel(cf.pmat, dim3(L.B * R, 2, L.SP / 32), dim3(256), args, cf.pmat_smem, inst->stream),
-           "codon pmat launch");
+        CK(cudaLaunchKernel(cf.pmat, dim3(L.B * R, 2), dim3(256), args, cf.pmat_smem, inst->stream), "codon pmat launch");
         if (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) {     // u = P p of partial tips (A2's tip step)
             pg::codon::CodonArgs c = codon_args(inst);
             void *targs[] = {&c};
@@ -1349,7 +1348,6 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
                                                                                                           : nullptr;
             if (inst->flow_ver == 2) {
                 f.split = inst->flow_split;
-                f.pflags = 2 * L.SP / 32;
                 const int items2 = (f.npost + (f.ntask - f.npost) * (f.split ? 2 : 1)) * R * L.n_tiles;
                 const int v = inst->flow_nst - 1;
                 // programmatic dependent launch right behind A1 (no partial-tip

@@ -411,7 +411,6 @@ struct FlowArgs {
     unsigned long long *trace;   // diagnostics (PG_FLOW_TRACE): [item][TRW] = {smid, t_take, t_ready, t_done, phase stamps}
     const int *pready;           // codon_flow2_kernel under PDL: [B][R] A1 done flags (null: A1 finished before launch)
     int split;                   // codon_flow2_kernel: one pre item per child (latency-bound shards)
-    int pflags;                  // pready count that marks a (branch, r) complete (pmat_flags<SP>)
 };
 
 // ---------------------------------------------------------------------------
@@ -903,22 +902,27 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
     // this CTA's outputs only after pready[branch][r] is published below
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     extern __shared__ __align__(16) unsigned char smem_p[];
-    // One CTA per (branch x category, P|D, block of 32 rows): the block's 32
-    // rows of V (A fragments, 8 SP B) are staged in shared memory, every warp
-    // computes 8-column strips of those rows, and the rows are scattered into
-    // the layouts right away -- no full SP x SP matrix in shared memory, so
-    // SP = 128 stages its operand too (A1 for S = 122: 203 -> ~30 us).
-    double *Ps = reinterpret_cast<double *>(smem_p);     // [32][SP+1] this block's rows
-    double *e = Ps + 32 * (SP + 1);                      // [SP]
-    double *Vs = e + SP;                                 // [4 mt][KT][32] A fragments of the block
+    double *Ps = reinterpret_cast<double *>(smem_p);     // [SP][SP+1]: P or D
+    double *e = Ps + SP * (SP + 1);                      // [SP]
+    // SP = 64: V's A fragments staged in shared memory once (all copies in
+    // flight together; ncu: L2 loads inside the DMMA loop were the top stall);
+    // SP = 128 reads them from L2 (no room next to the 132 KB output buffer)
+    constexpr bool STAGE_V = SP == 64;
+    double *Vs = e + 2 * SP;
     const int br = blockIdx.x, r = br % R, b = br / R;
-    const int pass = blockIdx.y, rb = blockIdx.z;       // pass 0: P (every branch), 1: D (tips only)
+    // blockIdx.y = 0: P (every branch), 1: D (tips only).  What each branch's
+    // consumers read: internal branches the B fragments of P' (post, u_k =
+    // p P') and P (pre, q_c = x_c P); tips the rows of P' (gathers), P 1
+    // (missing data) and D' (Eq. 8 numerators); partial tips also P'-fragments
+    // (codon_tipu_kernel).  Nothing else is formed or written.
+    const int pass = blockIdx.y;
     const bool tip = b < N;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     if (pass == 0 || tip) {
-        const double *Vsrc = VA + (size_t)rb * 4 * KT * 32;
-        for (int i = threadIdx.x; i < 4 * KT * 32 / 2; i += blockDim.x) cp_async16(Vs + 2 * i, Vsrc + 2 * i);
-        cp_async_commit();
+        if constexpr (STAGE_V) {
+            for (int i = threadIdx.x; i < (int)MAT / 2; i += blockDim.x) cp_async16(Vs + 2 * i, VA + 2 * i);
+            cp_async_commit();
+        }
         const double g = rates[r], t = g * bl[b];
         // P = M0 + V diag(e - 1) V^-1, D = gamma (Q + V diag(lambda (e - 1)) V^-1)
         // (M0 = V V^-1, Q formed once on the host; R15b)
@@ -926,61 +930,70 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
             const double em1 = k < S ? expm1(lam[k] * t) : 0.0;
             e[k] = pass ? (k < S ? g * lam[k] * em1 : 0.0) : em1;
         }
-        cp_async_wait<0>();
+        if constexpr (STAGE_V) cp_async_wait<0>();
         __syncthreads();
         const size_t base = (size_t)br * MAT;
+        const double *Vsrc = STAGE_V ? Vs : VA;
+        // Warp w computes column strips 8 cs .. 8 cs + 7, cs = w, w + nw, ...
 #pragma unroll 1
         for (int cs = w; cs < NW; cs += nw) {
             double bfr[KT];
             load_bfrag<SP>(bfr, ViB, cs, lane);
-            double ap[4][2];
+#pragma unroll 1
+            for (int h = 0; h < SP / 32; ++h) {      // rows 32h .. 32h+31
+                double ap[4][2];
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt) ap[mt][0] = ap[mt][1] = 0.0;
+                for (int mt = 0; mt < 4; ++mt) ap[mt][0] = ap[mt][1] = 0.0;
+                const double *A = Vsrc + h * TILE + lane;
 #pragma unroll
-            for (int kt = 0; kt < KT; ++kt) {
-                const double ek = e[kt * 4 + (lane & 3)];
+                for (int kt = 0; kt < KT; ++kt) {
+                    const double ek = e[kt * 4 + (lane & 3)];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) dmma(ap[mt], Vs[(mt * KT + kt) * 32 + lane] * ek, bfr[kt]);
-            }
+                    for (int mt = 0; mt < 4; ++mt) {
+                        const double v = STAGE_V ? A[(mt * KT + kt) * 32] : __ldg(A + (mt * KT + kt) * 32);
+                        dmma(ap[mt], v * ek, bfr[kt]);
+                    }
+                }
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt) {
-                const int ml = mt * 8 + (lane >> 2), m = rb * 32 + ml, n = cs * 8 + 2 * (lane & 3);
-                const double2 z = *reinterpret_cast<const double2 *>((pass ? Qd : M0) + m * SP + n);
-                const double zs = pass ? g : 1.0;
-                Ps[ml * (SP + 1) + n] = fma(zs, z.x, ap[mt][0]);
-                Ps[ml * (SP + 1) + n + 1] = fma(zs, z.y, ap[mt][1]);
+                for (int mt = 0; mt < 4; ++mt) {
+                    const int m = h * 32 + mt * 8 + (lane >> 2), n = cs * 8 + 2 * (lane & 3);
+                    const double2 z = *reinterpret_cast<const double2 *>((pass ? Qd : M0) + m * SP + n);
+                    const double zs = pass ? g : 1.0;
+                    Ps[m * (SP + 1) + n] = fma(zs, z.x, ap[mt][0]);
+                    Ps[m * (SP + 1) + n + 1] = fma(zs, z.y, ap[mt][1]);
+                }
             }
         }
         __syncthreads();
         const bool frag_post = !tip || tip_partials, frag_pre = !tip;
-        for (int idx = threadIdx.x; idx < 32 * SP; idx += blockDim.x) {
-            const int ml = idx / SP, col = idx % SP, row = rb * 32 + ml;    // element P[row][col] (or D)
-            const double v = Ps[ml * (SP + 1) + col];
+        for (int idx = threadIdx.x; idx < (int)MAT; idx += blockDim.x) {
+            const int row = idx / SP, col = idx % SP;
             if (pass == 0) {
-                // B[k=t][n=s] = P[s][t] (u = p P'), B[k=s][n=t] = P[s][t] (q = x P), P'[t][s]
-                if (frag_post) PBpost[base + (((row >> 3) * KT + (col >> 2)) << 5) + ((row & 7) << 2) + (col & 3)] = v;
-                if (frag_pre) PBpre[base + (((col >> 3) * KT + (row >> 2)) << 5) + ((col & 7) << 2) + (row & 3)] = v;
-                if (tip) PT[base + (size_t)col * SP + row] = v;
+                const int ln = idx & 31, kt = (idx >> 5) & (KT - 1), nt = idx / (32 * KT);
+                const int kk = kt * 4 + (ln & 3), nn = nt * 8 + (ln >> 2);
+                if (frag_post) PBpost[base + idx] = Ps[nn * (SP + 1) + kk];    // B[k=t][n=s] = P[s][t]
+                if (frag_pre) PBpre[base + idx] = Ps[kk * (SP + 1) + nn];      // B[k=s][n=t] = P[s][t]
+                if (tip) PT[base + idx] = Ps[col * (SP + 1) + row];            // P'[t][s] = P[s][t]
             } else {
-                DT[base + (size_t)col * SP + row] = v;                 // D'
+                DT[base + idx] = Ps[col * (SP + 1) + row];                     // D'
             }
         }
-        if (pass == 0 && tip && threadIdx.x < 32) {
-            double acc = 0.0;
-            for (int u = 0; u < SP; ++u) acc += Ps[threadIdx.x * (SP + 1) + u];
-            PONE[(size_t)br * SP + rb * 32 + threadIdx.x] = acc;
-        }
+        if (pass == 0 && tip)
+            for (int s2 = threadIdx.x; s2 < SP; s2 += blockDim.x) {
+                double acc = 0.0;
+                for (int u = 0; u < SP; ++u) acc += Ps[s2 * (SP + 1) + u];
+                PONE[(size_t)br * SP + s2] = acc;
+            }
         __syncthreads();
     }
-    if (pready && threadIdx.x == 0) {                    // publish (release): 2 * SP / 32 CTAs per (branch, r)
+    if (pready && threadIdx.x == 0) {                    // publish (release): 2 CTAs per (branch, r)
         __threadfence();
         atomicAdd(pready + br, 1);
     }
 }
 template <int SP>
-constexpr size_t pmat_smem() { return ((size_t)32 * (SP + 1) + SP + (size_t)32 * SP) * 8; }
-// pready count per (branch, r): the P and D CTAs of every 32-row block
-template <int SP> constexpr int pmat_flags() { return 2 * SP / 32; }
+constexpr size_t pmat_smem() { return ((size_t)SP * (SP + 1) + 2 * SP + (SP == 64 ? (size_t)SP * SP : 0)) * 8; }
+constexpr int PMAT_FLAGS = 2;                            // pready count per (branch, r): the P and D CTAs
 
 }  // namespace codon
 }  // namespace pg

@@ -124,7 +124,7 @@ constexpr size_t flow2_smem() {
 // start while codon_pmat_kernel is still running; an item then also waits
 // until the transition matrices it reads are published (pready[branch][r]).
 __device__ __forceinline__ void wait_p(const FlowArgs &f, int node, int r, int R, int root, int *status) {
-    if (f.pready && node != root) wait_count2(f.pready + (size_t)node * R + r, f.pflags, status);
+    if (f.pready && node != root) wait_count2(f.pready + (size_t)node * R + r, PMAT_FLAGS, status);
 }
 
 template <int SP, int NST, int RS = 1>
