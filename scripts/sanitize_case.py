@@ -23,7 +23,14 @@ CASES = {
     "yeast": lambda: ps.config3_yeast(N=20, C=77),
     "yeast_levels": lambda: ps.config3_yeast(N=20, C=77),
     "s122": lambda: ps.config5_yeast_mmm(N=10, C=40),
+    "s256": lambda: ps.small_problem(5, "codon4", R=1, C=33, seed=7, simulate=True),
+    "codon_fp32": lambda: _fp32(ps.small_problem(9, "codon", R=2, C=150, seed=5, missing=0.05, simulate=True)),
 }
+
+
+def _fp32(pb):
+    pb.precision = "fp32"
+    return pb
 
 
 def main():
@@ -32,7 +39,7 @@ def main():
         os.environ["PG_CODON_FLOW"] = "0"
     import paper_2303_04390_b200 as pg
     pb = CASES[name]()
-    inst = pg.from_problem(pb)
+    inst = pg.from_problem(pb, precision=pb.precision)
     logl, g = inst.compute()
     logl2, g2 = inst.compute()               # a replay of the captured graph
     ref = oracle.loglik_grad(pb, threads=4)
