@@ -52,10 +52,10 @@ __device__ __forceinline__ void tma_load_tile(uint32_t dst, const CUtensorMap *m
         "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(row), "r"(bar)
         : "memory");
 }
-// arrive on `bar` when this thread's prior cp.async copies have landed
-// (pending count incremented now, decremented at completion)
+// arrive on `bar` (one of its expected arrivals) when this thread's prior
+// cp.async copies have landed
 __device__ __forceinline__ void cp_async_mbar_arrive(uint32_t bar) {
-    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void consumer_sync(int nthreads) {
     asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
@@ -152,7 +152,9 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
     auto tileA = [&](int s) { return reinterpret_cast<double *>(ring + s * STG); };
     auto meta = [&](int s) { return reinterpret_cast<Meta2 *>(ring + s * STG + 3 * (size_t)TILE * 8); };
     if (threadIdx.x == 0) {
-        for (int i = 0; i < NST; ++i) { mbar_init(full + i, 2); mbar_init(empty + i, 1); }
+        // full: lane 0's expect_tx arrive + the 32 lanes' cp.async arrives +
+        // lane 0's final arrive (after the metadata stores)
+        for (int i = 0; i < NST; ++i) { mbar_init(full + i, 34); mbar_init(empty + i, 1); }
         fence_mbar_init();
     }
     __syncthreads();
@@ -168,8 +170,10 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
             Meta2 *m = meta(s);
             const uint32_t bar = full_u + 8u * s;
             if (item >= nitems) {
+                if (lane == 0) m->item = -1;
+                cp_async_mbar_arrive(bar);
+                __syncwarp();
                 if (lane == 0) {
-                    m->item = -1;
                     mbar_arrive_u32(bar);
                     mbar_arrive_u32(bar);
                 }

@@ -156,7 +156,17 @@ struct SmallCfg {
     static constexpr int ND = W * 2 * 32 * 16;                 // (num, den) window per warp
     static constexpr int XGS = VB + 16;                        // exchange stride per lane group (bank skew)
     static constexpr int XB = (LV > 1 && !MMA) ? (32 / LV) * XGS : 0;   // full-vector exchange buffer per warp
-    static constexpr int QOFF = 128;                           // Q (SP > 4 only; SP <= 4 keeps it in registers)
+#ifdef PG_OPS
+    static constexpr int OPS = PG_OPS;
+#else
+    static constexpr int OPS = 1;
+#endif
+    static constexpr int DS = D / OPS < 2 ? 2 : D / OPS;
+    // barriers (full[DS], empty[DS], post_done, prog_bar) below QOFF, then Q
+    // (SP > 4 only; SP <= 4 keeps it in registers).  QOFF follows DS: a fixed
+    // 128 B let an 8-stage ring's post_done / prog_bar overlap Q (found by
+    // compute-sanitizer synccheck on the S = 16 tensor-core variant)
+    static constexpr int QOFF = (8 * (2 * DS + 2) + 127) / 128 * 128;
     static constexpr int BARS = QOFF + (SP > 4 ? SP * SP * (int)sizeof(Real) : 0);   // barriers + Q
     static __host__ __device__ int mat_slot(int R) { return MMA ? MMA_SLOT : MMA4 ? MMA4_SLOT : R * CS; }
     static __host__ __device__ int mat_rec(int R) { return MMA ? MMA_REC : MMA4 ? 2 * MMA4_SLOT : R * CS; }   // bytes per branch in HBM
@@ -176,12 +186,6 @@ struct SmallCfg {
     // producer refill only after both ops: 24 % slower for S = 4; for S = 16
     // (MMM) 2 stages x 2 ops vs 4 stages x 1 op measured 0.228 vs 0.222 ms
     // (scripts/gpu_mmm_stages.sh), so one op per stage everywhere.
-#ifdef PG_OPS
-    static constexpr int OPS = PG_OPS;
-#else
-    static constexpr int OPS = 1;
-#endif
-    static constexpr int DS = D / OPS < 2 ? 2 : D / OPS;
     static __host__ __device__ size_t smem(int R, int K, int depth) {
         return (size_t)BARS + (size_t)DS * OPS * stage(R, K) + (size_t)K * warp_bytes(depth);
     }
