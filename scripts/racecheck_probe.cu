@@ -45,6 +45,39 @@ __global__ void ring(const double *src, double *out) {
     out[threadIdx.x] = acc;
 }
 
+// the same ring with the producer's 32 lanes filling a stage by cp.async
+// (LDGSTS) and arriving through cp.async.mbarrier.arrive.noinc (the flow2
+// kernel's tip gathers)
+__global__ void ring_cpasync(const double *src, double *out) {
+    __shared__ __align__(128) double stage[D][CHUNK / 8];
+    __shared__ __align__(8) uint64_t full[D], empty[D];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < D; ++i) { pg::mbar_init(&full[i], 32); pg::mbar_init(&empty[i], CONS); }
+        pg::fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == CONS) {
+        for (int t = 0; t < STEPS; ++t) {
+            const int s = t % D;
+            if (t >= D) pg::mbar_wait(&empty[s], (uint32_t)((t / D + 1) & 1));
+            for (int i = lane; i < CHUNK / 16; i += 32)
+                pg::cp_async16(&stage[s][2 * i], src + (size_t)t * (CHUNK / 8) + 2 * i);
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(pg::smem_u32(&full[s])) : "memory");
+        }
+        return;
+    }
+    double acc = 0.0;
+    for (int t = 0; t < STEPS; ++t) {
+        const int s = t % D;
+        pg::mbar_wait(&full[s], (uint32_t)((t / D) & 1));
+        for (int i = lane; i < CHUNK / 8; i += 32) acc += stage[s][i];
+        __syncwarp();
+        if (lane == 0) pg::mbar_arrive(&empty[s]);
+    }
+    out[threadIdx.x] = acc;
+}
+
 int main() {
     const int n = STEPS * CHUNK / 8;
     double *h = new double[n], *src, *out;
@@ -52,11 +85,18 @@ int main() {
     cudaMalloc(&src, n * 8);
     cudaMalloc(&out, 32 * CONS * 8);
     cudaMemcpy(src, h, n * 8, cudaMemcpyHostToDevice);
-    ring<<<1, 32 * (CONS + 1)>>>(src, out);
-    double o[32 * CONS];
-    cudaMemcpy(o, out, sizeof(o), cudaMemcpyDeviceToHost);
-    bool ok = cudaGetLastError() == cudaSuccess;
-    for (int i = 0; i < 32 * CONS; ++i) ok = ok && o[i] == STEPS * 4.0;
-    printf("racecheck_probe: ring result %s\n", ok ? "correct" : "WRONG");
-    return ok ? 0 : 1;
+    bool all = true;
+    for (int v = 0; v < 2; ++v) {
+        cudaMemset(out, 0, 32 * CONS * 8);
+        if (v == 0) ring<<<1, 32 * (CONS + 1)>>>(src, out);
+        else ring_cpasync<<<1, 32 * (CONS + 1)>>>(src, out);
+        double o[32 * CONS];
+        cudaMemcpy(o, out, sizeof(o), cudaMemcpyDeviceToHost);
+        bool ok = cudaGetLastError() == cudaSuccess;
+        for (int i = 0; i < 32 * CONS; ++i) ok = ok && o[i] == STEPS * 4.0;
+        printf("racecheck_probe: %s ring result %s\n", v ? "cp.async + mbarrier" : "bulk-copy + mbarrier",
+               ok ? "correct" : "WRONG");
+        all = all && ok;
+    }
+    return all ? 0 : 1;
 }
