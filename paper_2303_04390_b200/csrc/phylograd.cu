@@ -45,7 +45,7 @@ struct Layout {
         off_post, off_pre, total;
     // codon (variant 2) extras
     size_t off_M0one = 0, off_PBpre = 0, off_DT = 0, off_PONE = 0, off_QB = 0, off_q = 0, off_E = 0, off_child = 0,
-           off_levels = 0, off_lev4 = 0, off_tipmode = 0, off_utip = 0, off_tipmask = 0, off_tipmasked = 0, off_VA = 0, off_ViB = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0,
+           off_levels = 0, off_lev4 = 0, off_taskoff = 0, off_tipmode = 0, off_utip = 0, off_tipmask = 0, off_tipmasked = 0, off_VA = 0, off_ViB = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0,
            off_flow = 0, flow_bytes = 0, reset_bytes = 0;
     // time-tree parameterisation: parent/child_a/child_b [3][2N-1], heights, rate scalars, branch sets
     size_t off_tree = 0, off_h = 0, off_rho = 0, off_bset = 0;
@@ -185,6 +185,7 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         L->off_child = take((size_t)2 * (2 * N - 1) * 4);
         L->off_levels = take((size_t)2 * (N - 1) * 4);
         L->off_lev4 = take((size_t)2 * (N - 1) * 16);
+        L->off_taskoff = take((size_t)(2 * (N - 1) + 1) * 4);
         L->off_tipmode = take((size_t)N);
     }
     L->total = o;
@@ -237,6 +238,9 @@ struct pg_instance {
     int flow_ver = 2;                   // codon flow kernel: 2 = warp-specialised TMA ring (codon_flow2_kernel), 1 = round-1 kernel
     int flow_nst = 2;                   // codon_flow2_kernel ring stages (1: latency, 2: throughput)
     int flow_pdl = 0;                   // A1 -> flow programmatic dependent launch (PG_FLOW_PDL=0/1 overrides)
+    int flow_pub = 1;                   // flow v2: publisher warp (PG_FLOW_PUB)
+    int flow_pprod = 0;                 // flow v2: the producer forms p = u_a o u_b (PG_FLOW_PPROD)
+    int split_items = 0;                // items of the split schedule (task offsets table)
     int flow_split = 0;                 // codon_flow2_kernel: one pre item per child (PG_FLOW_SPLIT=0/1 overrides)
     int flow_rs = 1;                    // codon_flow2_kernel: rows of a product split over 2x the warps (PG_FLOW_RS)
     pg::codon::TmaMaps tmaps{};         // TMA tensor maps of u, q, utip (codon_flow2_kernel)
@@ -1032,6 +1036,10 @@ static int configure(pg_instance *inst) {
             // 0.297 -> 0.206 ms, WNV x8 0.579 -> 0.462 ms; scripts/gpu_codon3.sh)
             const char *se = getenv("PG_FLOW_SPLIT");
             inst->flow_split = se ? (atoi(se) != 0) : latency;
+            const char *ppe = getenv("PG_FLOW_PPROD");
+            inst->flow_pprod = ppe ? (atoi(ppe) != 0) : 0;
+            const char *pbe = getenv("PG_FLOW_PUB");
+            inst->flow_pub = pbe ? (atoi(pbe) != 0) : 1;
             const char *re = getenv("PG_FLOW_RS");
             inst->flow_rs = (L.SP == 64 && inst->flow_nst == 2 && re && atoi(re) == 2) ? 2 : 1;
             if (cf.flow2rs)
@@ -1119,6 +1127,21 @@ static int refresh_plan(pg_instance *inst) {
         }
         CK(cudaMemcpyAsync(inst->ws + inst->L.off_lev4, l4.data(), l4.size() * 4, cudaMemcpyHostToDevice, inst->stream),
            "level table upload");
+        // flow v2 split schedule: first item of every task.  A pre task is
+        // split into one item group per child only when BOTH children are
+        // internal (two q GEMMs to run in parallel); a parent with a tip child
+        // has at most one q GEMM, and a tip child's Eq. 8 terms are a row
+        // gather, too little work for an item of its own
+        const int per = inst->cfg.categories * inst->L.n_tiles;
+        std::vector<int32_t> toff(inst->plan.level_nodes.size() + 1, 0);
+        const int npost_tasks = inst->plan.post_off.back();
+        for (size_t i = 0; i < inst->plan.level_nodes.size(); ++i) {
+            const bool two = (int)i >= npost_tasks && l4[4 * i + 1] >= N && l4[4 * i + 2] >= N;
+            toff[i + 1] = toff[i] + (two ? 2 : 1) * per;
+        }
+        inst->split_items = toff.back();
+        CK(cudaMemcpyAsync(inst->ws + inst->L.off_taskoff, toff.data(), toff.size() * 4, cudaMemcpyHostToDevice,
+                           inst->stream), "task offsets upload");
     }
     CK(cudaStreamSynchronize(inst->stream), "plan upload sync");
     int rc = configure(inst);
@@ -1348,7 +1371,10 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
                                                                                                           : nullptr;
             if (inst->flow_ver == 2) {
                 f.split = inst->flow_split;
-                const int items2 = (f.npost + (f.ntask - f.npost) * (f.split ? 2 : 1)) * R * L.n_tiles;
+                f.task_off = inst->at<int>(L.off_taskoff);
+                f.pprod = inst->flow_pprod;
+                f.pub = inst->flow_pub;
+                const int items2 = f.split ? inst->split_items : f.ntask * R * L.n_tiles;
                 const int v = inst->flow_nst - 1;
                 // programmatic dependent launch right behind A1 (no partial-tip
                 // kernels or timing events in between): items wait on pready

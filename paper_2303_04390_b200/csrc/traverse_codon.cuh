@@ -411,6 +411,9 @@ struct FlowArgs {
     unsigned long long *trace;   // diagnostics (PG_FLOW_TRACE): [item][TRW] = {smid, t_take, t_ready, t_done, phase stamps}
     const int *pready;           // codon_flow2_kernel under PDL: [B][R] A1 done flags (null: A1 finished before launch)
     int split;                   // codon_flow2_kernel: one pre item per child (latency-bound shards)
+    const int *task_off;         // split schedule: [ntask + 1] first item of each task
+    int pprod;                   // codon_flow2_kernel: the producer forms p = u_a o u_b of post items
+    int pub;                     // codon_flow2_kernel: a publisher warp raises the completion flags
 };
 
 // ---------------------------------------------------------------------------

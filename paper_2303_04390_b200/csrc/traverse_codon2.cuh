@@ -113,7 +113,8 @@ struct alignas(16) Meta2 {
 // 8 h + w: output columns 8w..8w+7, row blocks 2h, 2h+1): half the DMMA chain
 // per warp on the latency-bound shards (SP = 64 only: 16 + 1 warps)
 template <int SP, int NST, int RS = 1> constexpr int flow2_ctas() { return RS == 2 ? 1 : SP == 64 ? (NST == 1 ? 3 : 2) : 1; }
-template <int SP, int RS = 1> constexpr int flow2_threads() { return (SP / 8 * RS + 1) * 32; }
+// consumer warps + the producer warp + the publisher warp
+template <int SP, int RS = 1> constexpr int flow2_threads() { return (SP / 8 * RS + 2) * 32; }
 template <int SP> constexpr size_t flow2_stage() { return (size_t)3 * T * SP * 8 + ((sizeof(Meta2) + 127) / 128) * 128; }
 template <int SP, int NST>
 constexpr size_t flow2_smem() {
@@ -138,29 +139,39 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
     extern __shared__ __align__(128) unsigned char smem2[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem2);
     uint64_t *empty = full + NST;
+    uint64_t *ldb = full + 2 * NST;              // f.pprod: the stage's copies landed (producer-side p)
+    uint64_t *pub = full + 3 * NST;              // f.pub: the consumer warps' outputs are issued
     unsigned char *ring = smem2 + 128;
     double *part = reinterpret_cast<double *>(ring + NST * STG);          // [3][NW][T]
-    const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty);
+    const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty), ldb_u = smem_u32(ldb), pub_u = smem_u32(pub);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int R = a.R, ntiles = a.ntiles, N = a.N;
     const int root = 2 * N - 2;
     // items: post (task, r, tile); pre (task, r, tile) for both children, or
-    // with f.split (task, child, r, tile): one child each -- the two q GEMMs
-    // of a parent then run on different CTAs (shorter pre-order chain links)
+    // with f.split, for a parent whose children are both internal, (task,
+    // child, r, tile): one child each -- the two q GEMMs of the parent then
+    // run on different CTAs (shorter pre-order chain links); f.task_off holds
+    // the first item of every task
     const int npost_items = f.npost * R * ntiles;
-    const int nitems = npost_items + (f.ntask - f.npost) * R * ntiles * (f.split ? 2 : 1);
+    const int nitems = f.split ? f.task_off[f.ntask] : f.ntask * R * ntiles;
     auto tileA = [&](int s) { return reinterpret_cast<double *>(ring + s * STG); };
     auto meta = [&](int s) { return reinterpret_cast<Meta2 *>(ring + s * STG + 3 * (size_t)TILE * 8); };
     if (threadIdx.x == 0) {
         // full: lane 0's expect_tx arrive + the 32 lanes' cp.async arrives +
         // lane 0's final arrive (after the metadata stores)
-        for (int i = 0; i < NST; ++i) { mbar_init(full + i, 34); mbar_init(empty + i, 1); }
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(full + i, 34);
+            mbar_init(empty + i, 1);
+            mbar_init(ldb + i, 34);
+            mbar_init(pub + i, NWC);
+        }
         fence_mbar_init();
     }
     __syncthreads();
 
     // ================================ producer ================================
     if (warp == NWC) {
+        uint32_t ldph = 0;                           // ldb phase bits per stage
         for (int g = 0;; ++g) {
             const int s = g % NST;
             if (g >= NST) mbar_wait_sleep(empty_u + 8u * s, (uint32_t)(g / NST + 1) & 1u);
@@ -168,8 +179,8 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
             if (lane == 0) item = atomicAdd(f.ctr, 1);
             item = __shfl_sync(0xffffffffu, item, 0);
             Meta2 *m = meta(s);
-            const uint32_t bar = full_u + 8u * s;
             if (item >= nitems) {
+                const uint32_t bar = full_u + 8u * s;
                 if (lane == 0) m->item = -1;
                 cp_async_mbar_arrive(bar);
                 __syncwarp();
@@ -192,16 +203,29 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
                 task = item / (R * ntiles);
                 rem = item - task * R * ntiles;
             } else {
-                const int i2 = item - npost_items, per = 2 * R * ntiles;
-                task = f.npost + i2 / per;
-                const int rr = i2 - (task - f.npost) * per;
-                cs = rr / (R * ntiles);
-                rem = rr - cs * R * ntiles;
+                int lo = f.npost, hi = f.ntask - 1;      // last task starting at or before item
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (__ldg(f.task_off + mid) <= item) lo = mid;
+                    else hi = mid - 1;
+                }
+                task = lo;
+                const int rr = item - __ldg(f.task_off + task), per = R * ntiles;
+                if (__ldg(f.task_off + task + 1) - __ldg(f.task_off + task) == 2 * per) {
+                    cs = rr / per;
+                    rem = rr - cs * per;
+                } else {
+                    rem = rr;
+                }
             }
             const int r = rem / ntiles, tile = rem - r * ntiles;
             const int4 e = a.lev4[task];
             const int k = e.x, ca = e.y, cb = e.z, kinds = e.w;
             const bool post = task < f.npost;
+            // f.pprod: a post item's copies complete on ldb; the producer then
+            // forms p = u_a o u_b in place and completes "full" itself
+            const bool pp = f.pprod && post && k != root;
+            const uint32_t bar = (pp ? ldb_u : full_u) + 8u * s;
             if (lane == 0 && f.pready) {             // the item's P, P', D' rows written by A1
                 wait_p(f, k, r, R, root, a.status);
                 wait_p(f, ca, r, R, root, a.status);
@@ -305,6 +329,61 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
             cp_async_mbar_arrive(bar);
             __syncwarp();
             if (lane == 0) mbar_arrive_u32(bar);
+            if (pp) {
+                mbar_wait_sleep(bar, (ldph >> s) & 1u);
+                ldph ^= 1u << s;
+                double2 *pa = reinterpret_cast<double2 *>(tileA(s));
+                const double2 *pb = reinterpret_cast<const double2 *>(tileA(s) + TILE);
+                for (int i2 = lane; i2 < TILE / 2; i2 += 32) {
+                    double2 v = pa[i2];
+                    const double2 tb = pb[i2];
+                    v.x *= tb.x;
+                    v.y *= tb.y;
+                    pa[i2] = v;
+                }
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], 34;\n" ::"r"(full_u + 8u * s) : "memory");
+            }
+        }
+    }
+
+    // ================================ publisher ===============================
+    // f.pub: completion flags are raised by this warp, so the consumer warps
+    // never wait on the device-scope fence (its latency is ~1 us after a
+    // tile's stores).  Per stage use, every consumer warp arrives on "pub"
+    // once its outputs are issued (post: after the tile stores, which are also
+    // the warp's last reads of the stage; pre: after the q stores).  Ordering:
+    // each warp's stores -> __syncwarp -> mbarrier arrive (release.cta) ->
+    // this warp's wait (acquire.cta) -> __threadfence -> flag atomic; the
+    // reader acquires the flag at gpu scope (cumulativity of the PTX model,
+    // as with the bar.sync + thread-0 fence it replaces).
+    if (warp == NWC + 1) {
+        if (!f.pub) return;
+        for (int g = 0;; ++g) {
+            const int s = g % NST;
+            mbar_wait_sleep(pub_u + 8u * s, (uint32_t)(g / NST) & 1u);
+            const Meta2 *m = meta(s);
+            const int item = m->item;
+            if (item < 0) return;
+            if (lane == 0) {
+                const int k = m->lev.x, ca = m->lev.y, cb = m->lev.z, tile = m->tile, cs = m->cs;
+                unsigned long long *tr = f.trace ? f.trace + TRW * (size_t)item : nullptr;
+                if (m->task < f.npost) {
+                    mbar_arrive_u32(empty_u + 8u * s);   // fields read above: the stage is free
+                    __threadfence();
+                    atomicAdd(f.rpost + (size_t)(k - N) * ntiles + tile, 1);
+                } else {
+                    const bool pa = cs != 1 && ca >= N, pb = cs != 0 && cb >= N;
+                    if (pa || pb) {
+                        __threadfence();
+                        if (pa) atomicAdd(f.rpre + (size_t)(ca - N) * ntiles + tile, 1);
+                        if (pb) atomicAdd(f.rpre + (size_t)(cb - N) * ntiles + tile, 1);
+                    }
+                }
+                if (tr) tr[5] = gtimer();
+            }
+            __syncwarp();
         }
     }
 
@@ -315,7 +394,10 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
         mbar_wait_sleep(full_u + 8u * s, (uint32_t)(g / NST) & 1u);
         const Meta2 *m = meta(s);
         const int item = m->item;
-        if (item < 0) break;
+        if (item < 0) {
+            if (f.pub && lane == 0) mbar_arrive_u32(pub_u + 8u * s);   // the publisher sees the end too
+            break;
+        }
         const int r = m->r, tile = m->tile;
         const int k = m->lev.x, ca = m->lev.y, cb = m->lev.z, kinds = m->lev.w;
         const int pat0 = tile * T;
@@ -349,16 +431,19 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
             } else {
                 double bfr[KT];
                 load_bfrag<SP>(bfr, a.PBpost + ((size_t)k * R + r) * MAT, w, lane);
-                // p = u_a o u_b in place (one A operand for the GEMM)
-                for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += NTC) {
-                    double2 *pa = reinterpret_cast<double2 *>(As) + i2;
-                    const double2 tb = reinterpret_cast<const double2 *>(Bs)[i2];
-                    double2 v = *pa;
-                    v.x *= tb.x;
-                    v.y *= tb.y;
-                    *pa = v;
+                // p = u_a o u_b in place (one A operand for the GEMM), unless
+                // the producer formed it already
+                if (!f.pprod) {
+                    for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += NTC) {
+                        double2 *pa = reinterpret_cast<double2 *>(As) + i2;
+                        const double2 tb = reinterpret_cast<const double2 *>(Bs)[i2];
+                        double2 v = *pa;
+                        v.x *= tb.x;
+                        v.y *= tb.y;
+                        *pa = v;
+                    }
+                    consumer_sync(NTC);
                 }
-                consumer_sync(NTC);
                 double acc[MTW][2];
                 gemm_tile<SP, MTW>(acc, As + mt0 * KT * 32, bfr, lane);
                 if (tr) tr[4] = gtimer();
@@ -378,12 +463,19 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
                 }
             }
             fence_proxy_async_global();              // our generic stores -> later TMA reads (other CTAs)
+            if (f.pub) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive_u32(pub_u + 8u * s);
+                if (tr) tr[6] = gtimer();
+                continue;
+            }
+            if (tr) tr[5] = gtimer();
             consumer_sync(NTC);                      // stage consumed, outputs issued
             if (threadIdx.x == 0) {
                 __threadfence();
                 atomicAdd(f.rpost + (size_t)(k - N) * ntiles + tile, 1);
                 mbar_arrive_u32(empty_u + 8u * s);
-                if (tr) tr[5] = tr[6] = gtimer();
+                if (tr) tr[6] = gtimer();
             }
             continue;
         }
@@ -416,6 +508,12 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
             }
         };
         auto publish_q = [&](bool pa, bool pb) {
+            if (f.pub) {                             // every pre item arrives once
+                fence_proxy_async_global();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_u32(pub_u + 8u * s);
+                return;
+            }
             if (!pa && !pb) return;
             fence_proxy_async_global();
             consumer_sync(NTC);

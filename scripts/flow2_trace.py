@@ -28,11 +28,26 @@ R = len(pb.cat_rates)
 ntiles = (hi - lo + 31) // 32
 split = os.environ.get("PG_FLOW_SPLIT", "1" if ntiles * R < 296 else "0") != "0"
 npost = pb.n_tips - 1
-n_items = npost * R * ntiles * (3 if split else 2)
-t = t[:n_items]
-# per task rows: post tasks R*ntiles items, pre tasks (2 if split) R*ntiles
-bounds = [k * R * ntiles for k in range(npost + 1)]
-bounds += [bounds[-1] + (k + 1) * R * ntiles * (2 if split else 1) for k in range(npost)]
+# task order of schedule.cpp: post tasks by height, pre tasks by depth (stable
+# in op order); a split pre task has one item group per child only when both
+# children are internal
+N = pb.n_tips
+ops = np.asarray(pb.ops)
+height, depth = {}, {}
+for d, a_, b_ in ops:
+    height[d] = 1 + max(height.get(a_, 0), height.get(b_, 0))
+depth[ops[-1][0]] = 0
+for d, a_, b_ in ops[::-1]:
+    depth[a_] = depth[b_] = depth[d] + 1
+post_order = sorted(range(len(ops)), key=lambda o: (height[ops[o][0]], o))
+pre_order = sorted(range(len(ops)), key=lambda o: (depth[ops[o][0]], -o))
+bounds = [0]
+for o in post_order:
+    bounds.append(bounds[-1] + R * ntiles)
+for o in pre_order:
+    two = split and ops[o][1] >= N and ops[o][2] >= N
+    bounds.append(bounds[-1] + R * ntiles * (2 if two else 1))
+t = t[:bounds[-1]]
 ntask = len(bounds) - 1
 t0 = t[:, 1].min()
 claim, ready, full, gemm, pub, end = [(t[:, i] - t0) / 1e3 for i in range(1, 7)]
@@ -41,7 +56,22 @@ print(f"config {cfg} shards {shards}: items {len(t)} tasks {ntask} span {end.max
 print(f"mean us: claim->ready {np.mean(ready - claim):.2f}  ready->full {np.mean(full - ready):.2f}  "
       f"full->gemm {np.mean(gemm - full):.2f}  gemm->pub {np.mean(pub - gemm):.2f}  pub->end {np.mean(end - pub):.2f}  "
       f"full->end {np.mean(end - full):.2f}")
-npost = info.get("npost", None)
+npi = npost * R * ntiles
+for name, sl in (("post", slice(0, npi)), ("pre", slice(npi, None))):
+    print(f"{name:4s} items {len(t[sl])}: claim->ready {np.mean((ready - claim)[sl]):.2f}  ready->full "
+          f"{np.mean((full - ready)[sl]):.2f}  full->gemm {np.mean((gemm - full)[sl]):.2f}  gemm->pub "
+          f"{np.mean((pub - gemm)[sl]):.2f}  pub->end {np.mean((end - pub)[sl]):.2f}  full->end {np.mean((end - full)[sl]):.2f}")
+# consumer duty per CTA: time between one item's end and the next item's full
+cta = t[:, 7]
+gaps, busy = [], 0.0
+for c in np.unique(cta):
+    ii = np.where(cta == c)[0]
+    ii = ii[np.argsort(full[ii])]
+    gaps += list(full[ii][1:] - end[ii][:-1])
+    busy += float(np.sum(end[ii] - full[ii]))
+print(f"consumer idle between items: mean {np.mean(gaps):.2f} us; consumers busy {busy / (len(np.unique(cta)) * end.max()):.3f} of span")
+if os.environ.get("TRACE_SUMMARY_ONLY"):
+    sys.exit(0)
 for k in range(ntask):
     s = slice(bounds[k], bounds[k + 1])
     print(f"task {k:3d}  claim {claim[s].min():7.1f}  ready {ready[s].min():7.1f}..{ready[s].max():7.1f}  "

@@ -1,4 +1,9 @@
+#!/bin/bash
+# flow v2 item traces: full yeast, yeast 8-way shard, WNV
+set -x
+cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-timeout 300 python scripts/flow_trace.py 3 8 > gpurun_out/flow_trace_yeast8.txt 2>&1; head -8 gpurun_out/flow_trace_yeast8.txt
-timeout 300 python scripts/flow_trace.py 3 1 > gpurun_out/flow_trace_yeast1.txt 2>&1; head -4 gpurun_out/flow_trace_yeast1.txt
-bash scripts/gpu_sweep.sh
+TRACE_SUMMARY_ONLY=1 python scripts/flow2_trace.py 3 1 > gpurun_out/trace_3_1.txt 2>&1
+python scripts/flow2_trace.py 3 8 > gpurun_out/trace_3_8.txt 2>&1
+TRACE_SUMMARY_ONLY=1 python scripts/flow2_trace.py 4 1 > gpurun_out/trace_4_1.txt 2>&1
+head -8 gpurun_out/trace_3_1.txt gpurun_out/trace_3_8.txt gpurun_out/trace_4_1.txt

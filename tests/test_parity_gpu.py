@@ -448,6 +448,9 @@ def test_hmc_leapfrog_matches_oracle_trajectory(model, N, R, C):
                                  {"PG_FLOW_RS": "2"}, {"PG_FLOW_RS": "2", "PG_FLOW_SPLIT": "1"},
                                  {"PG_FLOW_RS": "2", "PG_FLOW_SPLIT": "0"},
                                  {"PG_FLOW_SPLIT": "0", "PG_FLOW_PDL": "1"}, {"PG_FLOW_SPLIT": "1", "PG_FLOW_NST": "1"},
+                                 {"PG_FLOW_PPROD": "1"}, {"PG_FLOW_PPROD": "1", "PG_FLOW_SPLIT": "1"},
+                                 {"PG_FLOW_PPROD": "1", "PG_FLOW_NST": "1"}, {"PG_FLOW_PUB": "0"},
+                                 {"PG_FLOW_PUB": "0", "PG_FLOW_SPLIT": "1"}, {"PG_FLOW_PUB": "1", "PG_FLOW_RS": "2"},
                                  {"PG_CODON_FLOW": "1", "PG_FLOW_TCH": "3"},
                                  {"PG_CODON_FLOW": "1", "PG_FLOW_TCH": "1"},
                                  {"PG_CODON_FLOW": "1", "PG_FLOW_DEFER": "1"},
