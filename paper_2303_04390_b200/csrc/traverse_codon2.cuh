@@ -118,7 +118,7 @@ template <int SP, int RS = 1> constexpr int flow2_threads() { return (SP / 8 * R
 template <int SP> constexpr size_t flow2_stage() { return (size_t)3 * T * SP * 8 + ((sizeof(Meta2) + 127) / 128) * 128; }
 template <int SP, int NST>
 constexpr size_t flow2_smem() {
-    return 128 + (size_t)NST * flow2_stage<SP>() + (size_t)3 * (SP / 8) * T * 8;   // barriers, ring, Eq. 8 partials
+    return 128 + (size_t)NST * flow2_stage<SP>() + (size_t)NST * 3 * (SP / 8) * T * 8;   // barriers, ring, Eq. 8 partials per stage
 }
 
 // A1 -> flow overlap (programmatic dependent launch): the flow kernel may
@@ -141,9 +141,12 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
     uint64_t *empty = full + NST;
     uint64_t *ldb = full + 2 * NST;              // f.pprod: the stage's copies landed (producer-side p)
     uint64_t *pub = full + 3 * NST;              // f.pub: the consumer warps' outputs are issued
+    uint64_t *done = full + 4 * NST;             // f.pub: a pre item's Eq. 8 partials are written
     unsigned char *ring = smem2 + 128;
-    double *part = reinterpret_cast<double *>(ring + NST * STG);          // [3][NW][T]
-    const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty), ldb_u = smem_u32(ldb), pub_u = smem_u32(pub);
+    double *part0 = reinterpret_cast<double *>(ring + NST * STG);         // [NST][3][NW][T]
+    auto partS = [&](int s) { return part0 + (size_t)s * 3 * NW * T; };
+    const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty), ldb_u = smem_u32(ldb), pub_u = smem_u32(pub),
+                   done_u = smem_u32(done);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int R = a.R, ntiles = a.ntiles, N = a.N;
     const int root = 2 * N - 2;
@@ -164,6 +167,7 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
             mbar_init(empty + i, 1);
             mbar_init(ldb + i, 34);
             mbar_init(pub + i, NWC);
+            mbar_init(done + i, NWC);
         }
         fence_mbar_init();
     }
@@ -348,6 +352,26 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
         }
     }
 
+    // Eq. 8 terms of a pre item -> numden: fixed-order sums over the column
+    // warps' partials (pattern mm), weights w_r and gamma_r w_r (Eq. 8)
+    auto finish_pre = [&](const Meta2 *m, const double *part, int mm) {
+        const int r = m->r, cs = m->cs, ca = m->lev.y, cb = m->lev.z, kinds = m->lev.w;
+        const int c0 = cs < 0 ? 0 : cs, c1 = cs < 0 ? 1 : cs;
+        double sd = 0.0, sn0 = 0.0, sn1 = 0.0;
+        for (int ww = 0; ww < NW; ++ww) {
+            if (c0 == 0) sn0 += part[ww * T + mm];
+            if (c1 == 1) sn1 += part[(NW + ww) * T + mm];
+            sd += part[(2 * NW + ww) * T + mm];
+        }
+        const double wr = a.cat_w[r], gr = a.cat_g[r];
+        double2 *nd = reinterpret_cast<double2 *>(a.numden);
+        const bool qa = ca >= N || (kinds & 3) == 2, qb = cb >= N || ((kinds >> 2) & 3) == 2;
+        const double s0 = qa ? gr * wr : wr, s1 = qb ? gr * wr : wr;
+        const size_t pat = (size_t)m->tile * T + mm;
+        if (c0 == 0) nd[((size_t)ca * R + r) * a.Cpad + pat] = make_double2(s0 * sn0, wr * sd);
+        if (c1 == 1) nd[((size_t)cb * R + r) * a.Cpad + pat] = make_double2(s1 * sn1, wr * sd);
+    };
+
     // ================================ publisher ===============================
     // f.pub: completion flags are raised by this warp, so the consumer warps
     // never wait on the device-scope fence (its latency is ~1 us after a
@@ -358,18 +382,24 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
     // this warp's wait (acquire.cta) -> __threadfence -> flag atomic; the
     // reader acquires the flag at gpu scope (cumulativity of the PTX model,
     // as with the bar.sync + thread-0 fence it replaces).
+    // A pre item's consumers then write their Eq. 8 partials and arrive on
+    // "done"; this warp forms the fixed-order sums (lane = pattern), stores
+    // numden and releases the stage -- the consumers go straight on to the
+    // next item.
     if (warp == NWC + 1) {
         if (!f.pub) return;
+        uint32_t dph = 0;                            // done phase bits per stage
         for (int g = 0;; ++g) {
             const int s = g % NST;
             mbar_wait_sleep(pub_u + 8u * s, (uint32_t)(g / NST) & 1u);
             const Meta2 *m = meta(s);
             const int item = m->item;
             if (item < 0) return;
+            const int k = m->lev.x, ca = m->lev.y, cb = m->lev.z, tile = m->tile, cs = m->cs;
+            const bool post = m->task < f.npost;
+            unsigned long long *tr = (f.trace && lane == 0) ? f.trace + TRW * (size_t)item : nullptr;
             if (lane == 0) {
-                const int k = m->lev.x, ca = m->lev.y, cb = m->lev.z, tile = m->tile, cs = m->cs;
-                unsigned long long *tr = f.trace ? f.trace + TRW * (size_t)item : nullptr;
-                if (m->task < f.npost) {
+                if (post) {
                     mbar_arrive_u32(empty_u + 8u * s);   // fields read above: the stage is free
                     __threadfence();
                     atomicAdd(f.rpost + (size_t)(k - N) * ntiles + tile, 1);
@@ -382,6 +412,14 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
                     }
                 }
                 if (tr) tr[5] = gtimer();
+            }
+            if (!post) {
+                mbar_wait_sleep(done_u + 8u * s, (dph >> s) & 1u);
+                dph ^= 1u << s;
+                finish_pre(m, partS(s), lane);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_u32(empty_u + 8u * s);
+                if (tr) tr[6] = gtimer();
             }
             __syncwarp();
         }
@@ -404,6 +442,7 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
         unsigned long long *tr = (f.trace && threadIdx.x == 0) ? f.trace + TRW * (size_t)item : nullptr;
         if (tr) tr[3] = gtimer();
         double *As = tileA(s), *Bs = As + TILE, *Qs = As + 2 * (size_t)TILE;
+        double *part = partS(s);
         const bool post = m->task < f.npost;
         if (post) {
             auto scA = [&](int mm) { return ca >= N ? pow2neg(lazy_exp(m->fa[mm])) : 1.0; };
@@ -639,23 +678,13 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
             eq8(0, true, xq(0));
             eq8(1, false, xq(1));
         }
-        const int c0 = cs < 0 ? 0 : cs, c1 = cs < 0 ? 1 : cs;
-        consumer_sync(NTC);                          // stage and partials complete
-        if (threadIdx.x < T) {                       // fixed-order sums over the warps
-            const int mm = threadIdx.x;
-            double sd = 0.0, sn0 = 0.0, sn1 = 0.0;
-            for (int ww = 0; ww < NW; ++ww) {
-                if (c0 == 0) sn0 += part[ww * T + mm];
-                if (c1 == 1) sn1 += part[(NW + ww) * T + mm];
-                sd += part[(2 * NW + ww) * T + mm];
-            }
-            const double wr = a.cat_w[r], gr = a.cat_g[r];
-            double2 *nd = reinterpret_cast<double2 *>(a.numden);
-            const bool qa = ca >= N || (kinds & 3) == 2, qb = cb >= N || ((kinds >> 2) & 3) == 2;
-            const double s0 = qa ? gr * wr : wr, s1 = qb ? gr * wr : wr;
-            if (c0 == 0) nd[((size_t)ca * R + r) * a.Cpad + pat0 + mm] = make_double2(s0 * sn0, wr * sd);
-            if (c1 == 1) nd[((size_t)cb * R + r) * a.Cpad + pat0 + mm] = make_double2(s1 * sn1, wr * sd);
+        if (f.pub) {                                 // the publisher sums the partials and frees the stage
+            __syncwarp();
+            if (lane == 0) mbar_arrive_u32(done_u + 8u * s);
+            continue;
         }
+        consumer_sync(NTC);                          // stage and partials complete
+        if (threadIdx.x < T) finish_pre(m, part, threadIdx.x);   // fixed-order sums over the warps
         consumer_sync(NTC);                          // partials read before the next item writes them
         if (threadIdx.x == 0) mbar_arrive_u32(empty_u + 8u * s);
         if (tr) tr[6] = gtimer();
