@@ -890,6 +890,7 @@ constexpr size_t tipu_smem() { return (size_t)2 * T * SP * 8; }
 // (V pre-arranged as A fragments, V^{-1} as B fragments at set_eigen); the
 // results are written as PBpost, PBpre, P', D', P 1.
 // ---------------------------------------------------------------------------
+constexpr int PMAT_P_DONE = 1, PMAT_D_DONE = 256;         // pready increments per (branch, r): P CTA, D CTA
 template <int SP>
 __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restrict__ VA,
                                                          const double *__restrict__ ViB,
@@ -989,14 +990,13 @@ __global__ void __launch_bounds__(256) codon_pmat_kernel(const double *__restric
             }
         __syncthreads();
     }
-    if (pready && threadIdx.x == 0) {                    // publish (release): 2 CTAs per (branch, r)
+    if (pready && threadIdx.x == 0) {                    // publish (release): P and D CTAs per (branch, r)
         __threadfence();
-        atomicAdd(pready + br, 1);
+        atomicAdd(pready + br, pass ? PMAT_D_DONE : PMAT_P_DONE);
     }
 }
 template <int SP>
 constexpr size_t pmat_smem() { return ((size_t)SP * (SP + 1) + 2 * SP + (SP == 64 ? (size_t)SP * SP : 0)) * 8; }
-constexpr int PMAT_FLAGS = 2;                            // pready count per (branch, r): the P and D CTAs
 
 }  // namespace codon
 }  // namespace pg

@@ -78,12 +78,12 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
 // ~20 s (a schedule bug, or a neighbour that never lets a CTA run) is
 // reported through status[1] instead of trapping, and the wait gives up so
 // the launch terminates; pg_check_status / pg_compute turn it into an error.
-__device__ __forceinline__ void wait_count2(const int *p, int v, int *status) {
+__device__ __forceinline__ void wait_count2(const int *p, int v, int *status, int mask = -1) {
     int x;
     const unsigned long long t0 = gtimer();
     for (unsigned it = 0;; ++it) {
         asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
-        if (x >= v) return;
+        if ((x & mask) >= v) return;
         if ((it & 1023u) == 1023u && gtimer() - t0 > 20000000000ull) {
             atomicExch(status + 1, 1);
             return;
@@ -123,9 +123,16 @@ constexpr size_t flow2_smem() {
 
 // A1 -> flow overlap (programmatic dependent launch): the flow kernel may
 // start while codon_pmat_kernel is still running; an item then also waits
-// until the transition matrices it reads are published (pready[branch][r]).
-__device__ __forceinline__ void wait_p(const FlowArgs &f, int node, int r, int R, int root, int *status) {
-    if (f.pready && node != root) wait_count2(f.pready + (size_t)node * R + r, PMAT_FLAGS, status);
+// until the transition matrices it reads are published (pready[branch][r]:
+// + PMAT_P_DONE by the branch's P CTA, + PMAT_D_DONE by its D CTA).  Post
+// items read P of the node and of tip children; pre items P of the children
+// and D of tip children.
+__device__ __forceinline__ void wait_p(const FlowArgs &f, int node, int r, int R, int root, bool need_d, int *status) {
+    if (f.pready && node != root) {
+        const int *p = f.pready + (size_t)node * R + r;
+        if (need_d) wait_count2(p, PMAT_P_DONE + PMAT_D_DONE, status);
+        else wait_count2(p, PMAT_P_DONE, status, PMAT_D_DONE - 1);
+    }
 }
 
 template <int SP, int NST, int RS = 1>
@@ -231,9 +238,14 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
             const bool pp = f.pprod && post && k != root;
             const uint32_t bar = (pp ? ldb_u : full_u) + 8u * s;
             if (lane == 0 && f.pready) {             // the item's P, P', D' rows written by A1
-                wait_p(f, k, r, R, root, a.status);
-                wait_p(f, ca, r, R, root, a.status);
-                wait_p(f, cb, r, R, root, a.status);
+                if (post) {
+                    wait_p(f, k, r, R, root, false, a.status);
+                    if (ca < N) wait_p(f, ca, r, R, root, false, a.status);
+                    if (cb < N) wait_p(f, cb, r, R, root, false, a.status);
+                } else {
+                    if (cs != 1) wait_p(f, ca, r, R, root, ca < N, a.status);
+                    if (cs != 0) wait_p(f, cb, r, R, root, cb < N, a.status);
+                }
             }
             __syncwarp();
             // ---- what does not depend on other items, before the wait:
