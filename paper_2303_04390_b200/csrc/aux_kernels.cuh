@@ -39,6 +39,17 @@ __global__ void __launch_bounds__(256) pmat_kernel(const double *__restrict__ V,
         Pm[idx] = (Real)acc;
         if (PTm) PTm[u * SP + s] = (Real)acc;
     }
+    // a category pad that holds SP Reals carries P 1 (row sums, summed in
+    // column order like the traversal's missing-state tip gather): the
+    // small-S kernel then reads column `state` or this vector without a branch
+    if (cs >= SP * SP + SP) {
+        __syncthreads();
+        for (int s = threadIdx.x; s < SP; s += blockDim.x) {
+            Real acc = Pm[s * SP];
+            for (int u = 1; u < SP; ++u) acc += Pm[s * SP + u];
+            Pm[SP * SP + s] = acc;
+        }
+    }
 }
 
 // A1 for the FP64 tensor-core S = 16 traversal (traverse_small.cuh,

@@ -40,9 +40,6 @@
 #pragma once
 #include "common.cuh"
 
-#ifndef PG_SMALL_W
-#define PG_SMALL_W 2
-#endif
 #ifndef PG_MMA_STAGES
 #define PG_MMA_STAGES 8
 #endif
@@ -148,12 +145,23 @@ struct SmallCfg {
 #else
     static constexpr int PF = 32;                              // L2 prefetch distance (steps; 16: +0.4 %, scripts/gpu_pf.sh)
 #endif
-    static constexpr int W = PG_SMALL_W;                       // gradient window (steps)
+    // gradient window (steps): per pre step the lanes of a pattern sum their
+    // (num_a, num_b, den) shares (xor shuffles) and one lane stores the three
+    // totals; every W steps the warp forms the Eq. 8 ratios of W x TP
+    // (step, pattern) items, PPL per lane (ILP instead of a per-2-step
+    // latency chain); W TP 3 doubles per warp
+#ifdef PG_SMALL_W
+    static constexpr int W = PG_SMALL_W;
+#else
+    static constexpr int W = (64 / TP) < 32 ? ((64 / TP) > 0 ? 64 / TP : 1) : 32;
+#endif
+    static constexpr int LPS = 32 / W;                         // lanes per window step
+    static constexpr int PPL = TP / LPS > 0 ? TP / LPS : 1;    // patterns per lane in a flush
     static constexpr int VB = SP * (int)sizeof(Real);          // vector bytes
     static constexpr int VBL = VL * (int)sizeof(Real);         // one lane's part of a vector
     static constexpr int MATB = SP * SP * (int)sizeof(Real);   // one category's matrix
     static constexpr int CS = MATB + (RP > 1 ? small_cat_pad(sizeof(Real), SP) : 0);   // padded category stride
-    static constexpr int ND = W * 2 * 32 * 16;                 // (num, den) window per warp
+    static constexpr int ND = W * TP * 3 * 8;                  // (num_a, num_b, den) window per warp
     static constexpr int XGS = VB + 16;                        // exchange stride per lane group (bank skew)
     static constexpr int XB = (LV > 1 && !MMA) ? (32 / LV) * XGS : 0;   // full-vector exchange buffer per warp
 #ifdef PG_OPS
@@ -292,8 +300,16 @@ __device__ __forceinline__ void lds_rot(Real (&x)[SP], const unsigned char *src,
     }
 }
 // u = entries [h VL, +VL) of column s of M (observed tip state) or of M 1 (missing, s >= S)
-template <typename Real, int SP, int VL>
+// ONECOL: M 1 is stored right after M (pmat_kernel fills the category pad),
+// so both cases are one gather with no divergent branch
+template <typename Real, int SP, int VL, bool ONECOL = false>
 __device__ __forceinline__ void mcol(Real (&u)[VL], const Real *M, int s, int S, int h) {
+    if constexpr (ONECOL) {
+        const bool obs = s < S;
+#pragma unroll
+        for (int x = 0; x < VL; ++x) u[x] = M[obs ? (h * VL + x) * SP + s : SP * SP + h * VL + x];
+        return;
+    }
     if (s < S) {
 #pragma unroll
         for (int x = 0; x < VL; ++x) u[x] = M[(h * VL + x) * SP + s];
@@ -600,7 +616,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     unsigned char *wsm = stages + DS * OPS * ST + (size_t)warp * Cfg::warp_bytes(a.depth);
     unsigned char *stackb = wsm;
     const int pi_slot = a.depth;
-    double2 *nd = reinterpret_cast<double2 *>(wsm + (a.depth + 1) * 32 * VBL);     // [W][2][32]
+    double *nd = reinterpret_cast<double *>(wsm + (a.depth + 1) * 32 * VBL);       // [W][TP][3]
     unsigned char *xb = wsm + (a.depth + 1) * 32 * VBL + Cfg::ND;                  // exchange [32/LV][XGS]
     double *wbuf = reinterpret_cast<double *>(xb + Cfg::XB);                        // [TP]
     int *nodes_w = reinterpret_cast<int *>(wbuf + TP);                              // [W][2] branch ids
@@ -716,7 +732,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             lds_rot<Real, SP, VL>(tp, vs + tipp_vec, h);
             mv<Real, SP, VL>(u, M, tp, h);
         } else {
-            mcol<Real, SP, VL>(u, M, vs[tip_idx], S, h);
+            mcol<Real, SP, VL, (CS - Cfg::MATB >= VB)>(u, M, vs[tip_idx], S, h);
         }
     };
 
@@ -895,19 +911,19 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             }
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 6, qc[0][0] + qc[1][0]);
         release(t);                                 // stage no longer needed
-        double2 *ndw = nd + (n % W) * 64 + lane;
+        // Eq. 8 terms: my states' shares of num_c = x_c' Q u_c for both
+        // children and of den = x_c' u_c, which is the same number for both
+        // children (q_k o u_a o u_b, Eq. 5): formed once
+        Real num[2], den = 0;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-            if (lane == 0) nodes_w[(n % W) * 2 + c] = cs[c] & ~kTipPartialBit;
-            // my states' share of num = x' Q u_c and den = x' u_c (summed over
-            // the pattern's lanes in the window flush)
-            Real num = 0, den = 0;
+            num[c] = 0;
             if constexpr (MMA4) {                  // weighted over the lane's categories here
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const double Qu = dmma4(uc[c][q], QB[0]);
-                    num = fma(gwR[q] * x[c][q], Qu, num);
-                    den = fma(wR[q] * x[c][q], uc[c][q], den);
+                    num[c] = fma(gwR[q] * x[c][q], Qu, num[c]);
+                    if (c == 0) den = fma(wR[q] * x[c][q], uc[c][q], den);
                 }
             }
             if constexpr (MMA) {
@@ -915,8 +931,8 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
                 dmma16r(Qu, uc[c], QB);
 #pragma unroll
                 for (int s = 0; s < 4; ++s) {
-                    num = fma(x[c][s], Qu[s], num);
-                    den = fma(x[c][s], uc[c][s], den);
+                    num[c] = fma(x[c][s], Qu[s], num[c]);
+                    if (c == 0) den = fma(x[c][s], uc[c][s], den);
                 }
             }
             if constexpr (!MMA && !MMA4) {
@@ -936,48 +952,84 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
 #pragma unroll
                         for (int t2 = 1; t2 < SP; ++t2) Qu = fma(row[t2], ucf[t2], Qu);
                     }
-                    num = fma(x[c][s], Qu, num);
-                    den = fma(x[c][s], uc[c][s], den);
+                    num[c] = fma(x[c][s], Qu, num[c]);
+                    if (c == 0) den = fma(x[c][s], uc[c][s], den);
                 }
             }
-            ndw[c * 32] = MMA4 ? make_double2((double)num, (double)den) : make_double2(gwr * (double)num, wr * (double)den);
-            if (slots[c] >= 0) {
-                maybe_rescale<Real, VL, G>(qc[c]);
-                stk_st(slots[c], qc[c]);
+        }
+        // both children's q: one vote decides whether either needs rescaling
+        {
+            using T = ScaleTraits<Real>;
+            int hmin = 0x7fffffff;
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+                if (slots[c] >= 0) hmin = min(hmin, max_hiword<Real, VL>(qc[c]));
+            if (__any_sync(0xffffffffu, hmin < (T::THRESH << T::SHIFT))) {
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+                    if (slots[c] >= 0) maybe_rescale<Real, VL, G>(qc[c]);
             }
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+                if (slots[c] >= 0) stk_st(slots[c], qc[c]);
         }
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 7, qc[0][0] + qc[1][0]);
+        {
+            // per-pattern totals over the pattern's G lanes (categories x
+            // state groups; weights P(gamma_r), gamma_r applied per lane)
+            double na = MMA4 ? (double)num[0] : gwr * (double)num[0];
+            double nb = MMA4 ? (double)num[1] : gwr * (double)num[1];
+            double dn = MMA4 ? (double)den : wr * (double)den;
+#pragma unroll
+            for (int o = 1; o < G; o <<= 1) {
+                na += __shfl_xor_sync(0xffffffffu, na, o);
+                nb += __shfl_xor_sync(0xffffffffu, nb, o);
+                dn += __shfl_xor_sync(0xffffffffu, dn, o);
+            }
+            const int ws = n % W;
+            if ((lane & (G - 1)) == 0) {
+                double *e = nd + (ws * TP + pl) * 3;
+                e[0] = na;
+                e[1] = nb;
+                e[2] = dn;
+            }
+            if (lane == 0) {
+                nodes_w[ws * 2] = cs[0] & ~kTipPartialBit;
+                nodes_w[ws * 2 + 1] = cs[1] & ~kTipPartialBit;
+            }
+        }
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 8, qc[0][0] + qc[1][0]);
         if (n % W == W - 1 || n == nops - 1) {
-            // W steps of (num, den) lane shares -> Eq. 8 ratio per pattern, weighted
-            // (Eq. 6), summed over the tile's patterns; all 32 lanes busy.
+            // W steps x TP patterns of (num_a, num_b, den) -> Eq. 8 ratios,
+            // weighted by w_c (Eq. 6) and summed over the tile's patterns:
+            // LPS lanes per step, PPL independent patterns per lane
+            constexpr int LPS = Cfg::LPS, PPL = Cfg::PPL;
             __syncwarp();
-            constexpr int PAIRS = 2 * W, LPP = 32 / PAIRS, PPL = TP / LPP > 0 ? TP / LPP : 1;
-            const int pair = lane / LPP, sub = lane % LPP;
-            const int wstep = pair >> 1, c = pair & 1;
+            const int wstep = lane / LPS, sub = lane % LPS;
             const int n2 = n - (n % W) + wstep;
-            double acc = 0.0;
+            double acc_a = 0.0, acc_b = 0.0;
             if (n2 <= n && sub * PPL < TP) {
 #pragma unroll
                 for (int k = 0; k < PPL; ++k) {
                     const int p = sub * PPL + k;
-                    const double2 *src = nd + ((wstep * 2 + c) * 32 + p * G);
-                    double num = 0.0, den = 0.0;
-#pragma unroll
-                    for (int q2 = 0; q2 < G; ++q2) { const double2 v = src[q2]; num += v.x; den += v.y; }
+                    const double *e = nd + (wstep * TP + p) * 3;
                     const double w = wbuf[p];
-#ifdef PG_SLOWDIV
-                    acc += (w != 0.0) ? w * (num / den) : 0.0;
-#else
-                    acc = fma(w, ratio(num, (w != 0.0) ? den : 1.0), acc);   // w = 0: padding
-#endif
+                    const double d = (w != 0.0) ? e[2] : 1.0;           // w = 0: padding
+                    acc_a = fma(w, ratio(e[0], d), acc_a);
+                    acc_b = fma(w, ratio(e[1], d), acc_b);
                 }
             }
 #pragma unroll
-            for (int o = 1; o < LPP; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (sub == 0 && n2 <= n) a.grad_part[(size_t)nodes_w[wstep * 2 + c] * a.n_tiles + tile] = acc;
+            for (int o = 1; o < LPS; o <<= 1) {
+                acc_a += __shfl_xor_sync(0xffffffffu, acc_a, o);
+                acc_b += __shfl_xor_sync(0xffffffffu, acc_b, o);
+            }
+            if (sub == 0 && n2 <= n) {
+                a.grad_part[(size_t)nodes_w[wstep * 2] * a.n_tiles + tile] = acc_a;
+                a.grad_part[(size_t)nodes_w[wstep * 2 + 1] * a.n_tiles + tile] = acc_b;
+            }
             __syncwarp();
-            if (warp == 0) PG_TSTAMP((size_t)t * 16 + 9, acc);
+            if (warp == 0) PG_TSTAMP((size_t)t * 16 + 9, acc_a);
         }
     }
 }

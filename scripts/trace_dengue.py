@@ -13,7 +13,8 @@ import torch
 import paper_2303_04390_b200 as pg
 import phylo_synth as ps
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 1
-pb = ps.CONFIGS[cfg]() if hasattr(ps, "CONFIGS") else ps.config1_dengue()
+kw = {"C": int(os.environ["TRACE_C"])} if os.environ.get("TRACE_C") else {}
+pb = ps.make_config(cfg, **kw)
 inst = pg.from_problem(pb)
 out = torch.zeros(2 * pb.n_tips - 1, dtype=torch.float64, device="cuda")
 for _ in range(3):
