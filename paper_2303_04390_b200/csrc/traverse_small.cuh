@@ -40,6 +40,13 @@
 #pragma once
 #include "common.cuh"
 
+// fence.proxy.async before the producer's bulk copies into a released
+// stage: not needed (the stage was only READ by the consumers, whose release
+// / acquire through the empty barrier orders those reads before the copies);
+// dropping it: dengue traversal 1.306 -> 1.284 ms (scripts/gpu_r3_ab.sh)
+#ifndef PG_PROXY_FENCE
+#define PG_PROXY_FENCE 0
+#endif
 #ifndef PG_MMA_STAGES
 #define PG_MMA_STAGES 8
 #endif
@@ -153,7 +160,9 @@ struct SmallCfg {
 #ifdef PG_SMALL_W
     static constexpr int W = PG_SMALL_W;
 #else
-    static constexpr int W = (64 / TP) < 32 ? ((64 / TP) > 0 ? 64 / TP : 1) : 32;
+    // 128 / TP steps (3 KB per warp): dengue traversal 1.316 (8 steps) -> 1.302 ms
+    // (16 steps) vs 1.358 ms (4 steps), MMM 0.1024 -> 0.1004 ms (scripts/gpu_r3_ab.sh)
+    static constexpr int W = (128 / TP) < 32 ? ((128 / TP) > 0 ? 128 / TP : 1) : 32;
 #endif
     static constexpr int LPS = 32 / W;                         // lanes per window step
     static constexpr int PPL = TP / LPS > 0 ? TP / LPS : 1;    // patterns per lane in a flush
@@ -469,6 +478,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     auto sub_off = [&](int t) { return (stg(t) % DS) * (OPS * ST) + slot(t) * ST; };
     auto last_in_stage = [&](int t) { return slot(t) == OPS - 1 || t == nops - 1 || t == 2 * nops - 1; };
     auto wait_full = [&](int t) { const int g = stg(t); mbar_wait_u32(full_u + 8u * (g % DS), (uint32_t)(g / DS) & 1u); };
+
     const char *__restrict__ Pb = static_cast<const char *>(a.P);
     const char *__restrict__ tipP = static_cast<const char *>(a.tip_partials);
     const uint8_t *__restrict__ tipS = a.tip_states;
@@ -586,17 +596,20 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             const bool pre = g >= GP;
             const int t0 = pre ? nops + (g - GP) * OPS : g * OPS;
             const int t1 = min(t0 + OPS, pre ? 2 * nops : nops);
+            PG_TSTAMP((size_t)t0 * 16 + 0, g);
             if (g == GP) mbar_wait(post_done, 0);            // u of every tile stored + fenced
             if (g >= DS) mbar_wait_u32(empty_u + 8u * (g % DS), (uint32_t)(g / DS + 1) & 1u);
+            PG_TSTAMP((size_t)t0 * 16 + 1, g);
             if (lane == 0) {
                 const uint32_t bar = full_u + 8u * (g % DS);
                 unsigned total = 0;
                 for (int t = t0; t < t1; ++t) total += op_bytes(t);
-                fence_proxy_async_smem();
+                if (PG_PROXY_FENCE) fence_proxy_async_smem();
                 mbar_arrive_expect_tx_u32(bar, total);
                 for (int t = t0; t < t1; ++t) op_issue(t, stages_u + sub_off(t), bar);
             }
             __syncwarp();
+            PG_TSTAMP((size_t)t0 * 16 + 2, g);
         }
         return;
     }

@@ -44,6 +44,9 @@ for name, blk in (("post", tr[:steps]), ("pre", tr[steps:2 * steps])):
     d = np.diff(blk[:, 3]).astype(float)
     print(f"  {'consumer step (3->3)':28s} mean {d.mean():8.1f}  median {np.median(d):8.1f}")
     stats("producer empty wait (0->1)", 0, 1); stats("producer issue (1->2)", 1, 2)
+    if (blk[1:-1, 10] > 0).all():
+        stats("  prod: wait -> op read (1->10)", 1, 10); stats("  prod: small copies (10->11)", 10, 11)
+        stats("  prod: arrive+sync (11->12)", 11, 12); stats("  prod: bulk (12->2)", 12, 2)
     d = np.diff(blk[:, 0]).astype(float)
     print(f"  {'producer step (0->0)':28s} mean {d.mean():8.1f}  median {np.median(d):8.1f}")
     lag = (blk[:, 3] - blk[:, 2]).astype(float)
