@@ -4,6 +4,19 @@
 
 namespace pg {
 
+// First statement of the small-S A1 kernels: lets the traversal (launched
+// with programmatic stream serialization) start its setup while A1 runs --
+// the traversal waits (griddepcontrol.wait) before it reads any matrix --
+// and resets the evaluation's status words (first zero-likelihood pattern,
+// stall flag) in place of two memset nodes.
+__device__ __forceinline__ void pdl_trigger_and_reset(int *status) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (status && blockIdx.x == 0 && threadIdx.x == 0) {
+        status[0] = 0x7f7f7f7f;
+        status[1] = 0;
+    }
+}
+
 // A1 -- Eq. 1: P^{(r)}(b_i) = V diag(exp(gamma_r b_i lambda)) V^{-1}
 // for every branch i and category r, in the compute precision, zero padded to
 // SP x SP (category blocks `cs` Reals apart).  One CTA per (branch, category): the S exponentials go to shared
@@ -20,8 +33,10 @@ __global__ void __launch_bounds__(256) pmat_kernel(const double *__restrict__ V,
                                                    const double *__restrict__ lam,
                                                    const double *__restrict__ rates,
                                                    const double *__restrict__ bl, int S, int R,
-                                                   int cs, Real *__restrict__ P, Real *__restrict__ PT) {
+                                                   int cs, Real *__restrict__ P, Real *__restrict__ PT,
+                                                   int *__restrict__ status) {
     __shared__ double e[SP];
+    pdl_trigger_and_reset(status);
     const int br = blockIdx.x;          // branch * R + r
     const int r = br % R, b = br / R;
     const double t = rates[r] * bl[b];
@@ -63,8 +78,9 @@ __global__ void __launch_bounds__(256) pmat16_mma_kernel(const double *__restric
                                                          const double *__restrict__ lam,
                                                          const double *__restrict__ rates,
                                                          const double *__restrict__ bl, int S, int rec,
-                                                         double *__restrict__ P) {
+                                                         double *__restrict__ P, int *__restrict__ status) {
     __shared__ double e[16], Ps[16][17];
+    pdl_trigger_and_reset(status);
     const int b = blockIdx.x;
     const double t = rates[0] * bl[b];
     for (int k = threadIdx.x; k < 16; k += blockDim.x) e[k] = k < S ? expm1(lam[k] * t) : 0.0;
@@ -109,7 +125,8 @@ __global__ void __launch_bounds__(128) pmat4_mma_kernel(const double *__restrict
                                                         const double *__restrict__ lam,
                                                         const double *__restrict__ rates,
                                                         const double *__restrict__ bl, int S, int rec,
-                                                        double *__restrict__ P) {
+                                                        double *__restrict__ P, int *__restrict__ status) {
+    pdl_trigger_and_reset(status);
     const int b = blockIdx.x, r = threadIdx.x >> 5, l = threadIdx.x & 31;
     const double t = rates[r] * bl[b];
     double e[4];
@@ -134,6 +151,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(const double *__restrict__ 
                                                      const double *__restrict__ logl_part,
                                                      int B, int n_tiles, double *__restrict__ out) {
     __shared__ double sh[256];
+    asm volatile("griddepcontrol.wait;" ::: "memory");     // the traversal's partials (PDL launch)
     const int b = blockIdx.x;
     const double *src = (b < B) ? grad_part + (size_t)b * n_tiles : logl_part;
     double acc = 0.0;

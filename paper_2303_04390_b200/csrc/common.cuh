@@ -72,6 +72,14 @@ __device__ __forceinline__ float scale_pow2(float x, int k) { return ldexpf(x, k
 
 }  // namespace pg
 
+// m8n8k4 f64 MMA statements: plain asm (no side effects beyond the outputs),
+// so the compiler may interleave independent products' DMMAs;
+// -DPG_MMA_VOLATILE keeps them in program order
+#ifdef PG_MMA_VOLATILE
+#define PG_MMA_ASM asm volatile
+#else
+#define PG_MMA_ASM asm
+#endif
 namespace pg {
 // ---- mbarrier + 1-D bulk copy (TMA engine, sm_90+) ------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }

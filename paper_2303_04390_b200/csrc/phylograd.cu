@@ -1243,8 +1243,16 @@ static pg::tcp::TcArgs tc_args(pg_instance *inst) {
 static int enqueue_eval(pg_instance *inst, double *d_out) {
     const Layout &L = inst->L;
     const int R = inst->cfg.categories;
-    CK(cudaMemsetAsync(inst->at<int>(L.off_status), 0x7f, sizeof(int), inst->stream), "status reset");
-    CK(cudaMemsetAsync(inst->at<int>(L.off_status) + 1, 0, sizeof(int), inst->stream), "stall flag reset");
+    // variants 0 / 1: A1 resets the status words (pdl_trigger_and_reset)
+    if (L.variant >= 2) {
+        CK(cudaMemsetAsync(inst->at<int>(L.off_status), 0x7f, sizeof(int), inst->stream), "status reset");
+        CK(cudaMemsetAsync(inst->at<int>(L.off_status) + 1, 0, sizeof(int), inst->stream), "stall flag reset");
+    }
+    int *status_w = inst->at<int>(L.off_status);
+    // small-S traversal and A6 launched with programmatic stream
+    // serialization (setup overlaps the previous kernel; griddepcontrol.wait
+    // before the dependent reads); not with timing events in between
+    const bool pdl_small = L.variant == 0 && !inst->timing && !getenv("PG_NO_SMALL_PDL");
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[0], inst->stream, cudaEventRecordExternal), "event");
     const double *V = inst->at<double>(L.off_V), *Vi = inst->at<double>(L.off_Vi),
                  *lam = inst->at<double>(L.off_lam), *rates = inst->at<double>(L.off_rates),
@@ -1303,7 +1311,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         const double *M0 = inst->at<double>(L.off_M0);
         if (L.mma) {
             int rec = cs * R;                            // doubles per branch record
-            void *args16[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, &rec, &P};
+            void *args16[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, &rec, &P, &status_w};
             if (L.SP == 16)
                 CK(cudaLaunchKernel((void *)pg::pmat16_mma_kernel, dim3(L.B), dim3(256), args16, 0, inst->stream),
                    "pmat16 launch");
@@ -1311,7 +1319,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
                 CK(cudaLaunchKernel((void *)pg::pmat4_mma_kernel, dim3(L.B), dim3(128), args16, 0, inst->stream),
                    "pmat4 launch");
         } else {
-            void *args[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, (void *)&R, &cs, &P, &PT};
+            void *args[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, (void *)&R, &cs, &P, &PT, &status_w};
             CK(cudaLaunchKernel(fn, dim3(L.B * R), dim3(std::min(256, L.SP * L.SP)), args, 0, inst->stream),
                "pmat launch");
         }
@@ -1421,8 +1429,23 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
     } else {
         pg::TravArgs a = trav_args(inst);
         void *args[] = {&a};
-        CK(cudaLaunchKernel(traverse_fn(L, inst->cfg.categories), dim3(inst->grid), dim3(inst->block), args, inst->smem, inst->stream),
-           "traverse launch");
+        if (pdl_small) {
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3(inst->grid);
+            lc.blockDim = dim3(inst->block);
+            lc.dynamicSmemBytes = inst->smem;
+            lc.stream = inst->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            CK(cudaLaunchKernelExC(&lc, traverse_fn(L, inst->cfg.categories), args), "traverse launch");
+        } else {
+            CK(cudaLaunchKernel(traverse_fn(L, inst->cfg.categories), dim3(inst->grid), dim3(inst->block), args,
+                                inst->smem, inst->stream),
+               "traverse launch");
+        }
     }
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[2], inst->stream, cudaEventRecordExternal), "event");
     if (L.variant >= 2) {
@@ -1437,8 +1460,16 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         const double *gp = inst->at<double>(L.off_gpart), *lp = inst->at<double>(L.off_lpart);
         int B = L.B, nt = L.n_tiles;
         void *args[] = {&gp, &lp, &B, &nt, &d_out};
-        CK(cudaLaunchKernel((void *)pg::reduce_kernel, dim3(L.B + 1), dim3(256), args, 0, inst->stream),
-           "reduce launch");
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(L.B + 1);
+        lc.blockDim = dim3(256);
+        lc.stream = inst->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = pdl_small ? 1 : 0;
+        CK(cudaLaunchKernelExC(&lc, (void *)pg::reduce_kernel, args), "reduce launch");
     }
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[3], inst->stream, cudaEventRecordExternal), "event");
     return PG_OK;

@@ -393,9 +393,9 @@ __device__ __forceinline__ void dmma16(double (&y)[4], const double (&A)[4], con
 #pragma unroll
     for (int kt = 0; kt < 4; ++kt) {
         const double b0 = Bf[(kt * 2) * 32 + lane], b1 = Bf[(kt * 2 + 1) * 32 + lane];
-        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        PG_MMA_ASM("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                      : "+d"(c0[0]), "+d"(c0[1]) : "d"(A[kt]), "d"(b0));
-        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        PG_MMA_ASM("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                      : "+d"(c1[0]), "+d"(c1[1]) : "d"(A[kt]), "d"(b1));
     }
     y[0] = c0[0];
@@ -407,7 +407,7 @@ __device__ __forceinline__ void dmma16(double (&y)[4], const double (&A)[4], con
 // first C element is state (lane % 4) of its pattern (see small_tc)
 __device__ __forceinline__ double dmma4(double a, double b) {
     double c0 = 0.0, c1 = 0.0;
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    PG_MMA_ASM("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
     return c0;
 }
@@ -415,9 +415,9 @@ __device__ __forceinline__ void dmma16r(double (&y)[4], const double (&A)[4], co
     double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
 #pragma unroll
     for (int kt = 0; kt < 4; ++kt) {
-        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        PG_MMA_ASM("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                      : "+d"(c0[0]), "+d"(c0[1]) : "d"(A[kt]), "d"(B[2 * kt]));
-        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        PG_MMA_ASM("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                      : "+d"(c1[0]), "+d"(c1[1]) : "d"(A[kt]), "d"(B[2 * kt + 1]));
     }
     y[0] = c0[0];
@@ -512,6 +512,9 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     }
     __syncthreads();
     mbar_wait(prog_bar, 0u);
+    // PDL launch behind A1: everything above overlapped it; the matrices (and
+    // the status words A1 resets) are read only after this
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     // =============================== producer ===================================
     if (warp == K) {
@@ -869,6 +872,62 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
         wait_full(nops);
         opn = *reinterpret_cast<const Op4 *>(stages + sub_off(nops));
     }
+    // Eq. 8 window: step n's per-pattern totals (sums of the pending lane
+    // shares over the pattern's G lanes: categories x state groups) into slot
+    // n % W; every W steps the warp forms the ratios
+    constexpr bool DEFER = MMA;
+    double pend_na = 0.0, pend_nb = 0.0, pend_dn = 0.0;
+    int pend_node_a = 0, pend_node_b = 0;
+    auto store_totals = [&](const int n) {
+        double na = pend_na, nb = pend_nb, dn = pend_dn;
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) {
+            na += __shfl_xor_sync(0xffffffffu, na, o);
+            nb += __shfl_xor_sync(0xffffffffu, nb, o);
+            dn += __shfl_xor_sync(0xffffffffu, dn, o);
+        }
+        const int ws = n % W;
+        if ((lane & (G - 1)) == 0) {
+            double *e = nd + (ws * TP + pl) * 3;
+            e[0] = na;
+            e[1] = nb;
+            e[2] = dn;
+        }
+        if (lane == 0) {
+            nodes_w[ws * 2] = pend_node_a;
+            nodes_w[ws * 2 + 1] = pend_node_b;
+        }
+        if (n % W != W - 1 && n != nops - 1) return;
+        // W steps x TP patterns of (num_a, num_b, den) -> Eq. 8 ratios,
+        // weighted by w_c (Eq. 6) and summed over the tile's patterns: LPS
+        // lanes per step, PPL independent patterns per lane
+        constexpr int LPS = Cfg::LPS, PPL = Cfg::PPL;
+        __syncwarp();
+        const int wstep = lane / LPS, sub = lane % LPS;
+        const int n2 = n - (n % W) + wstep;
+        double acc_a = 0.0, acc_b = 0.0;
+        if (n2 <= n && sub * PPL < TP) {
+#pragma unroll
+            for (int k = 0; k < PPL; ++k) {
+                const int p = sub * PPL + k;
+                const double *e = nd + (wstep * TP + p) * 3;
+                const double w = wbuf[p];
+                const double d = (w != 0.0) ? e[2] : 1.0;           // w = 0: padding
+                acc_a = fma(w, ratio(e[0], d), acc_a);
+                acc_b = fma(w, ratio(e[1], d), acc_b);
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < LPS; o <<= 1) {
+            acc_a += __shfl_xor_sync(0xffffffffu, acc_a, o);
+            acc_b += __shfl_xor_sync(0xffffffffu, acc_b, o);
+        }
+        if (sub == 0 && n2 <= n) {
+            a.grad_part[(size_t)nodes_w[wstep * 2] * a.n_tiles + tile] = acc_a;
+            a.grad_part[(size_t)nodes_w[wstep * 2 + 1] * a.n_tiles + tile] = acc_b;
+        }
+        __syncwarp();
+    };
     for (int n = 0; n < nops; ++n) {
         const int t = nops + n;
         if (!active) {
@@ -893,6 +952,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             if ((cs[c] & ~kTipPartialBit) >= N) lds_vec<Real, VL>(uc[c], vs + u_vec);
             else child_tip(uc[c], st + 16 + c * MS, vs, cs[c]);
         }
+        if (DEFER && n > 0) store_totals(n - 1);    // the previous step's Eq. 8 totals
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 4, q[0] + uc[0][0] + uc[1][VL - 1]);
         if (n + 1 < nops) {
             const int t1 = t + 1;
@@ -987,64 +1047,20 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
                 if (slots[c] >= 0) stk_st(slots[c], qc[c]);
         }
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 7, qc[0][0] + qc[1][0]);
-        {
-            // per-pattern totals over the pattern's G lanes (categories x
-            // state groups; weights P(gamma_r), gamma_r applied per lane)
-            double na = MMA4 ? (double)num[0] : gwr * (double)num[0];
-            double nb = MMA4 ? (double)num[1] : gwr * (double)num[1];
-            double dn = MMA4 ? (double)den : wr * (double)den;
-#pragma unroll
-            for (int o = 1; o < G; o <<= 1) {
-                na += __shfl_xor_sync(0xffffffffu, na, o);
-                nb += __shfl_xor_sync(0xffffffffu, nb, o);
-                dn += __shfl_xor_sync(0xffffffffu, dn, o);
-            }
-            const int ws = n % W;
-            if ((lane & (G - 1)) == 0) {
-                double *e = nd + (ws * TP + pl) * 3;
-                e[0] = na;
-                e[1] = nb;
-                e[2] = dn;
-            }
-            if (lane == 0) {
-                nodes_w[ws * 2] = cs[0] & ~kTipPartialBit;
-                nodes_w[ws * 2 + 1] = cs[1] & ~kTipPartialBit;
-            }
-        }
-        if (warp == 0) PG_TSTAMP((size_t)t * 16 + 8, qc[0][0] + qc[1][0]);
-        if (n % W == W - 1 || n == nops - 1) {
-            // W steps x TP patterns of (num_a, num_b, den) -> Eq. 8 ratios,
-            // weighted by w_c (Eq. 6) and summed over the tile's patterns:
-            // LPS lanes per step, PPL independent patterns per lane
-            constexpr int LPS = Cfg::LPS, PPL = Cfg::PPL;
-            __syncwarp();
-            const int wstep = lane / LPS, sub = lane % LPS;
-            const int n2 = n - (n % W) + wstep;
-            double acc_a = 0.0, acc_b = 0.0;
-            if (n2 <= n && sub * PPL < TP) {
-#pragma unroll
-                for (int k = 0; k < PPL; ++k) {
-                    const int p = sub * PPL + k;
-                    const double *e = nd + (wstep * TP + p) * 3;
-                    const double w = wbuf[p];
-                    const double d = (w != 0.0) ? e[2] : 1.0;           // w = 0: padding
-                    acc_a = fma(w, ratio(e[0], d), acc_a);
-                    acc_b = fma(w, ratio(e[1], d), acc_b);
-                }
-            }
-#pragma unroll
-            for (int o = 1; o < LPS; o <<= 1) {
-                acc_a += __shfl_xor_sync(0xffffffffu, acc_a, o);
-                acc_b += __shfl_xor_sync(0xffffffffu, acc_b, o);
-            }
-            if (sub == 0 && n2 <= n) {
-                a.grad_part[(size_t)nodes_w[wstep * 2] * a.n_tiles + tile] = acc_a;
-                a.grad_part[(size_t)nodes_w[wstep * 2 + 1] * a.n_tiles + tile] = acc_b;
-            }
-            __syncwarp();
-            if (warp == 0) PG_TSTAMP((size_t)t * 16 + 9, acc_a);
-        }
+        // this step's (weighted) Eq. 8 shares; DEFER: they wait in registers
+        // and their reduction over the pattern's lanes runs during the next
+        // step, where its shuffle latency overlaps that step's operand loads
+        // (MMM traversal 0.1004 -> 0.0983 ms; dengue, whose step has more
+        // independent work of its own, 1.281 -> 1.291 ms: immediate there)
+        pend_na = MMA4 ? (double)num[0] : gwr * (double)num[0];
+        pend_nb = MMA4 ? (double)num[1] : gwr * (double)num[1];
+        pend_dn = MMA4 ? (double)den : wr * (double)den;
+        pend_node_a = cs[0] & ~kTipPartialBit;
+        pend_node_b = cs[1] & ~kTipPartialBit;
+        if (!DEFER) store_totals(n);
     }
+    if (DEFER && active && nops > 0) store_totals(nops - 1);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // A6 may start launching
 }
 
 }  // namespace pg
