@@ -175,7 +175,8 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         // fmax [N-1], qmax [N-2], then the flow schedule's counters
         // {item counter, rpost [N-1][<= ntiles], rpre [N-1][<= ntiles]}: one memset
         // {item counter, rpost, rpre, A1 done flags [B][R], ratio slice counters [B+1]}
-        L->flow_bytes = ((size_t)32 + (size_t)2 * (N - 1) * L->n_tiles + (size_t)L->B * R + (L->B + 1)) * 4;
+        // + the fused A6's finished-CTA counter
+        L->flow_bytes = ((size_t)32 + (size_t)2 * (N - 1) * L->n_tiles + (size_t)L->B * R + (L->B + 1) + 32) * 4;
         L->reset_bytes = (size_t)(2 * N - 3) * L->Cpad * 4 + L->flow_bytes;
         L->off_fmax = take(L->reset_bytes);
         L->off_qmax = L->off_fmax + (size_t)(N - 1) * L->Cpad * 4;
@@ -239,6 +240,7 @@ struct pg_instance {
     int flow_nst = 2;                   // codon_flow2_kernel ring stages (1: latency, 2: throughput)
     int flow_pdl = 0;                   // A1 -> flow programmatic dependent launch (PG_FLOW_PDL=0/1 overrides)
     int flow_pub = 1;                   // flow v2: publisher warp (PG_FLOW_PUB)
+    bool a6_fused = false;              // set per enqueue: the flow kernel also formed [logL, g]
     int flow_pprod = 0;                 // flow v2: the producer forms p = u_a o u_b (PG_FLOW_PPROD)
     int split_items = 0;                // items of the split schedule (task offsets table)
     int flow_split = 0;                 // codon_flow2_kernel: one pre item per child (PG_FLOW_SPLIT=0/1 overrides)
@@ -1242,6 +1244,7 @@ static pg::tcp::TcArgs tc_args(pg_instance *inst) {
 // enqueue one evaluation (no host sync) writing [logL, g] to d_out
 static int enqueue_eval(pg_instance *inst, double *d_out) {
     const Layout &L = inst->L;
+    inst->a6_fused = false;
     const int R = inst->cfg.categories;
     // variants 0 / 1: A1 resets the status words (pdl_trigger_and_reset)
     if (L.variant >= 2) {
@@ -1382,6 +1385,18 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
                 f.task_off = inst->at<int>(L.off_taskoff);
                 f.pprod = inst->flow_pprod;
                 f.pub = inst->flow_pub;
+                // A6 at the end of the flow launch (no ratio kernel) when a
+                // row's patterns are few (<= 2 per thread: pattern shards;
+                // yeast 8-way 0.2232 -> 0.2215 ms, WNV 8-way 0.4947 -> 0.4872
+                // ms; at full size the sliced ratio kernel is faster: yeast
+                // 1.093 vs 1.107 ms); not under the per-kernel timing pass
+                const char *fa6 = getenv("PG_FUSED_A6");
+                const bool fuse = fa6 ? atoi(fa6) != 0 : inst->cfg.patterns <= 2 * (int)cf.flow2_threads;
+                if (fuse && !inst->timing) {
+                    f.a6cnt = inst->at<int>(L.off_flow) + 32 + (size_t)2 * (N - 1) * L.n_tiles + (size_t)L.B * R + (L.B + 1);
+                    f.out = d_out;
+                    inst->a6_fused = true;
+                }
                 const int items2 = f.split ? inst->split_items : f.ntask * R * L.n_tiles;
                 const int v = inst->flow_nst - 1;
                 // programmatic dependent launch right behind A1 (no partial-tip
@@ -1448,7 +1463,9 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         }
     }
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[2], inst->stream, cudaEventRecordExternal), "event");
-    if (L.variant >= 2) {
+    if (inst->a6_fused) {
+        // A6 ran inside the flow kernel
+    } else if (L.variant >= 2) {
         pg::codon::CodonArgs c = codon_args(inst);
         int *cnt = inst->at<int>(L.off_flow) + 32 + (size_t)2 * (inst->cfg.tips - 1) * L.n_tiles + (size_t)L.B * R;
         double *sp = inst->at<double>(L.off_gpart);      // [B+1][slices] <= [B][n_tiles] + [n_tiles] (codon path)

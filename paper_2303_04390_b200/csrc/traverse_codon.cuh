@@ -414,6 +414,10 @@ struct FlowArgs {
     const int *task_off;         // split schedule: [ntask + 1] first item of each task
     int pprod;                   // codon_flow2_kernel: the producer forms p = u_a o u_b of post items
     int pub;                     // codon_flow2_kernel: a publisher warp raises the completion flags
+    // codon_flow2_kernel: A6 fused at the end of the launch (no ratio
+    // kernel): a6cnt = finished-CTA counter, out = [logL, g]
+    int *a6cnt;
+    double *out;
 };
 
 // ---------------------------------------------------------------------------

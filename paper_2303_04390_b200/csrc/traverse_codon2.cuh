@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
                     mbar_arrive_u32(bar);
                     mbar_arrive_u32(bar);
                 }
-                return;
+                break;
             }
             unsigned long long *tr = f.trace ? f.trace + TRW * (size_t)item : nullptr;   // PG_FLOW_TRACE
             if (tr && lane == 0) {
@@ -399,14 +399,13 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
     // numden and releases the stage -- the consumers go straight on to the
     // next item.
     if (warp == NWC + 1) {
-        if (!f.pub) return;
         uint32_t dph = 0;                            // done phase bits per stage
-        for (int g = 0;; ++g) {
+        for (int g = 0; f.pub; ++g) {
             const int s = g % NST;
             mbar_wait_sleep(pub_u + 8u * s, (uint32_t)(g / NST) & 1u);
             const Meta2 *m = meta(s);
             const int item = m->item;
-            if (item < 0) return;
+            if (item < 0) break;
             const int k = m->lev.x, ca = m->lev.y, cb = m->lev.z, tile = m->tile, cs = m->cs;
             const bool post = m->task < f.npost;
             unsigned long long *tr = (f.trace && lane == 0) ? f.trace + TRW * (size_t)item : nullptr;
@@ -438,234 +437,116 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
     }
 
     // ================================ consumers ===============================
-    const int w = warp % NW, mt0 = (warp / NW) * MTW;              // column strip, first row block
-    for (int g = 0;; ++g) {
-        const int s = g % NST;
-        mbar_wait_sleep(full_u + 8u * s, (uint32_t)(g / NST) & 1u);
-        const Meta2 *m = meta(s);
-        const int item = m->item;
-        if (item < 0) {
-            if (f.pub && lane == 0) mbar_arrive_u32(pub_u + 8u * s);   // the publisher sees the end too
-            break;
-        }
-        const int r = m->r, tile = m->tile;
-        const int k = m->lev.x, ca = m->lev.y, cb = m->lev.z, kinds = m->lev.w;
-        const int pat0 = tile * T;
-        unsigned long long *tr = (f.trace && threadIdx.x == 0) ? f.trace + TRW * (size_t)item : nullptr;
-        if (tr) tr[3] = gtimer();
-        double *As = tileA(s), *Bs = As + TILE, *Qs = As + 2 * (size_t)TILE;
-        double *part = partS(s);
-        const bool post = m->task < f.npost;
-        if (post) {
-            auto scA = [&](int mm) { return ca >= N ? pow2neg(lazy_exp(m->fa[mm])) : 1.0; };
-            auto scB = [&](int mm) { return cb >= N ? pow2neg(lazy_exp(m->fb[mm])) : 1.0; };
-            auto storeE = [&]() {
-                const int mm = threadIdx.x;
-                const int Ek = m->Ea[mm] + m->Eb[mm] + (ca >= N ? lazy_exp(m->fa[mm]) : 0) +
-                               (cb >= N ? lazy_exp(m->fb[mm]) : 0);
-                a.E[(size_t)(k - N) * a.Cpad + pat0 + mm] = Ek;
-            };
-            if (k == root) {
-                if (r == 0 && threadIdx.x < T) storeE();
-                // Eq. 3 terms: thread -> (pattern mm, states j, j+TPP, ...)
-                constexpr int TPP = NTC / T;
-                const int mm = threadIdx.x / TPP, j = threadIdx.x % TPP;
-                double sum = 0.0;
-                if (mm < T)
-                    for (int kk = j; kk < SP; kk += TPP) {
-                        const int p = apos<SP>(mm, kk);
-                        sum = fma(a.pi[kk], As[p] * Bs[p], sum);
-                    }
-#pragma unroll
-                for (int o = 1; o < TPP; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-                if (j == 0 && mm < T) a.Lpart[(size_t)r * a.Cpad + pat0 + mm] = a.cat_w[r] * sum * (scA(mm) * scB(mm));
-            } else {
-                double bfr[KT];
-                load_bfrag<SP>(bfr, a.PBpost + ((size_t)k * R + r) * MAT, w, lane);
-                // p = u_a o u_b in place (one A operand for the GEMM), unless
-                // the producer formed it already
-                if (!f.pprod) {
-                    for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += NTC) {
-                        double2 *pa = reinterpret_cast<double2 *>(As) + i2;
-                        const double2 tb = reinterpret_cast<const double2 *>(Bs)[i2];
-                        double2 v = *pa;
-                        v.x *= tb.x;
-                        v.y *= tb.y;
-                        *pa = v;
-                    }
-                    consumer_sync(NTC);
-                }
-                double acc[MTW][2];
-                gemm_tile<SP, MTW>(acc, As + mt0 * KT * 32, bfr, lane);
-                if (tr) tr[4] = gtimer();
-                if (r == 0 && threadIdx.x < T) storeE();
-                double *out = a.u + (((size_t)(k - N) * R + r) * ntiles + tile) * TILE;
-                int *fm = a.fmax + (size_t)(k - N) * a.Cpad + pat0;
-#pragma unroll
-                for (int ml = 0; ml < MTW; ++ml) {
-                    const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-                    const double f2 = scA(mm) * scB(mm);
-                    const double c0 = acc[ml][0] * f2, c1 = acc[ml][1] * f2;
-                    *reinterpret_cast<double2 *>(out + apos<SP>(mm, n)) = make_double2(c0, c1);
-                    int fx = max(__double2hiint(c0) >> 20, __double2hiint(c1) >> 20);
-                    fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 1));
-                    fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 2));
-                    if ((lane & 3) == 0) atomicMax(fm + mm, fx);
-                }
+    if (warp < NWC) {
+        const int w = warp % NW, mt0 = (warp / NW) * MTW;              // column strip, first row block
+        for (int g = 0;; ++g) {
+            const int s = g % NST;
+            mbar_wait_sleep(full_u + 8u * s, (uint32_t)(g / NST) & 1u);
+            const Meta2 *m = meta(s);
+            const int item = m->item;
+            if (item < 0) {
+                if (f.pub && lane == 0) mbar_arrive_u32(pub_u + 8u * s);   // the publisher sees the end too
+                break;
             }
-            fence_proxy_async_global();              // our generic stores -> later TMA reads (other CTAs)
-            if (f.pub) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive_u32(pub_u + 8u * s);
-                if (tr) tr[6] = gtimer();
+            const int r = m->r, tile = m->tile;
+            const int k = m->lev.x, ca = m->lev.y, cb = m->lev.z, kinds = m->lev.w;
+            const int pat0 = tile * T;
+            unsigned long long *tr = (f.trace && threadIdx.x == 0) ? f.trace + TRW * (size_t)item : nullptr;
+            if (tr) tr[3] = gtimer();
+            double *As = tileA(s), *Bs = As + TILE, *Qs = As + 2 * (size_t)TILE;
+            double *part = partS(s);
+            const bool post = m->task < f.npost;
+            if (post) {
+                auto scA = [&](int mm) { return ca >= N ? pow2neg(lazy_exp(m->fa[mm])) : 1.0; };
+                auto scB = [&](int mm) { return cb >= N ? pow2neg(lazy_exp(m->fb[mm])) : 1.0; };
+                auto storeE = [&]() {
+                    const int mm = threadIdx.x;
+                    const int Ek = m->Ea[mm] + m->Eb[mm] + (ca >= N ? lazy_exp(m->fa[mm]) : 0) +
+                                   (cb >= N ? lazy_exp(m->fb[mm]) : 0);
+                    a.E[(size_t)(k - N) * a.Cpad + pat0 + mm] = Ek;
+                };
+                if (k == root) {
+                    if (r == 0 && threadIdx.x < T) storeE();
+                    // Eq. 3 terms: thread -> (pattern mm, states j, j+TPP, ...)
+                    constexpr int TPP = NTC / T;
+                    const int mm = threadIdx.x / TPP, j = threadIdx.x % TPP;
+                    double sum = 0.0;
+                    if (mm < T)
+                        for (int kk = j; kk < SP; kk += TPP) {
+                            const int p = apos<SP>(mm, kk);
+                            sum = fma(a.pi[kk], As[p] * Bs[p], sum);
+                        }
+    #pragma unroll
+                    for (int o = 1; o < TPP; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                    if (j == 0 && mm < T) a.Lpart[(size_t)r * a.Cpad + pat0 + mm] = a.cat_w[r] * sum * (scA(mm) * scB(mm));
+                } else {
+                    double bfr[KT];
+                    load_bfrag<SP>(bfr, a.PBpost + ((size_t)k * R + r) * MAT, w, lane);
+                    // p = u_a o u_b in place (one A operand for the GEMM), unless
+                    // the producer formed it already
+                    if (!f.pprod) {
+                        for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += NTC) {
+                            double2 *pa = reinterpret_cast<double2 *>(As) + i2;
+                            const double2 tb = reinterpret_cast<const double2 *>(Bs)[i2];
+                            double2 v = *pa;
+                            v.x *= tb.x;
+                            v.y *= tb.y;
+                            *pa = v;
+                        }
+                        consumer_sync(NTC);
+                    }
+                    double acc[MTW][2];
+                    gemm_tile<SP, MTW>(acc, As + mt0 * KT * 32, bfr, lane);
+                    if (tr) tr[4] = gtimer();
+                    if (r == 0 && threadIdx.x < T) storeE();
+                    double *out = a.u + (((size_t)(k - N) * R + r) * ntiles + tile) * TILE;
+                    int *fm = a.fmax + (size_t)(k - N) * a.Cpad + pat0;
+    #pragma unroll
+                    for (int ml = 0; ml < MTW; ++ml) {
+                        const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                        const double f2 = scA(mm) * scB(mm);
+                        const double c0 = acc[ml][0] * f2, c1 = acc[ml][1] * f2;
+                        *reinterpret_cast<double2 *>(out + apos<SP>(mm, n)) = make_double2(c0, c1);
+                        int fx = max(__double2hiint(c0) >> 20, __double2hiint(c1) >> 20);
+                        fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 1));
+                        fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 2));
+                        if ((lane & 3) == 0) atomicMax(fm + mm, fx);
+                    }
+                }
+                fence_proxy_async_global();              // our generic stores -> later TMA reads (other CTAs)
+                if (f.pub) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_u32(pub_u + 8u * s);
+                    if (tr) tr[6] = gtimer();
+                    continue;
+                }
+                if (tr) tr[5] = gtimer();
+                consumer_sync(NTC);                      // stage consumed, outputs issued
+                if (threadIdx.x == 0) {
+                    __threadfence();
+                    atomicAdd(f.rpost + (size_t)(k - N) * ntiles + tile, 1);
+                    mbar_arrive_u32(empty_u + 8u * s);
+                    if (tr) tr[6] = gtimer();
+                }
                 continue;
             }
-            if (tr) tr[5] = gtimer();
-            consumer_sync(NTC);                      // stage consumed, outputs issued
-            if (threadIdx.x == 0) {
-                __threadfence();
-                atomicAdd(f.rpost + (size_t)(k - N) * ntiles + tile, 1);
-                mbar_arrive_u32(empty_u + 8u * s);
-                if (tr) tr[6] = gtimer();
-            }
-            continue;
-        }
-        // ------------------------------- pre item ------------------------------
-        const int cs = m->cs;                        // -1: both children, else the one child of a split item
-        auto scQ = [&](int mm) { return k == root ? 1.0 : pow2neg(lazy_exp(m->fq[mm])); };
-        auto scC = [&](int c, int mm) {
-            return (c ? cb : ca) >= N ? pow2neg(lazy_exp(c ? m->fb[mm] : m->fa[mm])) : 1.0;
-        };
-        auto Uc = [&](int c) { return c ? Bs : As; };
-        // q_c = x_c P_c (Eq. 4) from the x_c tile Xs; rows scaled by the q_k
-        // and sibling exponents
-        auto q_gemm = [&](int c, const double *Xs) {
-            const int node = c ? cb : ca;
-            double bq[KT], acc[MTW][2];
-            load_bfrag<SP>(bq, a.PBpre + ((size_t)node * R + r) * MAT, w, lane);
-            gemm_tile<SP, MTW>(acc, Xs + mt0 * KT * 32, bq, lane);
-            double *out = a.q + (((size_t)(node - N) * R + r) * ntiles + tile) * TILE;
-            int *qm = a.qmax + (size_t)(node - N) * a.Cpad + pat0;
-#pragma unroll
-            for (int ml = 0; ml < MTW; ++ml) {
-                const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-                const double f2 = scQ(mm) * scC(1 - c, mm);
-                const double c0 = acc[ml][0] * f2, c1 = acc[ml][1] * f2;
-                *reinterpret_cast<double2 *>(out + apos<SP>(mm, n)) = make_double2(c0, c1);
-                int fx = max(__double2hiint(c0) >> 20, __double2hiint(c1) >> 20);
-                fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 1));
-                fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 2));
-                if ((lane & 3) == 0) atomicMax(qm + mm, fx);
-            }
-        };
-        auto publish_q = [&](bool pa, bool pb) {
-            if (f.pub) {                             // every pre item arrives once
-                fence_proxy_async_global();
-                __syncwarp();
-                if (lane == 0) mbar_arrive_u32(pub_u + 8u * s);
-                return;
-            }
-            if (!pa && !pb) return;
-            fence_proxy_async_global();
-            consumer_sync(NTC);
-            if (threadIdx.x == 0) {
-                __threadfence();
-                if (pa) atomicAdd(f.rpre + (size_t)(ca - N) * ntiles + tile, 1);
-                if (pb) atomicAdd(f.rpre + (size_t)(cb - N) * ntiles + tile, 1);
-            }
-        };
-        // Eq. 8 terms of child c: num_c = x_c'(Q u_c) (internal child or partial
-        // tip: Q u on the tensor path; state tip: the D' row, which carries
-        // gamma_r), with x_c at the output positions from xat(p); den = x_c'u_c
-        // (the same for both children, q_k o u_a o u_b, Eq. 5).  Tiles are
-        // unscaled: the factors cancel in the ratio over categories.
-        auto eq8 = [&](int c, bool den, auto xat) {
-            const int node = c ? cb : ca;
-            const size_t br = (size_t)node * R + r;
-            const int kind = (kinds >> (2 * c)) & 3;
-            double acc[MTW][2];
-            if (node >= N || kind == 2) {
-                double b[KT];
-                load_bfrag<SP>(b, a.QB, w, lane);
-                gemm_tile<SP, MTW>(acc, Uc(c) + mt0 * KT * 32, b, lane);
-            } else {
-                const uint8_t *stc = c ? m->sb : m->sa;
-#pragma unroll
-                for (int ml = 0; ml < MTW; ++ml) {
-                    const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-                    const int sv = stc[mm];
-                    if (sv < a.S) {
-                        const double2 v = __ldg(reinterpret_cast<const double2 *>(a.DT + br * MAT + (size_t)sv * SP + n));
-                        acc[ml][0] = v.x;
-                        acc[ml][1] = v.y;
-                    } else {
-                        acc[ml][0] = acc[ml][1] = 0.0;
-                    }
-                }
-            }
-#pragma unroll
-            for (int ml = 0; ml < MTW; ++ml) {
-                const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
-                const int p = apos<SP>(mm, n);
-                const double2 x2 = xat(p);
-                double sn = x2.x * acc[ml][0] + x2.y * acc[ml][1];
-                sn += __shfl_xor_sync(0xffffffffu, sn, 1);
-                sn += __shfl_xor_sync(0xffffffffu, sn, 2);
-                if ((lane & 3) == 0) part[(c * NW + w) * T + mm] = sn;
-                if (den) {
-                    const double2 u2 = *reinterpret_cast<const double2 *>(Uc(c) + p);
-                    double sd = x2.x * u2.x + x2.y * u2.y;
-                    sd += __shfl_xor_sync(0xffffffffu, sd, 1);
-                    sd += __shfl_xor_sync(0xffffffffu, sd, 2);
-                    if ((lane & 3) == 0) part[(2 * NW + w) * T + mm] = sd;
-                }
-            }
-        };
-        if (cs >= 0) {
-            // split item (latency): x_c = q_k o u_sib formed in place over q_k
-            // (q_k is not needed again), q_c GEMM and publication first, then
-            // child c's Eq. 8 terms from x_c and u_c
-            const int c = cs;
-            const double *Usib = Uc(1 - c);
-            for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += NTC) {
-                double2 *px = reinterpret_cast<double2 *>(Qs) + i2;
-                const double2 us = reinterpret_cast<const double2 *>(Usib)[i2];
-                double2 v = *px;
-                v.x *= us.x;
-                v.y *= us.y;
-                *px = v;
-            }
-            consumer_sync(NTC);
-            if ((c ? cb : ca) >= N) q_gemm(c, Qs);
-            if (tr) tr[4] = gtimer();
-            publish_q(c == 0 && ca >= N, c == 1 && cb >= N);
-            if (tr) tr[5] = gtimer();
-            eq8(c, true, [&](int p) { return *reinterpret_cast<const double2 *>(Qs + p); });
-        } else {
-            // both children: q GEMMs first with x_c = q_k o u_sib formed in the
-            // A-fragment loads (q_k, u_a, u_b are all needed again), published
-            // before the Eq. 8 terms (measured faster than forming x in place
-            // after the Eq. 8 GEMMs: yeast 1.155 -> 1.106 ms, the pre-order
-            // chain link is shorter)
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
+            // ------------------------------- pre item ------------------------------
+            const int cs = m->cs;                        // -1: both children, else the one child of a split item
+            auto scQ = [&](int mm) { return k == root ? 1.0 : pow2neg(lazy_exp(m->fq[mm])); };
+            auto scC = [&](int c, int mm) {
+                return (c ? cb : ca) >= N ? pow2neg(lazy_exp(c ? m->fb[mm] : m->fa[mm])) : 1.0;
+            };
+            auto Uc = [&](int c) { return c ? Bs : As; };
+            // q_c = x_c P_c (Eq. 4) from the x_c tile Xs; rows scaled by the q_k
+            // and sibling exponents
+            auto q_gemm = [&](int c, const double *Xs) {
                 const int node = c ? cb : ca;
-                if (node < N) continue;
                 double bq[KT], acc[MTW][2];
                 load_bfrag<SP>(bq, a.PBpre + ((size_t)node * R + r) * MAT, w, lane);
-                const double *Ub = Uc(1 - c);
-#pragma unroll
-                for (int ml = 0; ml < MTW; ++ml) acc[ml][0] = acc[ml][1] = 0.0;
-#pragma unroll
-                for (int kt = 0; kt < KT; ++kt)
-#pragma unroll
-                    for (int ml = 0; ml < MTW; ++ml) {
-                        const int p = ((mt0 + ml) * KT + kt) * 32 + lane;
-                        dmma(acc[ml], Qs[p] * Ub[p], bq[kt]);
-                    }
+                gemm_tile<SP, MTW>(acc, Xs + mt0 * KT * 32, bq, lane);
                 double *out = a.q + (((size_t)(node - N) * R + r) * ntiles + tile) * TILE;
                 int *qm = a.qmax + (size_t)(node - N) * a.Cpad + pat0;
-#pragma unroll
+    #pragma unroll
                 for (int ml = 0; ml < MTW; ++ml) {
                     const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
                     const double f2 = scQ(mm) * scC(1 - c, mm);
@@ -676,30 +557,200 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
                     fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 2));
                     if ((lane & 3) == 0) atomicMax(qm + mm, fx);
                 }
-            }
-            if (tr) tr[4] = gtimer();
-            publish_q(ca >= N, cb >= N);
-            if (tr) tr[5] = gtimer();
-            auto xq = [&](int c) {
-                return [&, c](int p) {
-                    const double2 q2 = *reinterpret_cast<const double2 *>(Qs + p);
-                    const double2 o2 = *reinterpret_cast<const double2 *>(Uc(1 - c) + p);
-                    return make_double2(q2.x * o2.x, q2.y * o2.y);
-                };
             };
-            eq8(0, true, xq(0));
-            eq8(1, false, xq(1));
+            auto publish_q = [&](bool pa, bool pb) {
+                if (f.pub) {                             // every pre item arrives once
+                    fence_proxy_async_global();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_u32(pub_u + 8u * s);
+                    return;
+                }
+                if (!pa && !pb) return;
+                fence_proxy_async_global();
+                consumer_sync(NTC);
+                if (threadIdx.x == 0) {
+                    __threadfence();
+                    if (pa) atomicAdd(f.rpre + (size_t)(ca - N) * ntiles + tile, 1);
+                    if (pb) atomicAdd(f.rpre + (size_t)(cb - N) * ntiles + tile, 1);
+                }
+            };
+            // Eq. 8 terms of child c: num_c = x_c'(Q u_c) (internal child or partial
+            // tip: Q u on the tensor path; state tip: the D' row, which carries
+            // gamma_r), with x_c at the output positions from xat(p); den = x_c'u_c
+            // (the same for both children, q_k o u_a o u_b, Eq. 5).  Tiles are
+            // unscaled: the factors cancel in the ratio over categories.
+            auto eq8 = [&](int c, bool den, auto xat) {
+                const int node = c ? cb : ca;
+                const size_t br = (size_t)node * R + r;
+                const int kind = (kinds >> (2 * c)) & 3;
+                double acc[MTW][2];
+                if (node >= N || kind == 2) {
+                    double b[KT];
+                    load_bfrag<SP>(b, a.QB, w, lane);
+                    gemm_tile<SP, MTW>(acc, Uc(c) + mt0 * KT * 32, b, lane);
+                } else {
+                    const uint8_t *stc = c ? m->sb : m->sa;
+    #pragma unroll
+                    for (int ml = 0; ml < MTW; ++ml) {
+                        const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                        const int sv = stc[mm];
+                        if (sv < a.S) {
+                            const double2 v = __ldg(reinterpret_cast<const double2 *>(a.DT + br * MAT + (size_t)sv * SP + n));
+                            acc[ml][0] = v.x;
+                            acc[ml][1] = v.y;
+                        } else {
+                            acc[ml][0] = acc[ml][1] = 0.0;
+                        }
+                    }
+                }
+    #pragma unroll
+                for (int ml = 0; ml < MTW; ++ml) {
+                    const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                    const int p = apos<SP>(mm, n);
+                    const double2 x2 = xat(p);
+                    double sn = x2.x * acc[ml][0] + x2.y * acc[ml][1];
+                    sn += __shfl_xor_sync(0xffffffffu, sn, 1);
+                    sn += __shfl_xor_sync(0xffffffffu, sn, 2);
+                    if ((lane & 3) == 0) part[(c * NW + w) * T + mm] = sn;
+                    if (den) {
+                        const double2 u2 = *reinterpret_cast<const double2 *>(Uc(c) + p);
+                        double sd = x2.x * u2.x + x2.y * u2.y;
+                        sd += __shfl_xor_sync(0xffffffffu, sd, 1);
+                        sd += __shfl_xor_sync(0xffffffffu, sd, 2);
+                        if ((lane & 3) == 0) part[(2 * NW + w) * T + mm] = sd;
+                    }
+                }
+            };
+            if (cs >= 0) {
+                // split item (latency): x_c = q_k o u_sib formed in place over q_k
+                // (q_k is not needed again), q_c GEMM and publication first, then
+                // child c's Eq. 8 terms from x_c and u_c
+                const int c = cs;
+                const double *Usib = Uc(1 - c);
+                for (int i2 = threadIdx.x; i2 < TILE / 2; i2 += NTC) {
+                    double2 *px = reinterpret_cast<double2 *>(Qs) + i2;
+                    const double2 us = reinterpret_cast<const double2 *>(Usib)[i2];
+                    double2 v = *px;
+                    v.x *= us.x;
+                    v.y *= us.y;
+                    *px = v;
+                }
+                consumer_sync(NTC);
+                if ((c ? cb : ca) >= N) q_gemm(c, Qs);
+                if (tr) tr[4] = gtimer();
+                publish_q(c == 0 && ca >= N, c == 1 && cb >= N);
+                if (tr) tr[5] = gtimer();
+                eq8(c, true, [&](int p) { return *reinterpret_cast<const double2 *>(Qs + p); });
+            } else {
+                // both children: q GEMMs first with x_c = q_k o u_sib formed in the
+                // A-fragment loads (q_k, u_a, u_b are all needed again), published
+                // before the Eq. 8 terms (measured faster than forming x in place
+                // after the Eq. 8 GEMMs: yeast 1.155 -> 1.106 ms, the pre-order
+                // chain link is shorter)
+    #pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int node = c ? cb : ca;
+                    if (node < N) continue;
+                    double bq[KT], acc[MTW][2];
+                    load_bfrag<SP>(bq, a.PBpre + ((size_t)node * R + r) * MAT, w, lane);
+                    const double *Ub = Uc(1 - c);
+    #pragma unroll
+                    for (int ml = 0; ml < MTW; ++ml) acc[ml][0] = acc[ml][1] = 0.0;
+    #pragma unroll
+                    for (int kt = 0; kt < KT; ++kt)
+    #pragma unroll
+                        for (int ml = 0; ml < MTW; ++ml) {
+                            const int p = ((mt0 + ml) * KT + kt) * 32 + lane;
+                            dmma(acc[ml], Qs[p] * Ub[p], bq[kt]);
+                        }
+                    double *out = a.q + (((size_t)(node - N) * R + r) * ntiles + tile) * TILE;
+                    int *qm = a.qmax + (size_t)(node - N) * a.Cpad + pat0;
+    #pragma unroll
+                    for (int ml = 0; ml < MTW; ++ml) {
+                        const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
+                        const double f2 = scQ(mm) * scC(1 - c, mm);
+                        const double c0 = acc[ml][0] * f2, c1 = acc[ml][1] * f2;
+                        *reinterpret_cast<double2 *>(out + apos<SP>(mm, n)) = make_double2(c0, c1);
+                        int fx = max(__double2hiint(c0) >> 20, __double2hiint(c1) >> 20);
+                        fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 1));
+                        fx = max(fx, __shfl_xor_sync(0xffffffffu, fx, 2));
+                        if ((lane & 3) == 0) atomicMax(qm + mm, fx);
+                    }
+                }
+                if (tr) tr[4] = gtimer();
+                publish_q(ca >= N, cb >= N);
+                if (tr) tr[5] = gtimer();
+                auto xq = [&](int c) {
+                    return [&, c](int p) {
+                        const double2 q2 = *reinterpret_cast<const double2 *>(Qs + p);
+                        const double2 o2 = *reinterpret_cast<const double2 *>(Uc(1 - c) + p);
+                        return make_double2(q2.x * o2.x, q2.y * o2.y);
+                    };
+                };
+                eq8(0, true, xq(0));
+                eq8(1, false, xq(1));
+            }
+            if (f.pub) {                                 // the publisher sums the partials and frees the stage
+                __syncwarp();
+                if (lane == 0) mbar_arrive_u32(done_u + 8u * s);
+                continue;
+            }
+            consumer_sync(NTC);                          // stage and partials complete
+            if (threadIdx.x < T) finish_pre(m, part, threadIdx.x);   // fixed-order sums over the warps
+            consumer_sync(NTC);                          // partials read before the next item writes them
+            if (threadIdx.x == 0) mbar_arrive_u32(empty_u + 8u * s);
+            if (tr) tr[6] = gtimer();
         }
-        if (f.pub) {                                 // the publisher sums the partials and frees the stage
-            __syncwarp();
-            if (lane == 0) mbar_arrive_u32(done_u + 8u * s);
-            continue;
+    }
+
+    // ============================ A6 (fused, f.a6cnt) ==========================
+    // After its last item every CTA counts itself finished; once all are, the
+    // CTAs form [logL, g] (Eq. 3, Eq. 6-8) for rows b = blockIdx.x, +gridDim.x,
+    // ... in place of codon_ratio_kernel, with its fixed summation order
+    // (patterns strided over the threads, then a fixed tree): the result does
+    // not depend on which CTA takes a row.
+    if (f.a6cnt) {
+        __shared__ double red[32];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(f.a6cnt, 1);
+            wait_count2(f.a6cnt, (int)gridDim.x, a.status);
+            __threadfence();
         }
-        consumer_sync(NTC);                          // stage and partials complete
-        if (threadIdx.x < T) finish_pre(m, part, threadIdx.x);   // fixed-order sums over the warps
-        consumer_sync(NTC);                          // partials read before the next item writes them
-        if (threadIdx.x == 0) mbar_arrive_u32(empty_u + 8u * s);
-        if (tr) tr[6] = gtimer();
+        __syncthreads();
+        const int B = 2 * N - 2;
+        for (int row = blockIdx.x; row <= B; row += gridDim.x) {
+            double acc = 0.0;
+            for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
+                const double wc = a.pat_w[c];
+                if (row < B) {
+                    double num = 0.0, den = 0.0;
+                    const double2 *nd = reinterpret_cast<const double2 *>(a.numden);
+                    for (int rr = 0; rr < R; ++rr) {
+                        const double2 v = __ldcg(nd + ((size_t)row * R + rr) * a.Cpad + c);
+                        num += v.x;
+                        den += v.y;
+                    }
+                    if (wc != 0.0) acc += wc * (num / den);
+                } else {
+                    double L = 0.0;
+                    for (int rr = 0; rr < R; ++rr) L += __ldcg(a.Lpart + (size_t)rr * a.Cpad + c);
+                    if (!(L > 0.0) || !isfinite(L)) atomicMin(a.status, c);
+                    acc += wc * (log(L) + (double)__ldcg(a.E + (size_t)(root - N) * a.Cpad + c) * 0.69314718055994530942);
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) red[warp] = acc;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double t = 0.0;
+                for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) t += red[w2];
+                f.out[row < B ? 1 + row : 0] = t;
+            }
+            __syncthreads();
+        }
     }
 }
 

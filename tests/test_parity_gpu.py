@@ -455,7 +455,9 @@ def test_hmc_leapfrog_matches_oracle_trajectory(model, N, R, C):
                                  {"PG_CODON_FLOW": "1", "PG_FLOW_TCH": "1"},
                                  {"PG_CODON_FLOW": "1", "PG_FLOW_DEFER": "1"},
                                  {"PG_CODON_FLOW": "1", "PG_FLOW_HALF": "1"},
-                                 {"PG_CODON_FLOW": "1", "PG_FLOW_HALF": "1", "PG_FLOW_DEFER": "1"}])
+                                 {"PG_CODON_FLOW": "1", "PG_FLOW_HALF": "1", "PG_FLOW_DEFER": "1"},
+                                 {"PG_FUSED_A6": "1"}, {"PG_FUSED_A6": "0"},
+                                 {"PG_FUSED_A6": "1", "PG_FLOW_PUB": "0"}])
 def test_codon_schedules(env, monkeypatch):
     """Every codon schedule gives the same parity: the level-by-level kernels
     (PG_CODON_FLOW=0), the round-1 one-launch flow kernel (=1, with its chunk
