@@ -86,7 +86,12 @@ int pg_workspace_bytes(const pg_config *cfg, size_t *bytes);
  *                   creates (and owns) a non-blocking stream.
  *   dev_workspace   device memory of >= pg_workspace_bytes() bytes, owned by
  *                   the caller and kept alive until pg_destroy; NULL => the
- *                   library allocates (and frees) its own.
+ *                   library allocates (and frees) its own.  Nucleotide (S <= 4)
+ *                   instances with state tips also get library-allocated
+ *                   staging buffers for the post-order pass (per internal
+ *                   node one step record of its matrices, ~2 KB at R = 4 fp64,
+ *                   and per CTA its tip-code windows, ~0.2 KB per CTA and
+ *                   node), freed by pg_destroy.
  * Errors: PG_ERR_ARG, PG_ERR_UNSUPPORTED, PG_ERR_MEMORY, PG_ERR_CUDA. */
 int pg_create(const pg_config *cfg, void *cuda_stream, void *dev_workspace,
               size_t workspace_bytes, pg_instance **out);

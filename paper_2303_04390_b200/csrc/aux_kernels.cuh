@@ -34,7 +34,8 @@ __global__ void __launch_bounds__(256) pmat_kernel(const double *__restrict__ V,
                                                    const double *__restrict__ rates,
                                                    const double *__restrict__ bl, int S, int R,
                                                    int cs, Real *__restrict__ P, Real *__restrict__ PT,
-                                                   int *__restrict__ status) {
+                                                   int *__restrict__ status, unsigned char *__restrict__ recp,
+                                                   const int *__restrict__ pdst) {
     __shared__ double e[SP];
     pdl_trigger_and_reset(status);
     const int br = blockIdx.x;          // branch * R + r
@@ -43,6 +44,9 @@ __global__ void __launch_bounds__(256) pmat_kernel(const double *__restrict__ V,
     for (int k = threadIdx.x; k < SP; k += blockDim.x) e[k] = k < S ? expm1(lam[k] * t) : 0.0;
     __syncthreads();
     Real *Pm = P + (size_t)br * cs;     // cs = category stride (>= SP*SP, zero padded)
+    // grouped small-S staging: the branch's slot in its post-order step record
+    Real *Rm = nullptr;
+    if (recp && pdst[b] >= 0) Rm = reinterpret_cast<Real *>(recp + pdst[b]) + (size_t)r * cs;
     Real *PTm = PT ? PT + (size_t)br * SP * SP : nullptr;
     for (int idx = threadIdx.x; idx < SP * SP; idx += blockDim.x) {
         const int s = idx / SP, u = idx % SP;
@@ -52,6 +56,7 @@ __global__ void __launch_bounds__(256) pmat_kernel(const double *__restrict__ V,
             acc += M0[idx];
         }
         Pm[idx] = (Real)acc;
+        if (Rm) Rm[idx] = (Real)acc;
         if (PTm) PTm[u * SP + s] = (Real)acc;
     }
     // a category pad that holds SP Reals carries P 1 (row sums, summed in
@@ -63,6 +68,7 @@ __global__ void __launch_bounds__(256) pmat_kernel(const double *__restrict__ V,
             Real acc = Pm[s * SP];
             for (int u = 1; u < SP; ++u) acc += Pm[s * SP + u];
             Pm[SP * SP + s] = acc;
+            if (Rm) Rm[SP * SP + s] = acc;
         }
     }
 }
@@ -147,6 +153,25 @@ __global__ void __launch_bounds__(128) pmat4_mma_kernel(const double *__restrict
 // per-tile gradient partials of branch b, block B the per-tile logL partials,
 // in a fixed order (strided serial sums, then a fixed smem tree).  No atomics,
 // so fp64 results are bitwise reproducible run to run.
+// Grouped post-order staging of the small-S traversal: tip-code windows per
+// (CTA, post step, child) -> ts[cta][m][2][tipw] (child = tip with state
+// codes; other entries left as they are).  Window = the tip's codes of the
+// CTA's patterns from its first pattern rounded down to 16 (the same window
+// the per-step copies take); bytes past the padded row are not read.
+__global__ void tipstream_kernel(const Op4 *__restrict__ post, const uint8_t *__restrict__ tips,
+                                 uint8_t *__restrict__ ts, int N, int Cpad, int cta_pats, int tipw) {
+    const int cta = blockIdx.x, m = blockIdx.y;
+    const Op4 op = post[m];
+    const int p0 = cta * cta_pats, lead = p0 & 15;
+    for (int c = 0; c < 2; ++c) {
+        const int code = c ? op.z : op.y;
+        if (code < 0 || (code & kTipPartialBit)) continue;
+        const uint8_t *src = tips + (size_t)code * Cpad + (p0 - lead);
+        uint8_t *dst = ts + (((size_t)cta * (N - 1) + m) * 2 + c) * tipw;
+        for (int i = threadIdx.x; i < tipw; i += blockDim.x) dst[i] = (p0 - lead + i < Cpad) ? src[i] : (uint8_t)0;
+    }
+}
+
 __global__ void __launch_bounds__(256) reduce_kernel(const double *__restrict__ grad_part,
                                                      const double *__restrict__ logl_part,
                                                      int B, int n_tiles, double *__restrict__ out) {

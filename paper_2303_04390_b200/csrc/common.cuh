@@ -27,6 +27,13 @@ struct TravArgs {
     int *status;                // first zero-likelihood pattern (INT_MAX = none)
     int N, S, R, Cpad, C, n_tiles, depth, prefetch;
     int prog_smem_off;          // > 0: byte offset of the staged op programs in dynamic smem
+    // grouped post-order staging (small-S kernel): per post
+    // step a record [op][P_k][P_a][P_b] (A1 writes the matrices) and, per
+    // CTA, the step's two tip-code windows; GPOST steps per ring stage, two
+    // bulk copies per stage.  null: per-step copies.
+    const unsigned char *rec_post;
+    const unsigned char *tipstream;   // [CTA][N-1][2][tipw]
+    int tipw;
     long long *trace;           // PG_TRACE builds only: clock64 samples of CTA 0
 };
 

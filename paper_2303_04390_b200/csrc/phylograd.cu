@@ -241,6 +241,13 @@ struct pg_instance {
     int flow_pdl = 0;                   // A1 -> flow programmatic dependent launch (PG_FLOW_PDL=0/1 overrides)
     int flow_pub = 1;                   // flow v2: publisher warp (PG_FLOW_PUB)
     bool a6_fused = false;              // set per enqueue: the flow kernel also formed [logL, g]
+    // small-S grouped post-order staging (library-owned buffers)
+    bool grouped = false, tipstream_dirty = true;
+    int tipw = 0;
+    unsigned char *rec_post = nullptr, *tipstream = nullptr;
+    int *post_dst = nullptr;
+    std::vector<int32_t> post_dst_h;
+    size_t rec_cap = 0, ts_cap = 0, dst_cap = 0;
     int flow_pprod = 0;                 // flow v2: the producer forms p = u_a o u_b (PG_FLOW_PPROD)
     int split_items = 0;                // items of the split schedule (task offsets table)
     int flow_split = 0;                 // codon_flow2_kernel: one pre item per child (PG_FLOW_SPLIT=0/1 overrides)
@@ -391,6 +398,9 @@ int pg_destroy(pg_instance *inst) {
     if (inst->staged_ev) cudaEventDestroy(inst->staged_ev);
     if (inst->own_ws && inst->ws) cudaFree(inst->ws);
     if (inst->flow_trace) cudaFree(inst->flow_trace);
+    if (inst->rec_post) cudaFree(inst->rec_post);
+    if (inst->tipstream) cudaFree(inst->tipstream);
+    if (inst->post_dst) cudaFree(inst->post_dst);
     if (inst->bl_pinned) cudaFreeHost(inst->bl_pinned);
     if (inst->clock_pinned) cudaFreeHost(inst->clock_pinned);
     if (inst->out_pinned) cudaFreeHost(inst->out_pinned);
@@ -809,8 +819,8 @@ int pg_set_branch_lengths_device(pg_instance *inst, const double *d_b) {
 // launch configuration
 // -------------------------------------------------------------------------
 
-template <typename Real, int SP, int RP, int TC = 0>
-static void *small_kernel() { return (void *)pg::traverse_small_kernel<Real, SP, RP, TC>; }
+template <typename Real, int SP, int RP, int TC = 0, bool GRP = false>
+static void *small_kernel() { return (void *)pg::traverse_small_kernel<Real, SP, RP, TC, GRP>; }
 template <typename Real, int SP>
 static void *large_kernel() { return (void *)pg::traverse_large_kernel<Real, SP>; }
 template <typename Real, int SP>
@@ -845,18 +855,19 @@ static int pad_categories(int R) {
     return p;
 }
 
-template <typename Real, int SP>
+template <typename Real, int SP, bool GRP = false>
 static void *small_by_rp(int RP) {
     switch (RP) {
-        case 1: return small_kernel<Real, SP, 1>();
-        case 2: return small_kernel<Real, SP, 2>();
-        case 4: return small_kernel<Real, SP, 4>();
-        case 8: return small_kernel<Real, SP, 8>();
-        default: return small_kernel<Real, SP, 16>();
+        case 1: return small_kernel<Real, SP, 1, 0, GRP>();
+        case 2: return small_kernel<Real, SP, 2, 0, GRP>();
+        case 4: return small_kernel<Real, SP, 4, 0, GRP>();
+        case 8: return small_kernel<Real, SP, 8, 0, GRP>();
+        default: return small_kernel<Real, SP, 16, 0, GRP>();
     }
 }
 
-static void *traverse_fn(const Layout &L, int R) {
+// grouped: the small-S kernel with grouped post-order staging (SP = 4)
+static void *traverse_fn(const Layout &L, int R, bool grouped = false) {
     const bool d = L.real == 8;
     const int RP = pad_categories(R);
 #ifdef PG_SMALL_MMA4
@@ -865,7 +876,9 @@ static void *traverse_fn(const Layout &L, int R) {
     if (L.mma) return small_kernel<double, 16, 1, 1>();
 #endif
     switch (L.SP) {
-        case 4: return d ? small_by_rp<double, 4>(RP) : small_by_rp<float, 4>(RP);
+        case 4:
+            if (grouped) return d ? small_by_rp<double, 4, true>(RP) : small_by_rp<float, 4, true>(RP);
+            return d ? small_by_rp<double, 4>(RP) : small_by_rp<float, 4>(RP);
         case 8: return d ? small_by_rp<double, 8>(RP) : small_by_rp<float, 8>(RP);
         case 16: return d ? small_by_rp<double, 16>(RP) : small_by_rp<float, 16>(RP);
         case 32: return d ? large_kernel<double, 32>() : large_kernel<float, 32>();
@@ -888,25 +901,30 @@ static void *pmat_kernel_fn(const Layout &L) {
 }
 
 template <typename Real, int SP>
-static size_t small_smem_t(int RP, int R, int K, int depth) {
+static size_t small_smem_t(int RP, int R, int K, int depth, int tipw) {
     switch (RP) {
-        case 1: return pg::SmallCfg<Real, SP, 1>::smem(R, K, depth);
-        case 2: return pg::SmallCfg<Real, SP, 2>::smem(R, K, depth);
-        case 4: return pg::SmallCfg<Real, SP, 4>::smem(R, K, depth);
-        case 8: return pg::SmallCfg<Real, SP, 8>::smem(R, K, depth);
-        default: return pg::SmallCfg<Real, SP, 16>::smem(R, K, depth);
+        case 1: return pg::SmallCfg<Real, SP, 1>::smem(R, K, depth, tipw);
+        case 2: return pg::SmallCfg<Real, SP, 2>::smem(R, K, depth, tipw);
+        case 4: return pg::SmallCfg<Real, SP, 4>::smem(R, K, depth, tipw);
+        case 8: return pg::SmallCfg<Real, SP, 8>::smem(R, K, depth, tipw);
+        default: return pg::SmallCfg<Real, SP, 16>::smem(R, K, depth, tipw);
     }
 }
-static size_t small_smem(const Layout &L, int R, int K, int depth) {
+// tipw > 0: grouped post-order staging (its ring may be larger than the
+// per-step one)
+static size_t small_smem(const Layout &L, int R, int K, int depth, int tipw = 0) {
     const bool d = L.real == 8;
     const int RP = pad_categories(R);
     if (L.mma) return L.SP == 16 ? pg::SmallCfg<double, 16, 1, 1>::smem(R, K, depth) : pg::SmallCfg<double, 4, 4, 1>::smem(R, K, depth);
     switch (L.SP) {
-        case 4: return d ? small_smem_t<double, 4>(RP, R, K, depth) : small_smem_t<float, 4>(RP, R, K, depth);
-        case 8: return d ? small_smem_t<double, 8>(RP, R, K, depth) : small_smem_t<float, 8>(RP, R, K, depth);
-        default: return d ? small_smem_t<double, 16>(RP, R, K, depth) : small_smem_t<float, 16>(RP, R, K, depth);
+        case 4: return d ? small_smem_t<double, 4>(RP, R, K, depth, tipw) : small_smem_t<float, 4>(RP, R, K, depth, tipw);
+        case 8: return d ? small_smem_t<double, 8>(RP, R, K, depth, tipw) : small_smem_t<float, 8>(RP, R, K, depth, tipw);
+        default: return d ? small_smem_t<double, 16>(RP, R, K, depth, tipw) : small_smem_t<float, 16>(RP, R, K, depth, tipw);
     }
 }
+// tip-code window of a CTA of K tiles (bytes, whole 16-B units): the CTA's
+// first pattern rounded down to 16 plus K tiles of patterns
+static int small_tipw(const Layout &L, int K) { return (15 + K * L.tpl + 15) / 16 * 16; }
 static size_t large_smem(const Layout &L, int R, int depth) {
     const size_t nvec = (size_t)L.tpl * R;
     const size_t vb = nvec * L.SP * L.real;
@@ -974,6 +992,60 @@ static int configure(pg_instance *inst) {
         inst->prefetch = (L.SP <= 8) ? 4 : 2;
         inst->smem = (int)small_smem(L, R, K, depth);
         if (inst->smem > 227 * 1024) return inst->fail(PG_ERR_UNSUPPORTED, "traversal does not fit in shared memory");
+        // grouped post-order staging: state tips only, the
+        // SIMT kernel, library-owned memory, and when its ring fits
+        {
+            bool any_partial = false;
+            for (int t = 0; t < inst->cfg.tips; ++t) any_partial |= inst->tip_is_partial[t] != 0;
+            const char *ge = getenv("PG_GPOST");
+            const int tw = small_tipw(L, K);
+            inst->grouped = !L.mma && L.SP == 4 && !any_partial && !(ge && atoi(ge) == 0) &&
+                            small_smem(L, R, K, depth, tw) <= 227 * 1024;
+            if (getenv("PG_DEBUG_PLAN"))
+                fprintf(stderr, "[phylograd] small-S: K=%d grid=%d grouped=%d (partial=%d own_ws=%d smem=%zu)\n", K,
+                        inst->grid, (int)inst->grouped, (int)any_partial, (int)inst->own_ws,
+                        small_smem(L, R, K, depth, tw));
+            if (inst->grouped) {
+                inst->tipw = tw;
+                inst->smem = (int)small_smem(L, R, K, depth, tw);
+                const int N = inst->cfg.tips, B = L.B;
+                const size_t recb = 16 + 3 * (size_t)R * L.cat_stride * L.real;
+                const size_t rec_need = (size_t)(N - 1) * recb;
+                const size_t ts_need = (size_t)inst->grid * (N - 1) * 2 * tw;
+                if (inst->rec_cap < rec_need) {
+                    if (inst->rec_post) cudaFree(inst->rec_post);
+                    CK(cudaMalloc(&inst->rec_post, rec_need), "post records alloc");
+                    inst->rec_cap = rec_need;
+                }
+                if (inst->ts_cap < ts_need) {
+                    if (inst->tipstream) cudaFree(inst->tipstream);
+                    CK(cudaMalloc(&inst->tipstream, ts_need), "tip stream alloc");
+                    inst->ts_cap = ts_need;
+                }
+                if (inst->dst_cap < (size_t)B) {
+                    if (inst->post_dst) cudaFree(inst->post_dst);
+                    CK(cudaMalloc(&inst->post_dst, sizeof(int) * B), "record map alloc");
+                    inst->dst_cap = B;
+                }
+                // the records' op words (static per plan) and, per branch, the
+                // record slot A1 writes its matrices into
+                CK(cudaMemcpy2DAsync(inst->rec_post, recb, inst->plan.post.data(), sizeof(Op4), sizeof(Op4), N - 1,
+                                     cudaMemcpyHostToDevice, inst->stream), "record ops upload");
+                std::vector<int32_t> dst(B, -1);
+                const size_t ms = (size_t)R * L.cat_stride * L.real;
+                for (int m = 0; m < N - 1; ++m) {
+                    const Op4 op = inst->plan.post[m];
+                    if (op.x != 2 * N - 2) dst[op.x] = (int)(m * recb + 16);
+                    if (op.y >= 0) dst[op.y & ~pg::kTipPartialBit] = (int)(m * recb + 16 + ms);
+                    if (op.z >= 0) dst[op.z & ~pg::kTipPartialBit] = (int)(m * recb + 16 + 2 * ms);
+                }
+                inst->post_dst_h = dst;
+                CK(cudaMemcpyAsync(inst->post_dst, inst->post_dst_h.data(), sizeof(int) * B, cudaMemcpyHostToDevice,
+                                   inst->stream), "record map upload");
+                CK(cudaStreamSynchronize(inst->stream), "record upload sync");
+                inst->tipstream_dirty = true;
+            }
+        }
         // stage both op programs in smem when they fit (producer/consumers never read ops from HBM)
         const int prog_bytes = 2 * (inst->cfg.tips - 1) * (int)sizeof(Op4);
         const int off = (inst->smem + 15) / 16 * 16;
@@ -1094,6 +1166,7 @@ static int configure(pg_instance *inst) {
         inst->smem = (int)large_smem(L, R, depth);
         if (inst->smem > 227 * 1024) return inst->fail(PG_ERR_UNSUPPORTED, "traversal does not fit in shared memory");
     }
+    if (L.variant == 0) fn = traverse_fn(L, R, inst->grouped);
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, inst->smem), "smem attr");
     return PG_OK;
 }
@@ -1182,6 +1255,9 @@ static pg::TravArgs trav_args(pg_instance *inst) {
     a.prefetch = inst->prefetch;
     a.prog_smem_off = inst->prog_smem_off;
     a.trace = inst->trace;
+    a.rec_post = inst->grouped ? inst->rec_post : nullptr;
+    a.tipstream = inst->grouped ? inst->tipstream : nullptr;
+    a.tipw = inst->grouped ? inst->tipw : 0;
     return a;
 }
 
@@ -1322,7 +1398,9 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
                 CK(cudaLaunchKernel((void *)pg::pmat4_mma_kernel, dim3(L.B), dim3(128), args16, 0, inst->stream),
                    "pmat4 launch");
         } else {
-            void *args[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, (void *)&R, &cs, &P, &PT, &status_w};
+            unsigned char *recp = (L.variant == 0 && inst->grouped) ? inst->rec_post : nullptr;
+            const int *pdst = inst->post_dst;
+            void *args[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, (void *)&R, &cs, &P, &PT, &status_w, &recp, &pdst};
             CK(cudaLaunchKernel(fn, dim3(L.B * R), dim3(std::min(256, L.SP * L.SP)), args, 0, inst->stream),
                "pmat launch");
         }
@@ -1455,9 +1533,9 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
             at[0].val.programmaticStreamSerializationAllowed = 1;
             lc.attrs = at;
             lc.numAttrs = 1;
-            CK(cudaLaunchKernelExC(&lc, traverse_fn(L, inst->cfg.categories), args), "traverse launch");
+            CK(cudaLaunchKernelExC(&lc, traverse_fn(L, inst->cfg.categories, inst->grouped), args), "traverse launch");
         } else {
-            CK(cudaLaunchKernel(traverse_fn(L, inst->cfg.categories), dim3(inst->grid), dim3(inst->block), args,
+            CK(cudaLaunchKernel(traverse_fn(L, inst->cfg.categories, inst->grouped), dim3(inst->grid), dim3(inst->block), args,
                                 inst->smem, inst->stream),
                "traverse launch");
         }
@@ -1504,7 +1582,7 @@ static int prepare(pg_instance *inst, bool captured = false) {
     if (captured) {
         // inside the caller's stream capture nothing may synchronise: the
         // plan, launch configuration and tip data must already be on the device
-        if (inst->plan_dirty || inst->partial_modes_dirty || inst->tips_dirty)
+        if (inst->plan_dirty || inst->partial_modes_dirty || inst->tips_dirty || (inst->grouped && inst->tipstream_dirty))
             return inst->fail(PG_ERR_SEQUENCE, "pending uploads (operations, tips or launch plan): run one evaluation "
                                                "outside stream capture before capturing pg_compute_device");
         return PG_OK;
@@ -1516,6 +1594,20 @@ static int prepare(pg_instance *inst, bool captured = false) {
                            cudaMemcpyHostToDevice, inst->stream), "tips upload");
         CK(cudaStreamSynchronize(inst->stream), "tips sync");
         inst->tips_dirty = false;
+        inst->tipstream_dirty = true;
+    }
+    if (inst->grouped && inst->tipstream_dirty) {
+        // per CTA and post step, the tip-code windows of the step's tip
+        // children (static while tips and plan are unchanged)
+        const Layout &L = inst->L;
+        const int N = inst->cfg.tips, K = inst->tiles_per_cta;
+        const uint8_t *tips = inst->at<uint8_t>(L.off_tips);
+        const Op4 *post = inst->at<Op4>(L.off_post);
+        pg::tipstream_kernel<<<dim3(inst->grid, N - 1), 128, 0, inst->stream>>>(post, tips, inst->tipstream, N, L.Cpad,
+                                                                              K * L.tpl, inst->tipw);
+        CK(cudaGetLastError(), "tip stream launch");
+        CK(cudaStreamSynchronize(inst->stream), "tip stream sync");
+        inst->tipstream_dirty = false;
     }
     return PG_OK;
 }

@@ -47,6 +47,9 @@
 #ifndef PG_PROXY_FENCE
 #define PG_PROXY_FENCE 0
 #endif
+#ifndef PG_GPOST
+#define PG_GPOST 8
+#endif
 #ifndef PG_MMA_STAGES
 #define PG_MMA_STAGES 8
 #endif
@@ -179,11 +182,19 @@ struct SmallCfg {
     static constexpr int OPS = 1;
 #endif
     static constexpr int DS = D / OPS < 2 ? 2 : D / OPS;
+    // grouped post-order staging: GPOST steps per stage, DPG stages
+    static constexpr int GPOST = PG_GPOST, DPG = 4;
+    static __host__ __device__ int rec_bytes(int R) { return 16 + 3 * mat_slot(R); }
+    static __host__ __device__ int gstage(int R, int tipw) { return GPOST * (rec_bytes(R) + 2 * tipw); }
+    static __host__ __device__ size_t ring(int R, int K, int tipw) {
+        const size_t a = (size_t)DS * OPS * stage(R, K), b = tipw > 0 ? (size_t)DPG * gstage(R, tipw) : 0;
+        return a > b ? a : b;
+    }
     // barriers (full[DS], empty[DS], post_done, prog_bar) below QOFF, then Q
     // (SP > 4 only; SP <= 4 keeps it in registers).  QOFF follows DS: a fixed
     // 128 B let an 8-stage ring's post_done / prog_bar overlap Q (found by
     // compute-sanitizer synccheck on the S = 16 tensor-core variant)
-    static constexpr int QOFF = (8 * (2 * DS + 2) + 127) / 128 * 128;
+    static constexpr int QOFF = (8 * (2 * DS + 2 + 2 * DPG) + 127) / 128 * 128;
     static constexpr int BARS = QOFF + (SP > 4 ? SP * SP * (int)sizeof(Real) : 0);   // barriers + Q
     static __host__ __device__ int mat_slot(int R) { return MMA ? MMA_SLOT : MMA4 ? MMA4_SLOT : R * CS; }
     static __host__ __device__ int mat_rec(int R) { return MMA ? MMA_REC : MMA4 ? 2 * MMA4_SLOT : R * CS; }   // bytes per branch in HBM
@@ -203,8 +214,8 @@ struct SmallCfg {
     // producer refill only after both ops: 24 % slower for S = 4; for S = 16
     // (MMM) 2 stages x 2 ops vs 4 stages x 1 op measured 0.228 vs 0.222 ms
     // (scripts/gpu_mmm_stages.sh), so one op per stage everywhere.
-    static __host__ __device__ size_t smem(int R, int K, int depth) {
-        return (size_t)BARS + (size_t)DS * OPS * stage(R, K) + (size_t)K * warp_bytes(depth);
+    static __host__ __device__ size_t smem(int R, int K, int depth, int tipw = 0) {
+        return (size_t)BARS + ring(R, K, tipw) + (size_t)K * warp_bytes(depth);
     }
 };
 
@@ -442,7 +453,8 @@ __device__ __forceinline__ int maybe_rescale(Real (&v)[SP]) {
 }
 
 
-template <typename Real, int SP, int RP, int TC = 0>
+// GRP: grouped post-order staging (a.rec_post / a.tipstream; SP = 4 only)
+template <typename Real, int SP, int RP, int TC = 0, bool GRP = false>
 __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) traverse_small_kernel(const TravArgs a) {
     using Cfg = SmallCfg<Real, SP, RP, TC>;
     constexpr int TP = Cfg::TP, PF = Cfg::PF, W = Cfg::W, VB = Cfg::VB, CS = Cfg::CS;
@@ -466,13 +478,19 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);            // [D]
     uint64_t *empty = full + DS;                                    // [DS]
     uint64_t *post_done = empty + DS;                               // [1]
+    uint64_t *gfull = post_done + 2, *gempty = gfull + Cfg::DPG;    // grouped post stages
     unsigned char *stages = smem + Cfg::BARS;
+    constexpr bool grouped = GRP;
+    constexpr int GG = Cfg::GPOST, DPG = Cfg::DPG;
+    const int RECB = Cfg::rec_bytes(a.R), TW = a.tipw, GSTG = grouped ? Cfg::gstage(a.R, a.tipw) : 0;
     // shared-window addresses of the barriers and stages (loop-invariant bases)
     const uint32_t sbase = smem_u32(smem);
     const uint32_t full_u = sbase, empty_u = sbase + 8u * DS, stages_u = sbase + Cfg::BARS;
     // step t (post 0..nops-1, pre nops..2nops-1) -> ring stage and slot; the
     // pre program starts on a fresh stage
-    const int GP = (nops + OPS - 1) / OPS;
+    // grouped: the pre program's stages are numbered from 0 (the post
+    // program uses its own ring and barriers)
+    const int GP = grouped ? 0 : (nops + OPS - 1) / OPS;
     auto stg = [&](int t) { return t < nops ? t / OPS : GP + (t - nops) / OPS; };
     auto slot = [&](int t) { return t < nops ? t % OPS : (t - nops) % OPS; };
     auto sub_off = [&](int t) { return (stg(t) % DS) * (OPS * ST) + slot(t) * ST; };
@@ -494,6 +512,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     }
     if (threadIdx.x == 0) {
         for (int i = 0; i < DS; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, K); }
+        for (int i = 0; i < DPG; ++i) { mbar_init(gfull + i, 1); mbar_init(gempty + i, K); }
         mbar_init(post_done, K);
         mbar_init(prog_bar, 1);
         fence_mbar_init();
@@ -594,9 +613,27 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
                 }
             }
         };
+        if (grouped) {
+            // post program: GG steps per stage -- the steps' records (op,
+            // matrices) and this CTA's tip-code windows, two bulk copies
+            const int NGP = (nops + GG - 1) / GG;
+            for (int g = 0; g < NGP; ++g) {
+                const int sg = g % DPG;
+                if (g >= DPG) mbar_wait_u32(smem_u32(gempty + sg), (uint32_t)(g / DPG + 1) & 1u);
+                if (lane == 0) {
+                    const int m0 = g * GG, cnt = min(GG, nops - m0);
+                    const uint32_t bar = smem_u32(gfull + sg), dst = stages_u + sg * GSTG;
+                    mbar_arrive_expect_tx_u32(bar, (unsigned)cnt * (RECB + 2 * TW));
+                    bulk_g2s_u32(dst, a.rec_post + (size_t)m0 * RECB, (unsigned)cnt * RECB, bar);
+                    bulk_g2s_u32(dst + GG * RECB, a.tipstream + ((size_t)blockIdx.x * nops + m0) * 2 * TW,
+                                 (unsigned)cnt * 2 * TW, bar);
+                }
+                __syncwarp();
+            }
+        }
         const int NG = GP + (nops + OPS - 1) / OPS;
-        for (int g = 0; g < NG; ++g) {
-            const bool pre = g >= GP;
+        for (int g = grouped ? 0 : 0; g < NG; ++g) {
+            const bool pre = grouped || g >= GP;
             const int t0 = pre ? nops + (g - GP) * OPS : g * OPS;
             const int t1 = min(t0 + OPS, pre ? 2 * nops : nops);
             PG_TSTAMP((size_t)t0 * 16 + 0, g);
@@ -629,7 +666,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     const int pl = lane / G;
     const int pat0 = tile * TP;
     const int pat = pat0 + pl;
-    unsigned char *wsm = stages + DS * OPS * ST + (size_t)warp * Cfg::warp_bytes(a.depth);
+    unsigned char *wsm = stages + Cfg::ring(R, K, grouped ? TW : 0) + (size_t)warp * Cfg::warp_bytes(a.depth);
     unsigned char *stackb = wsm;
     const int pi_slot = a.depth;
     double *nd = reinterpret_cast<double *>(wsm + (a.depth + 1) * 32 * VBL);       // [W][TP][3]
@@ -761,9 +798,31 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     int prev_slot = -1;
     Real prev_u[VL];
     Op4 op_next = {0, 0, 0, 0};
+    // post-program stage addressing: grouped (GG steps per stage: records,
+    // then the tip windows) or one step per stage
+    auto post_st = [&](int t) -> const unsigned char * {
+        return grouped ? stages + (size_t)((t / GG) % DPG) * GSTG + (size_t)(t % GG) * RECB : stages + sub_off(t);
+    };
+    auto post_tip = [&](int t, int c) -> const unsigned char * {
+        return grouped ? stages + (size_t)((t / GG) % DPG) * GSTG + (size_t)GG * RECB + (size_t)(t % GG) * 2 * TW + c * TW
+                       : stages + sub_off(t) + 16 + 3 * MS + c * VS;
+    };
+    auto post_wait = [&](int t) {
+        if (grouped) {
+            if (t % GG == 0) mbar_wait_u32(smem_u32(gfull + (t / GG) % DPG), (uint32_t)((t / GG) / DPG) & 1u);
+        } else if (slot(t) == 0) {
+            wait_full(t);
+        }
+    };
+    auto post_release = [&](int t) {
+        if (!grouped) { release(t); return; }
+        if (t % GG != GG - 1 && t != nops - 1) return;
+        __syncwarp();
+        if (lane == 0) mbar_arrive_u32(smem_u32(gempty + (t / GG) % DPG));
+    };
     if (active && nops > 0) {
-        wait_full(0);
-        op_next = *reinterpret_cast<const Op4 *>(stages + sub_off(0));
+        post_wait(0);
+        op_next = *reinterpret_cast<const Op4 *>(post_st(0));
     }
     auto stack_or_fwd = [&](Real (&u)[VL], int code) {
         const int sl = -code - 1;
@@ -776,30 +835,29 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     };
     for (int t = 0; t < nops; ++t) {
         if (!active) {
-            if (slot(t) == 0) wait_full(t);
-            release(t);
+            post_wait(t);
+            post_release(t);
             continue;
         }
-        const unsigned char *st = stages + sub_off(t);
+        const unsigned char *st = post_st(t);
         const Op4 op = op_next;
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 3, op.x);
         Real ua[VL], ub[VL];
         if (op.y < 0) stack_or_fwd(ua, op.y);
-        else child_tip(ua, st + 16 + MS, st + 16 + 3 * MS, op.y);
+        else child_tip(ua, st + 16 + MS, post_tip(t, 0), op.y);
         if (op.z < 0) stack_or_fwd(ub, op.z);
-        else child_tip(ub, st + 16 + 2 * MS, st + 16 + 3 * MS + VS, op.z);
+        else child_tip(ub, st + 16 + 2 * MS, post_tip(t, 1), op.z);
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 4, ua[0] + ub[VL - 1]);
         if (t + 1 < nops) {
-            const int t1 = t + 1;
-            if (slot(t1) == 0) wait_full(t1);
-            op_next = *reinterpret_cast<const Op4 *>(stages + sub_off(t1));
+            post_wait(t + 1);
+            op_next = *reinterpret_cast<const Op4 *>(post_st(t + 1));
         }
         if (warp == 0) PG_TSTAMP((size_t)t * 16 + 5, op_next.x);
         Real p[VL];
 #pragma unroll
         for (int s = 0; s < VL; ++s) p[s] = ua[s] * ub[s];
         if (op.x == root) {
-            release(t);
+            post_release(t);
             double L = 0.0;
             if constexpr (MMA4) {
 #pragma unroll
@@ -830,7 +888,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
                 mv<Real, SP, VL>(u, reinterpret_cast<const Real *>(st + 16 + mat_lane), pf, h);
             }
             if (warp == 0) PG_TSTAMP((size_t)t * 16 + 7, u[0] + u[VL - 1]);
-            release(t);
+            post_release(t);
             stg_vec<Real, VL>(Ub + (size_t)(op.x - N) * u_node + u_lane, u);   // shadow lanes: same value
             stk_st(op.w, u);
 #pragma unroll

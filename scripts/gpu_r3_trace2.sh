@@ -6,6 +6,6 @@ for v in ${TV:-trace trace_bulk}; do
   L=$PWD/paper_2303_04390_b200/lib/libphylograd_$v.so
   for C in 1184 10000; do
     echo "=== $v C=$C"
-    TRACE_C=$C PHYLOGRAD_LIB=$L timeout 300 python scripts/trace_dengue.py 1 2>&1 | grep -A12 "== post\|== pre" | grep "consumer step\|prod\|=="
+    TRACE_C=$C PHYLOGRAD_LIB=$L timeout 300 python scripts/trace_dengue.py 1 2>&1 
   done
 done
