@@ -35,7 +35,8 @@ __global__ void __launch_bounds__(256) pmat_kernel(const double *__restrict__ V,
                                                    const double *__restrict__ bl, int S, int R,
                                                    int cs, Real *__restrict__ P, Real *__restrict__ PT,
                                                    int *__restrict__ status, unsigned char *__restrict__ recp,
-                                                   const int *__restrict__ pdst) {
+                                                   const int *__restrict__ pdst, unsigned char *__restrict__ recq,
+                                                   const int *__restrict__ qdst) {
     __shared__ double e[SP];
     pdl_trigger_and_reset(status);
     const int br = blockIdx.x;          // branch * R + r
@@ -45,8 +46,9 @@ __global__ void __launch_bounds__(256) pmat_kernel(const double *__restrict__ V,
     __syncthreads();
     Real *Pm = P + (size_t)br * cs;     // cs = category stride (>= SP*SP, zero padded)
     // grouped small-S staging: the branch's slot in its post-order step record
-    Real *Rm = nullptr;
+    Real *Rm = nullptr, *Qm = nullptr;
     if (recp && pdst[b] >= 0) Rm = reinterpret_cast<Real *>(recp + pdst[b]) + (size_t)r * cs;
+    if (recq && qdst[b] >= 0) Qm = reinterpret_cast<Real *>(recq + qdst[b]) + (size_t)r * cs;   // pre-order record
     Real *PTm = PT ? PT + (size_t)br * SP * SP : nullptr;
     for (int idx = threadIdx.x; idx < SP * SP; idx += blockDim.x) {
         const int s = idx / SP, u = idx % SP;
@@ -57,6 +59,7 @@ __global__ void __launch_bounds__(256) pmat_kernel(const double *__restrict__ V,
         }
         Pm[idx] = (Real)acc;
         if (Rm) Rm[idx] = (Real)acc;
+        if (Qm) Qm[idx] = (Real)acc;
         if (PTm) PTm[u * SP + s] = (Real)acc;
     }
     // a category pad that holds SP Reals carries P 1 (row sums, summed in
@@ -69,6 +72,7 @@ __global__ void __launch_bounds__(256) pmat_kernel(const double *__restrict__ V,
             for (int u = 1; u < SP; ++u) acc += Pm[s * SP + u];
             Pm[SP * SP + s] = acc;
             if (Rm) Rm[SP * SP + s] = acc;
+            if (Qm) Qm[SP * SP + s] = acc;
         }
     }
 }

@@ -32,6 +32,7 @@ struct TravArgs {
     // CTA, the step's two tip-code windows; GPOST steps per ring stage, two
     // bulk copies per stage.  null: per-step copies.
     const unsigned char *rec_post;
+    const unsigned char *rec_pre;     // per pre step [op][P_a][P_b] (grouped mode)
     const unsigned char *tipstream;   // [CTA][N-1][2][tipw]
     int tipw;
     long long *trace;           // PG_TRACE builds only: clock64 samples of CTA 0

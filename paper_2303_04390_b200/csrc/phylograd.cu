@@ -244,7 +244,7 @@ struct pg_instance {
     // small-S grouped post-order staging (library-owned buffers)
     bool grouped = false, tipstream_dirty = true;
     int tipw = 0;
-    unsigned char *rec_post = nullptr, *tipstream = nullptr;
+    unsigned char *rec_post = nullptr, *rec_pre = nullptr, *tipstream = nullptr;
     int *post_dst = nullptr;
     std::vector<int32_t> post_dst_h;
     size_t rec_cap = 0, ts_cap = 0, dst_cap = 0;
@@ -1010,7 +1010,8 @@ static int configure(pg_instance *inst) {
                 inst->smem = (int)small_smem(L, R, K, depth, tw);
                 const int N = inst->cfg.tips, B = L.B;
                 const size_t recb = 16 + 3 * (size_t)R * L.cat_stride * L.real;
-                const size_t rec_need = (size_t)(N - 1) * recb;
+                const size_t recpb = 16 + 2 * (size_t)R * L.cat_stride * L.real;
+                const size_t rec_need = (size_t)(N - 1) * (recb + recpb);
                 const size_t ts_need = (size_t)inst->grid * (N - 1) * 2 * tw;
                 if (inst->rec_cap < rec_need) {
                     if (inst->rec_post) cudaFree(inst->rec_post);
@@ -1022,25 +1023,31 @@ static int configure(pg_instance *inst) {
                     CK(cudaMalloc(&inst->tipstream, ts_need), "tip stream alloc");
                     inst->ts_cap = ts_need;
                 }
-                if (inst->dst_cap < (size_t)B) {
+                if (inst->dst_cap < (size_t)2 * B) {
                     if (inst->post_dst) cudaFree(inst->post_dst);
-                    CK(cudaMalloc(&inst->post_dst, sizeof(int) * B), "record map alloc");
-                    inst->dst_cap = B;
+                    CK(cudaMalloc(&inst->post_dst, sizeof(int) * 2 * B), "record map alloc");
+                    inst->dst_cap = 2 * B;
                 }
+                inst->rec_pre = inst->rec_post + (size_t)(N - 1) * recb;
                 // the records' op words (static per plan) and, per branch, the
                 // record slot A1 writes its matrices into
                 CK(cudaMemcpy2DAsync(inst->rec_post, recb, inst->plan.post.data(), sizeof(Op4), sizeof(Op4), N - 1,
                                      cudaMemcpyHostToDevice, inst->stream), "record ops upload");
-                std::vector<int32_t> dst(B, -1);
+                CK(cudaMemcpy2DAsync(inst->rec_pre, recpb, inst->plan.pre.data(), sizeof(Op4), sizeof(Op4), N - 1,
+                                     cudaMemcpyHostToDevice, inst->stream), "record ops upload");
+                std::vector<int32_t> dst(2 * B, -1);     // [post slot][pre slot] per branch
                 const size_t ms = (size_t)R * L.cat_stride * L.real;
                 for (int m = 0; m < N - 1; ++m) {
                     const Op4 op = inst->plan.post[m];
                     if (op.x != 2 * N - 2) dst[op.x] = (int)(m * recb + 16);
                     if (op.y >= 0) dst[op.y & ~pg::kTipPartialBit] = (int)(m * recb + 16 + ms);
                     if (op.z >= 0) dst[op.z & ~pg::kTipPartialBit] = (int)(m * recb + 16 + 2 * ms);
+                    const Op4 oq = inst->plan.pre[m];
+                    dst[B + (oq.y & ~pg::kTipPartialBit)] = (int)(m * recpb + 16);
+                    dst[B + (oq.z & ~pg::kTipPartialBit)] = (int)(m * recpb + 16 + ms);
                 }
                 inst->post_dst_h = dst;
-                CK(cudaMemcpyAsync(inst->post_dst, inst->post_dst_h.data(), sizeof(int) * B, cudaMemcpyHostToDevice,
+                CK(cudaMemcpyAsync(inst->post_dst, inst->post_dst_h.data(), sizeof(int) * 2 * B, cudaMemcpyHostToDevice,
                                    inst->stream), "record map upload");
                 CK(cudaStreamSynchronize(inst->stream), "record upload sync");
                 inst->tipstream_dirty = true;
@@ -1256,6 +1263,7 @@ static pg::TravArgs trav_args(pg_instance *inst) {
     a.prog_smem_off = inst->prog_smem_off;
     a.trace = inst->trace;
     a.rec_post = inst->grouped ? inst->rec_post : nullptr;
+    a.rec_pre = inst->grouped ? inst->rec_pre : nullptr;
     a.tipstream = inst->grouped ? inst->tipstream : nullptr;
     a.tipw = inst->grouped ? inst->tipw : 0;
     return a;
@@ -1400,7 +1408,10 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         } else {
             unsigned char *recp = (L.variant == 0 && inst->grouped) ? inst->rec_post : nullptr;
             const int *pdst = inst->post_dst;
-            void *args[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, (void *)&R, &cs, &P, &PT, &status_w, &recp, &pdst};
+            unsigned char *recq = recp ? inst->rec_pre : nullptr;
+            const int *qdst = recp ? inst->post_dst + L.B : nullptr;
+            void *args[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, (void *)&R, &cs, &P, &PT, &status_w, &recp, &pdst,
+                            &recq, &qdst};
             CK(cudaLaunchKernel(fn, dim3(L.B * R), dim3(std::min(256, L.SP * L.SP)), args, 0, inst->stream),
                "pmat launch");
         }

@@ -579,6 +579,23 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             const Op4 *gprog = pre ? a.pre : a.post;           // global copy (bulk source)
             const Op4 *prog = pre ? pre_prog : post_prog;       // smem copy when staged
             const Op4 op = prog[m];
+            if (grouped && pre) {
+                // the step's record: op and both children's matrices, one copy
+                const unsigned recpb = 16 + 2 * MS;
+                bulk_g2s_u32(st, a.rec_pre + (size_t)m * recpb, recpb, bar);
+                const int na = op.y & ~kTipPartialBit, nb = op.z & ~kTipPartialBit;
+                if (na >= N) bulk_g2s_u32(st + 16 + 3 * MS, u_src(na), u_bytes, bar);
+                else copy_tip(st + 16 + 3 * MS, op.y, bar);
+                if (nb >= N) bulk_g2s_u32(st + 16 + 3 * MS + VS, u_src(nb), u_bytes, bar);
+                else copy_tip(st + 16 + 3 * MS + VS, op.z, bar);
+                if (m + PF < nops) {
+                    const Op4 o2 = prog[m + PF];
+                    const int pa = o2.y & ~kTipPartialBit, pb = o2.z & ~kTipPartialBit;
+                    if (pa >= N) prefetch_l2(u_src(pa), u_bytes);
+                    if (pb >= N) prefetch_l2(u_src(pb), u_bytes);
+                }
+                return;
+            }
             bulk_g2s_u32(st, gprog + m, 16, bar);
             if (PG_TIPP_PF && tipP && m + PF < nops) {      // partial-tip chunks into L2 ahead (HBM latency)
                 const Op4 o2 = prog[m + PF];
