@@ -88,9 +88,7 @@ __global__ void __launch_bounds__(256) pmat16_mma_kernel(const double *__restric
                                                          const double *__restrict__ lam,
                                                          const double *__restrict__ rates,
                                                          const double *__restrict__ bl, int S, int rec,
-                                                         double *__restrict__ P, int *__restrict__ status,
-                                                         unsigned char *__restrict__ recp, const int *__restrict__ pdst,
-                                                         unsigned char *__restrict__ recq, const int *__restrict__ qdst) {
+                                                         double *__restrict__ P, int *__restrict__ status) {
     __shared__ double e[16], Ps[16][17];
     pdl_trigger_and_reset(status);
     const int b = blockIdx.x;
@@ -125,22 +123,6 @@ __global__ void __launch_bounds__(256) pmat16_mma_kernel(const double *__restric
             for (int c = 0; c < 16; ++c) v += Ps[row][c];
         }
         R2[i] = v;
-    }
-    // staging records (traverse_small_kernel GRP variant): the layout each
-    // record slot needs (destination = byte offset * 4 + layout), copied from
-    // the branch record just written (same block: visible after the barrier)
-    if (recp) {
-        __syncthreads();
-        const int dp = pdst[b], dq = qdst[b];
-        const double *Rs[3] = {R0, R1, R2};
-        if (dp >= 0) {
-            double *d = reinterpret_cast<double *>(recp + (dp >> 2));
-            for (int i = threadIdx.x; i < 16 * 17; i += blockDim.x) d[i] = Rs[dp & 3][i];
-        }
-        if (dq >= 0) {
-            double *d = reinterpret_cast<double *>(recq + (dq >> 2));
-            for (int i = threadIdx.x; i < 16 * 17; i += blockDim.x) d[i] = Rs[dq & 3][i];
-        }
     }
 }
 
