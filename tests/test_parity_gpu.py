@@ -284,6 +284,24 @@ def test_sequencing_errors_and_replanning():
     inst.close()
 
 
+@pytest.mark.parametrize("gpost", ["1", "0"])
+def test_tip_updates_between_computes(gpost, monkeypatch):
+    """New tip states after an evaluation reach the next one: the grouped
+    post-order staging (PG_GPOST=1, S = 4) rebuilds its per-CTA tip-code
+    streams; several CTAs of K > 1 tiles and a partial last CTA."""
+    monkeypatch.setenv("PG_GPOST", gpost)
+    pg = _pg()
+    pb = ps.small_problem(60, "hky", R=4, C=3000, seed=11, missing=0.05, simulate=True)
+    inst = pg.from_problem(pb)
+    _compare(pb, inst=inst)
+    rng = np.random.default_rng(3)
+    for t in rng.choice(pb.n_tips, 7, replace=False):
+        pb.tip_states[t] = rng.integers(0, 5, size=pb.patterns)   # code 4 = missing
+        inst.set_tip_states(int(t), pb.tip_states[t])
+    _compare(pb, inst=inst)
+    inst.close()
+
+
 def test_caller_owned_stream_and_virtual_sharding():
     """T3(a): g instances over disjoint pattern shards on one GPU, summed,
     equal the unsharded evaluation (the multi-GPU maths without g GPUs)."""
