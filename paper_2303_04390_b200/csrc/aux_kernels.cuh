@@ -14,6 +14,7 @@ __device__ __forceinline__ void pdl_trigger_and_reset(int *status) {
     if (status && blockIdx.x == 0 && threadIdx.x == 0) {
         status[0] = 0x7f7f7f7f;
         status[1] = 0;
+        status[2] = 0;                  // finished-CTA count of a fused A6
     }
 }
 

@@ -35,6 +35,10 @@ struct TravArgs {
     const unsigned char *rec_pre;     // per pre step [op][P_a][P_b] (grouped mode)
     const unsigned char *tipstream;   // [CTA][N-1][2][tipw]
     int tipw;
+    // A6 fused into the traversal (co-resident grids): finished-CTA counter
+    // (reset by A1) and the [logL, g] output; null: reduce_kernel
+    int *a6cnt;
+    double *out;
     long long *trace;           // PG_TRACE builds only: clock64 samples of CTA 0
 };
 

@@ -243,6 +243,7 @@ struct pg_instance {
     bool a6_fused = false;              // set per enqueue: the flow kernel also formed [logL, g]
     // small-S grouped post-order staging (library-owned buffers)
     bool grouped = false, tipstream_dirty = true;
+    bool small_coresident = false;      // small-S grid fits the GPU at once (fused A6 possible)
     int tipw = 0;
     unsigned char *rec_post = nullptr, *rec_pre = nullptr, *tipstream = nullptr;
     int *post_dst = nullptr;
@@ -1175,6 +1176,13 @@ static int configure(pg_instance *inst) {
     }
     if (L.variant == 0) fn = traverse_fn(L, R, inst->grouped);
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, inst->smem), "smem attr");
+    if (L.variant == 0) {
+        // A6 can be fused into the traversal only when the whole grid is
+        // co-resident (its CTAs wait for each other at the end)
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, inst->block, inst->smem), "occupancy");
+        inst->small_coresident = per_sm > 0 && inst->grid <= per_sm * inst->sm_count;
+    }
     return PG_OK;
 }
 
@@ -1340,6 +1348,13 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
     // serialization (setup overlaps the previous kernel; griddepcontrol.wait
     // before the dependent reads); not with timing events in between
     const bool pdl_small = L.variant == 0 && !inst->timing && !getenv("PG_NO_SMALL_PDL");
+    // A6 inside the traversal (no reduce launch) when its grid is co-resident;
+    // not under the per-kernel timing pass, which times A6 on its own
+    const char *fse = getenv("PG_SMALL_FUSED_A6");
+    // (measured slower than the separate launch: dengue 1.216 vs 1.246 ms, MMM
+    // 0.1159 vs 0.1174 ms -- the last CTA's wait, then one CTA per row; off
+    // unless PG_SMALL_FUSED_A6=1)
+    const bool fuse_small_a6 = L.variant == 0 && !L.mma && !inst->timing && inst->small_coresident && fse && atoi(fse) != 0;
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[0], inst->stream, cudaEventRecordExternal), "event");
     const double *V = inst->at<double>(L.off_V), *Vi = inst->at<double>(L.off_Vi),
                  *lam = inst->at<double>(L.off_lam), *rates = inst->at<double>(L.off_rates),
@@ -1532,6 +1547,10 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         }
     } else {
         pg::TravArgs a = trav_args(inst);
+        if (fuse_small_a6) {
+            a.a6cnt = status_w + 2;                  // reset by A1 (pdl_trigger_and_reset)
+            a.out = d_out;
+        }
         void *args[] = {&a};
         if (pdl_small) {
             cudaLaunchConfig_t lc{};
@@ -1552,8 +1571,8 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         }
     }
     if (inst->timing) CK(cudaEventRecordWithFlags(inst->ev[2], inst->stream, cudaEventRecordExternal), "event");
-    if (inst->a6_fused) {
-        // A6 ran inside the flow kernel
+    if (inst->a6_fused || fuse_small_a6) {
+        // A6 ran inside the flow kernel / the small-S traversal
     } else if (L.variant >= 2) {
         pg::codon::CodonArgs c = codon_args(inst);
         int *cnt = inst->at<int>(L.off_flow) + 32 + (size_t)2 * (inst->cfg.tips - 1) * L.n_tiles + (size_t)L.B * R;

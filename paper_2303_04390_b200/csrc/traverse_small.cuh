@@ -535,6 +535,55 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     // the status words A1 resets) are read only after this
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
+    // A6 fused (a.a6cnt; the host sets it only when the whole grid is
+    // co-resident): after its warps are done every CTA counts itself
+    // finished; once all are, CTA c sums rows c, c + grid, ... of the
+    // per-tile partials (threads stride the tiles, then a fixed tree) into
+    // out = [logL, g] -- in place of reduce_kernel, the same numbers whichever
+    // CTA takes a row.  Reached by the producer and the consumer warps at
+    // different points: named barrier 1.
+    auto a6_epilogue = [&]() {
+        if constexpr (MMA || MMA4) return;     // (not offered on the tensor path)
+        if (!a.a6cnt) return;
+        __shared__ double a6red[32];
+        asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(a.a6cnt, 1);
+            int x;
+            unsigned long long t0;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            for (unsigned it = 0;; ++it) {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(x) : "l"(a.a6cnt) : "memory");
+                if (x >= (int)gridDim.x) break;
+                if ((it & 1023u) == 1023u) {
+                    unsigned long long t1;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+                    if (t1 - t0 > 20000000000ull) { atomicExch(a.status + 1, 1); break; }   // reported as a stall
+                }
+                __nanosleep(64);
+            }
+            __threadfence();
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
+        const int B = 2 * N - 2, nw = blockDim.x >> 5;
+        for (int row = blockIdx.x; row <= B; row += gridDim.x) {
+            const double *src = row < B ? a.grad_part + (size_t)row * a.n_tiles : a.logl_part;
+            double acc = 0.0;
+            for (int i = threadIdx.x; i < a.n_tiles; i += blockDim.x) acc += __ldcg(src + i);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if ((threadIdx.x & 31) == 0) a6red[threadIdx.x >> 5] = acc;
+            asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
+            if (threadIdx.x == 0) {
+                double t = 0.0;
+                for (int w2 = 0; w2 < nw; ++w2) t += a6red[w2];
+                a.out[row < B ? 1 + row : 0] = t;
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x) : "memory");
+        }
+    };
+
     // =============================== producer ===================================
     if (warp == K) {
         const unsigned u_bytes = ntile * TP * R * VB;
@@ -668,6 +717,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             __syncwarp();
             PG_TSTAMP((size_t)t0 * 16 + 2, g);
         }
+        a6_epilogue();
         return;
     }
 
@@ -1136,6 +1186,7 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     }
     if (DEFER && active && nops > 0) store_totals(nops - 1);
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // A6 may start launching
+    a6_epilogue();
 }
 
 }  // namespace pg
