@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <algorithm>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)
@@ -113,9 +114,10 @@ __global__ void pre_level(const Ent *__restrict__ ent, int cnt, int N, int C, in
         na += __shfl_xor_sync(0xffffffffu, na, o);
         nb += __shfl_xor_sync(0xffffffffu, nb, o);
     }
-    if (live && (threadIdx.x & 31) == 0) {       // (per * 32 | C R: a warp stays in one node)
-        atomicAdd(grad + e.a, na);
-        atomicAdd(grad + e.b, nb);
+    if (live && (threadIdx.x & 31) == 0) {       // per-warp partials, summed later (no atomics)
+        const size_t wi = idx >> 5;
+        grad[2 * wi] = na;
+        grad[2 * wi + 1] = nb;
     }
 }
 
@@ -143,7 +145,9 @@ int main(int argc, char **argv) {
     CK(cudaMalloc(&q, V * (N - 1)));
     CK(cudaMalloc(&P, (size_t)B * R * 16 * 8));
     CK(cudaMalloc(&Q, 16 * 8));
-    CK(cudaMalloc(&grad, B * 8));
+    size_t maxw = 0;                               // per-warp partial slots of the widest pre level
+    for (auto &l : pre) maxw = std::max(maxw, l.size() * (size_t)C * R / 32 + 1);
+    CK(cudaMalloc(&grad, 2 * maxw * 8));
     CK(cudaMalloc(&L, (size_t)C * R * 8));
     CK(cudaMalloc(&flush, 256u << 20));
     CK(cudaMalloc(&dt, tips.size()));
@@ -162,7 +166,6 @@ int main(int argc, char **argv) {
     cudaGraph_t g;
     cudaGraphExec_t ge;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal));
-    CK(cudaMemsetAsync(grad, 0, B * 8, st));
     const int T = 256;
     for (int i = 0; i < npl; ++i) {
         const size_t n = post[i].size() * (size_t)C * R;
