@@ -1435,17 +1435,31 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
     if (L.variant == 4) {
         pg::tcp::TcArgs t = tc_args(inst);
         const auto &pl = inst->plan;
+        // every level launched with programmatic stream serialization: its
+        // CTAs set up (TMEM, barriers, tip states) while the previous level's
+        // last CTAs run, then griddepcontrol.wait (not with timing events)
+        const bool pdl = !inst->timing && !getenv("PG_NO_TC_PDL");
+        auto lvl = [&](void *fn, int off, int cnt, size_t smem) -> cudaError_t {
+            void *args[] = {&t, &off};
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3(L.n_tiles, cnt, R);
+            lc.blockDim = dim3(pg::tcp::TM);
+            lc.dynamicSmemBytes = smem;
+            lc.stream = inst->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            lc.attrs = at;
+            lc.numAttrs = pdl ? 1 : 0;
+            return cudaLaunchKernelExC(&lc, fn, args);
+        };
         for (size_t i = 0; i + 1 < pl.post_off.size(); ++i) {
             int off = pl.post_off[i], cnt = pl.post_off[i + 1] - off;
-            void *args[] = {&t, &off};
-            CK(cudaLaunchKernel((void *)pg::tcp::tc_post_kernel, dim3(L.n_tiles, cnt, R), dim3(pg::tcp::TM), args,
-                                pg::tcp::post_smem(), inst->stream), "tc post launch");
+            CK(lvl((void *)pg::tcp::tc_post_kernel, off, cnt, pg::tcp::post_smem()), "tc post launch");
         }
         for (size_t i = 0; i + 1 < pl.pre_off.size(); ++i) {
             int off = pl.pre_off[i], cnt = pl.pre_off[i + 1] - off;
-            void *args[] = {&t, &off};
-            CK(cudaLaunchKernel((void *)pg::tcp::tc_pre_kernel, dim3(L.n_tiles, cnt, R), dim3(pg::tcp::TM), args,
-                                pg::tcp::pre_smem(), inst->stream), "tc pre launch");
+            CK(lvl((void *)pg::tcp::tc_pre_kernel, off, cnt, pg::tcp::pre_smem()), "tc pre launch");
         }
     } else if (L.variant == 3) {
         pg::codon::CodonArgs c = codon_args(inst);
@@ -1579,8 +1593,16 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         double *sp = inst->at<double>(L.off_gpart);      // [B+1][slices] <= [B][n_tiles] + [n_tiles] (codon path)
         const int ns = std::min(pg::codon::RATIO_SLICES, L.n_tiles);
         void *args[] = {&c, &d_out, &sp, &cnt};
-        CK(cudaLaunchKernel((void *)pg::codon::codon_ratio_kernel, dim3(L.B + 1, ns), dim3(256), args, 0, inst->stream),
-           "codon ratio launch");
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(L.B + 1, ns);
+        lc.blockDim = dim3(256);
+        lc.stream = inst->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = (L.variant == 4 && !inst->timing && !getenv("PG_NO_TC_PDL")) ? 1 : 0;
+        CK(cudaLaunchKernelExC(&lc, (void *)pg::codon::codon_ratio_kernel, args), "codon ratio launch");
     } else {
         const double *gp = inst->at<double>(L.off_gpart), *lp = inst->at<double>(L.off_lpart);
         int B = L.B, nt = L.n_tiles;

@@ -144,11 +144,16 @@ __global__ void __launch_bounds__(TM, 1) tc_post_kernel(const TcArgs t, int leve
     const int k = e.x, ca = e.y, cb = e.z;
     const int root = 2 * a.N - 2, pat0 = tile * TM, m = threadIdx.x, warp = threadIdx.x >> 5;
     const bool isroot = k == root;
+    // programmatic dependent launch: the next level's CTAs may start their
+    // prologue; everything this level reads from earlier launches comes after
+    // griddepcontrol.wait
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (warp == 0 && !isroot) tc::tmem_alloc<64>(tmem_base);
     if (threadIdx.x == 0) { mbar_init(bar, 1); mbar_init(bar + 1, 1); fence_mbar_init(); }
     sta[m] = ca < a.N ? a.tip_states[(size_t)ca * a.Cpad + pat0 + m] : 0;
     stb[m] = cb < a.N ? a.tip_states[(size_t)cb * a.Cpad + pat0 + m] : 0;
     __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     uint32_t tx = 0;
     load_tile(S1, t, ca, r, tile, sta, bar, tx);
     load_tile(S2, t, cb, r, tile, stb, bar, tx);
@@ -223,11 +228,13 @@ __global__ void __launch_bounds__(TM, 1) tc_pre_kernel(const TcArgs t, int level
     const int4 e = a.lev4[level_off + blockIdx.y];
     const int k = e.x, ch[2] = {e.y, e.z};
     const int root = 2 * a.N - 2, pat0 = tile * TM, m = threadIdx.x, warp = threadIdx.x >> 5;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // (see tc_post_kernel)
     if (warp == 0) tc::tmem_alloc<128>(tmem_base);
     if (threadIdx.x == 0) { mbar_init(bar, 1); mbar_init(bar + 1, 1); mbar_init(bar + 2, 1); fence_mbar_init(); }
     sta[m] = ch[0] < a.N ? a.tip_states[(size_t)ch[0] * a.Cpad + pat0 + m] : 0;
     stb[m] = ch[1] < a.N ? a.tip_states[(size_t)ch[1] * a.Cpad + pat0 + m] : 0;
     __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     uint32_t tx = 0;
     if (k != root) {
         if (threadIdx.x == 0) bulk_g2s(Qk, t.q + (((size_t)(k - a.N) * a.R + r) * a.ntiles + tile) * TILE, TILE_B, bar);
@@ -334,6 +341,7 @@ __global__ void __launch_bounds__(256) tc_pmat_kernel(const double *__restrict__
     double *Vs = e + SP;                                     // V's A fragments [SP*SP]
     const int br = blockIdx.x, r = br % R, b = br / R;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the first post level may set up
     for (int i = threadIdx.x; i < SP * SP / 2; i += blockDim.x) cp_async16(Vs + 2 * i, VA + 2 * i);
     cp_async_commit();
     const double t = rates[r] * bl[b];
