@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(128) pmat4_mma_kernel(const double *__restrict
 // the per-step copies take); bytes past the padded row are not read.
 __global__ void tipstream_kernel(const Op4 *__restrict__ post, const uint8_t *__restrict__ tips,
                                  uint8_t *__restrict__ ts, int N, int Cpad, int cta_pats, int tipw) {
-    const int cta = blockIdx.x, m = blockIdx.y;
+    const int m = blockIdx.x, cta = blockIdx.y;     // steps on x (N - 1 may exceed 65535)
     const Op4 op = post[m];
     const int p0 = cta * cta_pats, lead = p0 & 15;
     for (int c = 0; c < 2; ++c) {

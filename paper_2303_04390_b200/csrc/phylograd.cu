@@ -1655,7 +1655,7 @@ static int prepare(pg_instance *inst, bool captured = false) {
         const int N = inst->cfg.tips, K = inst->tiles_per_cta;
         const uint8_t *tips = inst->at<uint8_t>(L.off_tips);
         const Op4 *post = inst->at<Op4>(L.off_post);
-        pg::tipstream_kernel<<<dim3(inst->grid, N - 1), 128, 0, inst->stream>>>(post, tips, inst->tipstream, N, L.Cpad,
+        pg::tipstream_kernel<<<dim3(N - 1, inst->grid), 128, 0, inst->stream>>>(post, tips, inst->tipstream, N, L.Cpad,
                                                                               K * L.tpl, inst->tipw);
         CK(cudaGetLastError(), "tip stream launch");
         CK(cudaStreamSynchronize(inst->stream), "tip stream sync");
