@@ -1,6 +1,7 @@
 // common.cuh -- device helpers shared by the phylograd kernels (sm_100a).
 #pragma once
 #include <cuda_runtime.h>
+#include <climits>
 #include <cstdint>
 
 #include "schedule.hpp"

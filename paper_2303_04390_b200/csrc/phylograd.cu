@@ -45,7 +45,7 @@ struct Layout {
         off_post, off_pre, total;
     // codon (variant 2) extras
     size_t off_M0one = 0, off_PBpre = 0, off_DT = 0, off_PONE = 0, off_QB = 0, off_q = 0, off_E = 0, off_child = 0,
-           off_levels = 0, off_lev4 = 0, off_taskoff = 0, off_tipmode = 0, off_utip = 0, off_tipmask = 0, off_tipmasked = 0, off_VA = 0, off_ViB = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0,
+           off_levels = 0, off_lev4 = 0, off_EQ = 0, off_Y = 0, off_taskoff = 0, off_tipmode = 0, off_utip = 0, off_tipmask = 0, off_tipmasked = 0, off_VA = 0, off_ViB = 0, off_fmax = 0, off_qmax = 0, off_numden = 0, off_Lpart = 0,
            off_flow = 0, flow_bytes = 0, reset_bytes = 0;
     // time-tree parameterisation: parent/child_a/child_b [3][2N-1], heights, rate scalars, branch sets
     size_t off_tree = 0, off_h = 0, off_rho = 0, off_bset = 0;
@@ -61,6 +61,10 @@ int padded_states(int S) {
     if (S <= 256) return 256;          // S = 256 class (NEXT-2): fp64 only
     return 0;
 }
+
+// ints of the flow schedules' completion counters {rpost, rpre}, per
+// (internal node, category, tile)
+static size_t flow_counter_ints(long long N, int R, int n_tiles) { return (size_t)2 * (N - 1) * R * n_tiles; }
 
 int make_layout(const pg_config *c, Layout *L, std::string *err) {
     if (!c) { if (err) *err = "config is NULL"; return PG_ERR_ARG; }
@@ -171,16 +175,22 @@ int make_layout(const pg_config *c, Layout *L, std::string *err) {
         // 0/1 mask partials with <= 4 ones (MMM hidden states): state lists, u by gathers
         L->off_tipmask = take((c->flags & PG_FLAG_TIP_PARTIALS) ? (size_t)N * L->Cpad * 4 : 0);
         L->off_tipmasked = take((size_t)N);
-        L->off_E = take((size_t)(N - 1) * L->Cpad * 4);
+        // exponent arrays and completion counters sized per category: the
+        // flow v2 kernel keeps them per (node, category) (its items depend
+        // only on their own category); the other schedules use the first
+        // [node][Cpad] / [node][chunk] part
+        L->off_E = take((size_t)(N - 1) * R * L->Cpad * 4);
+        L->off_EQ = take((size_t)(N - 2 > 0 ? N - 2 : 1) * R * L->Cpad * 4);
+        L->off_Y = take((size_t)L->B * R * L->Cpad * 4);
         // fmax [N-1], qmax [N-2], then the flow schedule's counters
         // {item counter, rpost [N-1][<= ntiles], rpre [N-1][<= ntiles]}: one memset
         // {item counter, rpost, rpre, A1 done flags [B][R], ratio slice counters [B+1]}
         // + the fused A6's finished-CTA counter
-        L->flow_bytes = ((size_t)32 + (size_t)2 * (N - 1) * L->n_tiles + (size_t)L->B * R + (L->B + 1) + 32) * 4;
-        L->reset_bytes = (size_t)(2 * N - 3) * L->Cpad * 4 + L->flow_bytes;
+        L->flow_bytes = ((size_t)32 + flow_counter_ints(N, R, L->n_tiles) + (size_t)L->B * R + (L->B + 1) + 32) * 4;
+        L->reset_bytes = (size_t)(2 * N - 3) * R * L->Cpad * 4 + L->flow_bytes;
         L->off_fmax = take(L->reset_bytes);
-        L->off_qmax = L->off_fmax + (size_t)(N - 1) * L->Cpad * 4;
-        L->off_flow = L->off_qmax + (size_t)(N - 2) * L->Cpad * 4;
+        L->off_qmax = L->off_fmax + (size_t)(N - 1) * R * L->Cpad * 4;
+        L->off_flow = L->off_qmax + (size_t)(N - 2) * R * L->Cpad * 4;
         L->off_numden = take((size_t)L->B * R * L->Cpad * 16);
         L->off_Lpart = take((size_t)R * L->Cpad * 8);
         L->off_child = take((size_t)2 * (2 * N - 1) * 4);
@@ -1307,6 +1317,11 @@ static pg::codon::CodonArgs codon_args(pg_instance *inst) {
     c.fmax = inst->at<int>(L.off_fmax);
     c.qmax = inst->at<int>(L.off_qmax);
     c.numden = inst->at<double>(L.off_numden);
+    // flow v2: per-category exponents (the ratio kernel reconciles them)
+    if (L.variant == 2 && inst->flow_ver == 2 && inst->flow_tch > 0 && inst->cfg.categories > 1) {
+        c.EQ = inst->at<int>(L.off_EQ);
+        c.Y = inst->at<int>(L.off_Y);
+    }
     c.Lpart = inst->at<double>(L.off_Lpart);
     c.grad_part = inst->at<double>(L.off_gpart);
     c.logl_part = inst->at<double>(L.off_lpart);
@@ -1391,7 +1406,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         const double *M0 = inst->at<double>(L.off_M0), *Qd = inst->at<double>(L.off_Q);
         // per-evaluation counters (rescaling maxima, flow counters, A1 flags)
         CK(cudaMemsetAsync(inst->ws + L.off_fmax, 0, L.reset_bytes, inst->stream), "fmax/flow reset");
-        int *pready = inst->at<int>(L.off_flow) + 32 + (size_t)2 * (inst->cfg.tips - 1) * L.n_tiles;
+        int *pready = inst->at<int>(L.off_flow) + 32 + flow_counter_ints(inst->cfg.tips, R, L.n_tiles);
         int Nt = inst->cfg.tips, tipp = (inst->cfg.flags & PG_FLAG_TIP_PARTIALS) ? 1 : 0;
         void *args[] = {&VA, &ViB, &M0, &Qd, &lam, &rates, &bl, &S, (void *)&R, &Nt, &tipp, &PBpost, &PBpre, &PT, &DT, &PONE, &pready};
         const CodonFns cf = codon_fns(L.SP);
@@ -1487,7 +1502,8 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
             f.tch = inst->flow_tch;
             f.nch = (L.n_tiles + f.tch - 1) / f.tch;
             f.rpost = f.ctr + 32;
-            f.rpre = f.rpost + (size_t)(N - 1) * f.nch;
+            // flow v2: per (node, category, tile); v1: per (node, chunk)
+            f.rpre = f.rpost + (size_t)(N - 1) * f.nch * (inst->flow_ver == 2 ? R : 1);
             f.npost = pl.post_off.back();
             f.ntask = (int)pl.level_nodes.size();
             f.defer = inst->flow_defer;
@@ -1511,7 +1527,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
                 const char *fa6 = getenv("PG_FUSED_A6");
                 const bool fuse = fa6 ? atoi(fa6) != 0 : inst->cfg.patterns <= 2 * (int)cf.flow2_threads;
                 if (fuse && !inst->timing) {
-                    f.a6cnt = inst->at<int>(L.off_flow) + 32 + (size_t)2 * (N - 1) * L.n_tiles + (size_t)L.B * R + (L.B + 1);
+                    f.a6cnt = inst->at<int>(L.off_flow) + 32 + flow_counter_ints(N, R, L.n_tiles) + (size_t)L.B * R + (L.B + 1);
                     f.out = d_out;
                     inst->a6_fused = true;
                 }
@@ -1520,7 +1536,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
                 // programmatic dependent launch right behind A1 (no partial-tip
                 // kernels or timing events in between): items wait on pready
                 const bool pdl = inst->flow_pdl && !inst->timing && !(inst->cfg.flags & PG_FLAG_TIP_PARTIALS);
-                f.pready = pdl ? inst->at<int>(L.off_flow) + 32 + (size_t)2 * (N - 1) * L.n_tiles : nullptr;
+                f.pready = pdl ? inst->at<int>(L.off_flow) + 32 + flow_counter_ints(N, R, L.n_tiles) : nullptr;
                 void *args2[] = {&c, &f, &inst->tmaps};
                 cudaLaunchConfig_t lc{};
                 const bool rs = inst->flow_rs == 2;
@@ -1589,7 +1605,7 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         // A6 ran inside the flow kernel / the small-S traversal
     } else if (L.variant >= 2) {
         pg::codon::CodonArgs c = codon_args(inst);
-        int *cnt = inst->at<int>(L.off_flow) + 32 + (size_t)2 * (inst->cfg.tips - 1) * L.n_tiles + (size_t)L.B * R;
+        int *cnt = inst->at<int>(L.off_flow) + 32 + flow_counter_ints(inst->cfg.tips, R, L.n_tiles) + (size_t)L.B * R;
         double *sp = inst->at<double>(L.off_gpart);      // [B+1][slices] <= [B][n_tiles] + [n_tiles] (codon path)
         const int ns = std::min(pg::codon::RATIO_SLICES, L.n_tiles);
         void *args[] = {&c, &d_out, &sp, &cnt};

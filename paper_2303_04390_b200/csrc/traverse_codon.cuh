@@ -71,6 +71,12 @@ struct CodonArgs {
     int *fmax;                        // [N-1][Cpad] max exponent field of u over categories (atomicMax)
     int *qmax;                        // [N-2][Cpad] same for q
     double *numden;                   // [B][R][Cpad][2] Eq. 8 terms per category
+    // per-category exponents (codon_flow2_kernel; null elsewhere): E, fmax and
+    // qmax above are then [node][R][Cpad]; EQ [N-2][R][Cpad] cumulative
+    // exponent inside the stored q; Y [B][R][Cpad] exponent of a branch's
+    // Eq. 8 terms (EQ of the parent + E of both children), reconciled over
+    // categories in A6
+    int *EQ, *Y;
     double *Lpart;                    // [R][Cpad] root likelihood terms per category
     double *grad_part;                // [B][ntiles]
     double *logl_part;                // [ntiles]
@@ -626,6 +632,53 @@ __global__ void __launch_bounds__(codon_threads<SP>(), codon_ctas_per_sm<SP>()) 
 // slice to finish (atomic counter) adds the slice sums in slice order, so the
 // result does not depend on which block finished last (deterministic).
 constexpr int RATIO_SLICES = 8;
+// 2^d for d <= 0 (0 below the normal range: such terms are 2^-1022 below the
+// largest and vanish in its rounding)
+__device__ __forceinline__ double pow2le0(int d) {
+    return d < -1022 ? 0.0 : __longlong_as_double((long long)(1023 + d) << 52);
+}
+// sum_r num_r and sum_r den_r of branch b, pattern c: with per-category
+// exponents (a.Y) each category's terms are first brought to the largest
+// exponent of the pattern (exact powers of two; a term 2^-1000 below the
+// largest underflows to 0, far below rounding)
+__device__ __forceinline__ void ratio_terms(const CodonArgs &a, int b, int c, double &num, double &den) {
+    const double2 *nd = reinterpret_cast<const double2 *>(a.numden);
+    num = 0.0;
+    den = 0.0;
+    if (!a.Y) {
+        for (int r = 0; r < a.R; ++r) {
+            const double2 v = __ldcg(nd + ((size_t)b * a.R + r) * a.Cpad + c);
+            num += v.x;
+            den += v.y;
+        }
+        return;
+    }
+    int ym = INT_MIN;
+    for (int r = 0; r < a.R; ++r) ym = max(ym, __ldcg(a.Y + ((size_t)b * a.R + r) * a.Cpad + c));
+    for (int r = 0; r < a.R; ++r) {
+        const double2 v = __ldcg(nd + ((size_t)b * a.R + r) * a.Cpad + c);
+        const double f = pow2le0(__ldcg(a.Y + ((size_t)b * a.R + r) * a.Cpad + c) - ym);
+        num = fma(v.x, f, num);
+        den = fma(v.y, f, den);
+    }
+}
+// sum_r Lpart_r of pattern c relative to 2^Em (Em = the root's exponent;
+// per category with a.Y: the largest of them)
+__device__ __forceinline__ double root_likelihood(const CodonArgs &a, int c, int &Em) {
+    const int root = 2 * a.N - 2;
+    double L = 0.0;
+    if (!a.Y) {
+        for (int r = 0; r < a.R; ++r) L += __ldcg(a.Lpart + (size_t)r * a.Cpad + c);
+        Em = __ldcg(a.E + (size_t)(root - a.N) * a.Cpad + c);
+        return L;
+    }
+    Em = INT_MIN;
+    for (int r = 0; r < a.R; ++r) Em = max(Em, __ldcg(a.E + ((size_t)(root - a.N) * a.R + r) * a.Cpad + c));
+    for (int r = 0; r < a.R; ++r)
+        L = fma(__ldcg(a.Lpart + (size_t)r * a.Cpad + c),
+                pow2le0(__ldcg(a.E + ((size_t)(root - a.N) * a.R + r) * a.Cpad + c) - Em), L);
+    return L;
+}
 __global__ void __launch_bounds__(256) codon_ratio_kernel(const CodonArgs a, double *out, double *slice_part,
                                                           int *slice_cnt) {
     __shared__ double sh[256];
@@ -638,18 +691,14 @@ __global__ void __launch_bounds__(256) codon_ratio_kernel(const CodonArgs a, dou
     for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
         const double wc = a.pat_w[c];
         if (b < B) {
-            double num = 0.0, den = 0.0;
-            for (int r = 0; r < a.R; ++r) {
-                const double2 v = reinterpret_cast<const double2 *>(a.numden)[((size_t)b * a.R + r) * a.Cpad + c];
-                num += v.x;
-                den += v.y;
-            }
+            double num, den;
+            ratio_terms(a, b, c, num, den);
             if (wc != 0.0) acc += wc * (num / den);
         } else {
-            double L = 0.0;
-            for (int r = 0; r < a.R; ++r) L += a.Lpart[(size_t)r * a.Cpad + c];
+            int Em;
+            const double L = root_likelihood(a, c, Em);
             if (!(L > 0.0) || !isfinite(L)) atomicMin(a.status, c);
-            acc += wc * (log(L) + (double)a.E[(size_t)(root - a.N) * a.Cpad + c] * 0.69314718055994530942);
+            acc += wc * (log(L) + (double)Em * 0.69314718055994530942);
         }
     }
     sh[threadIdx.x] = acc;

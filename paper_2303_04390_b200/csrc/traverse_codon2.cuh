@@ -100,7 +100,8 @@ struct alignas(16) Meta2 {
     int cs, pad0, pad1, pad2; // pre items: -1 both children, else the one child of a split item
     int fa[T], fb[T];         // children's fmax (IEEE exponent fields), internal children
     int fq[T];                // qmax of the parent (pre, non-root)
-    int Ea[T], Eb[T];         // children's cumulative exponents (post, r == 0)
+    int Ea[T], Eb[T];         // children's cumulative exponents (this category)
+    int Qe[T];                // cumulative exponent of q_k (pre, non-root; this category)
     uint8_t sa[T], sb[T];     // state codes of state-tip children
 };
 
@@ -157,6 +158,11 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int R = a.R, ntiles = a.ntiles, N = a.N;
     const int root = 2 * N - 2;
+    // per-category exponents and completion counters: an item depends only on
+    // its own category's inputs (round 1: on all R categories, through the
+    // exponent shared across categories)
+    auto fi = [&](int node, int r, int p) -> size_t { return ((size_t)(node - N) * R + r) * a.Cpad + p; };
+    auto ci = [&](int node, int r, int t) -> size_t { return ((size_t)(node - N) * R + r) * ntiles + t; };
     // items: post (task, r, tile); pre (task, r, tile) for both children, or
     // with f.split, for a parent whose children are both internal, (task,
     // child, r, tile): one child each -- the two q GEMMs of the parent then
@@ -300,10 +306,10 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
             // ---- inputs published by other items
             if (lane == 0) {
                 if (post || k == root) {
-                    if (ca >= N) wait_count2(f.rpost + (size_t)(ca - N) * ntiles + tile, R, a.status);
-                    if (cb >= N) wait_count2(f.rpost + (size_t)(cb - N) * ntiles + tile, R, a.status);
+                    if (ca >= N) wait_count2(f.rpost + ci(ca, r, tile), 1, a.status);
+                    if (cb >= N) wait_count2(f.rpost + ci(cb, r, tile), 1, a.status);
                 } else {
-                    wait_count2(f.rpre + (size_t)(k - N) * ntiles + tile, R, a.status);
+                    wait_count2(f.rpre + ci(k, r, tile), 1, a.status);
                 }
                 if (tr) tr[2] = gtimer();
                 fence_proxy_async_global();          // published generic stores -> our async-proxy reads
@@ -326,18 +332,24 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
             __syncwarp();
             // per-pattern rescaling exponents of the inputs (lane = pattern),
             // 4-byte cp.async into the stage's metadata
-            if (ca >= N) cp_async4(&m->fa[lane], a.fmax + (size_t)(ca - N) * a.Cpad + pat);
+            if (ca >= N) cp_async4(&m->fa[lane], a.fmax + fi(ca, r, pat));
             else m->fa[lane] = 0;
-            if (cb >= N) cp_async4(&m->fb[lane], a.fmax + (size_t)(cb - N) * a.Cpad + pat);
+            if (cb >= N) cp_async4(&m->fb[lane], a.fmax + fi(cb, r, pat));
             else m->fb[lane] = 0;
+            // (a.Y: exponents reconciled over R > 1 categories in A6; the pre
+            // items then also need q_k's and the children's cumulative ones)
             if (!post) {
-                if (k != root) cp_async4(&m->fq[lane], a.qmax + (size_t)(k - N) * a.Cpad + pat);
+                if (k != root) cp_async4(&m->fq[lane], a.qmax + fi(k, r, pat));
                 else m->fq[lane] = 0;
+                if (a.Y) {
+                    if (k != root) cp_async4(&m->Qe[lane], a.EQ + fi(k, r, pat));
+                    else m->Qe[lane] = 0;
+                }
             }
-            if (post && r == 0) {
-                if (ca >= N) cp_async4(&m->Ea[lane], a.E + (size_t)(ca - N) * a.Cpad + pat);
+            if (post || a.Y) {
+                if (ca >= N) cp_async4(&m->Ea[lane], a.E + fi(ca, r, pat));
                 else m->Ea[lane] = 0;
-                if (cb >= N) cp_async4(&m->Eb[lane], a.E + (size_t)(cb - N) * a.Cpad + pat);
+                if (cb >= N) cp_async4(&m->Eb[lane], a.E + fi(cb, r, pat));
                 else m->Eb[lane] = 0;
             }
             // the stage is complete when the TMA bytes, every lane's cp.async
@@ -382,6 +394,12 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
         const size_t pat = (size_t)m->tile * T + mm;
         if (c0 == 0) nd[((size_t)ca * R + r) * a.Cpad + pat] = make_double2(s0 * sn0, wr * sd);
         if (c1 == 1) nd[((size_t)cb * R + r) * a.Cpad + pat] = make_double2(s1 * sn1, wr * sd);
+        // the terms' exponent: q_k's and both children's (tiles are unscaled)
+        if (a.Y) {
+            const int y = m->Qe[mm] + m->Ea[mm] + m->Eb[mm];
+            if (c0 == 0) a.Y[((size_t)ca * R + r) * a.Cpad + pat] = y;
+            if (c1 == 1) a.Y[((size_t)cb * R + r) * a.Cpad + pat] = y;
+        }
     };
 
     // ================================ publisher ===============================
@@ -406,20 +424,20 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
             const Meta2 *m = meta(s);
             const int item = m->item;
             if (item < 0) break;
-            const int k = m->lev.x, ca = m->lev.y, cb = m->lev.z, tile = m->tile, cs = m->cs;
+            const int k = m->lev.x, ca = m->lev.y, cb = m->lev.z, tile = m->tile, cs = m->cs, r = m->r;
             const bool post = m->task < f.npost;
             unsigned long long *tr = (f.trace && lane == 0) ? f.trace + TRW * (size_t)item : nullptr;
             if (lane == 0) {
                 if (post) {
                     mbar_arrive_u32(empty_u + 8u * s);   // fields read above: the stage is free
                     __threadfence();
-                    atomicAdd(f.rpost + (size_t)(k - N) * ntiles + tile, 1);
+                    atomicAdd(f.rpost + ci(k, r, tile), 1);
                 } else {
                     const bool pa = cs != 1 && ca >= N, pb = cs != 0 && cb >= N;
                     if (pa || pb) {
                         __threadfence();
-                        if (pa) atomicAdd(f.rpre + (size_t)(ca - N) * ntiles + tile, 1);
-                        if (pb) atomicAdd(f.rpre + (size_t)(cb - N) * ntiles + tile, 1);
+                        if (pa) atomicAdd(f.rpre + ci(ca, r, tile), 1);
+                        if (pb) atomicAdd(f.rpre + ci(cb, r, tile), 1);
                     }
                 }
                 if (tr) tr[5] = gtimer();
@@ -463,10 +481,10 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
                     const int mm = threadIdx.x;
                     const int Ek = m->Ea[mm] + m->Eb[mm] + (ca >= N ? lazy_exp(m->fa[mm]) : 0) +
                                    (cb >= N ? lazy_exp(m->fb[mm]) : 0);
-                    a.E[(size_t)(k - N) * a.Cpad + pat0 + mm] = Ek;
+                    a.E[fi(k, r, pat0 + mm)] = Ek;
                 };
                 if (k == root) {
-                    if (r == 0 && threadIdx.x < T) storeE();
+                    if (threadIdx.x < T) storeE();
                     // Eq. 3 terms: thread -> (pattern mm, states j, j+TPP, ...)
                     constexpr int TPP = NTC / T;
                     const int mm = threadIdx.x / TPP, j = threadIdx.x % TPP;
@@ -498,9 +516,9 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
                     double acc[MTW][2];
                     gemm_tile<SP, MTW>(acc, As + mt0 * KT * 32, bfr, lane);
                     if (tr) tr[4] = gtimer();
-                    if (r == 0 && threadIdx.x < T) storeE();
+                    if (threadIdx.x < T) storeE();
                     double *out = a.u + (((size_t)(k - N) * R + r) * ntiles + tile) * TILE;
-                    int *fm = a.fmax + (size_t)(k - N) * a.Cpad + pat0;
+                    int *fm = a.fmax + fi(k, r, pat0);
     #pragma unroll
                     for (int ml = 0; ml < MTW; ++ml) {
                         const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
@@ -524,7 +542,7 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
                 consumer_sync(NTC);                      // stage consumed, outputs issued
                 if (threadIdx.x == 0) {
                     __threadfence();
-                    atomicAdd(f.rpost + (size_t)(k - N) * ntiles + tile, 1);
+                    atomicAdd(f.rpost + ci(k, r, tile), 1);
                     mbar_arrive_u32(empty_u + 8u * s);
                     if (tr) tr[6] = gtimer();
                 }
@@ -537,6 +555,14 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
                 return (c ? cb : ca) >= N ? pow2neg(lazy_exp(c ? m->fb[mm] : m->fa[mm])) : 1.0;
             };
             auto Uc = [&](int c) { return c ? Bs : As; };
+            // cumulative exponent inside the stored q_c (row mm): q_k's plus the
+            // sibling's u exponent, plus the factors applied to this product
+            auto q_exp = [&](int c, int node, int mm) {
+                const int fs = c ? m->fa[mm] : m->fb[mm], sib = c ? ca : cb;
+                const int e = m->Qe[mm] + (c ? m->Ea[mm] : m->Eb[mm]) + (k == root ? 0 : lazy_exp(m->fq[mm])) +
+                              (sib >= N ? lazy_exp(fs) : 0);
+                a.EQ[fi(node, r, pat0 + mm)] = e;
+            };
             // q_c = x_c P_c (Eq. 4) from the x_c tile Xs; rows scaled by the q_k
             // and sibling exponents
             auto q_gemm = [&](int c, const double *Xs) {
@@ -545,7 +571,8 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
                 load_bfrag<SP>(bq, a.PBpre + ((size_t)node * R + r) * MAT, w, lane);
                 gemm_tile<SP, MTW>(acc, Xs + mt0 * KT * 32, bq, lane);
                 double *out = a.q + (((size_t)(node - N) * R + r) * ntiles + tile) * TILE;
-                int *qm = a.qmax + (size_t)(node - N) * a.Cpad + pat0;
+                int *qm = a.qmax + fi(node, r, pat0);
+                if (a.Y && threadIdx.x < T) q_exp(c, node, threadIdx.x);
     #pragma unroll
                 for (int ml = 0; ml < MTW; ++ml) {
                     const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
@@ -570,8 +597,8 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
                 consumer_sync(NTC);
                 if (threadIdx.x == 0) {
                     __threadfence();
-                    if (pa) atomicAdd(f.rpre + (size_t)(ca - N) * ntiles + tile, 1);
-                    if (pb) atomicAdd(f.rpre + (size_t)(cb - N) * ntiles + tile, 1);
+                    if (pa) atomicAdd(f.rpre + ci(ca, r, tile), 1);
+                    if (pb) atomicAdd(f.rpre + ci(cb, r, tile), 1);
                 }
             };
             // Eq. 8 terms of child c: num_c = x_c'(Q u_c) (internal child or partial
@@ -664,7 +691,8 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
                             dmma(acc[ml], Qs[p] * Ub[p], bq[kt]);
                         }
                     double *out = a.q + (((size_t)(node - N) * R + r) * ntiles + tile) * TILE;
-                    int *qm = a.qmax + (size_t)(node - N) * a.Cpad + pat0;
+                    int *qm = a.qmax + fi(node, r, pat0);
+                    if (a.Y && threadIdx.x < T) q_exp(c, node, threadIdx.x);
     #pragma unroll
                     for (int ml = 0; ml < MTW; ++ml) {
                         const int mm = (mt0 + ml) * 8 + (lane >> 2), n = w * 8 + 2 * (lane & 3);
@@ -725,19 +753,14 @@ __global__ void __launch_bounds__(flow2_threads<SP, RS>(), (flow2_ctas<SP, NST, 
             for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
                 const double wc = a.pat_w[c];
                 if (row < B) {
-                    double num = 0.0, den = 0.0;
-                    const double2 *nd = reinterpret_cast<const double2 *>(a.numden);
-                    for (int rr = 0; rr < R; ++rr) {
-                        const double2 v = __ldcg(nd + ((size_t)row * R + rr) * a.Cpad + c);
-                        num += v.x;
-                        den += v.y;
-                    }
+                    double num, den;
+                    ratio_terms(a, row, c, num, den);
                     if (wc != 0.0) acc += wc * (num / den);
                 } else {
-                    double L = 0.0;
-                    for (int rr = 0; rr < R; ++rr) L += __ldcg(a.Lpart + (size_t)rr * a.Cpad + c);
+                    int Em;
+                    const double L = root_likelihood(a, c, Em);
                     if (!(L > 0.0) || !isfinite(L)) atomicMin(a.status, c);
-                    acc += wc * (log(L) + (double)__ldcg(a.E + (size_t)(root - N) * a.Cpad + c) * 0.69314718055994530942);
+                    acc += wc * (log(L) + (double)Em * 0.69314718055994530942);
                 }
             }
 #pragma unroll
