@@ -522,14 +522,15 @@ def run_ours(args):
 def run_extra_configs(args, peaks):
     """The codon (FP64 tensor) workloads beside the headline line, each timed
     on this GPU with the same protocol (BJ:configs[3], [4], and rank 0's
-    shard of the 8-GPU yeast run)."""
+    shard of the 8-GPU yeast and WNV runs -- BJ:configs[4] is the sharded
+    workload)."""
     import torch
     dev = torch.device("cuda", 0)
     flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     out = {}
     steps, warmup = min(args.steps, 200), max(3, min(args.warmup, 20))
     import paper_2303_04390_b200 as pg
-    for cfg, shard in ((3, 0), (4, 0), (3, 8), (2, 0), (5, 0)):
+    for cfg, shard in ((3, 0), (4, 0), (3, 8), (4, 8), (2, 0), (5, 0)):
         pb = make_problem(cfg, "fp64")
         C = pb.patterns
         lo, hi = pg.shard_range(C, shard, 0) if shard else (0, C)
