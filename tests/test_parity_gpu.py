@@ -163,6 +163,35 @@ def test_small_shapes(model, N, R, C):
     _compare(pb)
 
 
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("seed", range(6))
+def test_nucleotide_staging_shapes(seed, precision):
+    """Randomised nucleotide shapes through the grouped post-order staging
+    (per-step records, tip-code streams): tree sizes that are not multiples
+    of the 8-step group, 1-16 categories (category pads with and without the
+    P 1 column), several tiles per CTA and partial last CTAs."""
+    rng = np.random.default_rng(100 + seed)
+    N = int(rng.integers(2, 300))
+    R = int(rng.choice([1, 2, 3, 4, 5, 8, 16]))
+    C = int(rng.integers(1, 4000))
+    pb = ps.small_problem(N, str(rng.choice(["jc", "hky", "gtr"])), R=R, C=C, seed=seed,
+                          missing=float(rng.uniform(0, 0.3)), simulate=True)
+    _compare(pb, precision=precision)
+
+
+def test_large_tree_programs_not_staged():
+    """A tree whose two traversal programs do not fit in shared memory beside
+    the ring and stacks (4,000 tips: 128 KB of ops): the producer reads ops
+    from global memory; grouped post-order staging still on."""
+    pb = ps.small_problem(4000, "hky", R=4, C=600, seed=9, missing=0.05, simulate=True)
+    # floor the coalescent's shortest branches (3.5e-6 here): on those the
+    # literal fp64 Eq. 1 of the oracle is 2e-10 from exact while the CUDA
+    # path's identity-split A1 is 2e-13 (measured against oracle/extended.py;
+    # DESIGN.md R15b)
+    pb.branch_lengths[:] = np.maximum(pb.branch_lengths, 1e-3)
+    _compare(pb)
+
+
 @pytest.mark.parametrize("model,R", [("mmm4", 8), ("mmm2", 16), ("hky", 16)])
 def test_max_categories(model, R):
     # lane maps at their limits: S = 16 with 8 categories (4 lanes per vector x 8
