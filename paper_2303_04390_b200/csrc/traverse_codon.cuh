@@ -684,7 +684,7 @@ __global__ void __launch_bounds__(256) codon_ratio_kernel(const CodonArgs a, dou
     __shared__ double sh[256];
     __shared__ bool last;
     asm volatile("griddepcontrol.wait;" ::: "memory");      // (PDL launch behind the last pre level)
-    const int b = blockIdx.x, B = 2 * a.N - 2, root = 2 * a.N - 2;
+    const int b = blockIdx.x, B = 2 * a.N - 2;
     const int ns = gridDim.y, per = (a.C + ns - 1) / ns;
     const int c0 = blockIdx.y * per, c1 = min(a.C, c0 + per);
     double acc = 0.0;
