@@ -89,7 +89,8 @@ __global__ void __launch_bounds__(256) pmat16_mma_kernel(const double *__restric
                                                          const double *__restrict__ lam,
                                                          const double *__restrict__ rates,
                                                          const double *__restrict__ bl, int S, int rec,
-                                                         double *__restrict__ P, int *__restrict__ status) {
+                                                         double *__restrict__ P, int *__restrict__ status,
+                                                         const MaskTable mt) {
     __shared__ double e[16], Ps[16][17];
     pdl_trigger_and_reset(status);
     const int b = blockIdx.x;
@@ -117,11 +118,16 @@ __global__ void __launch_bounds__(256) pmat16_mma_kernel(const double *__restric
     for (int i = threadIdx.x; i < 16 * 17; i += blockDim.x) {
         const int row = i / 17, col = i % 17;
         double v;
-        if (col < 16) {
-            v = Ps[row][col];
-        } else {
+        if (col == 16) {
             v = 0.0;
             for (int c = 0; c < 16; ++c) v += Ps[row][c];
+        } else if (mt.n < 0) {
+            v = Ps[row][col];
+        } else {                                 // coded mask tips: column m = sum over mask m's states
+            v = 0.0;
+            if (col < mt.n)
+                for (int c = 0; c < 16; ++c)
+                    if (mt.mask[col] >> c & 1) v += Ps[row][c];
         }
         R2[i] = v;
     }

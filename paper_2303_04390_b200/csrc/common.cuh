@@ -8,6 +8,12 @@
 
 namespace pg {
 
+// Masks of coded partial tips on the S = 16 tensor path (n < 0: none).
+struct MaskTable {
+    int n = 0;
+    uint16_t mask[16] = {};
+};
+
 // Arguments of one traversal launch (both kernel variants).
 struct TravArgs {
     const Op4 *post;            // [N-1] post program (schedule.hpp)

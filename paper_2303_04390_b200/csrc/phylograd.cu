@@ -231,6 +231,13 @@ struct pg_instance {
     // host-side state
     std::vector<uint8_t> tips_h;        // [N][Cpad]
     std::vector<uint8_t> tip_is_partial, tip_set, tip_masked;
+    // S = 16 tensor path: tip partials that are 0/1 masks (e.g. the hidden
+    // copies of an observed nucleotide) -- per tip the pattern's mask as bits,
+    // empty when the tip's partials are not all masks; mask_mode: every tip
+    // is such a tip and there are <= 16 distinct masks (besides all-ones)
+    std::vector<std::vector<uint16_t>> tip_mask16;
+    bool mask_mode = false;
+    pg::MaskTable mask_table{};
     bool have_ops = false, have_eigen = false, have_pi = false, have_rates = false,
          have_cw = false, have_bl = false, have_patw = false;
     pg::Plan plan;
@@ -484,6 +491,23 @@ int pg_set_tip_partials(pg_instance *inst, int32_t tip, const double *partials) 
         }
     int rc = inst->L.variant == 3 ? PG_OK : upload_real(inst, inst->L.off_tipp + (size_t)tip * Cp * SP * inst->L.real, v);
     if (rc) return rc;
+    if (inst->L.variant == 0 && inst->L.mma && S <= 16) {
+        std::vector<uint16_t> mk((size_t)c.patterns);
+        bool ok = true;
+        for (int p = 0; p < c.patterns && ok; ++p) {
+            uint16_t b = 0;
+            for (int s2 = 0; s2 < S && ok; ++s2) {
+                const double x = partials[(size_t)p * S + s2];
+                if (x == 1.0) b |= (uint16_t)(1u << s2);
+                else if (x != 0.0) ok = false;
+            }
+            if (b == 0) ok = false;
+            mk[p] = b;
+        }
+        if (inst->tip_mask16.size() != (size_t)c.tips) inst->tip_mask16.resize(c.tips);
+        inst->tip_mask16[tip] = ok ? std::move(mk) : std::vector<uint16_t>();
+        inst->partial_modes_dirty = true;
+    }
     if (inst->L.variant >= 2) {
         // a 0/1 mask with 1..4 ones per pattern (e.g. the hidden copies of an
         // observed state): keep the state list so u = P p is a sum of <= 4
@@ -1196,9 +1220,55 @@ static int configure(pg_instance *inst) {
     return PG_OK;
 }
 
+// S = 16 tensor path: when every tip's partials are 0/1 masks drawn from at
+// most 16 distinct masks (besides all-ones), the tips become coded tips:
+// code = mask index (all-ones: 16, missing), and A1 writes the column sums
+// sum_{t in mask m} P[s][t] where the row-major layout keeps its columns --
+// a tip's u = P p is then a gather (as for observed states) instead of a
+// product, and the traversal copies one code byte per pattern instead of the
+// partial vector
+static void decide_mask_mode(pg_instance *inst) {
+    const pg_config &c = inst->cfg;
+    inst->mask_mode = false;
+    if (!(inst->L.variant == 0 && inst->L.mma) || inst->tip_mask16.size() != (size_t)c.tips) return;
+    if (getenv("PG_NO_MASK_TIPS")) return;
+    const uint16_t all = (uint16_t)((1u << c.states) - 1u);
+    pg::MaskTable mt{};
+    std::vector<uint8_t> codes((size_t)c.tips * inst->L.Cpad, 16);
+    for (int t = 0; t < c.tips; ++t) {
+        if (!inst->tip_is_partial[t] || inst->tip_mask16[t].size() != (size_t)c.patterns) return;
+        for (int p = 0; p < c.patterns; ++p) {
+            const uint16_t b = inst->tip_mask16[t][p];
+            int code = 16;
+            if (b != all) {
+                code = -1;
+                for (int m = 0; m < mt.n; ++m)
+                    if (mt.mask[m] == b) code = m;
+                if (code < 0) {
+                    if (mt.n == 16) return;          // too many distinct masks
+                    mt.mask[mt.n] = b;
+                    code = mt.n++;
+                }
+            }
+            codes[(size_t)t * inst->L.Cpad + p] = (uint8_t)code;
+        }
+    }
+    inst->mask_mode = true;
+    inst->mask_table = mt;
+    inst->tips_h = std::move(codes);
+    inst->tips_dirty = true;
+}
+
 static int refresh_plan(pg_instance *inst) {
     if (!inst->plan_dirty && !inst->partial_modes_dirty) return PG_OK;
-    pg::encode_tip_modes(&inst->plan, inst->tip_is_partial);
+    decide_mask_mode(inst);
+    if (inst->mask_mode) {
+        // coded tips: no partial-tip bit in the programs
+        const std::vector<uint8_t> none(inst->cfg.tips, 0);
+        pg::encode_tip_modes(&inst->plan, none);
+    } else {
+        pg::encode_tip_modes(&inst->plan, inst->tip_is_partial);
+    }
     const int N = inst->cfg.tips;
     CK(cudaMemcpyAsync(inst->ws + inst->L.off_post, inst->plan.post.data(), sizeof(Op4) * (N - 1),
                        cudaMemcpyHostToDevice, inst->stream), "plan upload");
@@ -1271,7 +1341,7 @@ static pg::TravArgs trav_args(pg_instance *inst) {
     a.logl_part = inst->at<double>(L.off_lpart);
     a.status = inst->at<int>(L.off_status);
     a.N = inst->cfg.tips;
-    a.S = inst->cfg.states;
+    a.S = inst->mask_mode ? inst->mask_table.n : inst->cfg.states;   // mask mode: codes < n are masks
     a.R = inst->cfg.categories;
     a.Cpad = L.Cpad;
     a.C = inst->cfg.patterns;
@@ -1428,7 +1498,9 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
         const double *M0 = inst->at<double>(L.off_M0);
         if (L.mma) {
             int rec = cs * R;                            // doubles per branch record
-            void *args16[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, &rec, &P, &status_w};
+            pg::MaskTable mt = inst->mask_table;
+            if (!inst->mask_mode) mt.n = -1;            // the plain row-major layout
+            void *args16[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, &rec, &P, &status_w, &mt};
             if (L.SP == 16)
                 CK(cudaLaunchKernel((void *)pg::pmat16_mma_kernel, dim3(L.B), dim3(256), args16, 0, inst->stream),
                    "pmat16 launch");
