@@ -90,7 +90,9 @@ __global__ void __launch_bounds__(256) pmat16_mma_kernel(const double *__restric
                                                          const double *__restrict__ rates,
                                                          const double *__restrict__ bl, int S, int rec,
                                                          double *__restrict__ P, int *__restrict__ status,
-                                                         const MaskTable mt) {
+                                                         const MaskTable mt, unsigned char *__restrict__ recp,
+                                                         const int *__restrict__ pdst, unsigned char *__restrict__ recq,
+                                                         const int *__restrict__ qdst) {
     __shared__ double e[16], Ps[16][17];
     pdl_trigger_and_reset(status);
     const int b = blockIdx.x;
@@ -130,6 +132,22 @@ __global__ void __launch_bounds__(256) pmat16_mma_kernel(const double *__restric
                     if (mt.mask[col] >> c & 1) v += Ps[row][c];
         }
         R2[i] = v;
+    }
+    // staging records (traverse_small_kernel GRP variant): the layout each
+    // record slot needs (destination = byte offset * 4 + layout), copied from
+    // the branch record just written (same block: visible after the barrier)
+    if (recp) {
+        __syncthreads();
+        const int dp = pdst[b], dq = qdst[b];
+        const double *Rs[3] = {R0, R1, R2};
+        if (dp >= 0) {
+            double *d = reinterpret_cast<double *>(recp + (dp >> 2));
+            for (int i = threadIdx.x; i < 16 * 17; i += blockDim.x) d[i] = Rs[dp & 3][i];
+        }
+        if (dq >= 0) {
+            double *d = reinterpret_cast<double *>(recq + (dq >> 2));
+            for (int i = threadIdx.x; i < 16 * 17; i += blockDim.x) d[i] = Rs[dq & 3][i];
+        }
     }
 }
 

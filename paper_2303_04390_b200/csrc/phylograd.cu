@@ -259,7 +259,7 @@ struct pg_instance {
     int flow_pub = 1;                   // flow v2: publisher warp (PG_FLOW_PUB)
     bool a6_fused = false;              // set per enqueue: the flow kernel also formed [logL, g]
     // small-S grouped post-order staging (library-owned buffers)
-    bool grouped = false, tipstream_dirty = true;
+    bool grouped = false, tipstream_on = false, tipstream_dirty = true;
     bool small_coresident = false;      // small-S grid fits the GPU at once (fused A6 possible)
     int tipw = 0;
     unsigned char *rec_post = nullptr, *rec_pre = nullptr, *tipstream = nullptr;
@@ -908,7 +908,7 @@ static void *traverse_fn(const Layout &L, int R, bool grouped = false) {
 #ifdef PG_SMALL_MMA4
     if (L.mma) return L.SP == 16 ? small_kernel<double, 16, 1, 1>() : small_kernel<double, 4, 4, 1>();
 #else
-    if (L.mma) return small_kernel<double, 16, 1, 1>();
+    if (L.mma) return grouped ? small_kernel<double, 16, 1, 1, true>() : small_kernel<double, 16, 1, 1>();
 #endif
     switch (L.SP) {
         case 4:
@@ -1034,20 +1034,24 @@ static int configure(pg_instance *inst) {
             for (int t = 0; t < inst->cfg.tips; ++t) any_partial |= inst->tip_is_partial[t] != 0;
             const char *ge = getenv("PG_GPOST");
             const int tw = small_tipw(L, K);
-            inst->grouped = !L.mma && L.SP == 4 && !any_partial && !(ge && atoi(ge) == 0) &&
-                            small_smem(L, R, K, depth, tw) <= 227 * 1024;
+            // S = 4, state tips: records + grouped post stages; the S = 16
+            // tensor path (MMM, partial tips): records only
+            const bool grp4 = !L.mma && L.SP == 4 && !any_partial && small_smem(L, R, K, depth, tw) <= 227 * 1024;
+            const bool rec16 = L.mma && L.SP == 16;
+            inst->grouped = (grp4 || rec16) && !(ge && atoi(ge) == 0);
+            inst->tipstream_on = inst->grouped && grp4;
             if (getenv("PG_DEBUG_PLAN"))
                 fprintf(stderr, "[phylograd] small-S: K=%d grid=%d grouped=%d (partial=%d own_ws=%d smem=%zu)\n", K,
                         inst->grid, (int)inst->grouped, (int)any_partial, (int)inst->own_ws,
                         small_smem(L, R, K, depth, tw));
             if (inst->grouped) {
-                inst->tipw = tw;
-                inst->smem = (int)small_smem(L, R, K, depth, tw);
+                inst->tipw = inst->tipstream_on ? tw : 0;
+                if (inst->tipstream_on) inst->smem = (int)small_smem(L, R, K, depth, tw);
                 const int N = inst->cfg.tips, B = L.B;
-                const size_t recb = 16 + 3 * (size_t)R * L.cat_stride * L.real;
-                const size_t recpb = 16 + 2 * (size_t)R * L.cat_stride * L.real;
+                const size_t ms = L.mma ? (size_t)pg::MMA_SLOT : (size_t)R * L.cat_stride * L.real;   // one slot
+                const size_t recb = 16 + 3 * ms, recpb = 16 + 2 * ms;
                 const size_t rec_need = (size_t)(N - 1) * (recb + recpb);
-                const size_t ts_need = (size_t)inst->grid * (N - 1) * 2 * tw;
+                const size_t ts_need = inst->tipstream_on ? (size_t)inst->grid * (N - 1) * 2 * tw : 1;
                 if (inst->rec_cap < rec_need) {
                     if (inst->rec_post) cudaFree(inst->rec_post);
                     CK(cudaMalloc(&inst->rec_post, rec_need), "post records alloc");
@@ -1070,16 +1074,22 @@ static int configure(pg_instance *inst) {
                                      cudaMemcpyHostToDevice, inst->stream), "record ops upload");
                 CK(cudaMemcpy2DAsync(inst->rec_pre, recpb, inst->plan.pre.data(), sizeof(Op4), sizeof(Op4), N - 1,
                                      cudaMemcpyHostToDevice, inst->stream), "record ops upload");
-                std::vector<int32_t> dst(2 * B, -1);     // [post slot][pre slot] per branch
-                const size_t ms = (size_t)R * L.cat_stride * L.real;
+                // [post slot][pre slot] per branch: byte offset (S = 16 tensor
+                // path: offset * 4 + which of the branch's three layouts the
+                // slot's reader takes, as mat_src in traverse_small.cuh)
+                std::vector<int32_t> dst(2 * B, -1);
+                const int pbit = pg::kTipPartialBit;
+                auto enc = [&](size_t off, int lay) { return L.mma ? (int)(off * 4 + lay) : (int)off; };
+                auto tip_lay = [&](int code) { return (code & pbit) ? 0 : 2; };
                 for (int m = 0; m < N - 1; ++m) {
                     const Op4 op = inst->plan.post[m];
-                    if (op.x != 2 * N - 2) dst[op.x] = (int)(m * recb + 16);
-                    if (op.y >= 0) dst[op.y & ~pg::kTipPartialBit] = (int)(m * recb + 16 + ms);
-                    if (op.z >= 0) dst[op.z & ~pg::kTipPartialBit] = (int)(m * recb + 16 + 2 * ms);
+                    if (op.x != 2 * N - 2) dst[op.x] = enc(m * recb + 16, 0);
+                    if (op.y >= 0) dst[op.y & ~pbit] = enc(m * recb + 16 + ms, tip_lay(op.y));
+                    if (op.z >= 0) dst[op.z & ~pbit] = enc(m * recb + 16 + 2 * ms, tip_lay(op.z));
                     const Op4 oq = inst->plan.pre[m];
-                    dst[B + (oq.y & ~pg::kTipPartialBit)] = (int)(m * recpb + 16);
-                    dst[B + (oq.z & ~pg::kTipPartialBit)] = (int)(m * recpb + 16 + ms);
+                    const int ny = oq.y & ~pbit, nz = oq.z & ~pbit;
+                    dst[B + ny] = enc(m * recpb + 16, ny >= N ? 1 : tip_lay(oq.y));
+                    dst[B + nz] = enc(m * recpb + 16 + ms, nz >= N ? 1 : tip_lay(oq.z));
                 }
                 inst->post_dst_h = dst;
                 CK(cudaMemcpyAsync(inst->post_dst, inst->post_dst_h.data(), sizeof(int) * 2 * B, cudaMemcpyHostToDevice,
@@ -1352,8 +1362,8 @@ static pg::TravArgs trav_args(pg_instance *inst) {
     a.trace = inst->trace;
     a.rec_post = inst->grouped ? inst->rec_post : nullptr;
     a.rec_pre = inst->grouped ? inst->rec_pre : nullptr;
-    a.tipstream = inst->grouped ? inst->tipstream : nullptr;
-    a.tipw = inst->grouped ? inst->tipw : 0;
+    a.tipstream = inst->tipstream_on ? inst->tipstream : nullptr;
+    a.tipw = inst->tipstream_on ? inst->tipw : 0;
     return a;
 }
 
@@ -1500,7 +1510,9 @@ static int enqueue_eval(pg_instance *inst, double *d_out) {
             int rec = cs * R;                            // doubles per branch record
             pg::MaskTable mt = inst->mask_table;
             if (!inst->mask_mode) mt.n = -1;            // the plain row-major layout
-            void *args16[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, &rec, &P, &status_w, &mt};
+            unsigned char *recp = inst->grouped ? inst->rec_post : nullptr, *recq = inst->grouped ? inst->rec_pre : nullptr;
+            const int *pdst = inst->post_dst, *qdst = inst->grouped ? inst->post_dst + L.B : nullptr;
+            void *args16[] = {&V, &Vi, &M0, &lam, &rates, &bl, &S, &rec, &P, &status_w, &mt, &recp, &pdst, &recq, &qdst};
             if (L.SP == 16)
                 CK(cudaLaunchKernel((void *)pg::pmat16_mma_kernel, dim3(L.B), dim3(256), args16, 0, inst->stream),
                    "pmat16 launch");
@@ -1722,7 +1734,7 @@ static int prepare(pg_instance *inst, bool captured = false) {
     if (captured) {
         // inside the caller's stream capture nothing may synchronise: the
         // plan, launch configuration and tip data must already be on the device
-        if (inst->plan_dirty || inst->partial_modes_dirty || inst->tips_dirty || (inst->grouped && inst->tipstream_dirty))
+        if (inst->plan_dirty || inst->partial_modes_dirty || inst->tips_dirty || (inst->tipstream_on && inst->tipstream_dirty))
             return inst->fail(PG_ERR_SEQUENCE, "pending uploads (operations, tips or launch plan): run one evaluation "
                                                "outside stream capture before capturing pg_compute_device");
         return PG_OK;
@@ -1736,7 +1748,7 @@ static int prepare(pg_instance *inst, bool captured = false) {
         inst->tips_dirty = false;
         inst->tipstream_dirty = true;
     }
-    if (inst->grouped && inst->tipstream_dirty) {
+    if (inst->tipstream_on && inst->tipstream_dirty) {
         // per CTA and post step, the tip-code windows of the step's tip
         // children (static while tips and plan are unchanged)
         const Layout &L = inst->L;

@@ -480,7 +480,9 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
     uint64_t *post_done = empty + DS;                               // [1]
     uint64_t *gfull = post_done + 2, *gempty = gfull + Cfg::DPG;    // grouped post stages
     unsigned char *stages = smem + Cfg::BARS;
-    constexpr bool grouped = GRP;
+    // GRP: staging records (A1 writes each step's matrices next to its op);
+    // S = 4 with state tips also groups GPOST post steps per ring stage
+    constexpr bool records = GRP, grouped = GRP && !Cfg::MMA && !Cfg::MMA4;
     constexpr int GG = Cfg::GPOST, DPG = Cfg::DPG;
     const int RECB = Cfg::rec_bytes(a.R), TW = a.tipw, GSTG = grouped ? Cfg::gstage(a.R, a.tipw) : 0;
     // shared-window addresses of the barriers and stages (loop-invariant bases)
@@ -616,6 +618,8 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             const bool pre = t >= nops;
             const int m = pre ? t - nops : t;
             const Op4 op = (pre ? pre_prog : post_prog)[m];
+            if (!pre && records)
+                return 16 + 3 * MS + (op.y >= 0 ? tip_bytes(op.y) : 0) + (op.z >= 0 ? tip_bytes(op.z) : 0);
             if (!pre)
                 return 16 + (op.x != root ? MS : 0) + (op.y >= 0 ? MS + tip_bytes(op.y) : 0) +
                        (op.z >= 0 ? MS + tip_bytes(op.z) : 0);
@@ -628,7 +632,14 @@ __global__ void __launch_bounds__(32 * (small_max_consumers(SP, RP) + 1), 1) tra
             const Op4 *gprog = pre ? a.pre : a.post;           // global copy (bulk source)
             const Op4 *prog = pre ? pre_prog : post_prog;       // smem copy when staged
             const Op4 op = prog[m];
-            if (grouped && pre) {
+            if (records && !pre) {
+                // the step's record: op, P_k and the tip children's matrices
+                bulk_g2s_u32(st, a.rec_post + (size_t)m * (16 + 3 * MS), 16 + 3 * MS, bar);
+                if (op.y >= 0) copy_tip(st + 16 + 3 * MS, op.y, bar);
+                if (op.z >= 0) copy_tip(st + 16 + 3 * MS + VS, op.z, bar);
+                return;
+            }
+            if (records && pre) {
                 // the step's record: op and both children's matrices, one copy
                 const unsigned recpb = 16 + 2 * MS;
                 bulk_g2s_u32(st, a.rec_pre + (size_t)m * recpb, recpb, bar);
