@@ -93,18 +93,25 @@ __global__ void __launch_bounds__(256) pmat16_mma_kernel(const double *__restric
                                                          const MaskTable mt, unsigned char *__restrict__ recp,
                                                          const int *__restrict__ pdst, unsigned char *__restrict__ recq,
                                                          const int *__restrict__ qdst) {
-    __shared__ double e[16], Ps[16][17];
+    __shared__ double e[16], Ps[16][17], Vs[256], Vis[256];
     pdl_trigger_and_reset(status);
     const int b = blockIdx.x;
     const double t = rates[0] * bl[b];
+    // V and V^-1 staged once (one load per thread) instead of 2 S loads per
+    // thread from L2 inside the sum
+    if (threadIdx.x < S * S) {
+        Vs[threadIdx.x] = V[threadIdx.x];
+        Vis[threadIdx.x] = Vi[threadIdx.x];
+    }
+    const double m0 = M0[threadIdx.x];
     for (int k = threadIdx.x; k < 16; k += blockDim.x) e[k] = k < S ? expm1(lam[k] * t) : 0.0;
     __syncthreads();
     {
         const int s = threadIdx.x >> 4, u = threadIdx.x & 15;
         double acc = 0.0;
         if (s < S && u < S) {
-            for (int k = 0; k < S; ++k) acc += V[s * S + k] * e[k] * Vi[k * S + u];
-            acc += M0[s * 16 + u];
+            for (int k = 0; k < S; ++k) acc += Vs[s * S + k] * e[k] * Vis[k * S + u];
+            acc += m0;
         }
         Ps[s][u] = acc;
     }
