@@ -116,45 +116,41 @@ __global__ void __launch_bounds__(256) pmat16_mma_kernel(const double *__restric
         Ps[s][u] = acc;
     }
     __syncthreads();
-    double *R0 = P + (size_t)b * rec, *R1 = R0 + 16 * 17, *R2 = R1 + 16 * 17;
-    {
-        const int idx = threadIdx.x, f = idx >> 5, l = idx & 31;
-        const int k = 4 * (f >> 1) + (l & 3), n = 8 * (f & 1) + (l >> 2);
-        const int sg = 4 * (2 * (n >> 3) + (n & 1)) + ((n & 7) >> 1);
-        R0[idx] = Ps[sg][k];
-        R1[idx] = Ps[k][sg];
-    }
-    for (int i = threadIdx.x; i < 16 * 17; i += blockDim.x) {
+    double *R0 = P + (size_t)b * rec;
+    // element i of layout lay (0: B of u = P p, 1: B of q = x P, both in
+    // fragment order over 256 entries; 2: row-major, stride 17, column 16 =
+    // P 1, mask-tip columns as sums), straight from the shared-memory P
+    auto elem = [&](int lay, int i) -> double {
+        if (lay < 2) {
+            if (i >= 256) return 0.0;
+            const int f = i >> 5, l = i & 31;
+            const int k = 4 * (f >> 1) + (l & 3), n = 8 * (f & 1) + (l >> 2);
+            const int sg = 4 * (2 * (n >> 3) + (n & 1)) + ((n & 7) >> 1);
+            return lay == 0 ? Ps[sg][k] : Ps[k][sg];
+        }
         const int row = i / 17, col = i % 17;
-        double v;
+        double v = 0.0;
         if (col == 16) {
-            v = 0.0;
             for (int c = 0; c < 16; ++c) v += Ps[row][c];
         } else if (mt.n < 0) {
             v = Ps[row][col];
-        } else {                                 // coded mask tips: column m = sum over mask m's states
-            v = 0.0;
-            if (col < mt.n)
-                for (int c = 0; c < 16; ++c)
-                    if (mt.mask[col] >> c & 1) v += Ps[row][c];
+        } else if (col < mt.n) {                 // coded mask tips: column m = sum over mask m's states
+            for (int c = 0; c < 16; ++c)
+                if (mt.mask[col] >> c & 1) v += Ps[row][c];
         }
-        R2[i] = v;
-    }
-    // staging records (traverse_small_kernel GRP variant): the layout each
-    // record slot needs (destination = byte offset * 4 + layout), copied from
-    // the branch record just written (same block: visible after the barrier)
-    if (recp) {
-        __syncthreads();
-        const int dp = pdst[b], dq = qdst[b];
-        const double *Rs[3] = {R0, R1, R2};
-        if (dp >= 0) {
-            double *d = reinterpret_cast<double *>(recp + (dp >> 2));
-            for (int i = threadIdx.x; i < 16 * 17; i += blockDim.x) d[i] = Rs[dp & 3][i];
+        return v;
+    };
+    // the branch's three layouts, and the staging-record slots that read it
+    // (traverse_small_kernel GRP variant; destination = byte offset * 4 + layout)
+    const int dp = recp ? pdst[b] : -1, dq = recp ? qdst[b] : -1;
+    for (int i = threadIdx.x; i < 16 * 17; i += blockDim.x) {
+        if (i < 256) {
+            R0[i] = elem(0, i);
+            R0[16 * 17 + i] = elem(1, i);
         }
-        if (dq >= 0) {
-            double *d = reinterpret_cast<double *>(recq + (dq >> 2));
-            for (int i = threadIdx.x; i < 16 * 17; i += blockDim.x) d[i] = Rs[dq & 3][i];
-        }
+        R0[2 * 16 * 17 + i] = elem(2, i);
+        if (dp >= 0) reinterpret_cast<double *>(recp + (dp >> 2))[i] = elem(dp & 3, i);
+        if (dq >= 0) reinterpret_cast<double *>(recq + (dq >> 2))[i] = elem(dq & 3, i);
     }
 }
 
